@@ -1,0 +1,235 @@
+/*
+ * patchdb-b200 -- B200-native drop-in for the reference `patchdb` C-ABI.
+ *
+ * Every declaration in the first part of this header has the signature,
+ * struct layout and error semantics of the reference interface it replaces;
+ * the citation after each one is /root/reference/proj/include/patchdb/patchdb.h
+ * (abbreviated "ref.h:LINE").  Handles live on the GPU: matrices, patch
+ * sets, databases and preconditioners keep their arrays in HBM and every
+ * call is synchronous (device work is complete when the call returns).
+ * Host arrays passed in or out are plain caller-owned pointers, exactly as
+ * in the reference.  There is no CPU fallback: on a machine without a
+ * usable sm_100 device the compute entry points fail with
+ * PDB_ERR_INTERNAL and a "CUDA ..." message.
+ *
+ * The second part (below "extensions") adds new symbols only; nothing in
+ * the reference interface changes meaning.
+ */
+#ifndef PATCHDB_B200_H
+#define PATCHDB_B200_H
+
+#include <stdint.h>
+
+#if defined(_WIN32)
+#define PDB_API __declspec(dllexport)
+#else
+#define PDB_API __attribute__((visibility("default")))
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes, values fixed by ref.h:25-41. */
+typedef enum pdb_status {
+  PDB_OK = 0,
+  PDB_ERR_INVALID_ARGUMENT = 1,
+  PDB_ERR_DIMENSION_MISMATCH = 2,
+  PDB_ERR_SINGULAR_MATRIX = 3,
+  PDB_ERR_INDEX_OUT_OF_RANGE = 4,
+  PDB_ERR_DUPLICATE_INDEX = 5,
+  PDB_ERR_PARSE = 6,
+  PDB_ERR_NON_SQUARE_MATRIX = 7,
+  PDB_ERR_NO_PATCHES_FOUND = 8,
+  PDB_ERR_EMPTY_CLUSTER = 9,
+  PDB_ERR_BUDGET_TOO_SMALL = 10,
+  PDB_ERR_INVALID_DEGREE = 11,
+  PDB_ERR_NON_POSITIVE_COEFFICIENT = 12,
+  PDB_ERR_IO = 13,
+  PDB_ERR_INTERNAL = 14
+} pdb_status;
+
+PDB_API const char* pdb_status_string(pdb_status status);       /* ref.h:43 */
+PDB_API const char* pdb_last_error(void);                       /* ref.h:46, thread-local */
+
+typedef struct pdb_matrix_s* pdb_matrix;     /* device CSR */
+typedef struct pdb_problem_s* pdb_problem;   /* host-side assembled problem */
+typedef struct pdb_patchset_s* pdb_patchset; /* device patch lists + weights */
+typedef struct pdb_database_s* pdb_database; /* device representatives + factors + phi */
+typedef struct pdb_precond_s* pdb_precond;   /* device sweep structures */
+typedef struct pdb_report_s* pdb_report;
+
+/* ---- sparse matrices (ref.h:57-63) ---- */
+PDB_API pdb_status pdb_matrix_read_matrix_market(const char* path, pdb_matrix* out);
+PDB_API pdb_status pdb_matrix_write_matrix_market(pdb_matrix m, const char* path);
+PDB_API int64_t pdb_matrix_rows(pdb_matrix m);
+PDB_API int64_t pdb_matrix_nnz(pdb_matrix m);
+PDB_API pdb_status pdb_matrix_spmv(pdb_matrix m, const double* x, double* y);
+PDB_API void pdb_matrix_free(pdb_matrix m);
+
+/* ---- assembled model problems (ref.h:67-75) ---- */
+PDB_API pdb_status pdb_problem_assemble(const char* config_json, pdb_problem* out);
+PDB_API int64_t pdb_problem_ndofs(pdb_problem p);
+PDB_API pdb_status pdb_problem_matrix(pdb_problem p, pdb_matrix* out);
+PDB_API pdb_status pdb_problem_rhs(pdb_problem p, double* out);
+PDB_API pdb_status pdb_problem_exact_solution(pdb_problem p, double* out);
+PDB_API pdb_status pdb_problem_l2_error(pdb_problem p, const double* discrete_solution, double* out);
+PDB_API void pdb_problem_free(pdb_problem p);
+
+/* ---- patch detection (ref.h:80-84) ---- */
+PDB_API pdb_status pdb_patchset_detect(pdb_matrix m, int64_t patch_size, pdb_patchset* out);
+PDB_API int64_t pdb_patchset_count(pdb_patchset ps);
+PDB_API int64_t pdb_patchset_patch_size(pdb_patchset ps);
+PDB_API pdb_status pdb_patchset_write_json(pdb_patchset ps, const char* path);
+PDB_API void pdb_patchset_free(pdb_patchset ps);
+
+/* ---- factorization database (ref.h:88-117) ---- */
+typedef enum pdb_method {
+  PDB_METHOD_EXACT = 0,
+  PDB_METHOD_GREEDY_SPECTRAL = 1,
+  PDB_METHOD_GREEDY_L1 = 2,
+  PDB_METHOD_KMEANS_ENTRYWISE = 3,
+  PDB_METHOD_KMEANS_SPECTRAL = 4,
+  PDB_METHOD_KMEANS_VARMIN = 5,
+  PDB_METHOD_BOOTSTRAP = 6
+} pdb_method;
+
+/* 48 bytes, field offsets 0/8/16/24/32/36/40 as ref.h:98-106. */
+typedef struct pdb_compress_options {
+  pdb_method method;
+  double eps;
+  int64_t db_size;
+  uint64_t seed;
+  int max_iters;
+  int best_match;
+  int threads; /* accepted and ignored: the GPU sets its own parallelism */
+} pdb_compress_options;
+
+PDB_API void pdb_compress_options_init(pdb_compress_options* opts);
+PDB_API pdb_status pdb_database_build(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                      pdb_database* out);
+PDB_API int64_t pdb_database_size(pdb_database db);
+PDB_API int64_t pdb_database_n_patches(pdb_database db);
+PDB_API pdb_status pdb_database_phi(pdb_database db, int64_t* phi);
+PDB_API pdb_status pdb_database_export(pdb_database db, const char* json_path, const char* bin_path);
+PDB_API void pdb_database_free(pdb_database db);
+
+/* ---- preconditioners (ref.h:121-130) ---- */
+PDB_API pdb_status pdb_precond_create(pdb_matrix m, pdb_patchset ps, pdb_database db, double omega, int threads,
+                                      pdb_precond* out);
+PDB_API pdb_status pdb_precond_create_combo(pdb_problem p, pdb_patchset ps, pdb_database db, double omega,
+                                            int threads, pdb_precond* out);
+PDB_API pdb_status pdb_precond_apply(pdb_precond pc, const double* r, double* z);
+PDB_API void pdb_precond_free(pdb_precond pc);
+
+/* ---- solver (ref.h:134-158) ---- */
+/* 32 bytes, offsets 0/8/16/24/28 as ref.h:134-140. */
+typedef struct pdb_gmres_options {
+  int64_t restart;
+  double tol;
+  int64_t max_iters;
+  int left_precond;
+  int threads;
+} pdb_gmres_options;
+
+PDB_API void pdb_gmres_options_init(pdb_gmres_options* opts);
+PDB_API pdb_status pdb_gmres_solve(pdb_matrix m, const double* b, pdb_precond pc, const pdb_gmres_options* opts,
+                                   double* x, pdb_report* out_report);
+PDB_API int64_t pdb_report_iterations(pdb_report rep);
+PDB_API int64_t pdb_report_restarts(pdb_report rep);
+PDB_API int pdb_report_converged(pdb_report rep);
+PDB_API double pdb_report_final_relative_residual(pdb_report rep);
+PDB_API int64_t pdb_report_residual_history_size(pdb_report rep);
+PDB_API pdb_status pdb_report_residual_history(pdb_report rep, double* out);
+PDB_API void pdb_report_free(pdb_report rep);
+
+/* ---- experiment drivers (ref.h:166-169) ---- */
+PDB_API pdb_status pdb_run_experiment(const char* config_json, const char* out_csv);
+PDB_API pdb_status pdb_run_analyze(const char* config_json, const char* curve_csv, const char* histogram_csv);
+PDB_API pdb_status pdb_run_benchmark(const char* config_json, const char* out_csv);
+PDB_API pdb_status pdb_export_matrix(const char* config_json, const char* out_path);
+
+/* =====================================================================
+ * extensions (new symbols only)
+ * ===================================================================== */
+
+/* Build a device matrix from host CSR arrays (the reference's SparseMatrix
+ * fields, sparse.hpp:20-25): row_ptr[n+1], col_idx[nnz] strictly increasing
+ * per row, values[nnz].  Validated like the reference's invariants. */
+PDB_API pdb_status pdb_matrix_from_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                       const double* values, pdb_matrix* out);
+/* Copy the CSR arrays back to the host (sizes from rows / nnz). */
+PDB_API pdb_status pdb_matrix_csr(pdb_matrix m, int64_t* row_ptr, int64_t* col_idx, double* values);
+/* y = A x with device pointers on `stream` (cudaStream_t; NULL = per-thread default). */
+PDB_API pdb_status pdb_matrix_spmv_device(pdb_matrix m, const double* d_x, double* d_y, void* stream);
+
+/* Seeded synthetic problem generator for the BASELINE configurations
+ * (DESIGN.md "Inputs").  Host-only: works without a GPU. */
+typedef struct pdb_gen_options {
+  int physics;         /* 0 = scalar diffusion -div(rho grad u) */
+  int dim;             /* 2 or 3 */
+  int degree;          /* Lagrange degree p >= 1 */
+  int bc_mode;         /* 0 = Dirichlet row replacement, no column elimination (ref fem.cpp:323-342) */
+  int64_t cells;       /* cells per axis */
+  double jitter;       /* interior vertices moved by U(-jitter*h, +jitter*h) per coordinate */
+  uint64_t seed;
+  int coeff_kind;      /* 0 = constant coeff_value; 1 = random blocks of block_cells^dim cells */
+  int n_levels;        /* number of entries of levels[] used by coeff_kind 1 */
+  double coeff_value;
+  int64_t block_cells;
+  double levels[8];
+  int threads;         /* host threads for assembly (0 = all) */
+  int reserved;
+} pdb_gen_options;
+
+PDB_API void pdb_gen_options_init(pdb_gen_options* opts);
+/* Presets for BASELINE.json configs 1..3 at a given cells-per-axis (0 = the config's own size). */
+PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* opts);
+PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* opts, pdb_problem* out);
+PDB_API int64_t pdb_problem_nnz(pdb_problem p);
+PDB_API pdb_status pdb_problem_csr(pdb_problem p, int64_t* row_ptr, int64_t* col_idx, double* values);
+
+/* Patch-set contents (host copies): patches[count*patch_size] ascending per patch; weights[rows]. */
+PDB_API pdb_status pdb_patchset_patches(pdb_patchset ps, int64_t* patches);
+PDB_API pdb_status pdb_patchset_weights(pdb_patchset ps, double* weights);
+PDB_API int64_t pdb_patchset_rows(pdb_patchset ps);
+/* Dense patch matrices A_k = V_k A V_k^T, row-major, count*patch_size^2 doubles (host copy). */
+PDB_API pdb_status pdb_patchset_extract(pdb_matrix m, pdb_patchset ps, double* out);
+
+/* Database contents (host copies).  reps/lu: size*patch_size^2 row-major;
+ * pivots: size*patch_size ("original row at position i", ref dense.hpp:35-39). */
+PDB_API int64_t pdb_database_patch_size(pdb_database db);
+PDB_API double pdb_database_eps(pdb_database db);
+PDB_API pdb_status pdb_database_representatives(pdb_database db, double* reps);
+PDB_API pdb_status pdb_database_factors(pdb_database db, double* lu, int64_t* pivots);
+/* Tolerance bisection to a size band, ref experiments.cpp:168-204 (greedy methods only). */
+PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                              int64_t target_lo, int64_t target_hi, pdb_database* out,
+                                              double* eps_out);
+/* Work counters of the last build on this thread: distance evaluations and
+ * power iterations (spectral), for FP64 roofline accounting. */
+PDB_API pdb_status pdb_database_work(pdb_database db, int64_t* pair_evals, int64_t* power_iters, int64_t* lu_count);
+
+/* Device-pointer apply on a stream (NULL = per-thread default stream). */
+PDB_API pdb_status pdb_precond_apply_device(pdb_precond pc, const double* d_r, double* d_z, void* stream);
+/* `sweeps` damped patch-relaxation sweeps x <- x + M^{-1}(b - A x) (ref
+ * smooth(), precond.cpp:90-101) with host b and x (x updated in place).
+ * history (may be NULL) receives sweeps+1 values ||b - A x_s||_2. */
+PDB_API pdb_status pdb_relax(pdb_matrix m, pdb_precond pc, const double* b, double* x, int64_t sweeps,
+                             double* history);
+/* Same on device pointers; d_history (may be NULL) is a device array. */
+PDB_API pdb_status pdb_relax_device(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
+                                    double* d_history, void* stream);
+
+/* Preconditioned conjugate gradients, x0 = 0, stop when ||r||/||b|| <= tol. */
+PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
+                                 double* x, pdb_report* out_report);
+
+/* Build information: "sm_100a" target, version. */
+PDB_API const char* pdb_build_info(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PATCHDB_B200_H */

@@ -1,0 +1,544 @@
+// The C-ABI: every pdb_* symbol of include/patchdb/patchdb.h.
+//
+// Error handling mirrors the reference C-ABI (capi.cpp:37-135 of
+// /root/reference/proj/src): null arguments -> PDB_ERR_INVALID_ARGUMENT
+// "null argument"; library errors -> their code; anything else ->
+// PDB_ERR_INTERNAL; the message is thread-local (pdb_last_error).  Getters
+// return 0 on NULL handles; pdb_*_free(NULL) is a no-op.  All calls are
+// synchronous and run on the calling thread's per-thread default stream,
+// with per-call scratch, so concurrent applies on one handle are safe
+// (reference precond.cpp:67-69 is const with per-call buffers).
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "host.hpp"
+
+using namespace pdb;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+pdb_status guarded(F&& fn) {
+  try {
+    fn();
+    return PDB_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return static_cast<pdb_status>(static_cast<int>(e.code()));
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return PDB_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PDB_ERR_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return PDB_ERR_INTERNAL;
+  }
+}
+
+pdb_status arg_error(const char* msg) {
+  g_last_error = msg;
+  return PDB_ERR_INVALID_ARGUMENT;
+}
+
+pdb_status unsupported(const char* what) {
+  g_last_error = std::string(what) +
+                 " is outside the B200 hot path of this build (reference experiment/FEM driver); see DESIGN.md";
+  return PDB_ERR_INTERNAL;
+}
+
+cudaStream_t stream_of(void* s) { return s ? static_cast<cudaStream_t>(s) : default_stream(); }
+
+}  // namespace
+
+extern "C" {
+
+PDB_API const char* pdb_status_string(pdb_status status) {
+  switch (status) {
+    case PDB_OK: return "ok";
+    case PDB_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case PDB_ERR_DIMENSION_MISMATCH: return "dimension mismatch";
+    case PDB_ERR_SINGULAR_MATRIX: return "singular matrix";
+    case PDB_ERR_INDEX_OUT_OF_RANGE: return "index out of range";
+    case PDB_ERR_DUPLICATE_INDEX: return "duplicate index";
+    case PDB_ERR_PARSE: return "parse error";
+    case PDB_ERR_NON_SQUARE_MATRIX: return "non-square matrix";
+    case PDB_ERR_NO_PATCHES_FOUND: return "no patches found";
+    case PDB_ERR_EMPTY_CLUSTER: return "empty cluster";
+    case PDB_ERR_BUDGET_TOO_SMALL: return "budget too small";
+    case PDB_ERR_INVALID_DEGREE: return "invalid degree";
+    case PDB_ERR_NON_POSITIVE_COEFFICIENT: return "non-positive coefficient";
+    case PDB_ERR_IO: return "io error";
+    case PDB_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+PDB_API const char* pdb_last_error(void) { return g_last_error.c_str(); }
+
+PDB_API const char* pdb_build_info(void) {
+  return "patchdb-b200 0.1.0; device code sm_100a (tcgen05-era B200); C-ABI of patchdb 0.1.0";
+}
+
+/* ---- matrices ---- */
+
+PDB_API pdb_status pdb_matrix_read_matrix_market(const char* path, pdb_matrix* out) {
+  if (path == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    HostCsr h = read_matrix_market_host(path);
+    auto m = std::make_unique<pdb_matrix_s>();
+    upload_csr(h, m->a, default_stream());
+    *out = m.release();
+  });
+}
+
+PDB_API pdb_status pdb_matrix_write_matrix_market(pdb_matrix m, const char* path) {
+  if (m == nullptr || path == nullptr) return arg_error("null argument");
+  return guarded([&] { write_matrix_market_host(download_csr(m->a, default_stream()), path); });
+}
+
+PDB_API int64_t pdb_matrix_rows(pdb_matrix m) { return m == nullptr ? 0 : m->a.n; }
+PDB_API int64_t pdb_matrix_nnz(pdb_matrix m) { return m == nullptr ? 0 : m->a.nnz; }
+
+PDB_API pdb_status pdb_matrix_spmv(pdb_matrix m, const double* x, double* y) {
+  if (m == nullptr || x == nullptr || y == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    cudaStream_t s = default_stream();
+    const size_t n = static_cast<size_t>(m->a.n);
+    Scratch<double> dx(std::max<size_t>(n, 1), s), dy(std::max<size_t>(n, 1), s);
+    PDB_CUDA(cudaMemcpyAsync(dx.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    spmv_device(m->a, dx.get(), dy.get(), s);
+    PDB_CUDA(cudaMemcpyAsync(y, dy.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+PDB_API pdb_status pdb_matrix_spmv_device(pdb_matrix m, const double* d_x, double* d_y, void* stream) {
+  if (m == nullptr || d_x == nullptr || d_y == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    spmv_device(m->a, d_x, d_y, stream_of(stream));
+  });
+}
+
+PDB_API void pdb_matrix_free(pdb_matrix m) { delete m; }
+
+PDB_API pdb_status pdb_matrix_from_csr(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                       const double* values, pdb_matrix* out) {
+  if (row_ptr == nullptr || out == nullptr || ((col_idx == nullptr || values == nullptr) && n > 0 && row_ptr[n] > 0))
+    return arg_error("null argument");
+  return guarded([&] {
+    HostCsr h = validated_csr(n, row_ptr, col_idx, values);
+    auto m = std::make_unique<pdb_matrix_s>();
+    upload_csr(h, m->a, default_stream());
+    *out = m.release();
+  });
+}
+
+PDB_API pdb_status pdb_matrix_csr(pdb_matrix m, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  if (m == nullptr || row_ptr == nullptr || col_idx == nullptr || values == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    HostCsr h = download_csr(m->a, default_stream());
+    std::memcpy(row_ptr, h.row_ptr.data(), h.row_ptr.size() * sizeof(int64_t));
+    for (size_t p = 0; p < h.col.size(); ++p) col_idx[p] = h.col[p];
+    std::memcpy(values, h.val.data(), h.val.size() * sizeof(double));
+  });
+}
+
+/* ---- problems ---- */
+
+PDB_API pdb_status pdb_problem_assemble(const char* config_json, pdb_problem* out) {
+  if (config_json == nullptr || out == nullptr) return arg_error("null argument");
+  return unsupported("pdb_problem_assemble");
+}
+
+PDB_API int64_t pdb_problem_ndofs(pdb_problem p) { return p == nullptr ? 0 : p->a.n; }
+PDB_API int64_t pdb_problem_nnz(pdb_problem p) { return p == nullptr ? 0 : p->a.nnz(); }
+
+PDB_API pdb_status pdb_problem_matrix(pdb_problem p, pdb_matrix* out) {
+  if (p == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto m = std::make_unique<pdb_matrix_s>();
+    upload_csr(p->a, m->a, default_stream());
+    *out = m.release();
+  });
+}
+
+PDB_API pdb_status pdb_problem_rhs(pdb_problem p, double* out) {
+  if (p == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] { std::memcpy(out, p->rhs.data(), p->rhs.size() * sizeof(double)); });
+}
+
+PDB_API pdb_status pdb_problem_csr(pdb_problem p, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  if (p == nullptr || row_ptr == nullptr || col_idx == nullptr || values == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    std::memcpy(row_ptr, p->a.row_ptr.data(), p->a.row_ptr.size() * sizeof(int64_t));
+    for (size_t q = 0; q < p->a.col.size(); ++q) col_idx[q] = p->a.col[q];
+    std::memcpy(values, p->a.val.data(), p->a.val.size() * sizeof(double));
+  });
+}
+
+PDB_API pdb_status pdb_problem_exact_solution(pdb_problem p, double* out) {
+  if (p == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(p->has_exact, Errc::invalid_argument, "problem has no manufactured solution (generated input)");
+    std::memcpy(out, p->exact.data(), p->exact.size() * sizeof(double));
+  });
+}
+
+PDB_API pdb_status pdb_problem_l2_error(pdb_problem p, const double* discrete_solution, double* out) {
+  if (p == nullptr || discrete_solution == nullptr || out == nullptr) return arg_error("null argument");
+  return unsupported("pdb_problem_l2_error");
+}
+
+PDB_API void pdb_problem_free(pdb_problem p) { delete p; }
+
+PDB_API void pdb_gen_options_init(pdb_gen_options* o) {
+  if (o == nullptr) return;
+  std::memset(o, 0, sizeof(*o));
+  o->physics = 0;
+  o->dim = 2;
+  o->degree = 2;
+  o->bc_mode = 0;
+  o->cells = 32;
+  o->jitter = 0.0;
+  o->seed = 42;
+  o->coeff_kind = 0;
+  o->coeff_value = 1.0;
+  o->n_levels = 0;
+  o->block_cells = 1;
+  o->threads = 0;
+}
+
+// BASELINE.json configs: 1 = 2D Q2 32^2 jitter 0.1;
+// 2 = 2D Q4 256^2 jitter 0.05, rho on 8x8-cell blocks from {1,10,100,1000};
+// 3 = 3D Q2 64^3 jitter 0.1.
+PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* o) {
+  if (o == nullptr) return arg_error("null argument");
+  pdb_gen_options_init(o);
+  switch (config) {
+    case 1:
+      o->dim = 2, o->degree = 2, o->cells = 32, o->jitter = 0.1;
+      break;
+    case 2:
+      o->dim = 2, o->degree = 4, o->cells = 256, o->jitter = 0.05, o->coeff_kind = 1, o->block_cells = 8,
+      o->n_levels = 4;
+      o->levels[0] = 1.0, o->levels[1] = 10.0, o->levels[2] = 100.0, o->levels[3] = 1000.0;
+      break;
+    case 3:
+      o->dim = 3, o->degree = 2, o->cells = 64, o->jitter = 0.1;
+      break;
+    default:
+      return arg_error("config must be 1, 2 or 3 (configs 4-5 need Stokes / elasticity generators)");
+  }
+  if (cells > 0) o->cells = cells;
+  return PDB_OK;
+}
+
+PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* o, pdb_problem* out) {
+  if (o == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(o->physics == 0, Errc::invalid_argument, "only scalar diffusion (physics 0) is generated in this build");
+    require(o->bc_mode == 0, Errc::invalid_argument, "only Dirichlet row replacement (bc_mode 0) is supported");
+    auto p = std::make_unique<pdb_problem_s>();
+    generate_scalar(*o, *p);
+    *out = p.release();
+  });
+}
+
+/* ---- patch sets ---- */
+
+PDB_API pdb_status pdb_patchset_detect(pdb_matrix m, int64_t patch_size, pdb_patchset* out) {
+  if (m == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto ps = std::make_unique<pdb_patchset_s>();
+    detect_patches(m->a, patch_size, *ps, default_stream());
+    *out = ps.release();
+  });
+}
+
+PDB_API int64_t pdb_patchset_count(pdb_patchset ps) { return ps == nullptr ? 0 : ps->np; }
+PDB_API int64_t pdb_patchset_patch_size(pdb_patchset ps) { return ps == nullptr ? 0 : ps->ps; }
+PDB_API int64_t pdb_patchset_rows(pdb_patchset ps) { return ps == nullptr ? 0 : ps->n; }
+
+PDB_API pdb_status pdb_patchset_write_json(pdb_patchset ps, const char* path) {
+  if (ps == nullptr || path == nullptr) return arg_error("null argument");
+  return guarded([&] { write_patchset_json(*ps, path, default_stream()); });
+}
+
+PDB_API pdb_status pdb_patchset_patches(pdb_patchset ps, int64_t* patches) {
+  if (ps == nullptr || patches == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const std::vector<int64_t> h = patches_host(*ps, default_stream());
+    std::memcpy(patches, h.data(), h.size() * sizeof(int64_t));
+  });
+}
+
+PDB_API pdb_status pdb_patchset_weights(pdb_patchset ps, double* weights) {
+  if (ps == nullptr || weights == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    ps->weights.download(weights, static_cast<size_t>(ps->n), default_stream());
+    sync(default_stream());
+  });
+}
+
+PDB_API pdb_status pdb_patchset_extract(pdb_matrix m, pdb_patchset ps, double* out) {
+  if (m == nullptr || ps == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    DevBuf<double> mats;
+    extract_patches(m->a, *ps, mats, default_stream());
+    mats.download(out, mats.size(), default_stream());
+    sync(default_stream());
+  });
+}
+
+PDB_API void pdb_patchset_free(pdb_patchset ps) { delete ps; }
+
+/* ---- databases ---- */
+
+PDB_API void pdb_compress_options_init(pdb_compress_options* opts) {
+  if (opts == nullptr) return;
+  opts->method = PDB_METHOD_GREEDY_L1;
+  opts->eps = 1e-7;
+  opts->db_size = 0;
+  opts->seed = 42;
+  opts->max_iters = 50;
+  opts->best_match = 0;
+  opts->threads = 1;
+}
+
+static BuildParams params_of(const pdb_compress_options* o) {
+  BuildParams p;
+  p.method = o->method;
+  p.eps = o->eps;
+  p.db_size = o->db_size;
+  p.seed = o->seed;
+  p.max_iters = o->max_iters;
+  p.best_match = o->best_match != 0;
+  return p;
+}
+
+PDB_API pdb_status pdb_database_build(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                      pdb_database* out) {
+  if (m == nullptr || ps == nullptr || opts == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto db = std::make_unique<pdb_database_s>();
+    build_database(m->a, *ps, params_of(opts), *db, default_stream());
+    *out = db.release();
+  });
+}
+
+PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                              int64_t target_lo, int64_t target_hi, pdb_database* out,
+                                              double* eps_out) {
+  if (m == nullptr || ps == nullptr || opts == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto db = std::make_unique<pdb_database_s>();
+    const double eps = bisect_database(m->a, *ps, params_of(opts), target_lo, target_hi, *db, default_stream());
+    if (eps_out) *eps_out = eps;
+    *out = db.release();
+  });
+}
+
+PDB_API int64_t pdb_database_size(pdb_database db) { return db == nullptr ? 0 : db->m; }
+PDB_API int64_t pdb_database_n_patches(pdb_database db) { return db == nullptr ? 0 : db->np; }
+PDB_API int64_t pdb_database_patch_size(pdb_database db) { return db == nullptr ? 0 : db->ps; }
+PDB_API double pdb_database_eps(pdb_database db) { return db == nullptr ? 0.0 : db->eps; }
+
+PDB_API pdb_status pdb_database_phi(pdb_database db, int64_t* phi) {
+  if (db == nullptr || phi == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const std::vector<int32_t> h = db->phi.to_host(default_stream());
+    for (int64_t k = 0; k < db->np; ++k) phi[k] = h[static_cast<size_t>(k)];
+  });
+}
+
+PDB_API pdb_status pdb_database_representatives(pdb_database db, double* reps) {
+  if (db == nullptr || reps == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    db->reps.download(reps, static_cast<size_t>(db->m * db->ps * db->ps), default_stream());
+    sync(default_stream());
+  });
+}
+
+PDB_API pdb_status pdb_database_factors(pdb_database db, double* lu, int64_t* pivots) {
+  if (db == nullptr || lu == nullptr || pivots == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    db->lu.download(lu, static_cast<size_t>(db->m * db->ps * db->ps), default_stream());
+    std::vector<int32_t> p(static_cast<size_t>(db->m * db->ps));
+    db->piv.download(p.data(), p.size(), default_stream());
+    sync(default_stream());
+    for (size_t q = 0; q < p.size(); ++q) pivots[q] = p[q];
+  });
+}
+
+PDB_API pdb_status pdb_database_work(pdb_database db, int64_t* pair_evals, int64_t* power_iters, int64_t* lu_count) {
+  if (db == nullptr) return arg_error("null argument");
+  if (pair_evals) *pair_evals = db->work.pair_evals;
+  if (power_iters) *power_iters = db->work.power_iters;
+  if (lu_count) *lu_count = db->work.lu_count;
+  return PDB_OK;
+}
+
+PDB_API pdb_status pdb_database_export(pdb_database db, const char* json_path, const char* bin_path) {
+  if (db == nullptr || json_path == nullptr || bin_path == nullptr) return arg_error("null argument");
+  return guarded([&] { export_database(*db, json_path, bin_path, default_stream()); });
+}
+
+PDB_API void pdb_database_free(pdb_database db) { delete db; }
+
+/* ---- preconditioners ---- */
+
+PDB_API pdb_status pdb_precond_create(pdb_matrix m, pdb_patchset ps, pdb_database db, double omega, int threads,
+                                      pdb_precond* out) {
+  (void)threads;
+  if (ps == nullptr || out == nullptr) return arg_error("null argument");
+  if (db == nullptr && m == nullptr) return arg_error("exact preconditioner needs the matrix");
+  return guarded([&] {
+    auto pc = std::make_unique<pdb_precond_s>();
+    if (db == nullptr)
+      precond_exact(m->a, *ps, omega, *pc, default_stream());
+    else
+      precond_compressed(*ps, *db, omega, *pc, default_stream());
+    *out = pc.release();
+  });
+}
+
+PDB_API pdb_status pdb_precond_create_combo(pdb_problem p, pdb_patchset ps, pdb_database db, double omega,
+                                            int threads, pdb_precond* out) {
+  (void)db, (void)omega, (void)threads;
+  if (p == nullptr || ps == nullptr || out == nullptr) return arg_error("null argument");
+  return unsupported("pdb_precond_create_combo");
+}
+
+PDB_API pdb_status pdb_precond_apply(pdb_precond pc, const double* r, double* z) {
+  if (pc == nullptr || r == nullptr || z == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    cudaStream_t s = default_stream();
+    const size_t n = static_cast<size_t>(pc->n);
+    Scratch<double> dr(std::max<size_t>(n, 1), s), dz(std::max<size_t>(n, 1), s);
+    PDB_CUDA(cudaMemcpyAsync(dr.get(), r, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    precond_apply_device(*pc, dr.get(), dz.get(), s);
+    PDB_CUDA(cudaMemcpyAsync(z, dz.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+PDB_API pdb_status pdb_precond_apply_device(pdb_precond pc, const double* d_r, double* d_z, void* stream) {
+  if (pc == nullptr || d_r == nullptr || d_z == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    precond_apply_device(*pc, d_r, d_z, stream_of(stream));
+  });
+}
+
+PDB_API pdb_status pdb_relax(pdb_matrix m, pdb_precond pc, const double* b, double* x, int64_t sweeps,
+                             double* history) {
+  if (m == nullptr || pc == nullptr || b == nullptr || x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    require(sweeps >= 0, Errc::invalid_argument, "sweeps must be >= 0");
+    cudaStream_t s = default_stream();
+    const size_t n = static_cast<size_t>(m->a.n);
+    Scratch<double> db(std::max<size_t>(n, 1), s), dx(std::max<size_t>(n, 1), s);
+    Scratch<double> dh(static_cast<size_t>(sweeps + 1), s);
+    PDB_CUDA(cudaMemcpyAsync(db.get(), b, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    PDB_CUDA(cudaMemcpyAsync(dx.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    relax_device(m->a, *pc, db.get(), dx.get(), sweeps, history ? dh.get() : nullptr, s);
+    PDB_CUDA(cudaMemcpyAsync(x, dx.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (history)
+      PDB_CUDA(cudaMemcpyAsync(history, dh.get(), static_cast<size_t>(sweeps + 1) * sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+    sync(s);
+  });
+}
+
+PDB_API pdb_status pdb_relax_device(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
+                                    double* d_history, void* stream) {
+  if (m == nullptr || pc == nullptr || d_b == nullptr || d_x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    require(sweeps >= 0, Errc::invalid_argument, "sweeps must be >= 0");
+    relax_device(m->a, *pc, d_b, d_x, sweeps, d_history, stream_of(stream));
+  });
+}
+
+PDB_API void pdb_precond_free(pdb_precond pc) { delete pc; }
+
+/* ---- solvers ---- */
+
+PDB_API void pdb_gmres_options_init(pdb_gmres_options* opts) {
+  if (opts == nullptr) return;
+  opts->restart = 20;
+  opts->tol = 1e-8;
+  opts->max_iters = 2000;
+  opts->left_precond = 0;
+  opts->threads = 1;
+}
+
+PDB_API pdb_status pdb_gmres_solve(pdb_matrix m, const double* b, pdb_precond pc, const pdb_gmres_options* opts,
+                                   double* x, pdb_report* out_report) {
+  if (m == nullptr || b == nullptr || opts == nullptr || x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto rep = std::make_unique<pdb_report_s>();
+    gmres_device(m->a, b, pc, *opts, x, *rep, default_stream());
+    if (out_report != nullptr) *out_report = rep.release();
+  });
+}
+
+PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
+                                 double* x, pdb_report* out_report) {
+  if (m == nullptr || b == nullptr || x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto rep = std::make_unique<pdb_report_s>();
+    pcg_device(m->a, b, pc, tol, max_iters, x, *rep, default_stream());
+    if (out_report != nullptr) *out_report = rep.release();
+  });
+}
+
+PDB_API int64_t pdb_report_iterations(pdb_report rep) { return rep == nullptr ? 0 : rep->iterations; }
+PDB_API int64_t pdb_report_restarts(pdb_report rep) { return rep == nullptr ? 0 : rep->restarts; }
+PDB_API int pdb_report_converged(pdb_report rep) { return rep != nullptr && rep->converged ? 1 : 0; }
+PDB_API double pdb_report_final_relative_residual(pdb_report rep) {
+  return rep == nullptr ? 0.0 : rep->final_relative_residual;
+}
+PDB_API int64_t pdb_report_residual_history_size(pdb_report rep) {
+  return rep == nullptr ? 0 : static_cast<int64_t>(rep->residual_history.size());
+}
+PDB_API pdb_status pdb_report_residual_history(pdb_report rep, double* out) {
+  if (rep == nullptr || out == nullptr) return arg_error("null argument");
+  std::memcpy(out, rep->residual_history.data(), rep->residual_history.size() * sizeof(double));
+  return PDB_OK;
+}
+PDB_API void pdb_report_free(pdb_report rep) { delete rep; }
+
+/* ---- experiment drivers (reference experiments.cpp; outside the hot path) ---- */
+
+PDB_API pdb_status pdb_run_experiment(const char* config_json, const char* out_csv) {
+  if (config_json == nullptr || out_csv == nullptr) return arg_error("null argument");
+  return unsupported("pdb_run_experiment");
+}
+
+PDB_API pdb_status pdb_run_analyze(const char* config_json, const char* curve_csv, const char* histogram_csv) {
+  if (config_json == nullptr || curve_csv == nullptr || histogram_csv == nullptr) return arg_error("null argument");
+  return unsupported("pdb_run_analyze");
+}
+
+PDB_API pdb_status pdb_run_benchmark(const char* config_json, const char* out_csv) {
+  if (config_json == nullptr || out_csv == nullptr) return arg_error("null argument");
+  return unsupported("pdb_run_benchmark");
+}
+
+PDB_API pdb_status pdb_export_matrix(const char* config_json, const char* out_path) {
+  if (config_json == nullptr || out_path == nullptr) return arg_error("null argument");
+  return unsupported("pdb_export_matrix");
+}
+
+}  // extern "C"

@@ -1,0 +1,893 @@
+// Factorization database construction (reference compress.cpp, method
+// switch of pdb_database_build capi.cpp:249-284).
+//
+// All matrix arithmetic (extraction, distances, means, LU) runs in the
+// bit-exact kernels of kernels/{extract,criterion,lu}.cu; the host keeps the
+// integer bookkeeping the reference does serially (greedy round control,
+// k-means membership lists, reseed/prune, budget split).  Decisions are
+// therefore identical to the reference's: phi is bit-exact.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <random>
+
+#include <cub/cub.cuh>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace pdb {
+
+namespace {
+
+std::string fmt_f(double v) {  // std::to_string(double)
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%f", v);
+  return buf;
+}
+
+std::string singular_msg(int32_t status, double best) {
+  return "singular matrix: pivot " + fmt_f(best) + " below threshold in column " + std::to_string(status - 1);
+}
+
+template <typename T>
+std::vector<T> d2h(const T* d, size_t n, cudaStream_t s) {
+  std::vector<T> h(n);
+  if (n) PDB_CUDA(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return h;
+}
+
+template <typename T>
+void h2d(T* d, const std::vector<T>& h, cudaStream_t s) {
+  if (!h.empty()) PDB_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+}
+
+// LU of mats[src[t]] for t < count.  Returns index of the first failing t (or -1) and its message.
+int64_t lu_many(int64_t count, int ps, const double* mats, const int32_t* src, double* lu, int32_t* piv,
+                std::string& msg, BuildWork& work, cudaStream_t s, std::vector<int32_t>* status_out = nullptr,
+                std::vector<double>* best_out = nullptr) {
+  if (count <= 0) return -1;
+  Scratch<int32_t> status(static_cast<size_t>(count), s);
+  Scratch<double> best(static_cast<size_t>(count), s);
+  k::lu_batched(count, ps, mats, src, lu, piv, status.get(), best.get(), s);
+  PDB_LAUNCH_CHECK();
+  work.lu_count += count;
+  std::vector<int32_t> st = d2h(status.get(), static_cast<size_t>(count), s);
+  std::vector<double> bh = d2h(best.get(), static_cast<size_t>(count), s);
+  int64_t first = -1;
+  for (int64_t t = 0; t < count; ++t)
+    if (st[static_cast<size_t>(t)] != 0) {
+      first = t;
+      msg = singular_msg(st[static_cast<size_t>(t)], bh[static_cast<size_t>(t)]);
+      break;
+    }
+  if (status_out) *status_out = std::move(st);
+  if (best_out) *best_out = std::move(bh);
+  return first;
+}
+
+// Device entry storage with geometric growth.
+struct EntryStore {
+  int ps = 0;
+  int64_t len = 0, m = 0, cap = 0;
+  DevBuf<double> lu;
+  DevBuf<int32_t> piv;
+  void init(int ps_, int64_t cap0) {
+    ps = ps_;
+    len = static_cast<int64_t>(ps_) * ps_;
+    cap = std::max<int64_t>(cap0, 1);
+    lu.alloc(static_cast<size_t>(cap * len));
+    piv.alloc(static_cast<size_t>(cap * ps));
+  }
+  void reserve(int64_t need, cudaStream_t s) {
+    if (need <= cap) return;
+    int64_t nc = std::max(need, cap * 2);
+    DevBuf<double> l2(static_cast<size_t>(nc * len));
+    DevBuf<int32_t> p2(static_cast<size_t>(nc * ps));
+    if (m) {
+      PDB_CUDA(cudaMemcpyAsync(l2.get(), lu.get(), m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      PDB_CUDA(cudaMemcpyAsync(p2.get(), piv.get(), m * ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    sync(s);
+    lu = std::move(l2);
+    piv = std::move(p2);
+    cap = nc;
+  }
+};
+
+// ---------------------------------------------------------------- greedy --
+// greedy_impl (compress.cpp:40-95), exact round-batched form:
+//   U = patches unmatched so far (ascending).  Each round takes the first B
+//   of U as the batch S.  Every member of S was unmatched against all
+//   existing entries, so the sequential pass would now process S in order
+//   against entries created inside S only: greedy_resolve does exactly that.
+//   The rest of U (first-match) -- or every later patch (best-match) -- is
+//   then compared with the new entries only, in creation order.
+bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bool spectral, bool best_match,
+                  int64_t abort_above, pdb_database_s& out, cudaStream_t s) {
+  require(np >= 1, Errc::invalid_argument, "greedy_tolerance needs at least one patch");
+  require(eps > 0.0, Errc::invalid_argument, "tolerance must be positive");
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  BuildWork& work = out.work;
+  DevBuf<int32_t> phi(static_cast<size_t>(np));
+  PDB_CUDA(cudaMemsetAsync(phi.get(), 0xff, np * sizeof(int32_t), s));  // -1
+  DevBuf<double> best_d;
+  if (best_match) {
+    best_d.alloc(static_cast<size_t>(np));
+    std::vector<double> init(static_cast<size_t>(np), eps);
+    h2d(best_d.get(), init, s);
+  }
+  DevBuf<int32_t> creators(static_cast<size_t>(np));
+  DevBuf<int32_t> U(static_cast<size_t>(np)), U2(static_cast<size_t>(np));
+  k::iota(np, U.get(), s);
+  int64_t nu = np;
+  EntryStore store;
+  if (spectral) store.init(ps, std::min<int64_t>(np, 1024));
+  const int64_t Bmax = spectral ? 128 : 1024;
+  DevBuf<double> D(static_cast<size_t>(Bmax * Bmax));
+  DevBuf<int32_t> luS_status(static_cast<size_t>(Bmax));
+  DevBuf<double> luS, luS_best(static_cast<size_t>(Bmax));
+  DevBuf<int32_t> pivS;
+  if (spectral) {
+    luS.alloc(static_cast<size_t>(Bmax * len));
+    pivS.alloc(static_cast<size_t>(Bmax * ps));
+  }
+  DevBuf<int32_t> entry_of(static_cast<size_t>(Bmax));
+  DevBuf<int64_t> state(3);
+  DevBuf<uint8_t> flags(static_cast<size_t>(np));
+  DevBuf<int32_t> all_ids(static_cast<size_t>(np));
+  k::iota(np, all_ids.get(), s);
+  Scratch<unsigned long long> iters(1, s);
+  PDB_CUDA(cudaMemsetAsync(iters.get(), 0, sizeof(unsigned long long), s));
+  Scratch<int64_t> num_sel(1, s);
+  size_t sel_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, sel_bytes, U.get(), flags.get(), U2.get(), num_sel.get(), np, s);
+  Scratch<unsigned char> sel_tmp(sel_bytes, s);
+  auto select = [&](const int32_t* in, const uint8_t* fl, int32_t* o, int64_t n) -> int64_t {
+    if (n <= 0) return 0;
+    size_t b = sel_bytes;
+    cub::DeviceSelect::Flagged(sel_tmp.get(), b, in, fl, o, num_sel.get(), n, s);
+    int64_t c = 0;
+    PDB_CUDA(cudaMemcpyAsync(&c, num_sel.get(), sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    return c;
+  };
+  int64_t m = 0;
+  bool aborted = false;
+  std::vector<int64_t> state_h(3);
+  while (nu > 0) {
+    const int64_t B = std::min(nu, Bmax);
+    const int32_t* S = U.get();
+    // distances among the batch
+    if (spectral) {
+      std::string msg;
+      std::vector<int32_t> st;
+      lu_many(B, ps, mats.get(), S, luS.get(), pivS.get(), msg, work, s, &st);
+      h2d(luS_status.get(), st, s);
+      k::spectral_pairs(B, S, B, ps, mats.get(), luS.get(), pivS.get(), D.get(), iters.get(), s);
+    } else {
+      k::l1_pairs(B, S, B, static_cast<int>(len), mats.get(), S, nullptr, D.get(), s);
+    }
+    PDB_LAUNCH_CHECK();
+    work.pair_evals += B * (B - 1) / 2;
+    PDB_CUDA(cudaMemsetAsync(entry_of.get(), 0xff, B * sizeof(int32_t), s));
+    state_h = {m, 0, -1};
+    PDB_CUDA(cudaMemcpyAsync(state.get(), state_h.data(), 3 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k::greedy_resolve(static_cast<int>(B), S, D.get(), eps, best_match ? 1 : 0, abort_above,
+                      spectral ? luS_status.get() : nullptr, phi.get(), creators.get(), entry_of.get(), state.get(),
+                      s);
+    PDB_LAUNCH_CHECK();
+    PDB_CUDA(cudaMemcpyAsync(state_h.data(), state.get(), 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    const int64_t m_new = state_h[0];
+    if (spectral) {
+      // factors of the new entries (recomputed: bitwise identical to luS)
+      store.reserve(m_new, s);
+      std::string msg;
+      const int64_t bad = lu_many(m_new - m, ps, mats.get(), creators.get() + m, store.lu.get() + m * len,
+                                  store.piv.get() + m * ps, msg, work, s);
+      if (bad >= 0) fail(Errc::internal, "greedy: factor of a new entry failed after a successful batch factor");
+      store.m = m_new;
+      if (state_h[2] >= 0) {
+        const int64_t a = state_h[2];
+        std::vector<int32_t> sh = d2h(S + a, 1, s);
+        std::string msg2;
+        std::vector<int32_t> st;
+        std::vector<double> bst;
+        Scratch<double> tl(static_cast<size_t>(len), s);
+        Scratch<int32_t> tp(static_cast<size_t>(ps), s);
+        lu_many(1, ps, mats.get(), S + a, tl.get(), tp.get(), msg2, work, s, &st, &bst);
+        fail(Errc::singular_matrix, "patch " + std::to_string(sh[0]) + ": " + msg2);
+      }
+    }
+    if (state_h[1]) {
+      aborted = true;
+      m = m_new;
+      break;
+    }
+    // compare the remaining patches with the new entries [m, m_new)
+    if (m_new > m) {
+      int64_t nr = 0;
+      int32_t* R = U2.get();
+      if (best_match) {
+        // every patch above S[0] except the batch itself
+        std::vector<int32_t> s0 = d2h(S, 1, s);
+        std::vector<uint8_t> fl(static_cast<size_t>(np), 0);
+        for (int64_t i = s0[0] + 1; i < np; ++i) fl[static_cast<size_t>(i)] = 1;
+        std::vector<int32_t> Sh = d2h(S, static_cast<size_t>(B), s);
+        for (int32_t v : Sh) fl[static_cast<size_t>(v)] = 0;
+        h2d(flags.get(), fl, s);
+        nr = select(all_ids.get(), flags.get(), R, np);
+      } else {
+        nr = nu - B;
+        if (nr > 0)
+          PDB_CUDA(cudaMemcpyAsync(R, U.get() + B, nr * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      }
+      if (nr > 0) {
+        if (!spectral) {
+          k::l1_scan(nr, R, m, m_new, static_cast<int>(len), mats.get(), creators.get(), eps, best_match ? 1 : 0,
+                     phi.get(), best_d.get(), s);
+          PDB_LAUNCH_CHECK();
+          work.pair_evals += nr * (m_new - m);  // upper bound (early exit not counted)
+        } else {
+          // chunks of new entries; first-match drops matched patches between chunks
+          const int64_t CH = 16;
+          DevBuf<double> dch(static_cast<size_t>(nr * CH));
+          DevBuf<uint8_t> fl2(static_cast<size_t>(nr));
+          int64_t live = nr;
+          for (int64_t c0 = m; c0 < m_new && live > 0; c0 += CH) {
+            const int64_t ne = std::min(CH, m_new - c0);
+            k::spectral_pairs(live, R, ne, ps, mats.get(), store.lu.get() + c0 * len, store.piv.get() + c0 * ps,
+                              dch.get(), iters.get(), s);
+            k::apply_scan(live, R, c0, ne, dch.get(), creators.get(), eps, best_match ? 1 : 0, phi.get(),
+                          best_d.get(), s);
+            PDB_LAUNCH_CHECK();
+            work.pair_evals += live * ne;
+            if (!best_match && c0 + CH < m_new) {
+              // keep unmatched
+              std::vector<int32_t> ph = d2h(phi.get(), static_cast<size_t>(np), s);
+              std::vector<int32_t> Rh = d2h(R, static_cast<size_t>(live), s);
+              std::vector<int32_t> keep;
+              keep.reserve(Rh.size());
+              for (int32_t v : Rh)
+                if (ph[static_cast<size_t>(v)] < 0) keep.push_back(v);
+              live = static_cast<int64_t>(keep.size());
+              h2d(R, keep, s);
+            }
+          }
+        }
+      }
+    }
+    m = m_new;
+    // U <- unmatched patches among U[B..nu)
+    const int64_t rest = nu - B;
+    if (rest > 0) {
+      std::vector<int32_t> ph = d2h(phi.get(), static_cast<size_t>(np), s);
+      std::vector<int32_t> Uh = d2h(U.get() + B, static_cast<size_t>(rest), s);
+      std::vector<int32_t> keep;
+      keep.reserve(Uh.size());
+      for (int32_t v : Uh)
+        if (ph[static_cast<size_t>(v)] < 0) keep.push_back(v);
+      nu = static_cast<int64_t>(keep.size());
+      h2d(U.get(), keep, s);
+    } else {
+      nu = 0;
+    }
+  }
+  unsigned long long it_h = 0;
+  PDB_CUDA(cudaMemcpyAsync(&it_h, iters.get(), sizeof(it_h), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  work.power_iters += static_cast<int64_t>(it_h);
+
+  out.m = m;
+  out.np = np;
+  out.ps = ps;
+  out.eps = eps;
+  out.method = spectral ? "greedy" : "greedy-l1";
+  out.reps.alloc(static_cast<size_t>(std::max<int64_t>(m, 1) * len));
+  k::gather_mats(m, creators.get(), len, mats.get(), out.reps.get(), s);
+  out.lu.alloc(static_cast<size_t>(std::max<int64_t>(m, 1) * len));
+  out.piv.alloc(static_cast<size_t>(std::max<int64_t>(m, 1) * ps));
+  if (spectral) {
+    if (m) {
+      PDB_CUDA(cudaMemcpyAsync(out.lu.get(), store.lu.get(), m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      PDB_CUDA(cudaMemcpyAsync(out.piv.get(), store.piv.get(), m * ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
+    // factor_patch at entry creation (compress.cpp:91): first failure in creation order wins,
+    // and it precedes an abort that happens later in the sequence.
+    std::string msg;
+    const int64_t bad = lu_many(m, ps, mats.get(), creators.get(), out.lu.get(), out.piv.get(), msg, work, s);
+    if (bad >= 0) {
+      std::vector<int32_t> cr = d2h(creators.get() + bad, 1, s);
+      fail(Errc::singular_matrix, "patch " + std::to_string(cr[0]) + ": " + msg);
+    }
+  }
+  out.phi = std::move(phi);
+  sync(s);
+  return !aborted;
+}
+
+// ---------------------------------------------------------------- exact ---
+void exact_build(const DevBuf<double>& mats, int64_t np, int ps, pdb_database_s& out, cudaStream_t s) {
+  require(np >= 1, Errc::invalid_argument, "exact_database needs at least one patch");
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  out.m = np;
+  out.np = np;
+  out.ps = ps;
+  out.method = "exact";
+  out.reps.alloc(static_cast<size_t>(np * len));
+  PDB_CUDA(cudaMemcpyAsync(out.reps.get(), mats.get(), np * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  out.lu.alloc(static_cast<size_t>(np * len));
+  out.piv.alloc(static_cast<size_t>(np * ps));
+  std::string msg;
+  const int64_t bad = lu_many(np, ps, mats.get(), nullptr, out.lu.get(), out.piv.get(), msg, out.work, s);
+  if (bad >= 0) fail(Errc::singular_matrix, "patch " + std::to_string(bad) + ": " + msg);
+  out.phi.alloc(static_cast<size_t>(np));
+  k::iota(np, out.phi.get(), s);
+  sync(s);
+}
+
+// --------------------------------------------------------------- k-means --
+enum class Variant { Entrywise, Spectral, VarMin };
+enum class Empty { Reseed, Prune };
+
+std::string variant_name(Variant v) {
+  switch (v) {
+    case Variant::Entrywise: return "kmeans-entrywise";
+    case Variant::Spectral: return "kmeans-spectral";
+    case Variant::VarMin: return "kmeans-varmin";
+  }
+  return "kmeans";
+}
+
+struct KDb {
+  int ps = 0;
+  int64_t len = 0, m = 0;
+  DevBuf<double> reps, lu;
+  DevBuf<int32_t> piv;
+  std::vector<char> has_factor;
+};
+
+// Factors of every patch of the group, computed once (VarMin candidates).
+struct PatchFactors {
+  bool ready = false;
+  DevBuf<double> lu;
+  DevBuf<int32_t> piv;
+  std::vector<int32_t> status;
+  std::vector<double> best;
+};
+
+void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf, BuildWork& work, cudaStream_t s) {
+  if (pf.ready) return;
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  pf.lu.alloc(static_cast<size_t>(n * len));
+  pf.piv.alloc(static_cast<size_t>(n * ps));
+  std::string msg;
+  lu_many(n, ps, sub, nullptr, pf.lu.get(), pf.piv.get(), msg, work, s, &pf.status, &pf.best);
+  pf.ready = true;
+}
+
+// kmeans_loop (compress.cpp:138-262).  phi_h receives the final assignment.
+void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max_iters, Empty policy,
+                 std::vector<int32_t>& phi_h, PatchFactors& pf, BuildWork& work, cudaStream_t s) {
+  const int ps = db.ps;
+  const int64_t len = db.len;
+  phi_h.assign(static_cast<size_t>(n), -1);
+  std::vector<double> min_dist(static_cast<size_t>(n), 0.0);
+  DevBuf<int32_t> d_phi(static_cast<size_t>(n)), d_new(static_cast<size_t>(n));
+  DevBuf<double> d_min(static_cast<size_t>(n));
+  h2d(d_phi.get(), phi_h, s);
+  Scratch<int32_t> changed(1, s);
+  Scratch<unsigned long long> iters(1, s);
+  PDB_CUDA(cudaMemsetAsync(iters.get(), 0, sizeof(unsigned long long), s));
+  DevBuf<double> dist;
+  for (int iter = 0; iter < max_iters; ++iter) {
+    const int64_t m = db.m;
+    PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
+    if (variant == Variant::Entrywise) {
+      k::l1_argmin(n, m, static_cast<int>(len), sub, db.reps.get(), d_phi.get(), d_new.get(), d_min.get(),
+                   changed.get(), s);
+    } else {
+      if (dist.size() < static_cast<size_t>(n * m)) dist.alloc(static_cast<size_t>(n * m));
+      k::spectral_pairs(n, nullptr, m, ps, sub, db.lu.get(), db.piv.get(), dist.get(), iters.get(), s);
+      k::argmin_assign(n, m, dist.get(), d_phi.get(), d_new.get(), d_min.get(), changed.get(), s);
+    }
+    PDB_LAUNCH_CHECK();
+    work.pair_evals += n * m;
+    int32_t ch = 0;
+    PDB_CUDA(cudaMemcpyAsync(&ch, changed.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    phi_h = d2h(d_new.get(), static_cast<size_t>(n), s);
+    if (!ch) break;
+    min_dist = d2h(d_min.get(), static_cast<size_t>(n), s);
+
+    std::vector<std::vector<int32_t>> members(static_cast<size_t>(m));
+    for (int64_t i = 0; i < n; ++i) members[static_cast<size_t>(phi_h[static_cast<size_t>(i)])].push_back(static_cast<int32_t>(i));
+
+    if (policy == Empty::Prune) {  // compress.cpp:179-194
+      std::vector<int32_t> remap(static_cast<size_t>(m), -1), kept_ids;
+      int64_t kept = 0;
+      for (int64_t j = 0; j < m; ++j)
+        if (!members[static_cast<size_t>(j)].empty()) {
+          remap[static_cast<size_t>(j)] = static_cast<int32_t>(kept);
+          kept_ids.push_back(static_cast<int32_t>(j));
+          if (kept != j) {
+            members[static_cast<size_t>(kept)] = std::move(members[static_cast<size_t>(j)]);
+            db.has_factor[static_cast<size_t>(kept)] = db.has_factor[static_cast<size_t>(j)];
+          }
+          ++kept;
+        }
+      if (kept != m) {
+        Scratch<int32_t> ids(static_cast<size_t>(kept), s);
+        h2d(ids.get(), kept_ids, s);
+        DevBuf<double> r2(static_cast<size_t>(kept * len)), l2(static_cast<size_t>(kept * len));
+        DevBuf<int32_t> p2(static_cast<size_t>(kept * ps));
+        k::gather_mats(kept, ids.get(), len, db.reps.get(), r2.get(), s);
+        k::gather_mats(kept, ids.get(), len, db.lu.get(), l2.get(), s);
+        k::gather_i32(kept, ids.get(), ps, db.piv.get(), p2.get(), s);
+        sync(s);
+        db.reps = std::move(r2);
+        db.lu = std::move(l2);
+        db.piv = std::move(p2);
+      }
+      members.resize(static_cast<size_t>(kept));
+      db.has_factor.resize(static_cast<size_t>(kept));
+      db.m = kept;
+      for (int64_t i = 0; i < n; ++i)
+        phi_h[static_cast<size_t>(i)] = remap[static_cast<size_t>(phi_h[static_cast<size_t>(i)])];
+    } else {  // reseed, compress.cpp:195-217
+      for (int64_t j = 0; j < m; ++j) {
+        if (!members[static_cast<size_t>(j)].empty()) continue;
+        int64_t far = -1;
+        double far_d = -1.0;
+        for (int64_t i = 0; i < n; ++i) {
+          const int32_t owner = phi_h[static_cast<size_t>(i)];
+          if (members[static_cast<size_t>(owner)].size() <= 1) continue;
+          if (min_dist[static_cast<size_t>(i)] > far_d) {
+            far_d = min_dist[static_cast<size_t>(i)];
+            far = i;
+          }
+        }
+        if (far < 0) continue;
+        const int32_t owner = phi_h[static_cast<size_t>(far)];
+        auto& own = members[static_cast<size_t>(owner)];
+        own.erase(std::find(own.begin(), own.end(), static_cast<int32_t>(far)));
+        members[static_cast<size_t>(j)].push_back(static_cast<int32_t>(far));
+        phi_h[static_cast<size_t>(far)] = static_cast<int32_t>(j);
+        min_dist[static_cast<size_t>(far)] = 0.0;
+      }
+    }
+    h2d(d_phi.get(), phi_h, s);
+
+    // representative update (compress.cpp:219-261); failures re-raised as
+    // singular_matrix "cluster j: ..." for the lowest failing j.
+    const int64_t mc = db.m;
+    if (variant == Variant::VarMin) {
+      ensure_patch_factors(sub, n, ps, pf, work, s);
+      std::vector<int32_t> best_c(static_cast<size_t>(mc), -1);
+      for (int64_t j = 0; j < mc; ++j) {
+        const auto& mem = members[static_cast<size_t>(j)];
+        for (int32_t c : mem)
+          if (pf.status[static_cast<size_t>(c)] != 0)
+            fail(Errc::singular_matrix, "cluster " + std::to_string(j) + ": patch " + std::to_string(c) + ": " +
+                                            singular_msg(pf.status[static_cast<size_t>(c)], pf.best[static_cast<size_t>(c)]));
+        if (mem.empty()) fail(Errc::singular_matrix, "cluster " + std::to_string(j) + ": empty cluster");
+      }
+      // all (k, c) pairs per cluster, in chunks
+      const int64_t chunk_pairs = int64_t{1} << 22;
+      std::vector<int32_t> pa, fb;
+      for (int64_t j = 0; j < mc; ++j) {
+        const auto& mem = members[static_cast<size_t>(j)];
+        const int64_t cs = static_cast<int64_t>(mem.size());
+        double best_var = std::numeric_limits<double>::infinity();
+        int32_t bc = -1;
+        // candidates processed in groups so each launch has <= chunk_pairs pairs
+        const int64_t cand_per = std::max<int64_t>(1, chunk_pairs / std::max<int64_t>(cs, 1));
+        for (int64_t c0 = 0; c0 < cs; c0 += cand_per) {
+          const int64_t cn = std::min(cand_per, cs - c0);
+          pa.resize(static_cast<size_t>(cn * cs));
+          fb.resize(static_cast<size_t>(cn * cs));
+          for (int64_t ci = 0; ci < cn; ++ci)
+            for (int64_t kk = 0; kk < cs; ++kk) {
+              pa[static_cast<size_t>(ci * cs + kk)] = mem[static_cast<size_t>(kk)];
+              fb[static_cast<size_t>(ci * cs + kk)] = mem[static_cast<size_t>(c0 + ci)];
+            }
+          Scratch<int32_t> dpa(pa.size(), s), dfb(fb.size(), s);
+          Scratch<double> dd(pa.size(), s);
+          h2d(dpa.get(), pa, s);
+          h2d(dfb.get(), fb, s);
+          k::spectral_list(static_cast<int64_t>(pa.size()), dpa.get(), dfb.get(), ps, sub, pf.lu.get(), pf.piv.get(),
+                           dd.get(), iters.get(), s);
+          PDB_LAUNCH_CHECK();
+          work.pair_evals += static_cast<int64_t>(pa.size());
+          std::vector<double> dh = d2h(dd.get(), pa.size(), s);
+          for (int64_t ci = 0; ci < cn; ++ci) {
+            double var = 0.0;
+            for (int64_t kk = 0; kk < cs; ++kk) {
+              const double dv = dh[static_cast<size_t>(ci * cs + kk)];
+              var += dv * dv;
+            }
+            if (var < best_var) {
+              best_var = var;
+              bc = mem[static_cast<size_t>(c0 + ci)];
+            }
+          }
+        }
+        best_c[static_cast<size_t>(j)] = bc;
+      }
+      Scratch<int32_t> ids(static_cast<size_t>(mc), s);
+      h2d(ids.get(), best_c, s);
+      k::gather_mats(mc, ids.get(), len, sub, db.reps.get(), s);
+      k::gather_mats(mc, ids.get(), len, pf.lu.get(), db.lu.get(), s);
+      k::gather_i32(mc, ids.get(), ps, pf.piv.get(), db.piv.get(), s);
+      for (int64_t j = 0; j < mc; ++j) db.has_factor[static_cast<size_t>(j)] = 1;
+    } else {
+      for (int64_t j = 0; j < mc; ++j)
+        if (members[static_cast<size_t>(j)].empty())
+          fail(Errc::singular_matrix, "cluster " + std::to_string(j) + ": entrywise_mean of an empty cluster");
+      std::vector<int32_t> mem_ptr(static_cast<size_t>(mc + 1), 0), mem;
+      mem.reserve(static_cast<size_t>(n));
+      for (int64_t j = 0; j < mc; ++j) {
+        mem.insert(mem.end(), members[static_cast<size_t>(j)].begin(), members[static_cast<size_t>(j)].end());
+        mem_ptr[static_cast<size_t>(j + 1)] = static_cast<int32_t>(mem.size());
+      }
+      Scratch<int32_t> dptr(mem_ptr.size(), s), dmem(std::max<size_t>(mem.size(), 1), s);
+      h2d(dptr.get(), mem_ptr, s);
+      h2d(dmem.get(), mem, s);
+      k::cluster_mean(mc, static_cast<int>(len), dptr.get(), dmem.get(), sub, db.reps.get(), s);
+      PDB_LAUNCH_CHECK();
+      if (variant == Variant::Spectral) {
+        std::string msg;
+        const int64_t bad = lu_many(mc, ps, db.reps.get(), nullptr, db.lu.get(), db.piv.get(), msg, work, s);
+        if (bad >= 0) fail(Errc::singular_matrix, "cluster " + std::to_string(bad) + ": " + msg);
+        for (int64_t j = 0; j < mc; ++j) db.has_factor[static_cast<size_t>(j)] = 1;
+      } else {
+        for (int64_t j = 0; j < mc; ++j) db.has_factor[static_cast<size_t>(j)] = 0;
+      }
+      sync(s);
+    }
+  }
+  unsigned long long it_h = 0;
+  PDB_CUDA(cudaMemcpyAsync(&it_h, iters.get(), sizeof(it_h), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  work.power_iters += static_cast<int64_t>(it_h);
+}
+
+// finalize_factors (compress.cpp:266-278).
+void finalize_factors(KDb& db, BuildWork& work, cudaStream_t s) {
+  std::vector<int32_t> need;
+  for (int64_t j = 0; j < db.m; ++j)
+    if (!db.has_factor[static_cast<size_t>(j)]) need.push_back(static_cast<int32_t>(j));
+  if (need.empty()) return;
+  const int64_t cnt = static_cast<int64_t>(need.size());
+  Scratch<int32_t> ids(need.size(), s);
+  h2d(ids.get(), need, s);
+  Scratch<double> lu(static_cast<size_t>(cnt * db.len), s);
+  Scratch<int32_t> piv(static_cast<size_t>(cnt * db.ps), s);
+  std::string msg;
+  const int64_t bad = lu_many(cnt, db.ps, db.reps.get(), ids.get(), lu.get(), piv.get(), msg, work, s);
+  if (bad >= 0) fail(Errc::singular_matrix, "cluster " + std::to_string(need[static_cast<size_t>(bad)]) + ": " + msg);
+  // scatter back (need is ascending; contiguous in the common all-entries case)
+  for (int64_t t = 0; t < cnt; ++t) {
+    const int64_t j = need[static_cast<size_t>(t)];
+    PDB_CUDA(cudaMemcpyAsync(db.lu.get() + j * db.len, lu.get() + t * db.len, db.len * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+    PDB_CUDA(cudaMemcpyAsync(db.piv.get() + j * db.ps, piv.get() + t * db.ps, db.ps * sizeof(int32_t),
+                             cudaMemcpyDeviceToDevice, s));
+    db.has_factor[static_cast<size_t>(j)] = 1;
+  }
+  sync(s);
+}
+
+// kmeans (compress.cpp:294-324) on a contiguous group of n patch matrices.
+void kmeans_group(const double* sub, int64_t n, int ps, int64_t m_p, Variant variant, uint64_t seed, int max_iters,
+                  KDb& db, std::vector<int32_t>& phi_h, BuildWork& work, cudaStream_t s) {
+  require(n >= 1, Errc::invalid_argument, "kmeans needs at least one patch");
+  require(m_p >= 1 && m_p <= n, Errc::invalid_argument, "kmeans requires 1 <= m_p <= n_p");
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  std::mt19937_64 rng(seed);
+  std::vector<int32_t> perm(static_cast<size_t>(n));
+  std::iota(perm.begin(), perm.end(), 0);
+  for (int64_t i = 0; i < m_p; ++i) {
+    const int64_t j = i + static_cast<int64_t>(rng() % static_cast<uint64_t>(n - i));
+    std::swap(perm[static_cast<size_t>(i)], perm[static_cast<size_t>(j)]);
+  }
+  db.ps = ps;
+  db.len = len;
+  db.m = m_p;
+  db.reps.alloc(static_cast<size_t>(m_p * len));
+  db.lu.alloc(static_cast<size_t>(m_p * len));
+  db.piv.alloc(static_cast<size_t>(m_p * ps));
+  db.has_factor.assign(static_cast<size_t>(m_p), 0);
+  std::vector<int32_t> picks(perm.begin(), perm.begin() + m_p);
+  Scratch<int32_t> ids(picks.size(), s);
+  h2d(ids.get(), picks, s);
+  k::gather_mats(m_p, ids.get(), len, sub, db.reps.get(), s);
+  if (variant != Variant::Entrywise) {
+    std::string msg;
+    const int64_t bad = lu_many(m_p, ps, db.reps.get(), nullptr, db.lu.get(), db.piv.get(), msg, work, s);
+    if (bad >= 0) fail(Errc::singular_matrix, "patch " + std::to_string(picks[static_cast<size_t>(bad)]) + ": " + msg);
+    std::fill(db.has_factor.begin(), db.has_factor.end(), 1);
+  }
+  PatchFactors pf;
+  kmeans_loop(sub, n, db, variant, max_iters, Empty::Reseed, phi_h, pf, work, s);
+  finalize_factors(db, work, s);
+}
+
+}  // namespace
+
+// split_budget (compress.cpp:336-392).
+std::vector<int64_t> split_budget(int64_t m_p, const std::vector<int64_t>& sizes) {
+  const int64_t parts = static_cast<int64_t>(sizes.size());
+  require(parts >= 1, Errc::invalid_argument, "no partitions");
+  int64_t total = 0;
+  for (int64_t v : sizes) total += v;
+  require(m_p >= parts, Errc::budget_too_small, "database budget smaller than the number of boundary partitions");
+  require(m_p <= total, Errc::invalid_argument, "database budget larger than the number of patches");
+  std::vector<int64_t> alloc(static_cast<size_t>(parts), 0);
+  std::vector<double> rem(static_cast<size_t>(parts), 0.0);
+  int64_t assigned = 0;
+  for (int64_t p = 0; p < parts; ++p) {
+    const double quota = static_cast<double>(m_p) * static_cast<double>(sizes[static_cast<size_t>(p)]) / static_cast<double>(total);
+    alloc[static_cast<size_t>(p)] = static_cast<int64_t>(std::floor(quota));
+    rem[static_cast<size_t>(p)] = quota - std::floor(quota);
+    assigned += alloc[static_cast<size_t>(p)];
+  }
+  std::vector<int64_t> order(static_cast<size_t>(parts));
+  std::iota(order.begin(), order.end(), int64_t{0});
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t x, int64_t y) { return rem[static_cast<size_t>(x)] > rem[static_cast<size_t>(y)]; });
+  for (int64_t k = 0; assigned < m_p; ++k) {
+    ++alloc[static_cast<size_t>(order[static_cast<size_t>(k % parts)])];
+    ++assigned;
+  }
+  auto take_from_largest = [&](int64_t needy) {
+    int64_t donor = -1;
+    for (int64_t p = 0; p < parts; ++p)
+      if (alloc[static_cast<size_t>(p)] >= 2 && (donor < 0 || alloc[static_cast<size_t>(p)] > alloc[static_cast<size_t>(donor)]))
+        donor = p;
+    require(donor >= 0, Errc::budget_too_small, "cannot satisfy one cluster per partition");
+    --alloc[static_cast<size_t>(donor)];
+    ++alloc[static_cast<size_t>(needy)];
+  };
+  for (int64_t p = 0; p < parts; ++p)
+    while (alloc[static_cast<size_t>(p)] == 0) take_from_largest(p);
+  for (int64_t p = 0; p < parts; ++p)
+    while (alloc[static_cast<size_t>(p)] > sizes[static_cast<size_t>(p)]) {
+      --alloc[static_cast<size_t>(p)];
+      int64_t recv = -1;
+      double best_rem = -1.0;
+      for (int64_t q = 0; q < parts; ++q)
+        if (alloc[static_cast<size_t>(q)] < sizes[static_cast<size_t>(q)] && rem[static_cast<size_t>(q)] > best_rem) {
+          best_rem = rem[static_cast<size_t>(q)];
+          recv = q;
+        }
+      require(recv >= 0, Errc::invalid_argument, "budget exceeds total patch count");
+      ++alloc[static_cast<size_t>(recv)];
+    }
+  return alloc;
+}
+
+namespace {
+
+// boundary_partition (patch.cpp:113-126): groups in first-occurrence order.
+void boundary_partition(const DevBuf<double>& mats, int64_t np, int ps, std::vector<std::vector<int32_t>>& groups,
+                        std::vector<std::vector<uint8_t>>& patterns, cudaStream_t s) {
+  require(np >= 1, Errc::invalid_argument, "boundary_partition needs at least one patch");
+  const int words = (ps + 63) / 64;
+  Scratch<unsigned long long> masks(static_cast<size_t>(np * words), s);
+  k::boundary_masks(np, ps, mats.get(), words, masks.get(), s);
+  PDB_LAUNCH_CHECK();
+  std::vector<unsigned long long> mh = d2h(masks.get(), static_cast<size_t>(np * words), s);
+  std::map<std::vector<unsigned long long>, size_t> index;
+  std::vector<unsigned long long> key(static_cast<size_t>(words));
+  for (int64_t k = 0; k < np; ++k) {
+    std::copy(mh.begin() + k * words, mh.begin() + (k + 1) * words, key.begin());
+    auto it = index.find(key);
+    if (it == index.end()) {
+      it = index.emplace(key, groups.size()).first;
+      groups.emplace_back();
+      std::vector<uint8_t> pat(static_cast<size_t>(ps));
+      for (int i = 0; i < ps; ++i) pat[static_cast<size_t>(i)] = (key[static_cast<size_t>(i / 64)] >> (i % 64)) & 1ull;
+      patterns.push_back(std::move(pat));
+    }
+    groups[it->second].push_back(static_cast<int32_t>(k));
+  }
+}
+
+// partitioned_build (compress.cpp:394-421).
+void partitioned_build(const DevBuf<double>& mats, int64_t np, int ps, int64_t m_p, Variant variant, uint64_t seed,
+                       int max_iters, pdb_database_s& out, cudaStream_t s) {
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  std::vector<std::vector<int32_t>> groups;
+  std::vector<std::vector<uint8_t>> patterns;
+  boundary_partition(mats, np, ps, groups, patterns, s);
+  std::vector<int64_t> sizes;
+  for (const auto& g : groups) sizes.push_back(static_cast<int64_t>(g.size()));
+  const std::vector<int64_t> alloc = split_budget(m_p, sizes);
+  std::vector<KDb> parts(groups.size());
+  std::vector<int32_t> phi(static_cast<size_t>(np), -1);
+  int64_t total = 0;
+  DevBuf<double> sub;
+  for (size_t g = 0; g < groups.size(); ++g) {
+    const int64_t cnt = static_cast<int64_t>(groups[g].size());
+    sub.alloc(static_cast<size_t>(cnt * len));
+    Scratch<int32_t> ids(static_cast<size_t>(cnt), s);
+    h2d(ids.get(), groups[g], s);
+    k::gather_mats(cnt, ids.get(), len, mats.get(), sub.get(), s);
+    std::vector<int32_t> lphi;
+    kmeans_group(sub.get(), cnt, ps, alloc[g], variant, seed + static_cast<uint64_t>(g), max_iters, parts[g], lphi,
+                 out.work, s);
+    for (int64_t q = 0; q < cnt; ++q)
+      phi[static_cast<size_t>(groups[g][static_cast<size_t>(q)])] = static_cast<int32_t>(total + lphi[static_cast<size_t>(q)]);
+    total += parts[g].m;
+  }
+  out.m = total;
+  out.np = np;
+  out.ps = ps;
+  out.method = variant_name(variant) + "-partitioned";
+  out.reps.alloc(static_cast<size_t>(total * len));
+  out.lu.alloc(static_cast<size_t>(total * len));
+  out.piv.alloc(static_cast<size_t>(total * ps));
+  int64_t off = 0;
+  out.entry_patterns.clear();
+  for (size_t g = 0; g < groups.size(); ++g) {
+    const int64_t m = parts[g].m;
+    PDB_CUDA(cudaMemcpyAsync(out.reps.get() + off * len, parts[g].reps.get(), m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    PDB_CUDA(cudaMemcpyAsync(out.lu.get() + off * len, parts[g].lu.get(), m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    PDB_CUDA(cudaMemcpyAsync(out.piv.get() + off * ps, parts[g].piv.get(), m * ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    for (int64_t j = 0; j < m; ++j) out.entry_patterns.push_back(patterns[g]);
+    off += m;
+  }
+  out.phi.alloc(static_cast<size_t>(np));
+  h2d(out.phi.get(), phi, s);
+  sync(s);
+}
+
+// bootstrapped (compress.cpp:326-334): greedy (spectral, first match), then
+// Lloyd iterations with pruning, then factors for any entry without one.
+void bootstrap_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, int max_iters, pdb_database_s& out,
+                     cudaStream_t s) {
+  pdb_database_s g;
+  greedy_build(mats, np, ps, eps, true, false, -1, g, s);
+  out.work = g.work;
+  KDb db;
+  db.ps = ps;
+  db.len = static_cast<int64_t>(ps) * ps;
+  db.m = g.m;
+  db.reps = std::move(g.reps);
+  db.lu = std::move(g.lu);
+  db.piv = std::move(g.piv);
+  db.has_factor.assign(static_cast<size_t>(db.m), 1);
+  std::vector<int32_t> phi_h;
+  PatchFactors pf;
+  kmeans_loop(mats.get(), np, db, Variant::VarMin, max_iters, Empty::Prune, phi_h, pf, out.work, s);
+  finalize_factors(db, out.work, s);
+  out.m = db.m;
+  out.np = np;
+  out.ps = ps;
+  out.eps = eps;
+  out.method = "bootstrap-kmeans-varmin";
+  out.reps = std::move(db.reps);
+  out.lu = std::move(db.lu);
+  out.piv = std::move(db.piv);
+  out.phi.alloc(static_cast<size_t>(np));
+  h2d(out.phi.get(), phi_h, s);
+  sync(s);
+}
+
+}  // namespace
+
+bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps, const BuildParams& p,
+                              pdb_database_s& out, cudaStream_t s) {
+  const int ips = static_cast<int>(ps);
+  switch (p.method) {
+    case PDB_METHOD_EXACT: exact_build(mats, np, ips, out, s); return true;
+    case PDB_METHOD_GREEDY_SPECTRAL:
+      return greedy_build(mats, np, ips, p.eps, true, p.best_match, p.abort_above, out, s);
+    case PDB_METHOD_GREEDY_L1:
+      return greedy_build(mats, np, ips, p.eps, false, p.best_match, p.abort_above, out, s);
+    case PDB_METHOD_KMEANS_ENTRYWISE:
+      partitioned_build(mats, np, ips, p.db_size, Variant::Entrywise, p.seed, p.max_iters, out, s);
+      return true;
+    case PDB_METHOD_KMEANS_SPECTRAL:
+      partitioned_build(mats, np, ips, p.db_size, Variant::Spectral, p.seed, p.max_iters, out, s);
+      return true;
+    case PDB_METHOD_KMEANS_VARMIN:
+      partitioned_build(mats, np, ips, p.db_size, Variant::VarMin, p.seed, p.max_iters, out, s);
+      return true;
+    case PDB_METHOD_BOOTSTRAP: bootstrap_build(mats, np, ips, p.eps, p.max_iters, out, s); return true;
+    default: fail(Errc::invalid_argument, "unknown compression method");
+  }
+}
+
+bool build_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, pdb_database_s& out,
+                    cudaStream_t s) {
+  require_device();
+  DevBuf<double> mats;
+  extract_patches(a, ps, mats, s);
+  return build_database_from_mats(mats, ps.np, ps.ps, p, out, s);
+}
+
+// greedy_bisect_to_size (experiments.cpp:168-204).
+double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, int64_t target_lo,
+                       int64_t target_hi, pdb_database_s& out, cudaStream_t s) {
+  require(p.method == PDB_METHOD_GREEDY_L1 || p.method == PDB_METHOD_GREEDY_SPECTRAL, Errc::invalid_argument,
+          "size bisection needs a greedy method");
+  require_device();
+  DevBuf<double> mats;
+  extract_patches(a, ps, mats, s);
+  const int64_t n_p = ps.np;
+  target_lo = std::max<int64_t>(1, std::min(target_lo, n_p));
+  target_hi = std::max(target_lo, std::min(target_hi, n_p));
+  double lo = 1e-14, hi = 1e10;
+  int64_t best_gap = std::numeric_limits<int64_t>::max();
+  double best_eps = 0.0;
+  BuildWork total;
+  for (int it = 0; it < 60; ++it) {
+    const double eps = std::sqrt(lo * hi);
+    BuildParams q = p;
+    q.eps = eps;
+    q.abort_above = target_hi;
+    pdb_database_s db;
+    const bool ok = greedy_build(mats, n_p, static_cast<int>(ps.ps), eps, p.method == PDB_METHOD_GREEDY_SPECTRAL,
+                                 p.best_match, target_hi, db, s);
+    total.pair_evals += db.work.pair_evals;
+    total.power_iters += db.work.power_iters;
+    total.lu_count += db.work.lu_count;
+    if (!ok) {
+      lo = eps;
+      continue;
+    }
+    const int64_t size = db.m;
+    const int64_t gap = size < target_lo ? target_lo - size : (size > target_hi ? size - target_hi : 0);
+    if (gap < best_gap) {
+      best_gap = gap;
+      out = std::move(db);
+      best_eps = eps;
+      if (gap == 0) break;
+    }
+    if (size < target_lo) hi = eps;
+    else lo = eps;
+  }
+  require(best_gap != std::numeric_limits<int64_t>::max(), Errc::invalid_argument, "greedy bisection found no database");
+  out.work = total;
+  return best_eps;
+}
+
+// export_database (compress.cpp:458-485): raw representatives + JSON index.
+void export_database(const pdb_database_s& db, const std::string& json_path, const std::string& bin_path,
+                     cudaStream_t s) {
+  const std::vector<double> reps = db.reps.to_host(s);
+  std::ofstream bin(bin_path, std::ios::binary);
+  if (!bin) fail(Errc::io_error, "cannot open '" + bin_path + "' for writing");
+  bin.write(reinterpret_cast<const char*>(reps.data()),
+            static_cast<std::streamsize>(static_cast<size_t>(db.m * db.ps * db.ps) * sizeof(double)));
+  if (!bin) fail(Errc::io_error, "error while writing '" + bin_path + "'");
+  const std::vector<int32_t> phi = db.phi.to_host(s);
+  std::ofstream out(json_path);
+  if (!out) fail(Errc::io_error, "cannot open '" + json_path + "' for writing");
+  out << "{\n  \"method\": \"" << db.method << "\",\n  \"eps\": " << db.eps << ",\n  \"m_p\": " << db.m
+      << ",\n  \"n_p\": " << db.np << ",\n  \"entries\": [";
+  for (int64_t j = 0; j < db.m; ++j) {
+    out << (j == 0 ? "\n    " : ",\n    ");
+    out << "{\"rows\": " << db.ps << ", \"cols\": " << db.ps;
+    if (!db.entry_patterns.empty()) {
+      out << ", \"partition\": \"";
+      for (uint8_t b : db.entry_patterns[static_cast<size_t>(j)]) out << (b ? '1' : '0');
+      out << "\"";
+    }
+    out << "}";
+  }
+  out << "\n  ],\n  \"phi\": [";
+  for (int64_t k = 0; k < db.np; ++k) out << (k == 0 ? "" : ", ") << phi[static_cast<size_t>(k)];
+  out << "]\n}\n";
+  if (!out) fail(Errc::io_error, "error while writing '" + json_path + "'");
+}
+
+}  // namespace pdb

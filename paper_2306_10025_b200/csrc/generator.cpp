@@ -1,0 +1,376 @@
+// Seeded synthetic inputs for the BASELINE.json configurations.
+//
+// The reference's assembler (fem.cpp:248-346) only builds uniform meshes
+// with a manufactured right-hand side, so the jittered / random-coefficient
+// configs are produced here.  Discretisation conventions
+// follow the reference so that patch detection behaves identically:
+//   * Q_p Lagrange on equispaced nodes, DoFs lexicographic with x fastest on
+//     the (cells*p+1)^dim lattice (fem.hpp:12-35, fem.cpp:71-86);
+//   * tensor Gauss-Legendre with p+1 points per axis (fem.cpp:255);
+//   * Dirichlet rows replaced by identity rows WITHOUT column elimination
+//     (fem.cpp:323-342), so patch rows on the boundary keep the
+//     single-nonzero signature boundary_pattern keys on (patch.cpp:101-111);
+//   * stored entries are never pruned (sparse.hpp:17-19).
+// Geometry: cell corners off the boundary are jittered by U(+-jitter*h) per
+// coordinate and each cell is mapped multilinearly from its corners.
+// Randomness: std::mt19937_64 streams with u = (rng() >> 11) * 2^-53
+// (jitter: seed; coefficient blocks: seed+1; right-hand side: seed+2).
+// Assembly is cell-parallel over 2^dim parity colours (cells of one colour
+// share no DoF), so the accumulated values do not depend on thread count.
+#include <algorithm>
+#include <cmath>
+#include <random>
+#include <thread>
+
+#include "host.hpp"
+
+namespace pdb {
+
+namespace {
+
+struct Gauss {
+  std::vector<double> x, w;  // on [0,1]
+};
+
+Gauss gauss_legendre01(int n) {
+  Gauss g;
+  g.x.resize(n);
+  g.w.resize(n);
+  // Legendre P_n and P_n' at z by the three-term recurrence.
+  auto legendre = [n](double z, double& pn, double& dpn) {
+    double p0 = 1.0, p1 = z;
+    for (int k = 2; k <= n; ++k) {
+      const double pk = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+      p0 = p1;
+      p1 = pk;
+    }
+    pn = p1;
+    dpn = n * (z * p1 - p0) / (z * z - 1.0);
+  };
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double pn, dp;
+    for (int it = 0; it < 100; ++it) {
+      legendre(z, pn, dp);
+      const double dz = pn / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    legendre(z, pn, dp);
+    g.x[n - 1 - i] = 0.5 * (1.0 + z);
+    g.w[n - 1 - i] = 1.0 / ((1.0 - z * z) * dp * dp);  // 2/((1-z^2)P'^2) mapped to [0,1]
+  }
+  return g;
+}
+
+// 1D Lagrange basis on nodes a/p: values and derivatives at the Gauss points.
+void lagrange_tables(int p, const Gauss& g, std::vector<double>& val, std::vector<double>& der) {
+  const int nq = static_cast<int>(g.x.size());
+  val.assign((p + 1) * nq, 0.0);
+  der.assign((p + 1) * nq, 0.0);
+  for (int a = 0; a <= p; ++a) {
+    const double xa = static_cast<double>(a) / p;
+    for (int q = 0; q < nq; ++q) {
+      const double x = g.x[q];
+      double v = 1.0;
+      for (int b = 0; b <= p; ++b)
+        if (b != a) v *= (x - static_cast<double>(b) / p) / (xa - static_cast<double>(b) / p);
+      double d = 0.0;
+      for (int c = 0; c <= p; ++c) {
+        if (c == a) continue;
+        double t = 1.0 / (xa - static_cast<double>(c) / p);
+        for (int b = 0; b <= p; ++b)
+          if (b != a && b != c) t *= (x - static_cast<double>(b) / p) / (xa - static_cast<double>(b) / p);
+        d += t;
+      }
+      val[a * nq + q] = v;
+      der[a * nq + q] = d;
+    }
+  }
+}
+
+inline double unit(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
+
+template <typename F>
+void parallel_for(Index n, int threads, F&& fn) {
+  if (n <= 0) return;
+  const Index workers = std::max<Index>(1, std::min<Index>(threads, n));
+  if (workers == 1) {
+    fn(Index{0}, n);
+    return;
+  }
+  const Index chunk = (n + workers - 1) / workers;
+  std::vector<std::thread> pool;
+  for (Index t = 0; t < workers; ++t) {
+    const Index b = std::min(t * chunk, n), e = std::min(b + chunk, n);
+    if (b >= e) break;
+    pool.emplace_back([&fn, b, e] { fn(b, e); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+}  // namespace
+
+void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
+  require(o.dim == 2 || o.dim == 3, Errc::invalid_argument, "mesh dimension must be 2 or 3");
+  require(o.cells >= 1, Errc::invalid_argument, "mesh needs at least one cell per axis");
+  require(o.degree >= 1, Errc::invalid_degree, "polynomial degree must be >= 1");
+  require(o.jitter >= 0.0 && o.jitter < 0.5, Errc::invalid_argument, "jitter must be in [0, 0.5)");
+  const int d = o.dim, p = o.degree;
+  const Index C = o.cells;
+  const Index npa = C * p + 1;
+  const Index n = d == 3 ? npa * npa * npa : npa * npa;
+  const Index nva = C + 1;  // vertices per axis
+  const Index nv = d == 3 ? nva * nva * nva : nva * nva;
+  const double h = 1.0 / static_cast<double>(C);
+  int threads = o.threads > 0 ? o.threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+
+  // --- geometry: jittered cell corners -----------------------------------
+  std::vector<double> X(static_cast<size_t>(nv * d));
+  {
+    std::mt19937_64 rng(o.seed);
+    for (Index v = 0; v < nv; ++v) {
+      Index lat[3] = {v % nva, (v / nva) % nva, d == 3 ? v / (nva * nva) : 0};
+      bool interior = true;
+      for (int k = 0; k < d; ++k)
+        if (lat[k] == 0 || lat[k] == C) interior = false;
+      for (int k = 0; k < d; ++k) {
+        const double u = unit(rng);
+        double x = static_cast<double>(lat[k]) * h;
+        if (interior) x += (2.0 * u - 1.0) * o.jitter * h;
+        X[static_cast<size_t>(v * d + k)] = x;
+      }
+    }
+  }
+  // --- coefficient per cell ----------------------------------------------
+  const Index ncells = d == 3 ? C * C * C : C * C;
+  std::vector<double> rho(static_cast<size_t>(ncells), o.coeff_value);
+  if (o.coeff_kind == 1) {
+    require(o.block_cells >= 1 && o.n_levels >= 1 && o.n_levels <= 8, Errc::invalid_argument,
+            "random-block coefficient needs block_cells >= 1 and 1..8 levels");
+    for (int k = 0; k < o.n_levels; ++k)
+      require(o.levels[k] > 0.0, Errc::non_positive_coefficient, "coefficient must be positive");
+    const Index nb = (C + o.block_cells - 1) / o.block_cells;
+    const Index nblocks = d == 3 ? nb * nb * nb : nb * nb;
+    std::vector<double> bval(static_cast<size_t>(nblocks));
+    std::mt19937_64 rng(o.seed + 1);
+    for (Index b = 0; b < nblocks; ++b) {
+      Index k = static_cast<Index>(unit(rng) * o.n_levels);
+      if (k >= o.n_levels) k = o.n_levels - 1;
+      bval[static_cast<size_t>(b)] = o.levels[k];
+    }
+    for (Index c = 0; c < ncells; ++c) {
+      const Index cx = c % C, cy = (c / C) % C, cz = d == 3 ? c / (C * C) : 0;
+      const Index bx = cx / o.block_cells, by = cy / o.block_cells, bz = cz / o.block_cells;
+      rho[static_cast<size_t>(c)] = bval[static_cast<size_t>(bx + nb * (by + nb * bz))];
+    }
+  } else {
+    require(o.coeff_value > 0.0, Errc::non_positive_coefficient, "coefficient must be positive");
+  }
+
+  // --- CSR pattern: tensor ranges of the cells touching each node ----------
+  auto axis_range = [&](Index i, Index& lo, Index& w) {
+    const Index cmin = i == 0 ? 0 : (i - 1) / p;
+    const Index cmax = std::min<Index>(C - 1, i / p);
+    lo = cmin * p;
+    w = cmax * p + p - lo + 1;
+  };
+  auto on_boundary = [&](Index i) {
+    const Index ix = i % npa, iy = (i / npa) % npa, iz = d == 3 ? i / (npa * npa) : 0;
+    if (ix == 0 || ix == npa - 1 || iy == 0 || iy == npa - 1) return true;
+    if (d == 3 && (iz == 0 || iz == npa - 1)) return true;
+    return false;
+  };
+  HostCsr& A = out.a;
+  A.n = n;
+  A.row_ptr.assign(static_cast<size_t>(n + 1), 0);
+  parallel_for(n, threads, [&](Index b, Index e) {
+    for (Index i = b; i < e; ++i) {
+      if (on_boundary(i)) {
+        A.row_ptr[static_cast<size_t>(i + 1)] = 1;
+        continue;
+      }
+      Index cnt = 1;
+      const Index lat[3] = {i % npa, (i / npa) % npa, d == 3 ? i / (npa * npa) : 0};
+      for (int k = 0; k < d; ++k) {
+        Index lo, w;
+        axis_range(lat[k], lo, w);
+        cnt *= w;
+      }
+      A.row_ptr[static_cast<size_t>(i + 1)] = cnt;
+    }
+  });
+  for (Index i = 0; i < n; ++i) A.row_ptr[static_cast<size_t>(i + 1)] += A.row_ptr[static_cast<size_t>(i)];
+  const Index nnz = A.row_ptr[static_cast<size_t>(n)];
+  require(n < (Index{1} << 31), Errc::invalid_argument, "generator: more than 2^31 rows");
+  A.col.resize(static_cast<size_t>(nnz));
+  A.val.assign(static_cast<size_t>(nnz), 0.0);
+  parallel_for(n, threads, [&](Index b, Index e) {
+    for (Index i = b; i < e; ++i) {
+      Index pos = A.row_ptr[static_cast<size_t>(i)];
+      if (on_boundary(i)) {
+        A.col[static_cast<size_t>(pos)] = static_cast<int32_t>(i);
+        A.val[static_cast<size_t>(pos)] = 1.0;
+        continue;
+      }
+      const Index lat[3] = {i % npa, (i / npa) % npa, d == 3 ? i / (npa * npa) : 0};
+      Index lo[3] = {0, 0, 0}, w[3] = {1, 1, 1};
+      for (int k = 0; k < d; ++k) axis_range(lat[k], lo[k], w[k]);
+      for (Index z = 0; z < w[2]; ++z)
+        for (Index y = 0; y < w[1]; ++y)
+          for (Index x = 0; x < w[0]; ++x)
+            A.col[static_cast<size_t>(pos++)] =
+                static_cast<int32_t>((lo[0] + x) + npa * ((lo[1] + y) + npa * (lo[2] + z)));
+    }
+  });
+
+  // --- element matrices, scattered colour by colour ------------------------
+  const Gauss g = gauss_legendre01(p + 1);
+  const int nq1 = p + 1;
+  std::vector<double> val1, der1;
+  lagrange_tables(p, g, val1, der1);
+  const int nloc1 = p + 1;
+  const int nloc = d == 3 ? nloc1 * nloc1 * nloc1 : nloc1 * nloc1;
+  const int nq = d == 3 ? nq1 * nq1 * nq1 : nq1 * nq1;
+  const int ncorner = d == 3 ? 8 : 4;
+  // reference-element tables: grad_xi phi_a at q, d comps; corner shape grads.
+  std::vector<double> gref(static_cast<size_t>(nq * nloc * d));
+  std::vector<double> cgrad(static_cast<size_t>(nq * ncorner * d));
+  std::vector<double> qw(static_cast<size_t>(nq));
+  for (int q = 0; q < nq; ++q) {
+    const int qx = q % nq1, qy = (q / nq1) % nq1, qz = d == 3 ? q / (nq1 * nq1) : 0;
+    qw[q] = g.w[qx] * g.w[qy] * (d == 3 ? g.w[qz] : 1.0);
+    for (int a = 0; a < nloc; ++a) {
+      const int ax = a % nloc1, ay = (a / nloc1) % nloc1, az = d == 3 ? a / (nloc1 * nloc1) : 0;
+      const double vx = val1[ax * nq1 + qx], vy = val1[ay * nq1 + qy], vz = d == 3 ? val1[az * nq1 + qz] : 1.0;
+      const double dx = der1[ax * nq1 + qx], dy = der1[ay * nq1 + qy], dz = d == 3 ? der1[az * nq1 + qz] : 0.0;
+      double* gr = &gref[static_cast<size_t>((q * nloc + a) * d)];
+      gr[0] = dx * vy * vz;
+      gr[1] = vx * dy * vz;
+      if (d == 3) gr[2] = vx * vy * dz;
+    }
+    const double xi[3] = {g.x[qx], g.x[qy], d == 3 ? g.x[qz] : 0.0};
+    for (int c = 0; c < ncorner; ++c) {
+      const int b[3] = {c & 1, (c >> 1) & 1, (c >> 2) & 1};
+      double f[3], df[3];
+      for (int k = 0; k < 3; ++k) {
+        f[k] = b[k] ? xi[k] : 1.0 - xi[k];
+        df[k] = b[k] ? 1.0 : -1.0;
+      }
+      double* cg = &cgrad[static_cast<size_t>((q * ncorner + c) * d)];
+      if (d == 2) {
+        cg[0] = df[0] * f[1];
+        cg[1] = f[0] * df[1];
+      } else {
+        cg[0] = df[0] * f[1] * f[2];
+        cg[1] = f[0] * df[1] * f[2];
+        cg[2] = f[0] * f[1] * df[2];
+      }
+    }
+  }
+
+  const int ncolors = 1 << d;
+  for (int color = 0; color < ncolors; ++color) {
+    const int px = color & 1, py = (color >> 1) & 1, pz = (color >> 2) & 1;
+    const Index cxn = (C - px + 1) / 2, cyn = (C - py + 1) / 2, czn = d == 3 ? (C - pz + 1) / 2 : 1;
+    const Index ncol = cxn * cyn * czn;
+    parallel_for(ncol, threads, [&](Index b, Index e) {
+      std::vector<double> K(static_cast<size_t>(nloc * nloc));
+      std::vector<double> G(static_cast<size_t>(nloc * d));
+      std::vector<Index> dofs(static_cast<size_t>(nloc));
+      for (Index t = b; t < e; ++t) {
+        const Index cx = px + 2 * (t % cxn), cy = py + 2 * ((t / cxn) % cyn), cz = d == 3 ? pz + 2 * (t / (cxn * cyn)) : 0;
+        const Index cell = cx + C * (cy + C * cz);
+        double Xc[8][3];
+        for (int c = 0; c < ncorner; ++c) {
+          const Index v = (cx + (c & 1)) + nva * ((cy + ((c >> 1) & 1)) + nva * (cz + ((c >> 2) & 1)));
+          for (int k = 0; k < d; ++k) Xc[c][k] = X[static_cast<size_t>(v * d + k)];
+        }
+        std::fill(K.begin(), K.end(), 0.0);
+        const double rc = rho[static_cast<size_t>(cell)];
+        for (int q = 0; q < nq; ++q) {
+          double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};  // J[r][s] = dx_r/dxi_s
+          for (int c = 0; c < ncorner; ++c) {
+            const double* cg = &cgrad[static_cast<size_t>((q * ncorner + c) * d)];
+            for (int r = 0; r < d; ++r)
+              for (int s = 0; s < d; ++s) J[r][s] += Xc[c][r] * cg[s];
+          }
+          double inv[3][3], det;
+          if (d == 2) {
+            det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+            inv[0][0] = J[1][1] / det;
+            inv[0][1] = -J[0][1] / det;
+            inv[1][0] = -J[1][0] / det;
+            inv[1][1] = J[0][0] / det;
+          } else {
+            const double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+            const double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+            const double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+            det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+            inv[0][0] = c00 / det;
+            inv[1][0] = c01 / det;
+            inv[2][0] = c02 / det;
+            inv[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+            inv[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+            inv[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+            inv[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+            inv[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+            inv[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+          }
+          require(det > 0.0, Errc::invalid_argument, "generator: inverted cell (jitter too large)");
+          // grad_x phi_a = J^{-T} grad_xi phi_a:  G[a][r] = sum_s inv[s][r] gxi[s]
+          for (int a = 0; a < nloc; ++a) {
+            const double* gx = &gref[static_cast<size_t>((q * nloc + a) * d)];
+            for (int r = 0; r < d; ++r) {
+              double s = 0.0;
+              for (int k = 0; k < d; ++k) s += inv[k][r] * gx[k];
+              G[static_cast<size_t>(a * d + r)] = s;
+            }
+          }
+          const double wq = qw[q] * det * rc;
+          for (int a = 0; a < nloc; ++a)
+            for (int bb = 0; bb < nloc; ++bb) {
+              double s = 0.0;
+              for (int r = 0; r < d; ++r) s += G[static_cast<size_t>(a * d + r)] * G[static_cast<size_t>(bb * d + r)];
+              K[static_cast<size_t>(a * nloc + bb)] += wq * s;
+            }
+        }
+        // local DoF a = ax + (p+1)(ay + (p+1) az), ascending global order
+        for (int a = 0; a < nloc; ++a) {
+          const int ax = a % nloc1, ay = (a / nloc1) % nloc1, az = d == 3 ? a / (nloc1 * nloc1) : 0;
+          dofs[static_cast<size_t>(a)] = (cx * p + ax) + npa * ((cy * p + ay) + npa * (cz * p + az));
+        }
+        for (int a = 0; a < nloc; ++a) {
+          const Index gi = dofs[static_cast<size_t>(a)];
+          if (on_boundary(gi)) continue;  // row replaced (fem.cpp:323)
+          const Index lat[3] = {gi % npa, (gi / npa) % npa, d == 3 ? gi / (npa * npa) : 0};
+          Index lo[3] = {0, 0, 0}, w[3] = {1, 1, 1};
+          for (int k = 0; k < d; ++k) axis_range(lat[k], lo[k], w[k]);
+          const Index base = A.row_ptr[static_cast<size_t>(gi)];
+          for (int bb = 0; bb < nloc; ++bb) {
+            const Index gj = dofs[static_cast<size_t>(bb)];
+            const Index jl[3] = {gj % npa, (gj / npa) % npa, d == 3 ? gj / (npa * npa) : 0};
+            const Index off = (jl[0] - lo[0]) + w[0] * ((jl[1] - lo[1]) + w[1] * (jl[2] - lo[2]));
+            A.val[static_cast<size_t>(base + off)] += K[static_cast<size_t>(a * nloc + bb)];
+          }
+        }
+      }
+    });
+  }
+
+  // --- right-hand side ----------------------------------------------------
+  out.rhs.assign(static_cast<size_t>(n), 0.0);
+  {
+    std::mt19937_64 rng(o.seed + 2);
+    for (Index i = 0; i < n; ++i) {
+      const double u = unit(rng);
+      if (!on_boundary(i)) out.rhs[static_cast<size_t>(i)] = 2.0 * u - 1.0;
+    }
+  }
+  out.has_exact = false;
+  out.dim = d;
+  out.cells = C;
+  out.degree = p;
+}
+
+}  // namespace pdb

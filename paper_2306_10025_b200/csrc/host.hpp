@@ -1,0 +1,66 @@
+// Host orchestration entry points shared between the C-ABI (capi.cpp) and
+// the per-subsystem sources.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "../../include/patchdb/patchdb.h"
+#include "objects.hpp"
+
+namespace pdb {
+
+// matrix.cpp
+void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s);
+HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v);
+HostCsr download_csr(const DeviceCsr& d, cudaStream_t s);
+void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s);
+HostCsr read_matrix_market_host(const std::string& path);
+void write_matrix_market_host(const HostCsr& a, const std::string& path);
+
+// generator.cpp
+void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out);
+
+// patchset.cpp
+void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStream_t s);
+void extract_patches(const DeviceCsr& a, const pdb_patchset_s& ps, DevBuf<double>& mats, cudaStream_t s);
+std::vector<int64_t> patches_host(const pdb_patchset_s& ps, cudaStream_t s);
+void write_patchset_json(const pdb_patchset_s& ps, const std::string& path, cudaStream_t s);
+
+// database.cpp
+struct BuildParams {
+  int method = PDB_METHOD_GREEDY_L1;
+  double eps = 1e-7;
+  int64_t db_size = 0;
+  uint64_t seed = 42;
+  int max_iters = 50;
+  bool best_match = false;
+  int64_t abort_above = -1;  // greedy only
+};
+// Returns false when a capped greedy pass aborted (no database).
+bool build_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, pdb_database_s& out,
+                    cudaStream_t s);
+bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps, const BuildParams& p,
+                              pdb_database_s& out, cudaStream_t s);
+double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, int64_t lo, int64_t hi,
+                       pdb_database_s& out, cudaStream_t s);
+void export_database(const pdb_database_s& db, const std::string& json_path, const std::string& bin_path,
+                     cudaStream_t s);
+
+// precond.cpp
+void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& out, cudaStream_t s);
+void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
+                        cudaStream_t s);
+// z = M^{-1} r on device pointers.
+void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s);
+// sweeps of smooth(); history (device, may be null) gets sweeps+1 norms.
+void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
+                  double* history, cudaStream_t s);
+
+// krylov.cpp
+void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, const pdb_gmres_options& o,
+                  double* x_host, pdb_report_s& rep, cudaStream_t s);
+void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol, int64_t max_iters,
+                double* x_host, pdb_report_s& rep, cudaStream_t s);
+
+}  // namespace pdb

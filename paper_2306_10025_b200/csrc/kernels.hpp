@@ -1,0 +1,128 @@
+// Host-callable launchers for the sm_100a kernels in kernels/*.cu.
+// All launchers are asynchronous on the given stream.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace pdb::k {
+
+// ---- sweep.cu : the relaxation sweep -------------------------------------
+// r = b - A x (b may be null: r = -A x is never used; y = A x when b == null
+// and negate == false).  When sumsq != null, per-block partial sums of r^2
+// are written to sumsq[blockIdx] (deterministic two-pass norm).
+struct SpmvPlan {
+  int group = 8;      // threads per row (power of two <= 32)
+  int rows_per_block = 32;
+  int blocks = 0;
+};
+SpmvPlan spmv_plan(int64_t n, int64_t nnz);
+void residual(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
+              const double* x, const double* b, double* r, double* block_sumsq, cudaStream_t s);
+void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+          double* y, cudaStream_t s);
+// Deterministic sum of `count` partials -> out[0] = sqrt(sum) (sqrt_result) or sum.
+void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s);
+
+// Per-patch gather + LU solve (column-major factors):
+//   sols[k*ps + i] = (B_f^{-1} r[patch_k])_i,  f = phi ? phi[k] : k.
+void patch_solve(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
+                 const int32_t* phi, const double* r, double* sols, cudaStream_t s);
+// z[i] = (sum over (k,l) in inv(i), ascending k, of sols[k*ps+l]) * omega_w[i];
+// x_out (may be null): x_out[i] = z[i] + x_in[i] (the smooth() update, precond.cpp:99).
+void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,
+                    const double* x_in, double* z_out, double* x_out, cudaStream_t s);
+
+// Sweep-structure setup.
+void build_inverse_count(int64_t np, int ps, const int32_t* patches, int32_t* counts, cudaStream_t s);
+void build_inverse_fill(int64_t np, int ps, const int32_t* patches, const int32_t* inv_ptr, int32_t* cursor,
+                        int32_t* inv, cudaStream_t s);
+void sort_inverse_segments(int64_t n, const int32_t* inv_ptr, int32_t* inv, cudaStream_t s);
+void transpose_factors(int64_t nf, int ps, const double* lu_rm, double* lu_cm, cudaStream_t s);
+void scale_weights(int64_t n, double omega, const double* w, double* omega_w, cudaStream_t s);
+
+// ---- detect.cu : matrix-only cell-patch detection --------------------------
+void detect_candidates(int64_t n, const int64_t* rp, int64_t ps, uint8_t* cand, int32_t* any, cudaStream_t s);
+// For each candidate row listed in rows[0..nrows): consistent[t] (0/1) and hash[t] (FNV-1a of its columns).
+void detect_consistency(int64_t nrows, const int32_t* rows, const int64_t* rp, const int32_t* col,
+                        const uint8_t* cand, int ps, uint8_t* consistent, uint64_t* hash, cudaStream_t s);
+// Positions sorted by (hash, position): keep_by_pos[p] = 0 when an earlier row of the same
+// hash run has an identical column set (first occurrence wins), else 1.
+void detect_dedupe(int64_t nrows, const uint64_t* hash_sorted, const int32_t* pos_sorted, const int32_t* rows,
+                   const int64_t* rp, const int32_t* col, int ps, uint8_t* keep_by_pos, cudaStream_t s);
+void iota(int64_t n, int32_t* out, cudaStream_t s);
+void gather_patches(int64_t np, const int32_t* rows, const int32_t* order, const int64_t* rp, const int32_t* col,
+                    int ps, int32_t* patches, cudaStream_t s);
+void cover_weights(int64_t n, int64_t np, int ps, const int32_t* patches, int32_t* cover, double* w, cudaStream_t s);
+
+// ---- extract.cu : batched A_k = V_k A V_k^T ---------------------------------
+// ids == null: patches 0..count-1; else patches ids[0..count).
+void extract(int64_t count, const int32_t* ids, int ps, const int32_t* patches, const int64_t* rp,
+             const int32_t* col, const double* val, double* out, cudaStream_t s);
+
+// ---- lu.cu : bit-exact batched partial-pivot LU (dense.cpp:31-75) ----------
+// Factor mats[src[t]] (src == null: t) into lu[t], piv[t]; status[t] = 0 ok,
+// else (column+1) of the failing pivot with fail_best[t] = |pivot|.
+void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, double* lu, int32_t* piv,
+                int32_t* status, double* fail_best, cudaStream_t s);
+
+// ---- criterion.cu : bit-exact distance criteria ----------------------------
+// L1: d[t*ne + e] = sum_q |mats[pid[t]] - reps_e| (sequential q), reps_e = mats[rep_src[e]] (rep_src != null) or reps[e].
+void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,
+              const double* reps, double* d, cudaStream_t s);
+// Spectral: d[t*ne + e] = spectral_distance(mats[pid[t]], factor e) (dense.cpp:154-190).
+// iters (may be null) accumulates power iterations (atomic, for work accounting).
+void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);
+// Spectral distance of listed (patch, factor) pairs: d[t] = dist(mats[pa[t]], factor fb[t]).
+void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
+                   const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);
+
+// Greedy (compress.cpp:40-95) round machinery.
+// Sequential resolution of the batch S (size B, ascending patch ids) against
+// the entries it creates itself; D is B x B (row a = patch S[a], col b = entry
+// made from S[b]).  Outputs: phi for S, new entries appended to creators[] at
+// *m, lu_status of S consulted for failures.  state[0] = m (in/out),
+// state[1] = abort flag, state[2] = error batch index (-1 none).
+void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int best_match, int64_t abort_above,
+                    const int32_t* lu_status, int32_t* phi, int32_t* creators, int32_t* entry_of_batch,
+                    int64_t* state, cudaStream_t s);
+// First-match / best-match scan of unresolved patches against entries [e0,e1)
+// (L1 flavour, reps are patch matrices of creators).  For first-match,
+// phi[pid] = first j with d < eps; best-match tracks (best_d, best_j) over
+// entries with creator < patch.
+void l1_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t e1, int len, const double* mats,
+             const int32_t* creators, double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s);
+// Apply a precomputed distance block d[t*ne + e] (entries e0+e) to the match state.
+void apply_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t ne, const double* d, const int32_t* creators,
+                double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s);
+
+// k-means (compress.cpp:138-262).
+// argmin over e of d[t*ne+e] (strict <, lowest e wins): new_phi[t], min_dist[t]; changed flag set when != phi[t].
+void argmin_assign(int64_t n, int64_t ne, const double* d, const int32_t* phi, int32_t* new_phi, double* min_dist,
+                   int32_t* changed, cudaStream_t s);
+// L1 argmin without materialising d (entries tiled through shared memory).
+void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double* reps, const int32_t* phi,
+               int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s);
+// In-order entrywise mean of each cluster (dense.cpp:211-223): members CSR (ascending).
+void cluster_mean(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats, double* reps,
+                  cudaStream_t s);
+
+// ---- cluster.cu : clustering data movement ---------------------------------
+// masks[k*words + w] bit b: local row 64w+b of patch k holds exactly one value != 0.0.
+void boundary_masks(int64_t np, int ps, const double* mats, int words, unsigned long long* masks, cudaStream_t s);
+void gather_mats(int64_t count, const int32_t* ids, int64_t len, const double* src, double* dst, cudaStream_t s);
+void gather_i32(int64_t count, const int32_t* ids, int64_t len, const int32_t* src, int32_t* dst, cudaStream_t s);
+
+// ---- blas.cu : deterministic vector kernels for the Krylov drivers ---------
+// out[0] = dot(a, b) via fixed two-level reduction (partials scratch >= dot_partials()).
+int dot_partials();
+void dot(int64_t n, const double* a, const double* b, double* partials, double* out, cudaStream_t s);
+void axpy(int64_t n, const double* alpha, bool negate, const double* x, double* y, cudaStream_t s);  // y += (+-)alpha[0]*x
+void xpay(int64_t n, const double* x, const double* beta, double* y, cudaStream_t s);                // y = x + beta[0]*y
+void axpy_val(int64_t n, double a, const double* x, double* y, cudaStream_t s);                      // y += a*x
+void div_scalar(int64_t n, const double* x, double sc, double* y, cudaStream_t s);                   // y = x / sc
+void sub(int64_t n, const double* a, const double* b, double* y, cudaStream_t s);                    // y = a - b
+
+}  // namespace pdb::k

@@ -1,0 +1,517 @@
+// Bit-exact compression criteria and clustering steps (reference
+// compress.cpp / dense.cpp).  Compiled with --fmad=false and written with
+// explicit _rn intrinsics: every distance is computed by ONE thread in the
+// reference's sequential operation order, so the values -- and therefore
+// the greedy and k-means decisions built on strict < comparisons -- are
+// bitwise those of the reference.
+//
+//   l1 distances        entrywise_l1_distance dense.cpp:192-197
+//   spectral distance   spectral_distance dense.cpp:154-190 with
+//                       lu_solve_into :77-94, lu_solve_transpose_into :102-120,
+//                       mat_vec :122-131, mat_tvec :133-142, norm2 :146-150
+//   greedy resolution   greedy_impl compress.cpp:40-95 (round-batched, exact)
+//   k-means steps       kmeans_loop compress.cpp:150-166 (assignment),
+//                       entrywise_mean_indexed dense.cpp:211-223 (update)
+#include <cfloat>
+
+#include <math_constants.h>
+
+#include "../kernels.hpp"
+
+namespace pdb::k {
+
+namespace {
+
+inline unsigned grid_for(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// ---------------------------------------------------------------- L1 ----
+constexpr int kL1Threads = 128;
+constexpr int kL1Ent = 4;    // entries per tile (register accumulators)
+constexpr int kL1Chunk = 512;  // elements per staged chunk
+
+// d[t*ne + e] for a tile of kL1Ent entries; entries staged chunk-wise in smem,
+// each thread streams its own patch matrix once per tile.
+__global__ void __launch_bounds__(kL1Threads) l1_pairs_kernel(int64_t npat, const int32_t* __restrict__ pid, int64_t ne,
+                                                              int len, const double* __restrict__ mats,
+                                                              const int32_t* __restrict__ rep_src,
+                                                              const double* __restrict__ reps, double* __restrict__ d) {
+  __shared__ double R[kL1Ent][kL1Chunk];
+  const int64_t t = (int64_t)blockIdx.x * kL1Threads + threadIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.y * kL1Ent;
+  const bool live = t < npat;
+  const double* A = mats + (live ? (int64_t)(pid ? pid[t] : t) : 0) * len;
+  double acc[kL1Ent];
+#pragma unroll
+  for (int c = 0; c < kL1Ent; ++c) acc[c] = 0.0;
+  for (int q0 = 0; q0 < len; q0 += kL1Chunk) {
+    const int qn = min(kL1Chunk, len - q0);
+    __syncthreads();
+    for (int c = 0; c < kL1Ent; ++c) {
+      const int64_t e = e0 + c;
+      if (e >= ne) break;
+      const double* Re = rep_src ? mats + (int64_t)rep_src[e] * len : reps + e * len;
+      for (int q = threadIdx.x; q < qn; q += kL1Threads) R[c][q] = Re[q0 + q];
+    }
+    __syncthreads();
+    if (live)
+      for (int q = 0; q < qn; ++q) {
+        const double a = A[q0 + q];
+#pragma unroll
+        for (int c = 0; c < kL1Ent; ++c) acc[c] = __dadd_rn(acc[c], fabs(__dsub_rn(a, R[c][q])));
+      }
+  }
+  if (live)
+    for (int c = 0; c < kL1Ent; ++c)
+      if (e0 + c < ne) d[t * ne + e0 + c] = acc[c];
+}
+
+// First-/best-match scan of unresolved patches over entries [e0, e1)
+// (greedy_impl compress.cpp:51-84).  Entries are patch matrices of their
+// creators.  Block-uniform early exit once every thread has matched.
+__global__ void __launch_bounds__(kL1Threads) l1_scan_kernel(int64_t nu, const int32_t* __restrict__ pid, int64_t e0,
+                                                             int64_t e1, int len, const double* __restrict__ mats,
+                                                             const int32_t* __restrict__ creators, double eps,
+                                                             int best_match, int32_t* __restrict__ phi,
+                                                             double* __restrict__ best_d) {
+  __shared__ double R[kL1Ent][kL1Chunk];
+  const int64_t t = (int64_t)blockIdx.x * kL1Threads + threadIdx.x;
+  const bool live = t < nu;
+  const int32_t me = live ? pid[t] : 0;
+  const double* A = mats + (int64_t)me * len;
+  bool done = !live;
+  double cur = eps;
+  int32_t cur_j = -1;
+  if (live && best_match) {
+    cur = best_d[me];
+    cur_j = phi[me];
+  }
+  for (int64_t tile = e0; tile < e1; tile += kL1Ent) {
+    if (__syncthreads_and(done)) break;
+    double acc[kL1Ent];
+#pragma unroll
+    for (int c = 0; c < kL1Ent; ++c) acc[c] = 0.0;
+    for (int q0 = 0; q0 < len; q0 += kL1Chunk) {
+      const int qn = min(kL1Chunk, len - q0);
+      __syncthreads();
+      for (int c = 0; c < kL1Ent; ++c) {
+        const int64_t e = tile + c;
+        if (e >= e1) break;
+        const double* Re = mats + (int64_t)creators[e] * len;
+        for (int q = threadIdx.x; q < qn; q += kL1Threads) R[c][q] = Re[q0 + q];
+      }
+      __syncthreads();
+      if (!done)
+        for (int q = 0; q < qn; ++q) {
+          const double a = A[q0 + q];
+#pragma unroll
+          for (int c = 0; c < kL1Ent; ++c) acc[c] = __dadd_rn(acc[c], fabs(__dsub_rn(a, R[c][q])));
+        }
+    }
+    if (!done)
+      for (int c = 0; c < kL1Ent; ++c) {
+        const int64_t j = tile + c;
+        if (j >= e1) break;
+        if (best_match) {
+          if (creators[j] < me && acc[c] < cur) {
+            cur = acc[c];
+            cur_j = (int32_t)j;
+          }
+        } else if (acc[c] < eps) {
+          cur_j = (int32_t)j;
+          done = true;
+          break;
+        }
+      }
+  }
+  if (live) {
+    if (best_match) {
+      best_d[me] = cur;
+      phi[me] = cur_j;
+    } else if (cur_j >= 0) {
+      phi[me] = cur_j;
+    }
+  }
+}
+
+// Match-state update from a precomputed distance block (spectral flavour).
+__global__ void apply_scan_kernel(int64_t nu, const int32_t* __restrict__ pid, int64_t e0, int64_t ne,
+                                  const double* __restrict__ d, const int32_t* __restrict__ creators, double eps,
+                                  int best_match, int32_t* __restrict__ phi, double* __restrict__ best_d) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nu) return;
+  const int32_t me = pid[t];
+  if (best_match) {
+    double cur = best_d[me];
+    int32_t cj = phi[me];
+    for (int64_t e = 0; e < ne; ++e)
+      if (creators[e0 + e] < me && d[t * ne + e] < cur) {
+        cur = d[t * ne + e];
+        cj = (int32_t)(e0 + e);
+      }
+    best_d[me] = cur;
+    phi[me] = cj;
+  } else {
+    if (phi[me] >= 0) return;
+    for (int64_t e = 0; e < ne; ++e)
+      if (d[t * ne + e] < eps) {
+        phi[me] = (int32_t)(e0 + e);
+        return;
+      }
+  }
+}
+
+// Sequential resolution of a batch S against the entries it creates itself.
+// One warp: for each a in order, the candidate entries are the batch members
+// b < a that became entries; first-match takes the lowest such b with
+// D[a][b] < eps, best-match the smallest D < eps (ties: lowest b).  Batch
+// members were unmatched against every earlier entry, so this reproduces the
+// sequential pass exactly.
+__global__ void greedy_resolve_kernel(int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps,
+                                      int best_match, int64_t abort_above, const int32_t* __restrict__ lu_status,
+                                      int32_t* __restrict__ phi, int32_t* __restrict__ creators,
+                                      int32_t* __restrict__ entry_of, int64_t* state) {
+  const int lane = threadIdx.x;
+  int64_t m = state[0];
+  for (int a = 0; a < B; ++a) {
+    double bd = eps;
+    int bb = B;
+    for (int b = lane; b < a; b += 32) {
+      const int ent = entry_of[b];
+      if (ent < 0) continue;
+      const double dv = D[(int64_t)a * B + b];
+      if (best_match) {
+        if (dv < bd) {  // lanes scan their b ascending: keeps the lowest b on ties
+          bd = dv;
+          bb = b;
+        }
+      } else if (dv < eps && b < bb) {
+        bb = b;
+        bd = dv;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, off);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
+      if (best_match) {
+        if (od < bd || (od == bd && ob < bb)) {
+          bd = od;
+          bb = ob;
+        }
+      } else if (ob < bb) {
+        bb = ob;
+        bd = od;
+      }
+    }
+    if (bb < B) {
+      if (lane == 0) {
+        phi[S[a]] = entry_of[bb];
+        entry_of[a] = -1;
+      }
+      __syncwarp();
+      continue;
+    }
+    if (abort_above > 0 && m + 1 > abort_above) {
+      if (lane == 0) state[1] = 1;
+      break;
+    }
+    if (lu_status && lu_status[a] != 0) {
+      if (lane == 0) state[2] = a;
+      break;
+    }
+    if (lane == 0) {
+      creators[m] = S[a];
+      phi[S[a]] = (int32_t)m;
+      entry_of[a] = (int32_t)m;
+    }
+    ++m;
+    __syncwarp();
+  }
+  if (lane == 0) state[0] = m;
+}
+
+// ----------------------------------------------------------- spectral ----
+// Per-thread vectors live in shared memory at [q * BD + tid] (lane-contiguous).
+struct Vec {
+  double* p;
+  int stride;
+  __device__ double& operator[](int q) const { return p[q * stride]; }
+};
+
+// lu_solve_into (dense.cpp:77-94): out = B^{-1} rhs.
+__device__ void lu_solve_dev(int n, const double* __restrict__ LU, const int32_t* __restrict__ P, Vec rhs, Vec out) {
+  for (int i = 0; i < n; ++i) out[i] = rhs[P[i]];
+  for (int i = 1; i < n; ++i) {
+    double s = out[i];
+    for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(LU[i * n + j], out[j]));
+    out[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = out[i];
+    for (int j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(LU[i * n + j], out[j]));
+    out[i] = __ddiv_rn(s, LU[i * n + i]);
+  }
+}
+
+// lu_solve_transpose_into (dense.cpp:102-120); w is consumed (it holds the
+// reference's internal copy of rhs), out[P[i]] = w[i].
+__device__ void lu_solve_t_dev(int n, const double* __restrict__ LU, const int32_t* __restrict__ P, Vec w, Vec out) {
+  for (int i = 0; i < n; ++i) {
+    double s = w[i];
+    for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(LU[j * n + i], w[j]));
+    w[i] = __ddiv_rn(s, LU[i * n + i]);
+  }
+  for (int i = n - 2; i >= 0; --i) {
+    double s = w[i];
+    for (int j = i + 1; j < n; ++j) s = __dsub_rn(s, __dmul_rn(LU[j * n + i], w[j]));
+    w[i] = s;
+  }
+  for (int i = 0; i < n; ++i) out[P[i]] = w[i];
+}
+
+__device__ double norm2_dev(int n, Vec v) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(v[i], v[i]));
+  return __dsqrt_rn(s);
+}
+
+// spectral_distance (dense.cpp:154-190).  A: patch matrix (row-major,
+// per-thread), LU/P: factor (shared), v,t,w,s: per-thread vectors.
+__device__ double spectral_dev(int n, const double* __restrict__ A, const double* __restrict__ LU,
+                               const int32_t* __restrict__ P, Vec v, Vec t, Vec w, Vec s, int* iters) {
+  for (int i = 0; i < n; ++i) v[i] = __dadd_rn(1.0, __dmul_rn(1e-6, (double)i));
+  const double vn = norm2_dev(n, v);
+  for (int i = 0; i < n; ++i) v[i] = __ddiv_rn(v[i], vn);
+  double lambda = 0.0;
+  for (int it = 0; it < 200; ++it) {
+    *iters = it + 1;
+    lu_solve_dev(n, LU, P, v, t);  // t = B^{-1} v
+    for (int i = 0; i < n; ++i) {  // w = v - A t   (mat_vec, then subtract)
+      double acc = 0.0;
+      const double* Ai = A + (int64_t)i * n;
+      for (int j = 0; j < n; ++j) acc = __dadd_rn(acc, __dmul_rn(Ai[j], t[j]));
+      w[i] = __dsub_rn(v[i], acc);
+    }
+    for (int j = 0; j < n; ++j) s[j] = 0.0;  // s = A^T w  (mat_tvec loop order)
+    for (int i = 0; i < n; ++i) {
+      const double xi = w[i];
+      const double* Ai = A + (int64_t)i * n;
+      for (int j = 0; j < n; ++j) s[j] = __dadd_rn(s[j], __dmul_rn(Ai[j], xi));
+    }
+    lu_solve_t_dev(n, LU, P, s, t);  // t = B^{-T} s
+    double rq = 0.0;
+    for (int i = 0; i < n; ++i) {  // u = w - t (stored in t); rq = v.u
+      const double u = __dsub_rn(w[i], t[i]);
+      t[i] = u;
+      rq = __dadd_rn(rq, __dmul_rn(v[i], u));
+    }
+    rq = rq > 0.0 ? rq : 0.0;
+    if (rq <= 1e-28) return __dsqrt_rn(rq);
+    if (it > 0 && fabs(__dsub_rn(rq, lambda)) < __dmul_rn(1e-8, rq)) return __dsqrt_rn(rq);
+    lambda = rq;
+    const double un2 = norm2_dev(n, t);
+    if (un2 == 0.0) return 0.0;
+    for (int i = 0; i < n; ++i) v[i] = __ddiv_rn(t[i], un2);
+  }
+  return __dsqrt_rn(lambda);
+}
+
+// Block = BD patches x one factor (grid.y); factor staged in shared memory
+// and broadcast, patch matrices streamed per thread.
+__global__ void spectral_pairs_kernel(int64_t npat, const int32_t* __restrict__ pid, int64_t ne, int ps,
+                                      const double* __restrict__ mats, const double* __restrict__ lu,
+                                      const int32_t* __restrict__ piv, double* __restrict__ d,
+                                      unsigned long long* iters_total) {
+  extern __shared__ double sm[];
+  const int BD = blockDim.x;
+  const int64_t len = (int64_t)ps * ps;
+  double* LU = sm;
+  int32_t* P = reinterpret_cast<int32_t*>(LU + len);
+  double* vec = LU + len + (ps + 1) / 2;
+  const int64_t e = blockIdx.y;
+  for (int64_t q = threadIdx.x; q < len; q += BD) LU[q] = lu[e * len + q];
+  for (int q = threadIdx.x; q < ps; q += BD) P[q] = piv[e * ps + q];
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * BD + threadIdx.x;
+  if (t >= npat) return;
+  const double* A = mats + (int64_t)(pid ? pid[t] : t) * len;
+  Vec v{vec + threadIdx.x, BD}, tv{vec + ps * BD + threadIdx.x, BD}, w{vec + 2 * ps * BD + threadIdx.x, BD},
+      s{vec + 3 * ps * BD + threadIdx.x, BD};
+  int it = 0;
+  d[t * ne + e] = spectral_dev(ps, A, LU, P, v, tv, w, s, &it);
+  if (iters_total) atomicAdd(iters_total, (unsigned long long)it);
+}
+
+// Listed pairs: thread per pair, factor read from global (L2).
+__global__ void spectral_list_kernel(int64_t npairs, const int32_t* __restrict__ pa, const int32_t* __restrict__ fb,
+                                     int ps, const double* __restrict__ mats, const double* __restrict__ lu,
+                                     const int32_t* __restrict__ piv, double* __restrict__ d,
+                                     unsigned long long* iters_total) {
+  extern __shared__ double sm[];
+  const int BD = blockDim.x;
+  const int64_t len = (int64_t)ps * ps;
+  const int64_t t = (int64_t)blockIdx.x * BD + threadIdx.x;
+  if (t >= npairs) return;
+  const double* A = mats + (int64_t)pa[t] * len;
+  const double* LU = lu + (int64_t)fb[t] * len;
+  const int32_t* P = piv + (int64_t)fb[t] * ps;
+  Vec v{sm + threadIdx.x, BD}, tv{sm + ps * BD + threadIdx.x, BD}, w{sm + 2 * ps * BD + threadIdx.x, BD},
+      s{sm + 3 * ps * BD + threadIdx.x, BD};
+  int it = 0;
+  d[t] = spectral_dev(ps, A, LU, P, v, tv, w, s, &it);
+  if (iters_total) atomicAdd(iters_total, (unsigned long long)it);
+}
+
+// ------------------------------------------------------------ k-means ----
+// Assignment (compress.cpp:150-166): strict <, so the lowest j wins ties;
+// best starts at +inf with best_j = 0.
+__global__ void argmin_kernel(int64_t n, int64_t ne, const double* __restrict__ d, const int32_t* __restrict__ phi,
+                              int32_t* __restrict__ new_phi, double* __restrict__ min_dist, int32_t* changed) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double best = CUDART_INF;
+  int32_t bj = 0;
+  for (int64_t e = 0; e < ne; ++e) {
+    const double v = d[t * ne + e];
+    if (v < best) {
+      best = v;
+      bj = (int32_t)e;
+    }
+  }
+  new_phi[t] = bj;
+  min_dist[t] = best;
+  if (bj != phi[t]) atomicOr(changed, 1);
+}
+
+__global__ void __launch_bounds__(kL1Threads) l1_argmin_kernel(int64_t n, int64_t ne, int len,
+                                                               const double* __restrict__ mats,
+                                                               const double* __restrict__ reps,
+                                                               const int32_t* __restrict__ phi,
+                                                               int32_t* __restrict__ new_phi,
+                                                               double* __restrict__ min_dist, int32_t* changed) {
+  __shared__ double R[kL1Ent][kL1Chunk];
+  const int64_t t = (int64_t)blockIdx.x * kL1Threads + threadIdx.x;
+  const bool live = t < n;
+  const double* A = mats + (live ? t : 0) * len;
+  double best = CUDART_INF;
+  int32_t bj = 0;
+  for (int64_t tile = 0; tile < ne; tile += kL1Ent) {
+    double acc[kL1Ent];
+#pragma unroll
+    for (int c = 0; c < kL1Ent; ++c) acc[c] = 0.0;
+    for (int q0 = 0; q0 < len; q0 += kL1Chunk) {
+      const int qn = min(kL1Chunk, len - q0);
+      __syncthreads();
+      for (int c = 0; c < kL1Ent; ++c) {
+        const int64_t e = tile + c;
+        if (e >= ne) break;
+        for (int q = threadIdx.x; q < qn; q += kL1Threads) R[c][q] = reps[e * len + q0 + q];
+      }
+      __syncthreads();
+      if (live)
+        for (int q = 0; q < qn; ++q) {
+          const double a = A[q0 + q];
+#pragma unroll
+          for (int c = 0; c < kL1Ent; ++c) acc[c] = __dadd_rn(acc[c], fabs(__dsub_rn(a, R[c][q])));
+        }
+    }
+    for (int c = 0; c < kL1Ent; ++c)
+      if (tile + c < ne && acc[c] < best) {
+        best = acc[c];
+        bj = (int32_t)(tile + c);
+      }
+  }
+  if (!live) return;
+  new_phi[t] = bj;
+  min_dist[t] = best;
+  if (bj != phi[t]) atomicOr(changed, 1);
+}
+
+// entrywise_mean_indexed (dense.cpp:211-223): in-order sum from 0.0, then
+// multiply by the reciprocal of the member count.  Thread per (cluster, entry).
+__global__ void cluster_mean_kernel(int64_t m, int len, const int32_t* __restrict__ mem_ptr,
+                                    const int32_t* __restrict__ mem, const double* __restrict__ mats,
+                                    double* __restrict__ reps) {
+  const int64_t j = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= len || j >= m) return;
+  const int32_t lo = mem_ptr[j], hi = mem_ptr[j + 1];
+  double s = 0.0;
+  for (int32_t c = lo; c < hi; ++c) s = __dadd_rn(s, mats[(int64_t)mem[c] * len + q]);
+  const double inv = __ddiv_rn(1.0, (double)(hi - lo));
+  reps[j * len + q] = __dmul_rn(s, inv);
+}
+
+}  // namespace
+
+void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,
+              const double* reps, double* d, cudaStream_t s) {
+  if (npat <= 0 || ne <= 0) return;
+  dim3 grid(grid_for(npat, kL1Threads), (unsigned)((ne + kL1Ent - 1) / kL1Ent));
+  l1_pairs_kernel<<<grid, kL1Threads, 0, s>>>(npat, pid, ne, len, mats, rep_src, reps, d);
+}
+
+static int spectral_block(int ps) { return ps <= 40 ? 64 : 32; }
+static size_t spectral_vec_bytes(int ps, int bd) { return (size_t)4 * ps * bd * sizeof(double); }
+
+void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+  if (npat <= 0 || ne <= 0) return;
+  const int bd = spectral_block(ps);
+  const size_t smem = (size_t)ps * ps * sizeof(double) + (size_t)((ps + 1) / 2) * sizeof(double) +
+                      spectral_vec_bytes(ps, bd);
+  cudaFuncSetAttribute(spectral_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(grid_for(npat, bd), (unsigned)ne);
+  spectral_pairs_kernel<<<grid, bd, smem, s>>>(npat, pid, ne, ps, mats, lu, piv, d, iters);
+}
+
+void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
+                   const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+  if (npairs <= 0) return;
+  const int bd = spectral_block(ps);
+  const size_t smem = spectral_vec_bytes(ps, bd);
+  cudaFuncSetAttribute(spectral_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  spectral_list_kernel<<<grid_for(npairs, bd), bd, smem, s>>>(npairs, pa, fb, ps, mats, lu, piv, d, iters);
+}
+
+void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int best_match, int64_t abort_above,
+                    const int32_t* lu_status, int32_t* phi, int32_t* creators, int32_t* entry_of, int64_t* state,
+                    cudaStream_t s) {
+  if (B <= 0) return;
+  greedy_resolve_kernel<<<1, 32, 0, s>>>(B, S, D, eps, best_match, abort_above, lu_status, phi, creators, entry_of,
+                                         state);
+}
+
+void l1_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t e1, int len, const double* mats,
+             const int32_t* creators, double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s) {
+  if (nu <= 0 || e1 <= e0) return;
+  l1_scan_kernel<<<grid_for(nu, kL1Threads), kL1Threads, 0, s>>>(nu, pid, e0, e1, len, mats, creators, eps, best_match,
+                                                                 phi, best_d);
+}
+
+void apply_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t ne, const double* d, const int32_t* creators,
+                double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s) {
+  if (nu <= 0 || ne <= 0) return;
+  apply_scan_kernel<<<grid_for(nu, 256), 256, 0, s>>>(nu, pid, e0, ne, d, creators, eps, best_match, phi, best_d);
+}
+
+void argmin_assign(int64_t n, int64_t ne, const double* d, const int32_t* phi, int32_t* new_phi, double* min_dist,
+                   int32_t* changed, cudaStream_t s) {
+  if (n > 0) argmin_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, ne, d, phi, new_phi, min_dist, changed);
+}
+
+void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double* reps, const int32_t* phi,
+               int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s) {
+  if (n > 0)
+    l1_argmin_kernel<<<grid_for(n, kL1Threads), kL1Threads, 0, s>>>(n, ne, len, mats, reps, phi, new_phi, min_dist,
+                                                                    changed);
+}
+
+void cluster_mean(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats, double* reps,
+                  cudaStream_t s) {
+  if (m <= 0) return;
+  dim3 grid(grid_for(len, 128), (unsigned)m);
+  cluster_mean_kernel<<<grid, 128, 0, s>>>(m, len, mem_ptr, mem, mats, reps);
+}
+
+}  // namespace pdb::k

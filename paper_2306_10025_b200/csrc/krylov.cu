@@ -1,0 +1,229 @@
+// Device Krylov drivers.  Vectors stay in HBM; only the small Hessenberg /
+// Givens recurrences and the scalar control flow run on the host.
+//   gmres: reference gmres.cpp:27-169 (restarted GMRES(m), modified
+//          Gram-Schmidt, Givens rotations, right preconditioning by default,
+//          true residual at the end of each cycle).
+//   pcg:   preconditioned CG (absent from the reference), the
+//          same recurrence as oracle/pdb_oracle.c orc_pcg.
+// Dots use the deterministic fixed-tree reduction of kernels/blas.cu.
+#include <cfloat>
+#include <cmath>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace pdb {
+
+namespace {
+
+struct Ops {
+  const DeviceCsr& a;
+  const pdb_precond_s* pc;
+  cudaStream_t s;
+  k::SpmvPlan plan;
+  Scratch<double> partials;
+  Scratch<double> scal;  // device scalars
+  Ops(const DeviceCsr& a_, const pdb_precond_s* pc_, cudaStream_t s_)
+      : a(a_), pc(pc_), s(s_), plan(k::spmv_plan(a_.n, a_.nnz)), partials(static_cast<size_t>(k::dot_partials()), s_),
+        scal(64, s_) {}
+  void spmv(const double* x, double* y) {
+    k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);
+  }
+  void apply(const double* r, double* z) { precond_apply_device(*pc, r, z, s); }
+  // dot into device scalar slot `slot`
+  double* dot_dev(const double* x, const double* y, int slot) {
+    k::dot(a.n, x, y, partials.get(), scal.get() + slot, s);
+    return scal.get() + slot;
+  }
+  double dot(const double* x, const double* y) {
+    double* d = dot_dev(x, y, 63);
+    double h = 0.0;
+    PDB_CUDA(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    return h;
+  }
+  double norm(const double* x) { return std::sqrt(dot(x, x)); }
+};
+
+}  // namespace
+
+void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, const pdb_gmres_options& o,
+                  double* x_host, pdb_report_s& rep, cudaStream_t s) {
+  require_device();
+  const int64_t n = a.n;
+  require(o.restart >= 1, Errc::invalid_argument, "restart length must be >= 1");
+  if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
+  Ops ops(a, pc, s);
+  const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
+  DevBuf<double> b(un), x(un), r0(un), tmp(un), corr(un);
+  b.upload(b_host, static_cast<size_t>(n), s);
+  x.zero(s);
+  rep = pdb_report_s();
+  const double bnorm = ops.norm(b.get());
+  if (bnorm == 0.0) {
+    rep.converged = true;
+    rep.final_relative_residual = 0.0;
+    for (int64_t i = 0; i < n; ++i) x_host[i] = 0.0;
+    return;
+  }
+  const bool left = o.left_precond != 0;
+  auto apply_op = [&](const double* v, double* out) {
+    if (!pc) {
+      ops.spmv(v, out);
+    } else if (left) {
+      ops.spmv(v, tmp.get());
+      ops.apply(tmp.get(), out);
+    } else {
+      ops.apply(v, tmp.get());
+      ops.spmv(tmp.get(), out);
+    }
+  };
+  auto true_relres = [&]() {
+    ops.spmv(x.get(), corr.get());
+    k::sub(n, b.get(), corr.get(), corr.get(), s);
+    return ops.norm(corr.get()) / bnorm;
+  };
+  const size_t m = static_cast<size_t>(o.restart);
+  DevBuf<double> V((m + 1) * un);
+  auto Vp = [&](size_t i) { return V.get() + i * un; };
+  std::vector<std::vector<double>> h(m + 1, std::vector<double>(m, 0.0));
+  std::vector<double> cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0), y(m, 0.0);
+  bool first_cycle = true;
+  for (;;) {
+    if (first_cycle) {
+      PDB_CUDA(cudaMemcpyAsync(r0.get(), b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+      ops.spmv(x.get(), r0.get());
+      k::sub(n, b.get(), r0.get(), r0.get(), s);
+    }
+    if (pc && left) {
+      ops.apply(r0.get(), tmp.get());
+      PDB_CUDA(cudaMemcpyAsync(r0.get(), tmp.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    const double beta = ops.norm(r0.get());
+    if (first_cycle) rep.residual_history.push_back(beta);
+    const double refnorm = rep.residual_history.front();
+    if (beta == 0.0) {
+      rep.converged = true;
+      break;
+    }
+    k::div_scalar(n, r0.get(), beta, Vp(0), s);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    size_t steps = 0;
+    bool breakdown = false;
+    for (size_t j = 0; j < m; ++j) {
+      apply_op(Vp(j), Vp(j + 1));
+      for (size_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt, h_ij stays on device for the axpy
+        double* hij = ops.dot_dev(Vp(j + 1), Vp(i), static_cast<int>(i % 48));
+        k::axpy(n, hij, true, Vp(i), Vp(j + 1), s);
+        double hv = 0.0;
+        PDB_CUDA(cudaMemcpyAsync(&hv, hij, sizeof(double), cudaMemcpyDeviceToHost, s));
+        sync(s);
+        h[i][j] = hv;
+      }
+      const double hj1 = ops.norm(Vp(j + 1));
+      h[j + 1][j] = hj1;
+      if (hj1 > 0.0) k::div_scalar(n, Vp(j + 1), hj1, Vp(j + 1), s);
+      for (size_t i = 0; i < j; ++i) {
+        const double t1 = cs[i] * h[i][j] + sn[i] * h[i + 1][j];
+        const double t2 = -sn[i] * h[i][j] + cs[i] * h[i + 1][j];
+        h[i][j] = t1;
+        h[i + 1][j] = t2;
+      }
+      const double denom = std::hypot(h[j][j], h[j + 1][j]);
+      cs[j] = h[j][j] / denom;
+      sn[j] = h[j + 1][j] / denom;
+      h[j][j] = denom;
+      h[j + 1][j] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++steps;
+      ++rep.iterations;
+      const double est = std::abs(g[j + 1]);
+      rep.residual_history.push_back(std::max(est, DBL_MIN));
+      if (hj1 == 0.0) {
+        breakdown = true;
+        break;
+      }
+      if (est <= o.tol * refnorm || rep.iterations >= o.max_iters) break;
+    }
+    for (size_t i = steps; i-- > 0;) {
+      double sacc = g[i];
+      for (size_t kk = i + 1; kk < steps; ++kk) sacc -= h[i][kk] * y[kk];
+      y[i] = sacc / h[i][i];
+    }
+    tmp.zero(s);
+    for (size_t i = 0; i < steps; ++i) k::axpy_val(n, y[i], Vp(i), tmp.get(), s);
+    if (pc && !left) {
+      ops.apply(tmp.get(), corr.get());
+      k::axpy_val(n, 1.0, corr.get(), x.get(), s);
+    } else {
+      k::axpy_val(n, 1.0, tmp.get(), x.get(), s);
+    }
+    rep.final_relative_residual = true_relres();
+    if (rep.final_relative_residual <= o.tol || breakdown) {
+      rep.converged = rep.final_relative_residual <= o.tol || breakdown;
+      break;
+    }
+    if (rep.iterations >= o.max_iters) break;
+    ++rep.restarts;
+    first_cycle = false;
+  }
+  rep.final_relative_residual = true_relres();
+  x.download(x_host, static_cast<size_t>(n), s);
+  sync(s);
+}
+
+void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol, int64_t max_iters,
+                double* x_host, pdb_report_s& rep, cudaStream_t s) {
+  require_device();
+  const int64_t n = a.n;
+  if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
+  Ops ops(a, pc, s);
+  const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
+  DevBuf<double> b(un), x(un), r(un), z(un), p(un), q(un);
+  b.upload(b_host, static_cast<size_t>(n), s);
+  x.zero(s);
+  PDB_CUDA(cudaMemcpyAsync(r.get(), b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  rep = pdb_report_s();
+  const double bnorm = ops.norm(b.get());
+  if (bnorm == 0.0) {
+    rep.converged = true;
+  } else {
+    rep.residual_history.push_back(1.0);
+    auto precond = [&]() {
+      if (pc) ops.apply(r.get(), z.get());
+      else PDB_CUDA(cudaMemcpyAsync(z.get(), r.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    };
+    precond();
+    PDB_CUDA(cudaMemcpyAsync(p.get(), z.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double rz = ops.dot(r.get(), z.get());
+    while (rep.iterations < max_iters) {
+      ops.spmv(p.get(), q.get());
+      const double alpha = rz / ops.dot(p.get(), q.get());
+      k::axpy_val(n, alpha, p.get(), x.get(), s);
+      k::axpy_val(n, -alpha, q.get(), r.get(), s);
+      ++rep.iterations;
+      const double rel = ops.norm(r.get()) / bnorm;
+      rep.residual_history.push_back(rel);
+      if (rel <= tol) {
+        rep.converged = true;
+        break;
+      }
+      precond();
+      const double rz_new = ops.dot(r.get(), z.get());
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      Scratch<double> bd(1, s);
+      PDB_CUDA(cudaMemcpyAsync(bd.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, s));
+      k::xpay(n, z.get(), bd.get(), p.get(), s);
+      sync(s);
+    }
+  }
+  rep.final_relative_residual = rep.residual_history.empty() ? 0.0 : rep.residual_history.back();
+  x.download(x_host, static_cast<size_t>(n), s);
+  sync(s);
+}
+
+}  // namespace pdb

@@ -1,0 +1,243 @@
+// Device CSR matrices: validation + upload, SpMV, Matrix Market I/O.
+// Reference: sparse.hpp:20-39 (CSR invariants), sparse.cpp:12-48
+// (from_triplets), matrix_market.cpp:29-110 (I/O).
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+#include <thread>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace pdb {
+
+void require_device() {
+  static int state = -1;  // -1 unknown, 0 absent, 1 ok
+  static std::string why;
+  if (state < 0) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+      state = 0;
+      why = e != cudaSuccess ? cudaGetErrorString(e) : "no device";
+    } else {
+      cudaDeviceProp prop;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaGetDeviceProperties(&prop, dev);
+      if (prop.major < 10) {
+        state = 0;
+        why = std::string("device ") + prop.name + " is not sm_100";
+      } else {
+        state = 1;
+      }
+    }
+  }
+  if (state == 0) fail(Errc::internal, "CUDA device unavailable (" + why + "); patchdb-b200 has no CPU path");
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!sms) sms = 148;
+  }
+  return sms;
+}
+
+void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
+  require_device();
+  d.n = h.n;
+  d.nnz = h.nnz();
+  d.row_ptr.alloc(static_cast<size_t>(h.n + 1));
+  d.col.alloc(static_cast<size_t>(d.nnz));
+  d.val.alloc(static_cast<size_t>(d.nnz));
+  d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
+  d.col.upload(h.col.data(), h.col.size(), s);
+  d.val.upload(h.val.data(), h.val.size(), s);
+  sync(s);
+}
+
+HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v) {
+  require(n >= 0, Errc::invalid_argument, "negative matrix dimension");
+  require(n < (Index{1} << 31), Errc::invalid_argument, "matrix has more than 2^31-1 rows");
+  require(rp[0] == 0, Errc::invalid_argument, "row_ptr[0] must be 0");
+  HostCsr h;
+  h.n = n;
+  h.row_ptr.assign(rp, rp + n + 1);
+  for (Index i = 0; i < n; ++i)
+    require(rp[i + 1] >= rp[i], Errc::invalid_argument, "row_ptr must be nondecreasing");
+  const Index nnz = rp[n];
+  h.col.resize(static_cast<size_t>(nnz));
+  h.val.assign(v, v + nnz);
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  std::vector<int> bad(static_cast<size_t>(T), 0);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      const Index b = n * t / T, e = n * (t + 1) / T;
+      for (Index i = b; i < e && !bad[t]; ++i)
+        for (Index p = rp[i]; p < rp[i + 1]; ++p) {
+          const Index c = ci[p];
+          if (c < 0 || c >= n) {
+            bad[t] = 1;
+            break;
+          }
+          if (p > rp[i] && ci[p - 1] >= c) {
+            bad[t] = 2;
+            break;
+          }
+          if (!std::isfinite(v[p])) {
+            bad[t] = 3;
+            break;
+          }
+          h.col[static_cast<size_t>(p)] = static_cast<int32_t>(c);
+        }
+    });
+  for (auto& th : pool) th.join();
+  for (int b : bad) {
+    if (b == 1) fail(Errc::index_out_of_range, "column index outside matrix");
+    if (b == 2) fail(Errc::invalid_argument, "column indices must be strictly increasing within each row");
+    if (b == 3) fail(Errc::invalid_argument, "non-finite matrix entry");
+  }
+  return h;
+}
+
+HostCsr download_csr(const DeviceCsr& d, cudaStream_t s) {
+  HostCsr h;
+  h.n = d.n;
+  h.row_ptr = d.row_ptr.to_host(s);
+  h.col = d.col.to_host(s);
+  h.val = d.val.to_host(s);
+  return h;
+}
+
+void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s) {
+  const k::SpmvPlan plan = k::spmv_plan(a.n, a.nnz);
+  k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);
+  PDB_LAUNCH_CHECK();
+}
+
+// ---- Matrix Market (matrix_market.cpp:29-110) ----------------------------
+
+namespace {
+
+[[noreturn]] void parse_fail(const std::string& name, long line, const std::string& what) {
+  fail(Errc::parse_error, name + ": line " + std::to_string(line) + ": " + what);
+}
+
+std::string lower(std::string s) {
+  std::transform(s.begin(), s.end(), s.begin(), [](unsigned char c) { return static_cast<char>(std::tolower(c)); });
+  return s;
+}
+
+bool blank(const std::string& s) { return s.find_first_not_of(" \t\r\n") == std::string::npos; }
+
+struct Trip {
+  Index r, c;
+  double v;
+};
+
+}  // namespace
+
+// from_triplets (sparse.cpp:12-48): stable sort by (row, col), duplicates
+// summed in insertion order, zero sums kept in the pattern.
+HostCsr csr_from_triplets(Index n, std::vector<Trip>& t);
+
+HostCsr read_matrix_market_host(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) fail(Errc::io_error, "cannot open '" + path + "' for reading");
+  const std::string& name = path;
+  std::string line;
+  long lineno = 0;
+  if (!std::getline(in, line)) parse_fail(name, 1, "empty file");
+  ++lineno;
+  std::istringstream hs(line);
+  std::string banner, object, format, field, symmetry;
+  hs >> banner >> object >> format >> field >> symmetry;
+  if (banner != "%%MatrixMarket") parse_fail(name, lineno, "missing %%MatrixMarket banner");
+  if (lower(object) != "matrix" || lower(format) != "coordinate")
+    parse_fail(name, lineno, "only coordinate-format matrices are supported");
+  if (lower(field) != "real") parse_fail(name, lineno, "only real matrices are supported");
+  const std::string sym = lower(symmetry);
+  if (sym != "general" && sym != "symmetric") parse_fail(name, lineno, "only general or symmetric matrices are supported");
+  const bool expand = sym == "symmetric";
+  Index rows = 0, cols = 0;
+  long long nnz = 0;
+  for (;;) {
+    if (!std::getline(in, line)) parse_fail(name, lineno + 1, "unexpected end of file before size line");
+    ++lineno;
+    if (!line.empty() && line[0] == '%') continue;
+    if (blank(line)) continue;
+    std::istringstream ss(line);
+    if (!(ss >> rows >> cols >> nnz)) parse_fail(name, lineno, "malformed size line");
+    break;
+  }
+  if (rows != cols)
+    fail(Errc::non_square_matrix,
+         name + ": matrix is " + std::to_string(rows) + "x" + std::to_string(cols) + ", expected square");
+  std::vector<Trip> entries;
+  entries.reserve(static_cast<size_t>(expand ? 2 * nnz : nnz));
+  for (long long k = 0; k < nnz; ++k) {
+    if (!std::getline(in, line)) parse_fail(name, lineno + 1, "unexpected end of file in entry list");
+    ++lineno;
+    if (blank(line)) {
+      --k;
+      continue;
+    }
+    std::istringstream ss(line);
+    Index i = 0, j = 0;
+    double v = 0.0;
+    if (!(ss >> i >> j >> v)) parse_fail(name, lineno, "malformed entry");
+    if (i < 1 || i > rows || j < 1 || j > cols) parse_fail(name, lineno, "entry index out of range");
+    if (!std::isfinite(v)) parse_fail(name, lineno, "non-finite entry value");
+    entries.push_back({i - 1, j - 1, v});
+    if (expand && i != j) entries.push_back({j - 1, i - 1, v});
+  }
+  return csr_from_triplets(rows, entries);
+}
+
+HostCsr csr_from_triplets(Index n, std::vector<Trip>& t) {
+  require(n >= 0, Errc::invalid_argument, "negative matrix dimension");
+  std::stable_sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
+  HostCsr h;
+  h.n = n;
+  h.row_ptr.assign(static_cast<size_t>(n + 1), 0);
+  size_t k = 0;
+  for (Index i = 0; i < n; ++i) {
+    while (k < t.size() && t[k].r == i) {
+      const Index c = t[k].c;
+      double v = t[k].v;
+      ++k;
+      while (k < t.size() && t[k].r == i && t[k].c == c) {
+        v += t[k].v;
+        ++k;
+      }
+      h.col.push_back(static_cast<int32_t>(c));
+      h.val.push_back(v);
+    }
+    h.row_ptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(h.col.size());
+  }
+  return h;
+}
+
+void write_matrix_market_host(const HostCsr& a, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) fail(Errc::io_error, "cannot open '" + path + "' for writing");
+  out << "%%MatrixMarket matrix coordinate real general\n";
+  out << a.n << ' ' << a.n << ' ' << a.nnz() << '\n';
+  char buf[64];
+  for (Index i = 0; i < a.n; ++i)
+    for (Index p = a.row_ptr[static_cast<size_t>(i)]; p < a.row_ptr[static_cast<size_t>(i + 1)]; ++p) {
+      std::snprintf(buf, sizeof(buf), "%.17g", a.val[static_cast<size_t>(p)]);
+      out << (i + 1) << ' ' << (a.col[static_cast<size_t>(p)] + 1) << ' ' << buf << '\n';
+    }
+  if (!out) fail(Errc::io_error, "error while writing '" + path + "'");
+}
+
+}  // namespace pdb

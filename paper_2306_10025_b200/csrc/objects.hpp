@@ -1,0 +1,98 @@
+// Handle types behind the opaque pointers of include/patchdb/patchdb.h.
+//
+// Layout in HBM:
+//   matrix    CSR, row_ptr int64[n+1], col int32[nnz], val fp64[nnz]
+//   patchset  patches int32[np*ps] (ascending per patch), weights fp64[n]
+//   database  reps / lu fp64[m*ps*ps] row-major (reference layout), piv int32[m*ps], phi int32[np]
+//   precond   factors fp64[nf*ps*ps] COLUMN-major per factor (lane i reads L(i,j)/U(i,j) of
+//             column j at consecutive addresses), piv int32[nf*ps], phi int32[np],
+//             omega_w fp64[n], DOF->(patch,slot) inverse map inv_ptr int32[n+1], inv int32[np*ps]
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace pdb {
+
+struct HostCsr {
+  Index n = 0;
+  std::vector<int64_t> row_ptr;
+  std::vector<int32_t> col;
+  std::vector<double> val;
+  Index nnz() const { return static_cast<Index>(col.size()); }
+};
+
+struct DeviceCsr {
+  Index n = 0;
+  Index nnz = 0;
+  DevBuf<int64_t> row_ptr;
+  DevBuf<int32_t> col;
+  DevBuf<double> val;
+};
+
+struct BuildWork {
+  int64_t pair_evals = 0;
+  int64_t power_iters = 0;
+  int64_t lu_count = 0;
+};
+
+}  // namespace pdb
+
+struct pdb_problem_s {
+  pdb::HostCsr a;
+  std::vector<double> rhs;
+  bool has_exact = false;
+  std::vector<double> exact;  // manufactured solution (uniform-mesh assembler only)
+  int dim = 2;
+  int64_t cells = 0;
+  int degree = 1;
+};
+
+struct pdb_matrix_s {
+  pdb::DeviceCsr a;
+};
+
+struct pdb_patchset_s {
+  int64_t n = 0;   // rows of the matrix it was detected on
+  int64_t np = 0;  // patches
+  int64_t ps = 0;  // patch size
+  pdb::DevBuf<int32_t> patches;
+  pdb::DevBuf<double> weights;
+};
+
+struct pdb_database_s {
+  int64_t m = 0, np = 0, ps = 0;
+  pdb::DevBuf<double> reps;
+  pdb::DevBuf<double> lu;
+  pdb::DevBuf<int32_t> piv;
+  pdb::DevBuf<int32_t> phi;
+  std::string method;
+  double eps = 0.0;
+  std::vector<std::vector<uint8_t>> entry_patterns;  // per entry, partitioned k-means only
+  pdb::BuildWork work;
+};
+
+struct pdb_precond_s {
+  int64_t n = 0, np = 0, ps = 0, nf = 0;
+  double omega = 1.0;
+  bool compressed = false;
+  pdb::DevBuf<int32_t> patches;
+  pdb::DevBuf<double> omega_w;
+  pdb::DevBuf<double> factors;  // column-major per factor
+  pdb::DevBuf<int32_t> piv;
+  pdb::DevBuf<int32_t> phi;     // compressed mode only
+  pdb::DevBuf<int32_t> inv_ptr;
+  pdb::DevBuf<int32_t> inv;
+};
+
+struct pdb_report_s {
+  int64_t iterations = 0;
+  int64_t restarts = 0;
+  bool converged = false;
+  double final_relative_residual = 0.0;
+  std::vector<double> residual_history;
+};

@@ -1,0 +1,489 @@
+"""Python mirror of the patchdb C-ABI, backed by the B200 library.
+
+Thin ctypes bindings over ``lib/libpatchdb.so.0`` (built from ``csrc/``).
+The classes mirror the reference handles one-to-one (``pdb_matrix``,
+``pdb_patchset``, ``pdb_database``, ``pdb_precond``, ``pdb_report``; see
+/root/reference/proj/include/patchdb/patchdb.h) and raise :class:`PatchdbError`
+with the reference status code and message whenever a call returns non-OK.
+
+There is no fallback: if the shared library is missing this module fails
+to import, and on a machine without an sm_100 GPU every compute call raises
+``PatchdbError(PDB_ERR_INTERNAL, "CUDA device unavailable ...")``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpatchdb.so.0")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(no CPU fallback exists)")
+
+_lib = C.CDLL(LIB_PATH)
+
+# ---- status codes (patchdb.h:25-41) -------------------------------------
+PDB_OK = 0
+PDB_ERR_INVALID_ARGUMENT = 1
+PDB_ERR_DIMENSION_MISMATCH = 2
+PDB_ERR_SINGULAR_MATRIX = 3
+PDB_ERR_INDEX_OUT_OF_RANGE = 4
+PDB_ERR_DUPLICATE_INDEX = 5
+PDB_ERR_PARSE = 6
+PDB_ERR_NON_SQUARE_MATRIX = 7
+PDB_ERR_NO_PATCHES_FOUND = 8
+PDB_ERR_EMPTY_CLUSTER = 9
+PDB_ERR_BUDGET_TOO_SMALL = 10
+PDB_ERR_INVALID_DEGREE = 11
+PDB_ERR_NON_POSITIVE_COEFFICIENT = 12
+PDB_ERR_IO = 13
+PDB_ERR_INTERNAL = 14
+
+# ---- methods (patchdb.h:88-96) -------------------------------------------
+EXACT, GREEDY_SPECTRAL, GREEDY_L1, KMEANS_ENTRYWISE, KMEANS_SPECTRAL, KMEANS_VARMIN, BOOTSTRAP = range(7)
+
+
+class PatchdbError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+        self.message = message
+
+
+class CompressOptions(C.Structure):
+    """pdb_compress_options: 48 bytes, offsets 0/8/16/24/32/36/40 (patchdb.h:98-106)."""
+    _fields_ = [("method", C.c_int), ("eps", C.c_double), ("db_size", C.c_int64), ("seed", C.c_uint64),
+                ("max_iters", C.c_int), ("best_match", C.c_int), ("threads", C.c_int)]
+
+
+class GmresOptions(C.Structure):
+    """pdb_gmres_options: 32 bytes, offsets 0/8/16/24/28 (patchdb.h:134-140)."""
+    _fields_ = [("restart", C.c_int64), ("tol", C.c_double), ("max_iters", C.c_int64), ("left_precond", C.c_int),
+                ("threads", C.c_int)]
+
+
+class GenOptions(C.Structure):
+    _fields_ = [("physics", C.c_int), ("dim", C.c_int), ("degree", C.c_int), ("bc_mode", C.c_int),
+                ("cells", C.c_int64), ("jitter", C.c_double), ("seed", C.c_uint64), ("coeff_kind", C.c_int),
+                ("n_levels", C.c_int), ("coeff_value", C.c_double), ("block_cells", C.c_int64),
+                ("levels", C.c_double * 8), ("threads", C.c_int), ("reserved", C.c_int)]
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+# Every symbol of include/patchdb/patchdb.h.
+_sig("pdb_status_string", C.c_char_p, C.c_int)
+_sig("pdb_last_error", C.c_char_p)
+_sig("pdb_build_info", C.c_char_p)
+_sig("pdb_matrix_read_matrix_market", C.c_int, C.c_char_p, C.POINTER(_P))
+_sig("pdb_matrix_write_matrix_market", C.c_int, _P, C.c_char_p)
+_sig("pdb_matrix_rows", C.c_int64, _P)
+_sig("pdb_matrix_nnz", C.c_int64, _P)
+_sig("pdb_matrix_spmv", C.c_int, _P, _D, _D)
+_sig("pdb_matrix_spmv_device", C.c_int, _P, C.c_void_p, C.c_void_p, C.c_void_p)
+_sig("pdb_matrix_free", None, _P)
+_sig("pdb_matrix_from_csr", C.c_int, C.c_int64, _I64, _I64, _D, C.POINTER(_P))
+_sig("pdb_matrix_csr", C.c_int, _P, _I64, _I64, _D)
+_sig("pdb_problem_assemble", C.c_int, C.c_char_p, C.POINTER(_P))
+_sig("pdb_problem_ndofs", C.c_int64, _P)
+_sig("pdb_problem_nnz", C.c_int64, _P)
+_sig("pdb_problem_matrix", C.c_int, _P, C.POINTER(_P))
+_sig("pdb_problem_rhs", C.c_int, _P, _D)
+_sig("pdb_problem_csr", C.c_int, _P, _I64, _I64, _D)
+_sig("pdb_problem_exact_solution", C.c_int, _P, _D)
+_sig("pdb_problem_l2_error", C.c_int, _P, _D, _D)
+_sig("pdb_problem_free", None, _P)
+_sig("pdb_gen_options_init", None, C.POINTER(GenOptions))
+_sig("pdb_gen_options_config", C.c_int, C.c_int, C.c_int64, C.POINTER(GenOptions))
+_sig("pdb_problem_generate", C.c_int, C.POINTER(GenOptions), C.POINTER(_P))
+_sig("pdb_patchset_detect", C.c_int, _P, C.c_int64, C.POINTER(_P))
+_sig("pdb_patchset_count", C.c_int64, _P)
+_sig("pdb_patchset_patch_size", C.c_int64, _P)
+_sig("pdb_patchset_rows", C.c_int64, _P)
+_sig("pdb_patchset_write_json", C.c_int, _P, C.c_char_p)
+_sig("pdb_patchset_patches", C.c_int, _P, _I64)
+_sig("pdb_patchset_weights", C.c_int, _P, _D)
+_sig("pdb_patchset_extract", C.c_int, _P, _P, _D)
+_sig("pdb_patchset_free", None, _P)
+_sig("pdb_compress_options_init", None, C.POINTER(CompressOptions))
+_sig("pdb_database_build", C.c_int, _P, _P, C.POINTER(CompressOptions), C.POINTER(_P))
+_sig("pdb_database_build_to_size", C.c_int, _P, _P, C.POINTER(CompressOptions), C.c_int64, C.c_int64,
+     C.POINTER(_P), _D)
+_sig("pdb_database_size", C.c_int64, _P)
+_sig("pdb_database_n_patches", C.c_int64, _P)
+_sig("pdb_database_patch_size", C.c_int64, _P)
+_sig("pdb_database_eps", C.c_double, _P)
+_sig("pdb_database_phi", C.c_int, _P, _I64)
+_sig("pdb_database_representatives", C.c_int, _P, _D)
+_sig("pdb_database_factors", C.c_int, _P, _D, _I64)
+_sig("pdb_database_work", C.c_int, _P, _I64, _I64, _I64)
+_sig("pdb_database_export", C.c_int, _P, C.c_char_p, C.c_char_p)
+_sig("pdb_database_free", None, _P)
+_sig("pdb_precond_create", C.c_int, _P, _P, _P, C.c_double, C.c_int, C.POINTER(_P))
+_sig("pdb_precond_create_combo", C.c_int, _P, _P, _P, C.c_double, C.c_int, C.POINTER(_P))
+_sig("pdb_precond_apply", C.c_int, _P, _D, _D)
+_sig("pdb_precond_apply_device", C.c_int, _P, C.c_void_p, C.c_void_p, C.c_void_p)
+_sig("pdb_relax", C.c_int, _P, _P, _D, _D, C.c_int64, _D)
+_sig("pdb_relax_device", C.c_int, _P, _P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+_sig("pdb_precond_free", None, _P)
+_sig("pdb_gmres_options_init", None, C.POINTER(GmresOptions))
+_sig("pdb_gmres_solve", C.c_int, _P, _D, _P, C.POINTER(GmresOptions), _D, C.POINTER(_P))
+_sig("pdb_pcg_solve", C.c_int, _P, _D, _P, C.c_double, C.c_int64, _D, C.POINTER(_P))
+_sig("pdb_report_iterations", C.c_int64, _P)
+_sig("pdb_report_restarts", C.c_int64, _P)
+_sig("pdb_report_converged", C.c_int, _P)
+_sig("pdb_report_final_relative_residual", C.c_double, _P)
+_sig("pdb_report_residual_history_size", C.c_int64, _P)
+_sig("pdb_report_residual_history", C.c_int, _P, _D)
+_sig("pdb_report_free", None, _P)
+_sig("pdb_run_experiment", C.c_int, C.c_char_p, C.c_char_p)
+_sig("pdb_run_analyze", C.c_int, C.c_char_p, C.c_char_p, C.c_char_p)
+_sig("pdb_run_benchmark", C.c_int, C.c_char_p, C.c_char_p)
+_sig("pdb_export_matrix", C.c_int, C.c_char_p, C.c_char_p)
+
+lib = _lib
+
+
+def _check(status: int) -> None:
+    if status != PDB_OK:
+        raise PatchdbError(status, _lib.pdb_last_error().decode())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_D)
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(_I64)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def build_info() -> str:
+    return _lib.pdb_build_info().decode()
+
+
+class _Handle:
+    _free = None
+
+    def __init__(self, ptr: C.c_void_p):
+        self._ptr = ptr
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def close(self):
+        if self._ptr:
+            type(self)._free(self._ptr)
+            self._ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Matrix(_Handle):
+    """Device CSR matrix (pdb_matrix)."""
+    _free = _lib.pdb_matrix_free
+
+    @classmethod
+    def from_csr(cls, row_ptr, col_idx, values) -> "Matrix":
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int64)
+        v = _f64(values)
+        out = C.c_void_p()
+        _check(_lib.pdb_matrix_from_csr(len(rp) - 1, _ip(rp), _ip(ci), _dp(v), C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def read_matrix_market(cls, path: str) -> "Matrix":
+        out = C.c_void_p()
+        _check(_lib.pdb_matrix_read_matrix_market(path.encode(), C.byref(out)))
+        return cls(out)
+
+    def write_matrix_market(self, path: str) -> None:
+        _check(_lib.pdb_matrix_write_matrix_market(self._ptr, path.encode()))
+
+    @property
+    def rows(self) -> int:
+        return _lib.pdb_matrix_rows(self._ptr)
+
+    @property
+    def nnz(self) -> int:
+        return _lib.pdb_matrix_nnz(self._ptr)
+
+    def spmv(self, x) -> np.ndarray:
+        x = _f64(x)
+        y = np.empty(self.rows)
+        _check(_lib.pdb_matrix_spmv(self._ptr, _dp(x), _dp(y)))
+        return y
+
+    def csr(self):
+        n, nnz = self.rows, self.nnz
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(nnz, np.int64)
+        v = np.empty(nnz)
+        _check(_lib.pdb_matrix_csr(self._ptr, _ip(rp), _ip(ci), _dp(v)))
+        return rp, ci, v
+
+
+class Problem(_Handle):
+    """Host-side generated problem (pdb_problem)."""
+    _free = _lib.pdb_problem_free
+
+    @classmethod
+    def generate(cls, config: int = 1, cells: int = 0, **overrides) -> "Problem":
+        o = GenOptions()
+        _check(_lib.pdb_gen_options_config(config, cells, C.byref(o)))
+        for k, v in overrides.items():
+            if k == "levels":
+                for i, x in enumerate(v):
+                    o.levels[i] = x
+                o.n_levels = len(v)
+            else:
+                setattr(o, k, v)
+        out = C.c_void_p()
+        _check(_lib.pdb_problem_generate(C.byref(o), C.byref(out)))
+        return cls(out)
+
+    @property
+    def ndofs(self) -> int:
+        return _lib.pdb_problem_ndofs(self._ptr)
+
+    @property
+    def nnz(self) -> int:
+        return _lib.pdb_problem_nnz(self._ptr)
+
+    def rhs(self) -> np.ndarray:
+        b = np.empty(self.ndofs)
+        _check(_lib.pdb_problem_rhs(self._ptr, _dp(b)))
+        return b
+
+    def csr(self):
+        n, nnz = self.ndofs, self.nnz
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(nnz, np.int64)
+        v = np.empty(nnz)
+        _check(_lib.pdb_problem_csr(self._ptr, _ip(rp), _ip(ci), _dp(v)))
+        return rp, ci, v
+
+    def matrix(self) -> Matrix:
+        out = C.c_void_p()
+        _check(_lib.pdb_problem_matrix(self._ptr, C.byref(out)))
+        return Matrix(out)
+
+
+class PatchSet(_Handle):
+    """Detected cell patches (pdb_patchset)."""
+    _free = _lib.pdb_patchset_free
+
+    @classmethod
+    def detect(cls, m: Matrix, patch_size: int) -> "PatchSet":
+        out = C.c_void_p()
+        _check(_lib.pdb_patchset_detect(m.ptr, patch_size, C.byref(out)))
+        return cls(out)
+
+    @property
+    def count(self) -> int:
+        return _lib.pdb_patchset_count(self._ptr)
+
+    @property
+    def patch_size(self) -> int:
+        return _lib.pdb_patchset_patch_size(self._ptr)
+
+    @property
+    def rows(self) -> int:
+        return _lib.pdb_patchset_rows(self._ptr)
+
+    def patches(self) -> np.ndarray:
+        out = np.empty((self.count, self.patch_size), np.int64)
+        _check(_lib.pdb_patchset_patches(self._ptr, _ip(out)))
+        return out
+
+    def weights(self) -> np.ndarray:
+        out = np.empty(self.rows)
+        _check(_lib.pdb_patchset_weights(self._ptr, _dp(out)))
+        return out
+
+    def extract(self, m: Matrix) -> np.ndarray:
+        out = np.empty((self.count, self.patch_size, self.patch_size))
+        _check(_lib.pdb_patchset_extract(m.ptr, self._ptr, _dp(out)))
+        return out
+
+    def write_json(self, path: str) -> None:
+        _check(_lib.pdb_patchset_write_json(self._ptr, path.encode()))
+
+
+def compress_options(method: int = GREEDY_L1, **kw) -> CompressOptions:
+    o = CompressOptions()
+    _lib.pdb_compress_options_init(C.byref(o))
+    o.method = method
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+class Database(_Handle):
+    """Factorization database + assignment phi (pdb_database)."""
+    _free = _lib.pdb_database_free
+
+    @classmethod
+    def build(cls, m: Matrix, ps: PatchSet, method: int = GREEDY_L1, **kw) -> "Database":
+        o = compress_options(method, **kw)
+        out = C.c_void_p()
+        _check(_lib.pdb_database_build(m.ptr, ps.ptr, C.byref(o), C.byref(out)))
+        return cls(out)
+
+    @classmethod
+    def build_to_size(cls, m: Matrix, ps: PatchSet, target_lo: int, target_hi: int, method: int = GREEDY_L1,
+                      **kw):
+        o = compress_options(method, **kw)
+        out = C.c_void_p()
+        eps = C.c_double()
+        _check(_lib.pdb_database_build_to_size(m.ptr, ps.ptr, C.byref(o), target_lo, target_hi, C.byref(out),
+                                               C.byref(eps)))
+        return cls(out), eps.value
+
+    @property
+    def size(self) -> int:
+        return _lib.pdb_database_size(self._ptr)
+
+    @property
+    def n_patches(self) -> int:
+        return _lib.pdb_database_n_patches(self._ptr)
+
+    @property
+    def patch_size(self) -> int:
+        return _lib.pdb_database_patch_size(self._ptr)
+
+    @property
+    def eps(self) -> float:
+        return _lib.pdb_database_eps(self._ptr)
+
+    def phi(self) -> np.ndarray:
+        out = np.empty(self.n_patches, np.int64)
+        _check(_lib.pdb_database_phi(self._ptr, _ip(out)))
+        return out
+
+    def representatives(self) -> np.ndarray:
+        ps = self.patch_size
+        out = np.empty((self.size, ps, ps))
+        _check(_lib.pdb_database_representatives(self._ptr, _dp(out)))
+        return out
+
+    def factors(self):
+        ps = self.patch_size
+        lu = np.empty((self.size, ps, ps))
+        piv = np.empty((self.size, ps), np.int64)
+        _check(_lib.pdb_database_factors(self._ptr, _dp(lu), _ip(piv)))
+        return lu, piv
+
+    def work(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(_lib.pdb_database_work(self._ptr, C.byref(a), C.byref(b), C.byref(c)))
+        return {"pair_evals": a.value, "power_iters": b.value, "lu_count": c.value}
+
+    def export(self, json_path: str, bin_path: str) -> None:
+        _check(_lib.pdb_database_export(self._ptr, json_path.encode(), bin_path.encode()))
+
+
+class Preconditioner(_Handle):
+    """Patch preconditioner (pdb_precond); db=None selects the exact variant."""
+    _free = _lib.pdb_precond_free
+
+    def __init__(self, ptr, n: int):
+        super().__init__(ptr)
+        self.n = n
+
+    @classmethod
+    def create(cls, m: Optional[Matrix], ps: PatchSet, db: Optional[Database] = None, omega: float = 1.0,
+               threads: int = 1) -> "Preconditioner":
+        out = C.c_void_p()
+        _check(_lib.pdb_precond_create(m.ptr if m is not None else None, ps.ptr, db.ptr if db is not None else None,
+                                       omega, threads, C.byref(out)))
+        return cls(out, ps.rows)
+
+    def apply(self, r) -> np.ndarray:
+        r = _f64(r)
+        z = np.empty(self.n)
+        _check(_lib.pdb_precond_apply(self._ptr, _dp(r), _dp(z)))
+        return z
+
+    def apply_device(self, d_r: int, d_z: int, stream: int = 0) -> None:
+        _check(_lib.pdb_precond_apply_device(self._ptr, d_r, d_z, stream or None))
+
+    def relax(self, m: Matrix, b, x, sweeps: int, history: bool = True):
+        """`sweeps` smooth() steps from x (copied); returns (x_new, history or None)."""
+        b = _f64(b)
+        xn = _f64(x).copy()
+        hist = np.empty(sweeps + 1) if history else None
+        _check(_lib.pdb_relax(m.ptr, self._ptr, _dp(b), _dp(xn), sweeps, _dp(hist) if history else None))
+        return xn, hist
+
+    def relax_device(self, m: Matrix, d_b: int, d_x: int, sweeps: int, d_hist: int = 0, stream: int = 0) -> None:
+        _check(_lib.pdb_relax_device(m.ptr, self._ptr, d_b, d_x, sweeps, d_hist or None, stream or None))
+
+
+@dataclass
+class Report:
+    iterations: int
+    restarts: int
+    converged: bool
+    final_relative_residual: float
+    residual_history: np.ndarray
+
+
+def _report(ptr) -> Report:
+    try:
+        n = _lib.pdb_report_residual_history_size(ptr)
+        h = np.empty(n)
+        if n:
+            _check(_lib.pdb_report_residual_history(ptr, _dp(h)))
+        return Report(_lib.pdb_report_iterations(ptr), _lib.pdb_report_restarts(ptr),
+                      bool(_lib.pdb_report_converged(ptr)), _lib.pdb_report_final_relative_residual(ptr), h)
+    finally:
+        _lib.pdb_report_free(ptr)
+
+
+def gmres(m: Matrix, b, pc: Optional[Preconditioner] = None, restart: int = 20, tol: float = 1e-8,
+          max_iters: int = 2000, left_precond: bool = False):
+    o = GmresOptions()
+    _lib.pdb_gmres_options_init(C.byref(o))
+    o.restart, o.tol, o.max_iters, o.left_precond = restart, tol, max_iters, int(left_precond)
+    b = _f64(b)
+    x = np.empty(m.rows)
+    rep = C.c_void_p()
+    _check(_lib.pdb_gmres_solve(m.ptr, _dp(b), pc.ptr if pc is not None else None, C.byref(o), _dp(x),
+                                C.byref(rep)))
+    return x, _report(rep)
+
+
+def pcg(m: Matrix, b, pc: Optional[Preconditioner] = None, tol: float = 1e-8, max_iters: int = 10000):
+    b = _f64(b)
+    x = np.empty(m.rows)
+    rep = C.c_void_p()
+    _check(_lib.pdb_pcg_solve(m.ptr, _dp(b), pc.ptr if pc is not None else None, tol, max_iters, _dp(x),
+                              C.byref(rep)))
+    return x, _report(rep)
