@@ -221,7 +221,19 @@ PDB_API pdb_status pdb_relax(pdb_matrix m, pdb_precond pc, const double* b, doub
 PDB_API pdb_status pdb_relax_device(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
                                     double* d_history, void* stream);
 
-/* Preconditioned conjugate gradients, x0 = 0, stop when ||r||/||b|| <= tol. */
+/* pdb_relax_device with CUDA events around each sweep kernel: ms_phase[3]
+ * (host) receives the average milliseconds of the residual SpMV, the patch
+ * solve and the scatter/update kernels (roofline accounting in bench.py). */
+PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
+                                     double* ms_phase, void* stream);
+/* Sweep-structure sizes: stored factors (n_p exact, m_p compressed), patches, patch size. */
+PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc);
+PDB_API int64_t pdb_precond_patch_count(pdb_precond pc);
+PDB_API int64_t pdb_precond_patch_size(pdb_precond pc);
+
+/* Preconditioned conjugate gradients, x0 = 0, stop when ||r||/||b|| <= tol.
+ * The patch preconditioner is applied with symmetric weighting
+ * omega W^1/2 S W^1/2 (CG needs a symmetric preconditioner). */
 PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
                                  double* x, pdb_report* out_report);
 

@@ -333,6 +333,14 @@ class RefLib:
         L.refh_assemble.argtypes = [C.c_int, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_int64, C.c_int64, _D,
                                     C.c_int64, C.POINTER(_P), _D]
         L.refh_matrix_csr.argtypes = [_P, _I64, _I64, _D]
+        L.refh_db_from_arrays.restype = _P
+        L.refh_db_from_arrays.argtypes = [C.c_int64, C.c_int64, C.c_int64, _D, _D, _I64, _I64]
+
+    def database(self, reps, lu, piv, phi):
+        reps, lu, piv, phi = _f64(reps), _f64(lu), _i64(piv), _i64(phi)
+        m, ps = reps.shape[0], reps.shape[1]
+        return RefDatabase(self, self.lib.refh_db_from_arrays(m, ps, len(phi), _dp(reps), _dp(lu), _ip(piv),
+                                                             _ip(phi)))
 
     def _check(self, st):
         if st != 0:

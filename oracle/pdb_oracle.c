@@ -1234,9 +1234,35 @@ int orc_gmres(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, 
   return ST_OK;
 }
 
+/* Symmetrically weighted patch preconditioner used by PCG:
+ *   z = omega W^{1/2} sum_k V_k^T B_phi(k)^{-1} V_k W^{1/2} r.
+ * CG needs a symmetric preconditioner; the reference's left scaling
+ * omega W S (precond.cpp:87) is not symmetric and makes CG stagnate, so the
+ * weight is split evenly between gather and scatter.
+ * Same patch solves and scatter order as orc_precond_apply. */
+static void pc_apply_sym(const pc_t* pc, const double* r, double* z) {
+  const int64_t ps = pc->ps, len = ps * ps;
+  double* sols = (double*)malloc(sizeof(double) * (size_t)(pc->np * ps));
+  double* local = (double*)malloc(sizeof(double) * (size_t)ps);
+  for (int64_t k = 0; k < pc->np; ++k) {
+    const int64_t* idx = pc->patches + k * ps;
+    for (int64_t i = 0; i < ps; ++i) local[i] = r[idx[i]] * sqrt(pc->weights[idx[i]]);
+    const int64_t f = pc->phi ? pc->phi[k] : k;
+    orc_lu_solve(ps, pc->lu + f * len, pc->piv + f * ps, local, sols + k * ps);
+  }
+  for (int64_t i = 0; i < pc->n; ++i) z[i] = 0.0;
+  for (int64_t k = 0; k < pc->np; ++k) {
+    const int64_t* idx = pc->patches + k * ps;
+    for (int64_t i = 0; i < ps; ++i) z[idx[i]] += sols[k * ps + i];
+  }
+  for (int64_t i = 0; i < pc->n; ++i) z[i] *= pc->omega * sqrt(pc->weights[i]);
+  free(sols);
+  free(local);
+}
+
 /* Preconditioned CG (not in the reference; SPEC.md:509 lists CG as absent).
- * Textbook Hestenes-Stiefel form with z = M^{-1} r; the GPU implementation
- * (pdb_pcg_solve) follows the same recurrence. */
+ * Textbook Hestenes-Stiefel form with z = M_sym^{-1} r (pc_apply_sym); the GPU
+ * implementation (pdb_pcg_solve) follows the same recurrence. */
 int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b, int64_t np, int64_t ps,
             const int64_t* patches, const double* weights, double omega, const double* lu, const int64_t* piv,
             const int64_t* phi, int have_pc, double tol, int64_t max_iters, double* x, int64_t* iters_out,
@@ -1260,7 +1286,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, co
   } else {
     if (hl < hcap) hist[hl] = 1.0;
     ++hl;
-    if (have_pc) pc_apply(&pc, r, z);
+    if (have_pc) pc_apply_sym(&pc, r, z);
     else memcpy(z, r, sizeof(double) * (size_t)n);
     memcpy(p, z, sizeof(double) * (size_t)n);
     double rz = dot(n, r, z);
@@ -1277,7 +1303,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, co
         converged = 1;
         break;
       }
-      if (have_pc) pc_apply(&pc, r, z);
+      if (have_pc) pc_apply_sym(&pc, r, z);
       else memcpy(z, r, sizeof(double) * (size_t)n);
       const double rz_new = dot(n, r, z);
       const double beta = rz_new / rz;

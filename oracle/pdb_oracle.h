@@ -91,7 +91,9 @@ int orc_gmres(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, 
               int left, double* x, int64_t* iters, int64_t* restarts, int* converged, double* relres, double* hist,
               int64_t* hist_len);
 /* Preconditioned CG (not in the reference): x0 = 0, stop when
- * ||r||/||b|| <= tol; hist[k] = ||r_k||/||b||. */
+ * ||r||/||b|| <= tol; hist[k] = ||r_k||/||b||.  The preconditioner is the
+ * symmetrically weighted patch relaxation omega W^1/2 S W^1/2 (CG needs a
+ * symmetric M; the reference's omega W S is not). */
 int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b, int64_t np, int64_t ps,
             const int64_t* patches, const double* weights, double omega, const double* lu, const int64_t* piv,
             const int64_t* phi, int have_pc, double tol, int64_t max_iters, double* x, int64_t* iters,

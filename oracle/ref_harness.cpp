@@ -203,6 +203,26 @@ RH_API int refh_db_bisect(void* m, void* ps, int spectral, int64_t lo, int64_t h
   });
 }
 
+// A Database from explicit arrays (representatives, factors, pivots, phi):
+// lets the CPU baseline time the reference sweep on a database built
+// elsewhere (the sweep cost depends only on the sizes).
+RH_API void* refh_db_from_arrays(int64_t m, int64_t ps, int64_t np, const double* reps, const double* lu,
+                                 const int64_t* piv, const int64_t* phi) {
+  auto* db = new Database();
+  db->method = "external";
+  db->entries.resize(static_cast<size_t>(m));
+  const int64_t len = ps * ps;
+  for (int64_t j = 0; j < m; ++j) {
+    auto& e = db->entries[static_cast<size_t>(j)];
+    e.representative = dense_from(ps, reps + j * len);
+    e.factor.dim = ps;
+    e.factor.lu = dense_from(ps, lu + j * len);
+    e.factor.pivots.assign(piv + j * ps, piv + (j + 1) * ps);
+  }
+  db->phi.assign(phi, phi + np);
+  return db;
+}
+
 RH_API int64_t refh_db_size(void* db) { return static_cast<Database*>(db)->size(); }
 RH_API int64_t refh_db_n_patches(void* db) { return static_cast<Database*>(db)->n_patches(); }
 RH_API double refh_db_eps(void* db) { return static_cast<Database*>(db)->eps; }

@@ -470,6 +470,21 @@ PDB_API pdb_status pdb_relax_device(pdb_matrix m, pdb_precond pc, const double* 
   });
 }
 
+PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
+                                     double* ms_phase, void* stream) {
+  if (m == nullptr || pc == nullptr || d_b == nullptr || d_x == nullptr || ms_phase == nullptr)
+    return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    require(sweeps >= 1, Errc::invalid_argument, "sweeps must be >= 1");
+    relax_profile(m->a, *pc, d_b, d_x, sweeps, ms_phase, stream_of(stream));
+  });
+}
+
+PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc) { return pc == nullptr ? 0 : pc->nf; }
+PDB_API int64_t pdb_precond_patch_count(pdb_precond pc) { return pc == nullptr ? 0 : pc->np; }
+PDB_API int64_t pdb_precond_patch_size(pdb_precond pc) { return pc == nullptr ? 0 : pc->ps; }
+
 PDB_API void pdb_precond_free(pdb_precond pc) { delete pc; }
 
 /* ---- solvers ---- */

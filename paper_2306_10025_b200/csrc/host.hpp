@@ -51,11 +51,16 @@ void export_database(const pdb_database_s& db, const std::string& json_path, con
 void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& out, cudaStream_t s);
 void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
                         cudaStream_t s);
-// z = M^{-1} r on device pointers.
-void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s);
+// z = M^{-1} r on device pointers (symmetric: omega W^1/2 S W^1/2, used by PCG).
+void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s,
+                          bool symmetric = false);
 // sweeps of smooth(); history (device, may be null) gets sweeps+1 norms.
 void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                   double* history, cudaStream_t s);
+// Same sweeps with CUDA events around each kernel: ms_phase[3] = average ms of
+// residual, patch_solve, scatter_update.
+void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
+                   double* ms_phase, cudaStream_t s);
 
 // krylov.cpp
 void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, const pdb_gmres_options& o,

@@ -26,9 +26,9 @@ void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col
 void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s);
 
 // Per-patch gather + LU solve (column-major factors):
-//   sols[k*ps + i] = (B_f^{-1} r[patch_k])_i,  f = phi ? phi[k] : k.
+//   sols[k*ps + i] = (B_f^{-1} (r .* in_scale)[patch_k])_i,  f = phi ? phi[k] : k; in_scale may be null.
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
-                 const int32_t* phi, const double* r, double* sols, cudaStream_t s);
+                 const int32_t* phi, const double* r, const double* in_scale, double* sols, cudaStream_t s);
 // z[i] = (sum over (k,l) in inv(i), ascending k, of sols[k*ps+l]) * omega_w[i];
 // x_out (may be null): x_out[i] = z[i] + x_in[i] (the smooth() update, precond.cpp:99).
 void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,
@@ -41,6 +41,7 @@ void build_inverse_fill(int64_t np, int ps, const int32_t* patches, const int32_
 void sort_inverse_segments(int64_t n, const int32_t* inv_ptr, int32_t* inv, cudaStream_t s);
 void transpose_factors(int64_t nf, int ps, const double* lu_rm, double* lu_cm, cudaStream_t s);
 void scale_weights(int64_t n, double omega, const double* w, double* omega_w, cudaStream_t s);
+void sqrt_weights(int64_t n, double omega, const double* w, double* sw, double* omega_sw, cudaStream_t s);
 
 // ---- detect.cu : matrix-only cell-patch detection --------------------------
 void detect_candidates(int64_t n, const int64_t* rp, int64_t ps, uint8_t* cand, int32_t* any, cudaStream_t s);

@@ -79,7 +79,9 @@ __global__ void __launch_bounds__(kBlock) patch_solve_kernel(int64_t np, int ps,
                                                              const double* __restrict__ F,
                                                              const int32_t* __restrict__ piv,
                                                              const int32_t* __restrict__ phi,
-                                                             const double* __restrict__ r, double* __restrict__ sols) {
+                                                             const double* __restrict__ r,
+                                                             const double* __restrict__ in_scale,
+                                                             double* __restrict__ sols) {
   const int i = threadIdx.x % W;
   const int64_t k = (int64_t)blockIdx.x * (kBlock / W) + threadIdx.x / W;
   const bool live = k < np;
@@ -89,7 +91,11 @@ __global__ void __launch_bounds__(kBlock) patch_solve_kernel(int64_t np, int ps,
   const bool row = i < ps;
   // out[i] = rhs[piv[i]] with rhs = r gathered on the patch (precond.cpp:72-73, dense.cpp:83)
   double s = 0.0;
-  if (row) s = __ldg(r + __ldg(patches + kk * ps + __ldg(piv + f * ps + i)));
+  if (row) {
+    const int32_t g = __ldg(patches + kk * ps + __ldg(piv + f * ps + i));
+    s = __ldg(r + g);
+    if (in_scale) s *= __ldg(in_scale + g);
+  }
   // forward substitution, unit lower triangle, column j broadcast by shuffle
   for (int j = 0; j < ps - 1; ++j) {
     const double yj = __shfl_sync(0xffffffffu, s, j, W);
@@ -109,12 +115,15 @@ __global__ void __launch_bounds__(kBlock) patch_solve_kernel(int64_t np, int ps,
 __global__ void patch_solve_block_kernel(int64_t np, int ps, const int32_t* __restrict__ patches,
                                          const double* __restrict__ F, const int32_t* __restrict__ piv,
                                          const int32_t* __restrict__ phi, const double* __restrict__ r,
-                                         double* __restrict__ sols) {
+                                         const double* __restrict__ in_scale, double* __restrict__ sols) {
   extern __shared__ double y[];
   const int64_t k = blockIdx.x;
   const int64_t f = phi ? (int64_t)phi[k] : k;
   const double* Fk = F + f * (int64_t)ps * ps;
-  for (int i = threadIdx.x; i < ps; i += blockDim.x) y[i] = r[patches[k * ps + piv[f * ps + i]]];
+  for (int i = threadIdx.x; i < ps; i += blockDim.x) {
+    const int32_t g = patches[k * ps + piv[f * ps + i]];
+    y[i] = in_scale ? r[g] * in_scale[g] : r[g];
+  }
   __syncthreads();
   for (int j = 0; j < ps - 1; ++j) {
     const double yj = y[j];
@@ -188,6 +197,15 @@ __global__ void scale_weights_kernel(int64_t n, double omega, const double* __re
   if (i < n) ow[i] = omega * w[i];
 }
 
+__global__ void sqrt_weights_kernel(int64_t n, double omega, const double* __restrict__ w, double* __restrict__ sw,
+                                    double* __restrict__ osw) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double r = sqrt(w[i]);
+  sw[i] = r;
+  osw[i] = omega * r;
+}
+
 inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 }  // namespace
@@ -240,11 +258,11 @@ void finish_sum(const double* partials, int count, double* out, bool sqrt_result
 }
 
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* F, const int32_t* piv, const int32_t* phi,
-                 const double* r, double* sols, cudaStream_t s) {
+                 const double* r, const double* in_scale, double* sols, cudaStream_t s) {
   if (np <= 0) return;
   if (ps > 32) {
     const int threads = ps >= 128 ? 128 : 64;
-    patch_solve_block_kernel<<<(unsigned)np, threads, ps * sizeof(double), s>>>(np, ps, patches, F, piv, phi, r, sols);
+    patch_solve_block_kernel<<<(unsigned)np, threads, ps * sizeof(double), s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols);
     return;
   }
   int W = 1;
@@ -252,11 +270,11 @@ void patch_solve(int64_t np, int ps, const int32_t* patches, const double* F, co
   const unsigned blocks = grid_for(np, kBlock / W);
   switch (W) {
     case 1:
-    case 2: patch_solve_kernel<2><<<grid_for(np, kBlock / 2), kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, sols); break;
-    case 4: patch_solve_kernel<4><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, sols); break;
-    case 8: patch_solve_kernel<8><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, sols); break;
-    case 16: patch_solve_kernel<16><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, sols); break;
-    default: patch_solve_kernel<32><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, sols); break;
+    case 2: patch_solve_kernel<2><<<grid_for(np, kBlock / 2), kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
+    case 4: patch_solve_kernel<4><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
+    case 8: patch_solve_kernel<8><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
+    case 16: patch_solve_kernel<16><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
+    default: patch_solve_kernel<32><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
   }
 }
 
@@ -288,6 +306,10 @@ void transpose_factors(int64_t nf, int ps, const double* lu_rm, double* lu_cm, c
 
 void scale_weights(int64_t n, double omega, const double* w, double* omega_w, cudaStream_t s) {
   if (n > 0) scale_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, w, omega_w);
+}
+
+void sqrt_weights(int64_t n, double omega, const double* w, double* sw, double* omega_sw, cudaStream_t s) {
+  if (n > 0) sqrt_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, w, sw, omega_sw);
 }
 
 }  // namespace pdb::k

@@ -193,7 +193,7 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
   } else {
     rep.residual_history.push_back(1.0);
     auto precond = [&]() {
-      if (pc) ops.apply(r.get(), z.get());
+      if (pc) precond_apply_device(*pc, r.get(), z.get(), s, /*symmetric=*/true);
       else PDB_CUDA(cudaMemcpyAsync(z.get(), r.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     };
     precond();

@@ -82,6 +82,8 @@ struct pdb_precond_s {
   bool compressed = false;
   pdb::DevBuf<int32_t> patches;
   pdb::DevBuf<double> omega_w;
+  pdb::DevBuf<double> sqrt_w;    // W^{1/2} and omega W^{1/2}: the symmetric weighting PCG uses
+  pdb::DevBuf<double> omega_sw;
   pdb::DevBuf<double> factors;  // column-major per factor
   pdb::DevBuf<int32_t> piv;
   pdb::DevBuf<int32_t> phi;     // compressed mode only

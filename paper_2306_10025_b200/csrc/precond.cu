@@ -44,6 +44,9 @@ void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cud
                            cudaMemcpyDeviceToDevice, s));
   pc.omega_w.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
   k::scale_weights(ps.n, omega, ps.weights.get(), pc.omega_w.get(), s);
+  pc.sqrt_w.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
+  pc.omega_sw.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
+  k::sqrt_weights(ps.n, omega, ps.weights.get(), pc.sqrt_w.get(), pc.omega_sw.get(), s);
   build_inverse(pc, s);
 }
 
@@ -99,11 +102,12 @@ void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, doub
   sync(s);
 }
 
-void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s) {
+void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s, bool symmetric) {
   Scratch<double> sols(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)), s);
   k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
-                 pc.compressed ? pc.phi.get() : nullptr, r, sols.get(), s);
-  k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(), pc.omega_w.get(), nullptr, z, nullptr, s);
+                 pc.compressed ? pc.phi.get() : nullptr, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
+  k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(),
+                    symmetric ? pc.omega_sw.get() : pc.omega_w.get(), nullptr, z, nullptr, s);
   PDB_LAUNCH_CHECK();
 }
 
@@ -121,10 +125,43 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
     if (history) k::finish_sum(partials.get(), plan.blocks, history + sw, true, s);
     if (sw == sweeps) break;
     k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
-                   pc.compressed ? pc.phi.get() : nullptr, r.get(), sols.get(), s);
+                   pc.compressed ? pc.phi.get() : nullptr, r.get(), nullptr, sols.get(), s);
     k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(), pc.omega_w.get(), x, nullptr, x, s);
   }
   PDB_LAUNCH_CHECK();
+}
+
+void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
+                   double* ms_phase, cudaStream_t s) {
+  require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
+  const k::SpmvPlan plan = k::spmv_plan(a.n, a.nnz);
+  Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
+  Scratch<double> sols(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)), s);
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(4 * std::max<int64_t>(sweeps, 1)));
+  for (auto& e : ev) PDB_CUDA(cudaEventCreate(&e));
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    cudaEvent_t* e = ev.data() + 4 * sw;
+    PDB_CUDA(cudaEventRecord(e[0], s));
+    k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), nullptr, s);
+    PDB_CUDA(cudaEventRecord(e[1], s));
+    k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
+                   pc.compressed ? pc.phi.get() : nullptr, r.get(), nullptr, sols.get(), s);
+    PDB_CUDA(cudaEventRecord(e[2], s));
+    k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(), pc.omega_w.get(), x, nullptr, x, s);
+    PDB_CUDA(cudaEventRecord(e[3], s));
+  }
+  PDB_LAUNCH_CHECK();
+  sync(s);
+  ms_phase[0] = ms_phase[1] = ms_phase[2] = 0.0;
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    cudaEvent_t* e = ev.data() + 4 * sw;
+    for (int p = 0; p < 3; ++p) {
+      float ms = 0.f;
+      PDB_CUDA(cudaEventElapsedTime(&ms, e[p], e[p + 1]));
+      ms_phase[p] += ms / static_cast<double>(sweeps);
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 }  // namespace pdb

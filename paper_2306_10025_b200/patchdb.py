@@ -487,3 +487,21 @@ def pcg(m: Matrix, b, pc: Optional[Preconditioner] = None, tol: float = 1e-8, ma
     _check(_lib.pdb_pcg_solve(m.ptr, _dp(b), pc.ptr if pc is not None else None, tol, max_iters, _dp(x),
                               C.byref(rep)))
     return x, _report(rep)
+
+
+_sig("pdb_relax_profile", C.c_int, _P, _P, C.c_void_p, C.c_void_p, C.c_int64, _D, C.c_void_p)
+_sig("pdb_precond_stored_factors", C.c_int64, _P)
+_sig("pdb_precond_patch_count", C.c_int64, _P)
+_sig("pdb_precond_patch_size", C.c_int64, _P)
+
+
+def relax_profile(pc: Preconditioner, m: Matrix, d_b: int, d_x: int, sweeps: int, stream: int = 0):
+    """Average ms per sweep of (residual, patch_solve, scatter_update), timed with CUDA events."""
+    ms = np.zeros(3)
+    _check(_lib.pdb_relax_profile(m.ptr, pc.ptr, d_b, d_x, sweeps, _dp(ms), stream or None))
+    return ms
+
+
+def precond_sizes(pc: Preconditioner):
+    return (_lib.pdb_precond_stored_factors(pc.ptr), _lib.pdb_precond_patch_count(pc.ptr),
+            _lib.pdb_precond_patch_size(pc.ptr))

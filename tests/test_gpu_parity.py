@@ -1,0 +1,237 @@
+"""GPU-vs-oracle parity through the C-ABI (pytest -m gpu).
+
+The oracle (oracle/pdb_oracle.c) is itself pinned bit-for-bit to the
+compiled reference in tests/test_oracle_pins.py.  Bars (BASELINE.json
+north_star): patch lists, weights, extraction, LU factors, cluster ids and
+representatives bit-exact; residual histories within 1e-9 relative;
+Krylov iteration counts identical.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RTOL_HIST = 1e-9  # north_star: residual histories within 1e-9 relative
+
+
+class Case:
+    def __init__(self, P, orc, config, cells, ps):
+        self.prob = P.Problem.generate(config, cells)
+        self.csr = self.prob.csr()
+        self.b = self.prob.rhs()
+        self.A = self.prob.matrix()
+        self.ps_size = ps
+        self.ps = P.PatchSet.detect(self.A, ps)
+        self.patches, self.w = orc.detect(self.csr, ps)
+        self.mats = orc.extract_all(self.csr, self.patches)
+
+
+@pytest.fixture(scope="module")
+def c1(P, orc):
+    return Case(P, orc, 1, 0, 9)
+
+
+@pytest.fixture(scope="module")
+def c2s(P, orc):
+    return Case(P, orc, 2, 16, 25)
+
+
+@pytest.fixture(scope="module")
+def c3s(P, orc):
+    return Case(P, orc, 3, 6, 27)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_detect_and_extract_bit_exact(name, request, P):
+    c = request.getfixturevalue(name)
+    assert c.ps.count == len(c.patches)
+    assert np.array_equal(c.ps.patches(), c.patches)
+    assert np.array_equal(c.ps.weights(), c.w)
+    assert np.array_equal(c.ps.extract(c.A), c.mats)
+
+
+def test_spmv(c1, orc):
+    x = np.random.default_rng(1).uniform(-1, 1, c1.A.rows)
+    y = c1.A.spmv(x)
+    np.testing.assert_allclose(y, orc.spmv(c1.csr, x), rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_exact_database_lu_bit_exact(name, request, P, orc):
+    c = request.getfixturevalue(name)
+    db = P.Database.build(c.A, c.ps, P.EXACT)
+    lu, piv = db.factors()
+    for k in range(0, len(c.mats), max(1, len(c.mats) // 64)):
+        lo, po = orc.lu_factor(c.mats[k])
+        assert np.array_equal(lu[k], lo) and np.array_equal(piv[k], po), k
+    assert np.array_equal(db.phi(), np.arange(len(c.mats)))
+    assert np.array_equal(db.representatives(), c.mats)
+
+
+def _eps_for(orc, mats, lo, hi, spectral):
+    return orc.greedy_bisect(mats, lo, hi, spectral=spectral)["eps"]
+
+
+@pytest.mark.parametrize("spectral", [False, True])
+@pytest.mark.parametrize("best_match", [False, True])
+def test_greedy_bit_exact(c1, P, orc, spectral, best_match):
+    eps = _eps_for(orc, c1.mats, 46, 57, spectral)  # 5% of 1024 patches (config 1)
+    want = orc.greedy(c1.mats, eps, spectral=spectral, best_match=best_match)
+    db = P.Database.build(c1.A, c1.ps, P.GREEDY_SPECTRAL if spectral else P.GREEDY_L1, eps=eps,
+                          best_match=int(best_match))
+    assert db.size == want["m"]
+    assert np.array_equal(db.phi(), want["phi"])
+    assert np.array_equal(db.representatives(), want["reps"])
+    lu, piv = db.factors()
+    assert np.array_equal(lu, want["lu"]) and np.array_equal(piv, want["piv"])
+
+
+@pytest.mark.parametrize("spectral", [False, True])
+def test_greedy_bisect_bit_exact(c1, P, orc, spectral):
+    want = orc.greedy_bisect(c1.mats, 46, 57, spectral=spectral)
+    db, eps = P.Database.build_to_size(c1.A, c1.ps, 46, 57, P.GREEDY_SPECTRAL if spectral else P.GREEDY_L1)
+    assert eps == want["eps"]
+    assert db.size == want["m"]
+    assert np.array_equal(db.phi(), want["phi"])
+
+
+def test_greedy_l1_larger(c3s, P, orc):
+    want = orc.greedy_bisect(c3s.mats, 9, 13, spectral=False)
+    db = P.Database.build(c3s.A, c3s.ps, P.GREEDY_L1, eps=want["eps"])
+    assert np.array_equal(db.phi(), want["phi"])
+
+
+@pytest.mark.parametrize("method,variant", [(3, 0), (4, 1), (5, 2)])
+def test_kmeans_partitioned_bit_exact(c1, P, orc, method, variant):
+    want = orc.partitioned_build(c1.mats, 51, variant, seed=42, max_iters=50)
+    db = P.Database.build(c1.A, c1.ps, method, db_size=51, seed=42, max_iters=50)
+    assert db.size == want["m"]
+    assert np.array_equal(db.phi(), want["phi"])
+    assert np.array_equal(db.representatives(), want["reps"])
+    lu, piv = db.factors()
+    assert np.array_equal(lu, want["lu"]) and np.array_equal(piv, want["piv"])
+
+
+def test_kmeans_entrywise_c2(c2s, P, orc):
+    want = orc.partitioned_build(c2s.mats, 64, 0, seed=7, max_iters=30)
+    db = P.Database.build(c2s.A, c2s.ps, P.KMEANS_ENTRYWISE, db_size=64, seed=7, max_iters=30)
+    assert np.array_equal(db.phi(), want["phi"])
+    assert np.array_equal(db.representatives(), want["reps"])
+
+
+def test_bootstrap_bit_exact(P, orc):
+    prob = P.Problem.generate(1, 12)
+    csr = prob.csr()
+    A = prob.matrix()
+    ps = P.PatchSet.detect(A, 9)
+    patches, _ = orc.detect(csr, 9)
+    mats = orc.extract_all(csr, patches)
+    eps = orc.greedy_bisect(mats, 10, 14, spectral=True)["eps"]
+    want = orc.bootstrapped(mats, eps, 2, 20)
+    db = P.Database.build(A, ps, P.BOOTSTRAP, eps=eps, max_iters=20)
+    assert db.size == want["m"]
+    assert np.array_equal(db.phi(), want["phi"])
+
+
+def _oracle_pc(orc, c, db=None):
+    if db is None:
+        f = [orc.lu_factor(m) for m in c.mats]
+        return np.stack([a for a, _ in f]), np.stack([p for _, p in f]), None
+    lu, piv = db.factors()
+    return lu, piv, db.phi()
+
+
+@pytest.mark.parametrize("compressed", [False, True])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_precond_apply(name, compressed, request, P, orc):
+    c = request.getfixturevalue(name)
+    budget = 12 if c.ps_size in (9, 25) else 32  # >= 9 boundary partitions in 2D, 27 in 3D
+    db = P.Database.build(c.A, c.ps, P.KMEANS_ENTRYWISE, db_size=budget) if compressed else None
+    pc = P.Preconditioner.create(c.A, c.ps, db, omega=0.7)
+    r = np.random.default_rng(3).uniform(-1, 1, c.A.rows)
+    lu, piv, phi = _oracle_pc(orc, c, db)
+    want = orc.precond_apply(c.patches, c.w, 0.7, lu, piv, phi, r)
+    np.testing.assert_allclose(pc.apply(r), want, rtol=1e-11, atol=1e-13 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("compressed", [False, True])
+@pytest.mark.parametrize("name", ["c1", "c3s"])
+def test_relax_history(name, compressed, request, P, orc):
+    """Config 1: damped Richardson, 20 sweeps; history within 1e-9 relative."""
+    c = request.getfixturevalue(name)
+    omega = 0.8
+    if compressed:
+        eps = _eps_for(orc, c.mats, max(1, int(0.045 * len(c.mats))), max(2, int(0.055 * len(c.mats)) + 1), False)
+        db = P.Database.build(c.A, c.ps, P.GREEDY_L1, eps=eps)
+    else:
+        db = None
+    pc = P.Preconditioner.create(c.A, c.ps, db, omega=omega)
+    x, hist = pc.relax(c.A, c.b, np.zeros_like(c.b), 20)
+    lu, piv, phi = _oracle_pc(orc, c, db)
+    xo, ho = orc.relax(c.csr, c.patches, c.w, omega, lu, piv, phi, c.b, np.zeros_like(c.b), 20)
+    np.testing.assert_allclose(hist, ho, rtol=RTOL_HIST, atol=0)
+    np.testing.assert_allclose(x, xo, rtol=RTOL_HIST, atol=RTOL_HIST * np.abs(xo).max())
+
+
+def test_gmres_iterations(c1, P, orc):
+    pc = P.Preconditioner.create(c1.A, c1.ps, None, omega=1.0)
+    x, rep = P.gmres(c1.A, c1.b, pc)
+    lu, piv, _ = _oracle_pc(orc, c1)
+    xo, ro = orc.gmres(c1.csr, c1.b, dict(patches=c1.patches, weights=c1.w, omega=1.0, lu=lu, piv=piv, phi=None))
+    assert rep.iterations == ro["iterations"] and rep.restarts == ro["restarts"]
+    assert rep.converged == ro["converged"]
+    np.testing.assert_allclose(rep.residual_history, ro["residual_history"], rtol=1e-7)
+
+
+def test_pcg_iterations(c2s, P, orc):
+    db = P.Database.build(c2s.A, c2s.ps, P.KMEANS_ENTRYWISE, db_size=16)
+    pc = P.Preconditioner.create(c2s.A, c2s.ps, db, omega=1.0)
+    x, rep = P.pcg(c2s.A, c2s.b, pc, tol=1e-8)
+    lu, piv, phi = _oracle_pc(orc, c2s, db)
+    xo, ro = orc.pcg(c2s.csr, c2s.b, dict(patches=c2s.patches, weights=c2s.w, omega=1.0, lu=lu, piv=piv, phi=phi),
+                     tol=1e-8)
+    assert rep.converged and ro["converged"]
+    assert rep.iterations == ro["iterations"]
+    np.testing.assert_allclose(rep.residual_history, ro["residual_history"], rtol=1e-6)
+
+
+def test_singular_patch_error(c1, P, orc):
+    rp, ci, v = [a.copy() for a in c1.csr]
+    # zero one cell-interior row (its stored entries stay in the pattern)
+    k = 37
+    row = c1.patches[k][4]
+    v[rp[row]:rp[row + 1]] = 0.0
+    A = P.Matrix.from_csr(rp, ci, v)
+    ps = P.PatchSet.detect(A, 9)
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.build(A, ps, P.EXACT)
+    assert e.value.status == P.PDB_ERR_SINGULAR_MATRIX
+    mats = orc.extract_all((rp, ci, v), c1.patches)
+    with pytest.raises(Exception) as eo:
+        orc.lu_factor(mats[k])
+    assert e.value.message == f"patch {k}: " + eo.value.message
+    with pytest.raises(P.PatchdbError) as e2:
+        P.Preconditioner.create(A, ps, None)
+    assert e2.value.status == P.PDB_ERR_SINGULAR_MATRIX and e2.value.message == e.value.message
+
+
+def test_error_paths(c1, P):
+    with pytest.raises(P.PatchdbError) as e:
+        P.PatchSet.detect(c1.A, 7)
+    assert e.value.status == P.PDB_ERR_NO_PATCHES_FOUND
+    assert e.value.message == "no row has exactly 7 stored entries"
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.build(c1.A, c1.ps, P.KMEANS_ENTRYWISE, db_size=5)
+    assert e.value.status == P.PDB_ERR_BUDGET_TOO_SMALL
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.build(c1.A, c1.ps, P.GREEDY_L1, eps=0.0)
+    assert e.value.status == P.PDB_ERR_INVALID_ARGUMENT
+
+
+def test_identity_phi_compressed_equals_exact(c1, P):
+    """SPEC acceptance 3: Exact == Compressed when m_p = n_p with identity phi."""
+    db = P.Database.build(c1.A, c1.ps, P.EXACT)
+    pe = P.Preconditioner.create(c1.A, c1.ps, None)
+    pcmp = P.Preconditioner.create(c1.A, c1.ps, db)
+    r = np.random.default_rng(5).uniform(-1, 1, c1.A.rows)
+    assert np.array_equal(pe.apply(r), pcmp.apply(r))
