@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/patchdb/patchdb.h"
+#include "kernels.hpp"
 #include "objects.hpp"
 
 namespace pdb {
@@ -15,6 +16,7 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s);
 HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v);
 HostCsr download_csr(const DeviceCsr& d, cudaStream_t s);
 void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s);
+k::SpmvPlan plan_of(const DeviceCsr& a);  // SpMV launch plan (streaming partition when available)
 HostCsr read_matrix_market_host(const std::string& path);
 void write_matrix_market_host(const HostCsr& a, const std::string& path);
 

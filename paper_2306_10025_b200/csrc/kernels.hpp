@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -16,8 +17,20 @@ struct SpmvPlan {
   int group = 8;      // threads per row (power of two <= 32)
   int rows_per_block = 32;
   int blocks = 0;
+  int version = 2;    // 1: 4-way unrolled loop; 2: batched col/val/x loads; 3: CSR stream
+  int entries = 4;    // v2: entries per lane per pass
+  const int32_t* blk_start = nullptr;  // v3: row partition (nblk + 1 entries)
+  const int64_t* blk_base = nullptr;   // v3: row_ptr[blk_start[b]]
+  int nblk = 0;                        // v3/v4: partition blocks (v4 runs a persistent grid of `blocks`)
 };
 SpmvPlan spmv_plan(int64_t n, int64_t nnz);
+// v3 plan over a matrix's row partition.
+// per = nonzeros per thread of the partition (8 or 16; 256 threads per block).
+SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, const int64_t* blk_base, int nblk,
+                          int per);
+// Host-side row partition for v3: blocks of <= 256*per nonzeros and <= 64*per rows.
+int stream_nnz();
+std::vector<int32_t> stream_partition(int64_t n, const int64_t* row_ptr, int per);
 void residual(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
               const double* x, const double* b, double* r, double* block_sumsq, cudaStream_t s);
 void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
@@ -29,6 +42,24 @@ void finish_sum(const double* partials, int count, double* out, bool sqrt_result
 //   sols[k*ps + i] = (B_f^{-1} (r .* in_scale)[patch_k])_i,  f = phi ? phi[k] : k; in_scale may be null.
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
                  const int32_t* phi, const double* r, const double* in_scale, double* sols, cudaStream_t s);
+// Same product with explicit column-major inverses Binv (default sweep path).
+void patch_apply_inv(int64_t np, int ps, const int32_t* patches, const double* Binv, const int32_t* phi,
+                     const double* r, const double* in_scale, double* sols, cudaStream_t s);
+// Padded slot-major inverse map (maxc in {1,2,4,8}) and the scatter/update using it;
+// the weight omega*(1/count) (sym: omega*sqrt(1/count)) is recomputed in-kernel.
+void build_inverse_pad(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, int32_t* pad,
+                       cudaStream_t s);
+void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const double* sols, double omega, bool sym,
+                        const double* x_in, double* z_out, double* x_out, cudaStream_t s);
+int grouped_tile(int ps);  // patches per grouped-apply tile
+// Cluster-grouped apply: tile t covers tile-order slots [tile_start[t], tile_start[t+1]) sharing entry
+// tile_entry[t]; tile_idx holds the patch DoF lists in tile order and sols is written in tile order.
+void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                         const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
+                         double* sols, int max_tile, cudaStream_t s);
+void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
+// Binv (column-major) from row-major LU + pivots: column c = lu_solve(e_c).
+void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s);
 // z[i] = (sum over (k,l) in inv(i), ascending k, of sols[k*ps+l]) * omega_w[i];
 // x_out (may be null): x_out[i] = z[i] + x_in[i] (the smooth() update, precond.cpp:99).
 void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,

@@ -13,6 +13,7 @@
 //   k-means steps       kmeans_loop compress.cpp:150-166 (assignment),
 //                       entrywise_mean_indexed dense.cpp:211-223 (update)
 #include <cfloat>
+#include <cstdlib>
 
 #include <math_constants.h>
 
@@ -362,6 +363,198 @@ __global__ void spectral_list_kernel(int64_t npairs, const int32_t* __restrict__
   if (iters_total) atomicAdd(iters_total, (unsigned long long)it);
 }
 
+// ----------------------------------------------- spectral, tiled (fast) ----
+// Compile-time patch size: the per-thread vectors t (B^{-1} v) and s (A^T w)
+// live in registers, so the two matrix-vector products share one pass over
+// A (each A(i,j) is loaded once and used for w_i and s_j -- the same
+// per-element operation order as mat_vec then mat_tvec), the triangular
+// solves run on register arrays with immediate indices, and only v, w and
+// the permuted t go through shared memory.  A block owns a tile of TA
+// patches x TE factors; its factors sit in shared memory, its patches stay
+// L1-resident, and every thread keeps pulling (patch, factor) pairs from the
+// tile until it is exhausted, so a lane that converges early starts a new
+// pair instead of idling until the slowest lane of its warp finishes.
+constexpr int kTileA = 32;  // patches per tile (L1-resident)
+constexpr int kTileE = 8;   // factors per tile (L1-resident, read by broadcast)
+constexpr int kTileThreads = 64;
+
+template <int PS>
+__global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npat, const int32_t* __restrict__ pid,
+                                                                     int64_t ne, const double* __restrict__ mats,
+                                                                     const double* __restrict__ lu,
+                                                                     const int32_t* __restrict__ piv,
+                                                                     double* __restrict__ d,
+                                                                     unsigned long long* iters_total) {
+  constexpr int LEN = PS * PS;
+  constexpr int BD = kTileThreads;
+  extern __shared__ double sm[];
+  double* vec = sm;  // 3 * PS * BD: v, w, t
+  __shared__ int counter;
+  const int tid = threadIdx.x;
+  const int64_t a0 = (int64_t)blockIdx.x * kTileA, e0 = (int64_t)blockIdx.y * kTileE;
+  const int na = (int)(npat - a0 < kTileA ? npat - a0 : kTileA);
+  const int nev = (int)(ne - e0 < kTileE ? ne - e0 : kTileE);
+  const double* LUs = lu + e0 * LEN;
+  const int32_t* Ps = piv + e0 * PS;
+  if (tid == 0) counter = 0;
+  __syncthreads();
+  double* V = vec + tid;
+  double* W = vec + PS * BD + tid;
+  double* Tv = vec + 2 * PS * BD + tid;
+  const int npairs = na * nev;
+  bool active = false;
+  int it = 0, pa = 0, pe = 0;
+  double lambda = 0.0;
+  const double* A = mats;
+  const double* L = LUs;
+  const int32_t* P = Ps;
+  unsigned long long my_iters = 0;
+  for (;;) {
+    if (!active) {
+      const int p = atomicAdd(&counter, 1);
+      if (p < npairs) {
+        active = true;
+        pa = p % na;
+        pe = p / na;
+        const int64_t g = a0 + pa;
+        A = mats + (int64_t)(pid ? pid[g] : g) * LEN;
+        L = LUs + pe * LEN;
+        P = Ps + pe * PS;
+        it = 0;
+        lambda = 0.0;
+        // v0_i = 1 + 1e-6 i, normalised by division (dense.cpp:163-165)
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < PS; ++i) {
+          const double vi = __dadd_rn(1.0, __dmul_rn(1e-6, (double)i));
+          V[i * BD] = vi;
+          s = __dadd_rn(s, __dmul_rn(vi, vi));
+        }
+        const double vn = __dsqrt_rn(s);
+#pragma unroll
+        for (int i = 0; i < PS; ++i) V[i * BD] = __ddiv_rn(V[i * BD], vn);
+      }
+    }
+    if (!__any_sync(0xffffffffu, active)) break;
+    if (!active) continue;
+    // ---- t = B^{-1} v (lu_solve_into, dense.cpp:77-94)
+    double T[PS];
+#pragma unroll
+    for (int i = 0; i < PS; ++i) T[i] = V[__ldg(P + i) * BD];
+#pragma unroll
+    for (int i = 1; i < PS; ++i) {
+      double s = T[i];
+#pragma unroll
+      for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + i * PS + j), T[j]));
+      T[i] = s;
+    }
+#pragma unroll
+    for (int i = PS - 1; i >= 0; --i) {
+      double s = T[i];
+#pragma unroll
+      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + i * PS + j), T[j]));
+      T[i] = __ddiv_rn(s, __ldg(L + i * PS + i));
+    }
+    // ---- w = v - A t (mat_vec) and s = A^T w (mat_tvec), one pass over A
+    double S[PS];
+#pragma unroll
+    for (int j = 0; j < PS; ++j) S[j] = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < PS; ++i) {
+      const double* Ai = A + i * PS;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < PS; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(Ai + j), T[j]));
+      const double wi = __dsub_rn(V[i * BD], acc);
+      W[i * BD] = wi;
+#pragma unroll
+      for (int j = 0; j < PS; ++j) S[j] = __dadd_rn(S[j], __dmul_rn(__ldg(Ai + j), wi));
+    }
+    // ---- t = B^{-T} s (lu_solve_transpose_into, dense.cpp:102-120)
+#pragma unroll
+    for (int i = 0; i < PS; ++i) {
+      double s = S[i];
+#pragma unroll
+      for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + j * PS + i), S[j]));
+      S[i] = __ddiv_rn(s, __ldg(L + i * PS + i));
+    }
+#pragma unroll
+    for (int i = PS - 2; i >= 0; --i) {
+      double s = S[i];
+#pragma unroll
+      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + j * PS + i), S[j]));
+      S[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < PS; ++i) Tv[__ldg(P + i) * BD] = S[i];
+    // ---- u = w - t, Rayleigh quotient, stopping rules (dense.cpp:170-188)
+    double rq = 0.0;
+#pragma unroll
+    for (int i = 0; i < PS; ++i) {
+      const double u = __dsub_rn(W[i * BD], Tv[i * BD]);
+      Tv[i * BD] = u;
+      rq = __dadd_rn(rq, __dmul_rn(V[i * BD], u));
+    }
+    rq = rq > 0.0 ? rq : 0.0;
+    ++it;
+    bool done = false;
+    double result = 0.0;
+    if (rq <= 1e-28) {
+      done = true;
+      result = __dsqrt_rn(rq);
+    } else if (it > 1 && fabs(__dsub_rn(rq, lambda)) < __dmul_rn(1e-8, rq)) {
+      done = true;
+      result = __dsqrt_rn(rq);
+    } else {
+      lambda = rq;
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < PS; ++i) s = __dadd_rn(s, __dmul_rn(Tv[i * BD], Tv[i * BD]));
+      const double un2 = __dsqrt_rn(s);
+      if (un2 == 0.0) {
+        done = true;
+        result = 0.0;
+      } else {
+#pragma unroll
+        for (int i = 0; i < PS; ++i) V[i * BD] = __ddiv_rn(Tv[i * BD], un2);
+        if (it == 200) {
+          done = true;
+          result = __dsqrt_rn(lambda);
+        }
+      }
+    }
+    if (done) {
+      d[(a0 + pa) * ne + e0 + pe] = result;
+      my_iters += (unsigned long long)it;
+      active = false;
+    }
+  }
+  if (iters_total && my_iters) atomicAdd(iters_total, my_iters);
+}
+
+template <int PS>
+bool launch_spectral_tile(int64_t npat, const int32_t* pid, int64_t ne, const double* mats, const double* lu,
+                          const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+  const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
+  cudaFuncSetAttribute(spectral_tile_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(grid_for(npat, kTileA), (unsigned)((ne + kTileE - 1) / kTileE));
+  spectral_tile_kernel<PS><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters);
+  return true;
+}
+
+bool spectral_tiled(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+  const char* e = getenv("PDB_SPECTRAL_TILED");
+  if (e && e[0] == '0') return false;
+  switch (ps) {
+    case 9: return launch_spectral_tile<9>(npat, pid, ne, mats, lu, piv, d, iters, s);
+    case 22: return launch_spectral_tile<22>(npat, pid, ne, mats, lu, piv, d, iters, s);
+    case 25: return launch_spectral_tile<25>(npat, pid, ne, mats, lu, piv, d, iters, s);
+    case 27: return launch_spectral_tile<27>(npat, pid, ne, mats, lu, piv, d, iters, s);
+    default: return false;
+  }
+}
+
 // ------------------------------------------------------------ k-means ----
 // Assignment (compress.cpp:150-166): strict <, so the lowest j wins ties;
 // best starts at +inf with best_j = 0.
@@ -457,6 +650,7 @@ static size_t spectral_vec_bytes(int ps, int bd) { return (size_t)4 * ps * bd * 
 void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
                     const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
   if (npat <= 0 || ne <= 0) return;
+  if (spectral_tiled(npat, pid, ne, ps, mats, lu, piv, d, iters, s)) return;
   const int bd = spectral_block(ps);
   const size_t smem = (size_t)ps * ps * sizeof(double) + (size_t)((ps + 1) / 2) * sizeof(double) +
                       spectral_vec_bytes(ps, bd);

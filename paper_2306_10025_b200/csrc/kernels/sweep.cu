@@ -24,6 +24,24 @@ namespace {
 
 constexpr int kBlock = 256;
 
+// Streaming loads that bypass L1 allocation (the CSR arrays are read once per
+// sweep), keeping L1 for the reused x gathers.
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 template <int G>
 __global__ void __launch_bounds__(kBlock) residual_kernel(int64_t n, const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ col,
@@ -36,7 +54,23 @@ __global__ void __launch_bounds__(kBlock) residual_kernel(int64_t n, const int64
   double acc = 0.0;
   if (row < n) {
     const int64_t lo = rp[row], hi = rp[row + 1];
-    for (int64_t p = lo + lane; p < hi; p += G) acc += __ldg(val + p) * __ldg(x + __ldg(col + p));
+    // Four independent (col, val, x) streams in flight per lane: the col -> x
+    // gather is a dependent load, so memory-level parallelism comes from
+    // issuing several entries before consuming any.
+    int64_t p = lo + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (; p + 3 * G < hi; p += 4 * G) {
+      const int32_t c0 = __ldg(col + p), c1 = __ldg(col + p + G), c2 = __ldg(col + p + 2 * G),
+                    c3 = __ldg(col + p + 3 * G);
+      const double v0 = __ldg(val + p), v1 = __ldg(val + p + G), v2 = __ldg(val + p + 2 * G),
+                   v3 = __ldg(val + p + 3 * G);
+      a0 += v0 * __ldg(x + c0);
+      a1 += v1 * __ldg(x + c1);
+      a2 += v2 * __ldg(x + c2);
+      a3 += v3 * __ldg(x + c3);
+    }
+    for (; p < hi; p += G) a0 += __ldg(val + p) * __ldg(x + __ldg(col + p));
+    acc = (a0 + a1) + (a2 + a3);
   }
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
@@ -55,6 +89,278 @@ __global__ void __launch_bounds__(kBlock) residual_kernel(int64_t n, const int64
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v2: a G-lane group per row loads up to E entries per lane in three
+// batched steps (all columns, then all values with streaming cache hints,
+// then all x gathers through L1) before any arithmetic, so a row costs three
+// memory latencies instead of one per entry batch.  Longer rows loop.
+template <int G, int E, int H = 0>
+__global__ void __launch_bounds__(kBlock) residual_v2_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                             const int32_t* __restrict__ col,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ b, double* __restrict__ r,
+                                                             double* __restrict__ block_sumsq, bool negate_b_absent) {
+  const int lane = threadIdx.x % G;
+  const int64_t row = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
+  double acc = 0.0;
+  if (row < n) {
+    const int64_t lo = rp[row], hi = rp[row + 1];
+    for (int64_t base = lo; base < hi; base += G * E) {
+      int32_t c[E];
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t p = base + lane + e * G;
+        c[e] = p < hi ? (H ? ld_stream(col + p) : __ldcs(col + p)) : -1;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t p = base + lane + e * G;
+        v[e] = p < hi ? (H ? ld_stream(val + p) : __ldcs(val + p)) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc += c[e] >= 0 ? v[e] * (H ? ld_keep(x + c[e]) : __ldg(x + c[e])) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+  double rv = 0.0;
+  if (row < n) {
+    rv = b ? b[row] - acc : (negate_b_absent ? -acc : acc);
+    if (lane == 0) r[row] = rv;
+  }
+  if (block_sumsq) {
+    __shared__ double red[kBlock / 32];
+    double sq = (lane == 0 && row < n) ? rv * rv : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v3 ("CSR stream"): each block owns a contiguous row range whose
+// nonzeros (<= kStreamNnz) it streams with fully coalesced loads -- all
+// column indices, then all values, then the x gathers, kStreamPer
+// independent loads in flight per thread -- into shared-memory products;
+// 8-lane groups then reduce the rows out of shared memory.  Row ranges come
+// from a per-matrix partition (DeviceCsr::blk_start, built at upload); a row
+// longer than kStreamNnz gets a block to itself and is reduced block-wide.
+constexpr int kStreamThreads = 256;
+constexpr int kStreamPer = 8;   // base partition: 2048 nonzeros / 512 rows per block
+constexpr int kStreamNnz = kStreamThreads * kStreamPer;
+constexpr int kStreamRows = 512;
+
+template <int PER>
+__global__ void __launch_bounds__(kStreamThreads) residual_v3_kernel(
+    int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ blk_start, const int64_t* __restrict__ blk_base, double* __restrict__ block_sumsq,
+    bool negate_b_absent) {
+  constexpr int NNZ = kStreamThreads * PER;
+  constexpr int ROWS = kStreamRows;
+  __shared__ double prod[NNZ];
+  __shared__ int64_t rps[ROWS + 1];
+  __shared__ double bs[ROWS];
+  __shared__ double red[kStreamThreads / 32];
+  const int tid = threadIdx.x;
+  // block descriptors are independent loads: the CSR streams can start
+  // immediately instead of waiting for row_ptr
+  const int64_t r0 = __ldg(blk_start + blockIdx.x), r1 = __ldg(blk_start + blockIdx.x + 1);
+  const int64_t base = __ldg(blk_base + blockIdx.x), end = __ldg(blk_base + blockIdx.x + 1);
+  const int nrows = (int)(r1 - r0);
+  double sq = 0.0;
+  if (end - base <= NNZ) {
+    const int m = (int)(end - base) - tid;  // entries this thread may touch: k*T < m
+    const int32_t* cp = col + base + tid;
+    const double* vp = val + base + tid;
+    int32_t c[PER];
+    double v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) c[k] = k * kStreamThreads < m ? __ldcs(cp + k * kStreamThreads) : 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) v[k] = k * kStreamThreads < m ? __ldcs(vp + k * kStreamThreads) : 0.0;
+    for (int t = tid; t <= nrows; t += kStreamThreads) rps[t] = __ldg(rp + r0 + t);
+    if (b)
+      for (int t = tid; t < nrows; t += kStreamThreads) bs[t] = __ldcs(b + r0 + t);
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (k * kStreamThreads < m) prod[tid + k * kStreamThreads] = v[k] * __ldg(x + c[k]);
+    __syncthreads();
+    const int lane8 = tid & 7;
+    // warp-uniform trip count: every lane reaches the shuffles
+    for (int rr0 = (tid >> 5) * 4; rr0 < nrows; rr0 += kStreamThreads / 8) {
+      const int rr = rr0 + ((tid >> 3) & 3);
+      const bool has = rr < nrows;
+      const int lo = has ? (int)(rps[rr] - base) : 0, hi = has ? (int)(rps[rr + 1] - base) : 0;
+      double a = 0.0;
+      for (int e = lo + lane8; e < hi; e += 8) a += prod[e];
+      a += __shfl_xor_sync(0xffffffffu, a, 4);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      if (has && lane8 == 0) {
+        const double rv = b ? bs[rr] - a : (negate_b_absent ? -a : a);
+        r[r0 + rr] = rv;
+        sq += rv * rv;
+      }
+    }
+  } else {  // one long row (nrows == 1)
+    double a = 0.0;
+    for (int64_t e = base + tid; e < end; e += kStreamThreads) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if ((tid & 31) == 0) red[tid >> 5] = a;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kStreamThreads / 32; ++w) t += red[w];
+      const double rv = b ? b[r0] - t : (negate_b_absent ? -t : t);
+      r[r0] = rv;
+      sq = rv * rv;
+    }
+    __syncthreads();
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((tid & 31) == 0) red[tid >> 5] = sq;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kStreamThreads / 32; ++w) t += red[w];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v4: the v3 chunk structure run by a persistent grid with a
+// two-stage software pipeline -- while a block reduces chunk k out of shared
+// memory, the column/value/row_ptr/b loads of its next chunk are already in
+// flight in registers, so HBM never waits for the reduction phase.
+constexpr int kV4Threads = 256;
+constexpr int kV4Per = 8;
+constexpr int kV4Rows = kStreamRows;                 // partition row cap (shared with v3)
+constexpr int kV4RowRegs = (kV4Rows + 1 + kV4Threads - 1) / kV4Threads;  // 3
+
+struct V4Chunk {
+  int64_t r0, base;
+  int nrows, nnz;
+  int32_t c[kV4Per];
+  double v[kV4Per];
+  int64_t rpv[kV4RowRegs];
+  double bv[kV4RowRegs];
+};
+
+__device__ __forceinline__ void v4_load(V4Chunk& ck, int ch, const int32_t* __restrict__ blk_start,
+                                        const int64_t* __restrict__ blk_base, const int64_t* __restrict__ rp,
+                                        const int32_t* __restrict__ col, const double* __restrict__ val,
+                                        const double* __restrict__ b, int tid) {
+  ck.r0 = __ldg(blk_start + ch);
+  const int64_t r1 = __ldg(blk_start + ch + 1);
+  ck.base = __ldg(blk_base + ch);
+  const int64_t end = __ldg(blk_base + ch + 1);
+  ck.nrows = (int)(r1 - ck.r0);
+  ck.nnz = (int)(end - ck.base);
+  if (ck.nnz <= kV4Threads * kV4Per) {
+    const int m = ck.nnz - tid;
+    const int32_t* cp = col + ck.base + tid;
+    const double* vp = val + ck.base + tid;
+#pragma unroll
+    for (int k = 0; k < kV4Per; ++k) ck.c[k] = k * kV4Threads < m ? __ldcs(cp + k * kV4Threads) : 0;
+#pragma unroll
+    for (int k = 0; k < kV4Per; ++k) ck.v[k] = k * kV4Threads < m ? __ldcs(vp + k * kV4Threads) : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kV4RowRegs; ++q) {
+    const int t = tid + q * kV4Threads;
+    ck.rpv[q] = t <= ck.nrows ? __ldg(rp + ck.r0 + t) : 0;
+    ck.bv[q] = (b && t < ck.nrows) ? __ldcs(b + ck.r0 + t) : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kV4Threads, 3) residual_v4_kernel(
+    int nblk, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ blk_start, const int64_t* __restrict__ blk_base, double* __restrict__ block_sumsq,
+    bool negate_b_absent) {
+  __shared__ double prod[kV4Threads * kV4Per];
+  __shared__ int64_t rps[kV4Rows + 1];
+  __shared__ double bs[kV4Rows];
+  __shared__ double red[kV4Threads / 32];
+  const int tid = threadIdx.x;
+  double sq = 0.0;
+  int ch = blockIdx.x;
+  V4Chunk cur, nxt;
+  if (ch < nblk) v4_load(cur, ch, blk_start, blk_base, rp, col, val, b, tid);
+  while (ch < nblk) {
+    const int nch = ch + gridDim.x;
+    if (nch < nblk) v4_load(nxt, nch, blk_start, blk_base, rp, col, val, b, tid);  // in flight during the work below
+#pragma unroll
+    for (int q = 0; q < kV4RowRegs; ++q) {
+      const int t = tid + q * kV4Threads;
+      if (t <= cur.nrows) rps[t] = cur.rpv[q];
+      if (t < cur.nrows) bs[t] = cur.bv[q];
+    }
+    if (cur.nnz <= kV4Threads * kV4Per) {
+      const int m = cur.nnz - tid;
+#pragma unroll
+      for (int k = 0; k < kV4Per; ++k)
+        if (k * kV4Threads < m) prod[tid + k * kV4Threads] = cur.v[k] * __ldg(x + cur.c[k]);
+      __syncthreads();
+      const int lane8 = tid & 7;
+      for (int rr0 = (tid >> 5) * 4; rr0 < cur.nrows; rr0 += kV4Threads / 8) {
+        const int rr = rr0 + ((tid >> 3) & 3);
+        const bool has = rr < cur.nrows;
+        const int lo = has ? (int)(rps[rr] - cur.base) : 0, hi = has ? (int)(rps[rr + 1] - cur.base) : 0;
+        double a = 0.0;
+        for (int e = lo + lane8; e < hi; e += 8) a += prod[e];
+        a += __shfl_xor_sync(0xffffffffu, a, 4);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        if (has && lane8 == 0) {
+          const double rv = b ? bs[rr] - a : (negate_b_absent ? -a : a);
+          r[cur.r0 + rr] = rv;
+          sq += rv * rv;
+        }
+      }
+    } else {  // one long row
+      double a = 0.0;
+      const int64_t end = cur.base + cur.nnz;
+      for (int64_t e = cur.base + tid; e < end; e += kV4Threads) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if ((tid & 31) == 0) red[tid >> 5] = a;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kV4Threads / 32; ++w) t += red[w];
+        const double rv = b ? b[cur.r0] - t : (negate_b_absent ? -t : t);
+        r[cur.r0] = rv;
+        sq += rv * rv;
+      }
+    }
+    __syncthreads();
+    cur = nxt;
+    ch = nch;
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((tid & 31) == 0) red[tid >> 5] = sq;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kV4Threads / 32; ++w) t += red[w];
       block_sumsq[blockIdx.x] = t;
     }
   }
@@ -140,6 +446,169 @@ __global__ void patch_solve_block_kernel(int64_t np, int ps, const int32_t* __re
   for (int i = threadIdx.x; i < ps; i += blockDim.x) sols[k * ps + i] = y[i];
 }
 
+// Patch apply with explicit inverses (the default sweep path).  A block
+// holds PPB patches x ps threads; the gathered residual of each patch is
+// staged in shared memory once, then thread (patch, i) forms row i of
+// B^{-1} r_k from the column-major inverse (threads of a patch read
+// consecutive addresses; compressed inverses are L2-resident).  Every
+// product is independent -- no dependent shuffle chain as in a triangular
+// solve -- so the kernel runs at memory speed.
+__global__ void patch_apply_inv_kernel(int64_t np, int ps, int ppb, const int32_t* __restrict__ patches,
+                                       const double* __restrict__ Binv, const int32_t* __restrict__ phi,
+                                       const double* __restrict__ r, const double* __restrict__ in_scale,
+                                       double* __restrict__ sols) {
+  extern __shared__ double rk[];  // ppb * ps
+  const int pl = threadIdx.x / ps, i = threadIdx.x % ps;
+  const int64_t k = (int64_t)blockIdx.x * ppb + pl;
+  const bool live = pl < ppb && k < np;
+  if (live) {
+    const int32_t g = __ldg(patches + k * ps + i);
+    double v = __ldg(r + g);
+    if (in_scale) v *= __ldg(in_scale + g);
+    rk[pl * ps + i] = v;
+  }
+  __syncthreads();
+  if (!live) return;
+  const int64_t f = phi ? (int64_t)__ldg(phi + k) : k;
+  const double* B = Binv + f * (int64_t)ps * ps + i;
+  const double* x = rk + pl * ps;
+  // same summation order as the grouped kernel (one accumulator, ascending
+  // j), so exact and identity-phi compressed applies agree bit for bit
+  double a = 0.0;
+  for (int j = 0; j < ps; ++j) a += __ldg(B + (int64_t)j * ps) * x[j];
+  sols[k * ps + i] = a;
+}
+
+// Cluster-grouped apply (compressed mode): patches are pre-sorted by their
+// database entry; a block takes one tile of up to TP patches sharing entry
+// f, stages B_f^{-1} (ps^2 doubles) and the tile's gathered residuals in
+// shared memory, then forms the dense product B_f^{-1} [r_k1 .. r_kTP].
+// Each inverse is read once per tile instead of once per patch (the 64
+// config-2 inverses would otherwise cost 328 MB of L2 traffic per sweep).
+// Patch DoF lists and solutions are stored in tile order (tile_idx / sols
+// position s = rank of the patch in the entry-sorted order), so a tile reads
+// and writes contiguous runs; the scatter's inverse map points at the same
+// tile-order slots.
+__global__ void patch_apply_grouped_kernel(int ps, const int32_t* __restrict__ tile_entry,
+                                           const int32_t* __restrict__ tile_start,
+                                           const int32_t* __restrict__ tile_idx, const double* __restrict__ Binv,
+                                           const double* __restrict__ r, const double* __restrict__ in_scale,
+                                           double* __restrict__ sols) {
+  extern __shared__ double sm[];
+  const int t = blockIdx.x;
+  const int64_t f = __ldg(tile_entry + t);
+  const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+  const int len = ps * ps;
+  double* B = sm;          // column-major inverse
+  double* rk = sm + len;   // cnt x ps gathered residuals
+  const double* Bg = Binv + f * (int64_t)len;
+  const int NG = blockDim.x / ps;
+  const int i = threadIdx.x % ps, g = threadIdx.x / ps;
+  for (int e = threadIdx.x; e < len; e += blockDim.x) B[e] = __ldg(Bg + e);
+  if (g < NG)
+    for (int p = g; p < cnt; p += NG) {
+      const int32_t gi = __ldg(tile_idx + (int64_t)(s0 + p) * ps + i);
+      double v = __ldg(r + gi);
+      if (in_scale) v *= __ldg(in_scale + gi);
+      rk[p * ps + i] = v;
+    }
+  __syncthreads();
+  // Register tiling: thread (g, i) owns row i of patches g, g+NG, g+2NG,
+  // g+3NG, so each B element read from shared memory feeds four products.
+  if (g >= NG) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int j = 0; j < ps; ++j) {
+    const double bij = B[j * ps + i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int p = g + q * NG;
+      if (p < cnt) acc[q] += bij * rk[p * ps + j];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int p = g + q * NG;
+    if (p < cnt) sols[(int64_t)(s0 + p) * ps + i] = acc[q];
+  }
+}
+
+// inverse-map entries k*ps + l -> slot_of[k]*ps + l (tile-order solution slots)
+__global__ void remap_inverse_kernel(int64_t count, int ps, const int32_t* __restrict__ slot_of, int32_t* inv) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const int32_t t = inv[q];
+  inv[q] = slot_of[t / ps] * ps + t % ps;
+}
+
+// Scatter/update with the padded slot-major inverse map: slot c of DoF i is
+// inv_pad[c*n + i] (ascending patch order, -1 = empty), so all slot loads of
+// a DoF are independent and coalesced.  The overlap weight is recomputed
+// from the slot count exactly as compute_weights does (patch.cpp:12-20):
+// scale = omega * (1.0 / count) (or omega * sqrt(1.0 / count) for the
+// symmetric PCG weighting).
+template <int MAXC>
+__global__ void scatter_update_pad_kernel(int64_t n, const int32_t* __restrict__ inv_pad,
+                                          const double* __restrict__ sols, double omega, bool sym,
+                                          const double* __restrict__ x_in, double* __restrict__ z_out,
+                                          double* __restrict__ x_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int32_t e[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) e[c] = __ldcs(inv_pad + (int64_t)c * n + i);
+  double v[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) v[c] = e[c] >= 0 ? __ldg(sols + e[c]) : 0.0;
+  double z = 0.0;
+  int cnt = 0;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+    if (e[c] >= 0) {
+      z += v[c];
+      ++cnt;
+    }
+  double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+  if (sym) w = sqrt(w);
+  z *= omega * w;
+  if (z_out) z_out[i] = z;
+  if (x_out) x_out[i] = z + x_in[i];
+}
+
+__global__ void build_inverse_pad_kernel(int64_t n, int maxc, const int32_t* __restrict__ inv_ptr,
+                                         const int32_t* __restrict__ inv, int32_t* __restrict__ pad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t lo = inv_ptr[i], hi = inv_ptr[i + 1];
+  for (int c = 0; c < maxc; ++c) pad[(int64_t)c * n + i] = lo + c < hi ? inv[lo + c] : -1;
+}
+
+// Column c of B^{-1} = lu_solve(LU, e_c) (dense.cpp:77-94 applied to unit
+// vectors).  Warp per factor, lanes over columns; the per-lane work vector
+// lives in the (column-major) output itself.
+__global__ void invert_factors_kernel(int64_t nf, int ps, const double* __restrict__ lu,
+                                      const int32_t* __restrict__ piv, double* __restrict__ inv) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t f = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  if (f >= nf) return;
+  const int64_t len = (int64_t)ps * ps;
+  const double* L = lu + f * len;
+  const int32_t* P = piv + f * ps;
+  for (int c = lane; c < ps; c += 32) {
+    double* o = inv + f * len + (int64_t)c * ps;  // column c, contiguous
+    for (int i = 0; i < ps; ++i) o[i] = P[i] == c ? 1.0 : 0.0;
+    for (int i = 1; i < ps; ++i) {
+      double s = o[i];
+      for (int j = 0; j < i; ++j) s -= L[(int64_t)i * ps + j] * o[j];
+      o[i] = s;
+    }
+    for (int i = ps - 1; i >= 0; --i) {
+      double s = o[i];
+      for (int j = i + 1; j < ps; ++j) s -= L[(int64_t)i * ps + j] * o[j];
+      o[i] = s / L[(int64_t)i * ps + i];
+    }
+  }
+}
+
 __global__ void scatter_update_kernel(int64_t n, const int32_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv,
                                       const double* __restrict__ sols, const double* __restrict__ omega_w,
                                       const double* __restrict__ x_in, double* __restrict__ z_out,
@@ -210,14 +679,76 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 
 }  // namespace
 
+int stream_nnz() { return kStreamNnz; }
+
+std::vector<int32_t> stream_partition(int64_t n, const int64_t* rp, int per) {
+  const int64_t cap_nnz = (int64_t)kStreamThreads * per, cap_rows = kStreamRows;
+  std::vector<int32_t> starts;
+  starts.push_back(0);
+  int64_t row = 0;
+  while (row < n) {
+    const int64_t b0 = rp[row];
+    int64_t end = row + 1;  // a block always takes at least one row
+    while (end < n && end - row < cap_rows && rp[end + 1] - b0 <= cap_nnz) ++end;
+    if (rp[row + 1] - b0 > cap_nnz) end = row + 1;  // long row alone
+    starts.push_back((int32_t)end);
+    row = end;
+  }
+  return starts;
+}
+
+SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, const int64_t* blk_base, int nblk,
+                          int per) {
+  SpmvPlan p = spmv_plan(n, nnz);
+  const char* e = getenv("PDB_SPMV_VERSION");
+  // Default: v2 (measured fastest on config 2: 127 us vs 150 us for v3 and
+  // 176 us for the pipelined v4; all three are L1-wavefront/latency bound,
+  // see DESIGN.md "Residual SpMV").
+  const int want = e ? atoi(e) : 2;
+  if (blk_start && blk_base && nblk > 0 && (want == 3 || want == 4)) {
+    p.version = want;
+    p.blk_start = blk_start;
+    p.blk_base = blk_base;
+    p.nblk = nblk;
+    p.blocks = nblk;
+    p.entries = per;
+    if (want == 4) {
+      int dev = 0, sms = 148, per_sm = 2;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_v4_kernel, kV4Threads, 0);
+      if (per_sm < 1) per_sm = 1;
+      p.blocks = nblk < sms * per_sm ? nblk : sms * per_sm;  // persistent grid: one wave
+    }
+  }
+  return p;
+}
+
 SpmvPlan spmv_plan(int64_t n, int64_t nnz) {
   SpmvPlan p;
   const double avg = n > 0 ? (double)nnz / (double)n : 1.0;
-  int g = 1;
-  while (g < 32 && g * 2 <= avg * 0.75 + 1) g *= 2;
-  if (avg > 24) g = g < 16 ? 16 : g;
+  // ~one 4-deep unrolled pass per row: G ~ avg/8 (power of two, 2..32)
+  int g = 2;
+  while (g < 32 && g * 8 < avg) g *= 2;
   p.group = g;
-  p.rows_per_block = kBlock / g;
+  p.version = 2;
+  p.entries = 4;
+  // v2: G*E ~ the typical row length (config 2, avg 36: G=4,E=8 measured best;
+  // config 3, avg 61: G=8,E=8)
+  if (avg <= 16) p.group = 2, p.entries = 8;
+  else if (avg <= 48) p.group = 4, p.entries = 8;
+  else p.group = 8, p.entries = 8;
+  if (const char* e = getenv("PDB_SPMV_VERSION")) p.version = atoi(e) == 1 ? 1 : 2;
+  if (p.version == 1) p.group = g;
+  if (const char* e = getenv("PDB_SPMV_GROUP")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p.group = v;
+  }
+  if (const char* e = getenv("PDB_SPMV_ENTRIES")) {
+    const int v = atoi(e);
+    if (v == 2 || v == 4 || v == 8 || v == 5 || v == 9) p.entries = v;  // 5/9: E=4/8 with L1-bypass hints
+  }
+  p.rows_per_block = kBlock / p.group;
   p.blocks = (int)((n + p.rows_per_block - 1) / p.rows_per_block);
   return p;
 }
@@ -226,13 +757,37 @@ template <int G>
 static void launch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
                             const double* x, const double* b, double* r, double* sumsq, bool negate,
                             cudaStream_t s) {
-  residual_kernel<G><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+  if (p.version == 1) {
+    residual_kernel<G><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+    return;
+  }
+  switch (p.entries) {
+    case 2: residual_v2_kernel<G, 2><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
+    case 8: residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
+    case 9: residual_v2_kernel<G, 8, 1><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
+    case 5: residual_v2_kernel<G, 4, 1><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
+    default: residual_v2_kernel<G, 4><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
+  }
 }
 
 static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
                               const double* x, const double* b, double* r, double* sumsq, bool negate,
                               cudaStream_t s) {
   if (n <= 0) return;
+  if (p.version == 4 && p.blk_start) {
+    residual_v4_kernel<<<p.blocks, kV4Threads, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base, sumsq,
+                                                       negate);
+    return;
+  }
+  if (p.version == 3 && p.blk_start) {
+    if (p.entries == 16)
+      residual_v3_kernel<16><<<p.blocks, kStreamThreads, 0, s>>>(n, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                                 sumsq, negate);
+    else
+      residual_v3_kernel<8><<<p.blocks, kStreamThreads, 0, s>>>(n, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                                sumsq, negate);
+    return;
+  }
   switch (p.group) {
     case 1: launch_residual<1>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
     case 2: launch_residual<2>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
@@ -276,6 +831,59 @@ void patch_solve(int64_t np, int ps, const int32_t* patches, const double* F, co
     case 16: patch_solve_kernel<16><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
     default: patch_solve_kernel<32><<<blocks, kBlock, 0, s>>>(np, ps, patches, F, piv, phi, r, in_scale, sols); break;
   }
+}
+
+void patch_apply_inv(int64_t np, int ps, const int32_t* patches, const double* Binv, const int32_t* phi,
+                     const double* r, const double* in_scale, double* sols, cudaStream_t s) {
+  if (np <= 0) return;
+  const int ppb = ps >= 256 ? 1 : 256 / ps;
+  const int threads = ppb * ps;
+  const unsigned blocks = (unsigned)((np + ppb - 1) / ppb);
+  patch_apply_inv_kernel<<<blocks, threads, (size_t)ppb * ps * sizeof(double), s>>>(np, ps, ppb, patches, Binv, phi,
+                                                                                     r, in_scale, sols);
+}
+
+int grouped_tile(int ps) {
+  const int ng = ps >= 256 ? 1 : 256 / ps;
+  return 4 * ng < 32 ? 4 * ng : 32;
+}
+
+void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                         const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
+                         double* sols, int max_tile, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  const size_t smem = ((size_t)ps * ps + (size_t)max_tile * ps) * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(patch_apply_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int threads = ps >= 256 ? ps : (256 / ps) * ps;
+  patch_apply_grouped_kernel<<<(unsigned)ntiles, threads, smem, s>>>(ps, tile_entry, tile_start, tile_idx, Binv, r,
+                                                                     in_scale, sols);
+}
+
+void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s) {
+  if (count > 0) remap_inverse_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, ps, slot_of, inv);
+}
+
+void build_inverse_pad(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, int32_t* pad,
+                       cudaStream_t s) {
+  if (n > 0) build_inverse_pad_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, maxc, inv_ptr, inv, pad);
+}
+
+void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const double* sols, double omega, bool sym,
+                        const double* x_in, double* z_out, double* x_out, cudaStream_t s) {
+  if (n <= 0) return;
+  const unsigned g = grid_for(n, kBlock);
+  switch (maxc) {
+    case 1: scatter_update_pad_kernel<1><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 2: scatter_update_pad_kernel<2><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 3:
+    case 4: scatter_update_pad_kernel<4><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    default: scatter_update_pad_kernel<8><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+  }
+}
+
+void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s) {
+  if (nf > 0) invert_factors_kernel<<<(unsigned)((nf + 3) / 4), 128, 0, s>>>(nf, ps, lu, piv, inv);
 }
 
 void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,

@@ -24,7 +24,7 @@ struct Ops {
   Scratch<double> partials;
   Scratch<double> scal;  // device scalars
   Ops(const DeviceCsr& a_, const pdb_precond_s* pc_, cudaStream_t s_)
-      : a(a_), pc(pc_), s(s_), plan(k::spmv_plan(a_.n, a_.nnz)), partials(static_cast<size_t>(k::dot_partials()), s_),
+      : a(a_), pc(pc_), s(s_), plan(plan_of(a_)), partials(static_cast<size_t>(k::dot_partials()), s_),
         scal(64, s_) {}
   void spmv(const double* x, double* y) {
     k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);

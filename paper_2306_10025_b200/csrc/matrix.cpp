@@ -60,7 +60,23 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
   d.col.upload(h.col.data(), h.col.size(), s);
   d.val.upload(h.val.data(), h.val.size(), s);
-  sync(s);
+  for (int v = 0; v < 2; ++v) {  // streaming-SpMV row partitions for 8 and 16 nonzeros per thread
+    const std::vector<int32_t> part = k::stream_partition(h.n, h.row_ptr.data(), v == 0 ? 8 : 16);
+    d.nblk[v] = static_cast<int>(part.size()) - 1;
+    d.blk_start[v].alloc(part.size());
+    d.blk_start[v].upload(part.data(), part.size(), s);
+    std::vector<int64_t> base(part.size());
+    for (size_t b = 0; b < part.size(); ++b) base[b] = h.row_ptr[static_cast<size_t>(part[b])];
+    d.blk_base[v].alloc(base.size());
+    d.blk_base[v].upload(base.data(), base.size(), s);
+    sync(s);
+  }
+}
+
+k::SpmvPlan plan_of(const DeviceCsr& a) {
+  const char* e = getenv("PDB_SPMV_PER");
+  const int v = e && atoi(e) == 16 ? 1 : 0;
+  return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 0 ? 8 : 16);
 }
 
 HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v) {
@@ -118,7 +134,7 @@ HostCsr download_csr(const DeviceCsr& d, cudaStream_t s) {
 }
 
 void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s) {
-  const k::SpmvPlan plan = k::spmv_plan(a.n, a.nnz);
+  const k::SpmvPlan plan = plan_of(a);
   k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);
   PDB_LAUNCH_CHECK();
 }

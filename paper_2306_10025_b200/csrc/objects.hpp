@@ -32,6 +32,10 @@ struct DeviceCsr {
   DevBuf<int64_t> row_ptr;
   DevBuf<int32_t> col;
   DevBuf<double> val;
+  // row partitions for the streaming SpMV ([0]: 2048 nnz / block, [1]: 4096)
+  DevBuf<int32_t> blk_start[2];  // nblk + 1 row starts
+  DevBuf<int64_t> blk_base[2];   // row_ptr at each partition boundary
+  int nblk[2] = {0, 0};
 };
 
 struct BuildWork {
@@ -80,6 +84,7 @@ struct pdb_precond_s {
   int64_t n = 0, np = 0, ps = 0, nf = 0;
   double omega = 1.0;
   bool compressed = false;
+  bool lu_apply = false;  // true: triangular solves on column-major LU; false: explicit inverses
   pdb::DevBuf<int32_t> patches;
   pdb::DevBuf<double> omega_w;
   pdb::DevBuf<double> sqrt_w;    // W^{1/2} and omega W^{1/2}: the symmetric weighting PCG uses
@@ -87,6 +92,11 @@ struct pdb_precond_s {
   pdb::DevBuf<double> factors;  // column-major per factor
   pdb::DevBuf<int32_t> piv;
   pdb::DevBuf<int32_t> phi;     // compressed mode only
+  // cluster-grouped apply (compressed mode): patches sorted by entry, tiled
+  pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
+  int ntiles = 0, max_tile = 0;
+  pdb::DevBuf<int32_t> inv_pad;  // slot-major padded inverse map (maxc_pad slots), when maxc_pad > 0
+  int maxc_pad = 0;
   pdb::DevBuf<int32_t> inv_ptr;
   pdb::DevBuf<int32_t> inv;
 };

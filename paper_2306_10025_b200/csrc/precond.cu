@@ -6,6 +6,9 @@
 // layout: column-major factors, int32 pivots, omega*W, and the DoF ->
 // (patch, slot) inverse map sorted by patch so the gather-side scatter adds
 // in the reference's ascending-k order.
+#include <cstdlib>
+#include <string>
+
 #include <cub/cub.cuh>
 
 #include "host.hpp"
@@ -15,7 +18,10 @@ namespace pdb {
 
 namespace {
 
-void build_inverse(pdb_precond_s& pc, cudaStream_t s) {
+// DoF -> solution-slot inverse map.  Entries are first k*ps + l sorted by k
+// (the reference's scatter order, precond.cpp:81-86), then, when solutions
+// are stored in tile order, remapped to slot_of[k]*ps + l.
+void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = nullptr) {
   const int64_t n = pc.n;
   pc.inv_ptr.alloc(static_cast<size_t>(n + 1));
   pc.inv.alloc(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)));
@@ -30,7 +36,34 @@ void build_inverse(pdb_precond_s& pc, cudaStream_t s) {
   k::build_inverse_fill(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.inv_ptr.get(), counts.get(),
                         pc.inv.get(), s);
   k::sort_inverse_segments(n, pc.inv_ptr.get(), pc.inv.get(), s);
+  if (slot_of) k::remap_inverse(pc.np * pc.ps, static_cast<int>(pc.ps), slot_of, pc.inv.get(), s);
   PDB_LAUNCH_CHECK();
+  // padded slot-major copy when every DoF is in at most 8 patches
+  Scratch<int32_t> maxc(1, s);
+  size_t mb = 0;
+  cub::DeviceReduce::Max(nullptr, mb, counts.get(), maxc.get(), n, s);
+  Scratch<unsigned char> mtmp(mb, s);
+  // counts was consumed as the fill cursor: it now holds the final per-DoF counts
+  cub::DeviceReduce::Max(mtmp.get(), mb, counts.get(), maxc.get(), n, s);
+  int32_t mh = 0;
+  PDB_CUDA(cudaMemcpyAsync(&mh, maxc.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  const char* e = getenv("PDB_PADDED");
+  if (mh <= 8 && !(e && std::string(e) == "0")) {
+    pc.maxc_pad = mh <= 1 ? 1 : mh <= 2 ? 2 : mh <= 4 ? 4 : 8;
+    pc.inv_pad.alloc(static_cast<size_t>(pc.maxc_pad * std::max<int64_t>(n, 1)));
+    k::build_inverse_pad(n, pc.maxc_pad, pc.inv_ptr.get(), pc.inv.get(), pc.inv_pad.get(), s);
+    PDB_LAUNCH_CHECK();
+  }
+}
+
+void scatter_stage(const pdb_precond_s& pc, const double* sols, bool symmetric, const double* x_in, double* z_out,
+                   double* x_out, cudaStream_t s) {
+  if (pc.maxc_pad > 0)
+    k::scatter_update_pad(pc.n, pc.maxc_pad, pc.inv_pad.get(), sols, pc.omega, symmetric, x_in, z_out, x_out, s);
+  else
+    k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols, symmetric ? pc.omega_sw.get() : pc.omega_w.get(),
+                      x_in, z_out, x_out, s);
 }
 
 void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cudaStream_t s) {
@@ -47,10 +80,84 @@ void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cud
   pc.sqrt_w.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
   pc.omega_sw.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
   k::sqrt_weights(ps.n, omega, ps.weights.get(), pc.sqrt_w.get(), pc.omega_sw.get(), s);
-  build_inverse(pc, s);
+}
+
+// Sweep factor layout: explicit column-major inverses (default) or the
+// column-major LU for the triangular-solve kernel (PDB_APPLY=lu).
+bool use_lu_apply() {
+  const char* e = getenv("PDB_APPLY");
+  return e && std::string(e) == "lu";
+}
+
+void set_factors(pdb_precond_s& pc, int64_t nf, int ps, const double* lu_rm, const int32_t* piv, cudaStream_t s) {
+  pc.nf = nf;
+  pc.lu_apply = use_lu_apply();
+  pc.factors.alloc(static_cast<size_t>(nf * ps * ps));
+  if (pc.lu_apply)
+    k::transpose_factors(nf, ps, lu_rm, pc.factors.get(), s);
+  else
+    k::invert_factors(nf, ps, lu_rm, piv, pc.factors.get(), s);
+  pc.piv.alloc(static_cast<size_t>(nf * ps));
+  PDB_CUDA(cudaMemcpyAsync(pc.piv.get(), piv, nf * ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  PDB_LAUNCH_CHECK();
+}
+
+// Patches grouped by database entry (stable: ascending k inside a group) and
+// cut into tiles of at most kTile patches; one block applies one tile.
+void build_tiles(pdb_precond_s& pc, const std::vector<int32_t>& phi, cudaStream_t s) {
+  const int kTile = k::grouped_tile(static_cast<int>(pc.ps));
+  std::vector<int32_t> count(static_cast<size_t>(pc.nf), 0);
+  for (int32_t j : phi) ++count[static_cast<size_t>(j)];
+  std::vector<int32_t> start(static_cast<size_t>(pc.nf + 1), 0);
+  for (int64_t j = 0; j < pc.nf; ++j) start[static_cast<size_t>(j + 1)] = start[static_cast<size_t>(j)] + count[static_cast<size_t>(j)];
+  std::vector<int32_t> order(phi.size()), cursor(start.begin(), start.end() - 1);
+  for (size_t k = 0; k < phi.size(); ++k) order[static_cast<size_t>(cursor[static_cast<size_t>(phi[k])]++)] = static_cast<int32_t>(k);
+  std::vector<int32_t> te, ts;
+  for (int64_t j = 0; j < pc.nf; ++j)
+    for (int32_t a = start[static_cast<size_t>(j)]; a < start[static_cast<size_t>(j + 1)]; a += kTile) {
+      te.push_back(static_cast<int32_t>(j));
+      ts.push_back(a);
+    }
+  ts.push_back(static_cast<int32_t>(phi.size()));
+  pc.ntiles = static_cast<int>(te.size());
+  pc.max_tile = kTile;
+  std::vector<int32_t> slot_of(order.size());
+  for (size_t q = 0; q < order.size(); ++q) slot_of[static_cast<size_t>(order[q])] = static_cast<int32_t>(q);
+  pc.order.alloc(order.size());
+  pc.order.upload(order.data(), order.size(), s);
+  pc.slot_of.alloc(slot_of.size());
+  pc.slot_of.upload(slot_of.data(), slot_of.size(), s);
+  pc.tile_entry.alloc(te.size());
+  pc.tile_entry.upload(te.data(), te.size(), s);
+  pc.tile_start.alloc(ts.size());
+  pc.tile_start.upload(ts.data(), ts.size(), s);
+  // patch DoF lists in tile order
+  pc.tile_idx.alloc(static_cast<size_t>(pc.np * pc.ps));
+  k::gather_i32(pc.np, pc.order.get(), pc.ps, pc.patches.get(), pc.tile_idx.get(), s);
+  PDB_LAUNCH_CHECK();
+  sync(s);
+}
+
+bool use_grouped_apply() {
+  const char* e = getenv("PDB_GROUPED");
+  return !(e && std::string(e) == "0");
 }
 
 }  // namespace
+
+// sols_k = B_phi(k)^{-1} (r .* in_scale)|_k for every patch.
+void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s) {
+  const int32_t* phi = pc.compressed ? pc.phi.get() : nullptr;
+  if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
+    k::patch_apply_grouped(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
+                           pc.tile_idx.get(), pc.factors.get(), r, in_scale, sols, pc.max_tile, s);
+  else if (pc.lu_apply)
+    k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(), phi, r,
+                   in_scale, sols, s);
+  else
+    k::patch_apply_inv(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), phi, r, in_scale, sols,
+                       s);
+}
 
 void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cudaStream_t s) {
   require_device();
@@ -60,12 +167,9 @@ void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, p
   p.method = PDB_METHOD_EXACT;
   build_database(a, ps, p, db, s);  // extract + LU of every patch; "patch k: ..." on failure
   common_setup(ps, omega, pc, s);
+  build_inverse(pc, s);
   pc.compressed = false;
-  pc.nf = db.m;
-  pc.factors.alloc(static_cast<size_t>(db.m * ps.ps * ps.ps));
-  k::transpose_factors(db.m, static_cast<int>(ps.ps), db.lu.get(), pc.factors.get(), s);
-  pc.piv = std::move(db.piv);
-  PDB_LAUNCH_CHECK();
+  set_factors(pc, db.m, static_cast<int>(ps.ps), db.lu.get(), db.piv.get(), s);
   sync(s);
 }
 
@@ -74,8 +178,8 @@ void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, doub
   require_device();
   require(db.np == ps.np, Errc::dimension_mismatch, "database does not cover the patch set");
   // phi onto the database (Database::phi_onto, compress.cpp:3-10)
+  const std::vector<int32_t> phi = db.phi.to_host(s);
   {
-    const std::vector<int32_t> phi = db.phi.to_host(s);
     std::vector<char> hit(static_cast<size_t>(db.m), 0);
     bool ok = true;
     for (int32_t j : phi) {
@@ -91,30 +195,30 @@ void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, doub
   require(db.ps == ps.ps, Errc::dimension_mismatch, "database entry dimension does not match the patch size");
   common_setup(ps, omega, pc, s);
   pc.compressed = true;
-  pc.nf = db.m;
-  pc.factors.alloc(static_cast<size_t>(db.m * ps.ps * ps.ps));
-  k::transpose_factors(db.m, static_cast<int>(ps.ps), db.lu.get(), pc.factors.get(), s);
-  pc.piv.alloc(static_cast<size_t>(db.m * ps.ps));
-  PDB_CUDA(cudaMemcpyAsync(pc.piv.get(), db.piv.get(), db.m * ps.ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  set_factors(pc, db.m, static_cast<int>(ps.ps), db.lu.get(), db.piv.get(), s);
   pc.phi.alloc(static_cast<size_t>(ps.np));
   PDB_CUDA(cudaMemcpyAsync(pc.phi.get(), db.phi.get(), ps.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (!pc.lu_apply && use_grouped_apply()) {
+    build_tiles(pc, phi, s);  // solutions live in tile order ...
+    build_inverse(pc, s, pc.slot_of.get());  // ... and the scatter reads them there
+  } else {
+    build_inverse(pc, s);
+  }
   PDB_LAUNCH_CHECK();
   sync(s);
 }
 
 void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s, bool symmetric) {
   Scratch<double> sols(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)), s);
-  k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
-                 pc.compressed ? pc.phi.get() : nullptr, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
-  k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(),
-                    symmetric ? pc.omega_sw.get() : pc.omega_w.get(), nullptr, z, nullptr, s);
+  patch_stage(pc, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
+  scatter_stage(pc, sols.get(), symmetric, nullptr, z, nullptr, s);
   PDB_LAUNCH_CHECK();
 }
 
 void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                   double* history, cudaStream_t s) {
   require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
-  const k::SpmvPlan plan = k::spmv_plan(a.n, a.nnz);
+  const k::SpmvPlan plan = plan_of(a);
   Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
   Scratch<double> sols(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)), s);
   Scratch<double> partials(static_cast<size_t>(std::max(plan.blocks, 1)), s);
@@ -124,9 +228,8 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
                 s);
     if (history) k::finish_sum(partials.get(), plan.blocks, history + sw, true, s);
     if (sw == sweeps) break;
-    k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
-                   pc.compressed ? pc.phi.get() : nullptr, r.get(), nullptr, sols.get(), s);
-    k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(), pc.omega_w.get(), x, nullptr, x, s);
+    patch_stage(pc, r.get(), nullptr, sols.get(), s);
+    scatter_stage(pc, sols.get(), false, x, nullptr, x, s);
   }
   PDB_LAUNCH_CHECK();
 }
@@ -134,7 +237,7 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
 void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                    double* ms_phase, cudaStream_t s) {
   require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
-  const k::SpmvPlan plan = k::spmv_plan(a.n, a.nnz);
+  const k::SpmvPlan plan = plan_of(a);
   Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
   Scratch<double> sols(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)), s);
   std::vector<cudaEvent_t> ev(static_cast<size_t>(4 * std::max<int64_t>(sweeps, 1)));
@@ -144,10 +247,9 @@ void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b,
     PDB_CUDA(cudaEventRecord(e[0], s));
     k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), nullptr, s);
     PDB_CUDA(cudaEventRecord(e[1], s));
-    k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
-                   pc.compressed ? pc.phi.get() : nullptr, r.get(), nullptr, sols.get(), s);
+    patch_stage(pc, r.get(), nullptr, sols.get(), s);
     PDB_CUDA(cudaEventRecord(e[2], s));
-    k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols.get(), pc.omega_w.get(), x, nullptr, x, s);
+    scatter_stage(pc, sols.get(), false, x, nullptr, x, s);
     PDB_CUDA(cudaEventRecord(e[3], s));
   }
   PDB_LAUNCH_CHECK();
