@@ -455,7 +455,9 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
       for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + i * PS + j), T[j]));
       T[i] = __ddiv_rn(s, __ldg(L + i * PS + i));
     }
-    // ---- w = v - A t (mat_vec) and s = A^T w (mat_tvec), one pass over A
+    // ---- w = v - A t (mat_vec) and s = A^T w (mat_tvec) in one pass over
+    // A: row i gives w_i, then immediately its contribution to every s_j
+    // (per-element order identical to mat_vec followed by mat_tvec).
     double S[PS];
 #pragma unroll
     for (int j = 0; j < PS; ++j) S[j] = 0.0;
