@@ -30,7 +30,8 @@ SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, cons
                           int per);
 // Host-side row partition for v3: blocks of <= 256*per nonzeros and <= 64*per rows.
 int stream_nnz();
-std::vector<int32_t> stream_partition(int64_t n, const int64_t* row_ptr, int per);
+std::vector<int32_t> stream_partition(int64_t n, const int64_t* row_ptr, int per);  // per 0: v5 warp partition
+std::vector<int32_t> row_partition(int64_t n, const int64_t* row_ptr, int64_t cap_nnz, int64_t cap_rows);
 void residual(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
               const double* x, const double* b, double* r, double* block_sumsq, cudaStream_t s);
 void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,

@@ -366,6 +366,106 @@ __global__ void __launch_bounds__(kV4Threads, 3) residual_v4_kernel(
   }
 }
 
+// Residual v5: warp-granular CSR streaming.  A precomputed partition gives
+// every warp a run of <= 31 consecutive rows holding <= 256 nonzeros.  The
+// warp loads that contiguous span with fully coalesced 32-lane loads (one
+// 128-byte line per column load, two per value load: ~8x fewer L1 wavefronts
+// than a group-per-row layout), gathers x, stages the products in a per-warp
+// shared-memory slice (no block barrier), then 4-lane groups reduce the rows.
+// A row longer than 256 nonzeros gets a warp to itself and loops.
+constexpr int kV5Warps = 8;
+constexpr int kV5Per = 8;
+constexpr int kV5Nnz = 32 * kV5Per;
+constexpr int kV5Rows = 31;
+
+template <int PER>
+__global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
+    int nwarps, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
+    bool negate_b_absent, int prefetch_dist) {
+  __shared__ double prod[kV5Warps][(32 * PER)];
+  __shared__ double red[kV5Warps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kV5Warps + wib;
+  double sq = 0.0;
+  if (w < nwarps) {
+    // Bulk L2 prefetch (cp.async.bulk.prefetch, one instruction per stream)
+    // of the CSR span a warp one prefetch distance ahead will read, so that
+    // warp finds its columns/values in L2 instead of waiting on HBM.
+    if (prefetch_dist > 0 && lane < 2) {
+      const int wf = w + prefetch_dist;
+      if (wf < nwarps) {
+        const int64_t fb = __ldg(wbase + wf), fe = __ldg(wbase + wf + 1);
+        const char* p0 = lane == 0 ? reinterpret_cast<const char*>(val + fb) : reinterpret_cast<const char*>(col + fb);
+        const char* p1 = lane == 0 ? reinterpret_cast<const char*>(val + fe) : reinterpret_cast<const char*>(col + fe);
+        const uintptr_t a0 = reinterpret_cast<uintptr_t>(p0) & ~uintptr_t(15);
+        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p1) + 15) & ~uintptr_t(15);
+        if (a1 > a0)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+      }
+    }
+    const int64_t r0 = __ldg(wstart + w), base = __ldg(wbase + w), end = __ldg(wbase + w + 1);
+    const int nrows = __ldg(wstart + w + 1) - (int)r0;
+    const int nnz = (int)(end - base);
+    const int64_t rpl = lane <= nrows ? __ldg(rp + r0 + lane) : end;
+    const double bl = (b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
+    if (nnz <= (32 * PER)) {
+      int32_t c[PER];
+      double v[PER];
+      const int32_t* cp = col + base + lane;
+      const double* vp = val + base + lane;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) c[e] = e * 32 + lane < nnz ? __ldcs(cp + e * 32) : 0;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(vp + e * 32) : 0.0;
+      double* pw = prod[wib];
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * __ldg(x + c[e]);
+      __syncwarp();
+      const int g4 = lane & 3, grp = lane >> 2;
+      for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
+        const int rr = rr0 + grp;
+        const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
+        const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
+        const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
+        double a = 0.0;
+        if (rr < nrows)
+          for (int e = lo + g4; e < hi; e += 4) a += pw[e];
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        if (rr < nrows && g4 == 0) {
+          const double rv = b ? brr - a : (negate_b_absent ? -a : a);
+          r[r0 + rr] = rv;
+          sq += rv * rv;
+        }
+      }
+    } else {  // one long row
+      double a = 0.0;
+      for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) {
+        const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
+        r[r0] = rv;
+        sq += rv * rv;
+      }
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kV5Warps; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
 __global__ void finish_sum_kernel(const double* __restrict__ partials, int count, double* out, bool take_sqrt) {
   __shared__ double red[1024];
   double t = 0.0;
@@ -682,7 +782,11 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 int stream_nnz() { return kStreamNnz; }
 
 std::vector<int32_t> stream_partition(int64_t n, const int64_t* rp, int per) {
-  const int64_t cap_nnz = (int64_t)kStreamThreads * per, cap_rows = kStreamRows;
+  if (per < 0) return row_partition(n, rp, 32 * (int64_t)(-per), kV5Rows);  // v5 warp partition
+  return row_partition(n, rp, (int64_t)kStreamThreads * per, kStreamRows);
+}
+
+std::vector<int32_t> row_partition(int64_t n, const int64_t* rp, int64_t cap_nnz, int64_t cap_rows) {
   std::vector<int32_t> starts;
   starts.push_back(0);
   int64_t row = 0;
@@ -701,11 +805,19 @@ SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, cons
                           int per) {
   SpmvPlan p = spmv_plan(n, nnz);
   const char* e = getenv("PDB_SPMV_VERSION");
-  // Default: v2 (measured fastest on config 2: 127 us vs 150 us for v3 and
-  // 176 us for the pipelined v4; all three are L1-wavefront/latency bound,
-  // see DESIGN.md "Residual SpMV").
-  const int want = e ? atoi(e) : 2;
-  if (blk_start && blk_base && nblk > 0 && (want == 3 || want == 4)) {
+  // Default: v5 (measured fastest on config 2: 117 us vs v2 127, v3 150, the
+  // pipelined v4 176; L2 bulk prefetch made v5 slower), see DESIGN.md §3.
+  const int want = e ? atoi(e) : 5;
+  if (blk_start && blk_base && nblk > 0 && want == 5 && per < 0) {
+    p.version = 5;
+    p.entries = -per;
+    p.blk_start = blk_start;
+    p.blk_base = blk_base;
+    p.nblk = nblk;  // warps
+    p.blocks = (nblk + kV5Warps - 1) / kV5Warps;
+    return p;
+  }
+  if (blk_start && blk_base && nblk > 0 && (want == 3 || want == 4) && per > 0) {
     p.version = want;
     p.blk_start = blk_start;
     p.blk_base = blk_base;
@@ -774,6 +886,21 @@ static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, c
                               const double* x, const double* b, double* r, double* sumsq, bool negate,
                               cudaStream_t s) {
   if (n <= 0) return;
+  if (p.version == 5 && p.blk_start) {
+    // prefetch distance in warps (PDB_SPMV_PREFETCH; 0 disables)
+    const char* pfe = getenv("PDB_SPMV_PREFETCH");
+    const int pf = pfe ? atoi(pfe) : 0;
+    if (p.entries == 16)
+      residual_v5_kernel<16><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
+                                                                 p.blk_base, sumsq, negate, pf);
+    else if (p.entries == 4)
+      residual_v5_kernel<4><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
+                                                                p.blk_base, sumsq, negate, pf);
+    else
+      residual_v5_kernel<8><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
+                                                                p.blk_base, sumsq, negate, pf);
+    return;
+  }
   if (p.version == 4 && p.blk_start) {
     residual_v4_kernel<<<p.blocks, kV4Threads, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base, sumsq,
                                                        negate);

@@ -60,8 +60,10 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
   d.col.upload(h.col.data(), h.col.size(), s);
   d.val.upload(h.val.data(), h.val.size(), s);
-  for (int v = 0; v < 2; ++v) {  // streaming-SpMV row partitions for 8 and 16 nonzeros per thread
-    const std::vector<int32_t> part = k::stream_partition(h.n, h.row_ptr.data(), v == 0 ? 8 : 16);
+  // row partitions: [0],[1] v3 blocks (8 / 16 nnz per thread); [2],[3],[4] v5 warps (8 / 16 / 4 per lane)
+  const int pers[5] = {8, 16, -8, -16, -4};
+  for (int v = 0; v < 5; ++v) {
+    const std::vector<int32_t> part = k::stream_partition(h.n, h.row_ptr.data(), pers[v]);
     d.nblk[v] = static_cast<int>(part.size()) - 1;
     d.blk_start[v].alloc(part.size());
     d.blk_start[v].upload(part.data(), part.size(), s);
@@ -74,7 +76,13 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
 }
 
 k::SpmvPlan plan_of(const DeviceCsr& a) {
+  const char* ver = getenv("PDB_SPMV_VERSION");
   const char* e = getenv("PDB_SPMV_PER");
+  if (!ver || atoi(ver) == 5) {  // default: warp-streaming v5
+    const int per = e ? atoi(e) : 8;
+    const int v = per == 16 ? 3 : per == 4 ? 4 : 2;
+    return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 3 ? -16 : v == 4 ? -4 : -8);
+  }
   const int v = e && atoi(e) == 16 ? 1 : 0;
   return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 0 ? 8 : 16);
 }

@@ -33,9 +33,9 @@ struct DeviceCsr {
   DevBuf<int32_t> col;
   DevBuf<double> val;
   // row partitions for the streaming SpMV ([0]: 2048 nnz / block, [1]: 4096)
-  DevBuf<int32_t> blk_start[2];  // nblk + 1 row starts
-  DevBuf<int64_t> blk_base[2];   // row_ptr at each partition boundary
-  int nblk[2] = {0, 0};
+  DevBuf<int32_t> blk_start[5];  // nblk + 1 row starts ([2..4]: per-warp partitions of the v5 kernel)
+  DevBuf<int64_t> blk_base[5];   // row_ptr at each partition boundary
+  int nblk[5] = {0, 0, 0, 0, 0};
 };
 
 struct BuildWork {
