@@ -237,6 +237,50 @@ PDB_API int64_t pdb_precond_patch_size(pdb_precond pc);
 PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
                                  double* x, pdb_report* out_report);
 
+/* ---- multi-GPU: slab-partitioned sweep ----------
+ * Rank r of N owns the contiguous patch range [np*r/N, np*(r+1)/N); DoFs are
+ * owned by the highest rank whose patches contain them.  Each sweep
+ * exchanges interface partial sums (towards the owner, preserving the
+ * reference's ascending-patch order) and the x halo over NCCL. */
+typedef struct pdb_shard_plan_s* pdb_shard_plan;
+typedef struct pdb_shard_s* pdb_shard;
+typedef enum pdb_shard_plan_array {
+  PDB_PLAN_DOFS = 0,      /* int64: local index -> global DoF */
+  PDB_PLAN_ROW_PTR = 1,   /* int64: local CSR */
+  PDB_PLAN_COLS = 2,      /* int64 (local indices) */
+  PDB_PLAN_VALUES = 3,    /* double */
+  PDB_PLAN_PATCHES = 4,   /* int64 (local indices) */
+  PDB_PLAN_WEIGHTS = 5,   /* double (global overlap weights) */
+  PDB_PLAN_OWNED = 6,     /* int64 local indices */
+  PDB_PLAN_UP = 7, PDB_PLAN_UP_PEER = 8,    /* interface partials sent */
+  PDB_PLAN_PIN = 9, PDB_PLAN_PIN_PEER = 10, /* interface partials received */
+  PDB_PLAN_XS = 11, PDB_PLAN_XS_PEER = 12,  /* x halo sent */
+  PDB_PLAN_XR = 13, PDB_PLAN_XR_PEER = 14,  /* x halo received */
+  PDB_PLAN_PATCH_RANGE = 15                 /* int64[2]: first, last+1 global patch */
+} pdb_shard_plan_array;
+
+/* Host-only planning (no GPU needed): the exchange schedule of rank `rank`. */
+PDB_API pdb_status pdb_shard_plan_create(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                         const double* values, int64_t n_patches, int64_t patch_size,
+                                         const int64_t* patches, const double* weights, int rank, int nranks,
+                                         pdb_shard_plan* out);
+PDB_API int64_t pdb_shard_plan_size(pdb_shard_plan plan, int which);
+PDB_API pdb_status pdb_shard_plan_get(pdb_shard_plan plan, int which, void* out);
+PDB_API void pdb_shard_plan_free(pdb_shard_plan plan);
+
+/* Device shard of (m, ps, db) for rank/nranks (db NULL = exact mode). */
+PDB_API pdb_status pdb_comm_unique_id(unsigned char* id128);
+PDB_API pdb_status pdb_shard_create(pdb_matrix m, pdb_patchset ps, pdb_database db, double omega, int rank,
+                                    int nranks, pdb_shard* out);
+PDB_API pdb_status pdb_shard_attach_comm(pdb_shard sh, const unsigned char* id128);
+PDB_API int64_t pdb_shard_local_size(pdb_shard sh);
+PDB_API pdb_status pdb_shard_local_dofs(pdb_shard sh, int64_t* global_ids);
+PDB_API int64_t pdb_shard_owned_count(pdb_shard sh);
+PDB_API pdb_status pdb_shard_owned(pdb_shard sh, int64_t* local_idx);
+/* `sweeps` sweeps on shard-local device vectors (layout of pdb_shard_local_dofs). */
+PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, double* d_x, int64_t sweeps, void* stream);
+PDB_API void pdb_shard_free(pdb_shard sh);
+
 /* Build information: "sm_100a" target, version. */
 PDB_API const char* pdb_build_info(void);
 

@@ -54,6 +54,43 @@ pdb_status unsupported(const char* what) {
 
 cudaStream_t stream_of(void* s) { return s ? static_cast<cudaStream_t>(s) : default_stream(); }
 
+template <typename T>
+int64_t copy_out(const std::vector<T>& v, void* out) {
+  if (out) {
+    if (std::is_same<T, double>::value)
+      std::memcpy(out, v.data(), v.size() * sizeof(double));
+    else
+      for (size_t i = 0; i < v.size(); ++i) static_cast<int64_t*>(out)[i] = static_cast<int64_t>(v[i]);
+  }
+  return static_cast<int64_t>(v.size());
+}
+
+// Plan arrays for pdb_shard_plan_get: integer arrays are widened to int64.
+int64_t plan_array(const ShardPlan& p, int which, void* out) {
+  switch (which) {
+    case PDB_PLAN_DOFS: return copy_out(p.dofs, out);
+    case PDB_PLAN_ROW_PTR: return copy_out(p.rp, out);
+    case PDB_PLAN_COLS: return copy_out(p.ci, out);
+    case PDB_PLAN_VALUES: return copy_out(p.val, out);
+    case PDB_PLAN_PATCHES: return copy_out(p.patches, out);
+    case PDB_PLAN_WEIGHTS: return copy_out(p.weights, out);
+    case PDB_PLAN_OWNED: return copy_out(p.owned, out);
+    case PDB_PLAN_UP: return copy_out(p.up, out);
+    case PDB_PLAN_UP_PEER: return copy_out(p.up_peer, out);
+    case PDB_PLAN_PIN: return copy_out(p.pin, out);
+    case PDB_PLAN_PIN_PEER: return copy_out(p.pin_peer, out);
+    case PDB_PLAN_XS: return copy_out(p.xs, out);
+    case PDB_PLAN_XS_PEER: return copy_out(p.xs_peer, out);
+    case PDB_PLAN_XR: return copy_out(p.xr, out);
+    case PDB_PLAN_XR_PEER: return copy_out(p.xr_peer, out);
+    case PDB_PLAN_PATCH_RANGE: {
+      const std::vector<int64_t> r = {p.k0, p.k1};
+      return copy_out(r, out);
+    }
+    default: return -1;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -533,6 +570,94 @@ PDB_API pdb_status pdb_report_residual_history(pdb_report rep, double* out) {
   return PDB_OK;
 }
 PDB_API void pdb_report_free(pdb_report rep) { delete rep; }
+
+/* ---- multi-GPU shards ---- */
+
+PDB_API pdb_status pdb_shard_plan_create(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                         const double* values, int64_t n_patches, int64_t patch_size,
+                                         const int64_t* patches, const double* weights, int rank, int nranks,
+                                         pdb_shard_plan* out) {
+  if (row_ptr == nullptr || col_idx == nullptr || values == nullptr || patches == nullptr || weights == nullptr ||
+      out == nullptr)
+    return arg_error("null argument");
+  return guarded([&] {
+    HostCsr h = validated_csr(n, row_ptr, col_idx, values);
+    std::vector<int32_t> p32(static_cast<size_t>(n_patches * patch_size));
+    for (size_t q = 0; q < p32.size(); ++q) {
+      require(patches[q] >= 0 && patches[q] < n, Errc::index_out_of_range, "patch index outside matrix");
+      p32[q] = static_cast<int32_t>(patches[q]);
+    }
+    auto plan = std::make_unique<pdb_shard_plan_s>();
+    plan->p = plan_shard(n, h.row_ptr.data(), h.col.data(), h.val.data(), n_patches, patch_size, p32.data(), weights,
+                         rank, nranks);
+    *out = plan.release();
+  });
+}
+
+PDB_API int64_t pdb_shard_plan_size(pdb_shard_plan plan, int which) {
+  return plan == nullptr ? 0 : plan_array(plan->p, which, nullptr);
+}
+
+PDB_API pdb_status pdb_shard_plan_get(pdb_shard_plan plan, int which, void* out) {
+  if (plan == nullptr || out == nullptr) return arg_error("null argument");
+  if (plan_array(plan->p, which, out) < 0) return arg_error("unknown plan array");
+  return PDB_OK;
+}
+
+PDB_API void pdb_shard_plan_free(pdb_shard_plan plan) { delete plan; }
+
+PDB_API pdb_status pdb_comm_unique_id(unsigned char* id128) {
+  if (id128 == nullptr) return arg_error("null argument");
+  return guarded([&] { comm_unique_id(id128); });
+}
+
+PDB_API pdb_status pdb_shard_create(pdb_matrix m, pdb_patchset ps, pdb_database db, double omega, int rank,
+                                    int nranks, pdb_shard* out) {
+  if (m == nullptr || ps == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    HostCsr h = download_csr(m->a, default_stream());
+    pdb_shard sh = shard_new();
+    try {
+      shard_create(h, *ps, db, omega, rank, nranks, *sh, default_stream());
+    } catch (...) {
+      shard_delete(sh);
+      throw;
+    }
+    *out = sh;
+  });
+}
+
+PDB_API pdb_status pdb_shard_attach_comm(pdb_shard sh, const unsigned char* id128) {
+  if (sh == nullptr || id128 == nullptr) return arg_error("null argument");
+  return guarded([&] { shard_attach(*sh, id128); });
+}
+
+PDB_API int64_t pdb_shard_local_size(pdb_shard sh) { return sh == nullptr ? 0 : shard_local_size(*sh); }
+
+PDB_API pdb_status pdb_shard_local_dofs(pdb_shard sh, int64_t* global_ids) {
+  if (sh == nullptr || global_ids == nullptr) return arg_error("null argument");
+  return guarded([&] { plan_array(shard_plan(*sh), PDB_PLAN_DOFS, global_ids); });
+}
+
+PDB_API int64_t pdb_shard_owned_count(pdb_shard sh) {
+  return sh == nullptr ? 0 : static_cast<int64_t>(shard_plan(*sh).owned.size());
+}
+
+PDB_API pdb_status pdb_shard_owned(pdb_shard sh, int64_t* local_idx) {
+  if (sh == nullptr || local_idx == nullptr) return arg_error("null argument");
+  return guarded([&] { plan_array(shard_plan(*sh), PDB_PLAN_OWNED, local_idx); });
+}
+
+PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, double* d_x, int64_t sweeps, void* stream) {
+  if (sh == nullptr || d_b == nullptr || d_x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require_device();
+    require(sweeps >= 0, Errc::invalid_argument, "sweeps must be >= 0");
+    shard_relax(*sh, d_b, d_x, sweeps, stream_of(stream));
+  });
+}
+
+PDB_API void pdb_shard_free(pdb_shard sh) { shard_delete(sh); }
 
 /* ---- experiment drivers (reference experiments.cpp; outside the hot path) ---- */
 

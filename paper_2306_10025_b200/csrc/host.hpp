@@ -9,6 +9,9 @@
 #include "kernels.hpp"
 #include "objects.hpp"
 
+struct pdb_shard_s;
+struct pdb_shard_plan_s;
+
 namespace pdb {
 
 // matrix.cpp
@@ -53,6 +56,9 @@ void export_database(const pdb_database_s& db, const std::string& json_path, con
 void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& out, cudaStream_t s);
 void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
                         cudaStream_t s);
+void precond_compressed_shard(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
+                              cudaStream_t s);
+void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s);
 // z = M^{-1} r on device pointers (symmetric: omega W^1/2 S W^1/2, used by PCG).
 void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s,
                           bool symmetric = false);
@@ -63,6 +69,40 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
 // residual, patch_solve, scatter_update.
 void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                    double* ms_phase, cudaStream_t s);
+
+// shard_plan.cpp -- slab partition of the sweep (host-only planning)
+struct ShardPlan {
+  int rank = 0, nranks = 1;
+  Index k0 = 0, k1 = 0;              // local patch range (global patch ids)
+  std::vector<int64_t> dofs;         // local index -> global DoF (ascending)
+  std::vector<int64_t> rp;           // local CSR (rows = local DoFs; non-patch rows empty)
+  std::vector<int32_t> ci;
+  std::vector<double> val;
+  std::vector<int32_t> patches;      // local patch DoF lists (local indices)
+  std::vector<double> weights;       // global overlap weights at local DoFs
+  std::vector<int32_t> owned;        // local indices of owned DoFs (ascending)
+  std::vector<int32_t> up, up_peer;  // interface partials sent to the owner: local idx, destination rank
+  std::vector<int32_t> pin, pin_peer;  // interface partials received: local idx (owned), source rank
+  std::vector<int32_t> xs, xs_peer;  // x halo sent: local idx (owned), destination rank
+  std::vector<int32_t> xr, xr_peer;  // x halo received: local idx, source rank
+};
+ShardPlan plan_shard(Index n, const int64_t* rp, const int32_t* ci, const double* val, Index np, Index ps,
+                     const int32_t* patches, const double* weights, int rank, int nranks);
+}  // namespace pdb
+struct pdb_shard_plan_s {
+  pdb::ShardPlan p;
+};
+namespace pdb {
+// shard.cu (pdb_shard_s is defined there: it holds the NCCL communicator)
+pdb_shard_s* shard_new();
+void shard_delete(pdb_shard_s* sh);
+int64_t shard_local_size(const pdb_shard_s& sh);
+const ShardPlan& shard_plan(const pdb_shard_s& sh);
+void comm_unique_id(unsigned char* id128);
+void shard_create(const HostCsr& A, const pdb_patchset_s& gps, const pdb_database_s* db, double omega, int rank,
+                  int nranks, pdb_shard_s& sh, cudaStream_t s);
+void shard_attach(pdb_shard_s& sh, const unsigned char* id);
+void shard_relax(pdb_shard_s& sh, const double* b, double* x, int64_t sweeps, cudaStream_t s);
 
 // krylov.cpp
 void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, const pdb_gmres_options& o,

@@ -59,6 +59,11 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
                          const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
                          double* sols, int max_tile, cudaStream_t s);
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
+// Multi-GPU shard helpers: list-driven scatter (see shard.cu), pack / unpack.
+void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
+                   const double* init, const double* omega_w, double* z_out, double* x, cudaStream_t s);
+void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+void scatter_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
 // Binv (column-major) from row-major LU + pivots: column c = lu_solve(e_c).
 void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s);
 // z[i] = (sum over (k,l) in inv(i), ascending k, of sols[k*ps+l]) * omega_w[i];

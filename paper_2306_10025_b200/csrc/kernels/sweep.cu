@@ -632,6 +632,35 @@ __global__ void patch_apply_grouped_kernel(int ps, const int32_t* __restrict__ t
   }
 }
 
+// Shard scatter over a DoF list: z = init[d] (or 0) + sum of the DoF's
+// solution slots in ascending patch order; optionally z_out[t] = z, and/or
+// x[d] += z * omega_w[d] (the smooth() update for owned DoFs).
+__global__ void shard_scatter_kernel(int64_t count, const int32_t* __restrict__ list,
+                                     const int32_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv,
+                                     const double* __restrict__ sols, const double* __restrict__ init,
+                                     const double* __restrict__ omega_w, double* __restrict__ z_out,
+                                     double* __restrict__ x) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int32_t d = list[t];
+  double z = init ? init[d] : 0.0;
+  for (int32_t q = inv_ptr[d]; q < inv_ptr[d + 1]; ++q) z += __ldg(sols + __ldg(inv + q));
+  if (z_out) z_out[t] = z;
+  if (x) x[d] = z * omega_w[d] + x[d];
+}
+
+__global__ void gather_vals_kernel(int64_t count, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                                   double* __restrict__ dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) dst[t] = src[idx[t]];
+}
+
+__global__ void scatter_vals_kernel(int64_t count, const int32_t* __restrict__ idx, const double* __restrict__ src,
+                                    double* __restrict__ dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) dst[idx[t]] = src[t];
+}
+
 // inverse-map entries k*ps + l -> slot_of[k]*ps + l (tile-order solution slots)
 __global__ void remap_inverse_kernel(int64_t count, int ps, const int32_t* __restrict__ slot_of, int32_t* inv) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -985,6 +1014,21 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
   const int threads = ps >= 256 ? ps : (256 / ps) * ps;
   patch_apply_grouped_kernel<<<(unsigned)ntiles, threads, smem, s>>>(ps, tile_entry, tile_start, tile_idx, Binv, r,
                                                                      in_scale, sols);
+}
+
+void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
+                   const double* init, const double* omega_w, double* z_out, double* x, cudaStream_t s) {
+  if (count > 0)
+    shard_scatter_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, list, inv_ptr, inv, sols, init, omega_w,
+                                                                    z_out, x);
+}
+
+void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s) {
+  if (count > 0) gather_vals_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, idx, src, dst);
+}
+
+void scatter_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s) {
+  if (count > 0) scatter_vals_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, idx, src, dst);
 }
 
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s) {

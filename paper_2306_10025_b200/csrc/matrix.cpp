@@ -33,6 +33,13 @@ void require_device() {
         why = std::string("device ") + prop.name + " is not sm_100";
       } else {
         state = 1;
+        // keep freed stream-ordered scratch cached in the pool instead of
+        // returning it to the driver at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          uint64_t keep = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
       }
     }
   }

@@ -173,13 +173,27 @@ void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, p
   sync(s);
 }
 
+static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database_s& db, double omega,
+                                    pdb_precond_s& pc, cudaStream_t s, bool check_onto);
+
 void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& pc,
                         cudaStream_t s) {
+  precond_compressed_impl(ps, db, omega, pc, s, true);
+}
+
+// A shard's patches need not reference every database entry.
+void precond_compressed_shard(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& pc,
+                              cudaStream_t s) {
+  precond_compressed_impl(ps, db, omega, pc, s, false);
+}
+
+static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database_s& db, double omega,
+                                    pdb_precond_s& pc, cudaStream_t s, bool check_onto) {
   require_device();
   require(db.np == ps.np, Errc::dimension_mismatch, "database does not cover the patch set");
   // phi onto the database (Database::phi_onto, compress.cpp:3-10)
   const std::vector<int32_t> phi = db.phi.to_host(s);
-  {
+  if (check_onto) {
     std::vector<char> hit(static_cast<size_t>(db.m), 0);
     bool ok = true;
     for (int32_t j : phi) {

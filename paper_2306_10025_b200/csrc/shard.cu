@@ -1,0 +1,186 @@
+// Multi-GPU relaxation sweep: one slab shard per rank (plan in
+// shard_plan.cpp), NCCL point-to-point exchanges on the sweep stream.
+//
+// Per sweep on rank r:
+//   residual over the shard's patch-DoF rows            (local CSR, v5 SpMV)
+//   patch solves of the shard's patches                  (same kernels as 1 GPU)
+//   interface partial sums z_d (from 0, ascending patch) for DoFs finished by
+//   the upper neighbour  -> ncclSend / ncclRecv (grouped)
+//   owned DoFs: z = received partial (or 0) + own contributions in ascending
+//   patch order, x += z * omega * w                      (bitwise the serial order)
+//   x of owned DoFs needed by other shards -> ncclSend / ncclRecv (grouped)
+// Compressed mode replicates the m_p representative inverses on every rank
+// (config 2: 0.3 MB); exact mode keeps only the shard's own factors.
+#include <nccl.h>
+
+#include <cstring>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+#define PDB_NCCL(call)                                                                              \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess) ::pdb::fail(::pdb::Errc::internal, std::string("NCCL error in " #call ": ") + \
+                                                             ncclGetErrorString(r_));               \
+  } while (0)
+
+namespace pdb {
+void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s);
+}
+
+struct pdb_shard_s {
+  pdb::ShardPlan plan;
+  pdb::DeviceCsr a;
+  pdb_patchset_s ps;
+  pdb_precond_s pc;
+  pdb::DevBuf<int32_t> owned, up, pin, xs, xr;
+  pdb::DevBuf<double> zup, zin, init, xsend, xrecv, r, sols, omega_w;
+  // (peer, offset, count) segments of the exchange lists
+  struct Seg {
+    int peer;
+    int64_t off, cnt;
+  };
+  std::vector<Seg> up_seg, pin_seg, xs_seg, xr_seg;
+  ncclComm_t comm = nullptr;
+  ~pdb_shard_s() {
+    if (comm) ncclCommDestroy(comm);
+  }
+};
+
+namespace pdb {
+
+namespace {
+
+std::vector<pdb_shard_s::Seg> segments(const std::vector<int32_t>& peer) {
+  std::vector<pdb_shard_s::Seg> out;
+  for (size_t i = 0; i < peer.size(); ++i) {
+    if (out.empty() || out.back().peer != peer[i]) out.push_back({peer[i], static_cast<int64_t>(i), 0});
+    ++out.back().cnt;
+  }
+  return out;
+}
+
+template <typename T>
+void put(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  d.alloc(std::max<size_t>(h.size(), 1));
+  d.upload(h.data(), h.size(), s);
+}
+
+}  // namespace
+
+void shard_create(const HostCsr& A, const pdb_patchset_s& gps, const pdb_database_s* db, double omega, int rank,
+                  int nranks, pdb_shard_s& sh, cudaStream_t s) {
+  require_device();
+  const std::vector<int32_t> patches = gps.patches.to_host(s);
+  const std::vector<double> weights = gps.weights.to_host(s);
+  sh.plan = plan_shard(A.n, A.row_ptr.data(), A.col.data(), A.val.data(), gps.np, gps.ps, patches.data(),
+                       weights.data(), rank, nranks);
+  const ShardPlan& P = sh.plan;
+  HostCsr loc;
+  loc.n = static_cast<Index>(P.dofs.size());
+  loc.row_ptr = P.rp;
+  loc.col = P.ci;
+  loc.val = P.val;
+  upload_csr(loc, sh.a, s);
+  sh.ps.n = loc.n;
+  sh.ps.np = P.k1 - P.k0;
+  sh.ps.ps = gps.ps;
+  put(sh.ps.patches, P.patches, s);
+  put(sh.ps.weights, P.weights, s);
+  if (db) {
+    pdb_database_s ldb;
+    ldb.m = db->m;
+    ldb.np = sh.ps.np;
+    ldb.ps = db->ps;
+    const size_t len = static_cast<size_t>(db->ps * db->ps);
+    ldb.lu.alloc(db->m * len);
+    PDB_CUDA(cudaMemcpyAsync(ldb.lu.get(), db->lu.get(), db->m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    ldb.piv.alloc(static_cast<size_t>(db->m * db->ps));
+    PDB_CUDA(cudaMemcpyAsync(ldb.piv.get(), db->piv.get(), db->m * db->ps * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                             s));
+    ldb.phi.alloc(static_cast<size_t>(std::max<Index>(sh.ps.np, 1)));
+    PDB_CUDA(cudaMemcpyAsync(ldb.phi.get(), db->phi.get() + P.k0, sh.ps.np * sizeof(int32_t),
+                             cudaMemcpyDeviceToDevice, s));
+    // the shard may not reference every entry: skip the onto check by building through the exact path
+    // of precond_compressed with a relaxed onto requirement
+    precond_compressed_shard(sh.ps, ldb, omega, sh.pc, s);
+  } else {
+    precond_exact(sh.a, sh.ps, omega, sh.pc, s);
+  }
+  put(sh.owned, P.owned, s);
+  put(sh.up, P.up, s);
+  put(sh.pin, P.pin, s);
+  put(sh.xs, P.xs, s);
+  put(sh.xr, P.xr, s);
+  sh.up_seg = segments(P.up_peer);
+  sh.pin_seg = segments(P.pin_peer);
+  sh.xs_seg = segments(P.xs_peer);
+  sh.xr_seg = segments(P.xr_peer);
+  sh.zup.alloc(std::max<size_t>(P.up.size(), 1));
+  sh.zin.alloc(std::max<size_t>(P.pin.size(), 1));
+  sh.init.alloc(std::max<size_t>(P.dofs.size(), 1));
+  sh.init.zero(s);
+  sh.xsend.alloc(std::max<size_t>(P.xs.size(), 1));
+  sh.xrecv.alloc(std::max<size_t>(P.xr.size(), 1));
+  sh.r.alloc(std::max<size_t>(P.dofs.size(), 1));
+  sh.sols.alloc(static_cast<size_t>(std::max<Index>(sh.ps.np * sh.ps.ps, 1)));
+  std::vector<double> ow(P.weights.size());
+  for (size_t i = 0; i < ow.size(); ++i) ow[i] = omega * P.weights[i];
+  put(sh.omega_w, ow, s);
+  sync(s);
+}
+
+pdb_shard_s* shard_new() { return new pdb_shard_s(); }
+void shard_delete(pdb_shard_s* sh) { delete sh; }
+int64_t shard_local_size(const pdb_shard_s& sh) { return static_cast<int64_t>(sh.plan.dofs.size()); }
+const ShardPlan& shard_plan(const pdb_shard_s& sh) { return sh.plan; }
+
+void comm_unique_id(unsigned char* id128) {
+  ncclUniqueId uid;
+  PDB_NCCL(ncclGetUniqueId(&uid));
+  static_assert(sizeof(uid.internal) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id128, uid.internal, sizeof(uid.internal));
+}
+
+void shard_attach(pdb_shard_s& sh, const unsigned char* id) {
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, sizeof(uid.internal));
+  PDB_NCCL(ncclCommInitRank(&sh.comm, sh.plan.nranks, uid, sh.plan.rank));
+}
+
+void shard_relax(pdb_shard_s& sh, const double* b, double* x, int64_t sweeps, cudaStream_t s) {
+  const ShardPlan& P = sh.plan;
+  require(P.nranks == 1 || sh.comm, Errc::invalid_argument, "shard has no communicator (pdb_shard_attach_comm)");
+  const k::SpmvPlan plan = plan_of(sh.a);
+  const int64_t nl = static_cast<int64_t>(P.dofs.size());
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    k::residual(plan, nl, sh.a.row_ptr.get(), sh.a.col.get(), sh.a.val.get(), x, b, sh.r.get(), nullptr, s);
+    patch_stage(sh.pc, sh.r.get(), nullptr, sh.sols.get(), s);
+    // (a) interface partial sums towards their owners
+    k::shard_scatter(static_cast<int64_t>(P.up.size()), sh.up.get(), sh.pc.inv_ptr.get(), sh.pc.inv.get(),
+                     sh.sols.get(), nullptr, nullptr, sh.zup.get(), nullptr, s);
+    if (P.nranks > 1 && (!sh.up_seg.empty() || !sh.pin_seg.empty())) {
+      PDB_NCCL(ncclGroupStart());
+      for (const auto& g : sh.up_seg) PDB_NCCL(ncclSend(sh.zup.get() + g.off, g.cnt, ncclDouble, g.peer, sh.comm, s));
+      for (const auto& g : sh.pin_seg) PDB_NCCL(ncclRecv(sh.zin.get() + g.off, g.cnt, ncclDouble, g.peer, sh.comm, s));
+      PDB_NCCL(ncclGroupEnd());
+      k::scatter_vals(static_cast<int64_t>(P.pin.size()), sh.pin.get(), sh.zin.get(), sh.init.get(), s);
+    }
+    // (b) owned DoFs: z = partial + own contributions, x += z * omega * w
+    k::shard_scatter(static_cast<int64_t>(P.owned.size()), sh.owned.get(), sh.pc.inv_ptr.get(), sh.pc.inv.get(),
+                     sh.sols.get(), sh.init.get(), sh.omega_w.get(), nullptr, x, s);
+    // (c) x halo
+    if (P.nranks > 1 && (!sh.xs_seg.empty() || !sh.xr_seg.empty())) {
+      k::gather_vals(static_cast<int64_t>(P.xs.size()), sh.xs.get(), x, sh.xsend.get(), s);
+      PDB_NCCL(ncclGroupStart());
+      for (const auto& g : sh.xs_seg) PDB_NCCL(ncclSend(sh.xsend.get() + g.off, g.cnt, ncclDouble, g.peer, sh.comm, s));
+      for (const auto& g : sh.xr_seg) PDB_NCCL(ncclRecv(sh.xrecv.get() + g.off, g.cnt, ncclDouble, g.peer, sh.comm, s));
+      PDB_NCCL(ncclGroupEnd());
+      k::scatter_vals(static_cast<int64_t>(P.xr.size()), sh.xr.get(), sh.xrecv.get(), x, s);
+    }
+  }
+  PDB_LAUNCH_CHECK();
+}
+
+}  // namespace pdb

@@ -505,3 +505,82 @@ def relax_profile(pc: Preconditioner, m: Matrix, d_b: int, d_x: int, sweeps: int
 def precond_sizes(pc: Preconditioner):
     return (_lib.pdb_precond_stored_factors(pc.ptr), _lib.pdb_precond_patch_count(pc.ptr),
             _lib.pdb_precond_patch_size(pc.ptr))
+
+
+# ---- multi-GPU shards ----------------------------------------------------
+PLAN_ARRAYS = dict(dofs=0, row_ptr=1, cols=2, values=3, patches=4, weights=5, owned=6, up=7, up_peer=8, pin=9,
+                   pin_peer=10, xs=11, xs_peer=12, xr=13, xr_peer=14, patch_range=15)
+_sig("pdb_shard_plan_create", C.c_int, C.c_int64, _I64, _I64, _D, C.c_int64, C.c_int64, _I64, _D, C.c_int, C.c_int,
+     C.POINTER(_P))
+_sig("pdb_shard_plan_size", C.c_int64, _P, C.c_int)
+_sig("pdb_shard_plan_get", C.c_int, _P, C.c_int, C.c_void_p)
+_sig("pdb_shard_plan_free", None, _P)
+_sig("pdb_comm_unique_id", C.c_int, C.c_void_p)
+_sig("pdb_shard_create", C.c_int, _P, _P, _P, C.c_double, C.c_int, C.c_int, C.POINTER(_P))
+_sig("pdb_shard_attach_comm", C.c_int, _P, C.c_void_p)
+_sig("pdb_shard_local_size", C.c_int64, _P)
+_sig("pdb_shard_local_dofs", C.c_int, _P, _I64)
+_sig("pdb_shard_owned_count", C.c_int64, _P)
+_sig("pdb_shard_owned", C.c_int, _P, _I64)
+_sig("pdb_shard_relax_device", C.c_int, _P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+_sig("pdb_shard_free", None, _P)
+
+
+def shard_plan(csr, patches, weights, rank: int, nranks: int) -> dict:
+    """Host-only exchange schedule of one rank (no GPU needed)."""
+    rp = np.ascontiguousarray(csr[0], np.int64)
+    ci = np.ascontiguousarray(csr[1], np.int64)
+    v = _f64(csr[2])
+    pt = np.ascontiguousarray(patches, np.int64)
+    w = _f64(weights)
+    h = C.c_void_p()
+    _check(_lib.pdb_shard_plan_create(len(rp) - 1, _ip(rp), _ip(ci), _dp(v), pt.shape[0], pt.shape[1], _ip(pt), _dp(w),
+                                      rank, nranks, C.byref(h)))
+    try:
+        out = {}
+        for name, which in PLAN_ARRAYS.items():
+            size = _lib.pdb_shard_plan_size(h, which)
+            arr = np.empty(size, np.float64 if name in ("values", "weights") else np.int64)
+            if size:
+                _check(_lib.pdb_shard_plan_get(h, which, arr.ctypes.data_as(C.c_void_p)))
+            out[name] = arr
+        return out
+    finally:
+        _lib.pdb_shard_plan_free(h)
+
+
+def comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _check(_lib.pdb_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Shard(_Handle):
+    """One rank's slab of the sweep on this process's GPU."""
+    _free = _lib.pdb_shard_free
+
+    @classmethod
+    def create(cls, m: Matrix, ps: PatchSet, db: Optional[Database], omega: float, rank: int,
+               nranks: int) -> "Shard":
+        out = C.c_void_p()
+        _check(_lib.pdb_shard_create(m.ptr, ps.ptr, db.ptr if db is not None else None, omega, rank, nranks,
+                                     C.byref(out)))
+        return cls(out)
+
+    def attach(self, uid: bytes) -> None:
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        _check(_lib.pdb_shard_attach_comm(self._ptr, buf))
+
+    def local_dofs(self) -> np.ndarray:
+        out = np.empty(_lib.pdb_shard_local_size(self._ptr), np.int64)
+        _check(_lib.pdb_shard_local_dofs(self._ptr, _ip(out)))
+        return out
+
+    def owned(self) -> np.ndarray:
+        out = np.empty(_lib.pdb_shard_owned_count(self._ptr), np.int64)
+        if len(out):
+            _check(_lib.pdb_shard_owned(self._ptr, _ip(out)))
+        return out
+
+    def relax_device(self, d_b: int, d_x: int, sweeps: int, stream: int = 0) -> None:
+        _check(_lib.pdb_shard_relax_device(self._ptr, d_b, d_x, sweeps, stream or None))
