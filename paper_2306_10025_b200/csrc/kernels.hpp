@@ -22,7 +22,23 @@ struct SpmvPlan {
   const int32_t* blk_start = nullptr;  // v3: row partition (nblk + 1 entries)
   const int64_t* blk_base = nullptr;   // v3: row_ptr[blk_start[b]]
   int nblk = 0;                        // v3/v4: partition blocks (v4 runs a persistent grid of `blocks`)
+  // v8: block-local column windows (see DeviceCsr)
+  const uint16_t* lcol = nullptr;
+  const int32_t* win_ptr = nullptr;
+  const int32_t* win_runs = nullptr;
+  int win_max = 0;
+  // v9: SELL-C-sigma slices (see DeviceCsr)
+  const int64_t* sell_off = nullptr;
+  const int32_t* sell_row = nullptr;
+  const double* sell_val = nullptr;
+  const int32_t* sell_col = nullptr;
+  int64_t nslices = 0;
 };
+constexpr int kSellC = 32;          // rows per SELL slice (one warp)
+constexpr int kSellSigma = 8192;    // sorting window (rows)
+constexpr int kWindowItems = 8;     // v5/v8 warp items per block
+constexpr int kWindowCap = 4096;    // max staged x window per block (doubles)
+constexpr int kItemNnz = 256;       // v5/v8 item capacity (nonzeros)
 SpmvPlan spmv_plan(int64_t n, int64_t nnz);
 // v3 plan over a matrix's row partition.
 // per = nonzeros per thread of the partition (8 or 16; 256 threads per block).
@@ -58,6 +74,14 @@ int grouped_tile(int ps);  // patches per grouped-apply tile
 void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
                          const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
                          double* sols, int max_tile, cudaStream_t s);
+// Tensor-core grouped apply (FP64 mma.sync m8n8k4, ps <= 32, tiles <= 32 patches): sols_tile =
+// B_f^{-1} [r_k1 .. r_k32] with each inverse pre-arranged in A-fragment order by build_frag_inverses.
+bool dmma_apply_supported(int ps);
+int64_t frag_len(int ps);  // doubles per entry in fragment order
+void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag, cudaStream_t s);
+void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
+                      double* sols, cudaStream_t s);
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
 // Multi-GPU shard helpers: list-driven scatter (see shard.cu), pack / unpack.
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,

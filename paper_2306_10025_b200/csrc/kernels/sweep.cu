@@ -375,16 +375,26 @@ __global__ void __launch_bounds__(kV4Threads, 3) residual_v4_kernel(
 // A row longer than 256 nonzeros gets a warp to itself and loops.
 constexpr int kV5Warps = 8;
 constexpr int kV5Per = 8;
-constexpr int kV5Nnz = 32 * kV5Per;
 constexpr int kV5Rows = 31;
 
-template <int PER>
+// CHUNK selects the row reduction.  false: 4-lane groups stride through each
+// row's products (8 rows at a time; rows of unequal length leave lanes idle
+// and the 8 row offsets collide in smem banks).  true (v6): lane l sums its
+// own PER consecutive products, cutting at row starts (a 32*PER-bit boundary
+// mask), and writes each segment sum at the segment's first position; lane
+// rho then adds the segment sums of row rho in ascending position.  Products
+// live at i + i/PER so both the slot-interleaved stores and the lane-chunk
+// reads are bank-conflict free; ~3x fewer shared-memory wavefronts.
+template <int PER, bool CHUNK>
 __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
     int nwarps, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
     const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
     bool negate_b_absent, int prefetch_dist) {
-  __shared__ double prod[kV5Warps][(32 * PER)];
+  constexpr int kSlots = CHUNK ? 32 * PER + 32 : 32 * PER;
+  constexpr int kMaskWords = PER;  // 32*PER bits
+  __shared__ double prod[kV5Warps][kSlots];
+  __shared__ uint32_t bmask[kV5Warps][CHUNK ? kMaskWords : 1];
   __shared__ double red[kV5Warps];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kV5Warps + wib;
@@ -420,6 +430,51 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
 #pragma unroll
       for (int e = 0; e < PER; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(vp + e * 32) : 0.0;
       double* pw = prod[wib];
+      if constexpr (CHUNK) {
+        uint32_t* mk = bmask[wib];
+        if (lane < kMaskWords) mk[lane] = 0u;
+        // products at padded position i + i/PER
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int i = e * 32 + lane;
+          if (i < nnz) pw[i + i / PER] = v[e] * __ldg(x + c[e]);
+        }
+        __syncwarp();
+        const int o = (int)(rpl - base);  // start of row `lane` (lanes 1..nrows-1 mark a cut)
+        if (lane >= 1 && lane < nrows && o < nnz) atomicOr(mk + (o >> 5), 1u << (o & 31));
+        __syncwarp();
+        const int cb = lane * PER;
+        const uint32_t fl = (mk[cb >> 5] >> (cb & 31)) & (PER == 32 ? 0xffffffffu : ((1u << PER) - 1u));
+        double* pc = pw + cb + lane;  // = padded position of cb
+        double pr[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) pr[j] = cb + j < nnz ? pc[j] : 0.0;
+        double acc = 0.0;
+        int seg = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+          const double pj = pr[j];
+          if (j > 0 && ((fl >> j) & 1u)) {
+            pc[seg] = acc;
+            acc = 0.0;
+            seg = j;
+          }
+          acc += pj;
+        }
+        if (cb < nnz) pc[seg] = acc;
+        __syncwarp();
+        const int hi = (int)(__shfl_down_sync(0xffffffffu, rpl, 1) - base);
+        if (lane < nrows) {
+          double a = 0.0;
+          if (o < hi) {
+            a = pw[o + o / PER];
+            for (int q = o / PER + 1; q * PER < hi; ++q) a += pw[q * (PER + 1)];
+          }
+          const double rv = b ? bl - a : (negate_b_absent ? -a : a);
+          r[r0 + lane] = rv;
+          sq += rv * rv;
+        }
+      } else {
 #pragma unroll
       for (int e = 0; e < PER; ++e)
         if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * __ldg(x + c[e]);
@@ -441,6 +496,7 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
           sq += rv * rv;
         }
       }
+      }
     } else {  // one long row
       double a = 0.0;
       for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
@@ -461,6 +517,319 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int q = 0; q < kV5Warps; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v7: v5's warp items fed by the bulk-copy (TMA) engine.  A
+// persistent grid; warp gw processes items gw, gw + TW, ... (TW = all warps,
+// so the GPU sweeps a window of consecutive rows and x stays L2-hot).  Each
+// warp owns an S-stage ring in shared memory; lane 0 arms stage s's mbarrier
+// with the byte count and issues cp.async.bulk copies of the item's values
+// and columns S items ahead, so a warp always has S items of CSR bytes in
+// flight without holding them in registers (v5 keeps ~3 KB per warp in
+// flight only during its load phase, which left DRAM at ~50 % busy).  The
+// consumer then gathers x, forms the products in place and reduces rows as
+// v5.  Copies are 16-byte aligned: the span is widened to aligned bounds
+// (the device CSR arrays carry 32 elements of zero padding) and the data
+// sits at offset base & 1 (values) / base & 3 (columns) in the stage.
+constexpr int kV7Vals = 32 * kV5Per + 4;  // 256 + alignment slack, doubles
+constexpr int kV7Cols = 32 * kV5Per + 8;  // ints
+constexpr int kV7StageBytes = kV7Vals * 8 + kV7Cols * 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+template <int S>
+__global__ void __launch_bounds__(kV5Warps * 32) residual_v7_kernel(
+    int nitems, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
+    bool negate_b_absent) {
+  extern __shared__ __align__(128) unsigned char v7_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int TW = gridDim.x * kV5Warps;
+  const int gw = blockIdx.x * kV5Warps + wib;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(v7_smem) + wib * S;
+  unsigned char* ring = v7_smem + 128 * ((kV5Warps * S * 8 + 127) / 128) + (size_t)wib * S * kV7StageBytes;
+  __shared__ double red[kV5Warps];
+  if (lane < S) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + lane)) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // issue item j into stage st (lane 0 only)
+  auto issue = [&](int j, int st) {
+    unsigned char* sg = ring + (size_t)st * kV7StageBytes;
+    const int64_t base = __ldg(wbase + j), end = __ldg(wbase + j + 1);
+    const uint32_t bar = smem_addr(bars + st);
+    if (end - base <= 32 * kV5Per) {
+      const int64_t vb = base & ~int64_t(1), cb = base & ~int64_t(3);
+      const uint32_t vbytes = (uint32_t)(((end - vb) * 8 + 15) & ~int64_t(15));
+      const uint32_t cbytes = (uint32_t)(((end - cb) * 4 + 15) & ~int64_t(15));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vbytes + cbytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(sg)),
+          "l"(val + vb), "r"(vbytes), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(sg + kV7Vals * 8)),
+          "l"(col + cb), "r"(cbytes), "r"(bar)
+          : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+  };
+  if (lane == 0)
+    for (int q = 0; q < S; ++q)
+      if (gw + q * TW < nitems) issue(gw + q * TW, q);
+  __syncwarp();
+  double sq = 0.0;
+  int it = 0;
+  for (int j = gw; j < nitems; j += TW, ++it) {
+    const int st = it % S;
+    unsigned char* sg = ring + (size_t)st * kV7StageBytes;
+    // independent of the staged bytes: row pointers and b for this item
+    const int64_t r0 = __ldg(wstart + j);
+    const int nrows = __ldg(wstart + j + 1) - (int)r0;
+    const int64_t base = __ldg(wbase + j), end = __ldg(wbase + j + 1);
+    const int64_t rpl = lane <= nrows ? __ldg(rp + r0 + lane) : end;
+    const double bl = (b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
+    const int nnz = (int)(end - base);
+    mbar_wait(smem_addr(bars + st), (uint32_t)((it / S) & 1));
+    if (nnz <= 32 * kV5Per) {
+      double* vs = reinterpret_cast<double*>(sg) + (base & 1);
+      const int32_t* cs = reinterpret_cast<const int32_t*>(sg + kV7Vals * 8) + (base & 3);
+      int32_t c[kV5Per];
+#pragma unroll
+      for (int e = 0; e < kV5Per; ++e) c[e] = e * 32 + lane < nnz ? cs[e * 32 + lane] : 0;
+      double xv[kV5Per];
+#pragma unroll
+      for (int e = 0; e < kV5Per; ++e) xv[e] = e * 32 + lane < nnz ? __ldg(x + c[e]) : 0.0;
+#pragma unroll
+      for (int e = 0; e < kV5Per; ++e)
+        if (e * 32 + lane < nnz) vs[e * 32 + lane] *= xv[e];
+      __syncwarp();
+      const int g4 = lane & 3, grp = lane >> 2;
+      for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
+        const int rr = rr0 + grp;
+        const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
+        const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
+        const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
+        double a = 0.0;
+        if (rr < nrows)
+          for (int e = lo + g4; e < hi; e += 4) a += vs[e];
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        if (rr < nrows && g4 == 0) {
+          const double rv = b ? brr - a : (negate_b_absent ? -a : a);
+          r[r0 + rr] = rv;
+          sq += rv * rv;
+        }
+      }
+    } else {  // one long row, straight from global memory
+      double a = 0.0;
+      for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) {
+        const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
+        r[r0] = rv;
+        sq += rv * rv;
+      }
+    }
+    __syncwarp();
+    const int jn = j + S * TW;
+    if (lane == 0 && jn < nitems) issue(jn, st);
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kV5Warps; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v8: v5's warp items with block-local column windows (built by
+// build_windows, matrix.cpp).  The block first stages x over its window --
+// runs of consecutive columns, one warp per run, coalesced -- while every
+// warp already has its item's values and 16-bit local columns in flight;
+// after one block barrier the x gathers read shared memory.  Per nonzero the
+// kernel streams 10 bytes (value + local column) instead of 12, and the L1
+// no longer replays x gathers over ~6 cache lines per warp load.
+static_assert(kItemNnz == 32 * kV5Per, "v8 item capacity");
+static_assert(kWindowItems == kV5Warps, "v8 block = one window");
+
+template <int MINB>
+__global__ void __launch_bounds__(kV5Warps * 32, MINB) residual_v8_kernel(
+    int nitems, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const uint16_t* __restrict__ lcol, const int32_t* __restrict__ win_ptr, const int2* __restrict__ win_runs,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
+    bool negate_b_absent) {
+  extern __shared__ double xs[];
+  __shared__ double prod[kV5Warps][32 * kV5Per];
+  __shared__ double red[kV5Warps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kV5Warps + wib;
+  const bool has = w < nitems;
+  int64_t r0 = 0, base = 0, end = 0;
+  int nrows = 0;
+  if (has) {
+    r0 = __ldg(wstart + w);
+    nrows = __ldg(wstart + w + 1) - (int)r0;
+    base = __ldg(wbase + w);
+    end = __ldg(wbase + w + 1);
+  }
+  const int nnz = (int)(end - base);
+  const bool shortitem = has && nnz <= 32 * kV5Per;
+  // item bytes in flight before the window staging
+  uint16_t lc[kV5Per];
+  double v[kV5Per];
+  if (shortitem) {
+#pragma unroll
+    for (int e = 0; e < kV5Per; ++e) lc[e] = e * 32 + lane < nnz ? __ldcs(lcol + base + e * 32 + lane) : 0;
+#pragma unroll
+    for (int e = 0; e < kV5Per; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(val + base + e * 32 + lane) : 0.0;
+  }
+  const int64_t rpl = (has && lane <= nrows) ? __ldg(rp + r0 + lane) : end;
+  const double bl = (has && b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
+  {
+    const int q0 = __ldg(win_ptr + blockIdx.x), q1 = __ldg(win_ptr + blockIdx.x + 1) - 1;  // last: sentinel
+    for (int q = q0 + wib; q < q1; q += kV5Warps) {
+      const int2 a = __ldg(win_runs + q);
+      const int len = __ldg(win_runs + q + 1).y - a.y;
+      for (int j = lane; j < len; j += 32) xs[a.y + j] = __ldg(x + a.x + j);
+    }
+  }
+  __syncthreads();
+  double sq = 0.0;
+  if (shortitem) {
+    double* pw = prod[wib];
+#pragma unroll
+    for (int e = 0; e < kV5Per; ++e)
+      if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * xs[lc[e]];
+    __syncwarp();
+    const int g4 = lane & 3, grp = lane >> 2;
+    for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
+      const int rr = rr0 + grp;
+      const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
+      const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
+      const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
+      double a = 0.0;
+      if (rr < nrows)
+        for (int e = lo + g4; e < hi; e += 4) a += pw[e];
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      if (rr < nrows && g4 == 0) {
+        const double rv = b ? brr - a : (negate_b_absent ? -a : a);
+        r[r0 + rr] = rv;
+        sq += rv * rv;
+      }
+    }
+  } else if (has) {  // one long row, global columns
+    double a = 0.0;
+    for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+    if (lane == 0) {
+      const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
+      r[r0] = rv;
+      sq += rv * rv;
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kV5Warps; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// Residual v9 over the SELL-C-sigma copy (build_sell, matrix.cpp): warp per
+// slice of 32 rows, lane l owns slice row l.  Step j loads entry j of all 32
+// rows -- one 256-byte value span and one 128-byte column span, fully
+// coalesced -- and the x gathers of 32 similar rows hit a few lines.  U steps
+// are loaded before any is consumed (memory-level parallelism without a
+// shared-memory stage), lanes past their row's end are predicated off, and
+// each lane accumulates its row in CSR order with unfused multiply/add:
+// r = b - s bit for bit as the reference spmv + smooth (sparse.cpp:50-63,
+// precond.cpp:95-97).
+template <int U>
+__global__ void __launch_bounds__(256) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
+                                                            const int2* __restrict__ srow,
+                                                            const double* __restrict__ sval,
+                                                            const int32_t* __restrict__ scol,
+                                                            const double* __restrict__ x, const double* __restrict__ b,
+                                                            double* __restrict__ r, double* __restrict__ block_sumsq,
+                                                            bool negate_b_absent) {
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
+  double sq = 0.0;
+  if (sl < nslices) {
+    const int2 rl = __ldg(srow + sl * 32 + lane);
+    const int len = rl.y;
+    const int L = __reduce_max_sync(0xffffffffu, (unsigned)len);
+    const int64_t o = __ldg(soff + sl);
+    const double* vp = sval + o + lane;
+    const int32_t* cp = scol + o + lane;
+    const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
+    double acc = 0.0;
+    for (int j = 0; j < L; j += U) {
+      int32_t c[U];
+      double v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j + u < len ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    if (rl.x >= 0) {
+      const double rv = b ? __dsub_rn(bl, acc) : (negate_b_absent ? -acc : acc);
+      r[rl.x] = rv;
+      sq += rv * rv;
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q];
       block_sumsq[blockIdx.x] = t;
     }
   }
@@ -632,6 +1001,99 @@ __global__ void patch_apply_grouped_kernel(int ps, const int32_t* __restrict__ t
   }
 }
 
+// Tensor-core grouped apply.  A tile of up to 32 patches sharing entry f is
+// the dense product S (ps x 32) = B_f^{-1} (ps x ps) R (ps x 32), done with
+// FP64 mma.sync.m8n8k4: warp w owns rows [8w, 8w+8) of B_f^{-1} (MT = ps/8
+// warps), keeps its KS = ps/4 A-fragments in registers (loaded coalesced from
+// the fragment-ordered copy, L2-resident), and sweeps the four 8-patch column
+// blocks of R from shared memory.  Per tile: 4 x MT x KS DMMAs and MT x KS x 4
+// fragment loads, against ps x 32 x 5 shared loads for the CUDA-core version.
+// Fragment layouts (PTX ISA, mma.m8n8k4 .f64): A row-major, lane (g = lane/4,
+// t = lane%4) holds A[g][t]; B column-major, B[t][g]; C/D: C[g][2t], C[g][2t+1].
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
+
+template <int MT, int KS>
+__global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
+                                                                   const int32_t* __restrict__ tile_start,
+                                                                   const int32_t* __restrict__ tile_idx,
+                                                                   const double* __restrict__ frag,
+                                                                   const double* __restrict__ r,
+                                                                   const double* __restrict__ in_scale,
+                                                                   double* __restrict__ sols) {
+  // row stride of the staged residuals: KS*4, bumped by 4 when that is a
+  // multiple of 8 so the B-fragment loads (8 patches x 4 k) hit distinct banks
+  constexpr int KSTR = (KS % 2) ? KS * 4 : KS * 4 + 4;
+  constexpr int NTH = MT * 32;
+  constexpr int TOT = kDmmaTile * KSTR;
+  constexpr int ITER = (TOT + NTH - 1) / NTH;
+  __shared__ double rk[TOT];
+  const int t = blockIdx.x;
+  const int f = __ldg(tile_entry + t);
+  const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a[KS];
+  const double* fa = frag + ((int64_t)f * MT + w) * (KS * 32) + lane;
+#pragma unroll
+  for (int q = 0; q < KS; ++q) a[q] = __ldg(fa + q * 32);
+  // stage R (patch-major, zero padded in k and in patches) -- all index
+  // loads of a thread first, then all residual loads
+  const int32_t* ti = tile_idx + (int64_t)s0 * ps;
+  int32_t gi[ITER];
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int e = threadIdx.x + it * NTH;
+    const int p = e / KSTR, k = e - p * KSTR;
+    gi[it] = (e < TOT && p < cnt && k < ps) ? __ldg(ti + p * ps + k) : -1;
+  }
+#pragma unroll
+  for (int it = 0; it < ITER; ++it) {
+    const int e = threadIdx.x + it * NTH;
+    double v = 0.0;
+    if (gi[it] >= 0) {
+      v = __ldg(r + gi[it]);
+      if (in_scale) v *= __ldg(in_scale + gi[it]);
+    }
+    if (e < TOT) rk[e] = v;
+  }
+  __syncthreads();
+  const int g = lane >> 2, tg = lane & 3;
+  const int row = w * 8 + g;
+#pragma unroll
+  for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+    if (nt * 8 < cnt) {  // block-uniform
+      double c0 = 0.0, c1 = 0.0;
+      const double* bp = rk + (nt * 8 + g) * KSTR + tg;
+#pragma unroll
+      for (int q = 0; q < KS; ++q) dmma_m8n8k4(c0, c1, a[q], bp[q * 4]);
+      const int p0 = nt * 8 + 2 * tg;
+      if (row < ps) {
+        if (p0 < cnt) sols[(int64_t)(s0 + p0) * ps + row] = c0;
+        if (p0 + 1 < cnt) sols[(int64_t)(s0 + p0 + 1) * ps + row] = c1;
+      }
+    }
+  }
+}
+
+// frag[f][w][q][lane] = B_f^{-1}[8w + lane/4][4q + lane%4] (0 outside ps x ps)
+__global__ void build_frag_kernel(int64_t total, int ps, int mt, int ks, const double* __restrict__ inv_cm,
+                                  double* __restrict__ frag) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int lane = (int)(e & 31);
+  const int64_t rest = e >> 5;
+  const int q = (int)(rest % ks);
+  const int w = (int)((rest / ks) % mt);
+  const int64_t f = rest / ((int64_t)ks * mt);
+  const int row = w * 8 + (lane >> 2), c = q * 4 + (lane & 3);
+  frag[e] = (row < ps && c < ps) ? inv_cm[f * ps * ps + (int64_t)c * ps + row] : 0.0;
+}
+
 // Shard scatter over a DoF list: z = init[d] (or 0) + sum of the DoF's
 // solution slots in ascending patch order; optionally z_out[t] = z, and/or
 // x[d] += z * omega_w[d] (the smooth() update for owned DoFs).
@@ -675,32 +1137,50 @@ __global__ void remap_inverse_kernel(int64_t count, int ps, const int32_t* __res
 // from the slot count exactly as compute_weights does (patch.cpp:12-20):
 // scale = omega * (1.0 / count) (or omega * sqrt(1.0 / count) for the
 // symmetric PCG weighting).
+constexpr int kScatterU = 2;
+
 template <int MAXC>
 __global__ void scatter_update_pad_kernel(int64_t n, const int32_t* __restrict__ inv_pad,
                                           const double* __restrict__ sols, double omega, bool sym,
                                           const double* __restrict__ x_in, double* __restrict__ z_out,
                                           double* __restrict__ x_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int32_t e[MAXC];
+  // kScatterU DoFs per thread (blockDim apart, so every load stays
+  // coalesced): all index loads, then all solution / x loads are in flight
+  // together -- the kernel is latency-bound on the idx -> sols chain.
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kScatterU + threadIdx.x;
+  int32_t e[kScatterU][MAXC];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) e[c] = __ldcs(inv_pad + (int64_t)c * n + i);
-  double v[MAXC];
+  for (int u = 0; u < kScatterU; ++u) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) v[c] = e[c] >= 0 ? __ldg(sols + e[c]) : 0.0;
-  double z = 0.0;
-  int cnt = 0;
+    for (int c = 0; c < MAXC; ++c) e[u][c] = i < n ? __ldcs(inv_pad + (int64_t)c * n + i) : -1;
+  }
+  double v[kScatterU][MAXC], xi[kScatterU];
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c)
-    if (e[c] >= 0) {
-      z += v[c];
-      ++cnt;
-    }
-  double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
-  if (sym) w = sqrt(w);
-  z *= omega * w;
-  if (z_out) z_out[i] = z;
-  if (x_out) x_out[i] = z + x_in[i];
+  for (int u = 0; u < kScatterU; ++u) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
+    xi[u] = (x_out && i < n) ? __ldcs(x_in + i) : 0.0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) v[u][c] = e[u][c] >= 0 ? __ldg(sols + e[u][c]) : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kScatterU; ++u) {
+    const int64_t i = i0 + (int64_t)u * blockDim.x;
+    if (i >= n) break;
+    double z = 0.0;
+    int cnt = 0;
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (e[u][c] >= 0) {
+        z += v[u][c];
+        ++cnt;
+      }
+    double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+    if (sym) w = sqrt(w);
+    z *= omega * w;
+    if (z_out) z_out[i] = z;
+    if (x_out) x_out[i] = z + xi[u];
+  }
 }
 
 __global__ void build_inverse_pad_kernel(int64_t n, int maxc, const int32_t* __restrict__ inv_ptr,
@@ -830,6 +1310,10 @@ std::vector<int32_t> row_partition(int64_t n, const int64_t* rp, int64_t cap_nnz
   return starts;
 }
 
+int v7_stages();
+template <int S>
+int v7_grid(int nitems);
+
 SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, const int64_t* blk_base, int nblk,
                           int per) {
   SpmvPlan p = spmv_plan(n, nnz);
@@ -837,8 +1321,19 @@ SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, cons
   // Default: v5 (measured fastest on config 2: 117 us vs v2 127, v3 150, the
   // pipelined v4 176; L2 bulk prefetch made v5 slower), see DESIGN.md §3.
   const int want = e ? atoi(e) : 5;
-  if (blk_start && blk_base && nblk > 0 && want == 5 && per < 0) {
-    p.version = 5;
+  if (blk_start && blk_base && nblk > 0 && want == 7 && per == -kV5Per) {
+    // v7 reuses the v5 item partition; `entries` carries the stage count and
+    // `blocks` the persistent grid
+    p.version = 7;
+    p.entries = v7_stages();
+    p.blk_start = blk_start;
+    p.blk_base = blk_base;
+    p.nblk = nblk;
+    p.blocks = p.entries == 2 ? v7_grid<2>(nblk) : p.entries == 4 ? v7_grid<4>(nblk) : v7_grid<3>(nblk);
+    return p;
+  }
+  if (blk_start && blk_base && nblk > 0 && (want == 5 || want == 6) && per < 0) {
+    p.version = want;
     p.entries = -per;
     p.blk_start = blk_start;
     p.blk_base = blk_base;
@@ -911,23 +1406,114 @@ static void launch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, con
   }
 }
 
+int v7_stages() {
+  const char* e = getenv("PDB_SPMV_STAGES");
+  const int v = e ? atoi(e) : 3;
+  return v == 2 || v == 4 ? v : 3;
+}
+
+size_t v7_smem(int stages) {
+  return 128 * ((kV5Warps * stages * 8 + 127) / 128) + (size_t)kV5Warps * stages * kV7StageBytes;
+}
+
+template <int S>
+int v7_grid(int nitems) {
+  static int per_sm[5] = {0, 0, 0, 0, 0};
+  if (!per_sm[S]) {
+    const size_t smem = v7_smem(S);
+    cudaFuncSetAttribute(residual_v7_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, residual_v7_kernel<S>, kV5Warps * 32, smem);
+    per_sm[S] = occ > 0 ? occ : 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int need = (nitems + kV5Warps - 1) / kV5Warps;
+  return need < sms * per_sm[S] ? need : sms * per_sm[S];
+}
+
+template <int S>
+static void launch_v7_s(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+                        const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+  residual_v7_kernel<S><<<p.blocks, kV5Warps * 32, v7_smem(S), s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
+                                                                    p.blk_base, sumsq, negate);
+}
+
+static void launch_v7(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+                      const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+  if (p.entries == 2)
+    launch_v7_s<2>(p, rp, col, val, x, b, r, sumsq, negate, s);
+  else if (p.entries == 4)
+    launch_v7_s<4>(p, rp, col, val, x, b, r, sumsq, negate, s);
+  else
+    launch_v7_s<3>(p, rp, col, val, x, b, r, sumsq, negate, s);
+}
+
+template <bool CHUNK>
+static void launch_v5(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+                      const double* b, double* r, double* sumsq, bool negate, int pf, cudaStream_t s) {
+  const unsigned th = kV5Warps * 32;
+  if (p.entries == 16)
+    residual_v5_kernel<16, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                          sumsq, negate, pf);
+  else if (p.entries == 4)
+    residual_v5_kernel<4, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                         sumsq, negate, pf);
+  else
+    residual_v5_kernel<8, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                         sumsq, negate, pf);
+}
+
 static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
                               const double* x, const double* b, double* r, double* sumsq, bool negate,
                               cudaStream_t s) {
   if (n <= 0) return;
-  if (p.version == 5 && p.blk_start) {
+  if (p.version == 9 && p.sell_off) {
+    const unsigned g = (unsigned)p.blocks;
+    const int2* sr = reinterpret_cast<const int2*>(p.sell_row);
+    switch (p.entries) {
+      case 2: residual_sell_kernel<2><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
+      case 4: residual_sell_kernel<4><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
+      case 16: residual_sell_kernel<16><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
+      default: residual_sell_kernel<8><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
+    }
+    return;
+  }
+  if (p.version == 8 && p.blk_start && p.lcol) {
+    const size_t smem = (size_t)p.win_max * sizeof(double);
+    const char* mb = getenv("PDB_V8_MINB");
+    const bool capped = mb && atoi(mb) == 5;
+    static size_t opted[2] = {48 * 1024, 48 * 1024};
+    if (smem > opted[capped]) {
+      if (capped)
+        cudaFuncSetAttribute(residual_v8_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      else
+        cudaFuncSetAttribute(residual_v8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      opted[capped] = smem;
+    }
+    if (capped)
+      residual_v8_kernel<5><<<p.blocks, kV5Warps * 32, smem, s>>>(p.nblk, rp, col, val, p.lcol, p.win_ptr,
+                                                                  reinterpret_cast<const int2*>(p.win_runs), x, b, r,
+                                                                  p.blk_start, p.blk_base, sumsq, negate);
+    else
+      residual_v8_kernel<1><<<p.blocks, kV5Warps * 32, smem, s>>>(p.nblk, rp, col, val, p.lcol, p.win_ptr,
+                                                                  reinterpret_cast<const int2*>(p.win_runs), x, b, r,
+                                                                  p.blk_start, p.blk_base, sumsq, negate);
+    return;
+  }
+  if (p.version == 7 && p.blk_start) {
+    launch_v7(p, rp, col, val, x, b, r, sumsq, negate, s);
+    return;
+  }
+  if ((p.version == 5 || p.version == 6) && p.blk_start) {
     // prefetch distance in warps (PDB_SPMV_PREFETCH; 0 disables)
     const char* pfe = getenv("PDB_SPMV_PREFETCH");
     const int pf = pfe ? atoi(pfe) : 0;
-    if (p.entries == 16)
-      residual_v5_kernel<16><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
-                                                                 p.blk_base, sumsq, negate, pf);
-    else if (p.entries == 4)
-      residual_v5_kernel<4><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
-                                                                p.blk_base, sumsq, negate, pf);
+    if (p.version == 6)
+      launch_v5<true>(p, rp, col, val, x, b, r, sumsq, negate, pf, s);
     else
-      residual_v5_kernel<8><<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
-                                                                p.blk_base, sumsq, negate, pf);
+      launch_v5<false>(p, rp, col, val, x, b, r, sumsq, negate, pf, s);
     return;
   }
   if (p.version == 4 && p.blk_start) {
@@ -1016,6 +1602,38 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
                                                                      in_scale, sols);
 }
 
+bool dmma_apply_supported(int ps) { return ps >= 1 && ps <= 32 && grouped_tile(ps) <= kDmmaTile; }
+
+int64_t frag_len(int ps) { return (int64_t)((ps + 7) / 8) * ((ps + 3) / 4) * 32; }
+
+void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag, cudaStream_t s) {
+  const int64_t total = nf * frag_len(ps);
+  if (total > 0)
+    build_frag_kernel<<<grid_for(total, kBlock), kBlock, 0, s>>>(total, ps, (ps + 7) / 8, (ps + 3) / 4, inv_cm, frag);
+}
+
+void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
+                      double* sols, cudaStream_t s) {
+  if (ntiles <= 0) return;
+  const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
+#define PDB_DMMA_CASE(M, K)                                                                                  \
+  if (mt == M && ks == K) {                                                                                  \
+    patch_apply_dmma_kernel<M, K><<<(unsigned)ntiles, M * 32, 0, s>>>(ps, tile_entry, tile_start, tile_idx, \
+                                                                      frag, r, in_scale, sols);             \
+    return;                                                                                                  \
+  }
+  PDB_DMMA_CASE(1, 1)
+  PDB_DMMA_CASE(1, 2)
+  PDB_DMMA_CASE(2, 3)
+  PDB_DMMA_CASE(2, 4)
+  PDB_DMMA_CASE(3, 5)
+  PDB_DMMA_CASE(3, 6)
+  PDB_DMMA_CASE(4, 7)
+  PDB_DMMA_CASE(4, 8)
+#undef PDB_DMMA_CASE
+}
+
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
                    const double* init, const double* omega_w, double* z_out, double* x, cudaStream_t s) {
   if (count > 0)
@@ -1043,7 +1661,7 @@ void build_inverse_pad(int64_t n, int maxc, const int32_t* inv_ptr, const int32_
 void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const double* sols, double omega, bool sym,
                         const double* x_in, double* z_out, double* x_out, cudaStream_t s) {
   if (n <= 0) return;
-  const unsigned g = grid_for(n, kBlock);
+  const unsigned g = grid_for(n, kBlock * kScatterU);
   switch (maxc) {
     case 1: scatter_update_pad_kernel<1><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
     case 2: scatter_update_pad_kernel<2><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;

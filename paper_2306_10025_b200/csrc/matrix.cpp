@@ -57,13 +57,189 @@ int num_sms() {
   return sms;
 }
 
+// Block-local column windows for the v8 residual.  Block b of the v5 item
+// partition (items [8b, 8b+8)) touches a small set D_b of distinct columns
+// (for a FEM matrix: a few lattice lines around ~50 consecutive rows).  D_b is
+// stored as runs of consecutive columns; every nonzero of the block gets its
+// 16-bit position in D_b.  The kernel stages x[D_b] in shared memory once per
+// block, so column indices cost 2 bytes instead of 4 and the x gathers hit
+// shared memory instead of ~6 L1 lines per warp load.  Items holding one
+// overlong row (> kItemNnz) keep the global column path.  Returns false
+// (windows not built) when a block's window exceeds kWindowCap.
+bool build_windows(const HostCsr& h, const std::vector<int32_t>& items, DeviceCsr& d, cudaStream_t s) {
+  const int64_t nitems = static_cast<int64_t>(items.size()) - 1;
+  const int64_t nb = (nitems + k::kWindowItems - 1) / k::kWindowItems;
+  if (nb <= 0 || h.nnz() == 0) return false;
+  std::vector<uint16_t> lcol(static_cast<size_t>(h.nnz()), 0);
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  std::vector<std::vector<int32_t>> runs(static_cast<size_t>(T));
+  std::vector<std::vector<int32_t>> nrun(static_cast<size_t>(T));
+  std::vector<int> ok(static_cast<size_t>(T), 1), wmax(static_cast<size_t>(T), 0);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back([&, t] {
+      const int64_t b0 = nb * t / T, b1 = nb * (t + 1) / T;
+      std::vector<int32_t> cols;
+      for (int64_t b = b0; b < b1 && ok[t]; ++b) {
+        cols.clear();
+        const int64_t i0 = b * k::kWindowItems, i1 = std::min<int64_t>(nitems, i0 + k::kWindowItems);
+        for (int64_t it = i0; it < i1; ++it) {
+          const int64_t p0 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it)])];
+          const int64_t p1 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it + 1)])];
+          if (p1 - p0 > k::kItemNnz) continue;
+          cols.insert(cols.end(), h.col.begin() + p0, h.col.begin() + p1);
+        }
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        const int m = static_cast<int>(cols.size());
+        if (m > k::kWindowCap) {
+          ok[t] = 0;
+          break;
+        }
+        wmax[t] = std::max(wmax[t], m);
+        int count = 0;
+        for (int q = 0; q < m; ++q)
+          if (q == 0 || cols[static_cast<size_t>(q)] != cols[static_cast<size_t>(q - 1)] + 1) {
+            runs[t].push_back(cols[static_cast<size_t>(q)]);
+            runs[t].push_back(q);
+            ++count;
+          }
+        runs[t].push_back(-1);  // sentinel: window size
+        runs[t].push_back(m);
+        nrun[t].push_back(count + 1);
+        for (int64_t it = i0; it < i1; ++it) {
+          const int64_t p0 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it)])];
+          const int64_t p1 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it + 1)])];
+          if (p1 - p0 > k::kItemNnz) continue;
+          for (int64_t p = p0; p < p1; ++p)
+            lcol[static_cast<size_t>(p)] = static_cast<uint16_t>(
+                std::lower_bound(cols.begin(), cols.end(), h.col[static_cast<size_t>(p)]) - cols.begin());
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (int t = 0; t < T; ++t)
+    if (!ok[t]) return false;
+  std::vector<int32_t> ptr;
+  ptr.reserve(static_cast<size_t>(nb + 1));
+  std::vector<int32_t> all;
+  int32_t at = 0;
+  for (int t = 0; t < T; ++t) {
+    for (int32_t c : nrun[t]) {
+      ptr.push_back(at);
+      at += c;
+    }
+    all.insert(all.end(), runs[t].begin(), runs[t].end());
+  }
+  ptr.push_back(at);
+  d.lcol.alloc(lcol.size() + 64);
+  PDB_CUDA(cudaMemsetAsync(d.lcol.get(), 0, (lcol.size() + 64) * sizeof(uint16_t), s));
+  d.lcol.upload(lcol.data(), lcol.size(), s);
+  d.win_ptr.alloc(ptr.size());
+  d.win_ptr.upload(ptr.data(), ptr.size(), s);
+  d.win_runs.alloc(all.size());
+  d.win_runs.upload(all.data(), all.size(), s);
+  int m = 0;
+  for (int t = 0; t < T; ++t) m = std::max(m, wmax[t]);
+  d.win_max = std::max(32, (m + 31) / 32 * 32);
+  sync(s);
+  return true;
+}
+
+// SELL-C-sigma (Kreutzer et al., SIAM J. Sci. Comput. 2014) copy of the
+// matrix for the v9 residual: rows are sorted by length (descending, stable)
+// inside windows of kSellSigma rows and cut into slices of kSellC = 32; a
+// slice is stored column-major (entry j of its l-th row at off + 32 j + l),
+// so lane l of a warp walks row l and every load of the warp is one
+// contiguous 256-byte (values) / 128-byte (columns) span.  Each lane sums its
+// row sequentially in CSR order -- no cross-lane reduction, and with
+// unfused multiply/add the residual is bitwise the reference spmv's.
+void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
+  const int64_t n = h.n;
+  if (n == 0 || h.nnz() == 0) return;
+  const int64_t nwin = (n + k::kSellSigma - 1) / k::kSellSigma;
+  std::vector<int32_t> perm(static_cast<size_t>(n));
+  std::vector<int64_t> win_slices(static_cast<size_t>(nwin) + 1, 0);
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  auto len = [&](int64_t i) { return h.row_ptr[static_cast<size_t>(i + 1)] - h.row_ptr[static_cast<size_t>(i)]; };
+  auto par = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+      pool.emplace_back([&, t] {
+        for (int64_t w = nwin * t / T; w < nwin * (t + 1) / T; ++w) body(w);
+      });
+    for (auto& th : pool) th.join();
+  };
+  par([&](int64_t w) {
+    const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
+    for (int64_t i = r0; i < r1; ++i) perm[static_cast<size_t>(i)] = static_cast<int32_t>(i);
+    std::stable_sort(perm.begin() + r0, perm.begin() + r1, [&](int32_t a, int32_t b) { return len(a) > len(b); });
+    win_slices[static_cast<size_t>(w) + 1] = (r1 - r0 + k::kSellC - 1) / k::kSellC;
+  });
+  for (int64_t w = 0; w < nwin; ++w) win_slices[static_cast<size_t>(w) + 1] += win_slices[static_cast<size_t>(w)];
+  const int64_t ns = win_slices.back();
+  // slice widths and offsets (slices are numbered window by window)
+  std::vector<int64_t> off(static_cast<size_t>(ns) + 1, 0);
+  for (int64_t w = 0; w < nwin; ++w) {
+    const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
+    for (int64_t q = 0; q < win_slices[static_cast<size_t>(w) + 1] - win_slices[static_cast<size_t>(w)]; ++q) {
+      const int64_t sl = win_slices[static_cast<size_t>(w)] + q;
+      const int64_t first = r0 + q * k::kSellC;  // longest row of the slice
+      off[static_cast<size_t>(sl) + 1] = off[static_cast<size_t>(sl)] + k::kSellC * len(perm[static_cast<size_t>(first)]);
+      (void)r1;
+    }
+  }
+  std::vector<int32_t> rows(static_cast<size_t>(2 * ns * k::kSellC), 0);
+  std::vector<double> val(static_cast<size_t>(off.back()), 0.0);
+  std::vector<int32_t> col(static_cast<size_t>(off.back()), 0);
+  par([&](int64_t w) {
+    const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
+    for (int64_t q = 0; q < win_slices[static_cast<size_t>(w) + 1] - win_slices[static_cast<size_t>(w)]; ++q) {
+      const int64_t sl = win_slices[static_cast<size_t>(w)] + q;
+      const int64_t o = off[static_cast<size_t>(sl)];
+      for (int l = 0; l < k::kSellC; ++l) {
+        const int64_t at = r0 + q * k::kSellC + l;
+        const size_t ri = static_cast<size_t>(2 * (sl * k::kSellC + l));
+        if (at >= r1) {
+          rows[ri] = -1;
+          rows[ri + 1] = 0;
+          continue;
+        }
+        const int32_t row = perm[static_cast<size_t>(at)];
+        const int64_t p0 = h.row_ptr[static_cast<size_t>(row)], L = len(row);
+        rows[ri] = row;
+        rows[ri + 1] = static_cast<int32_t>(L);
+        for (int64_t j = 0; j < L; ++j) {
+          val[static_cast<size_t>(o + j * k::kSellC + l)] = h.val[static_cast<size_t>(p0 + j)];
+          col[static_cast<size_t>(o + j * k::kSellC + l)] = h.col[static_cast<size_t>(p0 + j)];
+        }
+      }
+    }
+  });
+  d.sell_off.alloc(off.size());
+  d.sell_off.upload(off.data(), off.size(), s);
+  d.sell_row.alloc(rows.size());
+  d.sell_row.upload(rows.data(), rows.size(), s);
+  d.sell_val.alloc(val.size());
+  d.sell_val.upload(val.data(), val.size(), s);
+  d.sell_col.alloc(col.size());
+  d.sell_col.upload(col.data(), col.size(), s);
+  d.nslices = ns;
+  sync(s);
+}
+
 void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   require_device();
   d.n = h.n;
   d.nnz = h.nnz();
   d.row_ptr.alloc(static_cast<size_t>(h.n + 1));
-  d.col.alloc(static_cast<size_t>(d.nnz));
-  d.val.alloc(static_cast<size_t>(d.nnz));
+  // 32 zeroed elements of tail padding: the bulk-copy SpMV widens spans to
+  // 16-byte bounds and may read past the last nonzero
+  constexpr size_t kPad = 32;
+  d.col.alloc(static_cast<size_t>(d.nnz) + kPad);
+  d.val.alloc(static_cast<size_t>(d.nnz) + kPad);
+  PDB_CUDA(cudaMemsetAsync(d.col.get() + d.nnz, 0, kPad * sizeof(int32_t), s));
+  PDB_CUDA(cudaMemsetAsync(d.val.get() + d.nnz, 0, kPad * sizeof(double), s));
   d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
   d.col.upload(h.col.data(), h.col.size(), s);
   d.val.upload(h.val.data(), h.val.size(), s);
@@ -79,13 +255,46 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
     d.blk_base[v].alloc(base.size());
     d.blk_base[v].upload(base.data(), base.size(), s);
     sync(s);
+    if (v == 2) {
+      const char* e = getenv("PDB_SPMV_WINDOWS");
+      if (e && std::string(e) == "1" && !build_windows(h, part, d, s)) d.win_max = 0;
+    }
   }
+  const char* e = getenv("PDB_SPMV_SELL");
+  if (!(e && std::string(e) == "0")) build_sell(h, d, s);
 }
 
 k::SpmvPlan plan_of(const DeviceCsr& a) {
   const char* ver = getenv("PDB_SPMV_VERSION");
   const char* e = getenv("PDB_SPMV_PER");
-  if (!ver || atoi(ver) == 5) {  // default: warp-streaming v5
+  if ((!ver || atoi(ver) == 9) && a.nslices > 0) {  // SELL-C-sigma
+    k::SpmvPlan p = k::spmv_plan(a.n, a.nnz);
+    p.version = 9;
+    p.entries = e ? atoi(e) : 8;  // unroll depth (measured: 8 > 4 > 2 on configs 2 and 3)
+    p.sell_off = a.sell_off.get();
+    p.sell_row = a.sell_row.get();
+    p.sell_val = a.sell_val.get();
+    p.sell_col = a.sell_col.get();
+    p.nslices = a.nslices;
+    p.blocks = static_cast<int>((a.nslices + 7) / 8);
+    return p;
+  }
+  if (ver && atoi(ver) == 8 && a.win_max > 0) {  // v5 items with block-local column windows
+    k::SpmvPlan p = k::spmv_plan(a.n, a.nnz);
+    p.version = 8;
+    p.entries = 8;
+    p.blk_start = a.blk_start[2].get();
+    p.blk_base = a.blk_base[2].get();
+    p.nblk = a.nblk[2];
+    p.blocks = (a.nblk[2] + k::kWindowItems - 1) / k::kWindowItems;
+    p.lcol = a.lcol.get();
+    p.win_ptr = a.win_ptr.get();
+    p.win_runs = a.win_runs.get();
+    p.win_max = a.win_max;
+    return p;
+  }
+  if (!ver || atoi(ver) == 5 || atoi(ver) == 6 || atoi(ver) == 7 || atoi(ver) == 8) {
+    // default: warp-streaming v5 (v6: chunked row reduction, v7: bulk-copy fed)
     const int per = e ? atoi(e) : 8;
     const int v = per == 16 ? 3 : per == 4 ? 4 : 2;
     return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 3 ? -16 : v == 4 ? -4 : -8);
@@ -145,6 +354,8 @@ HostCsr download_csr(const DeviceCsr& d, cudaStream_t s) {
   h.row_ptr = d.row_ptr.to_host(s);
   h.col = d.col.to_host(s);
   h.val = d.val.to_host(s);
+  h.col.resize(static_cast<size_t>(d.nnz));  // drop the tail padding
+  h.val.resize(static_cast<size_t>(d.nnz));
   return h;
 }
 

@@ -36,6 +36,21 @@ struct DeviceCsr {
   DevBuf<int32_t> blk_start[5];  // nblk + 1 row starts ([2..4]: per-warp partitions of the v5 kernel)
   DevBuf<int64_t> blk_base[5];   // row_ptr at each partition boundary
   int nblk[5] = {0, 0, 0, 0, 0};
+  // block-local column windows over the v5 item partition (v8 residual):
+  // lcol = column index into the block's staged x window, win_ptr = first
+  // run of each block, win_runs = (first column, window offset) per run plus
+  // one sentinel (-1, window size) per block
+  DevBuf<uint16_t> lcol;
+  DevBuf<int32_t> win_ptr;
+  DevBuf<int32_t> win_runs;
+  int win_max = 0;  // 0: windows not built (some block's window too large)
+  // SELL-C-sigma copy (v9 residual): slices of 32 rows of similar length,
+  // entry j of slice row l at sell_off[s] + 32 j + l; sell_row = {row, length}
+  DevBuf<int64_t> sell_off;
+  DevBuf<int32_t> sell_row;
+  DevBuf<double> sell_val;
+  DevBuf<int32_t> sell_col;
+  int64_t nslices = 0;  // 0: not built
 };
 
 struct BuildWork {
@@ -95,6 +110,7 @@ struct pdb_precond_s {
   // cluster-grouped apply (compressed mode): patches sorted by entry, tiled
   pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
   int ntiles = 0, max_tile = 0;
+  pdb::DevBuf<double> frag;  // inverses in DMMA A-fragment order (tensor-core grouped apply), when allocated
   pdb::DevBuf<int32_t> inv_pad;  // slot-major padded inverse map (maxc_pad slots), when maxc_pad > 0
   int maxc_pad = 0;
   pdb::DevBuf<int32_t> inv_ptr;

@@ -138,9 +138,19 @@ void build_tiles(pdb_precond_s& pc, const std::vector<int32_t>& phi, cudaStream_
   sync(s);
 }
 
-bool use_grouped_apply() {
+// Grouping pays when entries are shared: by default only with >= 4 patches
+// per entry on average (an identity-phi database keeps the per-patch kernel,
+// so Exact == Compressed holds bit for bit).  PDB_GROUPED=0/1 forces it.
+bool use_grouped_apply(int64_t np, int64_t nf) {
   const char* e = getenv("PDB_GROUPED");
-  return !(e && std::string(e) == "0");
+  if (e) return std::string(e) != "0";
+  return np >= 4 * nf;
+}
+
+// Tensor-core (DMMA) tiles for ps <= 32 unless PDB_DMMA=0.
+bool use_dmma_apply(int ps) {
+  const char* e = getenv("PDB_DMMA");
+  return k::dmma_apply_supported(ps) && !(e && std::string(e) == "0");
 }
 
 }  // namespace
@@ -148,7 +158,10 @@ bool use_grouped_apply() {
 // sols_k = B_phi(k)^{-1} (r .* in_scale)|_k for every patch.
 void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s) {
   const int32_t* phi = pc.compressed ? pc.phi.get() : nullptr;
-  if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
+  if (!pc.lu_apply && pc.compressed && pc.ntiles > 0 && pc.frag.get() && use_dmma_apply(static_cast<int>(pc.ps)))
+    k::patch_apply_dmma(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
+                        pc.tile_idx.get(), pc.frag.get(), r, in_scale, sols, s);
+  else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
     k::patch_apply_grouped(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
                            pc.tile_idx.get(), pc.factors.get(), r, in_scale, sols, pc.max_tile, s);
   else if (pc.lu_apply)
@@ -212,9 +225,13 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
   set_factors(pc, db.m, static_cast<int>(ps.ps), db.lu.get(), db.piv.get(), s);
   pc.phi.alloc(static_cast<size_t>(ps.np));
   PDB_CUDA(cudaMemcpyAsync(pc.phi.get(), db.phi.get(), ps.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  if (!pc.lu_apply && use_grouped_apply()) {
+  if (!pc.lu_apply && use_grouped_apply(ps.np, db.m)) {
     build_tiles(pc, phi, s);  // solutions live in tile order ...
     build_inverse(pc, s, pc.slot_of.get());  // ... and the scatter reads them there
+    if (use_dmma_apply(static_cast<int>(ps.ps))) {
+      pc.frag.alloc(static_cast<size_t>(db.m * k::frag_len(static_cast<int>(ps.ps))));
+      k::build_frag_inverses(db.m, static_cast<int>(ps.ps), pc.factors.get(), pc.frag.get(), s);
+    }
   } else {
     build_inverse(pc, s);
   }

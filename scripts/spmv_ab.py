@@ -24,10 +24,11 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "v3": {"PDB_SPMV_VERSION": "3"},
-    "v2_g8_e8": {"PDB_SPMV_VERSION": "2", "PDB_SPMV_GROUP": "8", "PDB_SPMV_ENTRIES": "8"},
-    "v2_g4_e8": {"PDB_SPMV_VERSION": "2", "PDB_SPMV_GROUP": "4", "PDB_SPMV_ENTRIES": "8"},
-    "v1_g2": {"PDB_SPMV_VERSION": "1", "PDB_SPMV_GROUP": "2"},
+    "v5": {"PDB_SPMV_VERSION": "5"},
+    "v6_p16": {"PDB_SPMV_VERSION": "6", "PDB_SPMV_PER": "16"},
+    "v9_u2": {"PDB_SPMV_VERSION": "9", "PDB_SPMV_PER": "2"},
+    "v9_u4": {"PDB_SPMV_VERSION": "9", "PDB_SPMV_PER": "4"},
+    "v9_u8": {"PDB_SPMV_VERSION": "9", "PDB_SPMV_PER": "8"},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2

@@ -57,6 +57,15 @@ def test_spmv(c1, orc):
 
 
 @pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_spmv_bit_exact(name, request, orc):
+    """The default SELL-C-sigma SpMV sums every row sequentially in CSR order
+    with unfused multiply/add, as the reference spmv (sparse.cpp:50-63)."""
+    c = request.getfixturevalue(name)
+    x = np.random.default_rng(11).uniform(-1, 1, c.A.rows)
+    assert np.array_equal(c.A.spmv(x), orc.spmv(c.csr, x))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
 def test_exact_database_lu_bit_exact(name, request, P, orc):
     c = request.getfixturevalue(name)
     db = P.Database.build(c.A, c.ps, P.EXACT)
