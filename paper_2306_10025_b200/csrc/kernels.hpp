@@ -82,6 +82,16 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
                       const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
                       double* sols, cudaStream_t s);
+// DoF-major variant: the tile gathers r through zfwd & (2^28-1) and stores each
+// solution value at Z[(zfwd >> 28) * n + (zfwd & (2^28-1))].
+void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
+                        const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
+                        cudaStream_t s);
+// zfwd / zcnt from the (tile-order) inverse map
+void build_zmap(int64_t n, const int32_t* inv_ptr, const int32_t* inv, int32_t* zfwd, uint8_t* zcnt, cudaStream_t s);
+// x_out = x_in + omega * w(count) * sum_{c < zcnt[i]} Z[c*n + i]  (and/or z_out)
+void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
+               double* z_out, double* x_out, cudaStream_t s);
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
 // Multi-GPU shard helpers: list-driven scatter (see shard.cu), pack / unpack.
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,

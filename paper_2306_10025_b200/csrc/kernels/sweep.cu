@@ -782,14 +782,14 @@ __global__ void __launch_bounds__(kV5Warps * 32, MINB) residual_v8_kernel(
 // each lane accumulates its row in CSR order with unfused multiply/add:
 // r = b - s bit for bit as the reference spmv + smooth (sparse.cpp:50-63,
 // precond.cpp:95-97).
-template <int U>
-__global__ void __launch_bounds__(256) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
                                                             const int2* __restrict__ srow,
                                                             const double* __restrict__ sval,
                                                             const int32_t* __restrict__ scol,
                                                             const double* __restrict__ x, const double* __restrict__ b,
                                                             double* __restrict__ r, double* __restrict__ block_sumsq,
-                                                            bool negate_b_absent) {
+                                                            bool negate_b_absent, int pf) {
   __shared__ double red[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
@@ -804,6 +804,18 @@ __global__ void __launch_bounds__(256) residual_sell_kernel(int64_t nslices, con
     const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
     double acc = 0.0;
     for (int j = 0; j < L; j += U) {
+      // pull the slice's next columns/values towards L2 (bulk prefetch, no
+      // registers held) so the loads pf iterations ahead find them there
+      if (pf > 0 && lane == 0) {
+        const int jn = j + pf * U;
+        if (jn < L) {
+          const int cnt = (L - jn < U ? L - jn : U) * 32;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + o + (int64_t)jn * 32),
+                       "r"((unsigned)(cnt * 8)));
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + o + (int64_t)jn * 32),
+                       "r"((unsigned)(cnt * 4)));
+        }
+      }
       int32_t c[U];
       double v[U], xv[U];
 #pragma unroll
@@ -1018,21 +1030,28 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
 
 constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
 
-template <int MT, int KS>
-__global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
+constexpr int32_t kDofMask = (1 << 28) - 1;  // zfwd = (slot rank << 28) | dof
+
+// Z = false: solutions to sols in tile order (idx = tile_idx).  Z = true:
+// idx = zfwd, each solution value goes to out[(f >> 28) * n + (f & mask)].
+// R is staged unpadded (patch p, local row k at p * ps + k), so the copy is a
+// flat, division-free loop; the A fragments are zero for k >= ps, which
+// cancels the neighbouring patch's values a B fragment reads there, and the
+// stage is zero-filled past the tile's cnt * ps live values (no NaN garbage).
+template <int MT, int KS, bool Z>
+__global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64_t n,
+                                                                   const int32_t* __restrict__ tile_entry,
                                                                    const int32_t* __restrict__ tile_start,
-                                                                   const int32_t* __restrict__ tile_idx,
+                                                                   const int32_t* __restrict__ idx,
                                                                    const double* __restrict__ frag,
                                                                    const double* __restrict__ r,
                                                                    const double* __restrict__ in_scale,
-                                                                   double* __restrict__ sols) {
-  // row stride of the staged residuals: KS*4, bumped by 4 when that is a
-  // multiple of 8 so the B-fragment loads (8 patches x 4 k) hit distinct banks
-  constexpr int KSTR = (KS % 2) ? KS * 4 : KS * 4 + 4;
+                                                                   double* __restrict__ out) {
   constexpr int NTH = MT * 32;
-  constexpr int TOT = kDmmaTile * KSTR;
+  constexpr int TOT = kDmmaTile * KS * 4;  // >= 31 * ps + 4 * KS: every B-fragment read
   constexpr int ITER = (TOT + NTH - 1) / NTH;
   __shared__ double rk[TOT];
+  __shared__ int32_t fk[Z ? TOT : 1];
   const int t = blockIdx.x;
   const int f = __ldg(tile_entry + t);
   const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
@@ -1041,23 +1060,23 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
   const double* fa = frag + ((int64_t)f * MT + w) * (KS * 32) + lane;
 #pragma unroll
   for (int q = 0; q < KS; ++q) a[q] = __ldg(fa + q * 32);
-  // stage R (patch-major, zero padded in k and in patches) -- all index
-  // loads of a thread first, then all residual loads
-  const int32_t* ti = tile_idx + (int64_t)s0 * ps;
+  const int live = cnt * ps;
+  const int32_t* ti = idx + (int64_t)s0 * ps;
   int32_t gi[ITER];
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     const int e = threadIdx.x + it * NTH;
-    const int p = e / KSTR, k = e - p * KSTR;
-    gi[it] = (e < TOT && p < cnt && k < ps) ? __ldg(ti + p * ps + k) : -1;
+    gi[it] = e < live ? __ldg(ti + e) : -1;
   }
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     const int e = threadIdx.x + it * NTH;
     double v = 0.0;
     if (gi[it] >= 0) {
-      v = __ldg(r + gi[it]);
-      if (in_scale) v *= __ldg(in_scale + gi[it]);
+      const int32_t d = Z ? (gi[it] & kDofMask) : gi[it];
+      v = __ldg(r + d);
+      if (in_scale) v *= __ldg(in_scale + d);
+      if constexpr (Z) fk[e] = gi[it];
     }
     if (e < TOT) rk[e] = v;
   }
@@ -1068,16 +1087,60 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
   for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
     if (nt * 8 < cnt) {  // block-uniform
       double c0 = 0.0, c1 = 0.0;
-      const double* bp = rk + (nt * 8 + g) * KSTR + tg;
+      const double* bp = rk + (nt * 8 + g) * ps + tg;
 #pragma unroll
       for (int q = 0; q < KS; ++q) dmma_m8n8k4(c0, c1, a[q], bp[q * 4]);
       const int p0 = nt * 8 + 2 * tg;
       if (row < ps) {
-        if (p0 < cnt) sols[(int64_t)(s0 + p0) * ps + row] = c0;
-        if (p0 + 1 < cnt) sols[(int64_t)(s0 + p0 + 1) * ps + row] = c1;
+        if constexpr (Z) {
+          if (p0 < cnt) {
+            const int32_t z0 = fk[p0 * ps + row];
+            out[(int64_t)(z0 >> 28) * n + (z0 & kDofMask)] = c0;
+          }
+          if (p0 + 1 < cnt) {
+            const int32_t z1 = fk[(p0 + 1) * ps + row];
+            out[(int64_t)(z1 >> 28) * n + (z1 & kDofMask)] = c1;
+          }
+        } else {
+          if (p0 < cnt) out[(int64_t)(s0 + p0) * ps + row] = c0;
+          if (p0 + 1 < cnt) out[(int64_t)(s0 + p0 + 1) * ps + row] = c1;
+        }
       }
     }
   }
+}
+
+__global__ void build_zmap_kernel(int64_t n, const int32_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv,
+                                  int32_t* __restrict__ zfwd, uint8_t* __restrict__ zcnt) {
+  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int32_t lo = inv_ptr[d], hi = inv_ptr[d + 1];
+  zcnt[d] = (uint8_t)(hi - lo);
+  for (int32_t q = lo; q < hi; ++q) zfwd[inv[q]] = ((q - lo) << 28) | (int32_t)d;
+}
+
+// Scatter over DoF-major slots: loads only the zcnt[i] live slots of DoF i
+// (ascending patch order), weight recomputed as scatter_update_pad_kernel.
+template <int MAXC>
+__global__ void scatter_z_kernel(int64_t n, const uint8_t* __restrict__ zcnt, const double* __restrict__ Z,
+                                 double omega, bool sym, const double* __restrict__ x_in,
+                                 double* __restrict__ z_out, double* __restrict__ x_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cnt = zcnt[i];
+  double v[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) v[c] = c < cnt ? __ldcs(Z + (int64_t)c * n + i) : 0.0;
+  const double xi = x_out ? __ldcs(x_in + i) : 0.0;
+  double z = 0.0;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+    if (c < cnt) z += v[c];
+  double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+  if (sym) w = sqrt(w);
+  z *= omega * w;
+  if (z_out) z_out[i] = z;
+  if (x_out) x_out[i] = z + xi;
 }
 
 // frag[f][w][q][lane] = B_f^{-1}[8w + lane/4][4q + lane%4] (0 outside ps x ps)
@@ -1472,12 +1535,21 @@ static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, c
   if (p.version == 9 && p.sell_off) {
     const unsigned g = (unsigned)p.blocks;
     const int2* sr = reinterpret_cast<const int2*>(p.sell_row);
-    switch (p.entries) {
-      case 2: residual_sell_kernel<2><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
-      case 4: residual_sell_kernel<4><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
-      case 16: residual_sell_kernel<16><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
-      default: residual_sell_kernel<8><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate); break;
-    }
+    // L2 bulk prefetch one step group ahead (measured: pf 1 best, 90.5 us vs
+    // 96.7 without on config 2; 263 vs 301 us on config 3)
+    const char* pfe = getenv("PDB_SELL_PF");
+    const int pf = pfe ? atoi(pfe) : 1;
+    const char* mbe = getenv("PDB_SELL_MINB");
+    const int minb = mbe ? atoi(mbe) : 0;
+#define PDB_SELL(U, M) \
+  residual_sell_kernel<U, M><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf)
+    if (p.entries == 2) PDB_SELL(2, 1);
+    else if (p.entries == 4) PDB_SELL(4, 1);
+    else if (p.entries == 16) PDB_SELL(16, 1);
+    else if (minb == 5) PDB_SELL(8, 5);
+    else if (minb == 6) PDB_SELL(8, 6);
+    else PDB_SELL(8, 1);
+#undef PDB_SELL
     return;
   }
   if (p.version == 8 && p.blk_start && p.lcol) {
@@ -1612,16 +1684,17 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
     build_frag_kernel<<<grid_for(total, kBlock), kBlock, 0, s>>>(total, ps, (ps + 7) / 8, (ps + 3) / 4, inv_cm, frag);
 }
 
-void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
-                      double* sols, cudaStream_t s) {
+template <bool Z>
+static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
+                        const int32_t* idx, const double* frag, const double* r, const double* in_scale, double* out,
+                        cudaStream_t s) {
   if (ntiles <= 0) return;
   const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
-#define PDB_DMMA_CASE(M, K)                                                                                  \
-  if (mt == M && ks == K) {                                                                                  \
-    patch_apply_dmma_kernel<M, K><<<(unsigned)ntiles, M * 32, 0, s>>>(ps, tile_entry, tile_start, tile_idx, \
-                                                                      frag, r, in_scale, sols);             \
-    return;                                                                                                  \
+#define PDB_DMMA_CASE(M, K)                                                                                    \
+  if (mt == M && ks == K) {                                                                                    \
+    patch_apply_dmma_kernel<M, K, Z><<<(unsigned)ntiles, M * 32, 0, s>>>(ps, n, tile_entry, tile_start, idx,  \
+                                                                         frag, r, in_scale, out);             \
+    return;                                                                                                    \
   }
   PDB_DMMA_CASE(1, 1)
   PDB_DMMA_CASE(1, 2)
@@ -1632,6 +1705,35 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
   PDB_DMMA_CASE(4, 7)
   PDB_DMMA_CASE(4, 8)
 #undef PDB_DMMA_CASE
+}
+
+void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
+                      double* sols, cudaStream_t s) {
+  launch_dmma<false>(ntiles, ps, 0, tile_entry, tile_start, tile_idx, frag, r, in_scale, sols, s);
+}
+
+void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
+                        const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
+                        cudaStream_t s) {
+  launch_dmma<true>(ntiles, ps, n, tile_entry, tile_start, zfwd, frag, r, in_scale, Z, s);
+}
+
+void build_zmap(int64_t n, const int32_t* inv_ptr, const int32_t* inv, int32_t* zfwd, uint8_t* zcnt, cudaStream_t s) {
+  if (n > 0) build_zmap_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, inv_ptr, inv, zfwd, zcnt);
+}
+
+void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
+               double* z_out, double* x_out, cudaStream_t s) {
+  if (n <= 0) return;
+  const unsigned g = grid_for(n, kBlock);
+  switch (maxc) {
+    case 1: scatter_z_kernel<1><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
+    case 2: scatter_z_kernel<2><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
+    case 3:
+    case 4: scatter_z_kernel<4><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
+    default: scatter_z_kernel<8><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
+  }
 }
 
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,

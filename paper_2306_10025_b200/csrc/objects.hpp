@@ -111,6 +111,12 @@ struct pdb_precond_s {
   pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
   int ntiles = 0, max_tile = 0;
   pdb::DevBuf<double> frag;  // inverses in DMMA A-fragment order (tensor-core grouped apply), when allocated
+  // DoF-major solution slots (single-GPU compressed path with DMMA tiles):
+  // zfwd[tile-order slot] = (c << 28) | dof, c = rank of the patch among the
+  // DoF's patches (ascending k); the apply writes solution values straight to
+  // Z[c * n + dof] and the scatter streams Z with zcnt[dof] live slots
+  pdb::DevBuf<int32_t> zfwd;
+  pdb::DevBuf<uint8_t> zcnt;
   pdb::DevBuf<int32_t> inv_pad;  // slot-major padded inverse map (maxc_pad slots), when maxc_pad > 0
   int maxc_pad = 0;
   pdb::DevBuf<int32_t> inv_ptr;
