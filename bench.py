@@ -299,10 +299,10 @@ def run_ours(args):
                   "pair_evals": work["pair_evals"], "power_iters": work["power_iters"], "lu": work["lu_count"],
                   "generator_s": t_gen},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "residual_kernel (r = b - A x)",
+                     "traffic": traffic, "kernel": "residual_sell_kernel<8> (r = b - A x over the SELL-C-sigma copy)",
                      "algorithmic_bytes_per_launch": rb, "ms_per_launch": phase[0], "peak_source": peak_src},
         "sweep_roofline": {"bytes_per_sweep": sb, "achieved_gbs": sweep_gbs, "frac": sweep_gbs / hbm,
-                           "kernel_ms": {"residual": phase[0], "patch_solve": phase[1], "scatter_update": phase[2]}},
+                           "kernel_ms": {"residual": phase[0], "patch_apply_dmma": phase[1], "scatter_update": phase[2]}},
         "e2e": e2e,
         "gpu_launches": 3 * args.steps,
         "clocks": clocks,

@@ -24,13 +24,9 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "v5": {"PDB_SPMV_VERSION": "5", "PDB_SELL_PF": "0"},
-    "v9_pf0": {"PDB_SPMV_VERSION": "9", "PDB_SELL_PF": "0"},
-    "v9_pf1": {"PDB_SPMV_VERSION": "9", "PDB_SELL_PF": "1"},
-    "v9_pf1_m5": {"PDB_SPMV_VERSION": "9", "PDB_SELL_PF": "1", "PDB_SELL_MINB": "5"},
-    "v9_pf1_m6": {"PDB_SPMV_VERSION": "9", "PDB_SELL_PF": "1", "PDB_SELL_MINB": "6"},
-    "v9_u4_pf1": {"PDB_SPMV_VERSION": "9", "PDB_SPMV_PER": "4", "PDB_SELL_PF": "1"},
-    "v9_pf1_nodmma": {"PDB_SPMV_VERSION": "9", "PDB_SELL_PF": "1", "PDB_DMMA": "0"},
+    "v9": {},
+    "v9_nodmma": {"PDB_DMMA": "0"},
+    "v9_zmap": {"PDB_ZMAP": "1"},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
