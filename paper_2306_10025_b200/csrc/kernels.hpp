@@ -70,25 +70,27 @@ void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const doubl
                         const double* x_in, double* z_out, double* x_out, cudaStream_t s);
 int grouped_tile(int ps);  // patches per grouped-apply tile
 // Cluster-grouped apply: tile t covers tile-order slots [tile_start[t], tile_start[t+1]) sharing entry
-// tile_entry[t]; tile_idx holds the patch DoF lists in tile order and sols is written in tile order.
+// tile_entry[t]; tile_idx holds the patch DoF lists in tile order.  Solutions are written in patch
+// order (sols[order[slot] * ps + i]), so a DoF's contributions sit next to its neighbours' in memory.
 void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                         const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
-                         double* sols, int max_tile, cudaStream_t s);
+                         const int32_t* tile_idx, const int32_t* order, const double* Binv, const double* r,
+                         const double* in_scale, double* sols, int max_tile, cudaStream_t s);
 // Tensor-core grouped apply (FP64 mma.sync m8n8k4, ps <= 32, tiles <= 32 patches): sols_tile =
 // B_f^{-1} [r_k1 .. r_k32] with each inverse pre-arranged in A-fragment order by build_frag_inverses.
 bool dmma_apply_supported(int ps);
 int64_t frag_len(int ps);  // doubles per entry in fragment order
 void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag, cudaStream_t s);
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
-                      double* sols, cudaStream_t s);
+                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
+                      const double* in_scale, double* sols, cudaStream_t s);
 // DoF-major variant: the tile gathers r through zfwd & (2^28-1) and stores each
 // solution value at Z[(zfwd >> 28) * n + (zfwd & (2^28-1))].
 void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
                         const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
                         cudaStream_t s);
-// zfwd / zcnt from the (tile-order) inverse map
-void build_zmap(int64_t n, const int32_t* inv_ptr, const int32_t* inv, int32_t* zfwd, uint8_t* zcnt, cudaStream_t s);
+// zfwd (tile order, via slot_of) / zcnt from the patch-order inverse map
+void build_zmap(int64_t n, int ps, const int32_t* inv_ptr, const int32_t* inv, const int32_t* slot_of, int32_t* zfwd,
+                uint8_t* zcnt, cudaStream_t s);
 // x_out = x_in + omega * w(count) * sum_{c < zcnt[i]} Z[c*n + i]  (and/or z_out)
 void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
                double* z_out, double* x_out, cudaStream_t s);

@@ -24,6 +24,37 @@ namespace {
 
 constexpr int kBlock = 256;
 
+// Programmatic dependent launch (sm_90+).  The three sweep kernels are
+// launched with programmatic stream serialization: each one issues the loads
+// that do not depend on its predecessor (matrix values/columns, tile indices,
+// inverse-map slots, x) before griddepcontrol.wait, which returns once the
+// predecessor grid has completed and its writes are visible.  Each kernel
+// lets its dependent launch only after its own wait (so completion stays
+// transitive along the stream); the dependent's CTAs then occupy SMs freed by
+// the primary's last wave.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled() {
+  const char* e = getenv("PDB_PDL");
+  return !(e && e[0] == '0');
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Streaming loads that bypass L1 allocation (the CSR arrays are read once per
 // sweep), keeping L1 for the reused x gathers.
 __device__ __forceinline__ double ld_stream(const double* p) {
@@ -794,6 +825,10 @@ __global__ void __launch_bounds__(256, MINB) residual_sell_kernel(int64_t nslice
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
   double sq = 0.0;
+  if (sl >= nslices) {
+    grid_dep_wait();
+    grid_dep_trigger();
+  }
   if (sl < nslices) {
     const int2 rl = __ldg(srow + sl * 32 + lane);
     const int len = rl.y;
@@ -803,6 +838,15 @@ __global__ void __launch_bounds__(256, MINB) residual_sell_kernel(int64_t nslice
     const int32_t* cp = scol + o + lane;
     const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
     double acc = 0.0;
+    int32_t c[U];
+    double v[U];
+    // first step group: independent of the predecessor (the scatter writing x)
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = u < len ? __ldcs(cp + (int64_t)u * 32) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = u < len ? __ldcs(vp + (int64_t)u * 32) : 0.0;
+    grid_dep_wait();
+    grid_dep_trigger();
     for (int j = 0; j < L; j += U) {
       // pull the slice's next columns/values towards L2 (bulk prefetch, no
       // registers held) so the loads pf iterations ahead find them there
@@ -816,12 +860,13 @@ __global__ void __launch_bounds__(256, MINB) residual_sell_kernel(int64_t nslice
                        "r"((unsigned)(cnt * 4)));
         }
       }
-      int32_t c[U];
-      double v[U], xv[U];
+      if (j > 0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
+        for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
 #pragma unroll
-      for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
+        for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
+      }
+      double xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) xv[u] = j + u < len ? __ldg(x + c[u]) : 0.0;
 #pragma unroll
@@ -972,7 +1017,8 @@ __global__ void patch_apply_inv_kernel(int64_t np, int ps, int ppb, const int32_
 // tile-order slots.
 __global__ void patch_apply_grouped_kernel(int ps, const int32_t* __restrict__ tile_entry,
                                            const int32_t* __restrict__ tile_start,
-                                           const int32_t* __restrict__ tile_idx, const double* __restrict__ Binv,
+                                           const int32_t* __restrict__ tile_idx, const int32_t* __restrict__ order,
+                                           const double* __restrict__ Binv,
                                            const double* __restrict__ r, const double* __restrict__ in_scale,
                                            double* __restrict__ sols) {
   extern __shared__ double sm[];
@@ -1009,7 +1055,7 @@ __global__ void patch_apply_grouped_kernel(int ps, const int32_t* __restrict__ t
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int p = g + q * NG;
-    if (p < cnt) sols[(int64_t)(s0 + p) * ps + i] = acc[q];
+    if (p < cnt) sols[(int64_t)__ldg(order + s0 + p) * ps + i] = acc[q];
   }
 }
 
@@ -1043,6 +1089,7 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
                                                                    const int32_t* __restrict__ tile_entry,
                                                                    const int32_t* __restrict__ tile_start,
                                                                    const int32_t* __restrict__ idx,
+                                                                   const int32_t* __restrict__ order,
                                                                    const double* __restrict__ frag,
                                                                    const double* __restrict__ r,
                                                                    const double* __restrict__ in_scale,
@@ -1052,9 +1099,11 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
   constexpr int ITER = (TOT + NTH - 1) / NTH;
   __shared__ double rk[TOT];
   __shared__ int32_t fk[Z ? TOT : 1];
+  __shared__ int32_t ko[kDmmaTile];  // patch index of each tile column (output in patch order)
   const int t = blockIdx.x;
   const int f = __ldg(tile_entry + t);
   const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+  if (!Z && threadIdx.x < cnt) ko[threadIdx.x] = __ldg(order + s0 + threadIdx.x);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[KS];
   const double* fa = frag + ((int64_t)f * MT + w) * (KS * 32) + lane;
@@ -1068,6 +1117,8 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
     const int e = threadIdx.x + it * NTH;
     gi[it] = e < live ? __ldg(ti + e) : -1;
   }
+  grid_dep_wait();  // r is the residual kernel's output
+  grid_dep_trigger();
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     const int e = threadIdx.x + it * NTH;
@@ -1102,21 +1153,25 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
             out[(int64_t)(z1 >> 28) * n + (z1 & kDofMask)] = c1;
           }
         } else {
-          if (p0 < cnt) out[(int64_t)(s0 + p0) * ps + row] = c0;
-          if (p0 + 1 < cnt) out[(int64_t)(s0 + p0 + 1) * ps + row] = c1;
+          if (p0 < cnt) out[(int64_t)ko[p0] * ps + row] = c0;
+          if (p0 + 1 < cnt) out[(int64_t)ko[p0 + 1] * ps + row] = c1;
         }
       }
     }
   }
 }
 
-__global__ void build_zmap_kernel(int64_t n, const int32_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv,
+__global__ void build_zmap_kernel(int64_t n, int ps, const int32_t* __restrict__ inv_ptr,
+                                  const int32_t* __restrict__ inv, const int32_t* __restrict__ slot_of,
                                   int32_t* __restrict__ zfwd, uint8_t* __restrict__ zcnt) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= n) return;
   const int32_t lo = inv_ptr[d], hi = inv_ptr[d + 1];
   zcnt[d] = (uint8_t)(hi - lo);
-  for (int32_t q = lo; q < hi; ++q) zfwd[inv[q]] = ((q - lo) << 28) | (int32_t)d;
+  for (int32_t q = lo; q < hi; ++q) {
+    const int32_t e = inv[q];  // k * ps + l
+    zfwd[(int64_t)slot_of[e / ps] * ps + e % ps] = ((q - lo) << 28) | (int32_t)d;
+  }
 }
 
 // Scatter over DoF-major slots: loads only the zcnt[i] live slots of DoF i
@@ -1212,17 +1267,18 @@ __global__ void scatter_update_pad_kernel(int64_t n, const int32_t* __restrict__
   // together -- the kernel is latency-bound on the idx -> sols chain.
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kScatterU + threadIdx.x;
   int32_t e[kScatterU][MAXC];
+  double v[kScatterU][MAXC], xi[kScatterU];
 #pragma unroll
   for (int u = 0; u < kScatterU; ++u) {
     const int64_t i = i0 + (int64_t)u * blockDim.x;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) e[u][c] = i < n ? __ldcs(inv_pad + (int64_t)c * n + i) : -1;
+    xi[u] = (x_out && i < n) ? __ldcs(x_in + i) : 0.0;
   }
-  double v[kScatterU][MAXC], xi[kScatterU];
+  grid_dep_wait();  // sols is the apply kernel's output
+  grid_dep_trigger();
 #pragma unroll
   for (int u = 0; u < kScatterU; ++u) {
-    const int64_t i = i0 + (int64_t)u * blockDim.x;
-    xi[u] = (x_out && i < n) ? __ldcs(x_in + i) : 0.0;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) v[u][c] = e[u][c] >= 0 ? __ldg(sols + e[u][c]) : 0.0;
   }
@@ -1541,8 +1597,9 @@ static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, c
     const int pf = pfe ? atoi(pfe) : 1;
     const char* mbe = getenv("PDB_SELL_MINB");
     const int minb = mbe ? atoi(mbe) : 0;
-#define PDB_SELL(U, M) \
-  residual_sell_kernel<U, M><<<g, 256, 0, s>>>(p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf)
+#define PDB_SELL(U, M)                                                                                             \
+  launch_pdl(residual_sell_kernel<U, M>, dim3(g), dim3(256), 0, s, p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, \
+             x, b, r, sumsq, negate, pf)
     if (p.entries == 2) PDB_SELL(2, 1);
     else if (p.entries == 4) PDB_SELL(4, 1);
     else if (p.entries == 16) PDB_SELL(16, 1);
@@ -1663,15 +1720,15 @@ int grouped_tile(int ps) {
 }
 
 void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                         const int32_t* tile_idx, const double* Binv, const double* r, const double* in_scale,
-                         double* sols, int max_tile, cudaStream_t s) {
+                         const int32_t* tile_idx, const int32_t* order, const double* Binv, const double* r,
+                         const double* in_scale, double* sols, int max_tile, cudaStream_t s) {
   if (ntiles <= 0) return;
   const size_t smem = ((size_t)ps * ps + (size_t)max_tile * ps) * sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(patch_apply_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = ps >= 256 ? ps : (256 / ps) * ps;
-  patch_apply_grouped_kernel<<<(unsigned)ntiles, threads, smem, s>>>(ps, tile_entry, tile_start, tile_idx, Binv, r,
-                                                                     in_scale, sols);
+  patch_apply_grouped_kernel<<<(unsigned)ntiles, threads, smem, s>>>(ps, tile_entry, tile_start, tile_idx, order,
+                                                                     Binv, r, in_scale, sols);
 }
 
 bool dmma_apply_supported(int ps) { return ps >= 1 && ps <= 32 && grouped_tile(ps) <= kDmmaTile; }
@@ -1686,14 +1743,14 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
 
 template <bool Z>
 static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
-                        const int32_t* idx, const double* frag, const double* r, const double* in_scale, double* out,
+                        const int32_t* idx, const int32_t* order, const double* frag, const double* r, const double* in_scale, double* out,
                         cudaStream_t s) {
   if (ntiles <= 0) return;
   const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
 #define PDB_DMMA_CASE(M, K)                                                                                    \
   if (mt == M && ks == K) {                                                                                    \
-    patch_apply_dmma_kernel<M, K, Z><<<(unsigned)ntiles, M * 32, 0, s>>>(ps, n, tile_entry, tile_start, idx,  \
-                                                                         frag, r, in_scale, out);             \
+    launch_pdl(patch_apply_dmma_kernel<M, K, Z>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, n, tile_entry, \
+               tile_start, idx, order, frag, r, in_scale, out);                                               \
     return;                                                                                                    \
   }
   PDB_DMMA_CASE(1, 1)
@@ -1708,19 +1765,20 @@ static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry
 }
 
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const double* frag, const double* r, const double* in_scale,
-                      double* sols, cudaStream_t s) {
-  launch_dmma<false>(ntiles, ps, 0, tile_entry, tile_start, tile_idx, frag, r, in_scale, sols, s);
+                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
+                      const double* in_scale, double* sols, cudaStream_t s) {
+  launch_dmma<false>(ntiles, ps, 0, tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols, s);
 }
 
 void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
                         const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
                         cudaStream_t s) {
-  launch_dmma<true>(ntiles, ps, n, tile_entry, tile_start, zfwd, frag, r, in_scale, Z, s);
+  launch_dmma<true>(ntiles, ps, n, tile_entry, tile_start, zfwd, nullptr, frag, r, in_scale, Z, s);
 }
 
-void build_zmap(int64_t n, const int32_t* inv_ptr, const int32_t* inv, int32_t* zfwd, uint8_t* zcnt, cudaStream_t s) {
-  if (n > 0) build_zmap_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, inv_ptr, inv, zfwd, zcnt);
+void build_zmap(int64_t n, int ps, const int32_t* inv_ptr, const int32_t* inv, const int32_t* slot_of, int32_t* zfwd,
+                uint8_t* zcnt, cudaStream_t s) {
+  if (n > 0) build_zmap_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, ps, inv_ptr, inv, slot_of, zfwd, zcnt);
 }
 
 void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
@@ -1765,11 +1823,11 @@ void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const doubl
   if (n <= 0) return;
   const unsigned g = grid_for(n, kBlock * kScatterU);
   switch (maxc) {
-    case 1: scatter_update_pad_kernel<1><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
-    case 2: scatter_update_pad_kernel<2><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 1: launch_pdl(scatter_update_pad_kernel<1>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 2: launch_pdl(scatter_update_pad_kernel<2>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
     case 3:
-    case 4: scatter_update_pad_kernel<4><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
-    default: scatter_update_pad_kernel<8><<<g, kBlock, 0, s>>>(n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 4: launch_pdl(scatter_update_pad_kernel<4>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    default: launch_pdl(scatter_update_pad_kernel<8>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
   }
 }
 

@@ -21,8 +21,8 @@ bool use_dmma_apply(int ps);
 namespace {
 
 // DoF -> solution-slot inverse map.  Entries are first k*ps + l sorted by k
-// (the reference's scatter order, precond.cpp:81-86), then, when solutions
-// are stored in tile order, remapped to slot_of[k]*ps + l.
+// (the reference's scatter order, precond.cpp:81-86); remapped to
+// slot_of[k]*ps + l only for callers that store solutions in tile order.
 void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = nullptr) {
   const int64_t n = pc.n;
   pc.inv_ptr.alloc(static_cast<size_t>(n + 1));
@@ -167,7 +167,7 @@ bool use_dmma_apply(int ps) {
 }
 
 
-// Solution scratch: tile-order sols, or the DoF-major slots Z (maxc_pad x n).
+// Solution scratch: patch-order sols, or the DoF-major slots Z (maxc_pad x n).
 int64_t sols_len(const pdb_precond_s& pc) {
   int64_t len = std::max<int64_t>(pc.np * pc.ps, 1);
   if (pc.zfwd.get()) len = std::max<int64_t>(len, pc.maxc_pad * pc.n);
@@ -182,10 +182,10 @@ void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scal
                           pc.zfwd.get(), pc.frag.get(), r, in_scale, sols, s);
   else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0 && pc.frag.get() && use_dmma_apply(static_cast<int>(pc.ps)))
     k::patch_apply_dmma(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
-                        pc.tile_idx.get(), pc.frag.get(), r, in_scale, sols, s);
+                        pc.tile_idx.get(), pc.order.get(), pc.frag.get(), r, in_scale, sols, s);
   else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
     k::patch_apply_grouped(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
-                           pc.tile_idx.get(), pc.factors.get(), r, in_scale, sols, pc.max_tile, s);
+                           pc.tile_idx.get(), pc.order.get(), pc.factors.get(), r, in_scale, sols, pc.max_tile, s);
   else if (pc.lu_apply)
     k::patch_solve(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(), phi, r,
                    in_scale, sols, s);
@@ -248,19 +248,20 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
   pc.phi.alloc(static_cast<size_t>(ps.np));
   PDB_CUDA(cudaMemcpyAsync(pc.phi.get(), db.phi.get(), ps.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   if (!pc.lu_apply && use_grouped_apply(ps.np, db.m)) {
-    build_tiles(pc, phi, s);  // solutions live in tile order ...
-    build_inverse(pc, s, pc.slot_of.get());  // ... and the scatter reads them there
+    build_tiles(pc, phi, s);  // tiles in entry order; solutions stay in patch order
+    build_inverse(pc, s);
     if (use_dmma_apply(static_cast<int>(ps.ps))) {
       pc.frag.alloc(static_cast<size_t>(db.m * k::frag_len(static_cast<int>(ps.ps))));
       k::build_frag_inverses(db.m, static_cast<int>(ps.ps), pc.factors.get(), pc.frag.get(), s);
       // single-GPU path: solutions go straight to DoF-major slots (a shard's
-      // interface scatter keeps the tile-order solutions and the inverse map)
+      // interface scatter keeps the patch-order solutions and the inverse map)
       // (opt-in, PDB_ZMAP=1: measured slower on config 3, ~1 us faster on config 2)
       const char* zm = getenv("PDB_ZMAP");
       if (zm && std::string(zm) == "1" && check_onto && pc.maxc_pad > 0 && pc.n < (int64_t{1} << 28)) {
         pc.zfwd.alloc(static_cast<size_t>(pc.np * pc.ps));
         pc.zcnt.alloc(static_cast<size_t>(pc.n));
-        k::build_zmap(pc.n, pc.inv_ptr.get(), pc.inv.get(), pc.zfwd.get(), pc.zcnt.get(), s);
+        k::build_zmap(pc.n, static_cast<int>(pc.ps), pc.inv_ptr.get(), pc.inv.get(), pc.slot_of.get(), pc.zfwd.get(),
+                      pc.zcnt.get(), s);
       }
     }
   } else {

@@ -24,9 +24,11 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "v9": {},
-    "v9_nodmma": {"PDB_DMMA": "0"},
-    "v9_zmap": {"PDB_ZMAP": "1"},
+    "pdl": {},
+    "nopdl": {"PDB_PDL": "0"},
+    "pdl_m5": {"PDB_SELL_MINB": "5"},
+    "pdl_u4": {"PDB_SPMV_PER": "4"},
+    "nopdl_m5": {"PDB_PDL": "0", "PDB_SELL_MINB": "5"},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
@@ -41,9 +43,16 @@ for rnd in range(3):
         os.environ.update(env)
         P.relax_profile(pc, A, b.data_ptr(), x.data_ptr(), 20, stream=s)
         ms = P.relax_profile(pc, A, b.data_ptr(), x.data_ptr(), 200, stream=s)
-        res[name].append([round(v * 1e3, 1) for v in ms])
+        # whole sweeps back to back (kernels may overlap through PDL)
+        pc.relax_device(A, b.data_ptr(), x.data_ptr(), 20, stream=s)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pc.relax_device(A, b.data_ptr(), x.data_ptr(), 200, stream=s)
+        e1.record()
+        torch.cuda.synchronize()
+        res[name].append([round(v * 1e3, 1) for v in ms] + [round(e0.elapsed_time(e1) / 200 * 1e3, 1)])
 n, nnz = prob.ndofs, prob.nnz
 rb = 12 * nnz + 4 * (n + 1) + 24 * n
 for name, r in res.items():
     best = min(x[0] for x in r)
-    print(f"{name:12s} residual us {[x[0] for x in r]}  best {best} -> {rb / best / 1e3:.0f} GB/s; patch {[x[1] for x in r]} scatter {[x[2] for x in r]}")
+    print(f"{name:12s} residual us {[x[0] for x in r]}  best {best} -> {rb / best / 1e3:.0f} GB/s; patch {[x[1] for x in r]} scatter {[x[2] for x in r]} SWEEP {[x[3] for x in r]}")
