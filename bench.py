@@ -264,8 +264,24 @@ def run_ours(args):
         t = torch.tensor([te], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         te = float(t.item())
+    # host-link floor: the same bytes as plain pinned copies (no compute)
+    hb = torch.empty(h2d // 8 // max(world, 1), dtype=torch.float64).pin_memory()
+    db_ = torch.empty_like(hb, device="cuda")
+    ob = torch.empty(d2h // 8 // max(world, 1), dtype=torch.float64).pin_memory()
+    od = torch.empty_like(ob, device="cuda")
+    for _ in range(3):
+        db_.copy_(hb, non_blocking=True)
+        ob.copy_(od, non_blocking=True)
+    torch.cuda.synchronize()
+    tl = time.perf_counter()
+    for _ in range(20):
+        db_.copy_(hb, non_blocking=True)
+        ob.copy_(od, non_blocking=True)
+        torch.cuda.synchronize()
+    tl = (time.perf_counter() - tl) / 20
     e2e = {"value": n * e2e_steps / te, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "steps": e2e_steps,
+           "steps": e2e_steps, "host_link_floor": {"value": n / tl, "ms_per_step": tl * 1e3,
+                                                   "note": "same H2D+D2H bytes as bare pinned copies, no compute"},
            "call": "pdb_relax (1 sweep, pinned host b/x)" if shard is None else
                    "pdb_shard_relax_device (1 sweep) with pinned host b/x copies per rank"}
 

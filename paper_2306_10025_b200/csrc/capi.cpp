@@ -482,18 +482,7 @@ PDB_API pdb_status pdb_relax(pdb_matrix m, pdb_precond pc, const double* b, doub
   return guarded([&] {
     require_device();
     require(sweeps >= 0, Errc::invalid_argument, "sweeps must be >= 0");
-    cudaStream_t s = default_stream();
-    const size_t n = static_cast<size_t>(m->a.n);
-    Scratch<double> db(std::max<size_t>(n, 1), s), dx(std::max<size_t>(n, 1), s);
-    Scratch<double> dh(static_cast<size_t>(sweeps + 1), s);
-    PDB_CUDA(cudaMemcpyAsync(db.get(), b, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    PDB_CUDA(cudaMemcpyAsync(dx.get(), x, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    relax_device(m->a, *pc, db.get(), dx.get(), sweeps, history ? dh.get() : nullptr, s);
-    PDB_CUDA(cudaMemcpyAsync(x, dx.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (history)
-      PDB_CUDA(cudaMemcpyAsync(history, dh.get(), static_cast<size_t>(sweeps + 1) * sizeof(double),
-                               cudaMemcpyDeviceToHost, s));
-    sync(s);
+    relax_host(m->a, *pc, b, x, sweeps, history, default_stream());
   });
 }
 

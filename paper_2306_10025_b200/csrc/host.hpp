@@ -67,6 +67,8 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
                   double* history, cudaStream_t s);
 // Same sweeps with CUDA events around each kernel: ms_phase[3] = average ms of
 // residual, patch_solve, scatter_update.
+void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, double* x_h, int64_t sweeps,
+                double* history_h, cudaStream_t s);
 void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                    double* ms_phase, cudaStream_t s);
 

@@ -48,6 +48,10 @@ SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, cons
 int stream_nnz();
 std::vector<int32_t> stream_partition(int64_t n, const int64_t* row_ptr, int per);  // per 0: v5 warp partition
 std::vector<int32_t> row_partition(int64_t n, const int64_t* row_ptr, int64_t cap_nnz, int64_t cap_rows);
+// SELL plans only: r = b - A x on slices [s0, s1) (whole sorting windows, i.e. rows
+// [s0 * kSellC, min(s1 * kSellC, n))), plain launch (ordered after events by the caller).
+void residual_slices(const SpmvPlan& plan, int64_t s0, int64_t s1, const double* x, const double* b, double* r,
+                     cudaStream_t s);
 void residual(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
               const double* x, const double* b, double* r, double* block_sumsq, cudaStream_t s);
 void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,

@@ -1674,6 +1674,15 @@ void residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* co
   dispatch_residual(p, n, rp, col, val, x, b, r, block_sumsq, true, s);
 }
 
+void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x, const double* b, double* r,
+                     cudaStream_t s) {
+  if (s1 <= s0 || p.version != 9) return;
+  const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
+  const unsigned g = (unsigned)((s1 - s0 + 7) / 8);
+  residual_sell_kernel<8, 1><<<g, 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x, b, r, nullptr,
+                                               true, 1);
+}
+
 void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
           double* y, cudaStream_t s) {
   dispatch_residual(p, n, rp, col, val, x, nullptr, y, nullptr, false, s);

@@ -297,6 +297,66 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
   PDB_LAUNCH_CHECK();
 }
 
+// pdb_relax with host vectors.  With the SELL residual the first sweep is
+// pipelined against the host link: x is copied first, b follows in chunks of
+// whole sorting windows on a copy stream, and the residual of each chunk
+// starts as soon as its rows of b have landed, so the b transfer hides the
+// residual.  Remaining sweeps run as relax_device; x is copied back at the end.
+void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, double* x_h, int64_t sweeps,
+                double* history_h, cudaStream_t s) {
+  require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
+  const size_t n = static_cast<size_t>(a.n);
+  Scratch<double> db(std::max<size_t>(n, 1), s), dx(std::max<size_t>(n, 1), s);
+  const k::SpmvPlan plan = plan_of(a);
+  const char* e = getenv("PDB_PIPELINE");
+  const bool pipelined = plan.version == 9 && sweeps >= 1 && history_h == nullptr && n > 0 &&
+                         !(e && std::string(e) == "0");
+  if (!pipelined) {
+    Scratch<double> dh(static_cast<size_t>(sweeps + 1), s);
+    PDB_CUDA(cudaMemcpyAsync(db.get(), b_h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    PDB_CUDA(cudaMemcpyAsync(dx.get(), x_h, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    relax_device(a, pc, db.get(), dx.get(), sweeps, history_h ? dh.get() : nullptr, s);
+    PDB_CUDA(cudaMemcpyAsync(x_h, dx.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (history_h)
+      PDB_CUDA(cudaMemcpyAsync(history_h, dh.get(), static_cast<size_t>(sweeps + 1) * sizeof(double),
+                               cudaMemcpyDeviceToHost, s));
+    sync(s);
+    return;
+  }
+  static thread_local cudaStream_t cs = nullptr;
+  if (!cs) PDB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  const int64_t win_slices = k::kSellSigma / k::kSellC;
+  const int64_t nwin = (a.n + k::kSellSigma - 1) / k::kSellSigma;
+  const int64_t chunks = std::min<int64_t>(8, nwin);
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(chunks + 2));
+  for (auto& ee : ev) PDB_CUDA(cudaEventCreateWithFlags(&ee, cudaEventDisableTiming));
+  PDB_CUDA(cudaEventRecord(ev[0], s));  // scratch allocations are ordered on s
+  PDB_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+  PDB_CUDA(cudaMemcpyAsync(dx.get(), x_h, n * sizeof(double), cudaMemcpyHostToDevice, cs));
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t w0 = nwin * c / chunks, w1 = nwin * (c + 1) / chunks;
+    const int64_t r0 = w0 * k::kSellSigma, r1 = std::min<int64_t>(a.n, w1 * k::kSellSigma);
+    PDB_CUDA(cudaMemcpyAsync(db.get() + r0, b_h + r0, static_cast<size_t>(r1 - r0) * sizeof(double),
+                             cudaMemcpyHostToDevice, cs));
+    PDB_CUDA(cudaEventRecord(ev[static_cast<size_t>(c + 1)], cs));
+  }
+  Scratch<double> r(std::max<size_t>(n, 1), s);
+  Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t w0 = nwin * c / chunks, w1 = nwin * (c + 1) / chunks;
+    PDB_CUDA(cudaStreamWaitEvent(s, ev[static_cast<size_t>(c + 1)], 0));
+    k::residual_slices(plan, w0 * win_slices, std::min<int64_t>(plan.nslices, w1 * win_slices), dx.get(), db.get(),
+                       r.get(), s);
+  }
+  patch_stage(pc, r.get(), nullptr, sols.get(), s);
+  scatter_stage(pc, sols.get(), false, dx.get(), nullptr, dx.get(), s);
+  if (sweeps > 1) relax_device(a, pc, db.get(), dx.get(), sweeps - 1, nullptr, s);
+  PDB_CUDA(cudaMemcpyAsync(x_h, dx.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PDB_LAUNCH_CHECK();
+  sync(s);
+  for (auto& ee : ev) cudaEventDestroy(ee);
+}
+
 void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                    double* ms_phase, cudaStream_t s) {
   require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");

@@ -264,3 +264,22 @@ def test_identity_phi_compressed_equals_exact(c1, P):
     pcmp = P.Preconditioner.create(c1.A, c1.ps, db)
     r = np.random.default_rng(5).uniform(-1, 1, c1.A.rows)
     assert np.array_equal(pe.apply(r), pcmp.apply(r))
+
+
+@pytest.mark.parametrize("sweeps", [1, 3])
+def test_pipelined_host_relax_matches_device_path(P, monkeypatch, sweeps):
+    """pdb_relax overlaps the b upload with the chunked residual (8 chunks of
+    whole SELL windows at 64x64 cells); the result must be bitwise the
+    unpipelined path's (same kernels, same row sums)."""
+    prob = P.Problem.generate(2, 64)
+    A = prob.matrix()
+    ps = P.PatchSet.detect(A, 25)
+    db = P.Database.build(A, ps, P.KMEANS_ENTRYWISE, db_size=16)
+    pc = P.Preconditioner.create(A, ps, db, omega=0.9)
+    b = prob.rhs()
+    x0 = np.random.default_rng(2).uniform(-1, 1, A.rows)
+    got, _ = pc.relax(A, b, x0, sweeps, history=False)
+    monkeypatch.setenv("PDB_PIPELINE", "0")
+    want, _ = pc.relax(A, b, x0, sweeps, history=False)
+    assert np.array_equal(got, want)
+    assert not np.array_equal(got, x0)
