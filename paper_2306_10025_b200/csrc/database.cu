@@ -387,6 +387,15 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   Scratch<unsigned long long> iters(1, s);
   PDB_CUDA(cudaMemsetAsync(iters.get(), 0, sizeof(unsigned long long), s));
   DevBuf<double> dist;
+  // interleaved copies for the spectral assignment (PDB_SPECTRAL_IL=0 keeps the plain layout)
+  const char* il_env = getenv("PDB_SPECTRAL_IL");
+  const bool il = variant != Variant::Entrywise && k::spectral_il_supported(ps) && !(il_env && il_env[0] == '0');
+  DevBuf<double> sub_il, lu_il;
+  DevBuf<int32_t> piv_il;
+  if (il) {
+    sub_il.alloc(static_cast<size_t>(k::interleaved_len(n, 32, len)));
+    k::interleave_patches(n, len, sub, sub_il.get(), s);
+  }
   for (int iter = 0; iter < max_iters; ++iter) {
     const int64_t m = db.m;
     PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
@@ -395,7 +404,14 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
                    changed.get(), s);
     } else {
       if (dist.size() < static_cast<size_t>(n * m)) dist.alloc(static_cast<size_t>(n * m));
-      k::spectral_pairs(n, nullptr, m, ps, sub, db.lu.get(), db.piv.get(), dist.get(), iters.get(), s);
+      if (il) {
+        lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
+        piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
+        k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), s);
+        k::spectral_tiled_il(n, m, ps, sub_il.get(), lu_il.get(), piv_il.get(), dist.get(), iters.get(), s);
+      } else {
+        k::spectral_pairs(n, nullptr, m, ps, sub, db.lu.get(), db.piv.get(), dist.get(), iters.get(), s);
+      }
       k::argmin_assign(n, m, dist.get(), d_phi.get(), d_new.get(), d_min.get(), changed.get(), s);
     }
     PDB_LAUNCH_CHECK();

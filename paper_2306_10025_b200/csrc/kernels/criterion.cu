@@ -378,7 +378,13 @@ constexpr int kTileA = 32;  // patches per tile (L1-resident)
 constexpr int kTileE = 8;   // factors per tile (L1-resident, read by broadcast)
 constexpr int kTileThreads = 64;
 
-template <int PS>
+// IL = true: patches and factors come pre-interleaved (interleave_mats):
+// element q of the tile's patch a at A[q * 32 + a], of factor e at
+// L[q * 8 + e], pivot i at P[i * 8 + e].  Lanes of a warp work on different
+// (patch, factor) pairs of one tile, so each load of the interleaved copy is
+// one contiguous 256-byte (patches) / 64-byte (factors) span instead of up to
+// 32 separate cache lines.
+template <int PS, bool IL, int MU = 1>
 __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npat, const int32_t* __restrict__ pid,
                                                                      int64_t ne, const double* __restrict__ mats,
                                                                      const double* __restrict__ lu,
@@ -387,6 +393,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
                                                                      unsigned long long* iters_total) {
   constexpr int LEN = PS * PS;
   constexpr int BD = kTileThreads;
+  constexpr int SA = IL ? kTileA : 1;  // element stride of a patch matrix
+  constexpr int SL = IL ? kTileE : 1;  // element stride of a factor / pivot vector
   extern __shared__ double sm[];
   double* vec = sm;  // 3 * PS * BD: v, w, t
   __shared__ int counter;
@@ -394,8 +402,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   const int64_t a0 = (int64_t)blockIdx.x * kTileA, e0 = (int64_t)blockIdx.y * kTileE;
   const int na = (int)(npat - a0 < kTileA ? npat - a0 : kTileA);
   const int nev = (int)(ne - e0 < kTileE ? ne - e0 : kTileE);
-  const double* LUs = lu + e0 * LEN;
-  const int32_t* Ps = piv + e0 * PS;
+  const double* LUs = IL ? lu + (int64_t)blockIdx.y * LEN * kTileE : lu + e0 * LEN;
+  const int32_t* Ps = IL ? piv + (int64_t)blockIdx.y * PS * kTileE : piv + e0 * PS;
   if (tid == 0) counter = 0;
   __syncthreads();
   double* V = vec + tid;
@@ -417,9 +425,15 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
         pa = p % na;
         pe = p / na;
         const int64_t g = a0 + pa;
-        A = mats + (int64_t)(pid ? pid[g] : g) * LEN;
-        L = LUs + pe * LEN;
-        P = Ps + pe * PS;
+        if (IL) {
+          A = mats + (int64_t)blockIdx.x * LEN * kTileA + pa;
+          L = LUs + pe;
+          P = Ps + pe;
+        } else {
+          A = mats + (int64_t)(pid ? pid[g] : g) * LEN;
+          L = LUs + pe * LEN;
+          P = Ps + pe * PS;
+        }
         it = 0;
         lambda = 0.0;
         // v0_i = 1 + 1e-6 i, normalised by division (dense.cpp:163-165)
@@ -440,20 +454,21 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     // ---- t = B^{-1} v (lu_solve_into, dense.cpp:77-94)
     double T[PS];
 #pragma unroll
-    for (int i = 0; i < PS; ++i) T[i] = V[__ldg(P + i) * BD];
+    for (int i = 0; i < PS; ++i) T[i] = V[__ldg(P + i * SL) * BD];
+    // column-oriented: once T[j] is final every later row takes its j-th
+    // term -- each row still subtracts in ascending j, but the rows' chains
+    // advance together (instruction-level parallelism PS - 1 - j)
 #pragma unroll
-    for (int i = 1; i < PS; ++i) {
-      double s = T[i];
+    for (int j = 0; j < PS - 1; ++j) {
 #pragma unroll
-      for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + i * PS + j), T[j]));
-      T[i] = s;
+      for (int i = j + 1; i < PS; ++i) T[i] = __dsub_rn(T[i], __dmul_rn(__ldg(L + (i * PS + j) * SL), T[j]));
     }
 #pragma unroll
     for (int i = PS - 1; i >= 0; --i) {
       double s = T[i];
 #pragma unroll
-      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + i * PS + j), T[j]));
-      T[i] = __ddiv_rn(s, __ldg(L + i * PS + i));
+      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + (i * PS + j) * SL), T[j]));
+      T[i] = __ddiv_rn(s, __ldg(L + (i * PS + i) * SL));
     }
     // ---- w = v - A t (mat_vec) and s = A^T w (mat_tvec) in one pass over
     // A: row i gives w_i, then immediately its contribution to every s_j
@@ -461,34 +476,33 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     double S[PS];
 #pragma unroll
     for (int j = 0; j < PS; ++j) S[j] = 0.0;
-#pragma unroll 1
+#pragma unroll MU
     for (int i = 0; i < PS; ++i) {
-      const double* Ai = A + i * PS;
+      const double* Ai = A + i * PS * SA;
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < PS; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(Ai + j), T[j]));
+      for (int j = 0; j < PS; ++j) acc = __dadd_rn(acc, __dmul_rn(__ldg(Ai + j * SA), T[j]));
       const double wi = __dsub_rn(V[i * BD], acc);
       W[i * BD] = wi;
 #pragma unroll
-      for (int j = 0; j < PS; ++j) S[j] = __dadd_rn(S[j], __dmul_rn(__ldg(Ai + j), wi));
+      for (int j = 0; j < PS; ++j) S[j] = __dadd_rn(S[j], __dmul_rn(__ldg(Ai + j * SA), wi));
     }
     // ---- t = B^{-T} s (lu_solve_transpose_into, dense.cpp:102-120)
 #pragma unroll
-    for (int i = 0; i < PS; ++i) {
-      double s = S[i];
+    for (int j = 0; j < PS; ++j) {  // column-oriented, as the forward solve above
+      S[j] = __ddiv_rn(S[j], __ldg(L + (j * PS + j) * SL));
 #pragma unroll
-      for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + j * PS + i), S[j]));
-      S[i] = __ddiv_rn(s, __ldg(L + i * PS + i));
+      for (int i = j + 1; i < PS; ++i) S[i] = __dsub_rn(S[i], __dmul_rn(__ldg(L + (j * PS + i) * SL), S[j]));
     }
 #pragma unroll
     for (int i = PS - 2; i >= 0; --i) {
       double s = S[i];
 #pragma unroll
-      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + j * PS + i), S[j]));
+      for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + (j * PS + i) * SL), S[j]));
       S[i] = s;
     }
 #pragma unroll
-    for (int i = 0; i < PS; ++i) Tv[__ldg(P + i) * BD] = S[i];
+    for (int i = 0; i < PS; ++i) Tv[__ldg(P + i * SL) * BD] = S[i];
     // ---- u = w - t, Rayleigh quotient, stopping rules (dense.cpp:170-188)
     double rq = 0.0;
 #pragma unroll
@@ -534,14 +548,39 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   if (iters_total && my_iters) atomicAdd(iters_total, my_iters);
 }
 
-template <int PS>
+template <int PS, bool IL = false, int MU = 1>
 bool launch_spectral_tile(int64_t npat, const int32_t* pid, int64_t ne, const double* mats, const double* lu,
                           const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
   const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
-  cudaFuncSetAttribute(spectral_tile_kernel<PS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(spectral_tile_kernel<PS, IL, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(grid_for(npat, kTileA), (unsigned)((ne + kTileE - 1) / kTileE));
-  spectral_tile_kernel<PS><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters);
+  spectral_tile_kernel<PS, IL, MU><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters);
   return true;
+}
+
+template <int PS>
+void launch_spectral_il(int64_t npat, int64_t ne, const double* mats_il, const double* lu_il, const int32_t* piv_il,
+                        double* d, unsigned long long* iters, cudaStream_t s) {
+  const char* e = getenv("PDB_SPECTRAL_MU");
+  const int mu = e ? atoi(e) : 1;
+  if (mu == 2)
+    launch_spectral_tile<PS, true, 2>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s);
+  else if (mu == 5)
+    launch_spectral_tile<PS, true, 5>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s);
+  else
+    launch_spectral_tile<PS, true, 1>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s);
+}
+
+// dst[((g * len) + q) * width + a] = src[(g * width + a) * len + q]; zero past `count` items
+template <typename T>
+__global__ void interleave_kernel(int64_t total, int64_t count, int width, int64_t len, const T* __restrict__ src,
+                                  T* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int a = (int)(e % width);
+  const int64_t q = (e / width) % len, g = e / (width * len);
+  const int64_t item = g * width + a;
+  dst[e] = item < count ? src[item * len + q] : T(0);
 }
 
 bool spectral_tiled(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
@@ -638,6 +677,35 @@ __global__ void cluster_mean_kernel(int64_t m, int len, const int32_t* __restric
 }
 
 }  // namespace
+
+bool spectral_il_supported(int ps) { return ps == 9 || ps == 22 || ps == 25 || ps == 27; }
+
+int64_t interleaved_len(int64_t count, int width, int64_t len) { return (count + width - 1) / width * width * len; }
+
+void interleave_patches(int64_t count, int64_t len, const double* src, double* dst, cudaStream_t s) {
+  const int64_t total = interleaved_len(count, kTileA, len);
+  if (total > 0) interleave_kernel<double><<<grid_for(total, 256), 256, 0, s>>>(total, count, kTileA, len, src, dst);
+}
+
+void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* piv, double* lu_il, int32_t* piv_il,
+                        cudaStream_t s) {
+  const int64_t len = (int64_t)ps * ps;
+  const int64_t t1 = interleaved_len(count, kTileE, len), t2 = interleaved_len(count, kTileE, ps);
+  if (t1 > 0) interleave_kernel<double><<<grid_for(t1, 256), 256, 0, s>>>(t1, count, kTileE, len, lu, lu_il);
+  if (t2 > 0) interleave_kernel<int32_t><<<grid_for(t2, 256), 256, 0, s>>>(t2, count, kTileE, ps, piv, piv_il);
+}
+
+void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
+                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s) {
+  switch (ps) {
+    case 9: launch_spectral_il<9>(npat, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 22: launch_spectral_il<22>(npat, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 25: launch_spectral_il<25>(npat, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 27: launch_spectral_il<27>(npat, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    default: break;
+  }
+}
+
 
 void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,
               const double* reps, double* d, cudaStream_t s) {
