@@ -166,24 +166,27 @@ PDB_API pdb_status pdb_matrix_spmv_device(pdb_matrix m, const double* d_x, doubl
 /* Seeded synthetic problem generator for the BASELINE configurations
  * (DESIGN.md "Inputs").  Host-only: works without a GPU. */
 typedef struct pdb_gen_options {
-  int physics;         /* 0 = scalar diffusion -div(rho grad u) */
-  int dim;             /* 2 or 3 */
-  int degree;          /* Lagrange degree p >= 1 */
+  int physics;         /* 0 = scalar diffusion -div(rho grad u); 1 = Stokes Q_p-Q_{p-1} (2D Taylor-Hood,
+                          symmetric-gradient viscous term, no pressure-pressure block); 2 = linear elasticity */
+  int dim;             /* 2 or 3 (Stokes: 2) */
+  int degree;          /* Lagrange degree p >= 1 (velocity / displacement; Stokes pressure is p-1 >= 1) */
   int bc_mode;         /* 0 = Dirichlet row replacement, no column elimination (ref fem.cpp:323-342) */
   int64_t cells;       /* cells per axis */
   double jitter;       /* interior vertices moved by U(-jitter*h, +jitter*h) per coordinate */
   uint64_t seed;
-  int coeff_kind;      /* 0 = constant coeff_value; 1 = random blocks of block_cells^dim cells */
+  int coeff_kind;      /* 0 = constant coeff_value; 1 = random blocks of block_cells^dim cells from levels[];
+                          2 = lognormal per cell, exp(coeff_value * N(0,1)) */
   int n_levels;        /* number of entries of levels[] used by coeff_kind 1 */
   double coeff_value;
   int64_t block_cells;
   double levels[8];
   int threads;         /* host threads for assembly (0 = all) */
   int reserved;
+  double poisson_ratio; /* physics 2: nu (Lame lambda = E nu / ((1+nu)(1-2nu)), mu = E / (2(1+nu))) */
 } pdb_gen_options;
 
 PDB_API void pdb_gen_options_init(pdb_gen_options* opts);
-/* Presets for BASELINE.json configs 1..3 at a given cells-per-axis (0 = the config's own size). */
+/* Presets for BASELINE.json configs 1..5 at a given cells-per-axis (0 = the config's own size). */
 PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* opts);
 PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* opts, pdb_problem* out);
 PDB_API int64_t pdb_problem_nnz(pdb_problem p);

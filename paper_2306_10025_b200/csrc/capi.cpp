@@ -251,11 +251,13 @@ PDB_API void pdb_gen_options_init(pdb_gen_options* o) {
   o->n_levels = 0;
   o->block_cells = 1;
   o->threads = 0;
+  o->poisson_ratio = 0.3;
 }
 
 // BASELINE.json configs: 1 = 2D Q2 32^2 jitter 0.1;
 // 2 = 2D Q4 256^2 jitter 0.05, rho on 8x8-cell blocks from {1,10,100,1000};
-// 3 = 3D Q2 64^3 jitter 0.1.
+// 3 = 3D Q2 64^3 jitter 0.1; 4 = 2D Stokes Q2-Q1 512^2, mu lognormal(0,1)
+// per cell; 5 = 3D elasticity Q3 96^3, E from {1,100} on 4^3-cell blocks, nu 0.3.
 PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* o) {
   if (o == nullptr) return arg_error("null argument");
   pdb_gen_options_init(o);
@@ -271,8 +273,16 @@ PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_opt
     case 3:
       o->dim = 3, o->degree = 2, o->cells = 64, o->jitter = 0.1;
       break;
+    case 4:
+      o->physics = 1, o->dim = 2, o->degree = 2, o->cells = 512, o->coeff_kind = 2, o->coeff_value = 1.0;
+      break;
+    case 5:
+      o->physics = 2, o->dim = 3, o->degree = 3, o->cells = 96, o->coeff_kind = 1, o->block_cells = 4,
+      o->n_levels = 2, o->poisson_ratio = 0.3;
+      o->levels[0] = 1.0, o->levels[1] = 100.0;
+      break;
     default:
-      return arg_error("config must be 1, 2 or 3 (configs 4-5 need Stokes / elasticity generators)");
+      return arg_error("config must be 1..5");
   }
   if (cells > 0) o->cells = cells;
   return PDB_OK;
@@ -281,10 +291,14 @@ PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_opt
 PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* o, pdb_problem* out) {
   if (o == nullptr || out == nullptr) return arg_error("null argument");
   return guarded([&] {
-    require(o->physics == 0, Errc::invalid_argument, "only scalar diffusion (physics 0) is generated in this build");
+    require(o->physics >= 0 && o->physics <= 2, Errc::invalid_argument,
+            "physics must be 0 (diffusion), 1 (Stokes) or 2 (elasticity)");
     require(o->bc_mode == 0, Errc::invalid_argument, "only Dirichlet row replacement (bc_mode 0) is supported");
     auto p = std::make_unique<pdb_problem_s>();
-    generate_scalar(*o, *p);
+    if (o->physics == 0)
+      generate_scalar(*o, *p);
+    else
+      generate_system(*o, *p);
     *out = p.release();
   });
 }

@@ -25,6 +25,8 @@ void write_matrix_market_host(const HostCsr& a, const std::string& path);
 
 // generator.cpp
 void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out);
+// physics 1 (Stokes Q_p-Q_{p-1}, 2D) and 2 (linear elasticity): node-major vector DoFs
+void generate_system(const pdb_gen_options& o, pdb_problem_s& out);
 
 // patchset.cpp
 void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStream_t s);

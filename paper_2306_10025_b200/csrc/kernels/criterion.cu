@@ -319,19 +319,28 @@ __device__ double spectral_dev(int n, const double* __restrict__ A, const double
 
 // Block = BD patches x one factor (grid.y); factor staged in shared memory
 // and broadcast, patch matrices streamed per thread.
+// stage = false (large patches whose factor does not fit next to the vectors):
+// the factor is read from global memory (L2-resident, shared by the block).
 __global__ void spectral_pairs_kernel(int64_t npat, const int32_t* __restrict__ pid, int64_t ne, int ps,
                                       const double* __restrict__ mats, const double* __restrict__ lu,
                                       const int32_t* __restrict__ piv, double* __restrict__ d,
-                                      unsigned long long* iters_total) {
+                                      unsigned long long* iters_total, bool stage) {
   extern __shared__ double sm[];
   const int BD = blockDim.x;
   const int64_t len = (int64_t)ps * ps;
-  double* LU = sm;
-  int32_t* P = reinterpret_cast<int32_t*>(LU + len);
-  double* vec = LU + len + (ps + 1) / 2;
   const int64_t e = blockIdx.y;
-  for (int64_t q = threadIdx.x; q < len; q += BD) LU[q] = lu[e * len + q];
-  for (int q = threadIdx.x; q < ps; q += BD) P[q] = piv[e * ps + q];
+  const double* LU = lu + e * len;
+  const int32_t* P = piv + e * ps;
+  double* vec = sm;
+  if (stage) {
+    double* LUs = sm;
+    int32_t* Ps = reinterpret_cast<int32_t*>(LUs + len);
+    vec = LUs + len + (ps + 1) / 2;
+    for (int64_t q = threadIdx.x; q < len; q += BD) LUs[q] = lu[e * len + q];
+    for (int q = threadIdx.x; q < ps; q += BD) Ps[q] = piv[e * ps + q];
+    LU = LUs;
+    P = Ps;
+  }
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * BD + threadIdx.x;
   if (t >= npat) return;
@@ -714,7 +723,7 @@ void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const doubl
   l1_pairs_kernel<<<grid, kL1Threads, 0, s>>>(npat, pid, ne, len, mats, rep_src, reps, d);
 }
 
-static int spectral_block(int ps) { return ps <= 40 ? 64 : 32; }
+static int spectral_block(int ps) { return ps <= 40 ? 64 : ps <= 96 ? 32 : 16; }
 static size_t spectral_vec_bytes(int ps, int bd) { return (size_t)4 * ps * bd * sizeof(double); }
 
 void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
@@ -722,11 +731,13 @@ void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const 
   if (npat <= 0 || ne <= 0) return;
   if (spectral_tiled(npat, pid, ne, ps, mats, lu, piv, d, iters, s)) return;
   const int bd = spectral_block(ps);
-  const size_t smem = (size_t)ps * ps * sizeof(double) + (size_t)((ps + 1) / 2) * sizeof(double) +
-                      spectral_vec_bytes(ps, bd);
+  size_t smem = (size_t)ps * ps * sizeof(double) + (size_t)((ps + 1) / 2) * sizeof(double) +
+                spectral_vec_bytes(ps, bd);
+  const bool stage = smem <= 200 * 1024;
+  if (!stage) smem = spectral_vec_bytes(ps, bd);
   cudaFuncSetAttribute(spectral_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(grid_for(npat, bd), (unsigned)ne);
-  spectral_pairs_kernel<<<grid, bd, smem, s>>>(npat, pid, ne, ps, mats, lu, piv, d, iters);
+  spectral_pairs_kernel<<<grid, bd, smem, s>>>(npat, pid, ne, ps, mats, lu, piv, d, iters, stage);
 }
 
 void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,

@@ -152,7 +152,12 @@ void build_tiles(pdb_precond_s& pc, const std::vector<int32_t>& phi, cudaStream_
 // Grouping pays when entries are shared: by default only with >= 4 patches
 // per entry on average (an identity-phi database keeps the per-patch kernel,
 // so Exact == Compressed holds bit for bit).  PDB_GROUPED=0/1 forces it.
-bool use_grouped_apply(int64_t np, int64_t nf) {
+bool use_grouped_apply(int64_t np, int64_t nf, int ps) {
+  // the CUDA-core tile kernel stages B^{-1} and the tile's residuals in shared memory
+  const bool fits = k::dmma_apply_supported(ps) ||
+                    (static_cast<size_t>(ps) * ps + static_cast<size_t>(k::grouped_tile(ps)) * ps) * sizeof(double) <=
+                        200 * 1024;
+  if (!fits) return false;
   const char* e = getenv("PDB_GROUPED");
   if (e) return std::string(e) != "0";
   return np >= 4 * nf;
@@ -247,7 +252,7 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
   set_factors(pc, db.m, static_cast<int>(ps.ps), db.lu.get(), db.piv.get(), s);
   pc.phi.alloc(static_cast<size_t>(ps.np));
   PDB_CUDA(cudaMemcpyAsync(pc.phi.get(), db.phi.get(), ps.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-  if (!pc.lu_apply && use_grouped_apply(ps.np, db.m)) {
+  if (!pc.lu_apply && use_grouped_apply(ps.np, db.m, static_cast<int>(ps.ps))) {
     build_tiles(pc, phi, s);  // tiles in entry order; solutions stay in patch order
     build_inverse(pc, s);
     if (use_dmma_apply(static_cast<int>(ps.ps))) {

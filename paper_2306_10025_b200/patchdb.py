@@ -73,7 +73,8 @@ class GenOptions(C.Structure):
     _fields_ = [("physics", C.c_int), ("dim", C.c_int), ("degree", C.c_int), ("bc_mode", C.c_int),
                 ("cells", C.c_int64), ("jitter", C.c_double), ("seed", C.c_uint64), ("coeff_kind", C.c_int),
                 ("n_levels", C.c_int), ("coeff_value", C.c_double), ("block_cells", C.c_int64),
-                ("levels", C.c_double * 8), ("threads", C.c_int), ("reserved", C.c_int)]
+                ("levels", C.c_double * 8), ("threads", C.c_int), ("reserved", C.c_int),
+                ("poisson_ratio", C.c_double)]
 
 
 _P = C.c_void_p
