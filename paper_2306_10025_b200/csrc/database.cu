@@ -390,7 +390,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   // interleaved copies for the spectral assignment (PDB_SPECTRAL_IL=0 keeps the plain layout)
   const char* il_env = getenv("PDB_SPECTRAL_IL");
   const bool il = variant != Variant::Entrywise && k::spectral_il_supported(ps) && !(il_env && il_env[0] == '0');
-  DevBuf<double> sub_il, lu_il;
+  DevBuf<double> sub_il, lu_il, rd_il;
   DevBuf<int32_t> piv_il;
   if (il) {
     sub_il.alloc(static_cast<size_t>(k::interleaved_len(n, 32, len)));
@@ -407,8 +407,10 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       if (il) {
         lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
         piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
-        k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), s);
-        k::spectral_tiled_il(n, m, ps, sub_il.get(), lu_il.get(), piv_il.get(), dist.get(), iters.get(), s);
+        rd_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
+        k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), rd_il.get(), s);
+        k::spectral_tiled_il(n, m, ps, sub_il.get(), lu_il.get(), piv_il.get(), rd_il.get(), dist.get(), iters.get(),
+                             s);
       } else {
         k::spectral_pairs(n, nullptr, m, ps, sub, db.lu.get(), db.piv.get(), dist.get(), iters.get(), s);
       }

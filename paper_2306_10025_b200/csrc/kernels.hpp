@@ -159,10 +159,12 @@ void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const 
 bool spectral_il_supported(int ps);
 int64_t interleaved_len(int64_t count, int width, int64_t len);
 void interleave_patches(int64_t count, int64_t len, const double* src, double* dst, cudaStream_t s);
+// (rdiag_il: RN(1/u_ii) interleaved like the pivots, for the reciprocal-based exact division)
 void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* piv, double* lu_il, int32_t* piv_il,
-                        cudaStream_t s);
+                        double* rdiag_il, cudaStream_t s);
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
-                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s);
+                       const int32_t* piv_il, const double* rdiag_il, double* d, unsigned long long* iters,
+                       cudaStream_t s);
 // Spectral distance of listed (patch, factor) pairs: d[t] = dist(mats[pa[t]], factor fb[t]).
 void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);

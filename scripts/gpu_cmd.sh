@@ -1,2 +1,3 @@
-timeout 300 python scripts/fp64_probe.py > gpurun_out/fp64.log 2>&1; echo "exit $?" >> gpurun_out/fp64.log
-cp profiles/fp64_peaks.json gpurun_out/fp64_peaks.json
+for r in 0 1 0 1; do
+PDB_SPECTRAL_RECIP=$r ITERS=10 timeout 300 python scripts/setup_small.py 256 >> gpurun_out/setup_rc.log 2>&1
+done
