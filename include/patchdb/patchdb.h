@@ -284,6 +284,17 @@ PDB_API pdb_status pdb_shard_owned(pdb_shard sh, int64_t* local_idx);
 PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, double* d_x, int64_t sweeps, void* stream);
 PDB_API void pdb_shard_free(pdb_shard sh);
 
+/* Sharded setup: a communicator over nranks processes (one GPU each; id from
+ * pdb_comm_unique_id on one rank, shared out of band), and a k-means database
+ * build whose assignment step is split across the ranks (every rank returns
+ * the same database, bitwise equal to pdb_database_build).  Other methods
+ * build redundantly on every rank. */
+typedef struct pdb_comm_s* pdb_comm;
+PDB_API pdb_status pdb_comm_create(const unsigned char* id128, int rank, int nranks, pdb_comm* out);
+PDB_API void pdb_comm_free(pdb_comm c);
+PDB_API pdb_status pdb_database_build_sharded(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                              pdb_comm comm, pdb_database* out);
+
 /* Build information: "sm_100a" target, version. */
 PDB_API const char* pdb_build_info(void);
 

@@ -385,6 +385,26 @@ PDB_API pdb_status pdb_database_build(pdb_matrix m, pdb_patchset ps, const pdb_c
   });
 }
 
+PDB_API pdb_status pdb_comm_create(const unsigned char* id128, int rank, int nranks, pdb_comm* out) {
+  if (id128 == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] { *out = comm_create(id128, rank, nranks); });
+}
+
+PDB_API void pdb_comm_free(pdb_comm c) { comm_delete(c); }
+
+PDB_API pdb_status pdb_database_build_sharded(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                              pdb_comm comm, pdb_database* out) {
+  if (m == nullptr || ps == nullptr || opts == nullptr || comm == nullptr || out == nullptr)
+    return arg_error("null argument");
+  return guarded([&] {
+    auto db = std::make_unique<pdb_database_s>();
+    BuildParams p = params_of(opts);
+    p.comm = &comm_of(comm);
+    build_database(m->a, *ps, p, *db, default_stream());
+    *out = db.release();
+  });
+}
+
 PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
                                               int64_t target_lo, int64_t target_hi, pdb_database* out,
                                               double* eps_out) {

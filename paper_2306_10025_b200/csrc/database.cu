@@ -17,6 +17,8 @@
 
 #include <cub/cub.cuh>
 
+#include <nccl.h>
+
 #include "host.hpp"
 #include "kernels.hpp"
 
@@ -374,14 +376,41 @@ void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf
 }
 
 // kmeans_loop (compress.cpp:138-262).  phi_h receives the final assignment.
+// Sharded assignment (SURVEY §8e "Setup"): the n patches are cut into W
+// chunks of ceil(n/W); rank r evaluates the distances and the argmin of
+// chunk r only, and an in-place ncclAllGather of the new assignment and the
+// minimum distances gives every rank the full arrays, so the rest of the
+// Lloyd iteration (reseed / prune, means in ascending member order, LU) runs
+// redundantly and identically on all ranks -- the result is bitwise the
+// single-GPU build.  PDB_SHARD_EMULATE=W runs all W chunks on one GPU (no
+// NCCL), which tests the decomposition without W devices.
+#define PDB_NCCL_DB(call)                                                                                 \
+  do {                                                                                                    \
+    ncclResult_t r_ = (call);                                                                             \
+    if (r_ != ncclSuccess)                                                                                \
+      ::pdb::fail(::pdb::Errc::internal, std::string("NCCL error in " #call ": ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+struct AssignSlot {
+  int64_t lo = 0, hi = 0;
+  DevBuf<double> sub_il;
+};
+
 void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max_iters, Empty policy,
-                 std::vector<int32_t>& phi_h, PatchFactors& pf, BuildWork& work, cudaStream_t s) {
+                 std::vector<int32_t>& phi_h, PatchFactors& pf, BuildWork& work, cudaStream_t s,
+                 const ShardComm* comm = nullptr) {
   const int ps = db.ps;
   const int64_t len = db.len;
+  const bool sharded = comm != nullptr;  // (a 1-rank communicator still runs the NCCL path)
+  int W = sharded ? comm->nranks : 1;
+  if (!sharded)
+    if (const char* e = getenv("PDB_SHARD_EMULATE")) W = std::max(1, atoi(e));
+  const int64_t chunk = (n + W - 1) / W;
+  const size_t cap = static_cast<size_t>(std::max<int64_t>(chunk * W, n));
   phi_h.assign(static_cast<size_t>(n), -1);
   std::vector<double> min_dist(static_cast<size_t>(n), 0.0);
-  DevBuf<int32_t> d_phi(static_cast<size_t>(n)), d_new(static_cast<size_t>(n));
-  DevBuf<double> d_min(static_cast<size_t>(n));
+  DevBuf<int32_t> d_phi(cap), d_new(cap);
+  DevBuf<double> d_min(cap);
   h2d(d_phi.get(), phi_h, s);
   Scratch<int32_t> changed(1, s);
   Scratch<unsigned long long> iters(1, s);
@@ -390,37 +419,60 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   // interleaved copies for the spectral assignment (PDB_SPECTRAL_IL=0 keeps the plain layout)
   const char* il_env = getenv("PDB_SPECTRAL_IL");
   const bool il = variant != Variant::Entrywise && k::spectral_il_supported(ps) && !(il_env && il_env[0] == '0');
-  DevBuf<double> sub_il, lu_il, rd_il;
-  DevBuf<int32_t> piv_il;
-  if (il) {
-    sub_il.alloc(static_cast<size_t>(k::interleaved_len(n, 32, len)));
-    k::interleave_patches(n, len, sub, sub_il.get(), s);
+  std::vector<AssignSlot> slots;
+  for (int r = 0; r < W; ++r) {
+    if (sharded && r != comm->rank) continue;
+    AssignSlot sl;
+    sl.lo = std::min<int64_t>(n, r * chunk);
+    sl.hi = std::min<int64_t>(n, (r + 1) * chunk);
+    if (il && sl.hi > sl.lo) {
+      sl.sub_il.alloc(static_cast<size_t>(k::interleaved_len(sl.hi - sl.lo, 32, len)));
+      k::interleave_patches(sl.hi - sl.lo, len, sub + sl.lo * len, sl.sub_il.get(), s);
+    }
+    slots.push_back(std::move(sl));
   }
+  DevBuf<double> lu_il, rd_il;
+  DevBuf<int32_t> piv_il;
   for (int iter = 0; iter < max_iters; ++iter) {
     const int64_t m = db.m;
     PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
-    if (variant == Variant::Entrywise) {
-      k::l1_argmin(n, m, static_cast<int>(len), sub, db.reps.get(), d_phi.get(), d_new.get(), d_min.get(),
-                   changed.get(), s);
-    } else {
-      if (dist.size() < static_cast<size_t>(n * m)) dist.alloc(static_cast<size_t>(n * m));
-      if (il) {
-        lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
-        piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
-        rd_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
-        k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), rd_il.get(), s);
-        k::spectral_tiled_il(n, m, ps, sub_il.get(), lu_il.get(), piv_il.get(), rd_il.get(), dist.get(), iters.get(),
-                             s);
+    if (variant != Variant::Entrywise && il) {
+      lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
+      piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
+      rd_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
+      k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), rd_il.get(), s);
+    }
+    for (AssignSlot& sl : slots) {
+      const int64_t cnt = sl.hi - sl.lo;
+      if (cnt <= 0) continue;
+      if (variant == Variant::Entrywise) {
+        k::l1_argmin(cnt, m, static_cast<int>(len), sub + sl.lo * len, db.reps.get(), d_phi.get() + sl.lo,
+                     d_new.get() + sl.lo, d_min.get() + sl.lo, changed.get(), s);
       } else {
-        k::spectral_pairs(n, nullptr, m, ps, sub, db.lu.get(), db.piv.get(), dist.get(), iters.get(), s);
+        if (dist.size() < static_cast<size_t>(cnt * m)) dist.alloc(static_cast<size_t>(cnt * m));
+        if (il)
+          k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), rd_il.get(), dist.get(),
+                               iters.get(), s);
+        else
+          k::spectral_pairs(cnt, nullptr, m, ps, sub + sl.lo * len, db.lu.get(), db.piv.get(), dist.get(),
+                            iters.get(), s);
+        k::argmin_assign(cnt, m, dist.get(), d_phi.get() + sl.lo, d_new.get() + sl.lo, d_min.get() + sl.lo,
+                         changed.get(), s);
       }
-      k::argmin_assign(n, m, dist.get(), d_phi.get(), d_new.get(), d_min.get(), changed.get(), s);
     }
     PDB_LAUNCH_CHECK();
+    if (sharded) {
+      PDB_NCCL_DB(ncclGroupStart());
+      PDB_NCCL_DB(ncclAllGather(d_new.get() + comm->rank * chunk, d_new.get(), static_cast<size_t>(chunk), ncclInt32,
+                                comm->comm, s));
+      PDB_NCCL_DB(ncclAllGather(d_min.get() + comm->rank * chunk, d_min.get(), static_cast<size_t>(chunk),
+                                ncclDouble, comm->comm, s));
+      PDB_NCCL_DB(ncclGroupEnd());
+    }
     work.pair_evals += n * m;
-    int32_t ch = 0;
-    PDB_CUDA(cudaMemcpyAsync(&ch, changed.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    const std::vector<int32_t> prev = phi_h;
     phi_h = d2h(d_new.get(), static_cast<size_t>(n), s);
+    const bool ch = prev != phi_h;  // every rank sees the gathered assignment
     if (!ch) break;
     min_dist = d2h(d_min.get(), static_cast<size_t>(n), s);
 
@@ -570,6 +622,8 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       sync(s);
     }
   }
+  if (sharded)  // every rank reports the whole job's power iterations
+    PDB_NCCL_DB(ncclAllReduce(iters.get(), iters.get(), 1, ncclUint64, ncclSum, comm->comm, s));
   unsigned long long it_h = 0;
   PDB_CUDA(cudaMemcpyAsync(&it_h, iters.get(), sizeof(it_h), cudaMemcpyDeviceToHost, s));
   sync(s);
@@ -604,7 +658,8 @@ void finalize_factors(KDb& db, BuildWork& work, cudaStream_t s) {
 
 // kmeans (compress.cpp:294-324) on a contiguous group of n patch matrices.
 void kmeans_group(const double* sub, int64_t n, int ps, int64_t m_p, Variant variant, uint64_t seed, int max_iters,
-                  KDb& db, std::vector<int32_t>& phi_h, BuildWork& work, cudaStream_t s) {
+                  KDb& db, std::vector<int32_t>& phi_h, BuildWork& work, cudaStream_t s,
+                  const ShardComm* comm = nullptr) {
   require(n >= 1, Errc::invalid_argument, "kmeans needs at least one patch");
   require(m_p >= 1 && m_p <= n, Errc::invalid_argument, "kmeans requires 1 <= m_p <= n_p");
   const int64_t len = static_cast<int64_t>(ps) * ps;
@@ -633,7 +688,8 @@ void kmeans_group(const double* sub, int64_t n, int ps, int64_t m_p, Variant var
     std::fill(db.has_factor.begin(), db.has_factor.end(), 1);
   }
   PatchFactors pf;
-  kmeans_loop(sub, n, db, variant, max_iters, Empty::Reseed, phi_h, pf, work, s);
+  kmeans_loop(sub, n, db, variant, max_iters, Empty::Reseed, phi_h, pf, work, s,
+              variant == Variant::VarMin ? nullptr : comm);
   finalize_factors(db, work, s);
 }
 
@@ -720,7 +776,7 @@ void boundary_partition(const DevBuf<double>& mats, int64_t np, int ps, std::vec
 
 // partitioned_build (compress.cpp:394-421).
 void partitioned_build(const DevBuf<double>& mats, int64_t np, int ps, int64_t m_p, Variant variant, uint64_t seed,
-                       int max_iters, pdb_database_s& out, cudaStream_t s) {
+                       int max_iters, pdb_database_s& out, cudaStream_t s, const ShardComm* comm = nullptr) {
   const int64_t len = static_cast<int64_t>(ps) * ps;
   std::vector<std::vector<int32_t>> groups;
   std::vector<std::vector<uint8_t>> patterns;
@@ -740,7 +796,7 @@ void partitioned_build(const DevBuf<double>& mats, int64_t np, int ps, int64_t m
     k::gather_mats(cnt, ids.get(), len, mats.get(), sub.get(), s);
     std::vector<int32_t> lphi;
     kmeans_group(sub.get(), cnt, ps, alloc[g], variant, seed + static_cast<uint64_t>(g), max_iters, parts[g], lphi,
-                 out.work, s);
+                 out.work, s, comm);
     for (int64_t q = 0; q < cnt; ++q)
       phi[static_cast<size_t>(groups[g][static_cast<size_t>(q)])] = static_cast<int32_t>(total + lphi[static_cast<size_t>(q)]);
     total += parts[g].m;
@@ -811,10 +867,10 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
     case PDB_METHOD_GREEDY_L1:
       return greedy_build(mats, np, ips, p.eps, false, p.best_match, p.abort_above, out, s);
     case PDB_METHOD_KMEANS_ENTRYWISE:
-      partitioned_build(mats, np, ips, p.db_size, Variant::Entrywise, p.seed, p.max_iters, out, s);
+      partitioned_build(mats, np, ips, p.db_size, Variant::Entrywise, p.seed, p.max_iters, out, s, p.comm);
       return true;
     case PDB_METHOD_KMEANS_SPECTRAL:
-      partitioned_build(mats, np, ips, p.db_size, Variant::Spectral, p.seed, p.max_iters, out, s);
+      partitioned_build(mats, np, ips, p.db_size, Variant::Spectral, p.seed, p.max_iters, out, s, p.comm);
       return true;
     case PDB_METHOD_KMEANS_VARMIN:
       partitioned_build(mats, np, ips, p.db_size, Variant::VarMin, p.seed, p.max_iters, out, s);

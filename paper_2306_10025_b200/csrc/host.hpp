@@ -10,6 +10,7 @@
 #include "objects.hpp"
 
 struct pdb_shard_s;
+struct pdb_comm_s;
 struct pdb_shard_plan_s;
 
 namespace pdb {
@@ -35,6 +36,16 @@ std::vector<int64_t> patches_host(const pdb_patchset_s& ps, cudaStream_t s);
 void write_patchset_json(const pdb_patchset_s& ps, const std::string& path, cudaStream_t s);
 
 // database.cpp
+// A communicator for the sharded setup (k-means assignment split across ranks).
+struct ShardComm {
+  struct ncclComm* comm = nullptr;
+  int rank = 0, nranks = 1;
+};
+
+pdb_comm_s* comm_create(const unsigned char* id128, int rank, int nranks);
+void comm_delete(pdb_comm_s* c);
+const ShardComm& comm_of(const pdb_comm_s* c);
+
 struct BuildParams {
   int method = PDB_METHOD_GREEDY_L1;
   double eps = 1e-7;
@@ -43,6 +54,7 @@ struct BuildParams {
   int max_iters = 50;
   bool best_match = false;
   int64_t abort_above = -1;  // greedy only
+  const ShardComm* comm = nullptr;  // k-means: patches' assignment sharded over comm->nranks ranks
 };
 // Returns false when a capped greedy pass aborted (no database).
 bool build_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, pdb_database_s& out,

@@ -183,4 +183,34 @@ void shard_relax(pdb_shard_s& sh, const double* b, double* x, int64_t sweeps, cu
   PDB_LAUNCH_CHECK();
 }
 
+// ---- communicator for the sharded setup ---------------------------------
+}  // namespace pdb
+
+struct pdb_comm_s {
+  pdb::ShardComm c;
+  ~pdb_comm_s() {
+    if (c.comm) ncclCommDestroy(c.comm);
+  }
+};
+
+namespace pdb {
+
+pdb_comm_s* comm_create(const unsigned char* id128, int rank, int nranks) {
+  require(nranks >= 1 && rank >= 0 && rank < nranks, Errc::invalid_argument, "rank must be in [0, nranks)");
+  require_device();
+  auto c = std::make_unique<pdb_comm_s>();
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id128, sizeof(uid.internal));
+  ncclComm_t comm = nullptr;
+  PDB_NCCL(ncclCommInitRank(&comm, nranks, uid, rank));
+  c->c.comm = comm;
+  c->c.rank = rank;
+  c->c.nranks = nranks;
+  return c.release();
+}
+
+void comm_delete(pdb_comm_s* c) { delete c; }
+
+const ShardComm& comm_of(const pdb_comm_s* c) { return c->c; }
+
 }  // namespace pdb

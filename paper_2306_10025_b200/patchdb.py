@@ -351,10 +351,15 @@ class Database(_Handle):
     _free = _lib.pdb_database_free
 
     @classmethod
-    def build(cls, m: Matrix, ps: PatchSet, method: int = GREEDY_L1, **kw) -> "Database":
+    def build(cls, m: Matrix, ps: PatchSet, method: int = GREEDY_L1, comm: "Comm" = None, **kw) -> "Database":
+        """comm: a Comm over the participating ranks -> the sharded build
+        (k-means assignment split across ranks, same database on every rank)."""
         o = compress_options(method, **kw)
         out = C.c_void_p()
-        _check(_lib.pdb_database_build(m.ptr, ps.ptr, C.byref(o), C.byref(out)))
+        if comm is None:
+            _check(_lib.pdb_database_build(m.ptr, ps.ptr, C.byref(o), C.byref(out)))
+        else:
+            _check(_lib.pdb_database_build_sharded(m.ptr, ps.ptr, C.byref(o), comm.ptr, C.byref(out)))
         return cls(out)
 
     @classmethod
@@ -554,6 +559,23 @@ def comm_unique_id() -> bytes:
     buf = (C.c_ubyte * 128)()
     _check(_lib.pdb_comm_unique_id(buf))
     return bytes(buf)
+
+
+_sig("pdb_comm_create", C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(_P))
+_sig("pdb_comm_free", None, _P)
+_sig("pdb_database_build_sharded", C.c_int, _P, _P, C.POINTER(CompressOptions), _P, C.POINTER(_P))
+
+
+class Comm(_Handle):
+    """NCCL communicator for the sharded setup (one process per GPU)."""
+    _free = _lib.pdb_comm_free
+
+    @classmethod
+    def create(cls, uid: bytes, rank: int, nranks: int) -> "Comm":
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        out = C.c_void_p()
+        _check(_lib.pdb_comm_create(buf, rank, nranks, C.byref(out)))
+        return cls(out)
 
 
 class Shard(_Handle):

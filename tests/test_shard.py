@@ -169,3 +169,40 @@ def test_single_rank_device_shard_equals_relax(P):
     got = np.zeros_like(b)
     got[dofs] = xd.cpu().numpy()
     np.testing.assert_allclose(got, x_ref, rtol=1e-12, atol=1e-14 * np.abs(x_ref).max())
+
+
+# --------------------------------------------------------- sharded setup ---
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method", [3, 4])
+def test_sharded_build_matches_single_gpu(P, orc, method):
+    """pdb_database_build_sharded over a 1-rank NCCL communicator (the
+    all-gather path) returns the single-GPU database bit for bit."""
+    prob = P.Problem.generate(2, 16)
+    A = prob.matrix()
+    ps = P.PatchSet.detect(A, 25)
+    want = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
+    comm = P.Comm.create(P.comm_unique_id(), 0, 1)
+    got = P.Database.build(A, ps, method, comm=comm, db_size=16, seed=3, max_iters=8)
+    assert np.array_equal(got.phi(), want.phi())
+    assert np.array_equal(got.representatives(), want.representatives())
+    lu, piv = got.factors()
+    lw, pw = want.factors()
+    assert np.array_equal(lu, lw) and np.array_equal(piv, pw)
+    assert got.work()["power_iters"] == want.work()["power_iters"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("method", [3, 4])
+def test_emulated_shard_chunks_match_single_gpu(P, monkeypatch, world, method):
+    """PDB_SHARD_EMULATE=W evaluates the W rank chunks of the assignment one
+    after another on this GPU: same decomposition as W ranks, bitwise result."""
+    prob = P.Problem.generate(2, 16)
+    A = prob.matrix()
+    ps = P.PatchSet.detect(A, 25)
+    want = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
+    monkeypatch.setenv("PDB_SHARD_EMULATE", str(world))
+    got = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
+    assert np.array_equal(got.phi(), want.phi())
+    assert np.array_equal(got.representatives(), want.representatives())
