@@ -82,6 +82,7 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
 // Tensor-core grouped apply (FP64 mma.sync m8n8k4, ps <= 32, tiles <= 32 patches): sols_tile =
 // B_f^{-1} [r_k1 .. r_k32] with each inverse pre-arranged in A-fragment order by build_frag_inverses.
 bool dmma_apply_supported(int ps);
+int apply_tile(int ps);  // patches per tile of the grouped apply (32 on the DMMA path)
 int64_t frag_len(int ps);  // doubles per entry in fragment order
 void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag, cudaStream_t s);
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,

@@ -1161,6 +1161,69 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
   }
 }
 
+// Large patches (32 < ps <= 256, e.g. the 192-DoF elasticity patches): the
+// same tile product with run-time shapes.  MT = ps/8 warps (<= 32), the
+// inverse's A fragments streamed from L2 in chunks of 8 k-steps (a 192x192
+// entry is 295 KB -- it cannot stay in registers or shared memory), R staged
+// with a row stride padded to avoid bank conflicts.  Each tile reads its
+// entry once instead of once per patch.
+__global__ void __launch_bounds__(1024) patch_apply_dmma_large_kernel(
+    int ps, int mt, int ks, int kstr, const int32_t* __restrict__ tile_entry, const int32_t* __restrict__ tile_start,
+    const int32_t* __restrict__ tile_idx, const int32_t* __restrict__ order, const double* __restrict__ frag,
+    const double* __restrict__ r, const double* __restrict__ in_scale, double* __restrict__ sols) {
+  extern __shared__ double rk[];  // kDmmaTile * kstr
+  __shared__ int32_t ko[kDmmaTile];
+  const int t = blockIdx.x;
+  const int f = __ldg(tile_entry + t);
+  const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+  const int nth = blockDim.x;
+  if ((int)threadIdx.x < cnt) ko[threadIdx.x] = __ldg(order + s0 + threadIdx.x);
+  const int32_t* ti = tile_idx + (int64_t)s0 * ps;
+  grid_dep_wait();
+  grid_dep_trigger();
+  const int tot = kDmmaTile * kstr;
+  for (int e = threadIdx.x; e < tot; e += nth) {
+    const int p = e / kstr, k = e - p * kstr;
+    double v = 0.0;
+    if (p < cnt && k < ps) {
+      const int32_t g = __ldg(ti + p * ps + k);
+      v = __ldg(r + g);
+      if (in_scale) v *= __ldg(in_scale + g);
+    }
+    rk[e] = v;
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tg = lane & 3;
+  double c[kDmmaTile / 8][2];
+#pragma unroll
+  for (int nt = 0; nt < kDmmaTile / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  const double* fa = frag + ((int64_t)f * mt + w) * ks * 32 + lane;
+  for (int kc = 0; kc < ks; kc += 8) {
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = kc + q < ks ? __ldg(fa + (int64_t)(kc + q) * 32) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+      if (nt * 8 < cnt) {
+        const double* bp = rk + (nt * 8 + g) * kstr + kc * 4 + tg;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (kc + q < ks) dmma_m8n8k4(c[nt][0], c[nt][1], a[q], bp[q * 4]);
+      }
+    }
+  }
+  const int row = w * 8 + g;
+  if (row < ps) {
+#pragma unroll
+    for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+      const int p0 = nt * 8 + 2 * tg;
+      if (p0 < cnt) sols[(int64_t)ko[p0] * ps + row] = c[nt][0];
+      if (p0 + 1 < cnt) sols[(int64_t)ko[p0 + 1] * ps + row] = c[nt][1];
+    }
+  }
+}
+
 __global__ void build_zmap_kernel(int64_t n, int ps, const int32_t* __restrict__ inv_ptr,
                                   const int32_t* __restrict__ inv, const int32_t* __restrict__ slot_of,
                                   int32_t* __restrict__ zfwd, uint8_t* __restrict__ zcnt) {
@@ -1740,7 +1803,9 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
                                                                      Binv, r, in_scale, sols);
 }
 
-bool dmma_apply_supported(int ps) { return ps >= 1 && ps <= 32 && grouped_tile(ps) <= kDmmaTile; }
+bool dmma_apply_supported(int ps) { return ps >= 1 && ps <= 256; }
+
+int apply_tile(int ps) { return dmma_apply_supported(ps) ? kDmmaTile : grouped_tile(ps); }
 
 int64_t frag_len(int ps) { return (int64_t)((ps + 7) / 8) * ((ps + 3) / 4) * 32; }
 
@@ -1756,6 +1821,20 @@ static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry
                         cudaStream_t s) {
   if (ntiles <= 0) return;
   const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
+  if (ps > 32) {  // run-time shapes, inverse streamed from L2
+    int kstr = ks * 4;
+    if (kstr % 8 == 0) kstr += 4;
+    const size_t smem = (size_t)kDmmaTile * kstr * sizeof(double);
+    static size_t opted = 48 * 1024;
+    if (smem > opted) {
+      cudaFuncSetAttribute(patch_apply_dmma_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      opted = smem;
+    }
+    if (!Z)
+      launch_pdl(patch_apply_dmma_large_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s, ps, mt, ks, kstr,
+                 tile_entry, tile_start, idx, order, frag, r, in_scale, out);
+    return;
+  }
 #define PDB_DMMA_CASE(M, K)                                                                                    \
   if (mt == M && ks == K) {                                                                                    \
     launch_pdl(patch_apply_dmma_kernel<M, K, Z>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, n, tile_entry, \

@@ -116,7 +116,8 @@ void set_factors(pdb_precond_s& pc, int64_t nf, int ps, const double* lu_rm, con
 // Patches grouped by database entry (stable: ascending k inside a group) and
 // cut into tiles of at most kTile patches; one block applies one tile.
 void build_tiles(pdb_precond_s& pc, const std::vector<int32_t>& phi, cudaStream_t s) {
-  const int kTile = k::grouped_tile(static_cast<int>(pc.ps));
+  const int kTile = use_dmma_apply(static_cast<int>(pc.ps)) ? k::apply_tile(static_cast<int>(pc.ps))
+                                                            : k::grouped_tile(static_cast<int>(pc.ps));
   std::vector<int32_t> count(static_cast<size_t>(pc.nf), 0);
   for (int32_t j : phi) ++count[static_cast<size_t>(j)];
   std::vector<int32_t> start(static_cast<size_t>(pc.nf + 1), 0);
@@ -262,7 +263,7 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
       // interface scatter keeps the patch-order solutions and the inverse map)
       // (opt-in, PDB_ZMAP=1: measured slower on config 3, ~1 us faster on config 2)
       const char* zm = getenv("PDB_ZMAP");
-      if (zm && std::string(zm) == "1" && check_onto && pc.maxc_pad > 0 && pc.n < (int64_t{1} << 28)) {
+      if (zm && std::string(zm) == "1" && check_onto && pc.maxc_pad > 0 && pc.n < (int64_t{1} << 28) && pc.ps <= 32) {
         pc.zfwd.alloc(static_cast<size_t>(pc.np * pc.ps));
         pc.zcnt.alloc(static_cast<size_t>(pc.n));
         k::build_zmap(pc.n, static_cast<int>(pc.ps), pc.inv_ptr.get(), pc.inv.get(), pc.slot_of.get(), pc.zfwd.get(),

@@ -1,2 +1,1 @@
-set -x
-timeout 900 python -m pytest tests/test_fullsize.py -x -q -m gpu --durations=5 > gpurun_out/t_full.log 2>&1; echo "exit $?" >> gpurun_out/t_full.log
+timeout 900 python -m pytest tests/test_configs45.py -x -q -m gpu > gpurun_out/t_c45b.log 2>&1; echo "exit $?" >> gpurun_out/t_c45b.log

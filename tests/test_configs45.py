@@ -195,3 +195,24 @@ def test_gpu_relax_history(name, dev, compressed, request, P, orc):
     xo, ho = orc.relax(c.csr, c.patches, c.w, omega, lu, piv, phi, c.b, np.zeros_like(c.b), 10)
     np.testing.assert_allclose(hist, ho, rtol=RTOL_HIST, atol=0)
     np.testing.assert_allclose(x, xo, rtol=RTOL_HIST, atol=RTOL_HIST * np.abs(xo).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dev", [("c4s", "dev4"), ("c5s", "dev5")])
+def test_gpu_compressed_apply(name, dev, request, P, orc):
+    """Cluster-grouped tensor-core apply (22-DoF tiles; 192-DoF tiles with the
+    inverse streamed from L2) against the oracle's apply.  Databases with >= 4
+    patches per entry so the grouped path is taken."""
+    c = request.getfixturevalue(name)
+    A, ps = request.getfixturevalue(dev)
+    if c.ps_size == 22:
+        db = P.Database.build(A, ps, P.KMEANS_ENTRYWISE, db_size=12, seed=2, max_iters=6)
+    else:  # 27 boundary partitions at 4^3 cells: use the (unpartitioned) greedy instead
+        eps = orc.greedy_bisect(c.mats, 6, 12, spectral=False)["eps"]
+        db = P.Database.build(A, ps, P.GREEDY_L1, eps=eps)
+    assert len(c.patches) >= 4 * db.size
+    pc = P.Preconditioner.create(A, ps, db, omega=0.8)
+    r = np.random.default_rng(9).uniform(-1, 1, A.rows)
+    lu, piv = db.factors()
+    want = orc.precond_apply(c.patches, c.w, 0.8, lu, piv, db.phi(), r)
+    np.testing.assert_allclose(pc.apply(r), want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
