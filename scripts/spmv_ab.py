@@ -24,11 +24,10 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "pdl": {},
-    "nopdl": {"PDB_PDL": "0"},
-    "pdl_m5": {"PDB_SELL_MINB": "5"},
-    "pdl_u4": {"PDB_SPMV_PER": "4"},
-    "nopdl_m5": {"PDB_PDL": "0", "PDB_SELL_MINB": "5"},
+    "pipe0": {},
+    "pipe2": {"PDB_APPLY_PIPE": "2"},
+    "pipe4": {"PDB_APPLY_PIPE": "4"},
+    "pipe8": {"PDB_APPLY_PIPE": "8"},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
