@@ -149,3 +149,14 @@ def test_out_of_scope_entry_points_fail_cleanly(P):
     assert L.pdb_problem_assemble(b"{}", C.byref(out)) == P.PDB_ERR_INTERNAL
     assert "outside the B200 hot path" in L.pdb_last_error().decode()
     assert L.pdb_run_experiment(b"{}", b"/tmp/x.csv") == P.PDB_ERR_INTERNAL
+
+
+def test_sharded_setup_entry_points_validate_before_device(P):
+    L = P.lib
+    out = C.c_void_p()
+    uid = (C.c_ubyte * 128)()
+    assert L.pdb_comm_create(None, 0, 1, C.byref(out)) == P.PDB_ERR_INVALID_ARGUMENT
+    assert L.pdb_comm_create(uid, 2, 2, C.byref(out)) == P.PDB_ERR_INVALID_ARGUMENT
+    assert "rank" in L.pdb_last_error().decode()
+    assert L.pdb_database_build_sharded(None, None, None, None, C.byref(out)) == P.PDB_ERR_INVALID_ARGUMENT
+    L.pdb_comm_free(None)
