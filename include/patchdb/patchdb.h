@@ -285,15 +285,20 @@ PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, doubl
 PDB_API void pdb_shard_free(pdb_shard sh);
 
 /* Sharded setup: a communicator over nranks processes (one GPU each; id from
- * pdb_comm_unique_id on one rank, shared out of band), and a k-means database
- * build whose assignment step is split across the ranks (every rank returns
- * the same database, bitwise equal to pdb_database_build).  Other methods
- * build redundantly on every rank. */
+ * pdb_comm_unique_id on one rank, shared out of band), and database builds
+ * whose dominant step is split across the ranks -- the k-means assignment, the
+ * greedy scan of the remaining patches against each round's new entries --
+ * with every rank returning the same database, bitwise equal to
+ * pdb_database_build.  EXACT and BOOTSTRAP build redundantly on every rank. */
 typedef struct pdb_comm_s* pdb_comm;
 PDB_API pdb_status pdb_comm_create(const unsigned char* id128, int rank, int nranks, pdb_comm* out);
 PDB_API void pdb_comm_free(pdb_comm c);
 PDB_API pdb_status pdb_database_build_sharded(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
                                               pdb_comm comm, pdb_database* out);
+/* Sharded greedy tolerance bisection (each probe a sharded greedy pass). */
+PDB_API pdb_status pdb_database_build_to_size_sharded(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                                      int64_t target_lo, int64_t target_hi, pdb_comm comm,
+                                                      pdb_database* out, double* eps_out);
 
 /* Build information: "sm_100a" target, version. */
 PDB_API const char* pdb_build_info(void);

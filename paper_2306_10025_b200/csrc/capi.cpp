@@ -405,6 +405,21 @@ PDB_API pdb_status pdb_database_build_sharded(pdb_matrix m, pdb_patchset ps, con
   });
 }
 
+PDB_API pdb_status pdb_database_build_to_size_sharded(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
+                                                      int64_t target_lo, int64_t target_hi, pdb_comm comm,
+                                                      pdb_database* out, double* eps_out) {
+  if (m == nullptr || ps == nullptr || opts == nullptr || comm == nullptr || out == nullptr)
+    return arg_error("null argument");
+  return guarded([&] {
+    auto db = std::make_unique<pdb_database_s>();
+    BuildParams p = params_of(opts);
+    p.comm = &comm_of(comm);
+    const double eps = bisect_database(m->a, *ps, p, target_lo, target_hi, *db, default_stream());
+    if (eps_out) *eps_out = eps;
+    *out = db.release();
+  });
+}
+
 PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
                                               int64_t target_lo, int64_t target_hi, pdb_database* out,
                                               double* eps_out) {

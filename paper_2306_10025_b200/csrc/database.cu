@@ -20,6 +20,14 @@
 #include <nccl.h>
 
 #include "host.hpp"
+
+#define PDB_NCCL_DB(call)                                                                                 \
+  do {                                                                                                    \
+    ncclResult_t r_ = (call);                                                                             \
+    if (r_ != ncclSuccess)                                                                                \
+      ::pdb::fail(::pdb::Errc::internal, std::string("NCCL error in " #call ": ") + ncclGetErrorString(r_)); \
+  } while (0)
+
 #include "kernels.hpp"
 
 namespace pdb {
@@ -110,8 +118,19 @@ struct EntryStore {
 //   against entries created inside S only: greedy_resolve does exactly that.
 //   The rest of U (first-match) -- or every later patch (best-match) -- is
 //   then compared with the new entries only, in creation order.
+// Sharding (comm, or PDB_SHARD_EMULATE=W on one GPU): every rank runs the
+// same rounds -- batch distances, the sequential resolution and the list
+// bookkeeping are replicated -- and only the dominant step, comparing the
+// remaining patches R with the round's new entries, is split: rank r scans
+// the r-th contiguous chunk of R.  Each patch is scanned by exactly one rank
+// and entry ids only grow, so an all-reduce MAX of phi (and MIN of the best
+// distance) merges the ranks' updates exactly; the database is bitwise the
+// single-GPU one.
 bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bool spectral, bool best_match,
-                  int64_t abort_above, pdb_database_s& out, cudaStream_t s) {
+                  int64_t abort_above, pdb_database_s& out, cudaStream_t s, const ShardComm* comm = nullptr) {
+  int W = comm ? comm->nranks : 1;
+  if (!comm)
+    if (const char* e = getenv("PDB_SHARD_EMULATE")) W = std::max(1, atoi(e));
   require(np >= 1, Errc::invalid_argument, "greedy_tolerance needs at least one patch");
   require(eps > 0.0, Errc::invalid_argument, "tolerance must be positive");
   const int64_t len = static_cast<int64_t>(ps) * ps;
@@ -230,39 +249,51 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
         if (nr > 0)
           PDB_CUDA(cudaMemcpyAsync(R, U.get() + B, nr * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
       }
-      if (nr > 0) {
+      const int64_t rchunk = (nr + W - 1) / W;
+      for (int rk = 0; rk < W && nr > 0; ++rk) {
+        if (comm && rk != comm->rank) continue;
+        const int64_t r0 = std::min<int64_t>(nr, rk * rchunk), r1 = std::min<int64_t>(nr, (rk + 1) * rchunk);
+        int32_t* Rr = R + r0;
+        const int64_t nrr = r1 - r0;
+        if (nrr <= 0) continue;
         if (!spectral) {
-          k::l1_scan(nr, R, m, m_new, static_cast<int>(len), mats.get(), creators.get(), eps, best_match ? 1 : 0,
+          k::l1_scan(nrr, Rr, m, m_new, static_cast<int>(len), mats.get(), creators.get(), eps, best_match ? 1 : 0,
                      phi.get(), best_d.get(), s);
           PDB_LAUNCH_CHECK();
-          work.pair_evals += nr * (m_new - m);  // upper bound (early exit not counted)
         } else {
           // chunks of new entries; first-match drops matched patches between chunks
           const int64_t CH = 16;
-          DevBuf<double> dch(static_cast<size_t>(nr * CH));
-          DevBuf<uint8_t> fl2(static_cast<size_t>(nr));
-          int64_t live = nr;
+          DevBuf<double> dch(static_cast<size_t>(nrr * CH));
+          int64_t live = nrr;
           for (int64_t c0 = m; c0 < m_new && live > 0; c0 += CH) {
             const int64_t ne = std::min(CH, m_new - c0);
-            k::spectral_pairs(live, R, ne, ps, mats.get(), store.lu.get() + c0 * len, store.piv.get() + c0 * ps,
+            k::spectral_pairs(live, Rr, ne, ps, mats.get(), store.lu.get() + c0 * len, store.piv.get() + c0 * ps,
                               dch.get(), iters.get(), s);
-            k::apply_scan(live, R, c0, ne, dch.get(), creators.get(), eps, best_match ? 1 : 0, phi.get(),
+            k::apply_scan(live, Rr, c0, ne, dch.get(), creators.get(), eps, best_match ? 1 : 0, phi.get(),
                           best_d.get(), s);
             PDB_LAUNCH_CHECK();
-            work.pair_evals += live * ne;
             if (!best_match && c0 + CH < m_new) {
               // keep unmatched
               std::vector<int32_t> ph = d2h(phi.get(), static_cast<size_t>(np), s);
-              std::vector<int32_t> Rh = d2h(R, static_cast<size_t>(live), s);
+              std::vector<int32_t> Rh = d2h(Rr, static_cast<size_t>(live), s);
               std::vector<int32_t> keep;
               keep.reserve(Rh.size());
               for (int32_t v : Rh)
                 if (ph[static_cast<size_t>(v)] < 0) keep.push_back(v);
               live = static_cast<int64_t>(keep.size());
-              h2d(R, keep, s);
+              h2d(Rr, keep, s);
             }
           }
         }
+      }
+      if (nr > 0) work.pair_evals += nr * (m_new - m);  // upper bound (early exits not counted)
+      if (comm && nr > 0) {  // merge: phi only grows (entry ids), best distances only shrink
+        PDB_NCCL_DB(ncclGroupStart());
+        PDB_NCCL_DB(ncclAllReduce(phi.get(), phi.get(), static_cast<size_t>(np), ncclInt32, ncclMax, comm->comm, s));
+        if (best_match)
+          PDB_NCCL_DB(ncclAllReduce(best_d.get(), best_d.get(), static_cast<size_t>(np), ncclDouble, ncclMin,
+                                    comm->comm, s));
+        PDB_NCCL_DB(ncclGroupEnd());
       }
     }
     m = m_new;
@@ -281,6 +312,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
       nu = 0;
     }
   }
+  if (comm) PDB_NCCL_DB(ncclAllReduce(iters.get(), iters.get(), 1, ncclUint64, ncclSum, comm->comm, s));
   unsigned long long it_h = 0;
   PDB_CUDA(cudaMemcpyAsync(&it_h, iters.get(), sizeof(it_h), cudaMemcpyDeviceToHost, s));
   sync(s);
@@ -384,12 +416,6 @@ void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf
 // redundantly and identically on all ranks -- the result is bitwise the
 // single-GPU build.  PDB_SHARD_EMULATE=W runs all W chunks on one GPU (no
 // NCCL), which tests the decomposition without W devices.
-#define PDB_NCCL_DB(call)                                                                                 \
-  do {                                                                                                    \
-    ncclResult_t r_ = (call);                                                                             \
-    if (r_ != ncclSuccess)                                                                                \
-      ::pdb::fail(::pdb::Errc::internal, std::string("NCCL error in " #call ": ") + ncclGetErrorString(r_)); \
-  } while (0)
 
 struct AssignSlot {
   int64_t lo = 0, hi = 0;
@@ -863,9 +889,9 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
   switch (p.method) {
     case PDB_METHOD_EXACT: exact_build(mats, np, ips, out, s); return true;
     case PDB_METHOD_GREEDY_SPECTRAL:
-      return greedy_build(mats, np, ips, p.eps, true, p.best_match, p.abort_above, out, s);
+      return greedy_build(mats, np, ips, p.eps, true, p.best_match, p.abort_above, out, s, p.comm);
     case PDB_METHOD_GREEDY_L1:
-      return greedy_build(mats, np, ips, p.eps, false, p.best_match, p.abort_above, out, s);
+      return greedy_build(mats, np, ips, p.eps, false, p.best_match, p.abort_above, out, s, p.comm);
     case PDB_METHOD_KMEANS_ENTRYWISE:
       partitioned_build(mats, np, ips, p.db_size, Variant::Entrywise, p.seed, p.max_iters, out, s, p.comm);
       return true;
@@ -910,7 +936,7 @@ double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const Build
     q.abort_above = target_hi;
     pdb_database_s db;
     const bool ok = greedy_build(mats, n_p, static_cast<int>(ps.ps), eps, p.method == PDB_METHOD_GREEDY_SPECTRAL,
-                                 p.best_match, target_hi, db, s);
+                                 p.best_match, target_hi, db, s, p.comm);
     total.pair_evals += db.work.pair_evals;
     total.power_iters += db.work.power_iters;
     total.lu_count += db.work.lu_count;

@@ -364,12 +364,16 @@ class Database(_Handle):
 
     @classmethod
     def build_to_size(cls, m: Matrix, ps: PatchSet, target_lo: int, target_hi: int, method: int = GREEDY_L1,
-                      **kw):
+                      comm: "Comm" = None, **kw):
         o = compress_options(method, **kw)
         out = C.c_void_p()
         eps = C.c_double()
-        _check(_lib.pdb_database_build_to_size(m.ptr, ps.ptr, C.byref(o), target_lo, target_hi, C.byref(out),
-                                               C.byref(eps)))
+        if comm is None:
+            _check(_lib.pdb_database_build_to_size(m.ptr, ps.ptr, C.byref(o), target_lo, target_hi, C.byref(out),
+                                                   C.byref(eps)))
+        else:
+            _check(_lib.pdb_database_build_to_size_sharded(m.ptr, ps.ptr, C.byref(o), target_lo, target_hi, comm.ptr,
+                                                           C.byref(out), C.byref(eps)))
         return cls(out), eps.value
 
     @property
@@ -564,6 +568,8 @@ def comm_unique_id() -> bytes:
 _sig("pdb_comm_create", C.c_int, C.c_void_p, C.c_int, C.c_int, C.POINTER(_P))
 _sig("pdb_comm_free", None, _P)
 _sig("pdb_database_build_sharded", C.c_int, _P, _P, C.POINTER(CompressOptions), _P, C.POINTER(_P))
+_sig("pdb_database_build_to_size_sharded", C.c_int, _P, _P, C.POINTER(CompressOptions), C.c_int64, C.c_int64, _P,
+     C.POINTER(_P), C.POINTER(C.c_double))
 
 
 class Comm(_Handle):

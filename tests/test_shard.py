@@ -173,17 +173,27 @@ def test_single_rank_device_shard_equals_relax(P):
 
 # --------------------------------------------------------- sharded setup ---
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("method", [3, 4])
-def test_sharded_build_matches_single_gpu(P, orc, method):
-    """pdb_database_build_sharded over a 1-rank NCCL communicator (the
-    all-gather path) returns the single-GPU database bit for bit."""
+def _sharded_case(P, method, best_match=0):
     prob = P.Problem.generate(2, 16)
     A = prob.matrix()
     ps = P.PatchSet.detect(A, 25)
-    want = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
+    if method in (1, 2):  # greedy: a tolerance giving ~16 entries
+        want, eps = P.Database.build_to_size(A, ps, 12, 20, method, best_match=best_match)
+        kw = dict(eps=eps, best_match=best_match)
+    else:
+        kw = dict(db_size=16, seed=3, max_iters=8)
+    want = P.Database.build(A, ps, method, **kw)
+    return A, ps, kw, want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("method,best", [(1, 0), (2, 0), (2, 1), (3, 0), (4, 0)])
+def test_sharded_build_matches_single_gpu(P, orc, method, best):
+    """pdb_database_build_sharded over a 1-rank NCCL communicator (the
+    all-gather / all-reduce paths) returns the single-GPU database bit for bit."""
+    A, ps, kw, want = _sharded_case(P, method, best)
     comm = P.Comm.create(P.comm_unique_id(), 0, 1)
-    got = P.Database.build(A, ps, method, comm=comm, db_size=16, seed=3, max_iters=8)
+    got = P.Database.build(A, ps, method, comm=comm, **kw)
     assert np.array_equal(got.phi(), want.phi())
     assert np.array_equal(got.representatives(), want.representatives())
     lu, piv = got.factors()
@@ -194,15 +204,24 @@ def test_sharded_build_matches_single_gpu(P, orc, method):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 5])
-@pytest.mark.parametrize("method", [3, 4])
-def test_emulated_shard_chunks_match_single_gpu(P, monkeypatch, world, method):
-    """PDB_SHARD_EMULATE=W evaluates the W rank chunks of the assignment one
-    after another on this GPU: same decomposition as W ranks, bitwise result."""
+@pytest.mark.parametrize("method,best", [(1, 0), (2, 0), (2, 1), (3, 0), (4, 0)])
+def test_emulated_shard_chunks_match_single_gpu(P, monkeypatch, world, method, best):
+    """PDB_SHARD_EMULATE=W evaluates the W rank chunks (k-means assignment,
+    greedy scan) one after another on this GPU: same decomposition as W
+    ranks, bitwise result."""
+    A, ps, kw, want = _sharded_case(P, method, best)
+    monkeypatch.setenv("PDB_SHARD_EMULATE", str(world))
+    got = P.Database.build(A, ps, method, **kw)
+    assert np.array_equal(got.phi(), want.phi())
+    assert np.array_equal(got.representatives(), want.representatives())
+
+
+@pytest.mark.gpu
+def test_sharded_bisection_matches_single_gpu(P):
     prob = P.Problem.generate(2, 16)
     A = prob.matrix()
     ps = P.PatchSet.detect(A, 25)
-    want = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
-    monkeypatch.setenv("PDB_SHARD_EMULATE", str(world))
-    got = P.Database.build(A, ps, method, db_size=16, seed=3, max_iters=8)
-    assert np.array_equal(got.phi(), want.phi())
-    assert np.array_equal(got.representatives(), want.representatives())
+    want, we = P.Database.build_to_size(A, ps, 12, 20, 2)
+    comm = P.Comm.create(P.comm_unique_id(), 0, 1)
+    got, ge = P.Database.build_to_size(A, ps, 12, 20, 2, comm=comm)
+    assert ge == we and np.array_equal(got.phi(), want.phi())
