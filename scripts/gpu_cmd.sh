@@ -1,5 +1,3 @@
-set -x
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_all.log 2>&1; echo "exit $?" >> gpurun_out/t_all.log
-for c in 1 3; do
-  timeout 900 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err; echo "exit $?" >> gpurun_out/bench_c$c.err
-done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_dcol.log 2>&1; echo "exit $?" >> gpurun_out/t_dcol.log
+timeout 300 python scripts/spmv_ab.py 2 > gpurun_out/ab_dcol.log 2>&1
+timeout 300 python scripts/spmv_ab.py 3 >> gpurun_out/ab_dcol.log 2>&1

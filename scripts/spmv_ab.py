@@ -24,10 +24,8 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "pipe0": {},
-    "pipe2": {"PDB_APPLY_PIPE": "2"},
-    "pipe4": {"PDB_APPLY_PIPE": "4"},
-    "pipe8": {"PDB_APPLY_PIPE": "8"},
+    "col32": {"PDB_SELL_DCOL": "0"},
+    "dcol16": {},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
