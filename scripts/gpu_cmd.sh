@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_dcol.log 2>&1; echo "exit $?" >> gpurun_out/t_dcol.log
-timeout 300 python scripts/spmv_ab.py 2 > gpurun_out/ab_dcol.log 2>&1
-timeout 300 python scripts/spmv_ab.py 3 >> gpurun_out/ab_dcol.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_color.log 2>&1; echo "exit $?" >> gpurun_out/t_color.log
+for c in 2 3 4; do timeout 300 python scripts/spmv_ab.py $c >> gpurun_out/ab_color.log 2>&1; done

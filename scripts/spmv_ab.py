@@ -14,18 +14,18 @@ from paper_2306_10025_b200 import patchdb as P  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 cells = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-ps_size = {1: 9, 2: 25, 3: 27}[cfg]
+ps_size = {1: 9, 2: 25, 3: 27, 4: 22, 5: 192}[cfg]
 prob = P.Problem.generate(cfg, cells)
 A = prob.matrix()
 ps = P.PatchSet.detect(A, ps_size)
-db = P.Database.build(A, ps, P.KMEANS_ENTRYWISE, db_size=64 if cfg != 3 else 128, max_iters=5)
+db = P.Database.build(A, ps, P.KMEANS_ENTRYWISE, db_size={3: 128, 4: 128}.get(cfg, 64), max_iters=5)
 pc = P.Preconditioner.create(A, ps, db)
 b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "col32": {"PDB_SELL_DCOL": "0"},
-    "dcol16": {},
+    "ordered": {"PDB_COLOR": "0"},
+    "colored": {},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
