@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_color.log 2>&1; echo "exit $?" >> gpurun_out/t_color.log
-for c in 2 3 4; do timeout 300 python scripts/spmv_ab.py $c >> gpurun_out/ab_color.log 2>&1; done
+for c in 2 3 4; do timeout 300 python scripts/spmv_ab.py $c >> gpurun_out/ab_head.log 2>&1; done
