@@ -119,7 +119,7 @@ PDB_API const char* pdb_status_string(pdb_status status) {
 PDB_API const char* pdb_last_error(void) { return g_last_error.c_str(); }
 
 PDB_API const char* pdb_build_info(void) {
-  return "patchdb-b200 0.1.0; device code sm_100a (tcgen05-era B200); C-ABI of patchdb 0.1.0";
+  return "patchdb-b200 0.1.0; device code sm_100a (B200); C-ABI of patchdb 0.1.0";
 }
 
 /* ---- matrices ---- */
