@@ -74,3 +74,17 @@ def test_config4_detect_spmv_bit_exact(P, orc):
     assert np.array_equal(ps.weights(), w)
     x = np.random.default_rng(8).uniform(-1, 1, A.rows)
     assert np.array_equal(A.spmv(x), orc.spmv(csr, x))
+
+
+def test_config3_detect_spmv_bit_exact(P, orc):
+    prob = P.Problem.generate(3, 0)
+    A = prob.matrix()
+    csr = prob.csr()
+    assert A.rows == 2146689 and prob.nnz == 130422149
+    ps = P.PatchSet.detect(A, 27)
+    patches, w = orc.detect(csr, 27)
+    assert patches.shape == (262144, 27)
+    assert np.array_equal(ps.patches(), patches)
+    assert np.array_equal(ps.weights(), w)
+    x = np.random.default_rng(17).uniform(-1, 1, A.rows)
+    assert np.array_equal(A.spmv(x), orc.spmv(csr, x))
