@@ -457,7 +457,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
     }
     slots.push_back(std::move(sl));
   }
-  DevBuf<double> lu_il, rd_il;
+  DevBuf<double> lu_il;
   DevBuf<int32_t> piv_il;
   for (int iter = 0; iter < max_iters; ++iter) {
     const int64_t m = db.m;
@@ -465,8 +465,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
     if (variant != Variant::Entrywise && il) {
       lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
       piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
-      rd_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
-      k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), rd_il.get(), s);
+      k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), s);
     }
     for (AssignSlot& sl : slots) {
       const int64_t cnt = sl.hi - sl.lo;
@@ -477,8 +476,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       } else {
         if (dist.size() < static_cast<size_t>(cnt * m)) dist.alloc(static_cast<size_t>(cnt * m));
         if (il)
-          k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), rd_il.get(), dist.get(),
-                               iters.get(), s);
+          k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), dist.get(), iters.get(), s);
         else
           k::spectral_pairs(cnt, nullptr, m, ps, sub + sl.lo * len, db.lu.get(), db.piv.get(), dist.get(),
                             iters.get(), s);

@@ -9,24 +9,19 @@
 
 namespace pdb::k {
 
-// ---- sweep.cu : the relaxation sweep -------------------------------------
-// r = b - A x (b may be null: r = -A x is never used; y = A x when b == null
-// and negate == false).  When sumsq != null, per-block partial sums of r^2
-// are written to sumsq[blockIdx] (deterministic two-pass norm).
+// ---- spmv.cu : residual and SpMV ------------------------------------------
+// r = b - A x (b may be null: y = A x when negate == false).  When sumsq !=
+// null, per-block partial sums of r^2 are written to sumsq[blockIdx]
+// (deterministic two-pass norm).
 struct SpmvPlan {
-  int group = 8;      // threads per row (power of two <= 32)
-  int rows_per_block = 32;
+  int version = 2;    // 9: SELL-C-sigma (default); 5: CSR warp items; 2: G lanes per row
   int blocks = 0;
-  int version = 2;    // 1: 4-way unrolled loop; 2: batched col/val/x loads; 3: CSR stream
-  int entries = 4;    // v2: entries per lane per pass
-  const int32_t* blk_start = nullptr;  // v3: row partition (nblk + 1 entries)
-  const int64_t* blk_base = nullptr;   // v3: row_ptr[blk_start[b]]
-  int nblk = 0;                        // v3/v4: partition blocks (v4 runs a persistent grid of `blocks`)
-  // v8: block-local column windows (see DeviceCsr)
-  const uint16_t* lcol = nullptr;
-  const int32_t* win_ptr = nullptr;
-  const int32_t* win_runs = nullptr;
-  int win_max = 0;
+  int group = 8;      // v2: lanes per row (power of two <= 32)
+  int rows_per_block = 32;
+  int entries = 8;    // v2: entries per lane per pass; v9: steps in flight per lane (4 or 8)
+  const int32_t* blk_start = nullptr;  // v5: item row starts (nblk + 1 entries)
+  const int64_t* blk_base = nullptr;   // v5: row_ptr at each item start
+  int nblk = 0;                        // v5: warp items
   // v9: SELL-C-sigma slices (see DeviceCsr)
   const int64_t* sell_off = nullptr;
   const int32_t* sell_row = nullptr;
@@ -36,18 +31,11 @@ struct SpmvPlan {
 };
 constexpr int kSellC = 32;          // rows per SELL slice (one warp)
 constexpr int kSellSigma = 8192;    // sorting window (rows)
-constexpr int kWindowItems = 8;     // v5/v8 warp items per block
-constexpr int kWindowCap = 4096;    // max staged x window per block (doubles)
-constexpr int kItemNnz = 256;       // v5/v8 item capacity (nonzeros)
 SpmvPlan spmv_plan(int64_t n, int64_t nnz);
-// v3 plan over a matrix's row partition.
-// per = nonzeros per thread of the partition (8 or 16; 256 threads per block).
-SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, const int64_t* blk_base, int nblk,
-                          int per);
-// Host-side row partition for v3: blocks of <= 256*per nonzeros and <= 64*per rows.
-int stream_nnz();
-std::vector<int32_t> stream_partition(int64_t n, const int64_t* row_ptr, int per);  // per 0: v5 warp partition
-std::vector<int32_t> row_partition(int64_t n, const int64_t* row_ptr, int64_t cap_nnz, int64_t cap_rows);
+// v5 plan over a warp-item partition (item_partition, built at upload).
+SpmvPlan spmv_plan_items(int64_t n, int64_t nnz, const int32_t* item_start, const int64_t* item_base, int nitems);
+// Host-side warp items: consecutive rows, <= 31 rows and <= 256 nonzeros (a longer row alone).
+std::vector<int32_t> item_partition(int64_t n, const int64_t* row_ptr);
 // SELL plans only: r = b - A x on slices [s0, s1) (whole sorting windows, i.e. rows
 // [s0 * kSellC, min(s1 * kSellC, n))), plain launch (ordered after events by the caller).
 void residual_slices(const SpmvPlan& plan, int64_t s0, int64_t s1, const double* x, const double* b, double* r,
@@ -59,6 +47,7 @@ void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col
 // Deterministic sum of `count` partials -> out[0] = sqrt(sum) (sqrt_result) or sum.
 void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s);
 
+// ---- sweep.cu : patch stage and scatter -----------------------------------
 // Per-patch gather + LU solve (column-major factors):
 //   sols[k*ps + i] = (B_f^{-1} (r .* in_scale)[patch_k])_i,  f = phi ? phi[k] : k; in_scale may be null.
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
@@ -88,17 +77,6 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
                       const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
                       const double* in_scale, double* sols, cudaStream_t s);
-// DoF-major variant: the tile gathers r through zfwd & (2^28-1) and stores each
-// solution value at Z[(zfwd >> 28) * n + (zfwd & (2^28-1))].
-void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
-                        const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
-                        cudaStream_t s);
-// zfwd (tile order, via slot_of) / zcnt from the patch-order inverse map
-void build_zmap(int64_t n, int ps, const int32_t* inv_ptr, const int32_t* inv, const int32_t* slot_of, int32_t* zfwd,
-                uint8_t* zcnt, cudaStream_t s);
-// x_out = x_in + omega * w(count) * sum_{c < zcnt[i]} Z[c*n + i]  (and/or z_out)
-void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
-               double* z_out, double* x_out, cudaStream_t s);
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
 // Multi-GPU shard helpers: list-driven scatter (see shard.cu), pack / unpack.
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
@@ -160,12 +138,10 @@ void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const 
 bool spectral_il_supported(int ps);
 int64_t interleaved_len(int64_t count, int width, int64_t len);
 void interleave_patches(int64_t count, int64_t len, const double* src, double* dst, cudaStream_t s);
-// (rdiag_il: RN(1/u_ii) interleaved like the pivots, for the reciprocal-based exact division)
 void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* piv, double* lu_il, int32_t* piv_il,
-                        double* rdiag_il, cudaStream_t s);
+                        cudaStream_t s);
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
-                       const int32_t* piv_il, const double* rdiag_il, double* d, unsigned long long* iters,
-                       cudaStream_t s);
+                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s);
 // Spectral distance of listed (patch, factor) pairs: d[t] = dist(mats[pa[t]], factor fb[t]).
 void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);

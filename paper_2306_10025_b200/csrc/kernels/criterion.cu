@@ -18,7 +18,6 @@
 #include <math_constants.h>
 
 #include "../kernels.hpp"
-#include "exact_div.cuh"
 
 namespace pdb::k {
 
@@ -394,14 +393,13 @@ constexpr int kTileThreads = 64;
 // (patch, factor) pairs of one tile, so each load of the interleaved copy is
 // one contiguous 256-byte (patches) / 64-byte (factors) span instead of up to
 // 32 separate cache lines.
-template <int PS, bool IL, int MU = 1, bool RC = false>
+template <int PS, bool IL>
 __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npat, const int32_t* __restrict__ pid,
                                                                      int64_t ne, const double* __restrict__ mats,
                                                                      const double* __restrict__ lu,
                                                                      const int32_t* __restrict__ piv,
                                                                      double* __restrict__ d,
-                                                                     unsigned long long* iters_total,
-                                                                     const double* __restrict__ rdiag) {
+                                                                     unsigned long long* iters_total) {
   constexpr int LEN = PS * PS;
   constexpr int BD = kTileThreads;
   constexpr int SA = IL ? kTileA : 1;  // element stride of a patch matrix
@@ -415,10 +413,6 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   const int nev = (int)(ne - e0 < kTileE ? ne - e0 : kTileE);
   const double* LUs = IL ? lu + (int64_t)blockIdx.y * LEN * kTileE : lu + e0 * LEN;
   const int32_t* Ps = IL ? piv + (int64_t)blockIdx.y * PS * kTileE : piv + e0 * PS;
-  // IL: reciprocals of the factors' diagonals (interleaved like the pivots), so
-  // every division by u_ii is div_rn_recip -- bitwise __ddiv_rn, 5 instructions
-  const double* Rs = IL ? rdiag + (int64_t)blockIdx.y * PS * kTileE : nullptr;
-  const double* R = Rs;
   if (tid == 0) counter = 0;
   __syncthreads();
   double* V = vec + tid;
@@ -444,7 +438,6 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
           A = mats + (int64_t)blockIdx.x * LEN * kTileA + pa;
           L = LUs + pe;
           P = Ps + pe;
-          R = Rs + pe;
         } else {
           A = mats + (int64_t)(pid ? pid[g] : g) * LEN;
           L = LUs + pe * LEN;
@@ -484,8 +477,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
       double s = T[i];
 #pragma unroll
       for (int j = i + 1; j < PS; ++j) s = __dsub_rn(s, __dmul_rn(__ldg(L + (i * PS + j) * SL), T[j]));
-      T[i] = RC ? div_rn_recip(s, __ldg(L + (i * PS + i) * SL), __ldg(R + i * SL))
-                : __ddiv_rn(s, __ldg(L + (i * PS + i) * SL));
+      T[i] = __ddiv_rn(s, __ldg(L + (i * PS + i) * SL));
     }
     // ---- w = v - A t (mat_vec) and s = A^T w (mat_tvec) in one pass over
     // A: row i gives w_i, then immediately its contribution to every s_j
@@ -493,7 +485,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     double S[PS];
 #pragma unroll
     for (int j = 0; j < PS; ++j) S[j] = 0.0;
-#pragma unroll MU
+#pragma unroll 1
     for (int i = 0; i < PS; ++i) {
       const double* Ai = A + i * PS * SA;
       double acc = 0.0;
@@ -507,8 +499,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     // ---- t = B^{-T} s (lu_solve_transpose_into, dense.cpp:102-120)
 #pragma unroll
     for (int j = 0; j < PS; ++j) {  // column-oriented, as the forward solve above
-      S[j] = RC ? div_rn_recip(S[j], __ldg(L + (j * PS + j) * SL), __ldg(R + j * SL))
-                : __ddiv_rn(S[j], __ldg(L + (j * PS + j) * SL));
+      S[j] = __ddiv_rn(S[j], __ldg(L + (j * PS + j) * SL));
 #pragma unroll
       for (int i = j + 1; i < PS; ++i) S[i] = __dsub_rn(S[i], __dmul_rn(__ldg(L + (j * PS + i) * SL), S[j]));
     }
@@ -549,14 +540,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
         done = true;
         result = 0.0;
       } else {
-        if (RC) {
-          const double y = __ddiv_rn(1.0, un2);
 #pragma unroll
-          for (int i = 0; i < PS; ++i) V[i * BD] = div_rn_recip(Tv[i * BD], un2, y);
-        } else {
-#pragma unroll
-          for (int i = 0; i < PS; ++i) V[i * BD] = __ddiv_rn(Tv[i * BD], un2);
-        }
+        for (int i = 0; i < PS; ++i) V[i * BD] = __ddiv_rn(Tv[i * BD], un2);
         if (it == 200) {
           done = true;
           result = __dsqrt_rn(lambda);
@@ -572,42 +557,16 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   if (iters_total && my_iters) atomicAdd(iters_total, my_iters);
 }
 
-template <int PS, bool IL = false, int MU = 1, bool RC = false>
+template <int PS, bool IL = false>
 bool launch_spectral_tile(int64_t npat, const int32_t* pid, int64_t ne, const double* mats, const double* lu,
-                          const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s,
-                          const double* rdiag = nullptr) {
+                          const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
   const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
-  cudaFuncSetAttribute(spectral_tile_kernel<PS, IL, MU, RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(spectral_tile_kernel<PS, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(grid_for(npat, kTileA), (unsigned)((ne + kTileE - 1) / kTileE));
-  spectral_tile_kernel<PS, IL, MU, RC><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters,
-                                                                         rdiag);
+  spectral_tile_kernel<PS, IL><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters);
   return true;
 }
 
-template <int PS>
-void launch_spectral_il(int64_t npat, int64_t ne, const double* mats_il, const double* lu_il, const int32_t* piv_il,
-                        const double* rdiag_il, double* d, unsigned long long* iters, cudaStream_t s) {
-  // reciprocal-based exact division: opt-in (PDB_SPECTRAL_RECIP=1); measured
-  // slower (584-718 vs 826 M pair-iterations/s at config 2) -- the inlined
-  // sequences cost more registers and scheduling slack than the IEEE
-  // division subroutine saves
-  const char* e = getenv("PDB_SPECTRAL_RECIP");
-  if (e && e[0] == '1')
-    launch_spectral_tile<PS, true, 1, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, rdiag_il);
-  else
-    launch_spectral_tile<PS, true, 1, false>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, rdiag_il);
-}
-
-// rdiag[((g * ps) + i) * 8 + a] = RN(1 / u_ii) of factor g * 8 + a (1 past count)
-__global__ void recip_diag_kernel(int64_t total, int64_t count, int ps, const double* __restrict__ lu,
-                                  double* __restrict__ rdiag) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= total) return;
-  const int a = (int)(e % kTileE);
-  const int64_t i = (e / kTileE) % ps, g = e / ((int64_t)kTileE * ps);
-  const int64_t f = g * kTileE + a;
-  rdiag[e] = f < count ? __ddiv_rn(1.0, lu[f * ps * ps + i * ps + i]) : 1.0;
-}
 
 // dst[((g * len) + q) * width + a] = src[(g * width + a) * len + q]; zero past `count` items
 template <typename T>
@@ -726,22 +685,20 @@ void interleave_patches(int64_t count, int64_t len, const double* src, double* d
 }
 
 void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* piv, double* lu_il, int32_t* piv_il,
-                        double* rdiag_il, cudaStream_t s) {
+                        cudaStream_t s) {
   const int64_t len = (int64_t)ps * ps;
   const int64_t t1 = interleaved_len(count, kTileE, len), t2 = interleaved_len(count, kTileE, ps);
   if (t1 > 0) interleave_kernel<double><<<grid_for(t1, 256), 256, 0, s>>>(t1, count, kTileE, len, lu, lu_il);
   if (t2 > 0) interleave_kernel<int32_t><<<grid_for(t2, 256), 256, 0, s>>>(t2, count, kTileE, ps, piv, piv_il);
-  if (t2 > 0) recip_diag_kernel<<<grid_for(t2, 256), 256, 0, s>>>(t2, count, ps, lu, rdiag_il);
 }
 
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
-                       const int32_t* piv_il, const double* rdiag_il, double* d, unsigned long long* iters,
-                       cudaStream_t s) {
+                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s) {
   switch (ps) {
-    case 9: launch_spectral_il<9>(npat, ne, mats_il, lu_il, piv_il, rdiag_il, d, iters, s); break;
-    case 22: launch_spectral_il<22>(npat, ne, mats_il, lu_il, piv_il, rdiag_il, d, iters, s); break;
-    case 25: launch_spectral_il<25>(npat, ne, mats_il, lu_il, piv_il, rdiag_il, d, iters, s); break;
-    case 27: launch_spectral_il<27>(npat, ne, mats_il, lu_il, piv_il, rdiag_il, d, iters, s); break;
+    case 9: launch_spectral_tile<9, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 22: launch_spectral_tile<22, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 25: launch_spectral_tile<25, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 27: launch_spectral_tile<27, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
     default: break;
   }
 }

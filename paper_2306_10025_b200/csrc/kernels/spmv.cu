@@ -1,0 +1,368 @@
+// Residual r = b - A x and SpMV y = A x (reference spmv sparse.cpp:50-63,
+// the residual of smooth precond.cpp:95-97).
+//
+// Three kernels, chosen by plan_of (matrix.cpp):
+//   residual_sell_kernel (default)  the SELL-C-sigma copy built at upload:
+//       warp per 32-row slice, lane per row, coalesced column-major steps,
+//       each row summed in CSR order with unfused multiply/add -> bitwise the
+//       reference's residual;
+//   residual_v5_kernel              CSR warp items (<= 31 rows / 256 nonzeros),
+//       coalesced item loads, products reduced per row through shared memory
+//       (PDB_SPMV_VERSION=5, or when no SELL copy exists);
+//   residual_v2_kernel              G lanes per row, for plans without a row
+//       partition (PDB_SPMV_VERSION=2).
+// With block_sumsq the kernels also write one sum of r^2 per block (residual
+// histories, finished by finish_sum in a fixed order: deterministic).
+#include "../kernels.hpp"
+#include "pdl.cuh"
+
+namespace pdb::k {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// -- v2: G lanes per row, E entries per lane loaded before use -------------
+template <int G, int E>
+__global__ void __launch_bounds__(kBlock) residual_v2_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                             const int32_t* __restrict__ col,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ x,
+                                                             const double* __restrict__ b, double* __restrict__ r,
+                                                             double* __restrict__ block_sumsq, bool negate_b_absent) {
+  const int lane = threadIdx.x % G;
+  const int64_t row = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
+  double acc = 0.0;
+  if (row < n) {
+    const int64_t lo = rp[row], hi = rp[row + 1];
+    for (int64_t base = lo; base < hi; base += G * E) {
+      int32_t c[E];
+      double v[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t p = base + lane + e * G;
+        c[e] = p < hi ? __ldcs(col + p) : -1;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t p = base + lane + e * G;
+        v[e] = p < hi ? __ldcs(val + p) : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc += c[e] >= 0 ? v[e] * __ldg(x + c[e]) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
+  double rv = 0.0;
+  if (row < n) {
+    rv = b ? b[row] - acc : (negate_b_absent ? -acc : acc);
+    if (lane == 0) r[row] = rv;
+  }
+  if (block_sumsq) {
+    __shared__ double red[kBlock / 32];
+    double sq = (lane == 0 && row < n) ? rv * rv : 0.0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < kBlock / 32; ++w) t += red[w];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// -- v5: warp items ---------------------------------------------------------
+// A precomputed partition gives every warp a run of <= 31 consecutive rows
+// holding <= 256 nonzeros.  The warp loads that contiguous span with fully
+// coalesced 32-lane loads, gathers x, stages the products in a per-warp
+// shared-memory slice (no block barrier), then 4-lane groups reduce the rows.
+// A row longer than 256 nonzeros gets a warp to itself and loops.
+constexpr int kV5Warps = 8;
+constexpr int kV5Per = 8;
+constexpr int kV5Rows = 31;
+
+__global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
+    int nwarps, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
+    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
+    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
+    bool negate_b_absent) {
+  constexpr int PER = kV5Per;
+  __shared__ double prod[kV5Warps][32 * PER];
+  __shared__ double red[kV5Warps];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kV5Warps + wib;
+  double sq = 0.0;
+  if (w < nwarps) {
+    const int64_t r0 = __ldg(wstart + w), base = __ldg(wbase + w), end = __ldg(wbase + w + 1);
+    const int nrows = __ldg(wstart + w + 1) - (int)r0;
+    const int nnz = (int)(end - base);
+    const int64_t rpl = lane <= nrows ? __ldg(rp + r0 + lane) : end;
+    const double bl = (b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
+    if (nnz <= 32 * PER) {
+      int32_t c[PER];
+      double v[PER];
+      const int32_t* cp = col + base + lane;
+      const double* vp = val + base + lane;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) c[e] = e * 32 + lane < nnz ? __ldcs(cp + e * 32) : 0;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(vp + e * 32) : 0.0;
+      double* pw = prod[wib];
+#pragma unroll
+      for (int e = 0; e < PER; ++e)
+        if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * __ldg(x + c[e]);
+      __syncwarp();
+      const int g4 = lane & 3, grp = lane >> 2;
+      for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
+        const int rr = rr0 + grp;
+        const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
+        const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
+        const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
+        double a = 0.0;
+        if (rr < nrows)
+          for (int e = lo + g4; e < hi; e += 4) a += pw[e];
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        if (rr < nrows && g4 == 0) {
+          const double rv = b ? brr - a : (negate_b_absent ? -a : a);
+          r[r0 + rr] = rv;
+          sq += rv * rv;
+        }
+      }
+    } else {  // one long row
+      double a = 0.0;
+      for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) {
+        const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
+        r[r0] = rv;
+        sq += rv * rv;
+      }
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kV5Warps; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+// -- SELL-C-sigma (default) -------------------------------------------------
+// Warp per slice of 32 rows, lane l owns slice row l.  Step j loads entry j
+// of all 32 rows -- one 256-byte value span and one 128-byte column span,
+// fully coalesced -- and the x gathers of 32 similar rows hit a few lines.  U
+// steps are loaded before any is consumed (the first group before the
+// programmatic-launch wait: matrix bytes do not depend on the predecessor),
+// an L2 bulk prefetch runs pf step groups ahead, lanes past their row's end
+// are predicated off, and each lane accumulates its row in CSR order with
+// unfused multiply/add: r = b - s bit for bit as the reference spmv + smooth
+// (sparse.cpp:50-63, precond.cpp:95-97).  The explicit minimum of 1 block
+// per SM lets ptxas keep the next step group's loads in flight (72 registers
+// at U = 8; without it the allocation drops to 48 and the kernel loses ~4 %).
+template <int U>
+__global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
+                                                            const int2* __restrict__ srow,
+                                                            const double* __restrict__ sval,
+                                                            const int32_t* __restrict__ scol,
+                                                            const double* __restrict__ x, const double* __restrict__ b,
+                                                            double* __restrict__ r, double* __restrict__ block_sumsq,
+                                                            bool negate_b_absent, int pf) {
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
+  double sq = 0.0;
+  if (sl >= nslices) {
+    grid_dep_wait();
+    grid_dep_trigger();
+  }
+  if (sl < nslices) {
+    const int2 rl = __ldg(srow + sl * 32 + lane);
+    const int len = rl.y;
+    const int L = __reduce_max_sync(0xffffffffu, (unsigned)len);
+    const int64_t o = __ldg(soff + sl);
+    const double* vp = sval + o + lane;
+    const int32_t* cp = scol + o + lane;
+    const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
+    double acc = 0.0;
+    int32_t c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = u < len ? __ldcs(cp + (int64_t)u * 32) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = u < len ? __ldcs(vp + (int64_t)u * 32) : 0.0;
+    grid_dep_wait();  // x is the predecessor's (the scatter's) output
+    grid_dep_trigger();
+    for (int j = 0; j < L; j += U) {
+      if (pf > 0 && lane == 0) {
+        const int jn = j + pf * U;
+        if (jn < L) {
+          const int cnt = (L - jn < U ? L - jn : U) * 32;
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + o + (int64_t)jn * 32),
+                       "r"((unsigned)(cnt * 8)));
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + o + (int64_t)jn * 32),
+                       "r"((unsigned)(cnt * 4)));
+        }
+      }
+      if (j > 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
+      }
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = j + u < len ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    if (rl.x >= 0) {
+      const double rv = b ? __dsub_rn(bl, acc) : (negate_b_absent ? -acc : acc);
+      r[rl.x] = rv;
+      sq += rv * rv;
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+__global__ void finish_sum_kernel(const double* __restrict__ partials, int count, double* out, bool take_sqrt) {
+  __shared__ double red[1024];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) t += partials[i];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = take_sqrt ? sqrt(red[0]) : red[0];
+}
+
+template <int G>
+void launch_v2(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+               const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+  if (p.entries == 4)
+    residual_v2_kernel<G, 4><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+  else
+    residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+}
+
+void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
+                       const double* x, const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+  if (n <= 0) return;
+  if (p.version == 9 && p.sell_off) {
+    const int2* sr = reinterpret_cast<const int2*>(p.sell_row);
+    // L2 bulk prefetch one step group ahead (PDB_SELL_PF; measured best at 1)
+    const char* pfe = getenv("PDB_SELL_PF");
+    const int pf = pfe ? atoi(pfe) : 1;
+    if (p.entries == 4)
+      launch_pdl(residual_sell_kernel<4>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf);
+    else
+      launch_pdl(residual_sell_kernel<8>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf);
+    return;
+  }
+  if (p.version == 5 && p.blk_start) {
+    residual_v5_kernel<<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
+                                                          sumsq, negate);
+    return;
+  }
+  switch (p.group) {
+    case 2: launch_v2<2>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+    case 4: launch_v2<4>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+    case 8: launch_v2<8>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+    case 16: launch_v2<16>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+    default: launch_v2<32>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+  }
+}
+
+}  // namespace
+
+std::vector<int32_t> item_partition(int64_t n, const int64_t* rp) {
+  // warp items: consecutive rows, <= kV5Rows rows and <= 32*kV5Per nonzeros;
+  // a longer row forms an item alone
+  const int64_t cap_nnz = 32 * (int64_t)kV5Per;
+  std::vector<int32_t> starts;
+  starts.push_back(0);
+  int64_t row = 0;
+  while (row < n) {
+    const int64_t b0 = rp[row];
+    int64_t end = row + 1;
+    while (end < n && end - row < kV5Rows && rp[end + 1] - b0 <= cap_nnz) ++end;
+    if (rp[row + 1] - b0 > cap_nnz) end = row + 1;
+    starts.push_back((int32_t)end);
+    row = end;
+  }
+  return starts;
+}
+
+SpmvPlan spmv_plan(int64_t n, int64_t nnz) {
+  SpmvPlan p;
+  const double avg = n > 0 ? (double)nnz / (double)n : 1.0;
+  // G * E ~ the typical row length (config 2, avg 36: G=4, E=8; config 3, avg 61: G=8, E=8)
+  p.version = 2;
+  p.entries = 8;
+  p.group = avg <= 16 ? 2 : avg <= 48 ? 4 : 8;
+  p.rows_per_block = kBlock / p.group;
+  p.blocks = (int)((n + p.rows_per_block - 1) / p.rows_per_block);
+  return p;
+}
+
+SpmvPlan spmv_plan_items(int64_t n, int64_t nnz, const int32_t* item_start, const int64_t* item_base, int nitems) {
+  SpmvPlan p = spmv_plan(n, nnz);
+  if (!item_start || !item_base || nitems <= 0) return p;
+  p.version = 5;
+  p.entries = kV5Per;
+  p.blk_start = item_start;
+  p.blk_base = item_base;
+  p.nblk = nitems;
+  p.blocks = (nitems + kV5Warps - 1) / kV5Warps;
+  return p;
+}
+
+void residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+              const double* b, double* r, double* block_sumsq, cudaStream_t s) {
+  dispatch_residual(p, n, rp, col, val, x, b, r, block_sumsq, true, s);
+}
+
+void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x, const double* b, double* r,
+                     cudaStream_t s) {
+  if (s1 <= s0 || p.version != 9) return;
+  const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
+  residual_sell_kernel<8><<<grid_for(s1 - s0, 8), 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x,
+                                                               b, r, nullptr, true, 1);
+}
+
+void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+          double* y, cudaStream_t s) {
+  dispatch_residual(p, n, rp, col, val, x, nullptr, y, nullptr, false, s);
+}
+
+void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s) {
+  finish_sum_kernel<<<1, 1024, 0, s>>>(partials, count, out, sqrt_result);
+}
+
+}  // namespace pdb::k

@@ -2,908 +2,27 @@
 // (reference: smooth precond.cpp:90-101, PatchPreconditioner::apply
 // precond.cpp:58-88, spmv sparse.cpp:50-63).
 //
-// Three kernels per sweep, each HBM- or L2-bound:
-//   residual      r = b - A x           sub-warp per row, coalesced CSR streams,
-//                                       optional deterministic per-block sum r^2
-//   patch_solve   sols_k = B^{-1} r|_k  sub-warp per patch, lane i owns local row i,
-//                                       column-major factors -> lane-contiguous loads,
-//                                       compressed factors stay L2-resident
-//   scatter_update x += omega W sum sols owner-computes gather through the
-//                                       DoF -> (patch, slot) inverse map in ascending
-//                                       patch order: the reference's serial scatter
-//                                       order (precond.cpp:81-86), no atomics
-// r (8n B) and sols (8 np ps B) are produced and consumed back to back, so
-// they are L2 hits on the 126 MB L2 for c1-c4 sizes.
+// Patch stage and scatter (the residual is in spmv.cu):
+//   patch_apply_dmma   compressed mode: tiles of <= 32 patches sharing a database
+//                      entry, B^{-1} [r_k1 .. r_k32] on the FP64 tensor cores
+//   patch_apply_inv    one patch per sub-block with its explicit inverse (exact
+//                      mode, small databases); patch_solve: triangular solves
+//                      on the LU factors (PDB_APPLY=lu)
+//   scatter_update_pad x += omega W sum sols: owner-computes gather through the
+//                      DoF -> (patch, slot) inverse map in ascending patch order,
+//                      the reference's serial scatter order (precond.cpp:81-86),
+//                      no atomics
+// plus the setup kernels of these structures (inverses, inverse maps).
 #include <cub/cub.cuh>
 
 #include "../kernels.hpp"
+#include "pdl.cuh"
 
 namespace pdb::k {
 
 namespace {
 
 constexpr int kBlock = 256;
-
-// Programmatic dependent launch (sm_90+).  The three sweep kernels are
-// launched with programmatic stream serialization: each one issues the loads
-// that do not depend on its predecessor (matrix values/columns, tile indices,
-// inverse-map slots, x) before griddepcontrol.wait, which returns once the
-// predecessor grid has completed and its writes are visible.  Each kernel
-// lets its dependent launch only after its own wait (so completion stays
-// transitive along the stream); the dependent's CTAs then occupy SMs freed by
-// the primary's last wave.  Without the launch attribute both are no-ops.
-__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void grid_dep_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
-bool pdl_enabled() {
-  const char* e = getenv("PDB_PDL");
-  return !(e && e[0] == '0');
-}
-
-template <typename... KArgs, typename... Args>
-void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
-// Streaming loads that bypass L1 allocation (the CSR arrays are read once per
-// sweep), keeping L1 for the reused x gathers.
-__device__ __forceinline__ double ld_stream(const double* p) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ int32_t ld_stream(const int32_t* p) {
-  int32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ double ld_keep(const double* p) {
-  double v;
-  asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-}
-
-template <int G>
-__global__ void __launch_bounds__(kBlock) residual_kernel(int64_t n, const int64_t* __restrict__ rp,
-                                                          const int32_t* __restrict__ col,
-                                                          const double* __restrict__ val,
-                                                          const double* __restrict__ x, const double* __restrict__ b,
-                                                          double* __restrict__ r, double* __restrict__ block_sumsq,
-                                                          bool negate_b_absent) {
-  const int lane = threadIdx.x % G;
-  const int64_t row = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
-  double acc = 0.0;
-  if (row < n) {
-    const int64_t lo = rp[row], hi = rp[row + 1];
-    // Four independent (col, val, x) streams in flight per lane: the col -> x
-    // gather is a dependent load, so memory-level parallelism comes from
-    // issuing several entries before consuming any.
-    int64_t p = lo + lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (; p + 3 * G < hi; p += 4 * G) {
-      const int32_t c0 = __ldg(col + p), c1 = __ldg(col + p + G), c2 = __ldg(col + p + 2 * G),
-                    c3 = __ldg(col + p + 3 * G);
-      const double v0 = __ldg(val + p), v1 = __ldg(val + p + G), v2 = __ldg(val + p + 2 * G),
-                   v3 = __ldg(val + p + 3 * G);
-      a0 += v0 * __ldg(x + c0);
-      a1 += v1 * __ldg(x + c1);
-      a2 += v2 * __ldg(x + c2);
-      a3 += v3 * __ldg(x + c3);
-    }
-    for (; p < hi; p += G) a0 += __ldg(val + p) * __ldg(x + __ldg(col + p));
-    acc = (a0 + a1) + (a2 + a3);
-  }
-#pragma unroll
-  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-  double rv = 0.0;
-  if (row < n) {
-    rv = b ? b[row] - acc : (negate_b_absent ? -acc : acc);
-    if (lane == 0) r[row] = rv;
-  }
-  if (block_sumsq) {
-    __shared__ double red[kBlock / 32];
-    double sq = (lane == 0 && row < n) ? rv * rv : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kBlock / 32; ++w) t += red[w];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v2: a G-lane group per row loads up to E entries per lane in three
-// batched steps (all columns, then all values with streaming cache hints,
-// then all x gathers through L1) before any arithmetic, so a row costs three
-// memory latencies instead of one per entry batch.  Longer rows loop.
-template <int G, int E, int H = 0>
-__global__ void __launch_bounds__(kBlock) residual_v2_kernel(int64_t n, const int64_t* __restrict__ rp,
-                                                             const int32_t* __restrict__ col,
-                                                             const double* __restrict__ val,
-                                                             const double* __restrict__ x,
-                                                             const double* __restrict__ b, double* __restrict__ r,
-                                                             double* __restrict__ block_sumsq, bool negate_b_absent) {
-  const int lane = threadIdx.x % G;
-  const int64_t row = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
-  double acc = 0.0;
-  if (row < n) {
-    const int64_t lo = rp[row], hi = rp[row + 1];
-    for (int64_t base = lo; base < hi; base += G * E) {
-      int32_t c[E];
-      double v[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t p = base + lane + e * G;
-        c[e] = p < hi ? (H ? ld_stream(col + p) : __ldcs(col + p)) : -1;
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int64_t p = base + lane + e * G;
-        v[e] = p < hi ? (H ? ld_stream(val + p) : __ldcs(val + p)) : 0.0;
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc += c[e] >= 0 ? v[e] * (H ? ld_keep(x + c[e]) : __ldg(x + c[e])) : 0.0;
-    }
-  }
-#pragma unroll
-  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off, G);
-  double rv = 0.0;
-  if (row < n) {
-    rv = b ? b[row] - acc : (negate_b_absent ? -acc : acc);
-    if (lane == 0) r[row] = rv;
-  }
-  if (block_sumsq) {
-    __shared__ double red[kBlock / 32];
-    double sq = (lane == 0 && row < n) ? rv * rv : 0.0;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kBlock / 32; ++w) t += red[w];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v3 ("CSR stream"): each block owns a contiguous row range whose
-// nonzeros (<= kStreamNnz) it streams with fully coalesced loads -- all
-// column indices, then all values, then the x gathers, kStreamPer
-// independent loads in flight per thread -- into shared-memory products;
-// 8-lane groups then reduce the rows out of shared memory.  Row ranges come
-// from a per-matrix partition (DeviceCsr::blk_start, built at upload); a row
-// longer than kStreamNnz gets a block to itself and is reduced block-wide.
-constexpr int kStreamThreads = 256;
-constexpr int kStreamPer = 8;   // base partition: 2048 nonzeros / 512 rows per block
-constexpr int kStreamNnz = kStreamThreads * kStreamPer;
-constexpr int kStreamRows = 512;
-
-template <int PER>
-__global__ void __launch_bounds__(kStreamThreads) residual_v3_kernel(
-    int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-    const int32_t* __restrict__ blk_start, const int64_t* __restrict__ blk_base, double* __restrict__ block_sumsq,
-    bool negate_b_absent) {
-  constexpr int NNZ = kStreamThreads * PER;
-  constexpr int ROWS = kStreamRows;
-  __shared__ double prod[NNZ];
-  __shared__ int64_t rps[ROWS + 1];
-  __shared__ double bs[ROWS];
-  __shared__ double red[kStreamThreads / 32];
-  const int tid = threadIdx.x;
-  // block descriptors are independent loads: the CSR streams can start
-  // immediately instead of waiting for row_ptr
-  const int64_t r0 = __ldg(blk_start + blockIdx.x), r1 = __ldg(blk_start + blockIdx.x + 1);
-  const int64_t base = __ldg(blk_base + blockIdx.x), end = __ldg(blk_base + blockIdx.x + 1);
-  const int nrows = (int)(r1 - r0);
-  double sq = 0.0;
-  if (end - base <= NNZ) {
-    const int m = (int)(end - base) - tid;  // entries this thread may touch: k*T < m
-    const int32_t* cp = col + base + tid;
-    const double* vp = val + base + tid;
-    int32_t c[PER];
-    double v[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) c[k] = k * kStreamThreads < m ? __ldcs(cp + k * kStreamThreads) : 0;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) v[k] = k * kStreamThreads < m ? __ldcs(vp + k * kStreamThreads) : 0.0;
-    for (int t = tid; t <= nrows; t += kStreamThreads) rps[t] = __ldg(rp + r0 + t);
-    if (b)
-      for (int t = tid; t < nrows; t += kStreamThreads) bs[t] = __ldcs(b + r0 + t);
-#pragma unroll
-    for (int k = 0; k < PER; ++k)
-      if (k * kStreamThreads < m) prod[tid + k * kStreamThreads] = v[k] * __ldg(x + c[k]);
-    __syncthreads();
-    const int lane8 = tid & 7;
-    // warp-uniform trip count: every lane reaches the shuffles
-    for (int rr0 = (tid >> 5) * 4; rr0 < nrows; rr0 += kStreamThreads / 8) {
-      const int rr = rr0 + ((tid >> 3) & 3);
-      const bool has = rr < nrows;
-      const int lo = has ? (int)(rps[rr] - base) : 0, hi = has ? (int)(rps[rr + 1] - base) : 0;
-      double a = 0.0;
-      for (int e = lo + lane8; e < hi; e += 8) a += prod[e];
-      a += __shfl_xor_sync(0xffffffffu, a, 4);
-      a += __shfl_xor_sync(0xffffffffu, a, 2);
-      a += __shfl_xor_sync(0xffffffffu, a, 1);
-      if (has && lane8 == 0) {
-        const double rv = b ? bs[rr] - a : (negate_b_absent ? -a : a);
-        r[r0 + rr] = rv;
-        sq += rv * rv;
-      }
-    }
-  } else {  // one long row (nrows == 1)
-    double a = 0.0;
-    for (int64_t e = base + tid; e < end; e += kStreamThreads) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-    if ((tid & 31) == 0) red[tid >> 5] = a;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kStreamThreads / 32; ++w) t += red[w];
-      const double rv = b ? b[r0] - t : (negate_b_absent ? -t : t);
-      r[r0] = rv;
-      sq = rv * rv;
-    }
-    __syncthreads();
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if ((tid & 31) == 0) red[tid >> 5] = sq;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kStreamThreads / 32; ++w) t += red[w];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v4: the v3 chunk structure run by a persistent grid with a
-// two-stage software pipeline -- while a block reduces chunk k out of shared
-// memory, the column/value/row_ptr/b loads of its next chunk are already in
-// flight in registers, so HBM never waits for the reduction phase.
-constexpr int kV4Threads = 256;
-constexpr int kV4Per = 8;
-constexpr int kV4Rows = kStreamRows;                 // partition row cap (shared with v3)
-constexpr int kV4RowRegs = (kV4Rows + 1 + kV4Threads - 1) / kV4Threads;  // 3
-
-struct V4Chunk {
-  int64_t r0, base;
-  int nrows, nnz;
-  int32_t c[kV4Per];
-  double v[kV4Per];
-  int64_t rpv[kV4RowRegs];
-  double bv[kV4RowRegs];
-};
-
-__device__ __forceinline__ void v4_load(V4Chunk& ck, int ch, const int32_t* __restrict__ blk_start,
-                                        const int64_t* __restrict__ blk_base, const int64_t* __restrict__ rp,
-                                        const int32_t* __restrict__ col, const double* __restrict__ val,
-                                        const double* __restrict__ b, int tid) {
-  ck.r0 = __ldg(blk_start + ch);
-  const int64_t r1 = __ldg(blk_start + ch + 1);
-  ck.base = __ldg(blk_base + ch);
-  const int64_t end = __ldg(blk_base + ch + 1);
-  ck.nrows = (int)(r1 - ck.r0);
-  ck.nnz = (int)(end - ck.base);
-  if (ck.nnz <= kV4Threads * kV4Per) {
-    const int m = ck.nnz - tid;
-    const int32_t* cp = col + ck.base + tid;
-    const double* vp = val + ck.base + tid;
-#pragma unroll
-    for (int k = 0; k < kV4Per; ++k) ck.c[k] = k * kV4Threads < m ? __ldcs(cp + k * kV4Threads) : 0;
-#pragma unroll
-    for (int k = 0; k < kV4Per; ++k) ck.v[k] = k * kV4Threads < m ? __ldcs(vp + k * kV4Threads) : 0.0;
-  }
-#pragma unroll
-  for (int q = 0; q < kV4RowRegs; ++q) {
-    const int t = tid + q * kV4Threads;
-    ck.rpv[q] = t <= ck.nrows ? __ldg(rp + ck.r0 + t) : 0;
-    ck.bv[q] = (b && t < ck.nrows) ? __ldcs(b + ck.r0 + t) : 0.0;
-  }
-}
-
-__global__ void __launch_bounds__(kV4Threads, 3) residual_v4_kernel(
-    int nblk, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-    const int32_t* __restrict__ blk_start, const int64_t* __restrict__ blk_base, double* __restrict__ block_sumsq,
-    bool negate_b_absent) {
-  __shared__ double prod[kV4Threads * kV4Per];
-  __shared__ int64_t rps[kV4Rows + 1];
-  __shared__ double bs[kV4Rows];
-  __shared__ double red[kV4Threads / 32];
-  const int tid = threadIdx.x;
-  double sq = 0.0;
-  int ch = blockIdx.x;
-  V4Chunk cur, nxt;
-  if (ch < nblk) v4_load(cur, ch, blk_start, blk_base, rp, col, val, b, tid);
-  while (ch < nblk) {
-    const int nch = ch + gridDim.x;
-    if (nch < nblk) v4_load(nxt, nch, blk_start, blk_base, rp, col, val, b, tid);  // in flight during the work below
-#pragma unroll
-    for (int q = 0; q < kV4RowRegs; ++q) {
-      const int t = tid + q * kV4Threads;
-      if (t <= cur.nrows) rps[t] = cur.rpv[q];
-      if (t < cur.nrows) bs[t] = cur.bv[q];
-    }
-    if (cur.nnz <= kV4Threads * kV4Per) {
-      const int m = cur.nnz - tid;
-#pragma unroll
-      for (int k = 0; k < kV4Per; ++k)
-        if (k * kV4Threads < m) prod[tid + k * kV4Threads] = cur.v[k] * __ldg(x + cur.c[k]);
-      __syncthreads();
-      const int lane8 = tid & 7;
-      for (int rr0 = (tid >> 5) * 4; rr0 < cur.nrows; rr0 += kV4Threads / 8) {
-        const int rr = rr0 + ((tid >> 3) & 3);
-        const bool has = rr < cur.nrows;
-        const int lo = has ? (int)(rps[rr] - cur.base) : 0, hi = has ? (int)(rps[rr + 1] - cur.base) : 0;
-        double a = 0.0;
-        for (int e = lo + lane8; e < hi; e += 8) a += prod[e];
-        a += __shfl_xor_sync(0xffffffffu, a, 4);
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        if (has && lane8 == 0) {
-          const double rv = b ? bs[rr] - a : (negate_b_absent ? -a : a);
-          r[cur.r0 + rr] = rv;
-          sq += rv * rv;
-        }
-      }
-    } else {  // one long row
-      double a = 0.0;
-      const int64_t end = cur.base + cur.nnz;
-      for (int64_t e = cur.base + tid; e < end; e += kV4Threads) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-      if ((tid & 31) == 0) red[tid >> 5] = a;
-      __syncthreads();
-      if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kV4Threads / 32; ++w) t += red[w];
-        const double rv = b ? b[cur.r0] - t : (negate_b_absent ? -t : t);
-        r[cur.r0] = rv;
-        sq += rv * rv;
-      }
-    }
-    __syncthreads();
-    cur = nxt;
-    ch = nch;
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if ((tid & 31) == 0) red[tid >> 5] = sq;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < kV4Threads / 32; ++w) t += red[w];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v5: warp-granular CSR streaming.  A precomputed partition gives
-// every warp a run of <= 31 consecutive rows holding <= 256 nonzeros.  The
-// warp loads that contiguous span with fully coalesced 32-lane loads (one
-// 128-byte line per column load, two per value load: ~8x fewer L1 wavefronts
-// than a group-per-row layout), gathers x, stages the products in a per-warp
-// shared-memory slice (no block barrier), then 4-lane groups reduce the rows.
-// A row longer than 256 nonzeros gets a warp to itself and loops.
-constexpr int kV5Warps = 8;
-constexpr int kV5Per = 8;
-constexpr int kV5Rows = 31;
-
-// CHUNK selects the row reduction.  false: 4-lane groups stride through each
-// row's products (8 rows at a time; rows of unequal length leave lanes idle
-// and the 8 row offsets collide in smem banks).  true (v6): lane l sums its
-// own PER consecutive products, cutting at row starts (a 32*PER-bit boundary
-// mask), and writes each segment sum at the segment's first position; lane
-// rho then adds the segment sums of row rho in ascending position.  Products
-// live at i + i/PER so both the slot-interleaved stores and the lane-chunk
-// reads are bank-conflict free; ~3x fewer shared-memory wavefronts.
-template <int PER, bool CHUNK>
-__global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
-    int nwarps, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
-    bool negate_b_absent, int prefetch_dist) {
-  constexpr int kSlots = CHUNK ? 32 * PER + 32 : 32 * PER;
-  constexpr int kMaskWords = PER;  // 32*PER bits
-  __shared__ double prod[kV5Warps][kSlots];
-  __shared__ uint32_t bmask[kV5Warps][CHUNK ? kMaskWords : 1];
-  __shared__ double red[kV5Warps];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int w = blockIdx.x * kV5Warps + wib;
-  double sq = 0.0;
-  if (w < nwarps) {
-    // Bulk L2 prefetch (cp.async.bulk.prefetch, one instruction per stream)
-    // of the CSR span a warp one prefetch distance ahead will read, so that
-    // warp finds its columns/values in L2 instead of waiting on HBM.
-    if (prefetch_dist > 0 && lane < 2) {
-      const int wf = w + prefetch_dist;
-      if (wf < nwarps) {
-        const int64_t fb = __ldg(wbase + wf), fe = __ldg(wbase + wf + 1);
-        const char* p0 = lane == 0 ? reinterpret_cast<const char*>(val + fb) : reinterpret_cast<const char*>(col + fb);
-        const char* p1 = lane == 0 ? reinterpret_cast<const char*>(val + fe) : reinterpret_cast<const char*>(col + fe);
-        const uintptr_t a0 = reinterpret_cast<uintptr_t>(p0) & ~uintptr_t(15);
-        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p1) + 15) & ~uintptr_t(15);
-        if (a1 > a0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
-      }
-    }
-    const int64_t r0 = __ldg(wstart + w), base = __ldg(wbase + w), end = __ldg(wbase + w + 1);
-    const int nrows = __ldg(wstart + w + 1) - (int)r0;
-    const int nnz = (int)(end - base);
-    const int64_t rpl = lane <= nrows ? __ldg(rp + r0 + lane) : end;
-    const double bl = (b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
-    if (nnz <= (32 * PER)) {
-      int32_t c[PER];
-      double v[PER];
-      const int32_t* cp = col + base + lane;
-      const double* vp = val + base + lane;
-#pragma unroll
-      for (int e = 0; e < PER; ++e) c[e] = e * 32 + lane < nnz ? __ldcs(cp + e * 32) : 0;
-#pragma unroll
-      for (int e = 0; e < PER; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(vp + e * 32) : 0.0;
-      double* pw = prod[wib];
-      if constexpr (CHUNK) {
-        uint32_t* mk = bmask[wib];
-        if (lane < kMaskWords) mk[lane] = 0u;
-        // products at padded position i + i/PER
-#pragma unroll
-        for (int e = 0; e < PER; ++e) {
-          const int i = e * 32 + lane;
-          if (i < nnz) pw[i + i / PER] = v[e] * __ldg(x + c[e]);
-        }
-        __syncwarp();
-        const int o = (int)(rpl - base);  // start of row `lane` (lanes 1..nrows-1 mark a cut)
-        if (lane >= 1 && lane < nrows && o < nnz) atomicOr(mk + (o >> 5), 1u << (o & 31));
-        __syncwarp();
-        const int cb = lane * PER;
-        const uint32_t fl = (mk[cb >> 5] >> (cb & 31)) & (PER == 32 ? 0xffffffffu : ((1u << PER) - 1u));
-        double* pc = pw + cb + lane;  // = padded position of cb
-        double pr[PER];
-#pragma unroll
-        for (int j = 0; j < PER; ++j) pr[j] = cb + j < nnz ? pc[j] : 0.0;
-        double acc = 0.0;
-        int seg = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-          const double pj = pr[j];
-          if (j > 0 && ((fl >> j) & 1u)) {
-            pc[seg] = acc;
-            acc = 0.0;
-            seg = j;
-          }
-          acc += pj;
-        }
-        if (cb < nnz) pc[seg] = acc;
-        __syncwarp();
-        const int hi = (int)(__shfl_down_sync(0xffffffffu, rpl, 1) - base);
-        if (lane < nrows) {
-          double a = 0.0;
-          if (o < hi) {
-            a = pw[o + o / PER];
-            for (int q = o / PER + 1; q * PER < hi; ++q) a += pw[q * (PER + 1)];
-          }
-          const double rv = b ? bl - a : (negate_b_absent ? -a : a);
-          r[r0 + lane] = rv;
-          sq += rv * rv;
-        }
-      } else {
-#pragma unroll
-      for (int e = 0; e < PER; ++e)
-        if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * __ldg(x + c[e]);
-      __syncwarp();
-      const int g4 = lane & 3, grp = lane >> 2;
-      for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
-        const int rr = rr0 + grp;
-        const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
-        const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
-        const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
-        double a = 0.0;
-        if (rr < nrows)
-          for (int e = lo + g4; e < hi; e += 4) a += pw[e];
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        if (rr < nrows && g4 == 0) {
-          const double rv = b ? brr - a : (negate_b_absent ? -a : a);
-          r[r0 + rr] = rv;
-          sq += rv * rv;
-        }
-      }
-      }
-    } else {  // one long row
-      double a = 0.0;
-      for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-      if (lane == 0) {
-        const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
-        r[r0] = rv;
-        sq += rv * rv;
-      }
-    }
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if (lane == 0) red[wib] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < kV5Warps; ++q) t += red[q];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v7: v5's warp items fed by the bulk-copy (TMA) engine.  A
-// persistent grid; warp gw processes items gw, gw + TW, ... (TW = all warps,
-// so the GPU sweeps a window of consecutive rows and x stays L2-hot).  Each
-// warp owns an S-stage ring in shared memory; lane 0 arms stage s's mbarrier
-// with the byte count and issues cp.async.bulk copies of the item's values
-// and columns S items ahead, so a warp always has S items of CSR bytes in
-// flight without holding them in registers (v5 keeps ~3 KB per warp in
-// flight only during its load phase, which left DRAM at ~50 % busy).  The
-// consumer then gathers x, forms the products in place and reduces rows as
-// v5.  Copies are 16-byte aligned: the span is widened to aligned bounds
-// (the device CSR arrays carry 32 elements of zero padding) and the data
-// sits at offset base & 1 (values) / base & 3 (columns) in the stage.
-constexpr int kV7Vals = 32 * kV5Per + 4;  // 256 + alignment slack, doubles
-constexpr int kV7Cols = 32 * kV5Per + 8;  // ints
-constexpr int kV7StageBytes = kV7Vals * 8 + kV7Cols * 4;
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-template <int S>
-__global__ void __launch_bounds__(kV5Warps * 32) residual_v7_kernel(
-    int nitems, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
-    bool negate_b_absent) {
-  extern __shared__ __align__(128) unsigned char v7_smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int TW = gridDim.x * kV5Warps;
-  const int gw = blockIdx.x * kV5Warps + wib;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(v7_smem) + wib * S;
-  unsigned char* ring = v7_smem + 128 * ((kV5Warps * S * 8 + 127) / 128) + (size_t)wib * S * kV7StageBytes;
-  __shared__ double red[kV5Warps];
-  if (lane < S) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + lane)) : "memory");
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-  // issue item j into stage st (lane 0 only)
-  auto issue = [&](int j, int st) {
-    unsigned char* sg = ring + (size_t)st * kV7StageBytes;
-    const int64_t base = __ldg(wbase + j), end = __ldg(wbase + j + 1);
-    const uint32_t bar = smem_addr(bars + st);
-    if (end - base <= 32 * kV5Per) {
-      const int64_t vb = base & ~int64_t(1), cb = base & ~int64_t(3);
-      const uint32_t vbytes = (uint32_t)(((end - vb) * 8 + 15) & ~int64_t(15));
-      const uint32_t cbytes = (uint32_t)(((end - cb) * 4 + 15) & ~int64_t(15));
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(vbytes + cbytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(sg)),
-          "l"(val + vb), "r"(vbytes), "r"(bar)
-          : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(sg + kV7Vals * 8)),
-          "l"(col + cb), "r"(cbytes), "r"(bar)
-          : "memory");
-    } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-    }
-  };
-  if (lane == 0)
-    for (int q = 0; q < S; ++q)
-      if (gw + q * TW < nitems) issue(gw + q * TW, q);
-  __syncwarp();
-  double sq = 0.0;
-  int it = 0;
-  for (int j = gw; j < nitems; j += TW, ++it) {
-    const int st = it % S;
-    unsigned char* sg = ring + (size_t)st * kV7StageBytes;
-    // independent of the staged bytes: row pointers and b for this item
-    const int64_t r0 = __ldg(wstart + j);
-    const int nrows = __ldg(wstart + j + 1) - (int)r0;
-    const int64_t base = __ldg(wbase + j), end = __ldg(wbase + j + 1);
-    const int64_t rpl = lane <= nrows ? __ldg(rp + r0 + lane) : end;
-    const double bl = (b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
-    const int nnz = (int)(end - base);
-    mbar_wait(smem_addr(bars + st), (uint32_t)((it / S) & 1));
-    if (nnz <= 32 * kV5Per) {
-      double* vs = reinterpret_cast<double*>(sg) + (base & 1);
-      const int32_t* cs = reinterpret_cast<const int32_t*>(sg + kV7Vals * 8) + (base & 3);
-      int32_t c[kV5Per];
-#pragma unroll
-      for (int e = 0; e < kV5Per; ++e) c[e] = e * 32 + lane < nnz ? cs[e * 32 + lane] : 0;
-      double xv[kV5Per];
-#pragma unroll
-      for (int e = 0; e < kV5Per; ++e) xv[e] = e * 32 + lane < nnz ? __ldg(x + c[e]) : 0.0;
-#pragma unroll
-      for (int e = 0; e < kV5Per; ++e)
-        if (e * 32 + lane < nnz) vs[e * 32 + lane] *= xv[e];
-      __syncwarp();
-      const int g4 = lane & 3, grp = lane >> 2;
-      for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
-        const int rr = rr0 + grp;
-        const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
-        const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
-        const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
-        double a = 0.0;
-        if (rr < nrows)
-          for (int e = lo + g4; e < hi; e += 4) a += vs[e];
-        a += __shfl_xor_sync(0xffffffffu, a, 2);
-        a += __shfl_xor_sync(0xffffffffu, a, 1);
-        if (rr < nrows && g4 == 0) {
-          const double rv = b ? brr - a : (negate_b_absent ? -a : a);
-          r[r0 + rr] = rv;
-          sq += rv * rv;
-        }
-      }
-    } else {  // one long row, straight from global memory
-      double a = 0.0;
-      for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-      if (lane == 0) {
-        const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
-        r[r0] = rv;
-        sq += rv * rv;
-      }
-    }
-    __syncwarp();
-    const int jn = j + S * TW;
-    if (lane == 0 && jn < nitems) issue(jn, st);
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if (lane == 0) red[wib] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < kV5Warps; ++q) t += red[q];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v8: v5's warp items with block-local column windows (built by
-// build_windows, matrix.cpp).  The block first stages x over its window --
-// runs of consecutive columns, one warp per run, coalesced -- while every
-// warp already has its item's values and 16-bit local columns in flight;
-// after one block barrier the x gathers read shared memory.  Per nonzero the
-// kernel streams 10 bytes (value + local column) instead of 12, and the L1
-// no longer replays x gathers over ~6 cache lines per warp load.
-static_assert(kItemNnz == 32 * kV5Per, "v8 item capacity");
-static_assert(kWindowItems == kV5Warps, "v8 block = one window");
-
-template <int MINB>
-__global__ void __launch_bounds__(kV5Warps * 32, MINB) residual_v8_kernel(
-    int nitems, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    const uint16_t* __restrict__ lcol, const int32_t* __restrict__ win_ptr, const int2* __restrict__ win_runs,
-    const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
-    const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
-    bool negate_b_absent) {
-  extern __shared__ double xs[];
-  __shared__ double prod[kV5Warps][32 * kV5Per];
-  __shared__ double red[kV5Warps];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int w = blockIdx.x * kV5Warps + wib;
-  const bool has = w < nitems;
-  int64_t r0 = 0, base = 0, end = 0;
-  int nrows = 0;
-  if (has) {
-    r0 = __ldg(wstart + w);
-    nrows = __ldg(wstart + w + 1) - (int)r0;
-    base = __ldg(wbase + w);
-    end = __ldg(wbase + w + 1);
-  }
-  const int nnz = (int)(end - base);
-  const bool shortitem = has && nnz <= 32 * kV5Per;
-  // item bytes in flight before the window staging
-  uint16_t lc[kV5Per];
-  double v[kV5Per];
-  if (shortitem) {
-#pragma unroll
-    for (int e = 0; e < kV5Per; ++e) lc[e] = e * 32 + lane < nnz ? __ldcs(lcol + base + e * 32 + lane) : 0;
-#pragma unroll
-    for (int e = 0; e < kV5Per; ++e) v[e] = e * 32 + lane < nnz ? __ldcs(val + base + e * 32 + lane) : 0.0;
-  }
-  const int64_t rpl = (has && lane <= nrows) ? __ldg(rp + r0 + lane) : end;
-  const double bl = (has && b && lane < nrows) ? __ldcs(b + r0 + lane) : 0.0;
-  {
-    const int q0 = __ldg(win_ptr + blockIdx.x), q1 = __ldg(win_ptr + blockIdx.x + 1) - 1;  // last: sentinel
-    for (int q = q0 + wib; q < q1; q += kV5Warps) {
-      const int2 a = __ldg(win_runs + q);
-      const int len = __ldg(win_runs + q + 1).y - a.y;
-      for (int j = lane; j < len; j += 32) xs[a.y + j] = __ldg(x + a.x + j);
-    }
-  }
-  __syncthreads();
-  double sq = 0.0;
-  if (shortitem) {
-    double* pw = prod[wib];
-#pragma unroll
-    for (int e = 0; e < kV5Per; ++e)
-      if (e * 32 + lane < nnz) pw[e * 32 + lane] = v[e] * xs[lc[e]];
-    __syncwarp();
-    const int g4 = lane & 3, grp = lane >> 2;
-    for (int rr0 = 0; rr0 < nrows; rr0 += 8) {  // warp-uniform trip count
-      const int rr = rr0 + grp;
-      const int lo = (int)(__shfl_sync(0xffffffffu, rpl, rr & 31) - base);
-      const int hi = (int)(__shfl_sync(0xffffffffu, rpl, (rr + 1) & 31) - base);
-      const double brr = __shfl_sync(0xffffffffu, bl, rr & 31);
-      double a = 0.0;
-      if (rr < nrows)
-        for (int e = lo + g4; e < hi; e += 4) a += pw[e];
-      a += __shfl_xor_sync(0xffffffffu, a, 2);
-      a += __shfl_xor_sync(0xffffffffu, a, 1);
-      if (rr < nrows && g4 == 0) {
-        const double rv = b ? brr - a : (negate_b_absent ? -a : a);
-        r[r0 + rr] = rv;
-        sq += rv * rv;
-      }
-    }
-  } else if (has) {  // one long row, global columns
-    double a = 0.0;
-    for (int64_t e = base + lane; e < end; e += 32) a += __ldcs(val + e) * __ldg(x + __ldcs(col + e));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-    if (lane == 0) {
-      const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
-      r[r0] = rv;
-      sq += rv * rv;
-    }
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if (lane == 0) red[wib] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < kV5Warps; ++q) t += red[q];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-// Residual v9 over the SELL-C-sigma copy (build_sell, matrix.cpp): warp per
-// slice of 32 rows, lane l owns slice row l.  Step j loads entry j of all 32
-// rows -- one 256-byte value span and one 128-byte column span, fully
-// coalesced -- and the x gathers of 32 similar rows hit a few lines.  U steps
-// are loaded before any is consumed (memory-level parallelism without a
-// shared-memory stage), lanes past their row's end are predicated off, and
-// each lane accumulates its row in CSR order with unfused multiply/add:
-// r = b - s bit for bit as the reference spmv + smooth (sparse.cpp:50-63,
-// precond.cpp:95-97).
-template <int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
-                                                            const int2* __restrict__ srow,
-                                                            const double* __restrict__ sval,
-                                                            const int32_t* __restrict__ scol,
-                                                            const double* __restrict__ x, const double* __restrict__ b,
-                                                            double* __restrict__ r, double* __restrict__ block_sumsq,
-                                                            bool negate_b_absent, int pf) {
-  __shared__ double red[8];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
-  double sq = 0.0;
-  if (sl >= nslices) {
-    grid_dep_wait();
-    grid_dep_trigger();
-  }
-  if (sl < nslices) {
-    const int2 rl = __ldg(srow + sl * 32 + lane);
-    const int len = rl.y;
-    const int L = __reduce_max_sync(0xffffffffu, (unsigned)len);
-    const int64_t o = __ldg(soff + sl);
-    const double* vp = sval + o + lane;
-    const int32_t* cp = scol + o + lane;
-    const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
-    double acc = 0.0;
-    int32_t c[U];
-    double v[U];
-    // first step group: independent of the predecessor (the scatter writing x)
-#pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = u < len ? __ldcs(cp + (int64_t)u * 32) : 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = u < len ? __ldcs(vp + (int64_t)u * 32) : 0.0;
-    grid_dep_wait();
-    grid_dep_trigger();
-    for (int j = 0; j < L; j += U) {
-      // pull the slice's next columns/values towards L2 (bulk prefetch, no
-      // registers held) so the loads pf iterations ahead find them there
-      if (pf > 0 && lane == 0) {
-        const int jn = j + pf * U;
-        if (jn < L) {
-          const int cnt = (L - jn < U ? L - jn : U) * 32;
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + o + (int64_t)jn * 32),
-                       "r"((unsigned)(cnt * 8)));
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + o + (int64_t)jn * 32),
-                       "r"((unsigned)(cnt * 4)));
-        }
-      }
-      if (j > 0) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
-      }
-      double xv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = j + u < len ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (j + u < len) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
-    }
-    if (rl.x >= 0) {
-      const double rv = b ? __dsub_rn(bl, acc) : (negate_b_absent ? -acc : acc);
-      r[rl.x] = rv;
-      sq += rv * rv;
-    }
-  }
-  if (block_sumsq) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
-    if (lane == 0) red[wib] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int q = 0; q < 8; ++q) t += red[q];
-      block_sumsq[blockIdx.x] = t;
-    }
-  }
-}
-
-__global__ void finish_sum_kernel(const double* __restrict__ partials, int count, double* out, bool take_sqrt) {
-  __shared__ double red[1024];
-  double t = 0.0;
-  for (int i = threadIdx.x; i < count; i += blockDim.x) t += partials[i];
-  red[threadIdx.x] = t;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[0] = take_sqrt ? sqrt(red[0]) : red[0];
-}
 
 // Sub-warp of W lanes per patch (ps <= W <= 32).  Lane i holds local row i.
 template <int W>
@@ -1076,17 +195,13 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
 
 constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
 
-constexpr int32_t kDofMask = (1 << 28) - 1;  // zfwd = (slot rank << 28) | dof
-
-// Z = false: solutions to sols in tile order (idx = tile_idx).  Z = true:
-// idx = zfwd, each solution value goes to out[(f >> 28) * n + (f & mask)].
-// R is staged unpadded (patch p, local row k at p * ps + k), so the copy is a
+// Solutions are written in patch order (sols[order[slot] * ps + i]).  R is
+// staged unpadded (patch p, local row k at p * ps + k), so the copy is a
 // flat, division-free loop; the A fragments are zero for k >= ps, which
 // cancels the neighbouring patch's values a B fragment reads there, and the
 // stage is zero-filled past the tile's cnt * ps live values (no NaN garbage).
-template <int MT, int KS, bool Z>
-__global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64_t n,
-                                                                   const int32_t* __restrict__ tile_entry,
+template <int MT, int KS>
+__global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
                                                                    const int32_t* __restrict__ tile_start,
                                                                    const int32_t* __restrict__ idx,
                                                                    const int32_t* __restrict__ order,
@@ -1098,12 +213,11 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
   constexpr int TOT = kDmmaTile * KS * 4;  // >= 31 * ps + 4 * KS: every B-fragment read
   constexpr int ITER = (TOT + NTH - 1) / NTH;
   __shared__ double rk[TOT];
-  __shared__ int32_t fk[Z ? TOT : 1];
-  __shared__ int32_t ko[kDmmaTile];  // patch index of each tile column (output in patch order)
+  __shared__ int32_t ko[kDmmaTile];  // patch index of each tile column
   const int t = blockIdx.x;
   const int f = __ldg(tile_entry + t);
   const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
-  if (!Z && threadIdx.x < cnt) ko[threadIdx.x] = __ldg(order + s0 + threadIdx.x);
+  if (threadIdx.x < cnt) ko[threadIdx.x] = __ldg(order + s0 + threadIdx.x);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double a[KS];
   const double* fa = frag + ((int64_t)f * MT + w) * (KS * 32) + lane;
@@ -1124,10 +238,8 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
     const int e = threadIdx.x + it * NTH;
     double v = 0.0;
     if (gi[it] >= 0) {
-      const int32_t d = Z ? (gi[it] & kDofMask) : gi[it];
-      v = __ldg(r + d);
-      if (in_scale) v *= __ldg(in_scale + d);
-      if constexpr (Z) fk[e] = gi[it];
+      v = __ldg(r + gi[it]);
+      if (in_scale) v *= __ldg(in_scale + gi[it]);
     }
     if (e < TOT) rk[e] = v;
   }
@@ -1143,19 +255,8 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, int64
       for (int q = 0; q < KS; ++q) dmma_m8n8k4(c0, c1, a[q], bp[q * 4]);
       const int p0 = nt * 8 + 2 * tg;
       if (row < ps) {
-        if constexpr (Z) {
-          if (p0 < cnt) {
-            const int32_t z0 = fk[p0 * ps + row];
-            out[(int64_t)(z0 >> 28) * n + (z0 & kDofMask)] = c0;
-          }
-          if (p0 + 1 < cnt) {
-            const int32_t z1 = fk[(p0 + 1) * ps + row];
-            out[(int64_t)(z1 >> 28) * n + (z1 & kDofMask)] = c1;
-          }
-        } else {
-          if (p0 < cnt) out[(int64_t)ko[p0] * ps + row] = c0;
-          if (p0 + 1 < cnt) out[(int64_t)ko[p0 + 1] * ps + row] = c1;
-        }
+        if (p0 < cnt) out[(int64_t)ko[p0] * ps + row] = c0;
+        if (p0 + 1 < cnt) out[(int64_t)ko[p0 + 1] * ps + row] = c1;
       }
     }
   }
@@ -1222,43 +323,6 @@ __global__ void __launch_bounds__(1024) patch_apply_dmma_large_kernel(
       if (p0 + 1 < cnt) sols[(int64_t)ko[p0 + 1] * ps + row] = c[nt][1];
     }
   }
-}
-
-__global__ void build_zmap_kernel(int64_t n, int ps, const int32_t* __restrict__ inv_ptr,
-                                  const int32_t* __restrict__ inv, const int32_t* __restrict__ slot_of,
-                                  int32_t* __restrict__ zfwd, uint8_t* __restrict__ zcnt) {
-  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (d >= n) return;
-  const int32_t lo = inv_ptr[d], hi = inv_ptr[d + 1];
-  zcnt[d] = (uint8_t)(hi - lo);
-  for (int32_t q = lo; q < hi; ++q) {
-    const int32_t e = inv[q];  // k * ps + l
-    zfwd[(int64_t)slot_of[e / ps] * ps + e % ps] = ((q - lo) << 28) | (int32_t)d;
-  }
-}
-
-// Scatter over DoF-major slots: loads only the zcnt[i] live slots of DoF i
-// (ascending patch order), weight recomputed as scatter_update_pad_kernel.
-template <int MAXC>
-__global__ void scatter_z_kernel(int64_t n, const uint8_t* __restrict__ zcnt, const double* __restrict__ Z,
-                                 double omega, bool sym, const double* __restrict__ x_in,
-                                 double* __restrict__ z_out, double* __restrict__ x_out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int cnt = zcnt[i];
-  double v[MAXC];
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) v[c] = c < cnt ? __ldcs(Z + (int64_t)c * n + i) : 0.0;
-  const double xi = x_out ? __ldcs(x_in + i) : 0.0;
-  double z = 0.0;
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c)
-    if (c < cnt) z += v[c];
-  double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
-  if (sym) w = sqrt(w);
-  z *= omega * w;
-  if (z_out) z_out[i] = z;
-  if (x_out) x_out[i] = z + xi;
 }
 
 // frag[f][w][q][lane] = B_f^{-1}[8w + lane/4][4q + lane%4] (0 outside ps x ps)
@@ -1470,291 +534,6 @@ inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 
 
 }  // namespace
 
-int stream_nnz() { return kStreamNnz; }
-
-std::vector<int32_t> stream_partition(int64_t n, const int64_t* rp, int per) {
-  if (per < 0) return row_partition(n, rp, 32 * (int64_t)(-per), kV5Rows);  // v5 warp partition
-  return row_partition(n, rp, (int64_t)kStreamThreads * per, kStreamRows);
-}
-
-std::vector<int32_t> row_partition(int64_t n, const int64_t* rp, int64_t cap_nnz, int64_t cap_rows) {
-  std::vector<int32_t> starts;
-  starts.push_back(0);
-  int64_t row = 0;
-  while (row < n) {
-    const int64_t b0 = rp[row];
-    int64_t end = row + 1;  // a block always takes at least one row
-    while (end < n && end - row < cap_rows && rp[end + 1] - b0 <= cap_nnz) ++end;
-    if (rp[row + 1] - b0 > cap_nnz) end = row + 1;  // long row alone
-    starts.push_back((int32_t)end);
-    row = end;
-  }
-  return starts;
-}
-
-int v7_stages();
-template <int S>
-int v7_grid(int nitems);
-
-SpmvPlan spmv_plan_stream(int64_t n, int64_t nnz, const int32_t* blk_start, const int64_t* blk_base, int nblk,
-                          int per) {
-  SpmvPlan p = spmv_plan(n, nnz);
-  const char* e = getenv("PDB_SPMV_VERSION");
-  // Default: v5 (measured fastest on config 2: 117 us vs v2 127, v3 150, the
-  // pipelined v4 176; L2 bulk prefetch made v5 slower), see DESIGN.md §3.
-  const int want = e ? atoi(e) : 5;
-  if (blk_start && blk_base && nblk > 0 && want == 7 && per == -kV5Per) {
-    // v7 reuses the v5 item partition; `entries` carries the stage count and
-    // `blocks` the persistent grid
-    p.version = 7;
-    p.entries = v7_stages();
-    p.blk_start = blk_start;
-    p.blk_base = blk_base;
-    p.nblk = nblk;
-    p.blocks = p.entries == 2 ? v7_grid<2>(nblk) : p.entries == 4 ? v7_grid<4>(nblk) : v7_grid<3>(nblk);
-    return p;
-  }
-  if (blk_start && blk_base && nblk > 0 && (want == 5 || want == 6) && per < 0) {
-    p.version = want;
-    p.entries = -per;
-    p.blk_start = blk_start;
-    p.blk_base = blk_base;
-    p.nblk = nblk;  // warps
-    p.blocks = (nblk + kV5Warps - 1) / kV5Warps;
-    return p;
-  }
-  if (blk_start && blk_base && nblk > 0 && (want == 3 || want == 4) && per > 0) {
-    p.version = want;
-    p.blk_start = blk_start;
-    p.blk_base = blk_base;
-    p.nblk = nblk;
-    p.blocks = nblk;
-    p.entries = per;
-    if (want == 4) {
-      int dev = 0, sms = 148, per_sm = 2;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, residual_v4_kernel, kV4Threads, 0);
-      if (per_sm < 1) per_sm = 1;
-      p.blocks = nblk < sms * per_sm ? nblk : sms * per_sm;  // persistent grid: one wave
-    }
-  }
-  return p;
-}
-
-SpmvPlan spmv_plan(int64_t n, int64_t nnz) {
-  SpmvPlan p;
-  const double avg = n > 0 ? (double)nnz / (double)n : 1.0;
-  // ~one 4-deep unrolled pass per row: G ~ avg/8 (power of two, 2..32)
-  int g = 2;
-  while (g < 32 && g * 8 < avg) g *= 2;
-  p.group = g;
-  p.version = 2;
-  p.entries = 4;
-  // v2: G*E ~ the typical row length (config 2, avg 36: G=4,E=8 measured best;
-  // config 3, avg 61: G=8,E=8)
-  if (avg <= 16) p.group = 2, p.entries = 8;
-  else if (avg <= 48) p.group = 4, p.entries = 8;
-  else p.group = 8, p.entries = 8;
-  if (const char* e = getenv("PDB_SPMV_VERSION")) p.version = atoi(e) == 1 ? 1 : 2;
-  if (p.version == 1) p.group = g;
-  if (const char* e = getenv("PDB_SPMV_GROUP")) {
-    const int v = atoi(e);
-    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) p.group = v;
-  }
-  if (const char* e = getenv("PDB_SPMV_ENTRIES")) {
-    const int v = atoi(e);
-    if (v == 2 || v == 4 || v == 8 || v == 5 || v == 9) p.entries = v;  // 5/9: E=4/8 with L1-bypass hints
-  }
-  p.rows_per_block = kBlock / p.group;
-  p.blocks = (int)((n + p.rows_per_block - 1) / p.rows_per_block);
-  return p;
-}
-
-template <int G>
-static void launch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
-                            const double* x, const double* b, double* r, double* sumsq, bool negate,
-                            cudaStream_t s) {
-  if (p.version == 1) {
-    residual_kernel<G><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
-    return;
-  }
-  switch (p.entries) {
-    case 2: residual_v2_kernel<G, 2><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
-    case 8: residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
-    case 9: residual_v2_kernel<G, 8, 1><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
-    case 5: residual_v2_kernel<G, 4, 1><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
-    default: residual_v2_kernel<G, 4><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate); break;
-  }
-}
-
-int v7_stages() {
-  const char* e = getenv("PDB_SPMV_STAGES");
-  const int v = e ? atoi(e) : 3;
-  return v == 2 || v == 4 ? v : 3;
-}
-
-size_t v7_smem(int stages) {
-  return 128 * ((kV5Warps * stages * 8 + 127) / 128) + (size_t)kV5Warps * stages * kV7StageBytes;
-}
-
-template <int S>
-int v7_grid(int nitems) {
-  static int per_sm[5] = {0, 0, 0, 0, 0};
-  if (!per_sm[S]) {
-    const size_t smem = v7_smem(S);
-    cudaFuncSetAttribute(residual_v7_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, residual_v7_kernel<S>, kV5Warps * 32, smem);
-    per_sm[S] = occ > 0 ? occ : 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int need = (nitems + kV5Warps - 1) / kV5Warps;
-  return need < sms * per_sm[S] ? need : sms * per_sm[S];
-}
-
-template <int S>
-static void launch_v7_s(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-                        const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
-  residual_v7_kernel<S><<<p.blocks, kV5Warps * 32, v7_smem(S), s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start,
-                                                                    p.blk_base, sumsq, negate);
-}
-
-static void launch_v7(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-                      const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
-  if (p.entries == 2)
-    launch_v7_s<2>(p, rp, col, val, x, b, r, sumsq, negate, s);
-  else if (p.entries == 4)
-    launch_v7_s<4>(p, rp, col, val, x, b, r, sumsq, negate, s);
-  else
-    launch_v7_s<3>(p, rp, col, val, x, b, r, sumsq, negate, s);
-}
-
-template <bool CHUNK>
-static void launch_v5(const SpmvPlan& p, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-                      const double* b, double* r, double* sumsq, bool negate, int pf, cudaStream_t s) {
-  const unsigned th = kV5Warps * 32;
-  if (p.entries == 16)
-    residual_v5_kernel<16, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                          sumsq, negate, pf);
-  else if (p.entries == 4)
-    residual_v5_kernel<4, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                         sumsq, negate, pf);
-  else
-    residual_v5_kernel<8, CHUNK><<<p.blocks, th, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                         sumsq, negate, pf);
-}
-
-static void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
-                              const double* x, const double* b, double* r, double* sumsq, bool negate,
-                              cudaStream_t s) {
-  if (n <= 0) return;
-  if (p.version == 9 && p.sell_off) {
-    const unsigned g = (unsigned)p.blocks;
-    const int2* sr = reinterpret_cast<const int2*>(p.sell_row);
-    // L2 bulk prefetch one step group ahead (measured: pf 1 best, 90.5 us vs
-    // 96.7 without on config 2; 263 vs 301 us on config 3)
-    const char* pfe = getenv("PDB_SELL_PF");
-    const int pf = pfe ? atoi(pfe) : 1;
-    const char* mbe = getenv("PDB_SELL_MINB");
-    const int minb = mbe ? atoi(mbe) : 0;
-#define PDB_SELL(U, M)                                                                                             \
-  launch_pdl(residual_sell_kernel<U, M>, dim3(g), dim3(256), 0, s, p.nslices, p.sell_off, sr, p.sell_val, p.sell_col, \
-             x, b, r, sumsq, negate, pf)
-    if (p.entries == 2) PDB_SELL(2, 1);
-    else if (p.entries == 4) PDB_SELL(4, 1);
-    else if (p.entries == 16) PDB_SELL(16, 1);
-    else if (minb == 5) PDB_SELL(8, 5);
-    else if (minb == 6) PDB_SELL(8, 6);
-    else PDB_SELL(8, 1);
-#undef PDB_SELL
-    return;
-  }
-  if (p.version == 8 && p.blk_start && p.lcol) {
-    const size_t smem = (size_t)p.win_max * sizeof(double);
-    const char* mb = getenv("PDB_V8_MINB");
-    const bool capped = mb && atoi(mb) == 5;
-    static size_t opted[2] = {48 * 1024, 48 * 1024};
-    if (smem > opted[capped]) {
-      if (capped)
-        cudaFuncSetAttribute(residual_v8_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      else
-        cudaFuncSetAttribute(residual_v8_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      opted[capped] = smem;
-    }
-    if (capped)
-      residual_v8_kernel<5><<<p.blocks, kV5Warps * 32, smem, s>>>(p.nblk, rp, col, val, p.lcol, p.win_ptr,
-                                                                  reinterpret_cast<const int2*>(p.win_runs), x, b, r,
-                                                                  p.blk_start, p.blk_base, sumsq, negate);
-    else
-      residual_v8_kernel<1><<<p.blocks, kV5Warps * 32, smem, s>>>(p.nblk, rp, col, val, p.lcol, p.win_ptr,
-                                                                  reinterpret_cast<const int2*>(p.win_runs), x, b, r,
-                                                                  p.blk_start, p.blk_base, sumsq, negate);
-    return;
-  }
-  if (p.version == 7 && p.blk_start) {
-    launch_v7(p, rp, col, val, x, b, r, sumsq, negate, s);
-    return;
-  }
-  if ((p.version == 5 || p.version == 6) && p.blk_start) {
-    // prefetch distance in warps (PDB_SPMV_PREFETCH; 0 disables)
-    const char* pfe = getenv("PDB_SPMV_PREFETCH");
-    const int pf = pfe ? atoi(pfe) : 0;
-    if (p.version == 6)
-      launch_v5<true>(p, rp, col, val, x, b, r, sumsq, negate, pf, s);
-    else
-      launch_v5<false>(p, rp, col, val, x, b, r, sumsq, negate, pf, s);
-    return;
-  }
-  if (p.version == 4 && p.blk_start) {
-    residual_v4_kernel<<<p.blocks, kV4Threads, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base, sumsq,
-                                                       negate);
-    return;
-  }
-  if (p.version == 3 && p.blk_start) {
-    if (p.entries == 16)
-      residual_v3_kernel<16><<<p.blocks, kStreamThreads, 0, s>>>(n, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                                 sumsq, negate);
-    else
-      residual_v3_kernel<8><<<p.blocks, kStreamThreads, 0, s>>>(n, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                                sumsq, negate);
-    return;
-  }
-  switch (p.group) {
-    case 1: launch_residual<1>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 2: launch_residual<2>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 4: launch_residual<4>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 8: launch_residual<8>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 16: launch_residual<16>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    default: launch_residual<32>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-  }
-}
-
-void residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-              const double* b, double* r, double* block_sumsq, cudaStream_t s) {
-  dispatch_residual(p, n, rp, col, val, x, b, r, block_sumsq, true, s);
-}
-
-void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x, const double* b, double* r,
-                     cudaStream_t s) {
-  if (s1 <= s0 || p.version != 9) return;
-  const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
-  const unsigned g = (unsigned)((s1 - s0 + 7) / 8);
-  residual_sell_kernel<8, 1><<<g, 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x, b, r, nullptr,
-                                               true, 1);
-}
-
-void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-          double* y, cudaStream_t s) {
-  dispatch_residual(p, n, rp, col, val, x, nullptr, y, nullptr, false, s);
-}
-
-void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s) {
-  finish_sum_kernel<<<1, 1024, 0, s>>>(partials, count, out, sqrt_result);
-}
-
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* F, const int32_t* piv, const int32_t* phi,
                  const double* r, const double* in_scale, double* sols, cudaStream_t s) {
   if (np <= 0) return;
@@ -1815,10 +594,9 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
     build_frag_kernel<<<grid_for(total, kBlock), kBlock, 0, s>>>(total, ps, (ps + 7) / 8, (ps + 3) / 4, inv_cm, frag);
 }
 
-template <bool Z>
-static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
-                        const int32_t* idx, const int32_t* order, const double* frag, const double* r, const double* in_scale, double* out,
-                        cudaStream_t s) {
+void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
+                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
+                      const double* in_scale, double* sols, cudaStream_t s) {
   if (ntiles <= 0) return;
   const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
   if (ps > 32) {  // run-time shapes, inverse streamed from L2
@@ -1830,16 +608,15 @@ static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry
       cudaFuncSetAttribute(patch_apply_dmma_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       opted = smem;
     }
-    if (!Z)
-      launch_pdl(patch_apply_dmma_large_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s, ps, mt, ks, kstr,
-                 tile_entry, tile_start, idx, order, frag, r, in_scale, out);
+    launch_pdl(patch_apply_dmma_large_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s, ps, mt, ks, kstr,
+               tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);
     return;
   }
-#define PDB_DMMA_CASE(M, K)                                                                                    \
-  if (mt == M && ks == K) {                                                                                    \
-    launch_pdl(patch_apply_dmma_kernel<M, K, Z>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, n, tile_entry, \
-               tile_start, idx, order, frag, r, in_scale, out);                                               \
-    return;                                                                                                    \
+#define PDB_DMMA_CASE(M, K)                                                                                 \
+  if (mt == M && ks == K) {                                                                                 \
+    launch_pdl(patch_apply_dmma_kernel<M, K>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, tile_entry,   \
+               tile_start, tile_idx, order, frag, r, in_scale, sols);                                       \
+    return;                                                                                                 \
   }
   PDB_DMMA_CASE(1, 1)
   PDB_DMMA_CASE(1, 2)
@@ -1850,36 +627,6 @@ static void launch_dmma(int ntiles, int ps, int64_t n, const int32_t* tile_entry
   PDB_DMMA_CASE(4, 7)
   PDB_DMMA_CASE(4, 8)
 #undef PDB_DMMA_CASE
-}
-
-void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
-                      const double* in_scale, double* sols, cudaStream_t s) {
-  launch_dmma<false>(ntiles, ps, 0, tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols, s);
-}
-
-void patch_apply_dmma_z(int ntiles, int ps, int64_t n, const int32_t* tile_entry, const int32_t* tile_start,
-                        const int32_t* zfwd, const double* frag, const double* r, const double* in_scale, double* Z,
-                        cudaStream_t s) {
-  launch_dmma<true>(ntiles, ps, n, tile_entry, tile_start, zfwd, nullptr, frag, r, in_scale, Z, s);
-}
-
-void build_zmap(int64_t n, int ps, const int32_t* inv_ptr, const int32_t* inv, const int32_t* slot_of, int32_t* zfwd,
-                uint8_t* zcnt, cudaStream_t s) {
-  if (n > 0) build_zmap_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, ps, inv_ptr, inv, slot_of, zfwd, zcnt);
-}
-
-void scatter_z(int64_t n, int maxc, const uint8_t* zcnt, const double* Z, double omega, bool sym, const double* x_in,
-               double* z_out, double* x_out, cudaStream_t s) {
-  if (n <= 0) return;
-  const unsigned g = grid_for(n, kBlock);
-  switch (maxc) {
-    case 1: scatter_z_kernel<1><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
-    case 2: scatter_z_kernel<2><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
-    case 3:
-    case 4: scatter_z_kernel<4><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
-    default: scatter_z_kernel<8><<<g, kBlock, 0, s>>>(n, zcnt, Z, omega, sym, x_in, z_out, x_out); break;
-  }
 }
 
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,

@@ -57,95 +57,6 @@ int num_sms() {
   return sms;
 }
 
-// Block-local column windows for the v8 residual.  Block b of the v5 item
-// partition (items [8b, 8b+8)) touches a small set D_b of distinct columns
-// (for a FEM matrix: a few lattice lines around ~50 consecutive rows).  D_b is
-// stored as runs of consecutive columns; every nonzero of the block gets its
-// 16-bit position in D_b.  The kernel stages x[D_b] in shared memory once per
-// block, so column indices cost 2 bytes instead of 4 and the x gathers hit
-// shared memory instead of ~6 L1 lines per warp load.  Items holding one
-// overlong row (> kItemNnz) keep the global column path.  Returns false
-// (windows not built) when a block's window exceeds kWindowCap.
-bool build_windows(const HostCsr& h, const std::vector<int32_t>& items, DeviceCsr& d, cudaStream_t s) {
-  const int64_t nitems = static_cast<int64_t>(items.size()) - 1;
-  const int64_t nb = (nitems + k::kWindowItems - 1) / k::kWindowItems;
-  if (nb <= 0 || h.nnz() == 0) return false;
-  std::vector<uint16_t> lcol(static_cast<size_t>(h.nnz()), 0);
-  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-  std::vector<std::vector<int32_t>> runs(static_cast<size_t>(T));
-  std::vector<std::vector<int32_t>> nrun(static_cast<size_t>(T));
-  std::vector<int> ok(static_cast<size_t>(T), 1), wmax(static_cast<size_t>(T), 0);
-  std::vector<std::thread> pool;
-  for (int t = 0; t < T; ++t)
-    pool.emplace_back([&, t] {
-      const int64_t b0 = nb * t / T, b1 = nb * (t + 1) / T;
-      std::vector<int32_t> cols;
-      for (int64_t b = b0; b < b1 && ok[t]; ++b) {
-        cols.clear();
-        const int64_t i0 = b * k::kWindowItems, i1 = std::min<int64_t>(nitems, i0 + k::kWindowItems);
-        for (int64_t it = i0; it < i1; ++it) {
-          const int64_t p0 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it)])];
-          const int64_t p1 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it + 1)])];
-          if (p1 - p0 > k::kItemNnz) continue;
-          cols.insert(cols.end(), h.col.begin() + p0, h.col.begin() + p1);
-        }
-        std::sort(cols.begin(), cols.end());
-        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
-        const int m = static_cast<int>(cols.size());
-        if (m > k::kWindowCap) {
-          ok[t] = 0;
-          break;
-        }
-        wmax[t] = std::max(wmax[t], m);
-        int count = 0;
-        for (int q = 0; q < m; ++q)
-          if (q == 0 || cols[static_cast<size_t>(q)] != cols[static_cast<size_t>(q - 1)] + 1) {
-            runs[t].push_back(cols[static_cast<size_t>(q)]);
-            runs[t].push_back(q);
-            ++count;
-          }
-        runs[t].push_back(-1);  // sentinel: window size
-        runs[t].push_back(m);
-        nrun[t].push_back(count + 1);
-        for (int64_t it = i0; it < i1; ++it) {
-          const int64_t p0 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it)])];
-          const int64_t p1 = h.row_ptr[static_cast<size_t>(items[static_cast<size_t>(it + 1)])];
-          if (p1 - p0 > k::kItemNnz) continue;
-          for (int64_t p = p0; p < p1; ++p)
-            lcol[static_cast<size_t>(p)] = static_cast<uint16_t>(
-                std::lower_bound(cols.begin(), cols.end(), h.col[static_cast<size_t>(p)]) - cols.begin());
-        }
-      }
-    });
-  for (auto& th : pool) th.join();
-  for (int t = 0; t < T; ++t)
-    if (!ok[t]) return false;
-  std::vector<int32_t> ptr;
-  ptr.reserve(static_cast<size_t>(nb + 1));
-  std::vector<int32_t> all;
-  int32_t at = 0;
-  for (int t = 0; t < T; ++t) {
-    for (int32_t c : nrun[t]) {
-      ptr.push_back(at);
-      at += c;
-    }
-    all.insert(all.end(), runs[t].begin(), runs[t].end());
-  }
-  ptr.push_back(at);
-  d.lcol.alloc(lcol.size() + 64);
-  PDB_CUDA(cudaMemsetAsync(d.lcol.get(), 0, (lcol.size() + 64) * sizeof(uint16_t), s));
-  d.lcol.upload(lcol.data(), lcol.size(), s);
-  d.win_ptr.alloc(ptr.size());
-  d.win_ptr.upload(ptr.data(), ptr.size(), s);
-  d.win_runs.alloc(all.size());
-  d.win_runs.upload(all.data(), all.size(), s);
-  int m = 0;
-  for (int t = 0; t < T; ++t) m = std::max(m, wmax[t]);
-  d.win_max = std::max(32, (m + 31) / 32 * 32);
-  sync(s);
-  return true;
-}
-
 // SELL-C-sigma (Kreutzer et al., SIAM J. Sci. Comput. 2014) copy of the
 // matrix for the v9 residual: rows are sorted by length (descending, stable)
 // inside windows of kSellSigma rows and cut into slices of kSellC = 32; a
@@ -243,34 +154,30 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
   d.col.upload(h.col.data(), h.col.size(), s);
   d.val.upload(h.val.data(), h.val.size(), s);
-  // row partitions: [0],[1] v3 blocks (8 / 16 nnz per thread); [2],[3],[4] v5 warps (8 / 16 / 4 per lane)
-  const int pers[5] = {8, 16, -8, -16, -4};
-  for (int v = 0; v < 5; ++v) {
-    const std::vector<int32_t> part = k::stream_partition(h.n, h.row_ptr.data(), pers[v]);
-    d.nblk[v] = static_cast<int>(part.size()) - 1;
-    d.blk_start[v].alloc(part.size());
-    d.blk_start[v].upload(part.data(), part.size(), s);
-    std::vector<int64_t> base(part.size());
-    for (size_t b = 0; b < part.size(); ++b) base[b] = h.row_ptr[static_cast<size_t>(part[b])];
-    d.blk_base[v].alloc(base.size());
-    d.blk_base[v].upload(base.data(), base.size(), s);
-    sync(s);
-    if (v == 2) {
-      const char* e = getenv("PDB_SPMV_WINDOWS");
-      if (e && std::string(e) == "1" && !build_windows(h, part, d, s)) d.win_max = 0;
-    }
-  }
+  // warp items of the CSR residual (v5)
+  const std::vector<int32_t> part = k::item_partition(h.n, h.row_ptr.data());
+  d.nitems = static_cast<int>(part.size()) - 1;
+  d.item_start.alloc(part.size());
+  d.item_start.upload(part.data(), part.size(), s);
+  std::vector<int64_t> base(part.size());
+  for (size_t b = 0; b < part.size(); ++b) base[b] = h.row_ptr[static_cast<size_t>(part[b])];
+  d.item_base.alloc(base.size());
+  d.item_base.upload(base.data(), base.size(), s);
+  sync(s);
   const char* e = getenv("PDB_SPMV_SELL");
   if (!(e && std::string(e) == "0")) build_sell(h, d, s);
 }
 
+// Residual plan: the SELL-C-sigma copy by default; PDB_SPMV_VERSION=5 / 2
+// selects the CSR warp-item / row-group kernels (A/B, or no SELL copy).
 k::SpmvPlan plan_of(const DeviceCsr& a) {
   const char* ver = getenv("PDB_SPMV_VERSION");
-  const char* e = getenv("PDB_SPMV_PER");
-  if ((!ver || atoi(ver) == 9) && a.nslices > 0) {  // SELL-C-sigma
+  const int v = ver ? atoi(ver) : 9;
+  if (v == 9 && a.nslices > 0) {
     k::SpmvPlan p = k::spmv_plan(a.n, a.nnz);
     p.version = 9;
-    p.entries = e ? atoi(e) : 8;  // unroll depth (measured: 8 > 4 > 2 on configs 2 and 3)
+    const char* e = getenv("PDB_SPMV_PER");
+    p.entries = e && atoi(e) == 4 ? 4 : 8;  // steps in flight per lane (measured: 8 > 4)
     p.sell_off = a.sell_off.get();
     p.sell_row = a.sell_row.get();
     p.sell_val = a.sell_val.get();
@@ -279,28 +186,8 @@ k::SpmvPlan plan_of(const DeviceCsr& a) {
     p.blocks = static_cast<int>((a.nslices + 7) / 8);
     return p;
   }
-  if (ver && atoi(ver) == 8 && a.win_max > 0) {  // v5 items with block-local column windows
-    k::SpmvPlan p = k::spmv_plan(a.n, a.nnz);
-    p.version = 8;
-    p.entries = 8;
-    p.blk_start = a.blk_start[2].get();
-    p.blk_base = a.blk_base[2].get();
-    p.nblk = a.nblk[2];
-    p.blocks = (a.nblk[2] + k::kWindowItems - 1) / k::kWindowItems;
-    p.lcol = a.lcol.get();
-    p.win_ptr = a.win_ptr.get();
-    p.win_runs = a.win_runs.get();
-    p.win_max = a.win_max;
-    return p;
-  }
-  if (!ver || atoi(ver) == 5 || atoi(ver) == 6 || atoi(ver) == 7 || atoi(ver) == 8) {
-    // default: warp-streaming v5 (v6: chunked row reduction, v7: bulk-copy fed)
-    const int per = e ? atoi(e) : 8;
-    const int v = per == 16 ? 3 : per == 4 ? 4 : 2;
-    return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 3 ? -16 : v == 4 ? -4 : -8);
-  }
-  const int v = e && atoi(e) == 16 ? 1 : 0;
-  return k::spmv_plan_stream(a.n, a.nnz, a.blk_start[v].get(), a.blk_base[v].get(), a.nblk[v], v == 0 ? 8 : 16);
+  if (v == 2) return k::spmv_plan(a.n, a.nnz);
+  return k::spmv_plan_items(a.n, a.nnz, a.item_start.get(), a.item_base.get(), a.nitems);
 }
 
 HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v) {

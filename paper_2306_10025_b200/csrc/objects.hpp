@@ -32,18 +32,10 @@ struct DeviceCsr {
   DevBuf<int64_t> row_ptr;
   DevBuf<int32_t> col;
   DevBuf<double> val;
-  // row partitions for the streaming SpMV ([0]: 2048 nnz / block, [1]: 4096)
-  DevBuf<int32_t> blk_start[5];  // nblk + 1 row starts ([2..4]: per-warp partitions of the v5 kernel)
-  DevBuf<int64_t> blk_base[5];   // row_ptr at each partition boundary
-  int nblk[5] = {0, 0, 0, 0, 0};
-  // block-local column windows over the v5 item partition (v8 residual):
-  // lcol = column index into the block's staged x window, win_ptr = first
-  // run of each block, win_runs = (first column, window offset) per run plus
-  // one sentinel (-1, window size) per block
-  DevBuf<uint16_t> lcol;
-  DevBuf<int32_t> win_ptr;
-  DevBuf<int32_t> win_runs;
-  int win_max = 0;  // 0: windows not built (some block's window too large)
+  // warp items of the CSR residual (v5): nitems + 1 row starts and row_ptr there
+  DevBuf<int32_t> item_start;
+  DevBuf<int64_t> item_base;
+  int nitems = 0;
   // SELL-C-sigma copy (v9 residual): slices of 32 rows of similar length,
   // entry j of slice row l at sell_off[s] + 32 j + l; sell_row = {row, length}
   DevBuf<int64_t> sell_off;
@@ -111,12 +103,6 @@ struct pdb_precond_s {
   pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
   int ntiles = 0, max_tile = 0;
   pdb::DevBuf<double> frag;  // inverses in DMMA A-fragment order (tensor-core grouped apply), when allocated
-  // DoF-major solution slots (single-GPU compressed path with DMMA tiles):
-  // zfwd[tile-order slot] = (c << 28) | dof, c = rank of the patch among the
-  // DoF's patches (ascending k); the apply writes solution values straight to
-  // Z[c * n + dof] and the scatter streams Z with zcnt[dof] live slots
-  pdb::DevBuf<int32_t> zfwd;
-  pdb::DevBuf<uint8_t> zcnt;
   pdb::DevBuf<int32_t> inv_pad;  // slot-major padded inverse map (maxc_pad slots), when maxc_pad > 0
   int maxc_pad = 0;
   pdb::DevBuf<int32_t> inv_ptr;

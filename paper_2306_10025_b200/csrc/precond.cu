@@ -59,18 +59,9 @@ void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = n
   }
 }
 
-// DoF-major solution slots in use (read at launch so A/B runs can toggle it)
-bool zmode(const pdb_precond_s& pc) {
-  if (!pc.zfwd.get() || !pc.frag.get() || !use_dmma_apply(static_cast<int>(pc.ps))) return false;
-  const char* e = getenv("PDB_ZMAP");
-  return !(e && std::string(e) == "0");
-}
-
 void scatter_stage(const pdb_precond_s& pc, const double* sols, bool symmetric, const double* x_in, double* z_out,
                    double* x_out, cudaStream_t s) {
-  if (zmode(pc))
-    k::scatter_z(pc.n, pc.maxc_pad, pc.zcnt.get(), sols, pc.omega, symmetric, x_in, z_out, x_out, s);
-  else if (pc.maxc_pad > 0)
+  if (pc.maxc_pad > 0)
     k::scatter_update_pad(pc.n, pc.maxc_pad, pc.inv_pad.get(), sols, pc.omega, symmetric, x_in, z_out, x_out, s);
   else
     k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols, symmetric ? pc.omega_sw.get() : pc.omega_w.get(),
@@ -173,20 +164,13 @@ bool use_dmma_apply(int ps) {
 }
 
 
-// Solution scratch: patch-order sols, or the DoF-major slots Z (maxc_pad x n).
-int64_t sols_len(const pdb_precond_s& pc) {
-  int64_t len = std::max<int64_t>(pc.np * pc.ps, 1);
-  if (pc.zfwd.get()) len = std::max<int64_t>(len, pc.maxc_pad * pc.n);
-  return len;
-}
+// Solution scratch (patch order).
+int64_t sols_len(const pdb_precond_s& pc) { return std::max<int64_t>(pc.np * pc.ps, 1); }
 
 // sols_k = B_phi(k)^{-1} (r .* in_scale)|_k for every patch.
 void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s) {
   const int32_t* phi = pc.compressed ? pc.phi.get() : nullptr;
-  if (zmode(pc))
-    k::patch_apply_dmma_z(pc.ntiles, static_cast<int>(pc.ps), pc.n, pc.tile_entry.get(), pc.tile_start.get(),
-                          pc.zfwd.get(), pc.frag.get(), r, in_scale, sols, s);
-  else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0 && pc.frag.get() && use_dmma_apply(static_cast<int>(pc.ps)))
+  if (!pc.lu_apply && pc.compressed && pc.ntiles > 0 && pc.frag.get() && use_dmma_apply(static_cast<int>(pc.ps)))
     k::patch_apply_dmma(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
                         pc.tile_idx.get(), pc.order.get(), pc.frag.get(), r, in_scale, sols, s);
   else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
@@ -259,16 +243,6 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
     if (use_dmma_apply(static_cast<int>(ps.ps))) {
       pc.frag.alloc(static_cast<size_t>(db.m * k::frag_len(static_cast<int>(ps.ps))));
       k::build_frag_inverses(db.m, static_cast<int>(ps.ps), pc.factors.get(), pc.frag.get(), s);
-      // single-GPU path: solutions go straight to DoF-major slots (a shard's
-      // interface scatter keeps the patch-order solutions and the inverse map)
-      // (opt-in, PDB_ZMAP=1: measured slower on config 3, ~1 us faster on config 2)
-      const char* zm = getenv("PDB_ZMAP");
-      if (zm && std::string(zm) == "1" && check_onto && pc.maxc_pad > 0 && pc.n < (int64_t{1} << 28) && pc.ps <= 32) {
-        pc.zfwd.alloc(static_cast<size_t>(pc.np * pc.ps));
-        pc.zcnt.alloc(static_cast<size_t>(pc.n));
-        k::build_zmap(pc.n, static_cast<int>(pc.ps), pc.inv_ptr.get(), pc.inv.get(), pc.slot_of.get(), pc.zfwd.get(),
-                      pc.zcnt.get(), s);
-      }
     }
   } else {
     build_inverse(pc, s);

@@ -24,10 +24,9 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "head0": {},
-    "head16": {"PDB_SELL_HEAD_MB": "16"},
-    "head32": {"PDB_SELL_HEAD_MB": "32"},
-    "head64": {"PDB_SELL_HEAD_MB": "64"},
+    "sell": {},
+    "v5": {"PDB_SPMV_VERSION": "5"},
+    "v2": {"PDB_SPMV_VERSION": "2"},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
