@@ -191,5 +191,6 @@ void xpay(int64_t n, const double* x, const double* beta, double* y, cudaStream_
 void axpy_val(int64_t n, double a, const double* x, double* y, cudaStream_t s);                      // y += a*x
 void div_scalar(int64_t n, const double* x, double sc, double* y, cudaStream_t s);                   // y = x / sc
 void sub(int64_t n, const double* a, const double* b, double* y, cudaStream_t s);                    // y = a - b
+void scalar_div(const double* a, const double* b, double* out, cudaStream_t s);                       // out = a/b (device scalars)
 
 }  // namespace pdb::k

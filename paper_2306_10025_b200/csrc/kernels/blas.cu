@@ -71,6 +71,10 @@ __global__ void sub_kernel(int64_t n, const double* __restrict__ a, const double
     y[i] = a[i] - b[i];
 }
 
+__global__ void scalar_div_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+  out[0] = a[0] / b[0];
+}
+
 inline unsigned ew_grid(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return (unsigned)(g < 4 * 148 * 8 ? (g > 0 ? g : 1) : 4 * 148 * 8);
@@ -99,6 +103,10 @@ void axpy_val(int64_t n, double a, const double* x, double* y, cudaStream_t s) {
 
 void div_scalar(int64_t n, const double* x, double sc, double* y, cudaStream_t s) {
   div_kernel<<<ew_grid(n), 256, 0, s>>>(n, x, sc, y);
+}
+
+void scalar_div(const double* a, const double* b, double* out, cudaStream_t s) {
+  scalar_div_kernel<<<1, 1, 0, s>>>(a, b, out);
 }
 
 void sub(int64_t n, const double* a, const double* b, double* y, cudaStream_t s) {

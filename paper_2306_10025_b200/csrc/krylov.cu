@@ -1,5 +1,8 @@
-// Device Krylov drivers.  Vectors stay in HBM; only the small Hessenberg /
-// Givens recurrences and the scalar control flow run on the host.
+// Device Krylov drivers.  Vectors and the recurrence scalars stay in HBM;
+// only the small Hessenberg / Givens recurrences and the convergence tests
+// run on the host, with one host synchronisation per iteration (GMRES: the
+// column of h_ij and ||w|| read in one copy; PCG: ||r||^2, with alpha and
+// beta formed on the device).
 //   gmres: reference gmres.cpp:27-169 (restarted GMRES(m), modified
 //          Gram-Schmidt, Givens rotations, right preconditioning by default,
 //          true residual at the end of each cycle).
@@ -23,9 +26,9 @@ struct Ops {
   k::SpmvPlan plan;
   Scratch<double> partials;
   Scratch<double> scal;  // device scalars
-  Ops(const DeviceCsr& a_, const pdb_precond_s* pc_, cudaStream_t s_)
+  Ops(const DeviceCsr& a_, const pdb_precond_s* pc_, cudaStream_t s_, size_t nscal = 64)
       : a(a_), pc(pc_), s(s_), plan(plan_of(a_)), partials(static_cast<size_t>(k::dot_partials()), s_),
-        scal(64, s_) {}
+        scal(std::max<size_t>(nscal, 64), s_) {}
   void spmv(const double* x, double* y) {
     k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);
   }
@@ -53,7 +56,7 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
   const int64_t n = a.n;
   require(o.restart >= 1, Errc::invalid_argument, "restart length must be >= 1");
   if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
-  Ops ops(a, pc, s);
+  Ops ops(a, pc, s, static_cast<size_t>(o.restart) + 2);
   const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
   DevBuf<double> b(un), x(un), r0(un), tmp(un), corr(un);
   b.upload(b_host, static_cast<size_t>(n), s);
@@ -114,15 +117,16 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
     bool breakdown = false;
     for (size_t j = 0; j < m; ++j) {
       apply_op(Vp(j), Vp(j + 1));
-      for (size_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt, h_ij stays on device for the axpy
-        double* hij = ops.dot_dev(Vp(j + 1), Vp(i), static_cast<int>(i % 48));
+      for (size_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt: h_ij in device slot i feeds the axpy
+        double* hij = ops.dot_dev(Vp(j + 1), Vp(i), static_cast<int>(i));
         k::axpy(n, hij, true, Vp(i), Vp(j + 1), s);
-        double hv = 0.0;
-        PDB_CUDA(cudaMemcpyAsync(&hv, hij, sizeof(double), cudaMemcpyDeviceToHost, s));
-        sync(s);
-        h[i][j] = hv;
       }
-      const double hj1 = ops.norm(Vp(j + 1));
+      ops.dot_dev(Vp(j + 1), Vp(j + 1), static_cast<int>(j + 1));
+      std::vector<double> hv(j + 2);
+      PDB_CUDA(cudaMemcpyAsync(hv.data(), ops.scal.get(), (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      sync(s);  // the iteration's only host synchronisation
+      for (size_t i = 0; i <= j; ++i) h[i][j] = hv[i];
+      const double hj1 = std::sqrt(hv[j + 1]);
       h[j + 1][j] = hj1;
       if (hj1 > 0.0) k::div_scalar(n, Vp(j + 1), hj1, Vp(j + 1), s);
       for (size_t i = 0; i < j; ++i) {
@@ -196,29 +200,34 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
       if (pc) precond_apply_device(*pc, r.get(), z.get(), s, /*symmetric=*/true);
       else PDB_CUDA(cudaMemcpyAsync(z.get(), r.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     };
+    // device scalar slots
+    constexpr int RZ = 0, PQ = 1, ALPHA = 2, RR = 3, RZN = 4, BETA = 5;
+    double* sc = ops.scal.get();
     precond();
     PDB_CUDA(cudaMemcpyAsync(p.get(), z.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    double rz = ops.dot(r.get(), z.get());
+    ops.dot_dev(r.get(), z.get(), RZ);
     while (rep.iterations < max_iters) {
       ops.spmv(p.get(), q.get());
-      const double alpha = rz / ops.dot(p.get(), q.get());
-      k::axpy_val(n, alpha, p.get(), x.get(), s);
-      k::axpy_val(n, -alpha, q.get(), r.get(), s);
+      ops.dot_dev(p.get(), q.get(), PQ);
+      k::scalar_div(sc + RZ, sc + PQ, sc + ALPHA, s);  // alpha = rz / (p, q)
+      k::axpy(n, sc + ALPHA, false, p.get(), x.get(), s);
+      k::axpy(n, sc + ALPHA, true, q.get(), r.get(), s);
+      ops.dot_dev(r.get(), r.get(), RR);
+      double rr = 0.0;
+      PDB_CUDA(cudaMemcpyAsync(&rr, sc + RR, sizeof(double), cudaMemcpyDeviceToHost, s));
+      sync(s);  // the iteration's only host synchronisation
       ++rep.iterations;
-      const double rel = ops.norm(r.get()) / bnorm;
+      const double rel = std::sqrt(rr) / bnorm;
       rep.residual_history.push_back(rel);
       if (rel <= tol) {
         rep.converged = true;
         break;
       }
       precond();
-      const double rz_new = ops.dot(r.get(), z.get());
-      const double beta = rz_new / rz;
-      rz = rz_new;
-      Scratch<double> bd(1, s);
-      PDB_CUDA(cudaMemcpyAsync(bd.get(), &beta, sizeof(double), cudaMemcpyHostToDevice, s));
-      k::xpay(n, z.get(), bd.get(), p.get(), s);
-      sync(s);
+      ops.dot_dev(r.get(), z.get(), RZN);
+      k::scalar_div(sc + RZN, sc + RZ, sc + BETA, s);  // beta = rz_new / rz
+      PDB_CUDA(cudaMemcpyAsync(sc + RZ, sc + RZN, sizeof(double), cudaMemcpyDeviceToDevice, s));
+      k::xpay(n, z.get(), sc + BETA, p.get(), s);
     }
   }
   rep.final_relative_residual = rep.residual_history.empty() ? 0.0 : rep.residual_history.back();

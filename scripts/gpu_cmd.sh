@@ -1,3 +1,2 @@
-timeout 300 python scripts/spmv_ab.py 2 > gpurun_out/ab_clean2.log 2>&1
-timeout 300 python scripts/spmv_ab.py 3 >> gpurun_out/ab_clean2.log 2>&1
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_clean2.log 2>&1; echo "exit $?" >> gpurun_out/t_clean2.log
+timeout 900 python -m pytest tests -x -q -m gpu -k "gmres or pcg or krylov" > gpurun_out/t_kry.log 2>&1; echo "exit $?" >> gpurun_out/t_kry.log
+timeout 600 python scripts/pcg_c2.py 2 entrywise > gpurun_out/pcg2.log 2>&1; echo "exit $?" >> gpurun_out/pcg2.log

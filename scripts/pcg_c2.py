@@ -17,7 +17,7 @@ pc = P.Preconditioner.create(A, ps, db, omega=1.0)
 b = prob.rhs()
 for rep in range(2):
     t = time.perf_counter()
-    x, r = P.pcg(A, b, pc, tol=1e-8)
+    x, r = P.pcg(A, b, pc, tol=1e-8, max_iters=int(os.environ.get("MAXIT", "500")))
     dt = time.perf_counter() - t
     print(f"rep {rep}: converged={r.converged} iterations={r.iterations} rel={r.final_relative_residual:.3e} "
           f"time {dt * 1e3:.1f} ms ({dt / max(r.iterations, 1) * 1e6:.0f} us/iteration)")
