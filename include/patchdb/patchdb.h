@@ -209,6 +209,10 @@ PDB_API pdb_status pdb_database_factors(pdb_database db, double* lu, int64_t* pi
 PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
                                               int64_t target_lo, int64_t target_hi, pdb_database* out,
                                               double* eps_out);
+/* Database import (setup reuse): the pair written by pdb_database_export
+ * (ref.h:114); factors are recomputed on the device, so the result equals the
+ * exported database bit for bit. */
+PDB_API pdb_status pdb_database_import(const char* json_path, const char* bin_path, pdb_database* out);
 /* Work counters of the last build on this thread: distance evaluations and
  * power iterations (spectral), for FP64 roofline accounting. */
 PDB_API pdb_status pdb_database_work(pdb_database db, int64_t* pair_evals, int64_t* power_iters, int64_t* lu_count);

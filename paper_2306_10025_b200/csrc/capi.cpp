@@ -472,6 +472,15 @@ PDB_API pdb_status pdb_database_work(pdb_database db, int64_t* pair_evals, int64
   return PDB_OK;
 }
 
+PDB_API pdb_status pdb_database_import(const char* json_path, const char* bin_path, pdb_database* out) {
+  if (json_path == nullptr || bin_path == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto db = std::make_unique<pdb_database_s>();
+    import_database(json_path, bin_path, *db, default_stream());
+    *out = db.release();
+  });
+}
+
 PDB_API pdb_status pdb_database_export(pdb_database db, const char* json_path, const char* bin_path) {
   if (db == nullptr || json_path == nullptr || bin_path == nullptr) return arg_error("null argument");
   return guarded([&] { export_database(*db, json_path, bin_path, default_stream()); });

@@ -988,4 +988,140 @@ void export_database(const pdb_database_s& db, const std::string& json_path, con
   if (!out) fail(Errc::io_error, "error while writing '" + json_path + "'");
 }
 
+
+// Import of an export_database pair (setup reuse across solves):
+// the JSON's phi, method, eps and entry partitions plus the binary
+// representatives; the factors are recomputed on the device by the same
+// bit-exact LU, so the imported database equals the exported one bit for
+// bit.  The files are parsed before any device work (errors: PDB_ERR_IO /
+// PDB_ERR_PARSE).
+namespace {
+
+struct JsonCursor {
+  const std::string& t;
+  const std::string& name;
+  size_t i = 0;
+  [[noreturn]] void bad(const std::string& what) const {
+    fail(Errc::parse_error, name + ": " + what + " at byte " + std::to_string(i));
+  }
+  void skip() {
+    while (i < t.size() && std::isspace(static_cast<unsigned char>(t[i]))) ++i;
+  }
+  bool key(const std::string& k) {  // moves to the value of "k"
+    const size_t at = t.find("\"" + k + "\"", i);
+    if (at == std::string::npos) return false;
+    i = at + k.size() + 2;
+    skip();
+    if (i >= t.size() || t[i] != ':') bad("expected ':' after \"" + k + "\"");
+    ++i;
+    skip();
+    return true;
+  }
+  std::string str() {
+    if (i >= t.size() || t[i] != '"') bad("expected a string");
+    const size_t e = t.find('"', i + 1);
+    if (e == std::string::npos) bad("unterminated string");
+    std::string v = t.substr(i + 1, e - i - 1);
+    i = e + 1;
+    return v;
+  }
+  double num() {
+    const char* b = t.c_str() + i;
+    char* e = nullptr;
+    const double v = std::strtod(b, &e);
+    if (e == b) bad("expected a number");
+    i += static_cast<size_t>(e - b);
+    return v;
+  }
+};
+
+}  // namespace
+
+void import_database(const std::string& json_path, const std::string& bin_path, pdb_database_s& db, cudaStream_t s) {
+  std::ifstream jf(json_path);
+  if (!jf) fail(Errc::io_error, "cannot open '" + json_path + "' for reading");
+  const std::string text((std::istreambuf_iterator<char>(jf)), std::istreambuf_iterator<char>());
+  JsonCursor c{text, json_path};
+  if (!c.key("method")) c.bad("missing \"method\"");
+  const std::string method = c.str();
+  c.i = 0;
+  if (!c.key("eps")) c.bad("missing \"eps\"");
+  const double eps = c.num();
+  c.i = 0;
+  if (!c.key("m_p")) c.bad("missing \"m_p\"");
+  const double mp = c.num();
+  c.i = 0;
+  if (!c.key("n_p")) c.bad("missing \"n_p\"");
+  const double np = c.num();
+  if (!(mp >= 1 && np >= mp && mp == std::floor(mp) && np == std::floor(np))) c.bad("invalid m_p / n_p");
+  const int64_t m = static_cast<int64_t>(mp), n = static_cast<int64_t>(np);
+  c.i = 0;
+  if (!c.key("entries")) c.bad("missing \"entries\"");
+  int64_t ps = -1;
+  std::vector<std::vector<uint8_t>> patterns;
+  for (int64_t j = 0; j < m; ++j) {
+    const size_t open = text.find('{', c.i);
+    const size_t close = text.find('}', open == std::string::npos ? c.i : open);
+    if (open == std::string::npos || close == std::string::npos) c.bad("entry list shorter than m_p");
+    c.i = open;
+    if (!c.key("rows") || c.i > close) c.bad("entry without \"rows\"");
+    const double rows = c.num();
+    if (!(rows >= 1 && rows == std::floor(rows))) c.bad("invalid entry size");
+    if (ps < 0) ps = static_cast<int64_t>(rows);
+    if (static_cast<int64_t>(rows) != ps) c.bad("entries of different sizes");
+    const size_t part = text.find("\"partition\"", open);
+    if (part != std::string::npos && part < close) {
+      c.i = part;
+      c.key("partition");
+      const std::string bits = c.str();
+      if (static_cast<int64_t>(bits.size()) != ps) c.bad("partition pattern length differs from the entry size");
+      std::vector<uint8_t> pat(bits.size());
+      for (size_t q = 0; q < bits.size(); ++q) pat[q] = bits[q] == '1';
+      patterns.push_back(std::move(pat));
+    }
+    c.i = close + 1;
+  }
+  if (!patterns.empty() && static_cast<int64_t>(patterns.size()) != m) c.bad("partition patterns on some entries only");
+  if (!c.key("phi")) c.bad("missing \"phi\"");
+  if (c.i >= text.size() || text[c.i] != '[') c.bad("expected '['");
+  ++c.i;
+  std::vector<int32_t> phi(static_cast<size_t>(n));
+  for (int64_t k = 0; k < n; ++k) {
+    c.skip();
+    if (k > 0) {
+      if (c.i >= text.size() || text[c.i] != ',') c.bad("expected ','");
+      ++c.i;
+      c.skip();
+    }
+    const double v = c.num();
+    if (!(v >= 0 && v < static_cast<double>(m) && v == std::floor(v))) c.bad("phi entry outside [0, m_p)");
+    phi[static_cast<size_t>(k)] = static_cast<int32_t>(v);
+  }
+  const int64_t len = ps * ps;
+  std::vector<double> reps(static_cast<size_t>(m * len));
+  std::ifstream bf(bin_path, std::ios::binary);
+  if (!bf) fail(Errc::io_error, "cannot open '" + bin_path + "' for reading");
+  bf.read(reinterpret_cast<char*>(reps.data()), static_cast<std::streamsize>(reps.size() * sizeof(double)));
+  if (bf.gcount() != static_cast<std::streamsize>(reps.size() * sizeof(double)))
+    fail(Errc::parse_error, bin_path + ": expected " + std::to_string(m * len) + " doubles");
+  require_device();
+  db.m = m;
+  db.np = n;
+  db.ps = ps;
+  db.eps = eps;
+  db.method = method;
+  db.entry_patterns = std::move(patterns);
+  db.reps.alloc(reps.size());
+  db.reps.upload(reps.data(), reps.size(), s);
+  db.lu.alloc(reps.size());
+  db.piv.alloc(static_cast<size_t>(m * ps));
+  std::string msg;
+  const int64_t bad = lu_many(m, static_cast<int>(ps), db.reps.get(), nullptr, db.lu.get(), db.piv.get(), msg,
+                              db.work, s);
+  if (bad >= 0) fail(Errc::singular_matrix, "entry " + std::to_string(bad) + ": " + msg);
+  db.phi.alloc(phi.size());
+  db.phi.upload(phi.data(), phi.size(), s);
+  sync(s);
+}
+
 }  // namespace pdb

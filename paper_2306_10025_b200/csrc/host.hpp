@@ -63,6 +63,7 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
                               pdb_database_s& out, cudaStream_t s);
 double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, int64_t lo, int64_t hi,
                        pdb_database_s& out, cudaStream_t s);
+void import_database(const std::string& json_path, const std::string& bin_path, pdb_database_s& db, cudaStream_t s);
 void export_database(const pdb_database_s& db, const std::string& json_path, const std::string& bin_path,
                      cudaStream_t s);
 

@@ -136,6 +136,7 @@ _sig("pdb_database_representatives", C.c_int, _P, _D)
 _sig("pdb_database_factors", C.c_int, _P, _D, _I64)
 _sig("pdb_database_work", C.c_int, _P, _I64, _I64, _I64)
 _sig("pdb_database_export", C.c_int, _P, C.c_char_p, C.c_char_p)
+_sig("pdb_database_import", C.c_int, C.c_char_p, C.c_char_p, C.POINTER(_P))
 _sig("pdb_database_free", None, _P)
 _sig("pdb_precond_create", C.c_int, _P, _P, _P, C.c_double, C.c_int, C.POINTER(_P))
 _sig("pdb_precond_create_combo", C.c_int, _P, _P, _P, C.c_double, C.c_int, C.POINTER(_P))
@@ -417,6 +418,13 @@ class Database(_Handle):
 
     def export(self, json_path: str, bin_path: str) -> None:
         _check(_lib.pdb_database_export(self._ptr, json_path.encode(), bin_path.encode()))
+
+    @classmethod
+    def load(cls, json_path: str, bin_path: str) -> "Database":
+        """pdb_database_import: a database written by export (setup reuse)."""
+        out = C.c_void_p()
+        _check(_lib.pdb_database_import(json_path.encode(), bin_path.encode(), C.byref(out)))
+        return cls(out)
 
 
 class Preconditioner(_Handle):

@@ -1,4 +1,1 @@
-for pf in 0 1 2 3; do
-  PDB_SPECTRAL_PF=$pf ITERS=10 timeout 300 python scripts/setup_small.py 256 >> gpurun_out/setup_pf.log 2>&1
-done
-PDB_SPECTRAL_PF=2 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "spectral" >> gpurun_out/setup_pf.log 2>&1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/t_imp.log 2>&1; echo "exit $?" >> gpurun_out/t_imp.log

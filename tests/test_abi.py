@@ -160,3 +160,21 @@ def test_sharded_setup_entry_points_validate_before_device(P):
     assert "rank" in L.pdb_last_error().decode()
     assert L.pdb_database_build_sharded(None, None, None, None, C.byref(out)) == P.PDB_ERR_INVALID_ARGUMENT
     L.pdb_comm_free(None)
+
+
+def test_database_import_errors_before_device(P, tmp_path):
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.load(str(tmp_path / "missing.json"), str(tmp_path / "missing.bin"))
+    assert e.value.status == P.PDB_ERR_IO
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"method": "kmeans", "eps": 0, "m_p": 2, "n_p": 3, "entries": [{"rows": 9, "cols": 9}]}')
+    (tmp_path / "bad.bin").write_bytes(b"")
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.load(str(bad), str(tmp_path / "bad.bin"))
+    assert e.value.status == P.PDB_ERR_PARSE
+    ok = tmp_path / "ok.json"
+    ok.write_text('{"method": "m", "eps": 0.5, "m_p": 1, "n_p": 2, "entries": [{"rows": 2, "cols": 2}], "phi": [0, 0]}')
+    (tmp_path / "short.bin").write_bytes(b"\0" * 8)
+    with pytest.raises(P.PatchdbError) as e:
+        P.Database.load(str(ok), str(tmp_path / "short.bin"))
+    assert e.value.status == P.PDB_ERR_PARSE and "expected 4 doubles" in e.value.message

@@ -283,3 +283,25 @@ def test_pipelined_host_relax_matches_device_path(P, monkeypatch, sweeps):
     want, _ = pc.relax(A, b, x0, sweeps, history=False)
     assert np.array_equal(got, want)
     assert not np.array_equal(got, x0)
+
+
+@pytest.mark.parametrize("method", [2, 3, 4])
+def test_database_export_import_round_trip(c1, P, tmp_path, method):
+    """pdb_database_import(pdb_database_export(db)) == db bit for bit (phi,
+    representatives, recomputed factors), and it drives the same sweep."""
+    kw = dict(eps=2.0) if method == 2 else dict(db_size=51, seed=42, max_iters=20)
+    db = P.Database.build(c1.A, c1.ps, method, **kw)
+    js, bn = str(tmp_path / "db.json"), str(tmp_path / "db.bin")
+    db.export(js, bn)
+    db2 = P.Database.load(js, bn)
+    assert db2.size == db.size and db2.n_patches == db.n_patches
+    assert np.array_equal(db2.phi(), db.phi())
+    assert np.array_equal(db2.representatives(), db.representatives())
+    l1, p1 = db.factors()
+    l2, p2 = db2.factors()
+    assert np.array_equal(l1, l2) and np.array_equal(p1, p2)
+    pc1 = P.Preconditioner.create(c1.A, c1.ps, db, omega=0.8)
+    pc2 = P.Preconditioner.create(c1.A, c1.ps, db2, omega=0.8)
+    x1, h1 = pc1.relax(c1.A, c1.b, np.zeros_like(c1.b), 5)
+    x2, h2 = pc2.relax(c1.A, c1.b, np.zeros_like(c1.b), 5)
+    assert np.array_equal(x1, x2) and np.array_equal(h1, h2)
