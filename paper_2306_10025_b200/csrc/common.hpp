@@ -131,6 +131,10 @@ class Scratch {
   }
   Scratch(const Scratch&) = delete;
   Scratch& operator=(const Scratch&) = delete;
+  Scratch(Scratch&& o) noexcept : s_(o.s_), p_(o.p_), n_(o.n_) {
+    o.p_ = nullptr;
+    o.n_ = 0;
+  }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
 

@@ -24,9 +24,8 @@ b = torch.from_numpy(prob.rhs()).cuda()
 x = torch.zeros_like(b)
 s = torch.cuda.current_stream().cuda_stream
 variants = {
-    "sell": {},
-    "v5": {"PDB_SPMV_VERSION": "5"},
-    "v2": {"PDB_SPMV_VERSION": "2"},
+    "two_kernel": {"PDB_FUSE": "0"},
+    "fused": {},
 }
 extra = [v for v in os.environ.get("AB_VARIANTS", "").split(";") if v]
 for v in extra:  # NAME=K1:V1,K2:V2
