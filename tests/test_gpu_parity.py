@@ -305,3 +305,30 @@ def test_database_export_import_round_trip(c1, P, tmp_path, method):
     x1, h1 = pc1.relax(c1.A, c1.b, np.zeros_like(c1.b), 5)
     x2, h2 = pc2.relax(c1.A, c1.b, np.zeros_like(c1.b), 5)
     assert np.array_equal(x1, x2) and np.array_equal(h1, h2)
+
+
+def _ragged_csr(seed, n):
+    """Random CSR with empty rows, single entries, rows longer than a warp item
+    (> 256) and than a SELL step group, unsorted lengths."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.choice([0, 1, 3, 17, 50, 300, 1100], size=n, p=[0.1, 0.2, 0.2, 0.2, 0.2, 0.08, 0.02]), n)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.sort(rng.choice(n, size=int(k), replace=False)) for k in lens if k > 0]).astype(np.int64)
+    v = rng.uniform(-1, 1, rp[-1])
+    return rp, ci, v
+
+
+@pytest.mark.parametrize("seed,n", [(1, 37), (2, 5000), (3, 9001)])
+def test_spmv_ragged_rows(P, orc, monkeypatch, seed, n):
+    """Empty, single-entry and long rows: the SELL kernel stays bitwise the
+    reference sum; the CSR warp-item (v5, long-row path) and row-group (v2)
+    kernels agree to rounding."""
+    csr = _ragged_csr(seed, n)
+    A = P.Matrix.from_csr(*csr)
+    x = np.random.default_rng(seed + 10).uniform(-1, 1, n)
+    want = orc.spmv(csr, x)
+    assert np.array_equal(A.spmv(x), want)
+    for ver in ("5", "2"):
+        monkeypatch.setenv("PDB_SPMV_VERSION", ver)
+        np.testing.assert_allclose(A.spmv(x), want, rtol=1e-12, atol=1e-12)
