@@ -237,6 +237,13 @@ PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double*
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc);
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc);
 PDB_API int64_t pdb_precond_patch_size(pdb_precond pc);
+/* Combo preconditioners (pdb_precond_create_combo): coarse-space size n_c and
+ * the band widths kl, ku of R0 A P0 (0 and PDB_OK with *nc = 0 for a plain
+ * patch preconditioner), and the device band LU copied out in the reference's
+ * BandedFactor layout (banded.hpp:13-24): band[(2*kl+ku+1) * n_c] row-major by
+ * band row, ipiv[n_c] absolute pivot rows.  Either output may be NULL. */
+PDB_API pdb_status pdb_precond_coarse_size(pdb_precond pc, int64_t* nc, int64_t* kl, int64_t* ku);
+PDB_API pdb_status pdb_precond_coarse_factor(pdb_precond pc, double* band, int64_t* ipiv);
 
 /* Preconditioned conjugate gradients, x0 = 0, stop when ||r||/||b|| <= tol.
  * The patch preconditioner is applied with symmetric weighting

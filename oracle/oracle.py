@@ -335,6 +335,31 @@ class RefLib:
         L.refh_matrix_csr.argtypes = [_P, _I64, _I64, _D]
         L.refh_db_from_arrays.restype = _P
         L.refh_db_from_arrays.argtypes = [C.c_int64, C.c_int64, C.c_int64, _D, _D, _I64, _I64]
+        L.refh_problem_assemble.argtypes = [C.c_char_p, C.POINTER(_P)]
+        L.refh_problem_free.argtypes = [_P]
+        for f in ("refh_problem_n", "refh_problem_nnz"):
+            getattr(L, f).restype = C.c_int64
+            getattr(L, f).argtypes = [_P]
+        L.refh_problem_csr.argtypes = [_P, _I64, _I64, _D]
+        L.refh_problem_rhs.argtypes = [_P, _D]
+        L.refh_problem_exact.argtypes = [_P, _D]
+        L.refh_problem_l2_error.argtypes = [_P, _D, _D]
+        L.refh_problem_matrix.restype = _P
+        L.refh_problem_matrix.argtypes = [_P]
+        L.refh_coarse_sizes.argtypes = [_P, _I64, _I64, _I64, _I64]
+        L.refh_coarse_csr.argtypes = [_P, _I64, _I64, _D, _I64, _I64, _D]
+        L.refh_coarse_factor.argtypes = [_P, _I64, _I64, _D, _I64]
+        L.refh_combo_new.argtypes = [_P, _P, _P, C.c_double, C.c_int, C.POINTER(_P)]
+        L.refh_export_matrix.argtypes = [C.c_char_p, C.c_char_p]
+
+    def export_matrix(self, config_json: str, path: str):
+        self._check(self.lib.refh_export_matrix(config_json.encode(), path.encode()))
+
+    def problem(self, config_json: str = ""):
+        """pdb_problem_assemble's recipe on the reference (capi.cpp:169-179)."""
+        out = _P()
+        self._check(self.lib.refh_problem_assemble(config_json.encode(), C.byref(out)))
+        return RefProblem(self, out.value)
 
     def database(self, reps, lu, piv, phi):
         reps, lu, piv, phi = _f64(reps), _f64(lu), _i64(piv), _i64(phi)
@@ -519,6 +544,74 @@ class RefDatabase:
         buf = C.create_string_buffer(128)
         self.L.refh_db_method(self.ptr, buf, 128)
         return buf.value.decode()
+
+
+class RefProblem:
+    """Reference DiscreteProblem (fem.hpp:55-61) with its coarse space."""
+
+    def __init__(self, ref: RefLib, ptr):
+        self.ref, self.ptr, self.L = ref, ptr, ref.lib
+
+    def __del__(self):
+        try:
+            self.L.refh_problem_free(self.ptr)
+        except Exception:
+            pass
+
+    @property
+    def n(self):
+        return self.L.refh_problem_n(self.ptr)
+
+    def csr(self):
+        n, nnz = self.n, self.L.refh_problem_nnz(self.ptr)
+        rp, ci, v = np.empty(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+        self.L.refh_problem_csr(self.ptr, _ip(rp), _ip(ci), _dp(v))
+        return rp, ci, v
+
+    def rhs(self):
+        out = np.empty(self.n)
+        self.L.refh_problem_rhs(self.ptr, _dp(out))
+        return out
+
+    def exact(self):
+        out = np.empty(self.n)
+        self.L.refh_problem_exact(self.ptr, _dp(out))
+        return out
+
+    def l2_error(self, u):
+        out = np.zeros(1)
+        self.ref._check(self.L.refh_problem_l2_error(self.ptr, _dp(_f64(u)), _dp(out)))
+        return float(out[0])
+
+    def matrix(self) -> "RefMatrix":
+        return RefMatrix(self.ref, self.L.refh_problem_matrix(self.ptr))
+
+    def coarse(self):
+        """(P0 csr, R0 A P0 csr) as int64/fp64 arrays (fem.cpp:433-479)."""
+        sz = np.zeros(4, np.int64)
+        self.ref._check(self.L.refh_coarse_sizes(self.ptr, _ip(sz[0:]), _ip(sz[1:]), _ip(sz[2:]), _ip(sz[3:])))
+        fine_n, nc, pnnz, cnnz = (int(v) for v in sz)
+        p_rp, p_ci, p_v = np.empty(fine_n + 1, np.int64), np.empty(pnnz, np.int64), np.empty(pnnz)
+        c_rp, c_ci, c_v = np.empty(nc + 1, np.int64), np.empty(cnnz, np.int64), np.empty(cnnz)
+        self.ref._check(self.L.refh_coarse_csr(self.ptr, _ip(p_rp), _ip(p_ci), _dp(p_v), _ip(c_rp), _ip(c_ci),
+                                               _dp(c_v)))
+        return (p_rp, p_ci, p_v), (c_rp, c_ci, c_v)
+
+    def coarse_factor(self):
+        """band_factor(R0 A P0): (kl, ku, ab[(2kl+ku+1), n], ipiv[n])."""
+        kk = np.zeros(2, np.int64)
+        self.ref._check(self.L.refh_coarse_factor(self.ptr, _ip(kk[0:]), _ip(kk[1:]), None, None))
+        kl, ku = int(kk[0]), int(kk[1])
+        nc = self.coarse()[1][0].shape[0] - 1
+        ab, ipiv = np.empty((2 * kl + ku + 1, nc)), np.empty(nc, np.int64)
+        self.ref._check(self.L.refh_coarse_factor(self.ptr, _ip(kk[0:]), _ip(kk[1:]), _dp(ab), _ip(ipiv)))
+        return kl, ku, ab, ipiv
+
+    def combo(self, m: "RefMatrix", ps: "RefPatchSet", db=None, omega=1.0, threads=1):
+        out = _P()
+        self.ref._check(self.L.refh_combo_new(self.ptr, ps.ptr, None if db is None else db.ptr, omega, threads,
+                                              C.byref(out)))
+        return RefPrecond(self.ref, out.value, m)
 
 
 class RefPrecond:

@@ -400,3 +400,98 @@ RH_API void refh_matrix_csr(void* m, int64_t* rp, int64_t* ci, double* v) {
   std::memcpy(ci, a->col_idx.data(), sizeof(int64_t) * a->col_idx.size());
   std::memcpy(v, a->values.data(), sizeof(double) * a->values.size());
 }
+
+/* ---- model problems and the combo preconditioner (capi.cpp:169-212, 320-333;
+ *      fem.cpp:248-479; banded.cpp:11-84; precond.cpp:103-121) ---- */
+
+// pdb_problem_assemble's exact recipe: parse_config + resolve_coefficient
+// (constant fallback) + assemble.
+RH_API int refh_problem_assemble(const char* json, void** out) {
+  return guarded([&] {
+    const ExperimentConfig cfg = parse_config(json);
+    const Coefficient coeff = resolve_coefficient(cfg, CoeffKind::Constant);
+    StructuredMesh mesh{cfg.dim, cfg.cells, cfg.degree};
+    *out = new DiscreteProblem(assemble(mesh, coeff));
+  });
+}
+RH_API void refh_problem_free(void* p) { delete static_cast<DiscreteProblem*>(p); }
+RH_API int64_t refh_problem_n(void* p) { return static_cast<DiscreteProblem*>(p)->matrix.n; }
+RH_API int64_t refh_problem_nnz(void* p) { return static_cast<DiscreteProblem*>(p)->matrix.nnz(); }
+RH_API void refh_problem_csr(void* p, int64_t* rp, int64_t* ci, double* v) {
+  const SparseMatrix& a = static_cast<DiscreteProblem*>(p)->matrix;
+  std::memcpy(rp, a.row_ptr.data(), sizeof(int64_t) * a.row_ptr.size());
+  std::memcpy(ci, a.col_idx.data(), sizeof(int64_t) * a.col_idx.size());
+  std::memcpy(v, a.values.data(), sizeof(double) * a.values.size());
+}
+RH_API void refh_problem_rhs(void* p, double* out) {
+  const auto& r = static_cast<DiscreteProblem*>(p)->rhs;
+  std::memcpy(out, r.data(), sizeof(double) * r.size());
+}
+RH_API void refh_problem_exact(void* p, double* out) {
+  const std::vector<double> u = exact_solution(static_cast<DiscreteProblem*>(p)->mesh);
+  std::memcpy(out, u.data(), sizeof(double) * u.size());
+}
+RH_API int refh_problem_l2_error(void* p, const double* u, double* out) {
+  auto* pr = static_cast<DiscreteProblem*>(p);
+  return guarded([&] { *out = l2_error(pr->mesh, {u, static_cast<size_t>(pr->matrix.n)}); });
+}
+// A copy of the problem's matrix as a harness matrix handle.
+RH_API void* refh_problem_matrix(void* p) { return new SparseMatrix(static_cast<DiscreteProblem*>(p)->matrix); }
+
+// Coarse space: sizes, then P0 and R0 A P0 as CSR, then the band factor.
+RH_API int refh_coarse_sizes(void* p, int64_t* fine_n, int64_t* nc, int64_t* p0_nnz, int64_t* c_nnz) {
+  auto* pr = static_cast<DiscreteProblem*>(p);
+  return guarded([&] {
+    const CoarseSpace cs = build_coarse_and_transfer(pr->mesh, pr->matrix);
+    *fine_n = cs.p0.fine_n;
+    *nc = cs.p0.coarse_n;
+    *p0_nnz = static_cast<int64_t>(cs.p0.col.size());
+    *c_nnz = cs.coarse_matrix.nnz();
+  });
+}
+RH_API int refh_coarse_csr(void* p, int64_t* p0_rp, int64_t* p0_ci, double* p0_v, int64_t* c_rp, int64_t* c_ci,
+                           double* c_v) {
+  auto* pr = static_cast<DiscreteProblem*>(p);
+  return guarded([&] {
+    const CoarseSpace cs = build_coarse_and_transfer(pr->mesh, pr->matrix);
+    std::memcpy(p0_rp, cs.p0.row_ptr.data(), sizeof(int64_t) * cs.p0.row_ptr.size());
+    std::memcpy(p0_ci, cs.p0.col.data(), sizeof(int64_t) * cs.p0.col.size());
+    std::memcpy(p0_v, cs.p0.val.data(), sizeof(double) * cs.p0.val.size());
+    const SparseMatrix& c = cs.coarse_matrix;
+    std::memcpy(c_rp, c.row_ptr.data(), sizeof(int64_t) * c.row_ptr.size());
+    std::memcpy(c_ci, c.col_idx.data(), sizeof(int64_t) * c.col_idx.size());
+    std::memcpy(c_v, c.values.data(), sizeof(double) * c.values.size());
+  });
+}
+// band: (2kl+ku+1) x n row-major (BandedFactor::ab), ipiv absolute rows.
+// Call with band == NULL first to get kl, ku.
+RH_API int refh_coarse_factor(void* p, int64_t* kl, int64_t* ku, double* band, int64_t* ipiv) {
+  auto* pr = static_cast<DiscreteProblem*>(p);
+  return guarded([&] {
+    const CoarseSpace cs = build_coarse_and_transfer(pr->mesh, pr->matrix);
+    const BandedFactor f = band_factor(cs.coarse_matrix);
+    *kl = f.kl;
+    *ku = f.ku;
+    if (band) std::memcpy(band, f.ab.data(), sizeof(double) * f.ab.size());
+    if (ipiv) std::memcpy(ipiv, f.ipiv.data(), sizeof(int64_t) * f.ipiv.size());
+  });
+}
+// Combo preconditioner exactly as pdb_precond_create_combo builds it.
+RH_API int refh_combo_new(void* p, void* ps, void* db, double omega, int threads, void** out) {
+  auto* pr = static_cast<DiscreteProblem*>(p);
+  return guarded([&] {
+    PatchPreconditioner patch_pc =
+        db == nullptr ? PatchPreconditioner::exact(pr->matrix, *static_cast<PatchSet*>(ps), omega, threads)
+                      : PatchPreconditioner::compressed(*static_cast<PatchSet*>(ps), *static_cast<Database*>(db),
+                                                        omega, threads);
+    const CoarseSpace cs = build_coarse_and_transfer(pr->mesh, pr->matrix);
+    auto h = std::make_unique<RefPc>();
+    h->pc = std::make_unique<ComboPreconditioner>(std::move(patch_pc), cs);
+    *out = h.release();
+  });
+}
+
+// pdb_export_matrix's recipe (capi.cpp:422-428, experiments.cpp:430-435).
+RH_API int refh_export_matrix(const char* json, const char* path) {
+  return guarded([&] { export_matrix(parse_config(json), path); });
+}

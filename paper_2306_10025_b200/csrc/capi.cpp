@@ -192,7 +192,13 @@ PDB_API pdb_status pdb_matrix_csr(pdb_matrix m, int64_t* row_ptr, int64_t* col_i
 
 PDB_API pdb_status pdb_problem_assemble(const char* config_json, pdb_problem* out) {
   if (config_json == nullptr || out == nullptr) return arg_error("null argument");
-  return unsupported("pdb_problem_assemble");
+  return guarded([&] {
+    ModelConfig m = parse_model_config(config_json);
+    resolve_model_coefficient(m);
+    auto p = std::make_unique<pdb_problem_s>();
+    assemble_model_problem(m, *p);
+    *out = p.release();
+  });
 }
 
 PDB_API int64_t pdb_problem_ndofs(pdb_problem p) { return p == nullptr ? 0 : p->a.n; }
@@ -231,7 +237,7 @@ PDB_API pdb_status pdb_problem_exact_solution(pdb_problem p, double* out) {
 
 PDB_API pdb_status pdb_problem_l2_error(pdb_problem p, const double* discrete_solution, double* out) {
   if (p == nullptr || discrete_solution == nullptr || out == nullptr) return arg_error("null argument");
-  return unsupported("pdb_problem_l2_error");
+  return guarded([&] { *out = model_l2_error(*p, discrete_solution); });
 }
 
 PDB_API void pdb_problem_free(pdb_problem p) { delete p; }
@@ -507,9 +513,25 @@ PDB_API pdb_status pdb_precond_create(pdb_matrix m, pdb_patchset ps, pdb_databas
 
 PDB_API pdb_status pdb_precond_create_combo(pdb_problem p, pdb_patchset ps, pdb_database db, double omega,
                                             int threads, pdb_precond* out) {
-  (void)db, (void)omega, (void)threads;
+  (void)threads;
   if (p == nullptr || ps == nullptr || out == nullptr) return arg_error("null argument");
-  return unsupported("pdb_precond_create_combo");
+  return guarded([&] {
+    cudaStream_t s = default_stream();
+    auto pc = std::make_unique<pdb_precond_s>();
+    if (db == nullptr) {
+      require_device();
+      DeviceCsr a;
+      upload_csr(p->a, a, s);
+      precond_exact(a, *ps, omega, *pc, s);
+    } else {
+      precond_compressed(*ps, *db, omega, *pc, s);
+    }
+    const CoarseSpaceHost cs = build_coarse_space(*p);
+    require(cs.p0.rows == pc->n, Errc::dimension_mismatch, "transfer operator does not match the patch term");
+    pc->coarse = std::make_shared<CoarseDev>();
+    coarse_setup(cs, *pc->coarse, s);
+    *out = pc.release();
+  });
 }
 
 PDB_API pdb_status pdb_precond_apply(pdb_precond pc, const double* r, double* z) {
@@ -568,6 +590,34 @@ PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double*
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc) { return pc == nullptr ? 0 : pc->nf; }
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc) { return pc == nullptr ? 0 : pc->np; }
 PDB_API int64_t pdb_precond_patch_size(pdb_precond pc) { return pc == nullptr ? 0 : pc->ps; }
+
+PDB_API pdb_status pdb_precond_coarse_size(pdb_precond pc, int64_t* nc, int64_t* kl, int64_t* ku) {
+  if (pc == nullptr || nc == nullptr || kl == nullptr || ku == nullptr) return arg_error("null argument");
+  const CoarseDev* c = pc->coarse.get();
+  *nc = c ? c->nc : 0;
+  *kl = c ? c->kl : 0;
+  *ku = c ? c->ku : 0;
+  return PDB_OK;
+}
+
+PDB_API pdb_status pdb_precond_coarse_factor(pdb_precond pc, double* band, int64_t* ipiv) {
+  if (pc == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const CoarseDev* c = pc->coarse.get();
+    require(c != nullptr, Errc::invalid_argument, "not a combo preconditioner");
+    cudaStream_t s = default_stream();
+    const size_t n = static_cast<size_t>(c->nc), ld = static_cast<size_t>(c->ldab);
+    if (band) {
+      const std::vector<double> cm = c->band.to_host(s);  // column-major [n][ldab]
+      for (size_t j = 0; j < n; ++j)
+        for (size_t r = 0; r < ld; ++r) band[r * n + j] = cm[j * ld + r];
+    }
+    if (ipiv) {
+      const std::vector<int32_t> p = c->ipiv.to_host(s);
+      for (size_t j = 0; j < n; ++j) ipiv[j] = p[j];
+    }
+  });
+}
 
 PDB_API void pdb_precond_free(pdb_precond pc) { delete pc; }
 
@@ -725,7 +775,13 @@ PDB_API pdb_status pdb_run_benchmark(const char* config_json, const char* out_cs
 
 PDB_API pdb_status pdb_export_matrix(const char* config_json, const char* out_path) {
   if (config_json == nullptr || out_path == nullptr) return arg_error("null argument");
-  return unsupported("pdb_export_matrix");
+  return guarded([&] {  // experiments.cpp:430-435: smooth (experiment 1) or piecewise (2) fallback
+    ModelConfig m = parse_model_config(config_json);
+    resolve_model_coefficient(m, m.experiment == 2 ? "piecewise" : "smooth");
+    pdb_problem_s p;
+    assemble_model_problem(m, p);
+    write_matrix_market_host(p.a, out_path);
+  });
 }
 
 }  // extern "C"

@@ -371,6 +371,7 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
   out.dim = d;
   out.cells = C;
   out.degree = p;
+  out.components = 1;
 }
 
 // ---- vector systems: Stokes (config 4) and linear elasticity (config 5) ----
@@ -780,6 +781,7 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
   out.dim = d;
   out.cells = C;
   out.degree = p;
+  out.components = 0;  // vector / mixed DoFs: no scalar lattice
 }
 
 }  // namespace pdb

@@ -29,6 +29,43 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out);
 // physics 1 (Stokes Q_p-Q_{p-1}, 2D) and 2 (linear elasticity): node-major vector DoFs
 void generate_system(const pdb_gen_options& o, pdb_problem_s& out);
 
+// model_problem.cpp -- the reference's uniform-mesh model problems and the
+// two-level coarse space (pdb_problem_assemble, pdb_precond_create_combo)
+struct ModelConfig {
+  int dim = 2;
+  Index cells = 60;
+  int degree = 2;
+  std::string kind;  // "", "constant", "smooth", "piecewise"
+  double value = 1.0;
+  Index blocks_x = 4, blocks_y = 4;
+  std::vector<double> block_values;
+  int experiment = 1;
+  enum Coeff { Constant, Smooth, Piecewise } coeff = Constant;
+};
+ModelConfig parse_model_config(const std::string& json);
+// An explicit coefficient.kind wins, else `fallback` ("constant" for
+// pdb_problem_assemble, "smooth"/"piecewise" by experiment for export).
+void resolve_model_coefficient(ModelConfig& m, const char* fallback = "constant");
+void assemble_model_problem(const ModelConfig& m, pdb_problem_s& out);
+double model_l2_error(const pdb_problem_s& p, const double* u);
+// Rectangular CSR operator (rows x cols).
+struct CoarseOp {
+  Index rows = 0, cols = 0;
+  std::vector<int64_t> ptr;
+  std::vector<int32_t> col;
+  std::vector<double> val;
+};
+struct CoarseSpaceHost {
+  CoarseOp p0;      // fine DoFs x coarse vertices (bilinear interpolation)
+  CoarseOp r0;      // P0^T, rows in ascending fine order
+  CoarseOp coarse;  // R0 A P0
+};
+CoarseSpaceHost build_coarse_space(const pdb_problem_s& p);
+
+// coarse.cu -- device coarse correction z += P0 (R0 A P0)^{-1} R0 r
+void coarse_setup(const CoarseSpaceHost& cs, pdb::CoarseDev& out, cudaStream_t s);
+void coarse_correct(const pdb::CoarseDev& c, const double* r, double* z, cudaStream_t s);
+
 // patchset.cpp
 void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStream_t s);
 void extract_patches(const DeviceCsr& a, const pdb_patchset_s& ps, DevBuf<double>& mats, cudaStream_t s);

@@ -45,6 +45,21 @@ struct DeviceCsr {
   int64_t nslices = 0;  // 0: not built
 };
 
+// Two-level coarse correction of the combo preconditioner (reference
+// ComboPreconditioner, precond.cpp:103-121): P0 and R0 = P0^T as CSR, the
+// banded LU of R0 A P0 in COLUMN-major band storage (column j holds band
+// rows 0..ldab-1 of the reference's LAPACK-style layout, banded.cpp:11-60).
+struct CoarseDev {
+  Index fine_n = 0, nc = 0, kl = 0, ku = 0, ldab = 0;
+  DevBuf<int32_t> p0_ptr, p0_col, r0_ptr, r0_col;
+  DevBuf<double> p0_val, r0_val;
+  DevBuf<double> band;   // [nc][ldab]
+  DevBuf<int32_t> ipiv;  // absolute pivot row per column
+  DevBuf<double> rdiag;  // 1 / U(j, j)
+  DevBuf<double> inv;    // dense (R0 A P0)^{-1}, row-major [nc][ld], when ld > 0
+  Index ld = 0;
+};
+
 struct BuildWork {
   int64_t pair_evals = 0;
   int64_t power_iters = 0;
@@ -61,6 +76,7 @@ struct pdb_problem_s {
   int dim = 2;
   int64_t cells = 0;
   int degree = 1;
+  int components = 1;  // DoFs per lattice node (vector generators: > 1)
 };
 
 struct pdb_matrix_s {
@@ -107,6 +123,7 @@ struct pdb_precond_s {
   int maxc_pad = 0;
   pdb::DevBuf<int32_t> inv_ptr;
   pdb::DevBuf<int32_t> inv;
+  std::shared_ptr<pdb::CoarseDev> coarse;  // combo preconditioner only
 };
 
 struct pdb_report_s {

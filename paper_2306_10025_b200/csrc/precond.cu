@@ -255,6 +255,7 @@ void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, c
   Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
   patch_stage(pc, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
   scatter_stage(pc, sols.get(), symmetric, nullptr, z, nullptr, s);
+  if (pc.coarse) coarse_correct(*pc.coarse, r, z, s);  // combo: z += P0 Ac^{-1} R0 r
   PDB_LAUNCH_CHECK();
 }
 
@@ -265,6 +266,8 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
   Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
   Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
   Scratch<double> partials(static_cast<size_t>(std::max(plan.blocks, 1)), s);
+  // combo: x + (patch term + coarse term), the reference's z += x order
+  Scratch<double> z(pc.coarse ? static_cast<size_t>(std::max<int64_t>(a.n, 1)) : 1, s);
   for (int64_t sw = 0; sw <= sweeps; ++sw) {
     if (sw == sweeps && !history) break;
     k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), history ? partials.get() : nullptr,
@@ -272,7 +275,13 @@ void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, 
     if (history) k::finish_sum(partials.get(), plan.blocks, history + sw, true, s);
     if (sw == sweeps) break;
     patch_stage(pc, r.get(), nullptr, sols.get(), s);
-    scatter_stage(pc, sols.get(), false, x, nullptr, x, s);
+    if (pc.coarse) {
+      scatter_stage(pc, sols.get(), false, nullptr, z.get(), nullptr, s);
+      coarse_correct(*pc.coarse, r.get(), z.get(), s);
+      k::axpy_val(a.n, 1.0, z.get(), x, s);
+    } else {
+      scatter_stage(pc, sols.get(), false, x, nullptr, x, s);
+    }
   }
   PDB_LAUNCH_CHECK();
 }
@@ -289,7 +298,7 @@ void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, 
   Scratch<double> db(std::max<size_t>(n, 1), s), dx(std::max<size_t>(n, 1), s);
   const k::SpmvPlan plan = plan_of(a);
   const char* e = getenv("PDB_PIPELINE");
-  const bool pipelined = plan.version == 9 && sweeps >= 1 && history_h == nullptr && n > 0 &&
+  const bool pipelined = plan.version == 9 && sweeps >= 1 && history_h == nullptr && n > 0 && !pc.coarse &&
                          !(e && std::string(e) == "0");
   if (!pipelined) {
     Scratch<double> dh(static_cast<size_t>(sweeps + 1), s);

@@ -13,6 +13,7 @@ to import, and on a machine without an sm_100 GPU every compute call raises
 from __future__ import annotations
 
 import ctypes as C
+import json
 import os
 from dataclasses import dataclass
 from typing import Optional
@@ -155,6 +156,8 @@ _sig("pdb_report_final_relative_residual", C.c_double, _P)
 _sig("pdb_report_residual_history_size", C.c_int64, _P)
 _sig("pdb_report_residual_history", C.c_int, _P, _D)
 _sig("pdb_report_free", None, _P)
+_sig("pdb_precond_coarse_size", C.c_int, _P, _I64, _I64, _I64)
+_sig("pdb_precond_coarse_factor", C.c_int, _P, _D, _I64)
 _sig("pdb_run_experiment", C.c_int, C.c_char_p, C.c_char_p)
 _sig("pdb_run_analyze", C.c_int, C.c_char_p, C.c_char_p, C.c_char_p)
 _sig("pdb_run_benchmark", C.c_int, C.c_char_p, C.c_char_p)
@@ -252,8 +255,34 @@ class Matrix(_Handle):
 
 
 class Problem(_Handle):
-    """Host-side generated problem (pdb_problem)."""
+    """Host-side problem (pdb_problem): the reference's uniform-mesh model
+    problem (assemble) or a seeded BASELINE configuration (generate)."""
     _free = _lib.pdb_problem_free
+
+    @classmethod
+    def assemble(cls, config=None, **keys) -> "Problem":
+        """pdb_problem_assemble(config_json): `config` is a JSON string or a
+        dict (keys as the reference's ExperimentConfig: dim, cells, degree,
+        coefficient={kind, value, blocks, values}); keyword arguments are
+        merged into it."""
+        if config is None or isinstance(config, dict):
+            cfg = dict(config or {})
+            cfg.update(keys)
+            config = json.dumps(cfg) if cfg else ""
+        out = C.c_void_p()
+        _check(_lib.pdb_problem_assemble(config.encode(), C.byref(out)))
+        return cls(out)
+
+    def exact_solution(self) -> np.ndarray:
+        u = np.empty(self.ndofs)
+        _check(_lib.pdb_problem_exact_solution(self._ptr, _dp(u)))
+        return u
+
+    def l2_error(self, u) -> float:
+        u = _f64(u)
+        out = C.c_double()
+        _check(_lib.pdb_problem_l2_error(self._ptr, _dp(u), C.byref(out)))
+        return out.value
 
     @classmethod
     def generate(cls, config: int = 1, cells: int = 0, **overrides) -> "Problem":
@@ -295,6 +324,15 @@ class Problem(_Handle):
         out = C.c_void_p()
         _check(_lib.pdb_problem_matrix(self._ptr, C.byref(out)))
         return Matrix(out)
+
+
+def export_matrix(config, path: str) -> None:
+    """pdb_export_matrix: assemble the experiment's model problem (smooth
+    coefficient for experiment 1, piecewise for 2 unless given) and write it
+    as Matrix Market."""
+    if isinstance(config, dict):
+        config = json.dumps(config)
+    _check(_lib.pdb_export_matrix(config.encode(), path.encode()))
 
 
 class PatchSet(_Handle):
@@ -442,6 +480,29 @@ class Preconditioner(_Handle):
         _check(_lib.pdb_precond_create(m.ptr if m is not None else None, ps.ptr, db.ptr if db is not None else None,
                                        omega, threads, C.byref(out)))
         return cls(out, ps.rows)
+
+    @classmethod
+    def create_combo(cls, problem: "Problem", ps: PatchSet, db: Optional[Database] = None, omega: float = 1.0,
+                     threads: int = 1) -> "Preconditioner":
+        """Patch term plus the coarse correction P0 (R0 A P0)^-1 R0
+        (pdb_precond_create_combo; reference ComboPreconditioner)."""
+        out = C.c_void_p()
+        _check(_lib.pdb_precond_create_combo(problem.ptr, ps.ptr, db.ptr if db is not None else None, omega, threads,
+                                             C.byref(out)))
+        return cls(out, ps.rows)
+
+    def coarse_size(self):
+        """(n_c, kl, ku) of the coarse band LU; (0, 0, 0) without one."""
+        v = np.zeros(3, np.int64)
+        _check(_lib.pdb_precond_coarse_size(self._ptr, _ip(v[0:]), _ip(v[1:]), _ip(v[2:])))
+        return tuple(int(x) for x in v)
+
+    def coarse_factor(self):
+        """The device band LU in the reference layout: (ab[(2kl+ku+1), n_c], ipiv)."""
+        nc, kl, ku = self.coarse_size()
+        ab, ipiv = np.empty((2 * kl + ku + 1, nc)), np.empty(nc, np.int64)
+        _check(_lib.pdb_precond_coarse_factor(self._ptr, _dp(ab), _ip(ipiv)))
+        return ab, ipiv
 
     def apply(self, r) -> np.ndarray:
         r = _f64(r)

@@ -145,10 +145,11 @@ def test_no_cpu_fallback(P):
 
 def test_out_of_scope_entry_points_fail_cleanly(P):
     L = P.lib
-    out = C.c_void_p()
-    assert L.pdb_problem_assemble(b"{}", C.byref(out)) == P.PDB_ERR_INTERNAL
-    assert "outside the B200 hot path" in L.pdb_last_error().decode()
+    # the experiment drivers (CSV reproduction of the paper's tables) are out of scope
     assert L.pdb_run_experiment(b"{}", b"/tmp/x.csv") == P.PDB_ERR_INTERNAL
+    assert "outside the B200 hot path" in L.pdb_last_error().decode()
+    assert L.pdb_run_benchmark(b"{}", b"/tmp/x.csv") == P.PDB_ERR_INTERNAL
+    assert L.pdb_run_analyze(b"{}", b"/tmp/x.csv", b"/tmp/y.csv") == P.PDB_ERR_INTERNAL
 
 
 def test_sharded_setup_entry_points_validate_before_device(P):
