@@ -137,6 +137,15 @@ class Scratch {
   }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
+  void upload(const T* h, std::size_t n) {
+    if (n) PDB_CUDA(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+  }
+  void download(T* h, std::size_t n) const {
+    if (n) PDB_CUDA(cudaMemcpyAsync(h, p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));
+  }
+  void zero() {
+    if (n_) PDB_CUDA(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
+  }
 
  private:
   cudaStream_t s_;

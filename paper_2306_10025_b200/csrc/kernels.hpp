@@ -192,5 +192,10 @@ void axpy_val(int64_t n, double a, const double* x, double* y, cudaStream_t s); 
 void div_scalar(int64_t n, const double* x, double sc, double* y, cudaStream_t s);                   // y = x / sc
 void sub(int64_t n, const double* a, const double* b, double* y, cudaStream_t s);                    // y = a - b
 void scalar_div(const double* a, const double* b, double* out, cudaStream_t s);                       // out = a/b (device scalars)
+// Modified Gram-Schmidt step of the Arnoldi process in ONE cooperative launch:
+// for i = 0..j: h[i] = (w, v_i), w -= h[i] v_i; then h[j+1] = (w, w).  The
+// vector stays in registers across the j+2 grid-wide reductions.  Returns
+// false (nothing launched) when n is too large for the register-resident form.
+bool mgs_fused(int64_t n, int j, const double* V, int64_t ldv, double* w, double* h, cudaStream_t s);
 
 }  // namespace pdb::k

@@ -2,6 +2,10 @@
 // PCG).  Reductions use a fixed grid and a fixed two-level tree, so results
 // are run-to-run identical for a given length (not order-identical to the
 // reference's sequential loops; histories agree to ~1e-15 relative).
+#include <algorithm>
+#include <cstdlib>
+
+#include "../common.hpp"
 #include "../kernels.hpp"
 
 namespace pdb::k {
@@ -80,7 +84,133 @@ inline unsigned ew_grid(int64_t n) {
   return (unsigned)(g < 4 * 148 * 8 ? (g > 0 ? g : 1) : 4 * 148 * 8);
 }
 
+// ---------------------------------------------------------------------------
+// Fused MGS (Arnoldi) with a software grid barrier; co-residency of every CTA
+// is guaranteed by the cooperative launch.
+
+constexpr int kMgsThreads = 256;
+constexpr int kMgsMaxBlocks = 1184;  // 8 per SM
+
+struct MgsSync {
+  unsigned count;
+  unsigned gen;
+  double partial[2][kMgsMaxBlocks];
+};
+
+__device__ __forceinline__ void grid_barrier(MgsSync* sy) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &sy->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&sy->count, 1u) == gridDim.x - 1) {
+      sy->count = 0;
+      __threadfence();
+      atomicAdd(&sy->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Block sum in a fixed tree; every thread gets the result.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < kMgsThreads / 32; ++w) t += red[w];
+  return t;
+}
+
+// Grid-wide sum of each CTA's `v` (same fixed order in every CTA).
+__device__ __forceinline__ double grid_sum(double v, MgsSync* sy, int buf, double* red) {
+  const double bs = block_sum(v, red);
+  if (threadIdx.x == 0) sy->partial[buf][blockIdx.x] = bs;
+  grid_barrier(sy);
+  double t = 0.0;
+  for (int b = threadIdx.x; b < gridDim.x; b += kMgsThreads) t += __ldcg(&sy->partial[buf][b]);
+  return block_sum(t, red);
+}
+
+template <int E>
+__global__ void __launch_bounds__(kMgsThreads) mgs_kernel(int64_t n, int j, const double* __restrict__ V, int64_t ldv,
+                                                          double* __restrict__ w, double* __restrict__ h,
+                                                          MgsSync* sy) {
+  __shared__ double red[kMgsThreads / 32];
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kMgsThreads;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kMgsThreads + threadIdx.x;
+  double x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t i = base + e * stride;
+    x[e] = i < n ? w[i] : 0.0;
+  }
+  int buf = 0;
+  for (int i = 0; i <= j; ++i) {
+    const double* v = V + static_cast<int64_t>(i) * ldv;
+    double vv[E];
+    double s = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int64_t q = base + e * stride;
+      vv[e] = q < n ? v[q] : 0.0;
+      s = fma(x[e], vv[e], s);
+    }
+    const double hij = grid_sum(s, sy, buf, red);
+    buf ^= 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = hij;
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = fma(-hij, vv[e], x[e]);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) s = fma(x[e], x[e], s);
+  const double nn = grid_sum(s, sy, buf, red);
+  if (blockIdx.x == 0 && threadIdx.x == 0) h[j + 1] = nn;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int64_t q = base + e * stride;
+    if (q < n) w[q] = x[e];
+  }
+}
+
+template <int E>
+bool launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* h, cudaStream_t s) {
+  static thread_local MgsSync* sy = nullptr;
+  if (!sy) {
+    PDB_CUDA(cudaMalloc(&sy, sizeof(MgsSync)));
+    PDB_CUDA(cudaMemset(sy, 0, sizeof(MgsSync)));
+  }
+  static int per_sm = -1;
+  if (per_sm < 0) PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel<E>, kMgsThreads, 0));
+  const int64_t need = (n + static_cast<int64_t>(kMgsThreads) * E - 1) / (static_cast<int64_t>(kMgsThreads) * E);
+  const int64_t cap = std::min<int64_t>(kMgsMaxBlocks, static_cast<int64_t>(per_sm) * num_sms());
+  if (need > cap) return false;
+  // small vectors: fewer CTAs make the barriers cheaper
+  const int grid = static_cast<int>(std::max<int64_t>(1, need));
+  void* args[] = {&n, &j, &V, &ldv, &w, &h, &sy};
+  PDB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mgs_kernel<E>), dim3(grid), dim3(kMgsThreads), args, 0, s));
+  return true;
+}
+
 }  // namespace
+
+bool mgs_fused(int64_t n, int j, const double* V, int64_t ldv, double* w, double* h, cudaStream_t s) {
+  const char* e = getenv("PDB_MGS");
+  if (e && e[0] == '0') return false;
+  const int64_t per = static_cast<int64_t>(kMgsThreads) * 4 * 148;  // elements at 4 CTAs/SM... per E
+  if (n <= per * 1 / 4) return launch_mgs<1>(n, j, V, ldv, w, h, s);
+  if (n <= per * 2 / 4) return launch_mgs<2>(n, j, V, ldv, w, h, s);
+  if (n <= per) return launch_mgs<4>(n, j, V, ldv, w, h, s);
+  if (n <= per * 2) return launch_mgs<8>(n, j, V, ldv, w, h, s);
+  return launch_mgs<16>(n, j, V, ldv, w, h, s);
+}
 
 int dot_partials() { return kDotBlocks; }
 

@@ -8,7 +8,11 @@
 //          true residual at the end of each cycle).
 //   pcg:   preconditioned CG (absent from the reference), the
 //          same recurrence as oracle/pdb_oracle.c orc_pcg.
-// Dots use the deterministic fixed-tree reduction of kernels/blas.cu.
+// Dots use the deterministic fixed-tree reduction of kernels/blas.cu.  The
+// GMRES Gram-Schmidt sweep is one cooperative kernel per Arnoldi step
+// (k::mgs_fused: the new vector stays in registers across the j + 2
+// grid-wide reductions) instead of 3 (j + 1) + 2 launches; work vectors come
+// from the stream-ordered pool, so a solve does no device-wide allocation.
 #include <cfloat>
 #include <cmath>
 
@@ -58,9 +62,10 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
   if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
   Ops ops(a, pc, s, static_cast<size_t>(o.restart) + 2);
   const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
-  DevBuf<double> b(un), x(un), r0(un), tmp(un), corr(un);
-  b.upload(b_host, static_cast<size_t>(n), s);
-  x.zero(s);
+  // pool (stream-ordered) allocations: no device-wide synchronisation per solve
+  Scratch<double> b(un, s), x(un, s), r0(un, s), tmp(un, s), corr(un, s);
+  b.upload(b_host, static_cast<size_t>(n));
+  x.zero();
   rep = pdb_report_s();
   const double bnorm = ops.norm(b.get());
   if (bnorm == 0.0) {
@@ -87,7 +92,7 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
     return ops.norm(corr.get()) / bnorm;
   };
   const size_t m = static_cast<size_t>(o.restart);
-  DevBuf<double> V((m + 1) * un);
+  Scratch<double> V((m + 1) * un, s);
   auto Vp = [&](size_t i) { return V.get() + i * un; };
   std::vector<std::vector<double>> h(m + 1, std::vector<double>(m, 0.0));
   std::vector<double> cs(m, 0.0), sn(m, 0.0), g(m + 1, 0.0), y(m, 0.0);
@@ -117,11 +122,16 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
     bool breakdown = false;
     for (size_t j = 0; j < m; ++j) {
       apply_op(Vp(j), Vp(j + 1));
-      for (size_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt: h_ij in device slot i feeds the axpy
-        double* hij = ops.dot_dev(Vp(j + 1), Vp(i), static_cast<int>(i));
-        k::axpy(n, hij, true, Vp(i), Vp(j + 1), s);
+      // modified Gram-Schmidt: one cooperative kernel (vector in registers,
+      // j + 2 grid-wide reductions), else per-i dot + axpy launches with h_ij
+      // in device slot i feeding the axpy
+      if (!k::mgs_fused(n, static_cast<int>(j), V.get(), static_cast<int64_t>(un), Vp(j + 1), ops.scal.get(), s)) {
+        for (size_t i = 0; i <= j; ++i) {
+          double* hij = ops.dot_dev(Vp(j + 1), Vp(i), static_cast<int>(i));
+          k::axpy(n, hij, true, Vp(i), Vp(j + 1), s);
+        }
+        ops.dot_dev(Vp(j + 1), Vp(j + 1), static_cast<int>(j + 1));
       }
-      ops.dot_dev(Vp(j + 1), Vp(j + 1), static_cast<int>(j + 1));
       std::vector<double> hv(j + 2);
       PDB_CUDA(cudaMemcpyAsync(hv.data(), ops.scal.get(), (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, s));
       sync(s);  // the iteration's only host synchronisation
@@ -157,7 +167,7 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
       for (size_t kk = i + 1; kk < steps; ++kk) sacc -= h[i][kk] * y[kk];
       y[i] = sacc / h[i][i];
     }
-    tmp.zero(s);
+    tmp.zero();
     for (size_t i = 0; i < steps; ++i) k::axpy_val(n, y[i], Vp(i), tmp.get(), s);
     if (pc && !left) {
       ops.apply(tmp.get(), corr.get());
@@ -175,7 +185,7 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
     first_cycle = false;
   }
   rep.final_relative_residual = true_relres();
-  x.download(x_host, static_cast<size_t>(n), s);
+  x.download(x_host, static_cast<size_t>(n));
   sync(s);
 }
 
@@ -186,9 +196,9 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
   if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
   Ops ops(a, pc, s);
   const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
-  DevBuf<double> b(un), x(un), r(un), z(un), p(un), q(un);
-  b.upload(b_host, static_cast<size_t>(n), s);
-  x.zero(s);
+  Scratch<double> b(un, s), x(un, s), r(un, s), z(un, s), p(un, s), q(un, s);
+  b.upload(b_host, static_cast<size_t>(n));
+  x.zero();
   PDB_CUDA(cudaMemcpyAsync(r.get(), b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   rep = pdb_report_s();
   const double bnorm = ops.norm(b.get());
@@ -231,7 +241,7 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
     }
   }
   rep.final_relative_residual = rep.residual_history.empty() ? 0.0 : rep.residual_history.back();
-  x.download(x_host, static_cast<size_t>(n), s);
+  x.download(x_host, static_cast<size_t>(n));
   sync(s);
 }
 

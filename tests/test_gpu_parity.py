@@ -332,3 +332,23 @@ def test_spmv_ragged_rows(P, orc, monkeypatch, seed, n):
     for ver in ("5", "2"):
         monkeypatch.setenv("PDB_SPMV_VERSION", ver)
         np.testing.assert_allclose(A.spmv(x), want, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("cells", [60, 120, 180, 250, 512])
+def test_gmres_fused_mgs_matches_per_vector_launches(P, cells, monkeypatch):
+    """The cooperative MGS kernel (vector in registers, one launch per Arnoldi
+    step; E = 1..16 elements per thread across these sizes) against the
+    per-i dot + axpy launches: same iteration count; the dot products sum in
+    another order, so histories agree to rounding (1e-7 relative after 40
+    restarted iterations, as against the reference)."""
+    p = P.Problem.assemble(dict(cells=cells, degree=2))
+    A = p.matrix()
+    ps = P.PatchSet.detect(A, 9)
+    pc = P.Preconditioner.create(A, ps)
+    b = p.rhs()
+    x1, r1 = P.gmres(A, b, pc, restart=12, tol=1e-10, max_iters=40)
+    monkeypatch.setenv("PDB_MGS", "0")
+    x0, r0 = P.gmres(A, b, pc, restart=12, tol=1e-10, max_iters=40)
+    assert r1.iterations == r0.iterations
+    np.testing.assert_allclose(r1.residual_history, r0.residual_history, rtol=1e-7)
+    np.testing.assert_allclose(x1, x0, rtol=0, atol=1e-8 * np.abs(x0).max())
