@@ -4,22 +4,24 @@
 //
 //   z += P0 (R0 A P0)^{-1} R0 r
 //
-// Setup factors R0 A P0 once on the device with one CTA per factorization:
-// the LAPACK-style partial-pivoting band LU runs column by column (pivot =
+// Setup factors R0 A P0 once on the device on a cooperative grid (one
+// barrier per column): the LAPACK-style partial-pivoting band LU (pivot =
 // first maximum |.|, full row swap inside the band, multipliers by true
 // division, a -= m*b updates unfused), so band, pivots and multipliers are
 // bitwise the reference's.  Each apply is three launches:
 //   restrict   rc = R0 r, one thread per coarse vertex summing its fine DoFs
 //              in ascending order from 0.0 (= the reference's scatter order,
 //              fem.cpp:373-382), bitwise;
-//   band solve one warp walks the n_c columns: the forward sweep (swap, then
-//              out[j+t] -= l_tj x_j, skipped when x_j == 0) is the
-//              reference's order exactly; the backward sweep is column
-//              oriented (x_i = out_i * (1/u_ii), then out[i-d] -= u x_i),
-//              which reorders the reference's row sums (parity 1e-12
-//              relative, tests/test_combo.py).  The band columns of the next
-//              D steps are loaded into registers while the current ones are
-//              applied, so the sweep runs at shared-memory latency;
+//   solve      one of three coarse solvers (PDB_COARSE=dense|blocked|band):
+//              dense    n_c <= 16384: the explicit inverse (its columns are
+//                       the reference's solves of unit vectors, bitwise),
+//                       one HBM-bound matrix-vector product per apply;
+//              blocked  larger n_c: 2 n_c / Bk dense block maps, one
+//                       cooperative kernel with a grid barrier per block;
+//              band     one warp walks the 2 n_c steps (forward in the
+//                       reference's order, backward column oriented);
+//              the product / reordered sums give parity 1e-12 relative
+//              (tests/test_combo.py), not bitwise;
 //   prolong    z_i += sum_q p0_iq xc_q (<= 4 terms, in order), bitwise.
 #include <algorithm>
 #include <cstdlib>
@@ -32,15 +34,46 @@ namespace pdb {
 namespace {
 
 // ---------------------------------------------------------------------------
-// Band LU, one CTA.  B is column-major band storage: B[j*ldab + r] holds the
-// reference's ab[r*n + j] (band row r of column j).
+// Band LU on a cooperative grid.  B is column-major band storage:
+// B[j*ldab + r] holds the reference's ab[r*n + j] (band row r of column j).
+// Step j: every CTA reads column j and finds the pivot itself (first maximum
+// of |a(j+t, j)| -- the same deterministic (value, index) reduction in every
+// CTA, so no broadcast is needed), applies the swap to its copy and forms the
+// multipliers by true division; CTA 0 writes column j back.  Columns
+// j+1..j+kv are dealt round-robin to the CTAs, each swapping rows j and p in
+// its columns and applying a -= m*b (unfused) in ascending t.  One grid
+// barrier per column.  Every element sees the reference's operations in the
+// reference's order, so band and pivots are bitwise banded.cpp:11-60's.
 
-constexpr int kFactorThreads = 1024;
+constexpr int kFactorThreads = 512;
+
+struct FactorSync {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void factor_barrier(FactorSync* sy) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &sy->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&sy->count, 1u) == gridDim.x - 1) {
+      sy->count = 0;
+      __threadfence();
+      atomicAdd(&sy->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 __global__ void __launch_bounds__(kFactorThreads) band_factor_kernel(int n, int kl, int ku, int ldab, double* B,
-                                                                     int32_t* ipiv, double* rdiag, int* bad_col) {
-  extern __shared__ double smem[];
-  double* mult = smem;  // kl multipliers of the current column
+                                                                     int32_t* ipiv, double* rdiag, int* bad_col,
+                                                                     FactorSync* sy) {
+  extern __shared__ double mult[];  // column j after the swap: [0] pivot, [t] multiplier t
   __shared__ double red_v[kFactorThreads / 32];
   __shared__ int red_t[kFactorThreads / 32];
   __shared__ double s_best;
@@ -50,13 +83,14 @@ __global__ void __launch_bounds__(kFactorThreads) band_factor_kernel(int n, int 
   for (int j = 0; j < n; ++j) {
     const int km = min(kl, n - 1 - j);
     double* col = B + static_cast<int64_t>(j) * ldab;
-    // pivot: first maximum of |a(j+t, j)|, t = 0..km (strict > in ascending t)
     double bv = -1.0;
     int bt = 0;
     for (int t = tid; t <= km; t += kFactorThreads) {
-      const double v = fabs(col[kv + t]);
-      if (v > bv) {
-        bv = v;
+      const double v = __ldcg(col + kv + t);
+      mult[t] = v;
+      const double a = fabs(v);
+      if (a > bv) {
+        bv = a;
         bt = t;
       }
     }
@@ -84,43 +118,53 @@ __global__ void __launch_bounds__(kFactorThreads) band_factor_kernel(int n, int 
         }
       s_best = v;
       s_jp = t;
-      if (v == 0.0) *bad_col = j;
-    }
-    __syncthreads();
-    if (s_best == 0.0) return;
-    const int jp = s_jp;
-    const int jend = min(j + kv, n - 1);
-    if (jp != 0)
-      for (int jj = j + tid; jj <= jend; jj += kFactorThreads) {
-        double* c = B + static_cast<int64_t>(jj) * ldab;
-        const double a = c[kv + j - jj], b = c[kv + j + jp - jj];
-        c[kv + j - jj] = b;
-        c[kv + j + jp - jj] = a;
+      if (t != 0) {
+        const double a = mult[0];
+        mult[0] = mult[t];
+        mult[t] = a;
       }
-    __syncthreads();
-    const double piv = col[kv];
-    for (int t = 1 + tid; t <= km; t += kFactorThreads) {
-      const double m = __ddiv_rn(col[kv + t], piv);
-      col[kv + t] = m;
-      mult[t] = m;
+      if (v == 0.0 && blockIdx.x == 0) *bad_col = j;
     }
-    if (tid == 0) {
+    __syncthreads();
+    if (s_best == 0.0) return;  // every CTA sees the same column: all stop here
+    const int jp = s_jp;
+    const double piv = mult[0];
+    __syncthreads();
+    for (int t = 1 + tid; t <= km; t += kFactorThreads) mult[t] = __ddiv_rn(mult[t], piv);
+    __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) {
       ipiv[j] = j + jp;
       rdiag[j] = __ddiv_rn(1.0, piv);
     }
-    __syncthreads();
-    // a(j+t, jj) -= m_t * a(j, jj) for t = 1..km, jj = j+1..jend
-    if (km > 0) {
-      const int total = km * (jend - j);
-      for (int idx = tid; idx < total; idx += kFactorThreads) {
-        const int t = 1 + idx % km, jj = j + 1 + idx / km;
+    // columns j+1..jend, round-robin over the CTAs: swap rows j, j+jp, then
+    // a(j+t, jj) -= m_t a(j, jj)
+    const int jend = min(j + kv, n - 1);
+    for (int jj = j + 1 + static_cast<int>(blockIdx.x); jj <= jend; jj += gridDim.x) {
+      double* c = B + static_cast<int64_t>(jj) * ldab;
+      const int r0 = kv + j - jj;  // band row of matrix row j in column jj
+      double u = __ldcg(c + r0);
+      if (jp != 0) {
+        const double w = __ldcg(c + r0 + jp);
+        __syncthreads();  // every thread has read u and w before they are overwritten
+        if (tid == 0) {
+          c[r0] = w;
+          c[r0 + jp] = u;
+        }
+        u = w;
+        __syncthreads();
+      }
+      for (int t = 1 + tid; t <= km; t += kFactorThreads) {
         const double m = mult[t];
         if (m == 0.0) continue;
-        double* c = B + static_cast<int64_t>(jj) * ldab;
-        c[kv + t + j - jj] = __dsub_rn(c[kv + t + j - jj], __dmul_rn(m, c[kv + j - jj]));
+        c[r0 + t] = __dsub_rn(__ldcg(c + r0 + t), __dmul_rn(m, u));
       }
     }
-    __syncthreads();
+    factor_barrier(sy);
+    // column j is written back only now: every CTA has finished reading it
+    if (blockIdx.x == 0) {
+      for (int t = tid; t <= km; t += kFactorThreads) col[kv + t] = mult[t];
+      __syncthreads();
+    }
   }
 }
 
@@ -371,6 +415,152 @@ __global__ void __launch_bounds__(kGemvWarps * 32) dense_apply_kernel(int nc, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked solve (n_c > kDenseMax): the 2 n_c dependent steps become
+// 2 n_c / Bk dense matrix-vector products over all SMs.
+//   forward  block k (steps J..J+Bk-1 of the pivoted elimination) touches
+//            only rows [J, J+Bk+kl): it is the dense map F_k of that segment
+//            (the Bk swaps and rank-1 updates applied to the identity);
+//   backward x_J = U_JJ^{-1} (y_J - U_JR x_R), R = the next kv rows:
+//            G_k = [U_JJ^{-1} | -U_JJ^{-1} U_JR].
+// Setup builds every F_k / G_k column in parallel (one thread per column,
+// the band factor's own steps); each apply is one cooperative kernel with a
+// grid barrier per block.  Rows [J, J+Bk) leave a forward block final; the
+// kl rows after them are carried (ping-pong) into the next block.
+
+__global__ void fwd_block_kernel(int n, int kl, int ku, int ldab, int bk, int nblk, const double* __restrict__ B,
+                                 const int32_t* __restrict__ ipiv, const int64_t* __restrict__ off,
+                                 double* __restrict__ F) {
+  const int k = blockIdx.y;
+  const int J = k * bk;
+  const int bj = min(bk, n - J), m = min(n, J + bk + kl) - J;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nblk || c >= m) return;
+  const int kv = kl + ku;
+  double* col = F + off[k] + c;  // element (r, c) at col[r * m]
+  for (int r = 0; r < m; ++r) col[static_cast<int64_t>(r) * m] = r == c ? 1.0 : 0.0;
+  for (int j = J; j < J + bj; ++j) {
+    const int lj = j - J, lp = ipiv[j] - J;
+    if (lp != lj) {
+      const double a = col[static_cast<int64_t>(lj) * m];
+      col[static_cast<int64_t>(lj) * m] = col[static_cast<int64_t>(lp) * m];
+      col[static_cast<int64_t>(lp) * m] = a;
+    }
+    const double xj = col[static_cast<int64_t>(lj) * m];
+    if (xj == 0.0) continue;
+    const int km = min(kl, n - 1 - j);
+    const double* l = B + static_cast<int64_t>(j) * ldab + kv;
+    for (int t = 1; t <= km; ++t) {
+      double& y = col[static_cast<int64_t>(lj + t) * m];
+      y = __dsub_rn(y, __dmul_rn(l[t], xj));
+    }
+  }
+}
+
+__global__ void bwd_block_kernel(int n, int kl, int ku, int ldab, int bk, int nblk, const double* __restrict__ B,
+                                 const int64_t* __restrict__ off, double* __restrict__ G) {
+  const int k = blockIdx.y;
+  const int J = k * bk;
+  const int bj = min(bk, n - J), nr = min(kl + ku, n - J - bj), w = bj + nr;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nblk || c >= w) return;
+  const int kv = kl + ku;
+  auto U = [&](int i, int col) -> double {  // U(i, col) of the band factor, 0 outside the band
+    return (col >= i && col - i <= kv) ? B[static_cast<int64_t>(col) * ldab + kv + i - col] : 0.0;
+  };
+  double* z = G + off[k] + c;  // element (r, c) at z[r * w]
+  for (int r = 0; r < bj; ++r) z[static_cast<int64_t>(r) * w] = c < bj ? (r == c ? 1.0 : 0.0) : U(J + r, J + c);
+  for (int i = bj - 1; i >= 0; --i) {
+    double sum = z[static_cast<int64_t>(i) * w];
+    const int kend = min(bj - 1, i + kv);
+    for (int q = i + 1; q <= kend; ++q) sum = __dsub_rn(sum, __dmul_rn(U(J + i, J + q), z[static_cast<int64_t>(q) * w]));
+    z[static_cast<int64_t>(i) * w] = __ddiv_rn(sum, U(J + i, J + i));
+  }
+  if (c >= bj)
+    for (int r = 0; r < bj; ++r) z[static_cast<int64_t>(r) * w] = -z[static_cast<int64_t>(r) * w];
+}
+
+struct BlockSync {
+  unsigned count;
+  unsigned gen;
+};
+
+__device__ __forceinline__ void coarse_grid_barrier(BlockSync* sy) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = &sy->gen;
+    const unsigned g = *vgen;
+    __threadfence();
+    if (atomicAdd(&sy->count, 1u) == gridDim.x - 1) {
+      sy->count = 0;
+      __threadfence();
+      atomicAdd(&sy->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kBlkThreads = 256;
+
+// Row r of a dense (rows x w) block times the staged vector v (shared).
+__device__ __forceinline__ double row_dot(const double* __restrict__ row, int w, const double* v, int lane) {
+  double s0 = 0.0, s1 = 0.0;
+  int c = lane;
+  for (; c + 32 < w; c += 64) {
+    s0 = fma(__ldcs(row + c), v[c], s0);
+    s1 = fma(__ldcs(row + c + 32), v[c + 32], s1);
+  }
+  if (c < w) s0 = fma(__ldcs(row + c), v[c], s0);
+  double sum = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  return sum;
+}
+
+__global__ void __launch_bounds__(kBlkThreads) blocked_solve_kernel(int n, int kl, int kv, int bk, int nblk,
+                                                                    const int64_t* __restrict__ foff,
+                                                                    const int64_t* __restrict__ goff,
+                                                                    const double* __restrict__ F,
+                                                                    const double* __restrict__ G,
+                                                                    const double* __restrict__ rhs, double* yf,
+                                                                    double* carry, double* x, BlockSync* sy) {
+  extern __shared__ double sv[];
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (kBlkThreads / 32) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (kBlkThreads / 32);
+  for (int k = 0; k < nblk; ++k) {
+    const int J = k * bk, bj = min(bk, n - J), m = min(n, J + bk + kl) - J;
+    const int cin = k == 0 ? 0 : min(kl, m);
+    const double* cur = carry + (k & 1) * kl;
+    double* nxt = carry + ((k + 1) & 1) * kl;
+    for (int i = threadIdx.x; i < m; i += kBlkThreads) sv[i] = i < cin ? __ldcg(cur + i) : rhs[J + i];
+    __syncthreads();
+    const double* Fk = F + foff[k];
+    for (int r = gw; r < m; r += nw) {
+      const double v = row_dot(Fk + static_cast<int64_t>(r) * m, m, sv, lane);
+      if (lane == 0) {
+        if (r < bj) yf[J + r] = v;
+        else nxt[r - bj] = v;
+      }
+    }
+    coarse_grid_barrier(sy);
+  }
+  for (int k = nblk - 1; k >= 0; --k) {
+    const int J = k * bk, bj = min(bk, n - J), nr = min(kv, n - J - bj), w = bj + nr;
+    for (int i = threadIdx.x; i < w; i += kBlkThreads) sv[i] = i < bj ? __ldcg(yf + J + i) : __ldcg(x + J + i);
+    __syncthreads();
+    const double* Gk = G + goff[k];
+    for (int r = gw; r < bj; r += nw) {
+      const double v = row_dot(Gk + static_cast<int64_t>(r) * w, w, sv, lane);
+      if (lane == 0) x[J + r] = v;
+    }
+    coarse_grid_barrier(sy);
+  }
+}
+
 constexpr size_t kSolveSmem = 200 * 1024;
 
 template <int R, int D>
@@ -430,10 +620,26 @@ void coarse_setup(const CoarseSpaceHost& cs, CoarseDev& out, cudaStream_t s) {
   require(smem <= 200 * 1024, Errc::invalid_argument, "coarse band too wide");
   if (smem > 48 * 1024)
     PDB_CUDA(cudaFuncSetAttribute(band_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  band_factor_kernel<<<1, kFactorThreads, smem, s>>>(static_cast<int>(n), static_cast<int>(kl), static_cast<int>(ku),
-                                                    static_cast<int>(ldab), out.band.get(), out.ipiv.get(),
-                                                    out.rdiag.get(), bad.get());
-  PDB_LAUNCH_CHECK();
+  {
+    Scratch<FactorSync> fsync(1, s);
+    PDB_CUDA(cudaMemsetAsync(fsync.get(), 0, sizeof(FactorSync), s));
+    int per_sm = 0;
+    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, band_factor_kernel, kFactorThreads, smem));
+    // about 4 trailing columns per CTA per step, at most one CTA per SM
+    const int grid = static_cast<int>(std::max<Index>(1, std::min<Index>((kv + 3) / 4, static_cast<Index>(num_sms()) *
+                                                                                       std::max(per_sm, 1))));
+    int n_ = static_cast<int>(n), kl_ = static_cast<int>(kl), ku_ = static_cast<int>(ku), ld_ = static_cast<int>(ldab);
+    double* bp = out.band.get();
+    int32_t* ip = out.ipiv.get();
+    double* rd = out.rdiag.get();
+    int* bc = bad.get();
+    FactorSync* fs = fsync.get();
+    void* args[] = {&n_, &kl_, &ku_, &ld_, &bp, &ip, &rd, &bc, &fs};
+    PDB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(band_factor_kernel), dim3(grid),
+                                         dim3(kFactorThreads), args, smem, s));
+    PDB_LAUNCH_CHECK();
+    sync(s);
+  }
   upload_op(cs.p0, out.p0_ptr, out.p0_col, out.p0_val, s);
   upload_op(cs.r0, out.r0_ptr, out.r0_col, out.r0_val, s);
   int bad_h = -1;
@@ -457,7 +663,41 @@ void coarse_setup(const CoarseSpaceHost& cs, CoarseDev& out, cudaStream_t s) {
     PDB_LAUNCH_CHECK();
     sync(s);
     out.ld = ld;
+    return;
   }
+  const bool blocked = e ? std::string(e) == "blocked" : true;
+  if (!blocked) return;
+  // blocked solve: Bk = 2 kl steps per block (>= 32)
+  const Index bk = std::max<Index>(32, 2 * kl);
+  const Index nblk = (n + bk - 1) / bk;
+  std::vector<int64_t> foff(static_cast<size_t>(nblk)), goff(static_cast<size_t>(nblk));
+  int64_t fo = 0, go = 0;
+  Index fmax = 0, gmax = 0;
+  for (Index k = 0; k < nblk; ++k) {
+    const Index J = k * bk, bj = std::min(bk, n - J), m = std::min(n, J + bk + kl) - J;
+    const Index w = bj + std::min(kv, n - J - bj);
+    foff[static_cast<size_t>(k)] = fo;
+    goff[static_cast<size_t>(k)] = go;
+    fo += m * m;
+    go += bj * w;
+    fmax = std::max(fmax, m);
+    gmax = std::max(gmax, w);
+  }
+  out.bk = bk;
+  out.nblk = nblk;
+  out.vmax = std::max(fmax, gmax);
+  upload_vec(out.foff, foff, s);
+  upload_vec(out.goff, goff, s);
+  out.fblk.alloc(static_cast<size_t>(fo));
+  out.gblk.alloc(static_cast<size_t>(go));
+  fwd_block_kernel<<<dim3(static_cast<unsigned>((fmax + 127) / 128), static_cast<unsigned>(nblk)), 128, 0, s>>>(
+      static_cast<int>(n), static_cast<int>(kl), static_cast<int>(ku), static_cast<int>(ldab), static_cast<int>(bk),
+      static_cast<int>(nblk), out.band.get(), out.ipiv.get(), out.foff.get(), out.fblk.get());
+  bwd_block_kernel<<<dim3(static_cast<unsigned>((gmax + 127) / 128), static_cast<unsigned>(nblk)), 128, 0, s>>>(
+      static_cast<int>(n), static_cast<int>(kl), static_cast<int>(ku), static_cast<int>(ldab), static_cast<int>(bk),
+      static_cast<int>(nblk), out.band.get(), out.goff.get(), out.gblk.get());
+  PDB_LAUNCH_CHECK();
+  sync(s);
 }
 
 void coarse_correct(const CoarseDev& c, const double* r, double* z, cudaStream_t s) {
@@ -476,6 +716,36 @@ void coarse_correct(const CoarseDev& c, const double* r, double* z, cudaStream_t
     const unsigned grid = static_cast<unsigned>(std::min<Index>((c.nc + rows_per - 1) / rows_per, 148 * 2));
     dense_apply_kernel<<<grid, kGemvWarps * 32, smem, s>>>(static_cast<int>(c.nc), static_cast<int>(c.ld), c.inv.get(),
                                                           rc.get(), xc.get());
+    prolong_add_kernel<<<static_cast<unsigned>((c.fine_n + 255) / 256), 256, 0, s>>>(
+        c.fine_n, c.p0_ptr.get(), c.p0_col.get(), c.p0_val.get(), xc.get(), z);
+    PDB_LAUNCH_CHECK();
+    return;
+  }
+  if (c.nblk > 0) {
+    const size_t smem = static_cast<size_t>(c.vmax) * sizeof(double);
+    require(smem <= kSolveSmem, Errc::invalid_argument, "coarse band too wide for the blocked solve");
+    if (smem > 48 * 1024)
+      PDB_CUDA(cudaFuncSetAttribute(blocked_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    Scratch<BlockSync> bsync(1, s);  // per call: concurrent applies on one handle stay independent
+    PDB_CUDA(cudaMemsetAsync(bsync.get(), 0, sizeof(BlockSync), s));
+    BlockSync* sy = bsync.get();
+    int per_sm = 0;
+    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blocked_solve_kernel, kBlkThreads, smem));
+    const int grid = std::max(1, std::min(per_sm, 2) * num_sms());
+    Scratch<double> yf(nc, s), carry(static_cast<size_t>(2 * std::max<Index>(c.kl, 1)), s);
+    int n_ = static_cast<int>(c.nc), kl_ = static_cast<int>(c.kl), kv_ = static_cast<int>(c.kl + c.ku),
+        bk_ = static_cast<int>(c.bk), nb_ = static_cast<int>(c.nblk);
+    const int64_t* fo = c.foff.get();
+    const int64_t* go = c.goff.get();
+    const double* F = c.fblk.get();
+    const double* G = c.gblk.get();
+    const double* rhs = rc.get();
+    double* yfp = yf.get();
+    double* cp = carry.get();
+    double* xp = xc.get();
+    void* args[] = {&n_, &kl_, &kv_, &bk_, &nb_, &fo, &go, &F, &G, &rhs, &yfp, &cp, &xp, &sy};
+    PDB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(blocked_solve_kernel), dim3(grid), dim3(kBlkThreads),
+                                         args, smem, s));
     prolong_add_kernel<<<static_cast<unsigned>((c.fine_n + 255) / 256), 256, 0, s>>>(
         c.fine_n, c.p0_ptr.get(), c.p0_col.get(), c.p0_val.get(), xc.get(), z);
     PDB_LAUNCH_CHECK();

@@ -58,6 +58,11 @@ struct CoarseDev {
   DevBuf<double> rdiag;  // 1 / U(j, j)
   DevBuf<double> inv;    // dense (R0 A P0)^{-1}, row-major [nc][ld], when ld > 0
   Index ld = 0;
+  // blocked solve (nblk > 0): forward maps F_k [m_k][m_k] and backward maps
+  // G_k [bk_k][bk_k + nr_k], row-major, concatenated at foff / goff
+  Index bk = 0, nblk = 0, vmax = 0;
+  DevBuf<int64_t> foff, goff;
+  DevBuf<double> fblk, gblk;
 };
 
 struct BuildWork {

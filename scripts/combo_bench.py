@@ -35,7 +35,7 @@ def dev_time(fn, reps=50):
 
 def main():
     ref = O.RefLib() if O.have_ref() else None
-    cases = [(60, 2), (60, 3), (120, 2), (250, 2)]
+    cases = [(60, 2), (60, 3), (120, 2), (250, 2), (256, 4)]
     if len(sys.argv) > 1:
         cases = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]]
     for cells, deg in cases:
@@ -51,9 +51,11 @@ def main():
         ms_plain = dev_time(lambda: plain.apply_device(r.data_ptr(), z.data_ptr(), s))
         b = p.rhs()
         row = dict(cells=cells, degree=deg, n=n, apply_plain_us=round(1e3 * ms_plain, 2))
-        for path in ("dense", "band"):
+        for path in ("dense", "blocked", "band"):
             nc = (cells + 1) ** 2
             if path == "dense" and nc > 16384:
+                continue
+            if path == "band" and nc > 20000:
                 continue
             os.environ["PDB_COARSE"] = path
             t = time.time()

@@ -1,2 +1,2 @@
-timeout 2400 python -m pytest tests/ -q -m gpu -x --durations=15 > gpurun_out/t_all.log 2>&1; echo "exit $?" >> gpurun_out/t_all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "exit $?" >> gpurun_out/smoke.log
+timeout 900 python -m pytest tests/test_combo.py -q -m gpu -x > gpurun_out/t_combo.log 2>&1; echo "exit $?" >> gpurun_out/t_combo.log
+timeout 900 python scripts/combo_bench.py > gpurun_out/combo_bench.log 2>&1; echo "exit $?" >> gpurun_out/combo_bench.log

@@ -24,10 +24,10 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["dense", "band"])
+@pytest.fixture(params=["dense", "blocked", "band"])
 def coarse_path(request, monkeypatch):
-    """Both device coarse solvers: the dense inverse (default for n_c <= 16384)
-    and the one-warp band sweep (larger coarse spaces)."""
+    """The device coarse solvers: the dense inverse (default for n_c <= 16384),
+    the blocked solve (default above) and the one-warp band sweep."""
     monkeypatch.setenv("PDB_COARSE", request.param)
     return request.param
 
