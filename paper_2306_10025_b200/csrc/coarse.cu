@@ -561,6 +561,78 @@ __global__ void __launch_bounds__(kBlkThreads) blocked_solve_kernel(int n, int k
   }
 }
 
+// Same solve with the next block's matrix row prefetched into registers
+// before each grid barrier (the HBM latency of the 2-5 MB block hides behind
+// the barrier); one row per warp, so it needs rows <= warps and width <= 32 R.
+template <int R>
+__global__ void __launch_bounds__(kBlkThreads) blocked_solve_pf_kernel(int n, int kl, int kv, int bk, int nblk,
+                                                                       const int64_t* __restrict__ foff,
+                                                                       const int64_t* __restrict__ goff,
+                                                                       const double* __restrict__ F,
+                                                                       const double* __restrict__ G,
+                                                                       const double* __restrict__ rhs, double* yf,
+                                                                       double* carry, double* x, BlockSync* sy) {
+  extern __shared__ double sv[];  // 32 R entries, zero past the block width
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (kBlkThreads / 32) + (threadIdx.x >> 5);
+  const int nsteps = 2 * nblk;
+  double fr[R];
+  auto prefetch = [&](int st) {
+    const bool fwd = st < nblk;
+    const int k = fwd ? st : nsteps - 1 - st;
+    const int J = k * bk, bj = min(bk, n - J);
+    const int width = fwd ? min(n, J + bk + kl) - J : bj + min(kv, n - J - bj);
+    const int rows = fwd ? width : bj;
+    const double* row = (fwd ? F + foff[k] : G + goff[k]) + static_cast<int64_t>(gw) * width;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int c = lane + 32 * i;
+      fr[i] = (gw < rows && c < width) ? __ldcs(row + c) : 0.0;
+    }
+  };
+  prefetch(0);
+  for (int st = 0; st < nsteps; ++st) {
+    const bool fwd = st < nblk;
+    const int k = fwd ? st : nsteps - 1 - st;
+    const int J = k * bk, bj = min(bk, n - J);
+    int width, rows;
+    if (fwd) {
+      width = min(n, J + bk + kl) - J;
+      rows = width;
+      const int cin = k == 0 ? 0 : min(kl, width);
+      const double* cur = carry + (k & 1) * kl;
+      for (int i = threadIdx.x; i < 32 * R; i += kBlkThreads)
+        sv[i] = i < cin ? __ldcg(cur + i) : (i < width ? rhs[J + i] : 0.0);
+    } else {
+      width = bj + min(kv, n - J - bj);
+      rows = bj;
+      for (int i = threadIdx.x; i < 32 * R; i += kBlkThreads)
+        sv[i] = i < bj ? __ldcg(yf + J + i) : (i < width ? __ldcg(x + J + i) : 0.0);
+    }
+    __syncthreads();
+    if (gw < rows) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < R; i += 4) {
+        a0 = fma(fr[i], sv[lane + 32 * i], a0);
+        if (i + 1 < R) a1 = fma(fr[i + 1], sv[lane + 32 * (i + 1)], a1);
+        if (i + 2 < R) a2 = fma(fr[i + 2], sv[lane + 32 * (i + 2)], a2);
+        if (i + 3 < R) a3 = fma(fr[i + 3], sv[lane + 32 * (i + 3)], a3);
+      }
+      double v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        if (!fwd) x[J + gw] = v;
+        else if (gw < bj) yf[J + gw] = v;
+        else carry[((k + 1) & 1) * kl + gw - bj] = v;
+      }
+    }
+    if (st + 1 < nsteps) prefetch(st + 1);
+    coarse_grid_barrier(sy);
+  }
+}
+
 constexpr size_t kSolveSmem = 200 * 1024;
 
 template <int R, int D>
@@ -667,8 +739,11 @@ void coarse_setup(const CoarseSpaceHost& cs, CoarseDev& out, cudaStream_t s) {
   }
   const bool blocked = e ? std::string(e) == "blocked" : true;
   if (!blocked) return;
-  // blocked solve: Bk = 2 kl steps per block (>= 32)
-  const Index bk = std::max<Index>(32, 2 * kl);
+  // blocked solve: Bk = 2 kl steps per block (>= 32), trimmed so that a
+  // backward row (Bk + kv wide) fits the 1024-column register row when that
+  // costs less than a quarter of the block
+  Index bk = std::max<Index>(32, 2 * kl);
+  if (bk + kv > 1024 && 1024 - kv >= (3 * bk) / 4) bk = 1024 - kv;
   const Index nblk = (n + bk - 1) / bk;
   std::vector<int64_t> foff(static_cast<size_t>(nblk)), goff(static_cast<size_t>(nblk));
   int64_t fo = 0, go = 0;
@@ -729,9 +804,6 @@ void coarse_correct(const CoarseDev& c, const double* r, double* z, cudaStream_t
     Scratch<BlockSync> bsync(1, s);  // per call: concurrent applies on one handle stay independent
     PDB_CUDA(cudaMemsetAsync(bsync.get(), 0, sizeof(BlockSync), s));
     BlockSync* sy = bsync.get();
-    int per_sm = 0;
-    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blocked_solve_kernel, kBlkThreads, smem));
-    const int grid = std::max(1, std::min(per_sm, 2) * num_sms());
     Scratch<double> yf(nc, s), carry(static_cast<size_t>(2 * std::max<Index>(c.kl, 1)), s);
     int n_ = static_cast<int>(c.nc), kl_ = static_cast<int>(c.kl), kv_ = static_cast<int>(c.kl + c.ku),
         bk_ = static_cast<int>(c.bk), nb_ = static_cast<int>(c.nblk);
@@ -744,8 +816,27 @@ void coarse_correct(const CoarseDev& c, const double* r, double* z, cudaStream_t
     double* cp = carry.get();
     double* xp = xc.get();
     void* args[] = {&n_, &kl_, &kv_, &bk_, &nb_, &fo, &go, &F, &G, &rhs, &yfp, &cp, &xp, &sy};
-    PDB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(blocked_solve_kernel), dim3(grid), dim3(kBlkThreads),
-                                         args, smem, s));
+    // register-prefetched variant when one row per warp suffices
+    const Index rows_max = c.bk + c.kl;  // forward block height
+    const char* pe = getenv("PDB_COARSE_PF");
+    const bool pf_ok = !(pe && pe[0] == '0') && c.vmax <= 32 * 48 && rows_max <= num_sms() * (kBlkThreads / 32);
+    void* kern = reinterpret_cast<void*>(blocked_solve_kernel);
+    size_t ksmem = smem;
+    if (pf_ok) {
+      const int R = c.vmax <= 256 ? 8 : c.vmax <= 512 ? 16 : c.vmax <= 1024 ? 32 : 48;
+      kern = R == 8 ? reinterpret_cast<void*>(blocked_solve_pf_kernel<8>)
+             : R == 16 ? reinterpret_cast<void*>(blocked_solve_pf_kernel<16>)
+             : R == 32 ? reinterpret_cast<void*>(blocked_solve_pf_kernel<32>)
+                       : reinterpret_cast<void*>(blocked_solve_pf_kernel<48>);
+      ksmem = static_cast<size_t>(32 * R) * sizeof(double);
+    }
+    int per_sm = 0;
+    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlkThreads, ksmem));
+    // the prefetch variant needs rows_max warps: one CTA per SM is enough and
+    // keeps the barrier cheap
+    const int grid = pf_ok ? num_sms() : std::max(1, std::min(per_sm, 2) * num_sms());
+    require(per_sm >= 1, Errc::internal, "coarse solve kernel cannot be resident");
+    PDB_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kBlkThreads), args, ksmem, s));
     prolong_add_kernel<<<static_cast<unsigned>((c.fine_n + 255) / 256), 256, 0, s>>>(
         c.fine_n, c.p0_ptr.get(), c.p0_col.get(), c.p0_val.get(), xc.get(), z);
     PDB_LAUNCH_CHECK();

@@ -62,9 +62,11 @@ def main():
             combo = P.Preconditioner.create_combo(p, ps)
             t_setup = time.time() - t
             ms_combo = dev_time(lambda: combo.apply_device(r.data_ptr(), z.data_ptr(), s))
-            t = time.time()
-            x, rep = P.gmres(A, b, combo)
-            t_gmres = time.time() - t
+            t_gmres = 1e30
+            for _ in range(2):  # the first solve also pays lazy module loading
+                t = time.time()
+                x, rep = P.gmres(A, b, combo)
+                t_gmres = min(t_gmres, time.time() - t)
             row.update({"nc": combo.coarse_size()[0], "band": combo.coarse_size()[1:],
                         f"{path}_setup_s": round(t_setup, 4), f"{path}_apply_us": round(1e3 * ms_combo, 2),
                         f"{path}_coarse_us": round(1e3 * (ms_combo - ms_plain), 2),

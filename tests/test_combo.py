@@ -24,11 +24,16 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["dense", "blocked", "band"])
+@pytest.fixture(params=["dense", "blocked", "blocked-nopf", "band"])
 def coarse_path(request, monkeypatch):
     """The device coarse solvers: the dense inverse (default for n_c <= 16384),
-    the blocked solve (default above) and the one-warp band sweep."""
-    monkeypatch.setenv("PDB_COARSE", request.param)
+    the blocked solve (default above; with and without the register-prefetched
+    rows) and the one-warp band sweep."""
+    path = request.param
+    if path == "blocked-nopf":
+        path = "blocked"
+        monkeypatch.setenv("PDB_COARSE_PF", "0")
+    monkeypatch.setenv("PDB_COARSE", path)
     return request.param
 
 CASES = [
