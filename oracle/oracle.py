@@ -351,6 +351,13 @@ class RefLib:
         L.refh_coarse_factor.argtypes = [_P, _I64, _I64, _D, _I64]
         L.refh_combo_new.argtypes = [_P, _P, _P, C.c_double, C.c_int, C.POINTER(_P)]
         L.refh_export_matrix.argtypes = [C.c_char_p, C.c_char_p]
+        L.refh_problem_from_csr.restype = _P
+        L.refh_problem_from_csr.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_int, C.c_int64, C.c_int]
+
+    def problem_from_csr(self, csr, rhs, dim, cells, degree):
+        rp, ci, v = (_i64(csr[0]), _i64(csr[1]), _f64(csr[2]))
+        return RefProblem(self, self.lib.refh_problem_from_csr(len(rp) - 1, _ip(rp), _ip(ci), _dp(v), _dp(_f64(rhs)),
+                                                               dim, cells, degree))
 
     def export_matrix(self, config_json: str, path: str):
         self._check(self.lib.refh_export_matrix(config_json.encode(), path.encode()))

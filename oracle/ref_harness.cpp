@@ -495,3 +495,17 @@ RH_API int refh_combo_new(void* p, void* ps, void* db, double omega, int threads
 RH_API int refh_export_matrix(const char* json, const char* path) {
   return guarded([&] { export_matrix(parse_config(json), path); });
 }
+
+// A reference DiscreteProblem around an external CSR on a uniform lattice
+// (dim, cells, degree): lets the reference's combo run on generated configs.
+RH_API void* refh_problem_from_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* rhs,
+                                   int dim, int64_t cells, int degree) {
+  auto* p = new DiscreteProblem();
+  p->matrix.n = n;
+  p->matrix.row_ptr.assign(rp, rp + n + 1);
+  p->matrix.col_idx.assign(ci, ci + rp[n]);
+  p->matrix.values.assign(v, v + rp[n]);
+  p->rhs.assign(rhs, rhs + n);
+  p->mesh = StructuredMesh{dim, cells, degree};
+  return p;
+}

@@ -420,6 +420,8 @@ void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf
 struct AssignSlot {
   int64_t lo = 0, hi = 0;
   DevBuf<double> sub_il;
+  DevBuf<double> dist, lbq;  // pruned spectral assignment: distances / quotient bounds kept across iterations
+  int64_t m = 0;             // columns of dist / lbq
 };
 
 void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max_iters, Empty policy,
@@ -459,6 +461,21 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   }
   DevBuf<double> lu_il;
   DevBuf<int32_t> piv_il;
+  // Assignment pruning (spectral variants, Lloyd iterations >= 1): each
+  // patch's distance to its current centroid is evaluated first; every
+  // other pair stops as soon as its Rayleigh quotient proves it larger
+  // (spectral_tiled_il ub).  The argmin, its distance and so the whole
+  // k-means run are unchanged; only the losing pairs' power iterations are
+  // cut short.  PDB_KMEANS_PRUNE=0 evaluates every pair to convergence.
+  const char* pr_env = getenv("PDB_KMEANS_PRUNE");
+  const bool prune = il && !(pr_env && pr_env[0] == '0');
+  DevBuf<double> ub;
+  DevBuf<int32_t> guess;  // iteration 0: l1-nearest entry, for the first bound
+  DevBuf<double> gmin;
+  Scratch<int32_t> gchanged(1, s);
+  DevBuf<uint8_t> d_chg;  // per entry: centroid changed since the previous assignment
+  std::vector<std::vector<int32_t>> prev_members;
+  if (prune) ub.alloc(cap);
   for (int iter = 0; iter < max_iters; ++iter) {
     const int64_t m = db.m;
     PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
@@ -474,14 +491,54 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
         k::l1_argmin(cnt, m, static_cast<int>(len), sub + sl.lo * len, db.reps.get(), d_phi.get() + sl.lo,
                      d_new.get() + sl.lo, d_min.get() + sl.lo, changed.get(), s);
       } else {
-        if (dist.size() < static_cast<size_t>(cnt * m)) dist.alloc(static_cast<size_t>(cnt * m));
+        double* dd = nullptr;
+        if (prune) {  // per-slot distance matrix, kept for the next iteration
+          if (sl.m != m) {
+            sl.dist.alloc(static_cast<size_t>(cnt * m));
+            sl.lbq.alloc(static_cast<size_t>(cnt * m));
+            sl.lbq.zero(s);
+            sl.m = m;
+          }
+          dd = sl.dist.get();
+        } else {
+          if (dist.size() < static_cast<size_t>(cnt * m)) dist.alloc(static_cast<size_t>(cnt * m));
+          dd = dist.get();
+        }
+        const bool pr = prune;
+        k::KmeansReuse ru;
+        const int32_t* cur_phi = d_phi.get() + sl.lo;
+        if (pr && iter == 0) {
+          // no assignment yet: bound each patch by its distance to the entry
+          // nearest in the entrywise l1 sense (any entry's distance bounds the min)
+          if (guess.size() < static_cast<size_t>(cap)) {
+            guess.alloc(cap);
+            gmin.alloc(cap);
+          }
+          k::l1_argmin(cnt, m, static_cast<int>(len), sub + sl.lo * len, db.reps.get(), d_phi.get() + sl.lo,
+                       guess.get() + sl.lo, gmin.get() + sl.lo, gchanged.get(), s);
+          cur_phi = guess.get() + sl.lo;
+          std::vector<uint8_t> ones(static_cast<size_t>(m), 1);
+          d_chg.alloc(static_cast<size_t>(m));
+          h2d(d_chg.get(), ones, s);
+        }
+        if (pr) {
+          ru.chg = d_chg.get();
+          ru.dprev = dd;
+          ru.mfull = m;
+          k::spectral_diag_il(cnt, ps, sl.sub_il.get(), db.lu.get(), db.piv.get(), cur_phi, ub.get() + sl.lo,
+                              iters.get(), s, ru);
+          work.pair_evals += cnt;
+          ru.ub = ub.get() + sl.lo;
+          ru.phi = cur_phi;
+          ru.lbq = sl.lbq.get();
+          ru.dprev = nullptr;
+        }
         if (il)
-          k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), dist.get(), iters.get(), s);
+          k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), dd, iters.get(), s, ru);
         else
-          k::spectral_pairs(cnt, nullptr, m, ps, sub + sl.lo * len, db.lu.get(), db.piv.get(), dist.get(),
-                            iters.get(), s);
-        k::argmin_assign(cnt, m, dist.get(), d_phi.get() + sl.lo, d_new.get() + sl.lo, d_min.get() + sl.lo,
-                         changed.get(), s);
+          k::spectral_pairs(cnt, nullptr, m, ps, sub + sl.lo * len, db.lu.get(), db.piv.get(), dd, iters.get(), s);
+        k::argmin_assign(cnt, m, dd, d_phi.get() + sl.lo, d_new.get() + sl.lo, d_min.get() + sl.lo, changed.get(),
+                         s);
       }
     }
     PDB_LAUNCH_CHECK();
@@ -502,6 +559,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
 
     std::vector<std::vector<int32_t>> members(static_cast<size_t>(m));
     for (int64_t i = 0; i < n; ++i) members[static_cast<size_t>(phi_h[static_cast<size_t>(i)])].push_back(static_cast<int32_t>(i));
+    const int64_t m_before = m;
 
     if (policy == Empty::Prune) {  // compress.cpp:179-194
       std::vector<int32_t> remap(static_cast<size_t>(m), -1), kept_ids;
@@ -557,6 +615,18 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       }
     }
     h2d(d_phi.get(), phi_h, s);
+    if (prune) {
+      // the update below is a deterministic function of each cluster's
+      // (ascending) member list: unchanged members -> bitwise unchanged centroid
+      const int64_t mc = db.m;
+      std::vector<uint8_t> chg(static_cast<size_t>(mc), 1);
+      if (iter > 0 && mc == m_before && static_cast<int64_t>(prev_members.size()) == mc)
+        for (int64_t j = 0; j < mc; ++j)
+          chg[static_cast<size_t>(j)] = members[static_cast<size_t>(j)] != prev_members[static_cast<size_t>(j)];
+      d_chg.alloc(static_cast<size_t>(std::max<int64_t>(mc, 1)));
+      h2d(d_chg.get(), chg, s);
+      prev_members = members;
+    }
 
     // representative update (compress.cpp:219-261); failures re-raised as
     // singular_matrix "cluster j: ..." for the lowest failing j.

@@ -140,8 +140,28 @@ int64_t interleaved_len(int64_t count, int width, int64_t len);
 void interleave_patches(int64_t count, int64_t len, const double* src, double* dst, cudaStream_t s);
 void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* piv, double* lu_il, int32_t* piv_il,
                         cudaStream_t s);
+// k-means assignment reuse (all optional): ub = per-patch distance to its
+// current centroid (pairs whose Rayleigh quotient exceeds
+// max(ub^2 (1 + 1e-4), 1e-8) stop with d = +inf: they cannot be the argmin);
+// chg = per-entry "centroid changed" flags -- pairs of unchanged centroids
+// keep d from the previous launch (exact) or stay +inf when lbq (the quotient
+// at which they were pruned) still exceeds the bound; dprev/mfull: the
+// previous distance matrix for the DIAG (bound) launch.
+struct KmeansReuse {
+  const double* ub = nullptr;
+  const int32_t* phi = nullptr;  // current assignment: the pair (i, phi[i]) is ub[i] itself
+  const uint8_t* chg = nullptr;
+  double* lbq = nullptr;
+  const double* dprev = nullptr;
+  int64_t mfull = 0;
+};
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
-                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s);
+                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s,
+                       KmeansReuse ru = KmeansReuse{});
+// d[t] = dist(patch t, factor phi[t]) for interleaved patches and plain-layout factors.
+void spectral_diag_il(int64_t npat, int ps, const double* mats_il, const double* lu, const int32_t* piv,
+                      const int32_t* phi, double* d, unsigned long long* iters, cudaStream_t s,
+                      KmeansReuse ru = KmeansReuse{});
 // Spectral distance of listed (patch, factor) pairs: d[t] = dist(mats[pa[t]], factor fb[t]).
 void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);

@@ -393,24 +393,40 @@ constexpr int kTileThreads = 64;
 // (patch, factor) pairs of one tile, so each load of the interleaved copy is
 // one contiguous 256-byte (patches) / 64-byte (factors) span instead of up to
 // 32 separate cache lines.
-template <int PS, bool IL>
+// DIAG (with IL): one pair per patch, (patch, its centroid diag_phi[patch]),
+// the factors in the plain layout (d[patch] is written) -- the pruning bound.
+// KmeansReuse (k-means assignment, all pointers may be null): ub = per-patch
+// bound, chg = per-entry "centroid changed since the previous assignment",
+// lbq = per-pair Rayleigh quotient at which a pair was pruned, dprev (DIAG) =
+// the previous distance matrix with mfull columns.  A pair whose centroid is
+// unchanged keeps its previous exact distance, or stays +inf when its stored
+// quotient already exceeds the bound; only pairs of changed centroids run.
+template <int PS, bool IL, bool DIAG = false>
 __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npat, const int32_t* __restrict__ pid,
                                                                      int64_t ne, const double* __restrict__ mats,
                                                                      const double* __restrict__ lu,
                                                                      const int32_t* __restrict__ piv,
                                                                      double* __restrict__ d,
-                                                                     unsigned long long* iters_total) {
+                                                                     unsigned long long* iters_total,
+                                                                     KmeansReuse ru,
+                                                                     const int32_t* __restrict__ diag_phi = nullptr) {
+  const double* __restrict__ ub = ru.ub;
   constexpr int LEN = PS * PS;
   constexpr int BD = kTileThreads;
-  constexpr int SA = IL ? kTileA : 1;  // element stride of a patch matrix
-  constexpr int SL = IL ? kTileE : 1;  // element stride of a factor / pivot vector
+  constexpr int SA = IL ? kTileA : 1;             // element stride of a patch matrix
+  constexpr int SL = (IL && !DIAG) ? kTileE : 1;  // element stride of a factor / pivot vector
   extern __shared__ double sm[];
   double* vec = sm;  // 3 * PS * BD: v, w, t
   __shared__ int counter;
   const int tid = threadIdx.x;
-  const int64_t a0 = (int64_t)blockIdx.x * kTileA, e0 = (int64_t)blockIdx.y * kTileE;
-  const int na = (int)(npat - a0 < kTileA ? npat - a0 : kTileA);
-  const int nev = (int)(ne - e0 < kTileE ? ne - e0 : kTileE);
+  constexpr int TA = DIAG ? 4 * kTileThreads : kTileA;  // DIAG: 256 patches pulled by 64 threads
+  const int64_t a0 = (int64_t)blockIdx.x * TA, e0 = (int64_t)blockIdx.y * kTileE;
+  const int na = (int)(npat - a0 < TA ? npat - a0 : TA);
+  // pruned k-means assignment (IL, bound given): one block takes every factor
+  // of its patches, so the few pairs that run to convergence overlap with
+  // many that are cut after an iteration or two
+  const bool all_e = IL && !DIAG && ru.ub != nullptr;
+  const int nev = all_e ? (int)ne : (int)(ne - e0 < kTileE ? ne - e0 : kTileE);
   const double* LUs = IL ? lu + (int64_t)blockIdx.y * LEN * kTileE : lu + e0 * LEN;
   const int32_t* Ps = IL ? piv + (int64_t)blockIdx.y * PS * kTileE : piv + e0 * PS;
   if (tid == 0) counter = 0;
@@ -418,7 +434,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   double* V = vec + tid;
   double* W = vec + PS * BD + tid;
   double* Tv = vec + 2 * PS * BD + tid;
-  const int npairs = na * nev;
+  const int npairs = DIAG ? na : na * nev;
   bool active = false;
   int it = 0, pa = 0, pe = 0;
   double lambda = 0.0;
@@ -427,17 +443,43 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   const int32_t* P = Ps;
   unsigned long long my_iters = 0;
   for (;;) {
-    if (!active) {
+    while (!active) {
       const int p = atomicAdd(&counter, 1);
-      if (p < npairs) {
-        active = true;
+      if (p >= npairs) break;
+      {
         pa = p % na;
         pe = p / na;
         const int64_t g = a0 + pa;
-        if (IL) {
+        if (ru.chg != nullptr) {  // reuse across Lloyd iterations
+          if (DIAG) {
+            const int32_t f = diag_phi[g];
+            if (!ru.chg[f]) {
+              d[g] = ru.dprev[g * ru.mfull + f];
+              continue;
+            }
+          } else if (ru.phi != nullptr && ru.phi[g] == e0 + pe) {
+            d[g * ne + e0 + pe] = ub[g];  // the bound is this pair's distance, computed the same way
+            continue;
+          } else if (!ru.chg[e0 + pe]) {
+            const int64_t q = g * ne + e0 + pe;
+            if (isfinite(d[q])) continue;  // exact distance of the unchanged centroid
+            if (isfinite(ub[g]) && ru.lbq[q] > fmax(ub[g] * ub[g] * (1.0 + 1e-4), 1e-8)) continue;  // still beaten
+          }
+        }
+        active = true;
+        if (DIAG) {
+          A = mats + (g / kTileA) * LEN * kTileA + g % kTileA;
+          L = lu + (int64_t)diag_phi[g] * LEN;
+          P = piv + (int64_t)diag_phi[g] * PS;
+        } else if (IL) {
           A = mats + (int64_t)blockIdx.x * LEN * kTileA + pa;
-          L = LUs + pe;
-          P = Ps + pe;
+          if (all_e) {  // factor pe of the interleaved groups of kTileE
+            L = lu + (int64_t)(pe / kTileE) * LEN * kTileE + pe % kTileE;
+            P = piv + (int64_t)(pe / kTileE) * PS * kTileE + pe % kTileE;
+          } else {
+            L = LUs + pe;
+            P = Ps + pe;
+          }
         } else {
           A = mats + (int64_t)(pid ? pid[g] : g) * LEN;
           L = LUs + pe * LEN;
@@ -530,6 +572,16 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     } else if (it > 1 && fabs(__dsub_rn(rq, lambda)) < __dmul_rn(1e-8, rq)) {
       done = true;
       result = __dsqrt_rn(rq);
+    } else if (ub != nullptr && isfinite(ub[a0 + pa]) && rq > fmax(ub[a0 + pa] * ub[a0 + pa] * (1.0 + 1e-4), 1e-8)) {
+      // k-means pruning: the Rayleigh quotients of the power iteration rise
+      // monotonically to the returned value, so this pair ends above the
+      // patch's distance to its current centroid and cannot be the argmin.
+      // The margin and the floor (distance 1e-4) keep the test clear of
+      // rounding: near-identical pairs (quotients at noise level, not
+      // monotone) always run to convergence.
+      done = true;
+      result = CUDART_INF;
+      if (!DIAG && ru.lbq != nullptr) ru.lbq[(a0 + pa) * ne + e0 + pe] = rq;
     } else {
       lambda = rq;
       double s = 0.0;
@@ -549,7 +601,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
       }
     }
     if (done) {
-      d[(a0 + pa) * ne + e0 + pe] = result;
+      d[DIAG ? a0 + pa : (a0 + pa) * ne + e0 + pe] = result;
       my_iters += (unsigned long long)it;
       active = false;
     }
@@ -559,11 +611,13 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
 
 template <int PS, bool IL = false>
 bool launch_spectral_tile(int64_t npat, const int32_t* pid, int64_t ne, const double* mats, const double* lu,
-                          const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+                          const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s,
+                          KmeansReuse ru = KmeansReuse{}) {
   const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
   cudaFuncSetAttribute(spectral_tile_kernel<PS, IL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid(grid_for(npat, kTileA), (unsigned)((ne + kTileE - 1) / kTileE));
-  spectral_tile_kernel<PS, IL><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters);
+  const bool all_e = IL && ru.ub != nullptr;  // must match the kernel's all_e
+  dim3 grid(grid_for(npat, kTileA), all_e ? 1u : (unsigned)((ne + kTileE - 1) / kTileE));
+  spectral_tile_kernel<PS, IL><<<grid, kTileThreads, smem, s>>>(npat, pid, ne, mats, lu, piv, d, iters, ru);
   return true;
 }
 
@@ -693,16 +747,39 @@ void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* 
 }
 
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
-                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s) {
+                       const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru) {
   switch (ps) {
-    case 9: launch_spectral_tile<9, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
-    case 22: launch_spectral_tile<22, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
-    case 25: launch_spectral_tile<25, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
-    case 27: launch_spectral_tile<27, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s); break;
+    case 9: launch_spectral_tile<9, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, ru); break;
+    case 22: launch_spectral_tile<22, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, ru); break;
+    case 25: launch_spectral_tile<25, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, ru); break;
+    case 27: launch_spectral_tile<27, true>(npat, nullptr, ne, mats_il, lu_il, piv_il, d, iters, s, ru); break;
     default: break;
   }
 }
 
+
+template <int PS>
+void launch_spectral_diag(int64_t npat, const double* mats_il, const double* lu, const int32_t* piv, const int32_t* phi,
+                          double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru) {
+  const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
+  cudaFuncSetAttribute(spectral_tile_kernel<PS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ru.ub = nullptr;
+  ru.lbq = nullptr;
+  spectral_tile_kernel<PS, true, true><<<grid_for(npat, 4 * kTileThreads), kTileThreads, smem, s>>>(
+      npat, nullptr, 1, mats_il, lu, piv, d, iters, ru, phi);
+}
+
+void spectral_diag_il(int64_t npat, int ps, const double* mats_il, const double* lu, const int32_t* piv,
+                      const int32_t* phi, double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru) {
+  if (npat <= 0) return;
+  switch (ps) {
+    case 9: launch_spectral_diag<9>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
+    case 22: launch_spectral_diag<22>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
+    case 25: launch_spectral_diag<25>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
+    case 27: launch_spectral_diag<27>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
+    default: break;
+  }
+}
 
 void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,
               const double* reps, double* d, cudaStream_t s) {

@@ -1,27 +1,18 @@
-"""PCG on config 2 with the Dirichlet columns eliminated (symmetric system) vs row replacement only."""
-import sys, time, numpy as np
+"""PCG to 1e-8 on BASELINE config 2 with the one-level patch preconditioner
+(exact, k-means entrywise k=64, k-means spectral k=64): iterations and time."""
+import json, os, sys, time, numpy as np
 sys.path.insert(0, ".")
 from paper_2306_10025_b200 import patchdb as P
 prob = P.Problem.generate(2, 0)
-rp, ci, v = prob.csr()
-b = prob.rhs()
-n = len(rp) - 1
-cnt = np.diff(rp)
-bnd = np.zeros(n, bool)
-# boundary rows: single stored entry on the diagonal
-one = np.flatnonzero(cnt == 1)
-bnd[one] = ci[rp[one]] == one
-rows = np.repeat(np.arange(n), cnt)
-mask = (~bnd[rows]) & bnd[ci]
-bs = b.copy()
-np.subtract.at(bs, rows[mask], v[mask] * b[ci[mask]])
-vs = v.copy(); vs[mask] = 0.0
-As = P.Matrix.from_csr(rp, ci, vs)
-A = prob.matrix()
-ps = P.PatchSet.detect(As, 25)
-for name, M, rhs in [("sym", As, bs), ("rowrep", A, b)]:
-    db = P.Database.build(M, ps, P.KMEANS_ENTRYWISE, db_size=64, seed=42, max_iters=50)
-    for pname, pc in [("compressed", P.Preconditioner.create(M, ps, db, omega=1.0)), ("exact", P.Preconditioner.create(M, ps, None, omega=1.0))]:
-        t = time.perf_counter(); x, r = P.pcg(M, rhs, pc, tol=1e-8, max_iters=8000); dt = time.perf_counter() - t
-        h = np.array(r.residual_history)
-        print(name, pname, "pcg", r.converged, r.iterations, f"{dt:.2f}s", [f"{h[i]:.1e}" for i in range(0, len(h), max(1, len(h)//10))], flush=True)
+A = prob.matrix(); ps = P.PatchSet.detect(A, 25); b = prob.rhs()
+maxit = int(os.environ.get("MAXIT", "40000"))
+for name in os.environ.get("VARIANTS", "exact,entrywise,spectral").split(","):
+    t = time.perf_counter()
+    db = None if name == "exact" else P.Database.build(A, ps, {"entrywise": P.KMEANS_ENTRYWISE, "spectral": P.KMEANS_SPECTRAL}[name], db_size=64, seed=42, max_iters=50)
+    pc = P.Preconditioner.create(A, ps, db, omega=1.0)
+    t_setup = time.perf_counter() - t
+    t = time.perf_counter(); x, r = P.pcg(A, b, pc, tol=1e-8, max_iters=maxit); dt = time.perf_counter() - t
+    h = np.array(r.residual_history)
+    print(json.dumps(dict(config=2, precond=name, setup_s=round(t_setup, 2), pcg_iters=r.iterations, converged=r.converged,
+                          final_rel=r.final_relative_residual, solve_s=round(dt, 3), us_per_iter=round(1e6 * dt / max(r.iterations, 1), 1),
+                          history_every_10pct=[float(f"{h[i]:.2e}") for i in range(0, len(h), max(1, len(h) // 10))])), flush=True)

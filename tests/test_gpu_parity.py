@@ -352,3 +352,25 @@ def test_gmres_fused_mgs_matches_per_vector_launches(P, cells, monkeypatch):
     assert r1.iterations == r0.iterations
     np.testing.assert_allclose(r1.residual_history, r0.residual_history, rtol=1e-7)
     np.testing.assert_allclose(x1, x0, rtol=0, atol=1e-8 * np.abs(x0).max())
+
+
+@pytest.mark.parametrize("cfg,cells,ps,k,method", [(2, 48, 25, 24, "KMEANS_SPECTRAL"), (1, 24, 9, 12, "KMEANS_SPECTRAL"),
+                                                   (3, 8, 27, 40, "KMEANS_SPECTRAL"), (4, 16, 22, 16, "KMEANS_SPECTRAL"),
+                                                   (2, 32, 25, 16, "BOOTSTRAP"), (1, 32, 9, 0, "BOOTSTRAP"),
+                                                   (4, 12, 22, 0, "BOOTSTRAP")])
+def test_kmeans_assignment_pruning_changes_nothing(P, cfg, cells, ps, k, method, monkeypatch):
+    """Cutting losing pairs' power iterations short (their Rayleigh quotient
+    already exceeds the patch's distance to its current centroid) leaves the
+    whole k-means run bitwise unchanged: phi, representatives, factors."""
+    prob = P.Problem.generate(cfg, cells)
+    A = prob.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    kw = dict(db_size=k, seed=7, max_iters=30) if method != "BOOTSTRAP" else dict(eps=1e-3 if k else 0.3, max_iters=10)
+    on = P.Database.build(A, pset, getattr(P, method), **kw)
+    monkeypatch.setenv("PDB_KMEANS_PRUNE", "0")
+    off = P.Database.build(A, pset, getattr(P, method), **kw)
+    assert np.array_equal(on.phi(), off.phi())
+    assert np.array_equal(on.representatives(), off.representatives())
+    for a, b in zip(on.factors(), off.factors()):
+        assert np.array_equal(a, b)
+    assert on.work()["power_iters"] <= off.work()["power_iters"]  # executed power iterations
