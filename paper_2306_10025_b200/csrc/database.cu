@@ -181,6 +181,12 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
   int64_t m = 0;
   bool aborted = false;
   std::vector<int64_t> state_h(3);
+  // Only distances below eps matter (first match: d < eps; best match: the
+  // smallest d < eps), so spectral pairs that provably end above eps stop
+  // early (Rayleigh-quotient bound, as the k-means pruning); PDB_GREEDY_PRUNE=0
+  // runs every pair to convergence.
+  const char* gp = getenv("PDB_GREEDY_PRUNE");
+  const double bound = (gp && gp[0] == '0') ? 0.0 : eps;
   while (nu > 0) {
     const int64_t B = std::min(nu, Bmax);
     const int32_t* S = U.get();
@@ -190,7 +196,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
       std::vector<int32_t> st;
       lu_many(B, ps, mats.get(), S, luS.get(), pivS.get(), msg, work, s, &st);
       h2d(luS_status.get(), st, s);
-      k::spectral_pairs(B, S, B, ps, mats.get(), luS.get(), pivS.get(), D.get(), iters.get(), s);
+      k::spectral_pairs(B, S, B, ps, mats.get(), luS.get(), pivS.get(), D.get(), iters.get(), s, bound);
     } else {
       k::l1_pairs(B, S, B, static_cast<int>(len), mats.get(), S, nullptr, D.get(), s);
     }
@@ -268,7 +274,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
           for (int64_t c0 = m; c0 < m_new && live > 0; c0 += CH) {
             const int64_t ne = std::min(CH, m_new - c0);
             k::spectral_pairs(live, Rr, ne, ps, mats.get(), store.lu.get() + c0 * len, store.piv.get() + c0 * ps,
-                              dch.get(), iters.get(), s);
+                              dch.get(), iters.get(), s, bound);
             k::apply_scan(live, Rr, c0, ne, dch.get(), creators.get(), eps, best_match ? 1 : 0, phi.get(),
                           best_d.get(), s);
             PDB_LAUNCH_CHECK();

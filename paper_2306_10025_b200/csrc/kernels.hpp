@@ -130,8 +130,10 @@ void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const doubl
               const double* reps, double* d, cudaStream_t s);
 // Spectral: d[t*ne + e] = spectral_distance(mats[pid[t]], factor e) (dense.cpp:154-190).
 // iters (may be null) accumulates power iterations (atomic, for work accounting).
+// bound > 0 (greedy tolerance): pairs that provably end at d > bound stop early with d = +inf
+// (patch sizes of the tiled kernel only; the others always run to convergence).
 void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
-                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s, double bound = 0.0);
 // Interleaved spectral path (k-means assignment): patches interleaved in groups of 32
 // (interleave_patches, once per patch set) and factors in groups of 8 (interleave_factors,
 // per Lloyd iteration); then d[t*ne + e] as spectral_pairs with pid = null.
@@ -149,6 +151,7 @@ void interleave_factors(int64_t count, int ps, const double* lu, const int32_t* 
 // previous distance matrix for the DIAG (bound) launch.
 struct KmeansReuse {
   const double* ub = nullptr;
+  double ubc = 0.0;  // > 0: the same bound for every patch (greedy tolerance), when ub is null
   const int32_t* phi = nullptr;  // current assignment: the pair (i, phi[i]) is ub[i] itself
   const uint8_t* chg = nullptr;
   double* lbq = nullptr;

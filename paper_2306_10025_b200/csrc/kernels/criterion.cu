@@ -572,7 +572,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     } else if (it > 1 && fabs(__dsub_rn(rq, lambda)) < __dmul_rn(1e-8, rq)) {
       done = true;
       result = __dsqrt_rn(rq);
-    } else if (ub != nullptr && isfinite(ub[a0 + pa]) && rq > fmax(ub[a0 + pa] * ub[a0 + pa] * (1.0 + 1e-4), 1e-8)) {
+    } else if ((ub != nullptr || ru.ubc > 0.0) && isfinite(ub ? ub[a0 + pa] : ru.ubc) &&
+               rq > fmax((ub ? ub[a0 + pa] * ub[a0 + pa] : ru.ubc * ru.ubc) * (1.0 + 1e-4), 1e-8)) {
       // k-means pruning: the Rayleigh quotients of the power iteration rise
       // monotonically to the returned value, so this pair ends above the
       // patch's distance to its current centroid and cannot be the argmin.
@@ -635,14 +636,16 @@ __global__ void interleave_kernel(int64_t total, int64_t count, int width, int64
 }
 
 bool spectral_tiled(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
-                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s, double bound) {
   const char* e = getenv("PDB_SPECTRAL_TILED");
   if (e && e[0] == '0') return false;
+  KmeansReuse ru;
+  ru.ubc = bound;
   switch (ps) {
-    case 9: return launch_spectral_tile<9>(npat, pid, ne, mats, lu, piv, d, iters, s);
-    case 22: return launch_spectral_tile<22>(npat, pid, ne, mats, lu, piv, d, iters, s);
-    case 25: return launch_spectral_tile<25>(npat, pid, ne, mats, lu, piv, d, iters, s);
-    case 27: return launch_spectral_tile<27>(npat, pid, ne, mats, lu, piv, d, iters, s);
+    case 9: return launch_spectral_tile<9>(npat, pid, ne, mats, lu, piv, d, iters, s, ru);
+    case 22: return launch_spectral_tile<22>(npat, pid, ne, mats, lu, piv, d, iters, s, ru);
+    case 25: return launch_spectral_tile<25>(npat, pid, ne, mats, lu, piv, d, iters, s, ru);
+    case 27: return launch_spectral_tile<27>(npat, pid, ne, mats, lu, piv, d, iters, s, ru);
     default: return false;
   }
 }
@@ -792,9 +795,9 @@ static int spectral_block(int ps) { return ps <= 40 ? 64 : ps <= 96 ? 32 : 16; }
 static size_t spectral_vec_bytes(int ps, int bd) { return (size_t)4 * ps * bd * sizeof(double); }
 
 void spectral_pairs(int64_t npat, const int32_t* pid, int64_t ne, int ps, const double* mats, const double* lu,
-                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s) {
+                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s, double bound) {
   if (npat <= 0 || ne <= 0) return;
-  if (spectral_tiled(npat, pid, ne, ps, mats, lu, piv, d, iters, s)) return;
+  if (spectral_tiled(npat, pid, ne, ps, mats, lu, piv, d, iters, s, bound)) return;
   const int bd = spectral_block(ps);
   size_t smem = (size_t)ps * ps * sizeof(double) + (size_t)((ps + 1) / 2) * sizeof(double) +
                 spectral_vec_bytes(ps, bd);

@@ -374,3 +374,20 @@ def test_kmeans_assignment_pruning_changes_nothing(P, cfg, cells, ps, k, method,
     for a, b in zip(on.factors(), off.factors()):
         assert np.array_equal(a, b)
     assert on.work()["power_iters"] <= off.work()["power_iters"]  # executed power iterations
+
+
+@pytest.mark.parametrize("best_match", [False, True])
+@pytest.mark.parametrize("cfg,cells,ps,eps", [(1, 32, 9, 1e-2), (1, 32, 9, 0.3), (2, 24, 25, 0.05), (3, 6, 27, 0.2)])
+def test_greedy_spectral_pruning_changes_nothing(P, cfg, cells, ps, eps, best_match, monkeypatch):
+    """Greedy only looks at distances below eps, so pairs cut short once their
+    Rayleigh quotient proves d > eps leave the database unchanged."""
+    prob = P.Problem.generate(cfg, cells)
+    A = prob.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    on = P.Database.build(A, pset, P.GREEDY_SPECTRAL, eps=eps, best_match=best_match)
+    monkeypatch.setenv("PDB_GREEDY_PRUNE", "0")
+    off = P.Database.build(A, pset, P.GREEDY_SPECTRAL, eps=eps, best_match=best_match)
+    assert on.size == off.size
+    assert np.array_equal(on.phi(), off.phi())
+    assert np.array_equal(on.representatives(), off.representatives())
+    assert on.work()["power_iters"] <= off.work()["power_iters"]
