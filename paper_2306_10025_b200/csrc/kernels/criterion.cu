@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   double* vec = sm;  // 3 * PS * BD: v, w, t
   __shared__ int counter;
   const int tid = threadIdx.x;
-  constexpr int TA = DIAG ? 4 * kTileThreads : kTileA;  // DIAG: 256 patches pulled by 64 threads
+  constexpr int TA = DIAG ? 2 * kTileThreads : kTileA;  // DIAG: 128 patches pulled by 64 threads
   const int64_t a0 = (int64_t)blockIdx.x * TA, e0 = (int64_t)blockIdx.y * kTileE;
   const int na = (int)(npat - a0 < TA ? npat - a0 : TA);
   // pruned k-means assignment (IL, bound given): one block takes every factor
@@ -768,7 +768,7 @@ void launch_spectral_diag(int64_t npat, const double* mats_il, const double* lu,
   cudaFuncSetAttribute(spectral_tile_kernel<PS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   ru.ub = nullptr;
   ru.lbq = nullptr;
-  spectral_tile_kernel<PS, true, true><<<grid_for(npat, 4 * kTileThreads), kTileThreads, smem, s>>>(
+  spectral_tile_kernel<PS, true, true><<<grid_for(npat, 2 * kTileThreads), kTileThreads, smem, s>>>(
       npat, nullptr, 1, mats_il, lu, piv, d, iters, ru, phi);
 }
 

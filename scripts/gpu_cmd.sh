@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_combo.py -q -m gpu -k "greedy or experiment1" > gpurun_out/t_gr.log 2>&1; echo "exit $?" >> gpurun_out/t_gr.log
-timeout 900 python scripts/greedy_prune_probe.py > gpurun_out/gr.log 2>&1; echo "exit $?" >> gpurun_out/gr.log
+timeout 900 python scripts/setup_c2.py > gpurun_out/setup_c2.log 2>&1; echo "exit $?" >> gpurun_out/setup_c2.log
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/setup_launches.csv python scripts/setup_one.py > gpurun_out/setup_ncu.log 2>&1; echo "exit $?" >> gpurun_out/setup_ncu.log
