@@ -725,7 +725,16 @@ __global__ void cluster_mean_kernel(int64_t m, int len, const int32_t* __restric
   if (q >= len || j >= m) return;
   const int32_t lo = mem_ptr[j], hi = mem_ptr[j + 1];
   double s = 0.0;
-  for (int32_t c = lo; c < hi; ++c) s = __dadd_rn(s, mats[(int64_t)mem[c] * len + q]);
+  int32_t c = lo;
+  // 8 member loads in flight, then the in-order additions
+  for (; c + 8 <= hi; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = mats[(int64_t)__ldg(mem + c + u) * len + q];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; c < hi; ++c) s = __dadd_rn(s, mats[(int64_t)mem[c] * len + q]);
   const double inv = __ddiv_rn(1.0, (double)(hi - lo));
   reps[j * len + q] = __dmul_rn(s, inv);
 }
