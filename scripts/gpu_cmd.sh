@@ -1,2 +1,4 @@
-timeout 900 python scripts/setup_c2.py > gpurun_out/setup_c2.log 2>&1; echo "exit $?" >> gpurun_out/setup_c2.log
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/setup_launches.csv python scripts/setup_one.py > gpurun_out/setup_ncu.log 2>&1; echo "exit $?" >> gpurun_out/setup_ncu.log
+timeout 2400 python -m pytest tests/ -q -m gpu -x > gpurun_out/t_all.log 2>&1; echo "exit $?" >> gpurun_out/t_all.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "exit $?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "exit $?" >> gpurun_out/bench_ref.log
