@@ -46,6 +46,15 @@ void spmv(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col
           double* y, cudaStream_t s);
 // Deterministic sum of `count` partials -> out[0] = sqrt(sum) (sqrt_result) or sum.
 void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s);
+// y = A x with per-block partial sums of x_i y_i (plan.blocks partials; CG's (p, A p)).
+void spmv_dot(const SpmvPlan& plan, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
+              const double* x, double* y, double* partials, cudaStream_t s);
+// CG building blocks (kernels/blas.cu): dot_partials() partials each.
+void dot_partial(int64_t n, const double* a, const double* b, double* partials, cudaStream_t s);
+void cg_update(int64_t n, const double* alpha, const double* p, const double* q, const double* x_in, double* x_out,
+               double* r, double* partials, cudaStream_t s);  // x_out = x_in + a p, r -= a q, partials of r.r
+// !beta: out = num / sum(partials);  beta: out = sum / num, then num = sum.
+void finish_ratio(const double* partials, int count, double* num, double* out, bool beta, cudaStream_t s);
 
 // ---- sweep.cu : patch stage and scatter -----------------------------------
 // Per-patch gather + LU solve (column-major factors):

@@ -79,6 +79,58 @@ __global__ void scalar_div_kernel(const double* __restrict__ a, const double* __
   out[0] = a[0] / b[0];
 }
 
+// CG update fused with its residual norm: x_out = x_in + a p, r -= a q
+// (unfused, as the oracle's loops), partials[block] = sum of r^2 over the
+// block's fixed grid-stride share (kDotBlocks blocks: deterministic).
+__global__ void __launch_bounds__(kDotThreads) cg_update_kernel(int64_t n, const double* __restrict__ alpha,
+                                                                const double* __restrict__ p,
+                                                                const double* __restrict__ q,
+                                                                const double* __restrict__ x_in,
+                                                                double* __restrict__ x_out, double* __restrict__ r,
+                                                                double* __restrict__ partials) {
+  __shared__ double red[kDotThreads / 32];
+  const double a = alpha[0];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kDotThreads) {
+    x_out[i] = __dadd_rn(x_in[i], __dmul_rn(a, p[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(a, q[i]));
+    r[i] = ri;
+    s += ri * ri;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kDotThreads / 32; ++w) t += red[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
+// mode 0: out[0] = num[0] / sum (alpha);  mode 1: out[0] = sum / num[0], num[0] = sum (beta, rz <- rz_new)
+__global__ void finish_ratio_kernel(const double* __restrict__ partials, int count, double* num, double* out,
+                                    int mode) {
+  __shared__ double red[1024];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) t += partials[i];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double sum = red[0];
+    if (mode == 0) {
+      out[0] = num[0] / sum;
+    } else {
+      out[0] = sum / num[0];
+      num[0] = sum;
+    }
+  }
+}
+
 inline unsigned ew_grid(int64_t n) {
   const int64_t g = (n + 255) / 256;
   return (unsigned)(g < 4 * 148 * 8 ? (g > 0 ? g : 1) : 4 * 148 * 8);
@@ -213,6 +265,19 @@ bool mgs_fused(int64_t n, int j, const double* V, int64_t ldv, double* w, double
 }
 
 int dot_partials() { return kDotBlocks; }
+
+void dot_partial(int64_t n, const double* a, const double* b, double* partials, cudaStream_t s) {
+  dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, partials);
+}
+
+void cg_update(int64_t n, const double* alpha, const double* p, const double* q, const double* x_in, double* x_out,
+               double* r, double* partials, cudaStream_t s) {
+  cg_update_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, alpha, p, q, x_in, x_out, r, partials);
+}
+
+void finish_ratio(const double* partials, int count, double* num, double* out, bool beta, cudaStream_t s) {
+  finish_ratio_kernel<<<1, 1024, 0, s>>>(partials, count, num, out, beta ? 1 : 0);
+}
 
 void dot(int64_t n, const double* a, const double* b, double* partials, double* out, cudaStream_t s) {
   dot_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(n, a, b, partials);

@@ -31,7 +31,8 @@ __global__ void __launch_bounds__(kBlock) residual_v2_kernel(int64_t n, const in
                                                              const double* __restrict__ val,
                                                              const double* __restrict__ x,
                                                              const double* __restrict__ b, double* __restrict__ r,
-                                                             double* __restrict__ block_sumsq, bool negate_b_absent) {
+                                                             double* __restrict__ block_sumsq, bool negate_b_absent,
+                                                             const double* __restrict__ dotv) {
   const int lane = threadIdx.x % G;
   const int64_t row = (int64_t)blockIdx.x * (kBlock / G) + threadIdx.x / G;
   double acc = 0.0;
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kBlock) residual_v2_kernel(int64_t n, const in
   }
   if (block_sumsq) {
     __shared__ double red[kBlock / 32];
-    double sq = (lane == 0 && row < n) ? rv * rv : 0.0;
+    double sq = (lane == 0 && row < n) ? rv * (dotv ? dotv[row] : rv) : 0.0;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
     int nwarps, const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
     const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ r,
     const int32_t* __restrict__ wstart, const int64_t* __restrict__ wbase, double* __restrict__ block_sumsq,
-    bool negate_b_absent) {
+    bool negate_b_absent, const double* __restrict__ dotv) {
   constexpr int PER = kV5Per;
   __shared__ double prod[kV5Warps][32 * PER];
   __shared__ double red[kV5Warps];
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
         if (rr < nrows && g4 == 0) {
           const double rv = b ? brr - a : (negate_b_absent ? -a : a);
           r[r0 + rr] = rv;
-          sq += rv * rv;
+          sq += rv * (dotv ? dotv[r0 + rr] : rv);
         }
       }
     } else {  // one long row
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
       if (lane == 0) {
         const double rv = b ? b[r0] - a : (negate_b_absent ? -a : a);
         r[r0] = rv;
-        sq += rv * rv;
+        sq += rv * (dotv ? dotv[r0] : rv);
       }
     }
   }
@@ -178,7 +179,8 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
                                                             const int32_t* __restrict__ scol,
                                                             const double* __restrict__ x, const double* __restrict__ b,
                                                             double* __restrict__ r, double* __restrict__ block_sumsq,
-                                                            bool negate_b_absent, int pf) {
+                                                            bool negate_b_absent, int pf,
+                                                            const double* __restrict__ dotv) {
   __shared__ double red[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
     if (rl.x >= 0) {
       const double rv = b ? __dsub_rn(bl, acc) : (negate_b_absent ? -acc : acc);
       r[rl.x] = rv;
-      sq += rv * rv;
+      sq += rv * (dotv ? dotv[rl.x] : rv);
     }
   }
   if (block_sumsq) {
@@ -262,15 +264,16 @@ __global__ void finish_sum_kernel(const double* __restrict__ partials, int count
 
 template <int G>
 void launch_v2(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
-               const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+               const double* b, double* r, double* sumsq, bool negate, const double* dotv, cudaStream_t s) {
   if (p.entries == 4)
-    residual_v2_kernel<G, 4><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+    residual_v2_kernel<G, 4><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate, dotv);
   else
-    residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate);
+    residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate, dotv);
 }
 
 void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
-                       const double* x, const double* b, double* r, double* sumsq, bool negate, cudaStream_t s) {
+                       const double* x, const double* b, double* r, double* sumsq, bool negate, cudaStream_t s,
+                       const double* dotv = nullptr) {
   if (n <= 0) return;
   if (p.version == 9 && p.sell_off) {
     const int2* sr = reinterpret_cast<const int2*>(p.sell_row);
@@ -279,23 +282,23 @@ void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const in
     const int pf = pfe ? atoi(pfe) : 1;
     if (p.entries == 4)
       launch_pdl(residual_sell_kernel<4>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
-                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf);
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv);
     else
       launch_pdl(residual_sell_kernel<8>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
-                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf);
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv);
     return;
   }
   if (p.version == 5 && p.blk_start) {
     residual_v5_kernel<<<p.blocks, kV5Warps * 32, 0, s>>>(p.nblk, rp, col, val, x, b, r, p.blk_start, p.blk_base,
-                                                          sumsq, negate);
+                                                          sumsq, negate, dotv);
     return;
   }
   switch (p.group) {
-    case 2: launch_v2<2>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 4: launch_v2<4>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 8: launch_v2<8>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    case 16: launch_v2<16>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
-    default: launch_v2<32>(p, n, rp, col, val, x, b, r, sumsq, negate, s); break;
+    case 2: launch_v2<2>(p, n, rp, col, val, x, b, r, sumsq, negate, dotv, s); break;
+    case 4: launch_v2<4>(p, n, rp, col, val, x, b, r, sumsq, negate, dotv, s); break;
+    case 8: launch_v2<8>(p, n, rp, col, val, x, b, r, sumsq, negate, dotv, s); break;
+    case 16: launch_v2<16>(p, n, rp, col, val, x, b, r, sumsq, negate, dotv, s); break;
+    default: launch_v2<32>(p, n, rp, col, val, x, b, r, sumsq, negate, dotv, s); break;
   }
 }
 
@@ -353,7 +356,7 @@ void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x,
   if (s1 <= s0 || p.version != 9) return;
   const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
   residual_sell_kernel<8><<<grid_for(s1 - s0, 8), 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x,
-                                                               b, r, nullptr, true, 1);
+                                                               b, r, nullptr, true, 1, nullptr);
 }
 
 void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
@@ -363,6 +366,11 @@ void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, c
 
 void finish_sum(const double* partials, int count, double* out, bool sqrt_result, cudaStream_t s) {
   finish_sum_kernel<<<1, 1024, 0, s>>>(partials, count, out, sqrt_result);
+}
+
+void spmv_dot(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,
+              double* y, double* partials, cudaStream_t s) {
+  dispatch_residual(p, n, rp, col, val, x, nullptr, y, partials, false, s, x);
 }
 
 }  // namespace pdb::k

@@ -196,12 +196,16 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
   if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
   Ops ops(a, pc, s);
   const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
-  Scratch<double> b(un, s), x(un, s), r(un, s), z(un, s), p(un, s), q(un, s);
+  Scratch<double> b(un, s), r(un, s), z(un, s), p(un, s), q(un, s);
+  Scratch<double> xb[2] = {Scratch<double>(un, s), Scratch<double>(un, s)};  // x_k alternates buffers
+  const int nparts = std::max(ops.plan.blocks, k::dot_partials());
+  Scratch<double> part1(static_cast<size_t>(nparts), s), part2(static_cast<size_t>(nparts), s);
   b.upload(b_host, static_cast<size_t>(n));
-  x.zero();
+  xb[0].zero();
   PDB_CUDA(cudaMemcpyAsync(r.get(), b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
   rep = pdb_report_s();
   const double bnorm = ops.norm(b.get());
+  int xres = 0;  // buffer holding the returned iterate
   if (bnorm == 0.0) {
     rep.converged = true;
   } else {
@@ -210,38 +214,58 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
       if (pc) precond_apply_device(*pc, r.get(), z.get(), s, /*symmetric=*/true);
       else PDB_CUDA(cudaMemcpyAsync(z.get(), r.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     };
-    // device scalar slots
-    constexpr int RZ = 0, PQ = 1, ALPHA = 2, RR = 3, RZN = 4, BETA = 5;
+    // device scalar slots; RR + (k & 1): the residual norms of two consecutive iterations
+    constexpr int RZ = 0, ALPHA = 2, BETA = 5, RR = 6;
     double* sc = ops.scal.get();
+    static thread_local double* rr_host = nullptr;  // pinned, 2 slots
+    if (!rr_host) PDB_CUDA(cudaMallocHost(&rr_host, 2 * sizeof(double)));
+    cudaEvent_t ev[2];
+    for (auto& e : ev) PDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     precond();
     PDB_CUDA(cudaMemcpyAsync(p.get(), z.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    ops.dot_dev(r.get(), z.get(), RZ);
-    while (rep.iterations < max_iters) {
-      ops.spmv(p.get(), q.get());
-      ops.dot_dev(p.get(), q.get(), PQ);
-      k::scalar_div(sc + RZ, sc + PQ, sc + ALPHA, s);  // alpha = rz / (p, q)
-      k::axpy(n, sc + ALPHA, false, p.get(), x.get(), s);
-      k::axpy(n, sc + ALPHA, true, q.get(), r.get(), s);
-      ops.dot_dev(r.get(), r.get(), RR);
-      double rr = 0.0;
-      PDB_CUDA(cudaMemcpyAsync(&rr, sc + RR, sizeof(double), cudaMemcpyDeviceToHost, s));
-      sync(s);  // the iteration's only host synchronisation
+    k::dot_partial(n, r.get(), z.get(), part2.get(), s);
+    k::finish_sum(part2.get(), k::dot_partials(), sc + RZ, false, s);
+    // Iteration k: q = A p with (p, q) fused, alpha = rz / (p, q); x and r
+    // updated with r.r fused; ||r||^2 copied to the host slot k & 1; then the
+    // preconditioner, rz_new and p for iteration k + 1.  The host enqueues
+    // iteration k + 1 before it reads the norm of iteration k, so the GPU never
+    // waits for the convergence test; a converged solve returns x_{k+1}, kept
+    // in its own buffer while the speculative iteration writes the other.
+    auto enqueue = [&](int64_t k) {
+      k::spmv_dot(ops.plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), p.get(), q.get(), part1.get(), s);
+      k::finish_ratio(part1.get(), ops.plan.blocks, sc + RZ, sc + ALPHA, false, s);
+      k::cg_update(n, sc + ALPHA, p.get(), q.get(), xb[k & 1].get(), xb[(k + 1) & 1].get(), r.get(), part2.get(), s);
+      k::finish_sum(part2.get(), k::dot_partials(), sc + RR + (k & 1), false, s);
+      PDB_CUDA(cudaMemcpyAsync(rr_host + (k & 1), sc + RR + (k & 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+      PDB_CUDA(cudaEventRecord(ev[k & 1], s));
+      precond();
+      k::dot_partial(n, r.get(), z.get(), part1.get(), s);
+      k::finish_ratio(part1.get(), k::dot_partials(), sc + RZ, sc + BETA, true, s);  // beta = rz_new / rz; rz = rz_new
+      k::xpay(n, z.get(), sc + BETA, p.get(), s);
+    };
+    const char* la = getenv("PDB_PCG_LOOKAHEAD");
+    const bool lookahead = !(la && la[0] == '0');
+    int64_t enq = 0;
+    if (max_iters > 0) enqueue(enq++);
+    for (int64_t k = 0; k < enq; ++k) {
+      if (lookahead && enq < max_iters) enqueue(enq++);
+      PDB_CUDA(cudaEventSynchronize(ev[k & 1]));
+      const double rr = rr_host[k & 1];
       ++rep.iterations;
+      xres = static_cast<int>((k + 1) & 1);
       const double rel = std::sqrt(rr) / bnorm;
       rep.residual_history.push_back(rel);
       if (rel <= tol) {
         rep.converged = true;
         break;
       }
-      precond();
-      ops.dot_dev(r.get(), z.get(), RZN);
-      k::scalar_div(sc + RZN, sc + RZ, sc + BETA, s);  // beta = rz_new / rz
-      PDB_CUDA(cudaMemcpyAsync(sc + RZ, sc + RZN, sizeof(double), cudaMemcpyDeviceToDevice, s));
-      k::xpay(n, z.get(), sc + BETA, p.get(), s);
+      if (!lookahead && enq < max_iters) enqueue(enq++);
     }
+    sync(s);
+    for (auto& e : ev) cudaEventDestroy(e);
   }
   rep.final_relative_residual = rep.residual_history.empty() ? 0.0 : rep.residual_history.back();
-  x.download(x_host, static_cast<size_t>(n));
+  xb[xres].download(x_host, static_cast<size_t>(n));
   sync(s);
 }
 

@@ -1,4 +1,3 @@
-timeout 2400 python -m pytest tests/ -q -m gpu -x > gpurun_out/t_all.log 2>&1; echo "exit $?" >> gpurun_out/t_all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "exit $?" >> gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "exit $?" >> gpurun_out/bench.log
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "exit $?" >> gpurun_out/bench_ref.log
+timeout 900 python -m pytest tests/ -q -m gpu -k "pcg" > gpurun_out/t_pcg.log 2>&1; echo "exit $?" >> gpurun_out/t_pcg.log
+VARIANTS=exact,spectral timeout 900 python scripts/pcg_probe.py > gpurun_out/pcg.log 2>&1; echo "exit $?" >> gpurun_out/pcg.log
+PDB_PCG_LOOKAHEAD=0 VARIANTS=exact timeout 900 python scripts/pcg_probe.py > gpurun_out/pcg0.log 2>&1; echo "exit $?" >> gpurun_out/pcg0.log
