@@ -352,6 +352,59 @@ void relax_profile(const DeviceCsr& a, const pdb_precond_s& pc, const double* b,
   const k::SpmvPlan plan = plan_of(a);
   Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
   Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
+  if (const char* oe = getenv("PDB_PROFILE_OVERLAP"); oe && oe[0] == '1') {
+    // Probe: residual on a low-priority stream concurrently with an
+    // independent apply + scatter on a high-priority stream.  ms_phase =
+    // {overlapped, residual alone, apply + scatter alone} per sweep.
+    int lo = 0, hi = 0;
+    PDB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    cudaStream_t sl = nullptr, sh = nullptr;
+    PDB_CUDA(cudaStreamCreateWithPriority(&sl, cudaStreamNonBlocking, lo));
+    PDB_CUDA(cudaStreamCreateWithPriority(&sh, cudaStreamNonBlocking, hi));
+    Scratch<double> r2(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s), x2(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
+    PDB_CUDA(cudaMemcpyAsync(x2.get(), x, a.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r2.get(), nullptr, s);
+    cudaEvent_t t[6], j0, j1;
+    for (auto& e : t) PDB_CUDA(cudaEventCreate(&e));
+    PDB_CUDA(cudaEventCreateWithFlags(&j0, cudaEventDisableTiming));
+    PDB_CUDA(cudaEventCreateWithFlags(&j1, cudaEventDisableTiming));
+    PDB_CUDA(cudaEventRecord(j0, s));
+    PDB_CUDA(cudaStreamWaitEvent(sl, j0, 0));
+    PDB_CUDA(cudaEventRecord(t[0], sl));
+    for (int64_t sw = 0; sw < sweeps; ++sw)
+      k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), nullptr, sl);
+    PDB_CUDA(cudaEventRecord(t[1], sl));
+    for (int64_t sw = 0; sw < sweeps; ++sw) {
+      patch_stage(pc, r2.get(), nullptr, sols.get(), sl);
+      scatter_stage(pc, sols.get(), false, x2.get(), nullptr, x2.get(), sl);
+    }
+    PDB_CUDA(cudaEventRecord(t[2], sl));
+    for (int64_t sw = 0; sw < sweeps; ++sw) {
+      PDB_CUDA(cudaEventRecord(j0, sl));
+      PDB_CUDA(cudaStreamWaitEvent(sh, j0, 0));
+      k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), nullptr, sl);
+      patch_stage(pc, r2.get(), nullptr, sols.get(), sh);
+      scatter_stage(pc, sols.get(), false, x2.get(), nullptr, x2.get(), sh);
+      PDB_CUDA(cudaEventRecord(j1, sh));
+      PDB_CUDA(cudaStreamWaitEvent(sl, j1, 0));
+    }
+    PDB_CUDA(cudaEventRecord(t[3], sl));
+    PDB_CUDA(cudaStreamSynchronize(sl));
+    float m01 = 0.f, m12 = 0.f, m23 = 0.f;
+    PDB_CUDA(cudaEventElapsedTime(&m01, t[0], t[1]));
+    PDB_CUDA(cudaEventElapsedTime(&m12, t[1], t[2]));
+    PDB_CUDA(cudaEventElapsedTime(&m23, t[2], t[3]));
+    const double sw = static_cast<double>(std::max<int64_t>(sweeps, 1));
+    ms_phase[0] = m23 / sw;
+    ms_phase[1] = m01 / sw;
+    ms_phase[2] = m12 / sw;
+    for (auto& e : t) cudaEventDestroy(e);
+    cudaEventDestroy(j0);
+    cudaEventDestroy(j1);
+    cudaStreamDestroy(sl);
+    cudaStreamDestroy(sh);
+    return;
+  }
   std::vector<cudaEvent_t> ev(static_cast<size_t>(4 * std::max<int64_t>(sweeps, 1)));
   const char* he = getenv("PDB_PROFILE_HOT");
   const bool hot = he && he[0] == '1';
