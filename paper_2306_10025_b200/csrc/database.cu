@@ -428,7 +428,56 @@ struct AssignSlot {
   DevBuf<double> sub_il;
   DevBuf<double> dist, lbq;  // pruned spectral assignment: distances / quotient bounds kept across iterations
   int64_t m = 0;             // columns of dist / lbq
+  DevBuf<double> sub_sorted;  // bound pass: the slot's patches interleaved in work order
+  DevBuf<int32_t> perm, itc;  // work order; power iterations of each patch's last bound pair
 };
+
+// Work order of the bound pass (one pair per thread, aligned groups of 32 =
+// one warp): patches whose centroid changed, sorted by centroid (the lanes of
+// a warp share the factor: broadcast loads) and by the power iterations their
+// previous bound pair took, descending (lanes of a warp finish together); the
+// groups of 32 then run longest first (a short tail), and the patches whose
+// centroid did not change (their distance is reused) come last.  The sorted
+// interleaved copy makes every patch load of a warp one 256-byte span.
+void diag_order(int64_t cnt, int64_t m, const std::vector<int32_t>& cur, const std::vector<uint8_t>& chg, int64_t len,
+                const double* sub, AssignSlot& sl, cudaStream_t s) {
+  if (sl.perm.size() < static_cast<size_t>(cnt)) {
+    sl.perm.alloc(static_cast<size_t>(cnt));
+    sl.itc.alloc(static_cast<size_t>(cnt));
+    sl.itc.zero(s);
+    sl.sub_sorted.alloc(static_cast<size_t>(k::interleaved_len(cnt, 32, len)));
+  }
+  const std::vector<int32_t> prev = d2h(sl.itc.get(), static_cast<size_t>(cnt), s);
+  std::vector<int32_t> live, idle;
+  for (int64_t i = 0; i < cnt; ++i) {
+    const int32_t f = cur[static_cast<size_t>(i)];
+    const bool c = f < 0 || f >= m || static_cast<size_t>(f) >= chg.size() || chg[static_cast<size_t>(f)];
+    (c ? live : idle).push_back(static_cast<int32_t>(i));
+  }
+  std::sort(live.begin(), live.end(), [&](int32_t a, int32_t b) {
+    const int32_t fa = cur[static_cast<size_t>(a)], fb = cur[static_cast<size_t>(b)];
+    if (fa != fb) return fa < fb;
+    const int32_t ia = prev[static_cast<size_t>(a)], ib = prev[static_cast<size_t>(b)];
+    if (ia != ib) return ia > ib;
+    return a < b;
+  });
+  const size_t full = live.size() / 32;  // whole groups; the partial one stays last (alignment)
+  std::vector<std::pair<int32_t, size_t>> grp(full);
+  for (size_t g = 0; g < full; ++g) {
+    int32_t mx = 0;
+    for (size_t a = 0; a < 32; ++a) mx = std::max(mx, prev[static_cast<size_t>(live[g * 32 + a])]);
+    grp[g] = {mx, g};
+  }
+  std::stable_sort(grp.begin(), grp.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+  std::vector<int32_t> perm;
+  perm.reserve(static_cast<size_t>(cnt));
+  for (const auto& gg : grp) perm.insert(perm.end(), live.begin() + static_cast<long>(gg.second * 32),
+                                         live.begin() + static_cast<long>(gg.second * 32 + 32));
+  perm.insert(perm.end(), live.begin() + static_cast<long>(full * 32), live.end());
+  perm.insert(perm.end(), idle.begin(), idle.end());
+  h2d(sl.perm.get(), perm, s);
+  k::interleave_patches_perm(cnt, len, sl.perm.get(), sub, sl.sub_sorted.get(), s);
+}
 
 void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max_iters, Empty policy,
                  std::vector<int32_t>& phi_h, PatchFactors& pf, BuildWork& work, cudaStream_t s,
@@ -475,6 +524,9 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   // cut short.  PDB_KMEANS_PRUNE=0 evaluates every pair to convergence.
   const char* pr_env = getenv("PDB_KMEANS_PRUNE");
   const bool prune = il && !(pr_env && pr_env[0] == '0');
+  const char* ds_env = getenv("PDB_DIAG_SORT");  // 0: bound pass in patch order with in-block refill
+  const bool diag_sort = !(ds_env && ds_env[0] == '0');
+  std::vector<uint8_t> chg_h;  // host copy of d_chg
   DevBuf<double> ub;
   DevBuf<int32_t> guess;  // iteration 0: l1-nearest entry, for the first bound
   DevBuf<double> gmin;
@@ -526,13 +578,25 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
           std::vector<uint8_t> ones(static_cast<size_t>(m), 1);
           d_chg.alloc(static_cast<size_t>(m));
           h2d(d_chg.get(), ones, s);
+          chg_h = ones;
         }
         if (pr) {
           ru.chg = d_chg.get();
           ru.dprev = dd;
           ru.mfull = m;
-          k::spectral_diag_il(cnt, ps, sl.sub_il.get(), db.lu.get(), db.piv.get(), cur_phi, ub.get() + sl.lo,
-                              iters.get(), s, ru);
+          const double* diag_mats = sl.sub_il.get();
+          const int32_t* dperm = nullptr;
+          if (diag_sort) {
+            diag_order(cnt, m, iter == 0 ? d2h(cur_phi, static_cast<size_t>(cnt), s)
+                                         : std::vector<int32_t>(phi_h.begin() + sl.lo, phi_h.begin() + sl.hi),
+                       chg_h, len, sub + sl.lo * len, sl, s);
+            diag_mats = sl.sub_sorted.get();
+            dperm = sl.perm.get();
+            ru.it_out = sl.itc.get();
+          }
+          k::spectral_diag_il(cnt, ps, diag_mats, db.lu.get(), db.piv.get(), cur_phi, ub.get() + sl.lo,
+                              iters.get(), s, ru, dperm);
+          ru.it_out = nullptr;
           work.pair_evals += cnt;
           ru.ub = ub.get() + sl.lo;
           ru.phi = cur_phi;
@@ -631,6 +695,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
           chg[static_cast<size_t>(j)] = members[static_cast<size_t>(j)] != prev_members[static_cast<size_t>(j)];
       d_chg.alloc(static_cast<size_t>(std::max<int64_t>(mc, 1)));
       h2d(d_chg.get(), chg, s);
+      chg_h = chg;
       prev_members = members;
     }
 

@@ -166,14 +166,21 @@ struct KmeansReuse {
   double* lbq = nullptr;
   const double* dprev = nullptr;
   int64_t mfull = 0;
+  int32_t* it_out = nullptr;  // DIAG: power iterations each patch's pair took
 };
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
                        const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s,
                        KmeansReuse ru = KmeansReuse{});
-// d[t] = dist(patch t, factor phi[t]) for interleaved patches and plain-layout factors.
+// d[t] = dist(patch t, factor phi[t]) for interleaved patches and plain-layout factors;
+// with perm, mats_il holds patches perm[0..npat) in that order, one pair per thread
+// (d, phi, dprev, it_out stay indexed by patch).
 void spectral_diag_il(int64_t npat, int ps, const double* mats_il, const double* lu, const int32_t* piv,
                       const int32_t* phi, double* d, unsigned long long* iters, cudaStream_t s,
-                      KmeansReuse ru = KmeansReuse{});
+                      KmeansReuse ru = KmeansReuse{}, const int32_t* perm = nullptr);
+// Interleaved (width 32) copy of patches perm[0..count) of the plain layout src
+// (the sorted copy for spectral_diag_il's perm).
+void interleave_patches_perm(int64_t count, int64_t len, const int32_t* perm, const double* src, double* dst,
+                             cudaStream_t s);
 // Spectral distance of listed (patch, factor) pairs: d[t] = dist(mats[pa[t]], factor fb[t]).
 void spectral_list(int64_t npairs, const int32_t* pa, const int32_t* fb, int ps, const double* mats, const double* lu,
                    const int32_t* piv, double* d, unsigned long long* iters, cudaStream_t s);

@@ -419,7 +419,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   double* vec = sm;  // 3 * PS * BD: v, w, t
   __shared__ int counter;
   const int tid = threadIdx.x;
-  constexpr int TA = DIAG ? 2 * kTileThreads : kTileA;  // DIAG: 128 patches pulled by 64 threads
+  // DIAG: 128 patches pulled by 64 threads; sorted DIAG (pid): 64, one per thread
+  const int TA = DIAG ? (pid ? kTileThreads : 2 * kTileThreads) : kTileA;
   const int64_t a0 = (int64_t)blockIdx.x * TA, e0 = (int64_t)blockIdx.y * kTileE;
   const int na = (int)(npat - a0 < TA ? npat - a0 : TA);
   // pruned k-means assignment (IL, bound given): one block takes every factor
@@ -437,6 +438,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   const int npairs = DIAG ? na : na * nev;
   bool active = false;
   int it = 0, pa = 0, pe = 0;
+  int64_t gcur = 0;
+  bool pulled = false;
   double lambda = 0.0;
   const double* A = mats;
   const double* L = LUs;
@@ -444,12 +447,24 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   unsigned long long my_iters = 0;
   for (;;) {
     while (!active) {
-      const int p = atomicAdd(&counter, 1);
+      // DIAG with pid (sorted copy): thread t keeps pair t -- the lanes of a
+      // warp stay on one aligned group of 32 patches (coalesced patch loads)
+      // that mostly share a centroid (broadcast factor loads); no refill
+      int p;
+      if (DIAG && pid) {
+        p = pulled ? npairs : tid;
+        pulled = true;
+      } else {
+        p = atomicAdd(&counter, 1);
+      }
       if (p >= npairs) break;
       {
         pa = p % na;
         pe = p / na;
-        const int64_t g = a0 + pa;
+        // DIAG with pid: position a0 + pa of a centroid-sorted copy of the
+        // patches; g is the patch's own index for d / dprev / phi
+        const int64_t g = (DIAG && pid) ? (int64_t)pid[a0 + pa] : a0 + pa;
+        gcur = g;
         if (ru.chg != nullptr) {  // reuse across Lloyd iterations
           if (DIAG) {
             const int32_t f = diag_phi[g];
@@ -468,7 +483,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
         }
         active = true;
         if (DIAG) {
-          A = mats + (g / kTileA) * LEN * kTileA + g % kTileA;
+          const int64_t q = a0 + pa;
+          A = mats + (q / kTileA) * LEN * kTileA + q % kTileA;
           L = lu + (int64_t)diag_phi[g] * LEN;
           P = piv + (int64_t)diag_phi[g] * PS;
         } else if (IL) {
@@ -602,7 +618,8 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
       }
     }
     if (done) {
-      d[DIAG ? a0 + pa : (a0 + pa) * ne + e0 + pe] = result;
+      d[DIAG ? gcur : (a0 + pa) * ne + e0 + pe] = result;
+      if (DIAG && ru.it_out) ru.it_out[gcur] = it;
       my_iters += (unsigned long long)it;
       active = false;
     }
@@ -772,25 +789,44 @@ void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, 
 
 template <int PS>
 void launch_spectral_diag(int64_t npat, const double* mats_il, const double* lu, const int32_t* piv, const int32_t* phi,
-                          double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru) {
+                          double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru, const int32_t* perm) {
   const size_t smem = (size_t)3 * PS * kTileThreads * sizeof(double);
   cudaFuncSetAttribute(spectral_tile_kernel<PS, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   ru.ub = nullptr;
   ru.lbq = nullptr;
-  spectral_tile_kernel<PS, true, true><<<grid_for(npat, 2 * kTileThreads), kTileThreads, smem, s>>>(
-      npat, nullptr, 1, mats_il, lu, piv, d, iters, ru, phi);
+  spectral_tile_kernel<PS, true, true>
+      <<<grid_for(npat, perm ? kTileThreads : 2 * kTileThreads), kTileThreads, smem, s>>>(npat, perm, 1, mats_il, lu,
+                                                                                         piv, d, iters, ru, phi);
 }
 
 void spectral_diag_il(int64_t npat, int ps, const double* mats_il, const double* lu, const int32_t* piv,
-                      const int32_t* phi, double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru) {
+                      const int32_t* phi, double* d, unsigned long long* iters, cudaStream_t s, KmeansReuse ru,
+                      const int32_t* perm) {
   if (npat <= 0) return;
   switch (ps) {
-    case 9: launch_spectral_diag<9>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
-    case 22: launch_spectral_diag<22>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
-    case 25: launch_spectral_diag<25>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
-    case 27: launch_spectral_diag<27>(npat, mats_il, lu, piv, phi, d, iters, s, ru); break;
+    case 9: launch_spectral_diag<9>(npat, mats_il, lu, piv, phi, d, iters, s, ru, perm); break;
+    case 22: launch_spectral_diag<22>(npat, mats_il, lu, piv, phi, d, iters, s, ru, perm); break;
+    case 25: launch_spectral_diag<25>(npat, mats_il, lu, piv, phi, d, iters, s, ru, perm); break;
+    case 27: launch_spectral_diag<27>(npat, mats_il, lu, piv, phi, d, iters, s, ru, perm); break;
     default: break;
   }
+}
+
+// dst = the interleaved (width kTileA) copy of items perm[0..count) of src
+__global__ void interleave_perm_kernel(int64_t total, int64_t count, int64_t len, const int32_t* __restrict__ perm,
+                                       const double* __restrict__ src, double* __restrict__ dst) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int a = (int)(e % kTileA);
+  const int64_t q = (e / kTileA) % len, g = e / (kTileA * len);
+  const int64_t item = g * kTileA + a;
+  dst[e] = item < count ? src[(int64_t)__ldg(perm + item) * len + q] : 0.0;
+}
+
+void interleave_patches_perm(int64_t count, int64_t len, const int32_t* perm, const double* src, double* dst,
+                             cudaStream_t s) {
+  const int64_t total = interleaved_len(count, kTileA, len);
+  if (total > 0) interleave_perm_kernel<<<grid_for(total, 256), 256, 0, s>>>(total, count, len, perm, src, dst);
 }
 
 void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,

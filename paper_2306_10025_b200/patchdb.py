@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpatchdb.so.0")
+LIB_PATH = os.environ.get("PDB_LIB_PATH") or os.path.join(_HERE, "lib", "libpatchdb.so.0")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -374,6 +374,13 @@ def test_kmeans_assignment_pruning_changes_nothing(P, cfg, cells, ps, k, method,
     for a, b in zip(on.factors(), off.factors()):
         assert np.array_equal(a, b)
     assert on.work()["power_iters"] <= off.work()["power_iters"]  # executed power iterations
+    # the bound pass in patch order (in-block refill) instead of the sorted work order
+    monkeypatch.setenv("PDB_KMEANS_PRUNE", "1")
+    monkeypatch.setenv("PDB_DIAG_SORT", "0")
+    plain = P.Database.build(A, pset, getattr(P, method), **kw)
+    assert np.array_equal(on.phi(), plain.phi())
+    assert np.array_equal(on.representatives(), plain.representatives())
+    assert on.work()["power_iters"] == plain.work()["power_iters"]
 
 
 @pytest.mark.parametrize("best_match", [False, True])
