@@ -5,7 +5,10 @@
 // (capi.cpp).  CUDA failures become Errc::internal.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -155,6 +158,36 @@ class Scratch {
 
 inline cudaStream_t default_stream() { return cudaStreamPerThread; }
 inline void sync(cudaStream_t s) { PDB_CUDA(cudaStreamSynchronize(s)); }
+
+// PDB_TRACE=1: wall time of a scope, stream-synchronised at both ends, on stderr.
+class TraceScope {
+ public:
+  TraceScope(const char* name, cudaStream_t s) : name_(name), s_(s) {
+    static const bool on = [] {
+      const char* e = std::getenv("PDB_TRACE");
+      return e && e[0] == '1';
+    }();
+    on_ = on;
+    if (on_) {
+      cudaStreamSynchronize(s_);
+      t0_ = std::chrono::steady_clock::now();
+    }
+  }
+  ~TraceScope() {
+    if (!on_) return;
+    cudaStreamSynchronize(s_);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
+    std::fprintf(stderr, "[trace] %s %.2f ms\n", name_, ms);
+  }
+  TraceScope(const TraceScope&) = delete;
+  TraceScope& operator=(const TraceScope&) = delete;
+
+ private:
+  const char* name_;
+  cudaStream_t s_;
+  bool on_ = false;
+  std::chrono::steady_clock::time_point t0_;
+};
 
 int num_sms();
 

@@ -8,6 +8,7 @@
 // therefore identical to the reference's: phi is bit-exact.
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <fstream>
 #include <limits>
@@ -454,12 +455,21 @@ void diag_order(int64_t cnt, int64_t m, const std::vector<int32_t>& cur, const s
     const bool c = f < 0 || f >= m || static_cast<size_t>(f) >= chg.size() || chg[static_cast<size_t>(f)];
     (c ? live : idle).push_back(static_cast<int32_t>(i));
   }
-  std::sort(live.begin(), live.end(), [&](int32_t a, int32_t b) {
-    const int32_t fa = cur[static_cast<size_t>(a)], fb = cur[static_cast<size_t>(b)];
-    if (fa != fb) return fa < fb;
-    const int32_t ia = prev[static_cast<size_t>(a)], ib = prev[static_cast<size_t>(b)];
-    if (ia != ib) return ia > ib;
-    return a < b;
+  // two stable counting sorts (O(n) per Lloyd iteration): iterations descending, then centroid
+  auto counting = [](std::vector<int32_t>& v, int64_t nkeys, auto key) {
+    std::vector<int32_t> start(static_cast<size_t>(nkeys + 1), 0), out(v.size());
+    for (int32_t i : v) ++start[static_cast<size_t>(key(i) + 1)];
+    for (int64_t k = 0; k < nkeys; ++k) start[static_cast<size_t>(k + 1)] += start[static_cast<size_t>(k)];
+    for (int32_t i : v) out[static_cast<size_t>(start[static_cast<size_t>(key(i))]++)] = i;
+    v.swap(out);
+  };
+  constexpr int32_t kMaxIt = 200;  // the power iteration's cap (dense.cpp:169)
+  counting(live, kMaxIt + 1, [&](int32_t i) {
+    return kMaxIt - std::min(std::max(prev[static_cast<size_t>(i)], 0), kMaxIt);
+  });
+  counting(live, m, [&](int32_t i) {
+    const int32_t f = cur[static_cast<size_t>(i)];
+    return (f >= 0 && f < m) ? f : 0;
   });
   const size_t full = live.size() / 32;  // whole groups; the partial one stays last (alignment)
   std::vector<std::pair<int32_t, size_t>> grp(full);
@@ -534,8 +544,21 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   DevBuf<uint8_t> d_chg;  // per entry: centroid changed since the previous assignment
   std::vector<std::vector<int32_t>> prev_members;
   if (prune) ub.alloc(cap);
+  // PDB_KMEANS_TRACE=1: wall time per phase on stderr (assignment incl. its
+  // device time / host update / means + LU)
+  const char* tr_env = getenv("PDB_KMEANS_TRACE");
+  const bool trace = tr_env && tr_env[0] == '1';
+  double tr[3] = {0, 0, 0};
+  auto tnow = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  double tmark = tnow();
   for (int iter = 0; iter < max_iters; ++iter) {
     const int64_t m = db.m;
+    if (trace) {
+      sync(s);
+      const double t = tnow();
+      tr[2] += t - tmark;
+      tmark = t;
+    }
     PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
     if (variant != Variant::Entrywise && il) {
       lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
@@ -623,6 +646,11 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
     work.pair_evals += n * m;
     const std::vector<int32_t> prev = phi_h;
     phi_h = d2h(d_new.get(), static_cast<size_t>(n), s);
+    if (trace) {
+      const double t = tnow();
+      tr[0] += t - tmark;
+      tmark = t;
+    }
     const bool ch = prev != phi_h;  // every rank sees the gathered assignment
     if (!ch) break;
     min_dist = d2h(d_min.get(), static_cast<size_t>(n), s);
@@ -699,6 +727,11 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       prev_members = members;
     }
 
+    if (trace) {
+      const double t = tnow();
+      tr[1] += t - tmark;
+      tmark = t;
+    }
     // representative update (compress.cpp:219-261); failures re-raised as
     // singular_matrix "cluster j: ..." for the lowest failing j.
     const int64_t mc = db.m;
@@ -787,6 +820,10 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       sync(s);
     }
   }
+  if (trace)
+    fprintf(stderr, "[kmeans] n=%lld m=%lld assign %.1f ms, host update %.1f ms, means+LU %.1f ms\n",
+            static_cast<long long>(n), static_cast<long long>(db.m), tr[0] * 1e3, tr[1] * 1e3,
+            (tr[2] + tnow() - tmark) * 1e3);
   if (sharded)  // every rank reports the whole job's power iterations
     PDB_NCCL_DB(ncclAllReduce(iters.get(), iters.get(), 1, ncclUint64, ncclSum, comm->comm, s));
   unsigned long long it_h = 0;
@@ -853,8 +890,12 @@ void kmeans_group(const double* sub, int64_t n, int ps, int64_t m_p, Variant var
     std::fill(db.has_factor.begin(), db.has_factor.end(), 1);
   }
   PatchFactors pf;
-  kmeans_loop(sub, n, db, variant, max_iters, Empty::Reseed, phi_h, pf, work, s,
-              variant == Variant::VarMin ? nullptr : comm);
+  {
+    TraceScope tk("kmeans_loop", s);
+    kmeans_loop(sub, n, db, variant, max_iters, Empty::Reseed, phi_h, pf, work, s,
+                variant == Variant::VarMin ? nullptr : comm);
+  }
+  TraceScope tf("finalize_factors", s);
   finalize_factors(db, work, s);
 }
 
@@ -945,7 +986,10 @@ void partitioned_build(const DevBuf<double>& mats, int64_t np, int ps, int64_t m
   const int64_t len = static_cast<int64_t>(ps) * ps;
   std::vector<std::vector<int32_t>> groups;
   std::vector<std::vector<uint8_t>> patterns;
-  boundary_partition(mats, np, ps, groups, patterns, s);
+  {
+    TraceScope tb("boundary_partition", s);
+    boundary_partition(mats, np, ps, groups, patterns, s);
+  }
   std::vector<int64_t> sizes;
   for (const auto& g : groups) sizes.push_back(static_cast<int64_t>(g.size()));
   const std::vector<int64_t> alloc = split_budget(m_p, sizes);
@@ -955,6 +999,7 @@ void partitioned_build(const DevBuf<double>& mats, int64_t np, int ps, int64_t m
   DevBuf<double> sub;
   for (size_t g = 0; g < groups.size(); ++g) {
     const int64_t cnt = static_cast<int64_t>(groups[g].size());
+    TraceScope tg("partition (gather + kmeans_group)", s);
     sub.alloc(static_cast<size_t>(cnt * len));
     Scratch<int32_t> ids(static_cast<size_t>(cnt), s);
     h2d(ids.get(), groups[g], s);
@@ -1048,8 +1093,12 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
 bool build_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, pdb_database_s& out,
                     cudaStream_t s) {
   require_device();
+  TraceScope tr("build_database", s);
   DevBuf<double> mats;
-  extract_patches(a, ps, mats, s);
+  {
+    TraceScope te("extract_patches", s);
+    extract_patches(a, ps, mats, s);
+  }
   return build_database_from_mats(mats, ps.np, ps.ps, p, out, s);
 }
 
