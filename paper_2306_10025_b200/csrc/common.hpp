@@ -90,13 +90,36 @@ class DevBuf {
   void alloc(std::size_t n) {
     reset();
     if (n == 0) return;
-    PDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    if (pooled()) {
+      // the device's stream-ordered pool (kept, not returned to the driver:
+      // require_device sets the release threshold), synchronised so the
+      // buffer is usable from any stream at once
+      PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), cudaStreamPerThread));
+      PDB_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
+    } else {
+      PDB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p_), n * sizeof(T)));
+    }
     n_ = n;
   }
   void reset() {
-    if (p_) cudaFree(p_);
+    if (p_) {
+      if (pooled()) {
+        cudaDeviceSynchronize();  // what cudaFree implies: no stream may still use the buffer
+        cudaFreeAsync(p_, cudaStreamPerThread);
+      } else {
+        cudaFree(p_);
+      }
+    }
     p_ = nullptr;
     n_ = 0;
+  }
+  // PDB_DEVBUF_POOL=0: plain cudaMalloc / cudaFree
+  static bool pooled() {
+    static const bool on = [] {
+      const char* e = std::getenv("PDB_DEVBUF_POOL");
+      return !(e && e[0] == '0');
+    }();
+    return on;
   }
   T* get() const { return p_; }
   std::size_t size() const { return n_; }
