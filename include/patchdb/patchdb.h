@@ -233,6 +233,12 @@ PDB_API pdb_status pdb_relax_device(pdb_matrix m, pdb_precond pc, const double* 
  * solve and the scatter/update kernels (roofline accounting in bench.py). */
 PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double* d_b, double* d_x, int64_t sweeps,
                                      double* ms_phase, void* stream);
+/* Residual storage of a matrix (its SELL-C-sigma copy): out[0] = column-
+ * pattern classes (0: explicit column indices), out[1] = column indices
+ * stored, out[2] = slices, out[3] = values stored (padding included).  All
+ * zero without a SELL copy.  (No reference counterpart: bench.py's roofline
+ * accounting.) */
+PDB_API pdb_status pdb_matrix_sell_info(pdb_matrix m, int64_t* out4);
 /* Sweep-structure sizes: stored factors (n_p exact, m_p compressed), patches, patch size. */
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc);
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc);

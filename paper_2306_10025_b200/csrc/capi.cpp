@@ -587,6 +587,18 @@ PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double*
   });
 }
 
+PDB_API pdb_status pdb_matrix_sell_info(pdb_matrix m, int64_t* out4) {
+  if (m == nullptr || out4 == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const DeviceCsr& a = m->a;
+    const bool sell = a.nslices > 0;
+    out4[0] = sell ? a.sell_classes : 0;
+    out4[1] = sell && a.sell_classes == 0 ? static_cast<int64_t>(a.sell_col.size()) : 0;
+    out4[2] = a.nslices;
+    out4[3] = sell ? static_cast<int64_t>(a.sell_val.size()) : 0;
+  });
+}
+
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc) { return pc == nullptr ? 0 : pc->nf; }
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc) { return pc == nullptr ? 0 : pc->np; }
 PDB_API int64_t pdb_precond_patch_size(pdb_precond pc) { return pc == nullptr ? 0 : pc->ps; }

@@ -28,6 +28,9 @@ struct SpmvPlan {
   const double* sell_val = nullptr;
   const int32_t* sell_col = nullptr;
   int64_t nslices = 0;
+  // all rows in column-pattern classes (see DeviceCsr): no column stream
+  const int32_t* sell_tab = nullptr;
+  const int32_t* sell_tstart = nullptr;
 };
 constexpr int kSellC = 32;          // rows per SELL slice (one warp)
 constexpr int kSellSigma = 8192;    // sorting window (rows)

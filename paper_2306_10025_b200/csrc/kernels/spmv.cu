@@ -172,7 +172,11 @@ __global__ void __launch_bounds__(kV5Warps * 32) residual_v5_kernel(
 // (sparse.cpp:50-63, precond.cpp:95-97).  The explicit minimum of 1 block
 // per SM lets ptxas keep the next step group's loads in flight (72 registers
 // at U = 8; without it the allocation drops to 48 and the kernel loses ~4 %).
-template <int U>
+// CLS: every row of the matrix is in a column-pattern class (build_sell):
+// srow.y = length | (class + 1) << 16 and the columns of a row are
+// row + tab[tstart[class] + j] -- no column stream (8 instead of 12 bytes per
+// nonzero); same per-row summation order, so still bitwise.
+template <int U, bool CLS = false>
 __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, const int64_t* __restrict__ soff,
                                                             const int2* __restrict__ srow,
                                                             const double* __restrict__ sval,
@@ -180,7 +184,9 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
                                                             const double* __restrict__ x, const double* __restrict__ b,
                                                             double* __restrict__ r, double* __restrict__ block_sumsq,
                                                             bool negate_b_absent, int pf,
-                                                            const double* __restrict__ dotv) {
+                                                            const double* __restrict__ dotv,
+                                                            const int32_t* __restrict__ tab = nullptr,
+                                                            const int32_t* __restrict__ tstart = nullptr) {
   __shared__ double red[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
@@ -191,17 +197,17 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
   }
   if (sl < nslices) {
     const int2 rl = __ldg(srow + sl * 32 + lane);
-    const int len = rl.y;
+    const int len = CLS ? (rl.y & 0xFFFF) : rl.y;
     const int L = __reduce_max_sync(0xffffffffu, (unsigned)len);
     const int64_t o = __ldg(soff + sl);
     const double* vp = sval + o + lane;
-    const int32_t* cp = scol + o + lane;
+    const int32_t* cp = CLS ? tab + (rl.x >= 0 ? __ldg(tstart + (rl.y >> 16) - 1) : 0) : scol + o + lane;
     const double bl = (rl.x >= 0 && b) ? __ldcs(b + rl.x) : 0.0;
     double acc = 0.0;
     int32_t c[U];
     double v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = u < len ? __ldcs(cp + (int64_t)u * 32) : 0;
+    for (int u = 0; u < U; ++u) c[u] = u < len ? (CLS ? rl.x + __ldg(cp + u) : __ldcs(cp + (int64_t)u * 32)) : 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = u < len ? __ldcs(vp + (int64_t)u * 32) : 0.0;
     grid_dep_wait();  // x is the predecessor's (the scatter's) output
@@ -213,13 +219,15 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
           const int cnt = (L - jn < U ? L - jn : U) * 32;
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + o + (int64_t)jn * 32),
                        "r"((unsigned)(cnt * 8)));
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + o + (int64_t)jn * 32),
-                       "r"((unsigned)(cnt * 4)));
+          if (!CLS)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + o + (int64_t)jn * 32),
+                         "r"((unsigned)(cnt * 4)));
         }
       }
       if (j > 0) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) c[u] = j + u < len ? __ldcs(cp + (int64_t)(j + u) * 32) : 0;
+        for (int u = 0; u < U; ++u)
+          c[u] = j + u < len ? (CLS ? rl.x + __ldg(cp + j + u) : __ldcs(cp + (int64_t)(j + u) * 32)) : 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = j + u < len ? __ldcs(vp + (int64_t)(j + u) * 32) : 0.0;
       }
@@ -280,12 +288,20 @@ void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const in
     // L2 bulk prefetch one step group ahead (PDB_SELL_PF; measured best at 1)
     const char* pfe = getenv("PDB_SELL_PF");
     const int pf = pfe ? atoi(pfe) : 1;
-    if (p.entries == 4)
+    if (p.sell_tab) {
+      const char* ue = getenv("PDB_SELL_CLS_U");
+      if (ue && atoi(ue) == 16)
+        launch_pdl(residual_sell_kernel<16, true>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off,
+                   sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, p.sell_tab, p.sell_tstart);
+      else
+        launch_pdl(residual_sell_kernel<8, true>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off,
+                   sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, p.sell_tab, p.sell_tstart);
+    } else if (p.entries == 4)
       launch_pdl(residual_sell_kernel<4>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
-                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv);
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, nullptr, nullptr);
     else
       launch_pdl(residual_sell_kernel<8>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
-                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv);
+                 p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, nullptr, nullptr);
     return;
   }
   if (p.version == 5 && p.blk_start) {
@@ -355,8 +371,13 @@ void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x,
                      cudaStream_t s) {
   if (s1 <= s0 || p.version != 9) return;
   const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
-  residual_sell_kernel<8><<<grid_for(s1 - s0, 8), 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x,
-                                                               b, r, nullptr, true, 1, nullptr);
+  if (p.sell_tab)
+    residual_sell_kernel<8, true><<<grid_for(s1 - s0, 8), 256, 0, s>>>(
+        s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x, b, r, nullptr, true, 1, nullptr, p.sell_tab,
+        p.sell_tstart);
+  else
+    residual_sell_kernel<8><<<grid_for(s1 - s0, 8), 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col,
+                                                                 x, b, r, nullptr, true, 1, nullptr);
 }
 
 void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,

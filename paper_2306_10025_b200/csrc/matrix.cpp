@@ -8,6 +8,7 @@
 #include <fstream>
 #include <sstream>
 #include <thread>
+#include <unordered_map>
 
 #include "host.hpp"
 #include "kernels.hpp"
@@ -81,10 +82,73 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
       });
     for (auto& th : pool) th.join();
   };
+  // ---- column-pattern classes: used only when every row falls into one
+  // (PDB_SELL_CLASSES=0 disables them)
+  std::vector<int32_t> cls(static_cast<size_t>(n), -1), tab, tstart(1, 0);
+  bool classed = false;
+  {
+    int64_t max_len = 0;
+    for (int64_t i = 0; i < n; ++i) max_len = std::max<int64_t>(max_len, len(i));
+    const char* ce = getenv("PDB_SELL_CLASSES");
+    if (!(ce && ce[0] == '0') && max_len <= 0xFFFF) {
+      std::vector<uint64_t> hash(static_cast<size_t>(n));
+      par([&](int64_t w) {
+        const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
+        for (int64_t i = r0; i < r1; ++i) {
+          uint64_t x = 1469598103934665603ull ^ static_cast<uint64_t>(len(i));
+          for (int64_t p = h.row_ptr[static_cast<size_t>(i)]; p < h.row_ptr[static_cast<size_t>(i + 1)]; ++p) {
+            x ^= static_cast<uint64_t>(static_cast<uint32_t>(h.col[static_cast<size_t>(p)] - static_cast<int32_t>(i)));
+            x *= 1099511628211ull;
+          }
+          hash[static_cast<size_t>(i)] = x;
+        }
+      });
+      auto same = [&](int64_t a, int64_t b) {
+        const int64_t la = len(a);
+        if (la != len(b)) return false;
+        const int32_t* ca = h.col.data() + h.row_ptr[static_cast<size_t>(a)];
+        const int32_t* cb = h.col.data() + h.row_ptr[static_cast<size_t>(b)];
+        for (int64_t j = 0; j < la; ++j)
+          if (ca[j] - static_cast<int32_t>(a) != cb[j] - static_cast<int32_t>(b)) return false;
+        return true;
+      };
+      std::unordered_map<uint64_t, int32_t> pid;
+      std::vector<int64_t> rep;
+      classed = true;
+      for (int64_t i = 0; i < n && classed; ++i) {
+        auto it = pid.find(hash[static_cast<size_t>(i)]);
+        if (it == pid.end()) {
+          // a lattice has a handful of patterns; past n/8 of them (or a 4 MB
+          // offset table) the rows do not share patterns: explicit columns
+          if (static_cast<int64_t>(rep.size()) >= std::max<int64_t>(1, std::min<int64_t>(4096, n / 8)) ||
+              tab.size() + static_cast<size_t>(len(i)) > (size_t{1} << 20)) {
+            classed = false;
+            break;
+          }
+          it = pid.emplace(hash[static_cast<size_t>(i)], static_cast<int32_t>(rep.size())).first;
+          rep.push_back(i);
+          const int32_t* c = h.col.data() + h.row_ptr[static_cast<size_t>(i)];
+          for (int64_t j = 0; j < len(i); ++j) tab.push_back(c[j] - static_cast<int32_t>(i));
+          tstart.push_back(static_cast<int32_t>(tab.size()));
+        }
+        classed = same(rep[static_cast<size_t>(it->second)], i);
+        cls[static_cast<size_t>(i)] = it->second;
+      }
+    }
+    if (!classed) {
+      std::fill(cls.begin(), cls.end(), -1);
+      tab.clear();
+      tstart.assign(1, 0);
+    }
+  }
   par([&](int64_t w) {
     const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
     for (int64_t i = r0; i < r1; ++i) perm[static_cast<size_t>(i)] = static_cast<int32_t>(i);
-    std::stable_sort(perm.begin() + r0, perm.begin() + r1, [&](int32_t a, int32_t b) { return len(a) > len(b); });
+    std::stable_sort(perm.begin() + r0, perm.begin() + r1, [&](int32_t a, int32_t b) {
+      const int64_t la = len(a), lb = len(b);
+      if (la != lb) return la > lb;
+      return cls[static_cast<size_t>(a)] < cls[static_cast<size_t>(b)];
+    });
     win_slices[static_cast<size_t>(w) + 1] = (r1 - r0 + k::kSellC - 1) / k::kSellC;
   });
   for (int64_t w = 0; w < nwin; ++w) win_slices[static_cast<size_t>(w) + 1] += win_slices[static_cast<size_t>(w)];
@@ -102,7 +166,7 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   }
   std::vector<int32_t> rows(static_cast<size_t>(2 * ns * k::kSellC), 0);
   std::vector<double> val(static_cast<size_t>(off.back()), 0.0);
-  std::vector<int32_t> col(static_cast<size_t>(off.back()), 0);
+  std::vector<int32_t> col(classed ? 1 : static_cast<size_t>(off.back()), 0);
   par([&](int64_t w) {
     const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
     for (int64_t q = 0; q < win_slices[static_cast<size_t>(w) + 1] - win_slices[static_cast<size_t>(w)]; ++q) {
@@ -119,10 +183,10 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
         const int32_t row = perm[static_cast<size_t>(at)];
         const int64_t p0 = h.row_ptr[static_cast<size_t>(row)], L = len(row);
         rows[ri] = row;
-        rows[ri + 1] = static_cast<int32_t>(L);
+        rows[ri + 1] = static_cast<int32_t>(classed ? (L | (static_cast<int64_t>(cls[static_cast<size_t>(row)] + 1) << 16)) : L);
         for (int64_t j = 0; j < L; ++j) {
           val[static_cast<size_t>(o + j * k::kSellC + l)] = h.val[static_cast<size_t>(p0 + j)];
-          col[static_cast<size_t>(o + j * k::kSellC + l)] = h.col[static_cast<size_t>(p0 + j)];
+          if (!classed) col[static_cast<size_t>(o + j * k::kSellC + l)] = h.col[static_cast<size_t>(p0 + j)];
         }
       }
     }
@@ -135,6 +199,13 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   d.sell_val.upload(val.data(), val.size(), s);
   d.sell_col.alloc(col.size());
   d.sell_col.upload(col.data(), col.size(), s);
+  d.sell_classes = classed ? static_cast<int64_t>(tstart.size()) - 1 : 0;
+  if (classed) {
+    d.sell_tab.alloc(tab.size());
+    d.sell_tab.upload(tab.data(), tab.size(), s);
+    d.sell_tstart.alloc(tstart.size());
+    d.sell_tstart.upload(tstart.data(), tstart.size(), s);
+  }
   d.nslices = ns;
   sync(s);
 }
@@ -183,6 +254,10 @@ k::SpmvPlan plan_of(const DeviceCsr& a) {
     p.sell_val = a.sell_val.get();
     p.sell_col = a.sell_col.get();
     p.nslices = a.nslices;
+    if (a.sell_classes > 0) {
+      p.sell_tab = a.sell_tab.get();
+      p.sell_tstart = a.sell_tstart.get();
+    }
     p.blocks = static_cast<int>((a.nslices + 7) / 8);
     return p;
   }

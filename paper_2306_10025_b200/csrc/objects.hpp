@@ -43,6 +43,12 @@ struct DeviceCsr {
   DevBuf<double> sell_val;
   DevBuf<int32_t> sell_col;
   int64_t nslices = 0;  // 0: not built
+  // Column-pattern classes (build_sell): when every row's columns are
+  // row + one of a few offset lists (structured FEM lattices: one list per
+  // node type), no column indices are stored; sell_row.y packs
+  // length | (class + 1) << 16 and the offsets sit in sell_tab.
+  DevBuf<int32_t> sell_tab, sell_tstart;
+  int64_t sell_classes = 0;  // 0: explicit columns
 };
 
 // Two-level coarse correction of the combo preconditioner (reference

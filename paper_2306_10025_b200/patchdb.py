@@ -102,6 +102,7 @@ _sig("pdb_matrix_spmv", C.c_int, _P, _D, _D)
 _sig("pdb_matrix_spmv_device", C.c_int, _P, C.c_void_p, C.c_void_p, C.c_void_p)
 _sig("pdb_matrix_free", None, _P)
 _sig("pdb_matrix_from_csr", C.c_int, C.c_int64, _I64, _I64, _D, C.POINTER(_P))
+_sig("pdb_matrix_sell_info", C.c_int, _P, _I64)
 _sig("pdb_matrix_csr", C.c_int, _P, _I64, _I64, _D)
 _sig("pdb_problem_assemble", C.c_int, C.c_char_p, C.POINTER(_P))
 _sig("pdb_problem_ndofs", C.c_int64, _P)
@@ -238,6 +239,14 @@ class Matrix(_Handle):
     @property
     def nnz(self) -> int:
         return _lib.pdb_matrix_nnz(self._ptr)
+
+    def sell_info(self) -> dict:
+        """Residual storage: column-pattern classes (0: explicit column
+        indices), column indices and values stored, slices."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(_lib.pdb_matrix_sell_info(self._ptr, _ip(out)))
+        return {"classes": int(out[0]), "col_entries": int(out[1]), "slices": int(out[2]),
+                "val_entries": int(out[3])}
 
     def spmv(self, x) -> np.ndarray:
         x = _f64(x)

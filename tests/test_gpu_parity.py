@@ -334,6 +334,55 @@ def test_spmv_ragged_rows(P, orc, monkeypatch, seed, n):
         np.testing.assert_allclose(A.spmv(x), want, rtol=1e-12, atol=1e-12)
 
 
+def _banded_csr(seed, n, band):
+    """Band matrix clipped at both ends: a few repeated column patterns
+    (row + offsets), i.e. every row in a column-pattern class."""
+    rows = [np.arange(max(0, i - band), min(n, i + band + 1)) for i in range(n)]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    return rp, np.concatenate(rows).astype(np.int64), np.random.default_rng(seed).uniform(-1, 1, rp[-1])
+
+
+@pytest.mark.parametrize("seed,n,band", [(4, 3000, 7), (5, 20000, 40), (6, 200, 3)])
+def test_spmv_pattern_classes(P, orc, monkeypatch, seed, n, band):
+    """Rows stored without column indices (every row in a column-pattern
+    class): bitwise the reference sum, and equal to the explicit-column copy."""
+    csr = _banded_csr(seed, n, band)
+    A = P.Matrix.from_csr(*csr)
+    info = A.sell_info()
+    assert info["classes"] >= 1 and info["col_entries"] == 0
+    x = np.random.default_rng(seed + 10).uniform(-1, 1, n)
+    want = orc.spmv(csr, x)
+    assert np.array_equal(A.spmv(x), want)
+    monkeypatch.setenv("PDB_SELL_CLASSES", "0")
+    B = P.Matrix.from_csr(*csr)
+    assert B.sell_info()["classes"] == 0 and B.sell_info()["col_entries"] >= csr[0][-1]
+    assert np.array_equal(B.spmv(x), want)
+
+
+def test_spmv_unclassed_rows_keep_columns(P, orc):
+    """Rows that do not share column patterns (more than n/8 patterns): the
+    copy keeps explicit column indices."""
+    rp, ci, v = _banded_csr(7, 4000, 5)
+    ci = ci.copy()
+    for i in range(100, 3900, 4):  # 950 rows: first column moved to a row-dependent place
+        ci[rp[i]] = (7 * i) % 90
+    A = P.Matrix.from_csr(rp, ci, v)
+    assert A.sell_info()["classes"] == 0
+    x = np.random.default_rng(8).uniform(-1, 1, 4000)
+    assert np.array_equal(A.spmv(x), orc.spmv((rp, ci, v), x))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s"])
+def test_fem_rows_are_classed(name, request):
+    """On the structured FEM lattices every row falls into a column-pattern
+    class (one per node type, Dirichlet identity rows): the residual streams
+    no column indices."""
+    c = request.getfixturevalue(name)
+    info = c.A.sell_info()
+    assert 1 <= info["classes"] <= 64 and info["col_entries"] == 0
+
+
 @pytest.mark.parametrize("cells", [60, 120, 180, 250, 512])
 def test_gmres_fused_mgs_matches_per_vector_launches(P, cells, monkeypatch):
     """The cooperative MGS kernel (vector in registers, one launch per Arnoldi
