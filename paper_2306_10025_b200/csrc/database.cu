@@ -424,6 +424,10 @@ void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf
 // single-GPU build.  PDB_SHARD_EMULATE=W runs all W chunks on one GPU (no
 // NCCL), which tests the decomposition without W devices.
 
+// Entrywise assignment: below this many patches per slot, one thread per
+// (patch, entry tile) instead of one per patch (l1_pairs + argmin).
+constexpr int64_t kL1PairsBelow = 16384;
+
 struct AssignSlot {
   int64_t lo = 0, hi = 0;
   DevBuf<double> sub_il;
@@ -569,8 +573,19 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       const int64_t cnt = sl.hi - sl.lo;
       if (cnt <= 0) continue;
       if (variant == Variant::Entrywise) {
-        k::l1_argmin(cnt, m, static_cast<int>(len), sub + sl.lo * len, db.reps.get(), d_phi.get() + sl.lo,
-                     d_new.get() + sl.lo, d_min.get() + sl.lo, changed.get(), s);
+        if (cnt < kL1PairsBelow && m > 1) {
+          // few patches (large ps): a thread per patch leaves the GPU idle, so
+          // every (patch, entry tile) pair gets its own thread, then the
+          // argmin -- the same sequential sums and strict-< scan, bitwise
+          if (dist.size() < static_cast<size_t>(cnt * m)) dist.alloc(static_cast<size_t>(cnt * m));
+          k::l1_pairs(cnt, nullptr, m, static_cast<int>(len), sub + sl.lo * len, nullptr, db.reps.get(), dist.get(),
+                      s);
+          k::argmin_assign(cnt, m, dist.get(), d_phi.get() + sl.lo, d_new.get() + sl.lo, d_min.get() + sl.lo,
+                           changed.get(), s);
+        } else {
+          k::l1_argmin(cnt, m, static_cast<int>(len), sub + sl.lo * len, db.reps.get(), d_phi.get() + sl.lo,
+                       d_new.get() + sl.lo, d_min.get() + sl.lo, changed.get(), s);
+        }
       } else {
         double* dd = nullptr;
         if (prune) {  // per-slot distance matrix, kept for the next iteration

@@ -177,6 +177,17 @@ def test_gpu_elastic_greedy_l1(c5s, dev5, P, orc):
 
 
 @pytest.mark.gpu
+def test_gpu_elastic_kmeans_entrywise(c5s, dev5, P, orc):
+    """Entrywise k-means at p_s = 192 (the (patch, entry tile) pair path of
+    the assignment): phi and representatives bitwise the oracle's."""
+    want = orc.partitioned_build(c5s.mats, 40, 0, seed=9, max_iters=8)
+    db = P.Database.build(dev5[0], dev5[1], P.KMEANS_ENTRYWISE, db_size=40, seed=9, max_iters=8)
+    assert db.size == want["m"]
+    assert np.array_equal(db.phi(), want["phi"])
+    assert np.array_equal(db.representatives(), want["reps"])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name,dev,compressed", [("c4s", "dev4", True), ("c5s", "dev5", False)])
 def test_gpu_relax_history(name, dev, compressed, request, P, orc):
     c = request.getfixturevalue(name)
