@@ -424,8 +424,9 @@ void ensure_patch_factors(const double* sub, int64_t n, int ps, PatchFactors& pf
 // single-GPU build.  PDB_SHARD_EMULATE=W runs all W chunks on one GPU (no
 // NCCL), which tests the decomposition without W devices.
 
-// Entrywise assignment: below this many patches per slot, one thread per
-// (patch, entry tile) instead of one per patch (l1_pairs + argmin).
+// Entrywise assignment: below this many patches per slot (or for patches of
+// >= 4096 entries), one thread per (patch, entry tile) instead of one per
+// patch (l1_pairs + argmin).
 constexpr int64_t kL1PairsBelow = 16384;
 
 struct AssignSlot {
@@ -573,7 +574,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       const int64_t cnt = sl.hi - sl.lo;
       if (cnt <= 0) continue;
       if (variant == Variant::Entrywise) {
-        if (cnt < kL1PairsBelow && m > 1) {
+        if ((cnt < kL1PairsBelow || len >= 4096) && m > 1) {
           // few patches (large ps): a thread per patch leaves the GPU idle, so
           // every (patch, entry tile) pair gets its own thread, then the
           // argmin -- the same sequential sums and strict-< scan, bitwise
