@@ -756,6 +756,59 @@ __global__ void cluster_mean_kernel(int64_t m, int len, const int32_t* __restric
   reps[j * len + q] = __dmul_rn(s, inv);
 }
 
+// Staged variant: block = one warp on 32 entries q of cluster j.  Each lane
+// streams its own column through shared memory with 8-byte cp.async, kMeanD-1
+// stages of kMeanS members ahead (160 loads in flight per lane without holding
+// registers), and adds them in ascending member order -- the same sequential
+// sum.  The register-pipelined kernel above exposes the full memory latency
+// once per group of members, which dominates a large cluster's chain.
+constexpr int kMeanS = 32, kMeanD = 6;
+
+__global__ void __launch_bounds__(32) cluster_mean_staged_kernel(int64_t m, int len, const int32_t* __restrict__ mem_ptr,
+                                                                 const int32_t* __restrict__ mem,
+                                                                 const double* __restrict__ mats,
+                                                                 double* __restrict__ reps) {
+  __shared__ double buf[kMeanD][kMeanS][32];
+  const int64_t j = blockIdx.y;
+  const int t = threadIdx.x;
+  const int q = blockIdx.x * 32 + t;
+  const int32_t lo = mem_ptr[j], hi = mem_ptr[j + 1];
+  const int cnt = hi - lo;
+  const int nst = (cnt + kMeanS - 1) / kMeanS;
+  const bool live = q < len;
+  auto issue = [&](int st) {
+    // lane t fetches member id t of the stage; the ids reach every lane by
+    // shuffle (no dependent L1 load per copy)
+    const int c0 = st * kMeanS;
+    const int32_t my_id = c0 + t < cnt ? __ldg(mem + lo + c0 + t) : 0;
+    const int un = cnt - c0 < kMeanS ? cnt - c0 : kMeanS;
+    const unsigned base = (unsigned)__cvta_generic_to_shared(&buf[st % kMeanD][0][t]);
+#pragma unroll 8
+    for (int u = 0; u < kMeanS; ++u) {
+      const int32_t id = __shfl_sync(0xffffffffu, my_id, u);
+      if (u < un && live)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(base + u * 32 * 8),
+                     "l"(mats + (int64_t)id * len + q)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int st = 0; st < kMeanD - 1; ++st) issue(st);  // (empty groups past the end keep the count uniform)
+  double s = 0.0;
+  for (int st = 0; st < nst; ++st) {
+    issue(st + kMeanD - 1);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kMeanD - 1) : "memory");
+    if (live) {
+      const double* b = &buf[st % kMeanD][0][t];
+      const int un = cnt - st * kMeanS < kMeanS ? cnt - st * kMeanS : kMeanS;
+      for (int u = 0; u < un; ++u) s = __dadd_rn(s, b[u * 32]);
+    }
+  }
+  if (!live) return;
+  const double inv = __ddiv_rn(1.0, (double)cnt);
+  reps[j * len + q] = __dmul_rn(s, inv);
+}
+
 }  // namespace
 
 bool spectral_il_supported(int ps) { return ps == 9 || ps == 22 || ps == 25 || ps == 27; }
@@ -898,6 +951,11 @@ void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double*
 void cluster_mean(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats, double* reps,
                   cudaStream_t s) {
   if (m <= 0) return;
+  const char* e = getenv("PDB_MEAN_STAGED");
+  if (!(e && e[0] == '0')) {
+    cluster_mean_staged_kernel<<<dim3(grid_for(len, 32), (unsigned)m), 32, 0, s>>>(m, len, mem_ptr, mem, mats, reps);
+    return;
+  }
   dim3 grid(grid_for(len, 128), (unsigned)m);
   cluster_mean_kernel<<<grid, 128, 0, s>>>(m, len, mem_ptr, mem, mats, reps);
 }
