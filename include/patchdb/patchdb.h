@@ -206,6 +206,17 @@ PDB_API double pdb_database_eps(pdb_database db);
 PDB_API pdb_status pdb_database_representatives(pdb_database db, double* reps);
 PDB_API pdb_status pdb_database_factors(pdb_database db, double* lu, int64_t* pivots);
 /* Tolerance bisection to a size band, ref experiments.cpp:168-204 (greedy methods only). */
+/* Reference evaluate_objective (compress.hpp:74-75, compress.cpp:423-440):
+ * *out = beta * |B| + sum_k ||I - A_k B_phi(k)^{-1}||_2^2, every distance the
+ * reference's spectral_distance (bitwise), summed in ascending k.  beta > 0. */
+PDB_API pdb_status pdb_database_objective(pdb_matrix m, pdb_patchset ps, pdb_database db, double beta,
+                                          double* out);
+/* Reference compressibility_curve (compress.hpp:77-85, compress.cpp:442-456):
+ * greedy_tolerance (first match) over an ascending grid of count tolerances;
+ * db_sizes[k] = |B|, ratios[k] = (n_p - |B|) / n_p.  method is
+ * PDB_METHOD_GREEDY_SPECTRAL or PDB_METHOD_GREEDY_L1. */
+PDB_API pdb_status pdb_compressibility_curve(pdb_matrix m, pdb_patchset ps, pdb_method method, const double* eps_grid,
+                                             int64_t count, int64_t* db_sizes, double* ratios);
 PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, const pdb_compress_options* opts,
                                               int64_t target_lo, int64_t target_hi, pdb_database* out,
                                               double* eps_out);

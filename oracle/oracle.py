@@ -309,6 +309,8 @@ class RefLib:
                                     C.POINTER(_P)]
         L.refh_db_greedy_capped.argtypes = [_P, _P, C.c_int, C.c_double, C.c_int64, C.c_int, C.c_int, C.POINTER(_P)]
         L.refh_db_bisect.argtypes = [_P, _P, C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(_P), _D]
+        L.refh_evaluate_objective.argtypes = [_P, _P, _P, C.c_double, C.c_int, _D]
+        L.refh_compressibility_curve.argtypes = [_P, _P, C.c_int, _D, C.c_int64, C.c_int, _I64, _D]
         L.refh_db_eps.restype = C.c_double
         L.refh_db_eps.argtypes = [_P]
         L.refh_db_phi.argtypes = [_P, _I64]
@@ -501,6 +503,21 @@ class RefPatchSet:
         self.ref._check(self.L.refh_db_bisect(m.ptr, self.ptr, int(spectral), lo, hi, int(best_match), threads,
                                               C.byref(out), C.byref(eps)))
         return RefDatabase(self.ref, out.value), eps.value
+
+    def objective(self, m: RefMatrix, db, beta, threads=1):
+        """evaluate_objective (compress.cpp:423-440)."""
+        out = C.c_double()
+        self.ref._check(self.L.refh_evaluate_objective(m.ptr, self.ptr, db.ptr, beta, threads, C.byref(out)))
+        return out.value
+
+    def curve(self, m: RefMatrix, spectral, grid, threads=1):
+        """compressibility_curve (compress.cpp:442-456): [(eps, db_size, ratio)]."""
+        g = np.ascontiguousarray(grid, dtype=np.float64)
+        sizes = np.zeros(len(g), np.int64)
+        ratios = np.zeros(len(g))
+        self.ref._check(self.L.refh_compressibility_curve(m.ptr, self.ptr, int(spectral), _dp(g), len(g), threads,
+                                                          _ip(sizes), _dp(ratios)))
+        return [(float(e), int(n), float(r)) for e, n, r in zip(g, sizes, ratios)]
 
     def precond(self, m: RefMatrix, db=None, omega=1.0, threads=1):
         out = _P()

@@ -180,6 +180,28 @@ RH_API int refh_db_build(void* m, void* ps, int method, double eps, int64_t db_s
   });
 }
 
+// evaluate_objective (compress.cpp:423-440) of a database on the set's patches.
+RH_API int refh_evaluate_objective(void* m, void* ps, void* db, double beta, int threads, double* out) {
+  return guarded([&] {
+    const auto mats = extract_all(*static_cast<SparseMatrix*>(m), *static_cast<PatchSet*>(ps), threads);
+    *out = evaluate_objective(*static_cast<Database*>(db), mats, beta, threads);
+  });
+}
+
+// compressibility_curve (compress.cpp:442-456).
+RH_API int refh_compressibility_curve(void* m, void* ps, int spectral, const double* grid, int64_t count, int threads,
+                                      int64_t* sizes, double* ratios) {
+  return guarded([&] {
+    const auto mats = extract_all(*static_cast<SparseMatrix*>(m), *static_cast<PatchSet*>(ps), threads);
+    const std::vector<double> g(grid, grid + count);
+    const auto curve = compressibility_curve(mats, g, spectral ? Flavor::Spectral : Flavor::EntrywiseL1, threads);
+    for (size_t k = 0; k < curve.size(); ++k) {
+      sizes[k] = curve[k].db_size;
+      ratios[k] = curve[k].ratio;
+    }
+  });
+}
+
 // greedy_tolerance_capped (compress.cpp:121-124); *out = NULL when aborted.
 RH_API int refh_db_greedy_capped(void* m, void* ps, int spectral, double eps, int64_t abort_above, int best_match,
                                  int threads, void** out) {

@@ -438,6 +438,24 @@ PDB_API pdb_status pdb_database_build_to_size(pdb_matrix m, pdb_patchset ps, con
   });
 }
 
+PDB_API pdb_status pdb_database_objective(pdb_matrix m, pdb_patchset ps, pdb_database db, double beta,
+                                          double* out) {
+  if (m == nullptr || ps == nullptr || db == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] { *out = database_objective(m->a, *ps, *db, beta, default_stream()); });
+}
+
+PDB_API pdb_status pdb_compressibility_curve(pdb_matrix m, pdb_patchset ps, pdb_method method, const double* eps_grid,
+                                             int64_t count, int64_t* db_sizes, double* ratios) {
+  if (m == nullptr || ps == nullptr || db_sizes == nullptr || ratios == nullptr || (count > 0 && eps_grid == nullptr))
+    return arg_error("null argument");
+  return guarded([&] {
+    require(method == PDB_METHOD_GREEDY_SPECTRAL || method == PDB_METHOD_GREEDY_L1, Errc::invalid_argument,
+            "compressibility_curve needs a greedy method (spectral or l1)");
+    compressibility_curve(m->a, *ps, method == PDB_METHOD_GREEDY_SPECTRAL, eps_grid, count, db_sizes, ratios,
+                          default_stream());
+  });
+}
+
 PDB_API int64_t pdb_database_size(pdb_database db) { return db == nullptr ? 0 : db->m; }
 PDB_API int64_t pdb_database_n_patches(pdb_database db) { return db == nullptr ? 0 : db->np; }
 PDB_API int64_t pdb_database_patch_size(pdb_database db) { return db == nullptr ? 0 : db->ps; }

@@ -1106,6 +1106,54 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
   }
 }
 
+// evaluate_objective (compress.cpp:423-440): beta |B| + sum_k d(A_k, B_phi(k))^2
+// with the bit-exact spectral distance of every (patch, its entry) pair on the
+// device and the terms summed in ascending k on the host, as the reference.
+double database_objective(const DeviceCsr& a, const pdb_patchset_s& ps, const pdb_database_s& db, double beta,
+                          cudaStream_t s) {
+  require_device();
+  require(beta > 0.0, Errc::invalid_argument, "beta must be positive");
+  require(db.np == ps.np, Errc::dimension_mismatch, "database does not match the patch list");
+  require(db.ps == ps.ps, Errc::dimension_mismatch, "spectral_distance dimension mismatch");
+  const int64_t n = ps.np;
+  DevBuf<double> mats;
+  extract_patches(a, ps, mats, s);
+  std::vector<int32_t> pa(static_cast<size_t>(n));
+  std::iota(pa.begin(), pa.end(), 0);
+  Scratch<int32_t> dpa(static_cast<size_t>(std::max<int64_t>(n, 1)), s);
+  Scratch<double> d(static_cast<size_t>(std::max<int64_t>(n, 1)), s);
+  Scratch<unsigned long long> iters(1, s);
+  h2d(dpa.get(), pa, s);
+  k::spectral_list(n, dpa.get(), db.phi.get(), static_cast<int>(ps.ps), mats.get(), db.lu.get(), db.piv.get(), d.get(),
+                   iters.get(), s);
+  PDB_LAUNCH_CHECK();
+  const std::vector<double> dh = d2h(d.get(), static_cast<size_t>(n), s);
+  double sum = 0.0;
+  for (double v : dh) sum += v * v;
+  return beta * static_cast<double>(db.m) + sum;
+}
+
+// compressibility_curve (compress.cpp:442-456): greedy_tolerance (first match)
+// at every tolerance of an ascending grid; the patches are extracted once.
+void compressibility_curve(const DeviceCsr& a, const pdb_patchset_s& ps, bool spectral, const double* grid,
+                           int64_t count, int64_t* sizes, double* ratios, cudaStream_t s) {
+  require_device();
+  require(count > 0, Errc::invalid_argument, "empty tolerance grid");
+  for (int64_t k = 0; k < count; ++k) {
+    require(grid[k] > 0.0, Errc::invalid_argument, "tolerances must be positive");
+    if (k > 0) require(grid[k] > grid[k - 1], Errc::invalid_argument, "tolerance grid must be ascending");
+  }
+  DevBuf<double> mats;
+  extract_patches(a, ps, mats, s);
+  const double n_p = static_cast<double>(ps.np);
+  for (int64_t k = 0; k < count; ++k) {
+    pdb_database_s db;
+    greedy_build(mats, ps.np, static_cast<int>(ps.ps), grid[k], spectral, false, -1, db, s);
+    sizes[k] = db.m;
+    ratios[k] = (n_p - static_cast<double>(db.m)) / n_p;
+  }
+}
+
 bool build_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, pdb_database_s& out,
                     cudaStream_t s) {
   require_device();

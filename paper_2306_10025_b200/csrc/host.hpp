@@ -101,6 +101,10 @@ bool build_database_from_mats(const DevBuf<double>& mats, int64_t np, int64_t ps
 double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const BuildParams& p, int64_t lo, int64_t hi,
                        pdb_database_s& out, cudaStream_t s);
 void import_database(const std::string& json_path, const std::string& bin_path, pdb_database_s& db, cudaStream_t s);
+double database_objective(const DeviceCsr& a, const pdb_patchset_s& ps, const pdb_database_s& db, double beta,
+                          cudaStream_t s);
+void compressibility_curve(const DeviceCsr& a, const pdb_patchset_s& ps, bool spectral, const double* grid,
+                           int64_t count, int64_t* sizes, double* ratios, cudaStream_t s);
 void export_database(const pdb_database_s& db, const std::string& json_path, const std::string& bin_path,
                      cudaStream_t s);
 

@@ -129,6 +129,8 @@ _sig("pdb_compress_options_init", None, C.POINTER(CompressOptions))
 _sig("pdb_database_build", C.c_int, _P, _P, C.POINTER(CompressOptions), C.POINTER(_P))
 _sig("pdb_database_build_to_size", C.c_int, _P, _P, C.POINTER(CompressOptions), C.c_int64, C.c_int64,
      C.POINTER(_P), _D)
+_sig("pdb_database_objective", C.c_int, _P, _P, _P, C.c_double, _D)
+_sig("pdb_compressibility_curve", C.c_int, _P, _P, C.c_int, _D, C.c_int64, _I64, _D)
 _sig("pdb_database_size", C.c_int64, _P)
 _sig("pdb_database_n_patches", C.c_int64, _P)
 _sig("pdb_database_patch_size", C.c_int64, _P)
@@ -463,6 +465,12 @@ class Database(_Handle):
         _check(_lib.pdb_database_work(self._ptr, C.byref(a), C.byref(b), C.byref(c)))
         return {"pair_evals": a.value, "power_iters": b.value, "lu_count": c.value}
 
+    def objective(self, m: Matrix, ps: "PatchSet", beta: float) -> float:
+        """Reference evaluate_objective: beta |B| + sum_k d(A_k, B_phi(k))^2."""
+        out = C.c_double()
+        _check(_lib.pdb_database_objective(m.ptr, ps.ptr, self._ptr, float(beta), C.byref(out)))
+        return out.value
+
     def export(self, json_path: str, bin_path: str) -> None:
         _check(_lib.pdb_database_export(self._ptr, json_path.encode(), bin_path.encode()))
 
@@ -691,3 +699,13 @@ class Shard(_Handle):
 
     def relax_device(self, d_b: int, d_x: int, sweeps: int, stream: int = 0) -> None:
         _check(_lib.pdb_shard_relax_device(self._ptr, d_b, d_x, sweeps, stream or None))
+
+
+def compressibility_curve(m: Matrix, ps: "PatchSet", method: int, eps_grid) -> list:
+    """Reference compressibility_curve: [(eps, db_size, ratio)] for greedy
+    first-match compression over an ascending tolerance grid."""
+    g = _f64(eps_grid)
+    sizes = np.zeros(len(g), dtype=np.int64)
+    ratios = np.zeros(len(g))
+    _check(_lib.pdb_compressibility_curve(m.ptr, ps.ptr, int(method), _dp(g), len(g), _ip(sizes), _dp(ratios)))
+    return [(float(e), int(n), float(r)) for e, n, r in zip(g, sizes, ratios)]

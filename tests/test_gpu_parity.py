@@ -447,3 +447,24 @@ def test_greedy_spectral_pruning_changes_nothing(P, cfg, cells, ps, eps, best_ma
     assert np.array_equal(on.phi(), off.phi())
     assert np.array_equal(on.representatives(), off.representatives())
     assert on.work()["power_iters"] <= off.work()["power_iters"]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s"])
+def test_objective_and_compressibility_curve(name, request, P, ref):
+    """pdb_database_objective / pdb_compressibility_curve against the
+    reference build on the same matrix: the objective bitwise (same distances,
+    same summation order), the curve's sizes and ratios exactly."""
+    c = request.getfixturevalue(name)
+    rm = ref.matrix(c.csr)
+    rps = rm.detect(c.ps_size)
+    grid = [1e-3, 1e-2, 0.1, 0.5, 2.0]
+    for method, spectral in ((P.GREEDY_L1, False), (P.GREEDY_SPECTRAL, True)):
+        assert P.compressibility_curve(c.A, c.ps, method, grid) == rps.curve(rm, spectral, grid)
+    for method, kw in ((P.GREEDY_SPECTRAL, dict(eps=0.5)), (P.KMEANS_SPECTRAL, dict(db_size=12, seed=3, max_iters=6))):
+        db = P.Database.build(c.A, c.ps, method, **kw)
+        rdb = rps.build(rm, method, **kw)
+        assert db.objective(c.A, c.ps, 0.25) == rps.objective(rm, rdb, 0.25)
+    with pytest.raises(P.PatchdbError):
+        db.objective(c.A, c.ps, -1.0)
+    with pytest.raises(P.PatchdbError):
+        P.compressibility_curve(c.A, c.ps, P.GREEDY_L1, [0.1, 0.01])
