@@ -436,6 +436,8 @@ struct AssignSlot {
   int64_t m = 0;             // columns of dist / lbq
   DevBuf<double> sub_sorted;  // bound pass: the slot's patches interleaved in work order
   DevBuf<int32_t> perm, itc;  // work order; power iterations of each patch's last bound pair
+  DevBuf<int32_t> tile_order;  // pruned pass: tiles of 32 patches, most power iterations first
+  DevBuf<unsigned long long> tile_iters;
 };
 
 // Work order of the bound pass (one pair per thread, aligned groups of 32 =
@@ -542,6 +544,8 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   const char* ds_env = getenv("PDB_DIAG_SORT");  // 0: bound pass in patch order with in-block refill
   const bool diag_sort = !(ds_env && ds_env[0] == '0');
   std::vector<uint8_t> chg_h;  // host copy of d_chg
+  const char* lpt_env = getenv("PDB_TILE_LPT");  // 0: pruned-pass tiles in patch order
+  const bool tile_lpt = !(lpt_env && lpt_env[0] == '0');
   DevBuf<double> ub;
   DevBuf<int32_t> guess;  // iteration 0: l1-nearest entry, for the first bound
   DevBuf<double> gmin;
@@ -641,6 +645,26 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
           ru.phi = cur_phi;
           ru.lbq = sl.lbq.get();
           ru.dprev = nullptr;
+          if (tile_lpt) {
+            // tiles in descending order of the power iterations they took in
+            // the previous Lloyd iteration (stable: ties keep tile order)
+            const int64_t nt = (cnt + 31) / 32;
+            std::vector<int32_t> order(static_cast<size_t>(nt));
+            std::iota(order.begin(), order.end(), 0);
+            if (sl.tile_iters.size() == static_cast<size_t>(nt)) {
+              const std::vector<unsigned long long> ti = d2h(sl.tile_iters.get(), static_cast<size_t>(nt), s);
+              std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+                return ti[static_cast<size_t>(a)] > ti[static_cast<size_t>(b)];
+              });
+            } else {
+              sl.tile_iters.alloc(static_cast<size_t>(nt));
+              sl.tile_order.alloc(static_cast<size_t>(nt));
+            }
+            h2d(sl.tile_order.get(), order, s);
+            sl.tile_iters.zero(s);
+            ru.tile_order = sl.tile_order.get();
+            ru.tile_iters = sl.tile_iters.get();
+          }
         }
         if (il)
           k::spectral_tiled_il(cnt, m, ps, sl.sub_il.get(), lu_il.get(), piv_il.get(), dd, iters.get(), s, ru);

@@ -170,6 +170,8 @@ struct KmeansReuse {
   const double* dprev = nullptr;
   int64_t mfull = 0;
   int32_t* it_out = nullptr;  // DIAG: power iterations each patch's pair took
+  const int32_t* tile_order = nullptr;       // pruned pass: block b works on tile tile_order[b]
+  unsigned long long* tile_iters = nullptr;  // ... and adds its power iterations to tile_iters[tile]
 };
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
                        const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s,

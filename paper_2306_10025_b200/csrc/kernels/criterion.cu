@@ -421,7 +421,10 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
   const int tid = threadIdx.x;
   // DIAG: 128 patches pulled by 64 threads; sorted DIAG (pid): 64, one per thread
   const int TA = DIAG ? (pid ? kTileThreads : 2 * kTileThreads) : kTileA;
-  const int64_t a0 = (int64_t)blockIdx.x * TA, e0 = (int64_t)blockIdx.y * kTileE;
+  // pruned assignment with ru.tile_order: blocks take their tiles longest
+  // first (the previous Lloyd iteration's power iterations per tile)
+  const int64_t tile = (!DIAG && ru.tile_order) ? (int64_t)ru.tile_order[blockIdx.x] : (int64_t)blockIdx.x;
+  const int64_t a0 = tile * TA, e0 = (int64_t)blockIdx.y * kTileE;
   const int na = (int)(npat - a0 < TA ? npat - a0 : TA);
   // pruned k-means assignment (IL, bound given): one block takes every factor
   // of its patches, so the few pairs that run to convergence overlap with
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
           L = lu + (int64_t)diag_phi[g] * LEN;
           P = piv + (int64_t)diag_phi[g] * PS;
         } else if (IL) {
-          A = mats + (int64_t)blockIdx.x * LEN * kTileA + pa;
+          A = mats + tile * LEN * kTileA + pa;
           if (all_e) {  // factor pe of the interleaved groups of kTileE
             L = lu + (int64_t)(pe / kTileE) * LEN * kTileE + pe % kTileE;
             P = piv + (int64_t)(pe / kTileE) * PS * kTileE + pe % kTileE;
@@ -625,6 +628,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     }
   }
   if (iters_total && my_iters) atomicAdd(iters_total, my_iters);
+  if (!DIAG && ru.tile_iters && my_iters) atomicAdd(ru.tile_iters + tile, my_iters);
 }
 
 template <int PS, bool IL = false>
