@@ -2,7 +2,7 @@
 // shard_plan.cpp), NCCL point-to-point exchanges on the sweep stream.
 //
 // Per sweep on rank r:
-//   residual over the shard's patch-DoF rows            (local CSR, v5 SpMV)
+//   residual over the shard's patch-DoF rows            (local matrix, SELL residual)
 //   patch solves of the shard's patches                  (same kernels as 1 GPU)
 //   interface partial sums z_d (from 0, ascending patch) for DoFs finished by
 //   the upper neighbour  -> ncclSend / ncclRecv (grouped)
