@@ -438,6 +438,7 @@ struct AssignSlot {
   DevBuf<int32_t> perm, itc;  // work order; power iterations of each patch's last bound pair
   DevBuf<int32_t> tile_order;  // pruned pass: tiles of 32 patches, most power iterations first
   DevBuf<unsigned long long> tile_iters;
+  DevBuf<uint8_t> lng[2];  // pruned pass: "ran long" per pair, by Lloyd iteration parity
 };
 
 // Work order of the bound pass (one pair per thread, aligned groups of 32 =
@@ -546,6 +547,8 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
   std::vector<uint8_t> chg_h;  // host copy of d_chg
   const char* lpt_env = getenv("PDB_TILE_LPT");  // 0: pruned-pass tiles in patch order
   const bool tile_lpt = !(lpt_env && lpt_env[0] == '0');
+  const char* lf_env = getenv("PDB_LONG_FIRST");  // 0: pairs of a tile in plain order
+  const bool long_first = !(lf_env && lf_env[0] == '0');
   DevBuf<double> ub;
   DevBuf<int32_t> guess;  // iteration 0: l1-nearest entry, for the first bound
   DevBuf<double> gmin;
@@ -598,6 +601,10 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
             sl.dist.alloc(static_cast<size_t>(cnt * m));
             sl.lbq.alloc(static_cast<size_t>(cnt * m));
             sl.lbq.zero(s);
+            for (auto& lb : sl.lng) {
+              lb.alloc(static_cast<size_t>(cnt * m));
+              lb.zero(s);
+            }
             sl.m = m;
           }
           dd = sl.dist.get();
@@ -664,6 +671,10 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
             sl.tile_iters.zero(s);
             ru.tile_order = sl.tile_order.get();
             ru.tile_iters = sl.tile_iters.get();
+          }
+          if (long_first) {
+            ru.long_prev = sl.lng[iter & 1].get();
+            ru.long_cur = sl.lng[(iter + 1) & 1].get();
           }
         }
         if (il)

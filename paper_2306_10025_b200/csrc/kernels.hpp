@@ -172,6 +172,8 @@ struct KmeansReuse {
   int32_t* it_out = nullptr;  // DIAG: power iterations each patch's pair took
   const int32_t* tile_order = nullptr;       // pruned pass: block b works on tile tile_order[b]
   unsigned long long* tile_iters = nullptr;  // ... and adds its power iterations to tile_iters[tile]
+  const uint8_t* long_prev = nullptr;  // pruned pass: pair ran > 2 iterations last Lloyd iteration
+  uint8_t* long_cur = nullptr;         // ... written for the next one
 };
 void spectral_tiled_il(int64_t npat, int64_t ne, int ps, const double* mats_il, const double* lu_il,
                        const int32_t* piv_il, double* d, unsigned long long* iters, cudaStream_t s,

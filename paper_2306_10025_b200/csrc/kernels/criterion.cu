@@ -460,10 +460,23 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
       } else {
         p = atomicAdd(&counter, 1);
       }
-      if (p >= npairs) break;
+      // pruned assignment with long_prev: two passes over the block's pairs,
+      // first those that ran past two power iterations in the previous Lloyd
+      // iteration (likely long again), then the rest -- the long chains start
+      // early instead of forming the block's tail
+      const bool two = !DIAG && ru.long_prev != nullptr;
+      if (p >= (two ? 2 * npairs : npairs)) break;
+      const bool second = p >= npairs;
+      if (second) p -= npairs;
       {
         pa = p % na;
         pe = p / na;
+        if (two) {
+          const int64_t q = (a0 + pa) * ne + e0 + pe;
+          const bool lng = ru.long_prev[q] != 0;
+          if (lng == second) continue;  // taken in the other pass
+          ru.long_cur[q] = lng;         // carried when the pair is not run below
+        }
         // DIAG with pid: position a0 + pa of a centroid-sorted copy of the
         // patches; g is the patch's own index for d / dprev / phi
         const int64_t g = (DIAG && pid) ? (int64_t)pid[a0 + pa] : a0 + pa;
@@ -622,6 +635,7 @@ __global__ void __launch_bounds__(kTileThreads) spectral_tile_kernel(int64_t npa
     }
     if (done) {
       d[DIAG ? gcur : (a0 + pa) * ne + e0 + pe] = result;
+      if (!DIAG && ru.long_cur) ru.long_cur[(a0 + pa) * ne + e0 + pe] = it > 2;
       if (DIAG && ru.it_out) ru.it_out[gcur] = it;
       my_iters += (unsigned long long)it;
       active = false;
