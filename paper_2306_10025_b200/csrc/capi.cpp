@@ -242,55 +242,12 @@ PDB_API pdb_status pdb_problem_l2_error(pdb_problem p, const double* discrete_so
 
 PDB_API void pdb_problem_free(pdb_problem p) { delete p; }
 
-PDB_API void pdb_gen_options_init(pdb_gen_options* o) {
-  if (o == nullptr) return;
-  std::memset(o, 0, sizeof(*o));
-  o->physics = 0;
-  o->dim = 2;
-  o->degree = 2;
-  o->bc_mode = 0;
-  o->cells = 32;
-  o->jitter = 0.0;
-  o->seed = 42;
-  o->coeff_kind = 0;
-  o->coeff_value = 1.0;
-  o->n_levels = 0;
-  o->block_cells = 1;
-  o->threads = 0;
-  o->poisson_ratio = 0.3;
-}
+PDB_API void pdb_gen_options_init(pdb_gen_options* o) { gen_options_defaults(o); }
 
-// BASELINE.json configs: 1 = 2D Q2 32^2 jitter 0.1;
-// 2 = 2D Q4 256^2 jitter 0.05, rho on 8x8-cell blocks from {1,10,100,1000};
-// 3 = 3D Q2 64^3 jitter 0.1; 4 = 2D Stokes Q2-Q1 512^2, mu lognormal(0,1)
-// per cell; 5 = 3D elasticity Q3 96^3, E from {1,100} on 4^3-cell blocks, nu 0.3.
+// BASELINE.json configs, presets in generator.cpp.
 PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* o) {
   if (o == nullptr) return arg_error("null argument");
-  pdb_gen_options_init(o);
-  switch (config) {
-    case 1:
-      o->dim = 2, o->degree = 2, o->cells = 32, o->jitter = 0.1;
-      break;
-    case 2:
-      o->dim = 2, o->degree = 4, o->cells = 256, o->jitter = 0.05, o->coeff_kind = 1, o->block_cells = 8,
-      o->n_levels = 4;
-      o->levels[0] = 1.0, o->levels[1] = 10.0, o->levels[2] = 100.0, o->levels[3] = 1000.0;
-      break;
-    case 3:
-      o->dim = 3, o->degree = 2, o->cells = 64, o->jitter = 0.1;
-      break;
-    case 4:
-      o->physics = 1, o->dim = 2, o->degree = 2, o->cells = 512, o->coeff_kind = 2, o->coeff_value = 1.0;
-      break;
-    case 5:
-      o->physics = 2, o->dim = 3, o->degree = 3, o->cells = 96, o->coeff_kind = 1, o->block_cells = 4,
-      o->n_levels = 2, o->poisson_ratio = 0.3;
-      o->levels[0] = 1.0, o->levels[1] = 100.0;
-      break;
-    default:
-      return arg_error("config must be 1..5");
-  }
-  if (cells > 0) o->cells = cells;
+  if (!gen_options_preset(config, cells, o)) return arg_error("config must be 1..5");
   return PDB_OK;
 }
 

@@ -784,4 +784,49 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
   out.components = 0;  // vector / mixed DoFs: no scalar lattice
 }
 
+void gen_options_defaults(pdb_gen_options* o) {
+  if (o == nullptr) return;
+  *o = pdb_gen_options{};
+  o->dim = 2;
+  o->degree = 2;
+  o->cells = 32;
+  o->seed = 42;
+  o->coeff_value = 1.0;
+  o->block_cells = 1;
+  o->poisson_ratio = 0.3;
+}
+
+// 1 = 2D Q2 32^2 jitter 0.1; 2 = 2D Q4 256^2 jitter 0.05, rho on 8x8-cell
+// blocks from {1,10,100,1000}; 3 = 3D Q2 64^3 jitter 0.1; 4 = 2D Stokes
+// Q2-Q1 512^2, mu lognormal(0,1) per cell; 5 = 3D elasticity Q3 96^3,
+// E from {1,100} on 4^3-cell blocks, nu 0.3.
+bool gen_options_preset(int config, int64_t cells, pdb_gen_options* o) {
+  gen_options_defaults(o);
+  switch (config) {
+    case 1:
+      o->dim = 2, o->degree = 2, o->cells = 32, o->jitter = 0.1;
+      break;
+    case 2:
+      o->dim = 2, o->degree = 4, o->cells = 256, o->jitter = 0.05, o->coeff_kind = 1, o->block_cells = 8;
+      o->n_levels = 4;
+      o->levels[0] = 1.0, o->levels[1] = 10.0, o->levels[2] = 100.0, o->levels[3] = 1000.0;
+      break;
+    case 3:
+      o->dim = 3, o->degree = 2, o->cells = 64, o->jitter = 0.1;
+      break;
+    case 4:
+      o->physics = 1, o->dim = 2, o->degree = 2, o->cells = 512, o->coeff_kind = 2, o->coeff_value = 1.0;
+      break;
+    case 5:
+      o->physics = 2, o->dim = 3, o->degree = 3, o->cells = 96, o->coeff_kind = 1, o->block_cells = 4;
+      o->n_levels = 2, o->poisson_ratio = 0.3;
+      o->levels[0] = 1.0, o->levels[1] = 100.0;
+      break;
+    default:
+      return false;
+  }
+  if (cells > 0) o->cells = cells;
+  return true;
+}
+
 }  // namespace pdb

@@ -28,6 +28,9 @@ void write_matrix_market_host(const HostCsr& a, const std::string& path);
 void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out);
 // physics 1 (Stokes Q_p-Q_{p-1}, 2D) and 2 (linear elasticity): node-major vector DoFs
 void generate_system(const pdb_gen_options& o, pdb_problem_s& out);
+// pdb_gen_options defaults and the BASELINE config presets (false: config not in 1..5)
+void gen_options_defaults(pdb_gen_options* o);
+bool gen_options_preset(int config, int64_t cells, pdb_gen_options* o);
 
 // model_problem.cpp -- the reference's uniform-mesh model problems and the
 // two-level coarse space (pdb_problem_assemble, pdb_precond_create_combo)

@@ -12,6 +12,9 @@
 // (dense.cpp:59-61).  The working matrix lives in shared memory with an odd
 // leading dimension (conflict-free 8-byte lane-strided accesses) when it
 // fits, else in the output buffer itself.
+#include <cstdlib>
+
+#include "../common.hpp"
 #include "../kernels.hpp"
 
 namespace pdb::k {
@@ -105,6 +108,176 @@ __global__ void __launch_bounds__(kWarps * 32) lu_kernel(int64_t count, int ps, 
   if (lane == 0) status[t] = 0;
 }
 
+// ---------------------------------------------------------------------------
+// CTA per matrix (ps > kSmemMaxPs; config 5's 192-DoF elasticity patches).
+//
+// A 192 x 192 fp64 matrix (295 KB) does not fit the 227 KB of shared memory,
+// but after step k of the right-looking elimination rows < k are final (the
+// pivot search and every later swap only involve rows >= k), so only the
+// trailing block has to stay on chip.  Steps k < k0 run on the output buffer
+// in global memory (L2-resident: one matrix per SM), with coalesced row-wise
+// swaps and updates (warp per row, lane per column); at k0 the trailing
+// (ps-k0) x (ps-k0) block moves to shared memory (odd leading dimension) and
+// the remaining steps run there; the columns < k0 of rows >= k0 (the L part
+// from the global phase) stay in global memory and are swapped there.  k0 is
+// the smallest step whose trailing block fits (k0 = 32 at ps = 192; 0 for
+// ps <= 165).  Every element still sees a_ij <- a_ij - l_ik * u_kj for
+// k = 0, 1, ... in order, unfused, with l_ik by IEEE division and the skip
+// at l_ik == 0 (dense.cpp:66-72), so factors and pivots are bitwise the
+// reference's.
+constexpr int kCtaThreads = 512;
+constexpr int kCtaWarps = kCtaThreads / 32;
+constexpr size_t kCtaSmemCap = 220 * 1024;
+
+__host__ __device__ inline size_t cta_smem_bytes(int ps, int k0) {
+  const int t = ps - k0;
+  return ((size_t)t * (t | 1) + 2 * (size_t)ps + 2 * kCtaWarps) * sizeof(double) + (size_t)ps * sizeof(int32_t);
+}
+
+inline int cta_k0(int ps) {
+  int k0 = 0;
+  while (k0 < ps && cta_smem_bytes(ps, k0) > kCtaSmemCap) ++k0;
+  return k0;
+}
+
+// pivot of column k over rows [k, ps): the first row holding the maximum |.|
+// (dense.cpp:49-58); `at(i)` gives the element; warp-level, result in lane 0..31.
+template <typename At>
+__device__ __forceinline__ void column_pivot(int k, int ps, At at, double& best, int& p) {
+  const int lane = threadIdx.x & 31;
+  best = -1.0;
+  p = ps;
+  for (int i = k + lane; i < ps; i += 32) {
+    const double v = fabs(at(i));
+    if (v > best) {
+      best = v;
+      p = i;
+    }
+  }
+  warp_pivot(best, p);
+}
+
+__global__ void __launch_bounds__(kCtaThreads, 1)
+    lu_cta_kernel(int64_t count, int ps, int k0, const double* __restrict__ mats, const int32_t* __restrict__ src,
+                  double* __restrict__ lu, int32_t* __restrict__ piv, int32_t* __restrict__ status,
+                  double* __restrict__ fail_best) {
+  extern __shared__ double smem[];
+  const int tn = ps - k0, ldt = tn | 1;
+  double* T = smem;                                 // trailing block [tn][ldt]
+  double* colmax = T + (size_t)tn * ldt;            // [ps]
+  double* lcol = colmax + ps;                       // [ps] multipliers of the current step
+  double* red = lcol + ps;                          // [2 * warps] scratch
+  int32_t* perm = reinterpret_cast<int32_t*>(red + 2 * kCtaWarps);  // [ps]
+  __shared__ double s_best;
+  __shared__ int s_p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t len = (int64_t)ps * ps;
+
+  for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
+    const double* A = mats + (src ? (int64_t)src[t] : t) * len;
+    double* W = lu + t * len;
+    // column maxima of the input (order-free: max is exact), the input copied
+    // to W (global phase) or straight into T (k0 == 0)
+    for (int j = threadIdx.x; j < ps; j += kCtaThreads) {
+      double m = 0.0;
+      for (int i = 0; i < ps; ++i) m = fmax(m, fabs(A[(int64_t)i * ps + j]));
+      colmax[j] = m;
+      perm[j] = j;
+    }
+    if (k0 > 0)
+      for (int64_t e = threadIdx.x; e < len; e += kCtaThreads) W[e] = A[e];
+    else
+      for (int64_t e = threadIdx.x; e < len; e += kCtaThreads) T[(e / ps) * ldt + e % ps] = A[e];
+    __syncthreads();
+
+    bool failed = false;
+    for (int k = 0; k < ps; ++k) {
+      const bool on_chip = k >= k0;
+      if (k == k0 && k0 > 0) {  // move the trailing block on chip
+        for (int64_t e = threadIdx.x; e < (int64_t)tn * tn; e += kCtaThreads) {
+          const int r = (int)(e / tn), c = (int)(e % tn);
+          T[(size_t)r * ldt + c] = W[(int64_t)(k0 + r) * ps + k0 + c];
+        }
+        __syncthreads();
+      }
+      auto elem = [&](int i, int j) -> double& {
+        return on_chip && j >= k0 ? T[(size_t)(i - k0) * ldt + (j - k0)] : W[(int64_t)i * ps + j];
+      };
+      if (warp == 0) {
+        double best;
+        int p;
+        column_pivot(k, ps, [&](int i) { return elem(i, k); }, best, p);
+        if (lane == 0) {
+          s_best = best;
+          s_p = p;
+        }
+      }
+      __syncthreads();
+      const double best = s_best;
+      const int p = s_p;
+      if (best == 0.0 || best < __dmul_rn(1e-14, colmax[k])) {
+        if (threadIdx.x == 0) {
+          status[t] = k + 1;
+          fail_best[t] = best;
+        }
+        failed = true;
+        break;
+      }
+      if (p != k) {  // full row swap (dense.cpp:62-65)
+        for (int j = threadIdx.x; j < ps; j += kCtaThreads) {
+          double& a = elem(k, j);
+          double& b = elem(p, j);
+          const double x = a;
+          a = b;
+          b = x;
+        }
+        if (threadIdx.x == 0) {
+          const int32_t x = perm[k];
+          perm[k] = perm[p];
+          perm[p] = x;
+        }
+        __syncthreads();
+      }
+      const double pv = elem(k, k);
+      for (int i = k + 1 + (int)threadIdx.x; i < ps; i += kCtaThreads) {
+        double& a = elem(i, k);
+        const double l = __ddiv_rn(a, pv);
+        a = l;
+        lcol[i] = l;
+      }
+      __syncthreads();
+      // trailing update: warp per row, lane per column (coalesced in either memory)
+      if (on_chip) {
+        const double* Uk = T + (size_t)(k - k0) * ldt - k0;
+        for (int i = k + 1 + warp; i < ps; i += kCtaWarps) {
+          const double l = lcol[i];
+          if (l == 0.0) continue;
+          double* Ti = T + (size_t)(i - k0) * ldt - k0;
+          for (int j = k + 1 + lane; j < ps; j += 32) Ti[j] = __dsub_rn(Ti[j], __dmul_rn(l, Uk[j]));
+        }
+      } else {
+        const double* Uk = W + (int64_t)k * ps;
+        for (int i = k + 1 + warp; i < ps; i += kCtaWarps) {
+          const double l = lcol[i];
+          if (l == 0.0) continue;
+          double* Wi = W + (int64_t)i * ps;
+          for (int j = k + 1 + lane; j < ps; j += 32) Wi[j] = __dsub_rn(Wi[j], __dmul_rn(l, Uk[j]));
+        }
+      }
+      __syncthreads();
+    }
+    if (!failed) {
+      for (int64_t e = threadIdx.x; e < (int64_t)tn * tn; e += kCtaThreads) {
+        const int r = (int)(e / tn), c = (int)(e % tn);
+        W[(int64_t)(k0 + r) * ps + k0 + c] = T[(size_t)r * ldt + c];
+      }
+      for (int j = threadIdx.x; j < ps; j += kCtaThreads) piv[t * ps + j] = perm[j];
+      if (threadIdx.x == 0) status[t] = 0;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, double* lu, int32_t* piv,
@@ -115,6 +288,20 @@ void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, d
     const size_t smem = (size_t)kWarps * ((size_t)ps * (ps | 1) + ps) * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(lu_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lu_kernel<true><<<grid, kWarps * 32, smem, s>>>(count, ps, mats, src, lu, piv, status, fail_best);
+  } else if (cta_smem_bytes(ps, cta_k0(ps)) <= kCtaSmemCap && std::getenv("PDB_LU_WARP") == nullptr) {
+    const int k0 = cta_k0(ps);
+    const size_t smem = cta_smem_bytes(ps, k0);
+    static int configured[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !configured[dev]) {
+      PDB_CUDA(cudaFuncSetAttribute(lu_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCtaSmemCap + 4096));
+      configured[dev] = 1;
+    }
+    int sms = 148;
+    PDB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned g = (unsigned)std::min<int64_t>(count, (int64_t)sms);
+    lu_cta_kernel<<<g, kCtaThreads, smem, s>>>(count, ps, k0, mats, src, lu, piv, status, fail_best);
   } else {
     const size_t smem = (size_t)kWarps * ps * sizeof(double);
     lu_kernel<false><<<grid, kWarps * 32, smem, s>>>(count, ps, mats, src, lu, piv, status, fail_best);

@@ -15,6 +15,7 @@
 // plus the setup kernels of these structures (inverses, inverse maps).
 #include <cub/cub.cuh>
 
+#include "../common.hpp"
 #include "../kernels.hpp"
 #include "pdl.cuh"
 
@@ -464,6 +465,93 @@ __global__ void invert_factors_kernel(int64_t nf, int ps, const double* __restri
   }
 }
 
+// Explicit inverse for larger patches (ps > 32): one CTA per (factor, block
+// of 32 columns), the 32 right-hand sides P e_c held in shared memory
+// [ps][33] (lane = column: conflict-free), L and U read as warp-uniform
+// broadcasts.  Forward then backward substitution in row blocks of 8: each
+// warp takes one row of the block and accumulates the contributions of all
+// rows before the block (the dense part), warp 0 finishes the 8 rows in
+// order.  Not bit-exact with the thread-per-column kernel (the sweep
+// tolerance is 1e-9).
+constexpr int kInvRows = 8;
+constexpr int kInvLd = 33;
+
+__global__ void __launch_bounds__(kInvRows * 32)
+    invert_block_kernel(int64_t nf, int ps, const double* __restrict__ lu, const int32_t* __restrict__ piv,
+                        double* __restrict__ inv) {
+  extern __shared__ double X[];  // [ps][kInvLd]
+  double* part = X + (size_t)ps * kInvLd;  // [kInvRows][32]
+  const int nb = (ps + 31) / 32;
+  const int64_t f = blockIdx.x / nb;
+  const int c0 = (int)(blockIdx.x % nb) * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* L = lu + f * (int64_t)ps * ps;
+  const int32_t* P = piv + f * ps;
+  for (int i = warp; i < ps; i += kInvRows) X[i * kInvLd + lane] = P[i] == c0 + lane ? 1.0 : 0.0;
+  __syncthreads();
+  // forward: L y = P e_c (unit lower)
+  for (int b0 = 0; b0 < ps; b0 += kInvRows) {
+    const int i = b0 + warp;
+    if (i < ps) {
+      const double* Li = L + (int64_t)i * ps;
+      double s0 = X[i * kInvLd + lane], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = 0;
+      for (; j + 4 <= b0; j += 4) {
+        s0 -= Li[j] * X[j * kInvLd + lane];
+        s1 -= Li[j + 1] * X[(j + 1) * kInvLd + lane];
+        s2 -= Li[j + 2] * X[(j + 2) * kInvLd + lane];
+        s3 -= Li[j + 3] * X[(j + 3) * kInvLd + lane];
+      }
+      for (; j < b0; ++j) s0 -= Li[j] * X[j * kInvLd + lane];
+      part[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+    if (warp == 0)
+      for (int r = 0; r < kInvRows && b0 + r < ps; ++r) {
+        const int ii = b0 + r;
+        const double* Li = L + (int64_t)ii * ps;
+        double s = part[r * 32 + lane];
+        for (int j = b0; j < ii; ++j) s -= Li[j] * X[j * kInvLd + lane];
+        X[ii * kInvLd + lane] = s;
+      }
+    __syncthreads();
+  }
+  // backward: U x = y
+  for (int e0 = ps; e0 > 0; e0 -= kInvRows) {  // rows [max(e0-8,0), e0)
+    const int lo = e0 - kInvRows > 0 ? e0 - kInvRows : 0;
+    const int i = e0 - 1 - warp;
+    if (i >= lo) {
+      const double* Ui = L + (int64_t)i * ps;
+      double s0 = X[i * kInvLd + lane], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = e0;
+      for (; j + 4 <= ps; j += 4) {
+        s0 -= Ui[j] * X[j * kInvLd + lane];
+        s1 -= Ui[j + 1] * X[(j + 1) * kInvLd + lane];
+        s2 -= Ui[j + 2] * X[(j + 2) * kInvLd + lane];
+        s3 -= Ui[j + 3] * X[(j + 3) * kInvLd + lane];
+      }
+      for (; j < ps; ++j) s0 -= Ui[j] * X[j * kInvLd + lane];
+      part[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+    if (warp == 0)
+      for (int ii = e0 - 1; ii >= lo; --ii) {
+        const double* Ui = L + (int64_t)ii * ps;
+        double s = part[(e0 - 1 - ii) * 32 + lane];
+        for (int j = ii + 1; j < e0; ++j) s -= Ui[j] * X[j * kInvLd + lane];
+        X[ii * kInvLd + lane] = s / Ui[ii];
+      }
+    __syncthreads();
+  }
+  // column-major output: column c0 + c, rows contiguous
+  const int nc = ps - c0 < 32 ? ps - c0 : 32;
+  double* out = inv + f * (int64_t)ps * ps + (int64_t)c0 * ps;
+  for (int e = threadIdx.x; e < nc * ps; e += kInvRows * 32) {
+    const int c = e / ps, i = e % ps;
+    out[(int64_t)c * ps + i] = X[i * kInvLd + c];
+  }
+}
+
 __global__ void scatter_update_kernel(int64_t n, const int32_t* __restrict__ inv_ptr, const int32_t* __restrict__ inv,
                                       const double* __restrict__ sols, const double* __restrict__ omega_w,
                                       const double* __restrict__ x_in, double* __restrict__ z_out,
@@ -576,7 +664,7 @@ void patch_apply_grouped(int ntiles, int ps, const int32_t* tile_entry, const in
   if (ntiles <= 0) return;
   const size_t smem = ((size_t)ps * ps + (size_t)max_tile * ps) * sizeof(double);
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(patch_apply_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PDB_CUDA(cudaFuncSetAttribute(patch_apply_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int threads = ps >= 256 ? ps : (256 / ps) * ps;
   patch_apply_grouped_kernel<<<(unsigned)ntiles, threads, smem, s>>>(ps, tile_entry, tile_start, tile_idx, order,
                                                                      Binv, r, in_scale, sols);
@@ -603,10 +691,14 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
     int kstr = ks * 4;
     if (kstr % 8 == 0) kstr += 4;
     const size_t smem = (size_t)kDmmaTile * kstr * sizeof(double);
-    static size_t opted = 48 * 1024;
-    if (smem > opted) {
-      cudaFuncSetAttribute(patch_apply_dmma_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      opted = smem;
+    // the opt-in is per device: cache the largest size set on each
+    static size_t opted[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (smem > 48 * 1024 && (dev >= 64 || smem > opted[dev])) {
+      PDB_CUDA(cudaFuncSetAttribute(patch_apply_dmma_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      if (dev < 64) opted[dev] = smem;
     }
     launch_pdl(patch_apply_dmma_large_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s, ps, mt, ks, kstr,
                tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);
@@ -667,7 +759,23 @@ void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const doubl
 }
 
 void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s) {
-  if (nf > 0) invert_factors_kernel<<<(unsigned)((nf + 3) / 4), 128, 0, s>>>(nf, ps, lu, piv, inv);
+  if (nf <= 0) return;
+  if (ps <= 32) {
+    invert_factors_kernel<<<(unsigned)((nf + 3) / 4), 128, 0, s>>>(nf, ps, lu, piv, inv);
+    return;
+  }
+  const size_t smem = ((size_t)ps * kInvLd + kInvRows * 32) * sizeof(double);
+  if (smem > 48 * 1024) {
+    static int configured[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (dev < 64 && !configured[dev]) {
+      PDB_CUDA(cudaFuncSetAttribute(invert_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      configured[dev] = 1;
+    }
+  }
+  const int64_t blocks = nf * ((ps + 31) / 32);
+  invert_block_kernel<<<(unsigned)blocks, kInvRows * 32, smem, s>>>(nf, ps, lu, piv, inv);
 }
 
 void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,

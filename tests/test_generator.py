@@ -1,8 +1,13 @@
 """The seeded input generator (host-only, no GPU): sizes of the BASELINE
 configs, agreement with the reference assembler on uniform meshes,
 determinism, Dirichlet-row conventions."""
+import os
+import sys
+
 import numpy as np
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_config1_sizes(P):
@@ -85,3 +90,15 @@ def test_invalid_generator_options(P):
     with pytest.raises(P.PatchdbError) as e:
         P.Problem.generate(1, jitter=0.6)
     assert e.value.status == P.PDB_ERR_INVALID_ARGUMENT
+
+
+@pytest.mark.parametrize("cfg,cells", [(1, 0), (2, 16), (3, 6), (4, 8), (5, 3)])
+def test_standalone_generator_library_matches(P, cfg, cells):
+    """inputs/libpdbgen.so (the generator without libpatchdb, used by the
+    reference arm of bench.py) produces the same bytes as pdb_problem_generate."""
+    sys.path.insert(0, os.path.join(ROOT, "inputs"))
+    import pdbgen
+    g = pdbgen.Generated(cfg, cells)
+    p = P.Problem.generate(cfg, cells)
+    assert all(np.array_equal(x, y) for x, y in zip(g.csr(), p.csr()))
+    assert np.array_equal(g.rhs(), p.rhs())
