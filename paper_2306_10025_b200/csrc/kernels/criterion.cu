@@ -12,6 +12,7 @@
 //   greedy resolution   greedy_impl compress.cpp:40-95 (round-batched, exact)
 //   k-means steps       kmeans_loop compress.cpp:150-166 (assignment),
 //                       entrywise_mean_indexed dense.cpp:211-223 (update)
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 
@@ -64,6 +65,218 @@ __global__ void __launch_bounds__(kL1Threads) l1_pairs_kernel(int64_t npat, cons
   if (live)
     for (int c = 0; c < kL1Ent; ++c)
       if (e0 + c < ne) d[t * ne + e0 + c] = acc[c];
+}
+
+// ------------------------------------------------------- tiled L1 ----
+// One block = 64 patches x tiles of 32 entries; thread (tp, te) keeps the
+// 16 running sums of patches tp + 16 i and entries te + 8 j (i, j < 4) in
+// registers.  The patch and entry matrices are staged k-chunk by k-chunk
+// (32 entries of each matrix, 8-byte cp.async, double-buffered) into shared
+// memory rows of odd stride, so every load of the inner loop is a
+// bank-conflict-free broadcast and each staged value feeds 4 (patch) or 8
+// (entry) pairs.  Each pair is still summed by one thread in ascending k
+// from 0.0 with |a - b| (dense.cpp:192-197), so distances are bitwise the
+// sequential kernel's.  Modes: all pair distances, the greedy first-/best-
+// match scan (compress.cpp:63-83), the k-means argmin (compress.cpp:154-160).
+constexpr int kTP = 64, kTE = 32, kTK = 32, kTL = kTK + 1, kTThreads = 128;
+constexpr size_t kTStage = (size_t)(kTP + kTE) * kTL;  // doubles per stage
+enum L1Mode { kL1Pairs = 0, kL1Scan = 1, kL1Argmin = 2 };
+
+struct L1Args {
+  int64_t npat;
+  const int32_t* pid;  // patch rows (null: 0..npat-1)
+  int len;
+  const double* mats;
+  int64_t e0, e1;         // entries [e0, e1)
+  const int32_t* rep_src;  // entry e -> patch id in mats, else reps + e*len
+  const double* reps;
+  double* d;  // pairs: d[t * (e1 - e0) + (e - e0)]
+  double eps;
+  int best_match;
+  int32_t* phi;  // scan: match (phi[me]); argmin: previous assignment (read)
+  double* best_d;
+  int32_t* new_phi;
+  double* min_dist;
+  int32_t* changed;
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int Mode>
+__global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
+  extern __shared__ double sm[];  // 2 stages [kTP + kTE][kTL]; the epilogue tile aliases stage 0
+  __shared__ const double* psrc[kTP];
+  __shared__ const double* esrc[kTE];
+  __shared__ int32_t pme[kTP];
+  const int t = threadIdx.x, tp = t >> 3, te = t & 7;
+  const int64_t p0 = (int64_t)blockIdx.x * kTP;
+  const int len = a.len;
+  if (t < kTP) {
+    const int64_t g = p0 + t;
+    const int32_t id = g < a.npat ? (a.pid ? a.pid[g] : (int32_t)g) : -1;
+    pme[t] = id;
+    psrc[t] = id >= 0 ? a.mats + (int64_t)id * len : nullptr;
+  }
+  // per-patch state, owned by thread t < kTP
+  bool done = true;
+  double cur = CUDART_INF;
+  int32_t cur_j = -1;
+  if (t < kTP && p0 + t < a.npat) {
+    done = false;
+    if (Mode == kL1Scan) {
+      cur = a.eps;
+      if (a.best_match) {
+        const int32_t me = a.pid[p0 + t];
+        cur = a.best_d[me];
+        cur_j = a.phi[me];
+      }
+    } else if (Mode == kL1Argmin) {
+      cur_j = 0;
+    }
+  }
+  const int nchunk = (len + kTK - 1) / kTK;
+  // pairs: entry tiles split over gridDim.y; scan / argmin keep one block per patch tile (ordered state)
+  for (int64_t et0 = a.e0 + (int64_t)blockIdx.y * kTE; et0 < a.e1; et0 += (int64_t)gridDim.y * kTE) {
+    if (Mode == kL1Scan && !a.best_match) {
+      if (__syncthreads_and(done)) break;
+    } else {
+      __syncthreads();
+    }
+    const int ne = a.e1 - et0 < kTE ? (int)(a.e1 - et0) : kTE;
+    if (t < kTE) {
+      const int64_t e = et0 + t;
+      esrc[t] = t < ne ? (a.rep_src ? a.mats + (int64_t)a.rep_src[e] * len : a.reps + e * len) : nullptr;
+    }
+    __syncthreads();
+    auto issue = [&](int c) {
+      double* st = sm + (size_t)(c & 1) * kTStage;
+      const int k0 = c * kTK;
+      const int qn = min(kTK, len - k0);
+      for (int idx = t; idx < (kTP + kTE) * kTK; idx += kTThreads) {
+        const int r = idx / kTK, k = idx % kTK;
+        const double* src = r < kTP ? psrc[r] : esrc[r - kTP];
+        if (k < qn && src) cp_async8(st + r * kTL + k, src + k0 + k);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    issue(0);
+    for (int c = 0; c < nchunk; ++c) {
+      if (c + 1 < nchunk) {
+        issue(c + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const double* A = sm + (size_t)(c & 1) * kTStage;
+      const double* B = A + kTP * kTL;
+      const int qn = min(kTK, len - c * kTK);
+#pragma unroll 4
+      for (int k = 0; k < qn; ++k) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = A[(tp + 16 * i) * kTL + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = B[(te + 8 * j) * kTL + k];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
+      }
+      __syncthreads();  // the stage is refilled by issue(c + 2)
+    }
+    if (Mode == kL1Pairs) {
+      const int64_t ld = a.e1 - a.e0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int64_t g = p0 + tp + 16 * i;
+        if (g >= a.npat) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int e = te + 8 * j;
+          if (e < ne) a.d[g * ld + (et0 - a.e0) + e] = acc[i][j];
+        }
+      }
+      continue;
+    }
+    // scan / argmin: the tile's distances through shared memory, then each
+    // patch walks its entries in ascending order
+    double* D = sm;  // [kTP][kTE + 1], aliases stage 0 (all reads of it are done)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) D[(tp + 16 * i) * (kTE + 1) + te + 8 * j] = acc[i][j];
+    __syncthreads();
+    if (t < kTP && !done) {
+      const double* Dr = D + t * (kTE + 1);
+      if (Mode == kL1Argmin) {
+        for (int e = 0; e < ne; ++e)
+          if (Dr[e] < cur) {  // strict <: lowest index wins ties (compress.cpp:154-160)
+            cur = Dr[e];
+            cur_j = (int32_t)(et0 + e);
+          }
+      } else if (a.best_match) {
+        const int32_t me = pme[t];
+        for (int e = 0; e < ne; ++e) {
+          const int64_t j = et0 + e;
+          if (a.rep_src[j] < me && Dr[e] < cur) {
+            cur = Dr[e];
+            cur_j = (int32_t)j;
+          }
+        }
+      } else {
+        for (int e = 0; e < ne; ++e)
+          if (Dr[e] < a.eps) {  // first match (compress.cpp:77-80)
+            cur_j = (int32_t)(et0 + e);
+            done = true;
+            break;
+          }
+      }
+    }
+  }
+  if (t >= kTP || p0 + t >= a.npat) return;
+  if (Mode == kL1Scan) {
+    const int32_t me = pme[t];
+    if (a.best_match) {
+      a.best_d[me] = cur;
+      a.phi[me] = cur_j;
+    } else if (cur_j >= 0) {
+      a.phi[me] = cur_j;
+    }
+  } else if (Mode == kL1Argmin) {
+    const int64_t g = p0 + t;
+    a.new_phi[g] = cur_j;
+    a.min_dist[g] = cur;
+    if (cur_j != a.phi[g]) atomicOr(a.changed, 1);
+  }
+}
+
+template <int Mode>
+void l1_tile_launch(const L1Args& a, cudaStream_t s) {
+  const size_t smem = 2 * kTStage * sizeof(double);
+  static_assert(2 * kTStage >= (size_t)kTP * (kTE + 1), "epilogue tile must fit stage memory");
+  if (smem > 48 * 1024) cudaFuncSetAttribute(l1_tile_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  unsigned gy = 1;
+  if (Mode == kL1Pairs) {
+    // enough blocks to fill the GPU when the patch count is small (greedy batches: 1024 x 1024)
+    const int64_t tiles = (a.e1 - a.e0 + kTE - 1) / kTE;
+    const int64_t px = (a.npat + kTP - 1) / kTP;
+    gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (4 * 148 + px - 1) / px));
+  }
+  l1_tile_kernel<Mode><<<dim3(grid_for(a.npat, kTP), gy), kTThreads, smem, s>>>(a);
+}
+
+bool l1_tiled_enabled() {  // PDB_L1_TILED=0: the thread-per-patch kernels below (A/B runs, tests)
+  const char* e = getenv("PDB_L1_TILED");
+  return !(e && e[0] == '0');
 }
 
 // First-/best-match scan of unresolved patches over entries [e0, e1)
@@ -167,6 +380,96 @@ __global__ void apply_scan_kernel(int64_t nu, const int32_t* __restrict__ pid, i
 // D[a][b] < eps, best-match the smallest D < eps (ties: lowest b).  Batch
 // members were unmatched against every earlier entry, so this reproduces the
 // sequential pass exactly.
+// Batch resolution, two phases (one block of 1024 threads).  Whether b < a
+// is a candidate for a (D[a][b] < eps) does not depend on the sequential
+// state, so all candidate bits are computed first in parallel (one ballot
+// per 32 columns) into shared memory; the sequential pass over a then only
+// intersects a's candidate words with the bit set of batch members that
+// became entries (lane l holds word l): first match = the lowest set bit;
+// best match = the smallest D among the set bits, ties to the lowest b --
+// exactly the scan of the one-warp kernel below (compress.cpp:63-92).
+constexpr int kResolveMax = 1024;
+
+__global__ void __launch_bounds__(1024) greedy_resolve_bits_kernel(
+    int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps, int best_match,
+    int64_t abort_above, const int32_t* __restrict__ lu_status, int32_t* __restrict__ phi,
+    int32_t* __restrict__ creators, int32_t* __restrict__ entry_of, int64_t* state) {
+  extern __shared__ uint32_t cand[];  // [B][32]
+  __shared__ int32_t ent_s[kResolveMax];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int words = (B + 31) / 32;
+  for (int a = warp; a < B; a += 32) {
+    for (int w = 0; w < words; ++w) {
+      const int b = w * 32 + lane;
+      const bool c = b < a && D[(int64_t)a * B + b] < eps;
+      const uint32_t bits = __ballot_sync(0xffffffffu, c);
+      if (lane == 0) cand[a * 32 + w] = bits;
+    }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  uint32_t ent = 0;  // word `lane` of the entry bit set
+  int64_t m = state[0];
+  for (int a = 0; a < B; ++a) {
+    const uint32_t w = lane < words ? cand[a * 32 + lane] & ent : 0u;
+    int bb = B;
+    if (!best_match) {
+      const uint32_t any = __ballot_sync(0xffffffffu, w != 0);
+      if (any) {
+        const int L = __ffs(any) - 1;
+        const uint32_t wl = __shfl_sync(0xffffffffu, w, L);
+        bb = L * 32 + __ffs(wl) - 1;
+      }
+    } else {
+      double bd = eps;
+      uint32_t r = w;
+      while (r) {
+        const int b = lane * 32 + __ffs(r) - 1;
+        r &= r - 1;
+        const double dv = D[(int64_t)a * B + b];
+        if (dv < bd) {
+          bd = dv;
+          bb = b;
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, bd, off);
+        const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
+        if (od < bd || (od == bd && ob < bb)) {
+          bd = od;
+          bb = ob;
+        }
+      }
+    }
+    if (bb < B) {
+      if (lane == 0) {
+        phi[S[a]] = ent_s[bb];
+        entry_of[a] = -1;
+      }
+      continue;
+    }
+    if (abort_above > 0 && m + 1 > abort_above) {
+      if (lane == 0) state[1] = 1;
+      break;
+    }
+    if (lu_status && lu_status[a] != 0) {
+      if (lane == 0) state[2] = a;
+      break;
+    }
+    if (lane == 0) {
+      creators[m] = S[a];
+      phi[S[a]] = (int32_t)m;
+      entry_of[a] = (int32_t)m;
+      ent_s[a] = (int32_t)m;
+    }
+    if (lane == (a >> 5)) ent |= 1u << (a & 31);
+    ++m;
+    __syncwarp();
+  }
+  if (lane == 0) state[0] = m;
+}
+
 __global__ void greedy_resolve_kernel(int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps,
                                       int best_match, int64_t abort_above, const int32_t* __restrict__ lu_status,
                                       int32_t* __restrict__ phi, int32_t* __restrict__ creators,
@@ -903,6 +1206,13 @@ void interleave_patches_perm(int64_t count, int64_t len, const int32_t* perm, co
 void l1_pairs(int64_t npat, const int32_t* pid, int64_t ne, int len, const double* mats, const int32_t* rep_src,
               const double* reps, double* d, cudaStream_t s) {
   if (npat <= 0 || ne <= 0) return;
+  if (l1_tiled_enabled()) {
+    L1Args a{};
+    a.npat = npat, a.pid = pid, a.len = len, a.mats = mats, a.e0 = 0, a.e1 = ne, a.rep_src = rep_src, a.reps = reps;
+    a.d = d;
+    l1_tile_launch<kL1Pairs>(a, s);
+    return;
+  }
   dim3 grid(grid_for(npat, kL1Threads), (unsigned)((ne + kL1Ent - 1) / kL1Ent));
   l1_pairs_kernel<<<grid, kL1Threads, 0, s>>>(npat, pid, ne, len, mats, rep_src, reps, d);
 }
@@ -937,6 +1247,15 @@ void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int be
                     const int32_t* lu_status, int32_t* phi, int32_t* creators, int32_t* entry_of, int64_t* state,
                     cudaStream_t s) {
   if (B <= 0) return;
+  const char* e = getenv("PDB_RESOLVE_BITS");
+  if (B <= kResolveMax && !(e && e[0] == '0')) {
+    const size_t smem = (size_t)B * 32 * sizeof(uint32_t);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(greedy_resolve_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    greedy_resolve_bits_kernel<<<1, 1024, smem, s>>>(B, S, D, eps, best_match, abort_above, lu_status, phi, creators,
+                                                     entry_of, state);
+    return;
+  }
   greedy_resolve_kernel<<<1, 32, 0, s>>>(B, S, D, eps, best_match, abort_above, lu_status, phi, creators, entry_of,
                                          state);
 }
@@ -944,6 +1263,13 @@ void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int be
 void l1_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t e1, int len, const double* mats,
              const int32_t* creators, double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s) {
   if (nu <= 0 || e1 <= e0) return;
+  if (l1_tiled_enabled()) {
+    L1Args a{};
+    a.npat = nu, a.pid = pid, a.len = len, a.mats = mats, a.e0 = e0, a.e1 = e1, a.rep_src = creators;
+    a.eps = eps, a.best_match = best_match, a.phi = phi, a.best_d = best_d;
+    l1_tile_launch<kL1Scan>(a, s);
+    return;
+  }
   l1_scan_kernel<<<grid_for(nu, kL1Threads), kL1Threads, 0, s>>>(nu, pid, e0, e1, len, mats, creators, eps, best_match,
                                                                  phi, best_d);
 }
@@ -961,6 +1287,13 @@ void argmin_assign(int64_t n, int64_t ne, const double* d, const int32_t* phi, i
 
 void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double* reps, const int32_t* phi,
                int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s) {
+  if (n > 0 && l1_tiled_enabled()) {
+    L1Args a{};
+    a.npat = n, a.len = len, a.mats = mats, a.e0 = 0, a.e1 = ne, a.reps = reps;
+    a.phi = const_cast<int32_t*>(phi), a.new_phi = new_phi, a.min_dist = min_dist, a.changed = changed;
+    l1_tile_launch<kL1Argmin>(a, s);
+    return;
+  }
   if (n > 0)
     l1_argmin_kernel<<<grid_for(n, kL1Threads), kL1Threads, 0, s>>>(n, ne, len, mats, reps, phi, new_phi, min_dist,
                                                                     changed);

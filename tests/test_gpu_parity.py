@@ -468,3 +468,28 @@ def test_objective_and_compressibility_curve(name, request, P, ref):
         db.objective(c.A, c.ps, -1.0)
     with pytest.raises(P.PatchdbError):
         P.compressibility_curve(c.A, c.ps, P.GREEDY_L1, [0.1, 0.01])
+
+
+@pytest.mark.parametrize("name,ps", [("c1", 9), ("c2s", 25), ("c3s", 27)])
+def test_l1_tiled_kernels_match_thread_per_patch(name, ps, request, P, monkeypatch):
+    """The tiled l1 kernels (64 patches x 32 entries per block, staged k-chunks)
+    and the candidate-bit batch resolution give bitwise the databases of the
+    thread-per-patch kernels and the one-warp resolution: greedy first / best
+    match and entrywise k-means (assignment by argmin and by pairs)."""
+    case = request.getfixturevalue(name)
+    A, pset = case.A, case.ps
+    builds = [dict(method=P.GREEDY_L1, eps=e, best_match=bm) for e in (0.5, 2.0) for bm in (False, True)]
+    builds.append(dict(method=P.KMEANS_ENTRYWISE, db_size=max(30, pset.count // 8), seed=3, max_iters=12))
+    for kw in builds:
+        kw = dict(kw)
+        method = kw.pop("method")
+        monkeypatch.setenv("PDB_L1_TILED", "1")
+        a = P.Database.build(A, pset, method, **kw)
+        monkeypatch.setenv("PDB_L1_TILED", "0")
+        monkeypatch.setenv("PDB_RESOLVE_BITS", "0")  # and the one-warp batch resolution
+        b = P.Database.build(A, pset, method, **kw)
+        monkeypatch.delenv("PDB_L1_TILED")
+        monkeypatch.delenv("PDB_RESOLVE_BITS")
+        assert a.size == b.size, kw
+        assert np.array_equal(a.phi(), b.phi()), kw
+        assert np.array_equal(a.representatives(), b.representatives()), kw
