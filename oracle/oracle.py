@@ -353,8 +353,25 @@ class RefLib:
         L.refh_coarse_factor.argtypes = [_P, _I64, _I64, _D, _I64]
         L.refh_combo_new.argtypes = [_P, _P, _P, C.c_double, C.c_int, C.POINTER(_P)]
         L.refh_export_matrix.argtypes = [C.c_char_p, C.c_char_p]
+        L.refh_read_mm.argtypes = [C.c_char_p, C.POINTER(_P)]
+        L.refh_write_mm.argtypes = [_P, C.c_char_p]
         L.refh_problem_from_csr.restype = _P
         L.refh_problem_from_csr.argtypes = [C.c_int64, _I64, _I64, _D, _D, C.c_int, C.c_int64, C.c_int]
+
+    def read_matrix_market(self, path: str):
+        """read_matrix_market (matrix_market.cpp:29-91): CSR arrays, or CheckerError."""
+        out = _P()
+        self._check(self.lib.refh_read_mm(path.encode(), C.byref(out)))
+        m = out.value
+        n, nnz = self.lib.refh_matrix_n(m), self.lib.refh_matrix_nnz(m)
+        rp, ci, v = np.empty(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+        self.lib.refh_matrix_csr(m, _ip(rp), _ip(ci), _dp(v))
+        self.lib.refh_matrix_free(m)
+        return rp, ci, v
+
+    def write_matrix_market(self, csr, path: str):
+        m = self.matrix(csr)
+        self._check(self.lib.refh_write_mm(m.ptr, path.encode()))
 
     def problem_from_csr(self, csr, rhs, dim, cells, degree):
         rp, ci, v = (_i64(csr[0]), _i64(csr[1]), _f64(csr[2]))

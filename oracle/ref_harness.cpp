@@ -28,6 +28,7 @@
 #include "core/experiments.hpp"
 #include "core/fem.hpp"
 #include "core/gmres.hpp"
+#include "core/matrix_market.hpp"
 #include "core/patch.hpp"
 #include "core/precond.hpp"
 #include "core/sparse.hpp"
@@ -98,6 +99,16 @@ struct RefPc {
 RH_API const char* refh_last_error(void) { return g_err.c_str(); }
 
 /* ---- matrices ---- */
+
+// read_matrix_market(path) (matrix_market.cpp:87-91): status + matrix
+RH_API int refh_read_mm(const char* path, void** out) {
+  return guarded([&] { *out = new SparseMatrix(read_matrix_market(std::string(path))); });
+}
+
+// write_matrix_market(a, path) (matrix_market.cpp:105-110)
+RH_API int refh_write_mm(void* m, const char* path) {
+  return guarded([&] { write_matrix_market(*static_cast<SparseMatrix*>(m), std::string(path)); });
+}
 
 RH_API void* refh_matrix_new(int64_t n, const int64_t* rp, const int64_t* ci, const double* v) {
   auto* m = new SparseMatrix();

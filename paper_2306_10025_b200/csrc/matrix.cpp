@@ -1,6 +1,5 @@
-// Device CSR matrices: validation + upload, SpMV, Matrix Market I/O.
-// Reference: sparse.hpp:20-39 (CSR invariants), sparse.cpp:12-48
-// (from_triplets), matrix_market.cpp:29-110 (I/O).
+// Device CSR matrices: validation + upload, SpMV (Matrix Market I/O in
+// mmio.cpp).  Reference: sparse.hpp:20-39 (CSR invariants).
 #include <algorithm>
 #include <cctype>
 #include <cmath>
@@ -325,123 +324,6 @@ void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s)
   const k::SpmvPlan plan = plan_of(a);
   k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, y, s);
   PDB_LAUNCH_CHECK();
-}
-
-// ---- Matrix Market (matrix_market.cpp:29-110) ----------------------------
-
-namespace {
-
-[[noreturn]] void parse_fail(const std::string& name, long line, const std::string& what) {
-  fail(Errc::parse_error, name + ": line " + std::to_string(line) + ": " + what);
-}
-
-std::string lower(std::string s) {
-  std::transform(s.begin(), s.end(), s.begin(), [](unsigned char c) { return static_cast<char>(std::tolower(c)); });
-  return s;
-}
-
-bool blank(const std::string& s) { return s.find_first_not_of(" \t\r\n") == std::string::npos; }
-
-struct Trip {
-  Index r, c;
-  double v;
-};
-
-}  // namespace
-
-// from_triplets (sparse.cpp:12-48): stable sort by (row, col), duplicates
-// summed in insertion order, zero sums kept in the pattern.
-HostCsr csr_from_triplets(Index n, std::vector<Trip>& t);
-
-HostCsr read_matrix_market_host(const std::string& path) {
-  std::ifstream in(path);
-  if (!in) fail(Errc::io_error, "cannot open '" + path + "' for reading");
-  const std::string& name = path;
-  std::string line;
-  long lineno = 0;
-  if (!std::getline(in, line)) parse_fail(name, 1, "empty file");
-  ++lineno;
-  std::istringstream hs(line);
-  std::string banner, object, format, field, symmetry;
-  hs >> banner >> object >> format >> field >> symmetry;
-  if (banner != "%%MatrixMarket") parse_fail(name, lineno, "missing %%MatrixMarket banner");
-  if (lower(object) != "matrix" || lower(format) != "coordinate")
-    parse_fail(name, lineno, "only coordinate-format matrices are supported");
-  if (lower(field) != "real") parse_fail(name, lineno, "only real matrices are supported");
-  const std::string sym = lower(symmetry);
-  if (sym != "general" && sym != "symmetric") parse_fail(name, lineno, "only general or symmetric matrices are supported");
-  const bool expand = sym == "symmetric";
-  Index rows = 0, cols = 0;
-  long long nnz = 0;
-  for (;;) {
-    if (!std::getline(in, line)) parse_fail(name, lineno + 1, "unexpected end of file before size line");
-    ++lineno;
-    if (!line.empty() && line[0] == '%') continue;
-    if (blank(line)) continue;
-    std::istringstream ss(line);
-    if (!(ss >> rows >> cols >> nnz)) parse_fail(name, lineno, "malformed size line");
-    break;
-  }
-  if (rows != cols)
-    fail(Errc::non_square_matrix,
-         name + ": matrix is " + std::to_string(rows) + "x" + std::to_string(cols) + ", expected square");
-  std::vector<Trip> entries;
-  entries.reserve(static_cast<size_t>(expand ? 2 * nnz : nnz));
-  for (long long k = 0; k < nnz; ++k) {
-    if (!std::getline(in, line)) parse_fail(name, lineno + 1, "unexpected end of file in entry list");
-    ++lineno;
-    if (blank(line)) {
-      --k;
-      continue;
-    }
-    std::istringstream ss(line);
-    Index i = 0, j = 0;
-    double v = 0.0;
-    if (!(ss >> i >> j >> v)) parse_fail(name, lineno, "malformed entry");
-    if (i < 1 || i > rows || j < 1 || j > cols) parse_fail(name, lineno, "entry index out of range");
-    if (!std::isfinite(v)) parse_fail(name, lineno, "non-finite entry value");
-    entries.push_back({i - 1, j - 1, v});
-    if (expand && i != j) entries.push_back({j - 1, i - 1, v});
-  }
-  return csr_from_triplets(rows, entries);
-}
-
-HostCsr csr_from_triplets(Index n, std::vector<Trip>& t) {
-  require(n >= 0, Errc::invalid_argument, "negative matrix dimension");
-  std::stable_sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) { return a.r != b.r ? a.r < b.r : a.c < b.c; });
-  HostCsr h;
-  h.n = n;
-  h.row_ptr.assign(static_cast<size_t>(n + 1), 0);
-  size_t k = 0;
-  for (Index i = 0; i < n; ++i) {
-    while (k < t.size() && t[k].r == i) {
-      const Index c = t[k].c;
-      double v = t[k].v;
-      ++k;
-      while (k < t.size() && t[k].r == i && t[k].c == c) {
-        v += t[k].v;
-        ++k;
-      }
-      h.col.push_back(static_cast<int32_t>(c));
-      h.val.push_back(v);
-    }
-    h.row_ptr[static_cast<size_t>(i + 1)] = static_cast<int64_t>(h.col.size());
-  }
-  return h;
-}
-
-void write_matrix_market_host(const HostCsr& a, const std::string& path) {
-  std::ofstream out(path);
-  if (!out) fail(Errc::io_error, "cannot open '" + path + "' for writing");
-  out << "%%MatrixMarket matrix coordinate real general\n";
-  out << a.n << ' ' << a.n << ' ' << a.nnz() << '\n';
-  char buf[64];
-  for (Index i = 0; i < a.n; ++i)
-    for (Index p = a.row_ptr[static_cast<size_t>(i)]; p < a.row_ptr[static_cast<size_t>(i + 1)]; ++p) {
-      std::snprintf(buf, sizeof(buf), "%.17g", a.val[static_cast<size_t>(p)]);
-      out << (i + 1) << ' ' << (a.col[static_cast<size_t>(p)] + 1) << ' ' << buf << '\n';
-    }
-  if (!out) fail(Errc::io_error, "error while writing '" + path + "'");
 }
 
 }  // namespace pdb
