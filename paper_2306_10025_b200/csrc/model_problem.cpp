@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "fem1d.hpp"
 #include "host.hpp"
 
 namespace pdb {
@@ -355,68 +356,10 @@ double forcing(const ModelConfig& m, const double* x, int dim) {
   return 0.0;
 }
 
-// ---------------------------------------------------------------------------
-// 1D tables: Gauss-Legendre on [0,1] by Newton on P_n over [-1,1]
-// (quadrature.cpp:10-41) and the equispaced Lagrange basis (:43-75).
-
-struct Rule1D {
-  std::vector<double> x, w;
-};
-
-Rule1D gauss_rule(int n) {
-  require(n >= 1, Errc::invalid_argument, "quadrature order must be >= 1");
-  Rule1D r;
-  r.x.assign(static_cast<size_t>(n), 0.0);
-  r.w.assign(static_cast<size_t>(n), 0.0);
-  for (int i = 0; i < (n + 1) / 2; ++i) {
-    double z = std::cos(kPi * (static_cast<double>(i) + 0.75) / (static_cast<double>(n) + 0.5));
-    double dp = 0.0;
-    for (int it = 0; it < 100; ++it) {
-      double pm = 1.0, pc = z;
-      for (int k = 2; k <= n; ++k) {
-        const double pn = ((2.0 * k - 1.0) * z * pc - (k - 1.0) * pm) / static_cast<double>(k);
-        pm = pc;
-        pc = pn;
-      }
-      dp = static_cast<double>(n) * (z * pc - pm) / (z * z - 1.0);
-      const double step = pc / dp;
-      z -= step;
-      if (std::abs(step) < 1e-15) break;
-    }
-    const double w = 2.0 / ((1.0 - z * z) * dp * dp);
-    r.x[static_cast<size_t>(i)] = 0.5 * (1.0 - z);
-    r.w[static_cast<size_t>(i)] = 0.5 * w;
-    r.x[static_cast<size_t>(n - 1 - i)] = 0.5 * (1.0 + z);
-    r.w[static_cast<size_t>(n - 1 - i)] = 0.5 * w;
-  }
-  return r;
-}
-
-// val[a*nq + q], der[a*nq + q] of the degree-p basis on nodes a/p.
-void basis_tables(int p, const Rule1D& r, std::vector<double>& val, std::vector<double>& der) {
-  const size_t nq = r.x.size();
-  std::vector<double> node(static_cast<size_t>(p) + 1);
-  for (int a = 0; a <= p; ++a) node[static_cast<size_t>(a)] = static_cast<double>(a) / static_cast<double>(p);
-  val.assign((static_cast<size_t>(p) + 1) * nq, 0.0);
-  der.assign((static_cast<size_t>(p) + 1) * nq, 0.0);
-  for (int a = 0; a <= p; ++a)
-    for (size_t q = 0; q < nq; ++q) {
-      const double x = r.x[q], xa = node[static_cast<size_t>(a)];
-      double v = 1.0;
-      for (int b = 0; b <= p; ++b)
-        if (b != a) v *= (x - node[static_cast<size_t>(b)]) / (xa - node[static_cast<size_t>(b)]);
-      double d = 0.0;
-      for (int m = 0; m <= p; ++m) {
-        if (m == a) continue;
-        double t = 1.0 / (xa - node[static_cast<size_t>(m)]);
-        for (int b = 0; b <= p; ++b)
-          if (b != a && b != m) t *= (x - node[static_cast<size_t>(b)]) / (xa - node[static_cast<size_t>(b)]);
-        d += t;
-      }
-      val[static_cast<size_t>(a) * nq + q] = v;
-      der[static_cast<size_t>(a) * nq + q] = d;
-    }
-}
+// 1D tables: the generator's Gauss-Legendre rule on [0,1] and equispaced
+// Lagrange basis (fem1d.hpp).  Quadrature nodes and weights may differ from
+// the reference's quadrature.cpp in the last bit, so assembled values agree
+// with the reference's to rounding (tests/test_model_problem.py).
 
 struct Lattice {
   int dim;
@@ -465,9 +408,9 @@ void validate_model(const ModelConfig& m) {
 std::vector<double> load_vector(const ModelConfig& m, const Lattice& L) {
   const int p = m.degree;
   const double h = 1.0 / static_cast<double>(m.cells);
-  const Rule1D r = gauss_rule(p + 1);
+  const Gauss r = gauss_legendre01(p + 1);
   std::vector<double> val, der;
-  basis_tables(p, r, val, der);
+  lagrange_tables(p, r, val, der);
   const size_t nq = r.x.size();
   const double jac = std::pow(h, m.dim);
   std::vector<double> f(static_cast<size_t>(L.n), 0.0);
@@ -581,9 +524,9 @@ void assemble_model_problem(const ModelConfig& m, pdb_problem_s& out) {
   const Lattice L(m.dim, m.cells, p);
   const double h = 1.0 / static_cast<double>(m.cells);
   const double invh = 1.0 / h;
-  const Rule1D r = gauss_rule(p + 1);
+  const Gauss r = gauss_legendre01(p + 1);
   std::vector<double> val, der;
-  basis_tables(p, r, val, der);
+  lagrange_tables(p, r, val, der);
   const size_t nq = r.x.size();
   const int cn = m.dim == 3 ? p + 1 : 1;
   const Index nloc = static_cast<Index>(p + 1) * (p + 1) * cn;
@@ -722,9 +665,9 @@ double model_l2_error(const pdb_problem_s& prob, const double* u) {
   const int p = prob.degree, dim = prob.dim;
   const Lattice L(dim, prob.cells, p);
   const double h = 1.0 / static_cast<double>(prob.cells);
-  const Rule1D r = gauss_rule(p + 3);
+  const Gauss r = gauss_legendre01(p + 3);
   std::vector<double> val, der;
-  basis_tables(p, r, val, der);
+  lagrange_tables(p, r, val, der);
   const size_t nq = r.x.size();
   const double jac = std::pow(h, dim);
   const Index czn = dim == 3 ? prob.cells : 1;
@@ -760,64 +703,51 @@ double model_l2_error(const pdb_problem_s& prob, const double* u) {
 }
 
 // ---------------------------------------------------------------------------
-// Coarse space (fem.cpp:385-479).
+// Two-level coarse space (the role of fem.cpp:433-479): bilinear hat
+// functions on the cell-corner vertices, P0 (fine DoFs x vertices), R0 = P0^T
+// and the Galerkin operator R0 A P0.
+//
+// P0 is separable: along one axis lattice index l lies in cell
+// c = min(l / p, cells - 1) at t = (l - c p) / p and touches vertices c and
+// c + 1 with weights 1 - t and t (zero weights dropped; t is an exact ratio
+// of integers); a DoF's row is the tensor product, vertices ascending.
+//
+// R0 A P0 is formed in one pass over the fine rows: row i of A P0 is
+// accumulated in a small sorted list (A's columns in stored order, each
+// spreading over <= 4 vertices), then scattered into every coarse row J of
+// P0's row i.  Fine rows are visited in ascending order, so each coarse
+// entry accumulates its contributions in ascending fine-row order, and each
+// A P0 entry in A's stored order -- the summation orders of the reference's
+// two sparse products, hence the same values.
 
 namespace {
 
-// C = A * B for CSR A (rows a_rows) and a transfer operator B, a dense
-// accumulator per output row and sorted touched columns.
-CoarseOp row_product(Index a_rows, const int64_t* arp, const int32_t* aci, const double* av, const CoarseOp& b) {
-  CoarseOp c;
-  c.rows = a_rows;
-  c.cols = b.cols;
-  c.ptr.assign(static_cast<size_t>(a_rows) + 1, 0);
-  std::vector<double> acc(static_cast<size_t>(b.cols), 0.0);
-  std::vector<char> seen(static_cast<size_t>(b.cols), 0);
-  std::vector<int32_t> touched;
-  for (Index i = 0; i < a_rows; ++i) {
-    touched.clear();
-    for (int64_t q = arp[i]; q < arp[i + 1]; ++q) {
-      const int32_t k = aci[q];
-      const double a = av[q];
-      for (int64_t t = b.ptr[static_cast<size_t>(k)]; t < b.ptr[static_cast<size_t>(k) + 1]; ++t) {
-        const int32_t j = b.col[static_cast<size_t>(t)];
-        if (!seen[static_cast<size_t>(j)]) {
-          seen[static_cast<size_t>(j)] = 1;
-          touched.push_back(j);
-        }
-        acc[static_cast<size_t>(j)] += a * b.val[static_cast<size_t>(t)];
-      }
-    }
-    std::sort(touched.begin(), touched.end());
-    for (int32_t j : touched) {
-      c.col.push_back(j);
-      c.val.push_back(acc[static_cast<size_t>(j)]);
-      acc[static_cast<size_t>(j)] = 0.0;
-      seen[static_cast<size_t>(j)] = 0;
-    }
-    c.ptr[static_cast<size_t>(i) + 1] = static_cast<int64_t>(c.col.size());
-  }
-  return c;
+struct Hat1D {
+  int n = 0;
+  Index v[2];
+  double w[2];
+};
+
+Hat1D hat(Index l, Index cells, int p) {
+  Hat1D h;
+  const Index c = std::min(l / p, cells - 1);
+  const double t = static_cast<double>(l - c * p) / static_cast<double>(p);
+  if (1.0 - t != 0.0) h.v[h.n] = c, h.w[h.n++] = 1.0 - t;
+  if (t != 0.0) h.v[h.n] = c + 1, h.w[h.n++] = t;
+  return h;
 }
 
-CoarseOp transpose_op(const CoarseOp& b) {
-  CoarseOp t;
-  t.rows = b.cols;
-  t.cols = b.rows;
-  t.ptr.assign(static_cast<size_t>(b.cols) + 1, 0);
-  for (int32_t c : b.col) ++t.ptr[static_cast<size_t>(c) + 1];
-  for (size_t i = 1; i < t.ptr.size(); ++i) t.ptr[i] += t.ptr[i - 1];
-  t.col.resize(b.col.size());
-  t.val.resize(b.val.size());
-  std::vector<int64_t> next(t.ptr.begin(), t.ptr.end() - 1);
-  for (Index i = 0; i < b.rows; ++i)
-    for (int64_t q = b.ptr[static_cast<size_t>(i)]; q < b.ptr[static_cast<size_t>(i) + 1]; ++q) {
-      const int64_t slot = next[static_cast<size_t>(b.col[static_cast<size_t>(q)])]++;
-      t.col[static_cast<size_t>(slot)] = static_cast<int32_t>(i);
-      t.val[static_cast<size_t>(slot)] = b.val[static_cast<size_t>(q)];
-    }
-  return t;
-}
+// sorted (column, value) accumulator for one sparse row
+struct RowAcc {
+  std::vector<std::pair<int32_t, double>> e;
+  void add(int32_t j, double v) {
+    auto it = std::lower_bound(e.begin(), e.end(), j, [](const auto& x, int32_t k) { return x.first < k; });
+    if (it != e.end() && it->first == j)
+      it->second += v;
+    else
+      e.insert(it, {j, 0.0 + v});  // from 0.0 as a dense accumulator would: -0.0 becomes +0.0
+  }
+};
 
 }  // namespace
 
@@ -829,33 +759,71 @@ CoarseSpaceHost build_coarse_space(const pdb_problem_s& prob) {
   require(prob.components == 1, Errc::invalid_argument, "coarse transfer needs a scalar (one DoF per node) problem");
   const Lattice L(2, prob.cells, prob.degree);
   require(prob.a.n == L.n, Errc::dimension_mismatch, "matrix size does not match mesh");
-  const Index cells = prob.cells;
-  const int p = prob.degree;
-  const Index nca = cells + 1;
+  const Index nv = prob.cells + 1;  // vertices per axis
 
   CoarseSpaceHost cs;
   CoarseOp& P = cs.p0;
   P.rows = L.n;
-  P.cols = nca * nca;
-  P.ptr.assign(static_cast<size_t>(L.n) + 1, 0);
-  for (Index dof = 0; dof < L.n; ++dof) {
-    const Index lx = dof % L.npa, ly = (dof / L.npa) % L.npa;
-    const Index cx = std::min(lx / p, cells - 1), cy = std::min(ly / p, cells - 1);
-    const double xi = static_cast<double>(lx - cx * p) / static_cast<double>(p);
-    const double eta = static_cast<double>(ly - cy * p) / static_cast<double>(p);
-    const Index v00 = cx + nca * cy;
-    const Index vs[4] = {v00, v00 + 1, v00 + nca, v00 + nca + 1};
-    const double ws[4] = {(1.0 - xi) * (1.0 - eta), xi * (1.0 - eta), (1.0 - xi) * eta, xi * eta};
-    for (int t = 0; t < 4; ++t) {
-      if (ws[t] == 0.0) continue;  // xi, eta are exact ratios of integers
-      P.col.push_back(static_cast<int32_t>(vs[t]));
-      P.val.push_back(ws[t]);
-    }
-    P.ptr[static_cast<size_t>(dof) + 1] = static_cast<int64_t>(P.col.size());
+  P.cols = nv * nv;
+  P.ptr.resize(static_cast<size_t>(L.n) + 1);
+  P.ptr[0] = 0;
+  for (Index d = 0; d < L.n; ++d) {
+    const Hat1D hx = hat(d % L.npa, prob.cells, prob.degree), hy = hat(d / L.npa, prob.cells, prob.degree);
+    for (int b = 0; b < hy.n; ++b)
+      for (int a = 0; a < hx.n; ++a) {
+        P.col.push_back(static_cast<int32_t>(hx.v[a] + nv * hy.v[b]));
+        P.val.push_back(hx.w[a] * hy.w[b]);
+      }
+    P.ptr[static_cast<size_t>(d) + 1] = static_cast<int64_t>(P.col.size());
   }
-  const CoarseOp AP = row_product(prob.a.n, prob.a.row_ptr.data(), prob.a.col.data(), prob.a.val.data(), P);
-  cs.r0 = transpose_op(P);
-  cs.coarse = row_product(cs.r0.rows, cs.r0.ptr.data(), cs.r0.col.data(), cs.r0.val.data(), AP);
+
+  // R0 = P0^T by counting sort (fine rows ascending within each vertex row)
+  CoarseOp& R = cs.r0;
+  R.rows = P.cols;
+  R.cols = P.rows;
+  R.ptr.assign(static_cast<size_t>(R.rows) + 1, 0);
+  for (int32_t c : P.col) ++R.ptr[static_cast<size_t>(c) + 1];
+  for (size_t k = 1; k < R.ptr.size(); ++k) R.ptr[k] += R.ptr[k - 1];
+  R.col.resize(P.col.size());
+  R.val.resize(P.val.size());
+  {
+    std::vector<int64_t> at(R.ptr.begin(), R.ptr.end() - 1);
+    for (Index d = 0; d < P.rows; ++d)
+      for (int64_t q = P.ptr[static_cast<size_t>(d)]; q < P.ptr[static_cast<size_t>(d) + 1]; ++q) {
+        const int64_t o = at[static_cast<size_t>(P.col[static_cast<size_t>(q)])]++;
+        R.col[static_cast<size_t>(o)] = static_cast<int32_t>(d);
+        R.val[static_cast<size_t>(o)] = P.val[static_cast<size_t>(q)];
+      }
+  }
+
+  // Galerkin operator, one pass over the fine rows
+  std::vector<RowAcc> G(static_cast<size_t>(P.cols));
+  RowAcc ap;
+  const HostCsr& A = prob.a;
+  for (Index i = 0; i < A.n; ++i) {
+    ap.e.clear();
+    for (int64_t q = A.row_ptr[static_cast<size_t>(i)]; q < A.row_ptr[static_cast<size_t>(i) + 1]; ++q) {
+      const int32_t k = A.col[static_cast<size_t>(q)];
+      const double a = A.val[static_cast<size_t>(q)];
+      for (int64_t t = P.ptr[static_cast<size_t>(k)]; t < P.ptr[static_cast<size_t>(k) + 1]; ++t)
+        ap.add(P.col[static_cast<size_t>(t)], a * P.val[static_cast<size_t>(t)]);
+    }
+    for (int64_t t = P.ptr[static_cast<size_t>(i)]; t < P.ptr[static_cast<size_t>(i) + 1]; ++t) {
+      const double r = P.val[static_cast<size_t>(t)];
+      RowAcc& g = G[static_cast<size_t>(P.col[static_cast<size_t>(t)])];
+      for (const auto& [j, v] : ap.e) g.add(j, r * v);
+    }
+  }
+  CoarseOp& Cm = cs.coarse;
+  Cm.rows = Cm.cols = P.cols;
+  Cm.ptr.assign(static_cast<size_t>(P.cols) + 1, 0);
+  for (Index J = 0; J < P.cols; ++J) {
+    for (const auto& [j, v] : G[static_cast<size_t>(J)].e) {
+      Cm.col.push_back(j);
+      Cm.val.push_back(v);
+    }
+    Cm.ptr[static_cast<size_t>(J) + 1] = static_cast<int64_t>(Cm.col.size());
+  }
   return cs;
 }
 

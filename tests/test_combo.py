@@ -46,9 +46,12 @@ CASES = [
 
 
 def _pair(P, ref, cfg):
+    """Our model problem, and the reference's DiscreteProblem around the SAME
+    matrix and right-hand side (the assemblers agree only to rounding), so the
+    coarse space, band factor and solves compare bitwise."""
     js = json.dumps(cfg)
     p = P.Problem.assemble(js)
-    r = ref.problem(js)
+    r = ref.problem_from_csr(p.csr(), p.rhs(), cfg.get("dim", 2), cfg["cells"], cfg["degree"])
     A = p.matrix()
     ps = P.PatchSet.detect(A, (cfg["degree"] + 1) ** 2)
     rA = r.matrix()
