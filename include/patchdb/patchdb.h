@@ -190,6 +190,17 @@ PDB_API void pdb_gen_options_init(pdb_gen_options* opts);
 PDB_API pdb_status pdb_gen_options_config(int config, int64_t cells, pdb_gen_options* opts);
 PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* opts, pdb_problem* out);
 PDB_API int64_t pdb_problem_nnz(pdb_problem p);
+/* Slab of rank `rank` of `nranks` along the slowest mesh axis (cells
+ * [C rank / nranks, C (rank+1) / nranks), at least two cell layers each):
+ * only the rows of the slab's DoFs are generated, bitwise equal to the same
+ * rows of pdb_problem_generate, with GLOBAL column ids; pdb_problem_rows /
+ * _nnz / _csr / _rhs describe those local rows.  Input of pdb_shard_create_local. */
+PDB_API pdb_status pdb_problem_generate_slab(const pdb_gen_options* opts, int rank, int nranks, pdb_problem* out);
+/* Global row count of the (slab) problem, and its global row ranges
+ * [lo, hi) as 2 * count int64 values (count = pdb_problem_row_range_count). */
+PDB_API int64_t pdb_problem_rows_global(pdb_problem p);
+PDB_API int64_t pdb_problem_row_range_count(pdb_problem p);
+PDB_API pdb_status pdb_problem_row_ranges(pdb_problem p, int64_t* ranges);
 PDB_API pdb_status pdb_problem_csr(pdb_problem p, int64_t* row_ptr, int64_t* col_idx, double* values);
 
 /* Patch-set contents (host copies): patches[count*patch_size] ascending per patch; weights[rows]. */

@@ -207,6 +207,8 @@ PDB_API int64_t pdb_problem_nnz(pdb_problem p) { return p == nullptr ? 0 : p->a.
 PDB_API pdb_status pdb_problem_matrix(pdb_problem p, pdb_matrix* out) {
   if (p == nullptr || out == nullptr) return arg_error("null argument");
   return guarded([&] {
+    require(!p->is_slab(), Errc::invalid_argument,
+            "slab problem holds a row block with global columns: use pdb_shard_create_local");
     auto m = std::make_unique<pdb_matrix_s>();
     upload_csr(p->a, m->a, default_stream());
     *out = m.release();
@@ -263,6 +265,47 @@ PDB_API pdb_status pdb_problem_generate(const pdb_gen_options* o, pdb_problem* o
     else
       generate_system(*o, *p);
     *out = p.release();
+  });
+}
+
+PDB_API pdb_status pdb_problem_generate_slab(const pdb_gen_options* o, int rank, int nranks, pdb_problem* out) {
+  if (o == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(o->physics >= 0 && o->physics <= 2, Errc::invalid_argument,
+            "physics must be 0 (diffusion), 1 (Stokes) or 2 (elasticity)");
+    require(o->bc_mode == 0, Errc::invalid_argument, "only Dirichlet row replacement (bc_mode 0) is supported");
+    const RowWindow w = slab_window(*o, rank, nranks);
+    auto p = std::make_unique<pdb_problem_s>();
+    if (o->physics == 0)
+      generate_scalar(*o, *p, &w);
+    else
+      generate_system(*o, *p, &w);
+    p->slab_rank = rank;
+    p->slab_ranks = nranks;
+    *out = p.release();
+  });
+}
+
+PDB_API int64_t pdb_problem_rows_global(pdb_problem p) {
+  return p == nullptr ? 0 : (p->is_slab() ? p->n_global : p->a.n);
+}
+
+PDB_API int64_t pdb_problem_row_range_count(pdb_problem p) {
+  return p == nullptr ? 0 : (p->is_slab() ? static_cast<int64_t>(p->row_ranges.size()) : 1);
+}
+
+PDB_API pdb_status pdb_problem_row_ranges(pdb_problem p, int64_t* r) {
+  if (p == nullptr || r == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    if (!p->is_slab()) {
+      r[0] = 0;
+      r[1] = p->a.n;
+      return;
+    }
+    for (size_t k = 0; k < p->row_ranges.size(); ++k) {
+      r[2 * k] = p->row_ranges[k].first;
+      r[2 * k + 1] = p->row_ranges[k].second;
+    }
   });
 }
 

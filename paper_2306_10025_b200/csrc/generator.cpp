@@ -51,7 +51,7 @@ void parallel_for(Index n, int threads, F&& fn) {
 
 }  // namespace
 
-void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
+void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win) {
   require(o.dim == 2 || o.dim == 3, Errc::invalid_argument, "mesh dimension must be 2 or 3");
   require(o.cells >= 1, Errc::invalid_argument, "mesh needs at least one cell per axis");
   require(o.degree >= 1, Errc::invalid_degree, "polynomial degree must be >= 1");
@@ -121,13 +121,18 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
     if (d == 3 && (iz == 0 || iz == npa - 1)) return true;
     return false;
   };
+  RowWindow all;
+  all.ranges = {{0, n}};
+  const RowWindow& Wn = win ? *win : all;
+  const Index nr = Wn.rows();
   HostCsr& A = out.a;
-  A.n = n;
-  A.row_ptr.assign(static_cast<size_t>(n + 1), 0);
-  parallel_for(n, threads, [&](Index b, Index e) {
-    for (Index i = b; i < e; ++i) {
+  A.n = nr;
+  A.row_ptr.assign(static_cast<size_t>(nr + 1), 0);
+  parallel_for(nr, threads, [&](Index b, Index e) {
+    for (Index li = b; li < e; ++li) {
+      const Index i = Wn.global(li);
       if (on_boundary(i)) {
-        A.row_ptr[static_cast<size_t>(i + 1)] = 1;
+        A.row_ptr[static_cast<size_t>(li + 1)] = 1;
         continue;
       }
       Index cnt = 1;
@@ -137,17 +142,18 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
         axis_range(lat[k], lo, w);
         cnt *= w;
       }
-      A.row_ptr[static_cast<size_t>(i + 1)] = cnt;
+      A.row_ptr[static_cast<size_t>(li + 1)] = cnt;
     }
   });
-  for (Index i = 0; i < n; ++i) A.row_ptr[static_cast<size_t>(i + 1)] += A.row_ptr[static_cast<size_t>(i)];
-  const Index nnz = A.row_ptr[static_cast<size_t>(n)];
+  for (Index i = 0; i < nr; ++i) A.row_ptr[static_cast<size_t>(i + 1)] += A.row_ptr[static_cast<size_t>(i)];
+  const Index nnz = A.row_ptr[static_cast<size_t>(nr)];
   require(n < (Index{1} << 31), Errc::invalid_argument, "generator: more than 2^31 rows");
   A.col.resize(static_cast<size_t>(nnz));
   A.val.assign(static_cast<size_t>(nnz), 0.0);
-  parallel_for(n, threads, [&](Index b, Index e) {
-    for (Index i = b; i < e; ++i) {
-      Index pos = A.row_ptr[static_cast<size_t>(i)];
+  parallel_for(nr, threads, [&](Index b, Index e) {
+    for (Index li = b; li < e; ++li) {
+      const Index i = Wn.global(li);
+      Index pos = A.row_ptr[static_cast<size_t>(li)];
       if (on_boundary(i)) {
         A.col[static_cast<size_t>(pos)] = static_cast<int32_t>(i);
         A.val[static_cast<size_t>(pos)] = 1.0;
@@ -221,6 +227,8 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
       for (Index t = b; t < e; ++t) {
         const Index cx = px + 2 * (t % cxn), cy = py + 2 * ((t / cxn) % cyn), cz = d == 3 ? pz + 2 * (t / (cxn * cyn)) : 0;
         const Index cell = cx + C * (cy + C * cz);
+        const Index slow = d == 3 ? cz : cy;
+        if (slow < Wn.cell_lo || slow > Wn.cell_hi) continue;  // touches no window row
         double Xc[8][3];
         for (int c = 0; c < ncorner; ++c) {
           const Index v = (cx + (c & 1)) + nva * ((cy + ((c >> 1) & 1)) + nva * (cz + ((c >> 2) & 1)));
@@ -283,10 +291,12 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
         for (int a = 0; a < nloc; ++a) {
           const Index gi = dofs[static_cast<size_t>(a)];
           if (on_boundary(gi)) continue;  // row replaced (fem.cpp:323)
+          const Index li = win ? Wn.local(gi) : gi;
+          if (li < 0) continue;
           const Index lat[3] = {gi % npa, (gi / npa) % npa, d == 3 ? gi / (npa * npa) : 0};
           Index lo[3] = {0, 0, 0}, w[3] = {1, 1, 1};
           for (int k = 0; k < d; ++k) axis_range(lat[k], lo[k], w[k]);
-          const Index base = A.row_ptr[static_cast<size_t>(gi)];
+          const Index base = A.row_ptr[static_cast<size_t>(li)];
           for (int bb = 0; bb < nloc; ++bb) {
             const Index gj = dofs[static_cast<size_t>(bb)];
             const Index jl[3] = {gj % npa, (gj / npa) % npa, d == 3 ? gj / (npa * npa) : 0};
@@ -299,12 +309,17 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
   }
 
   // --- right-hand side ----------------------------------------------------
-  out.rhs.assign(static_cast<size_t>(n), 0.0);
+  out.rhs.assign(static_cast<size_t>(nr), 0.0);
   {
-    std::mt19937_64 rng(o.seed + 2);
-    for (Index i = 0; i < n; ++i) {
-      const double u = unit(rng);
-      if (!on_boundary(i)) out.rhs[static_cast<size_t>(i)] = 2.0 * u - 1.0;
+    std::mt19937_64 rng(o.seed + 2);  // one draw per global row
+    Index at = 0, li = 0;
+    for (const auto& g : Wn.ranges) {
+      rng.discard(static_cast<unsigned long long>(g.first - at));
+      for (Index i = g.first; i < g.second; ++i, ++li) {
+        const double u = unit(rng);
+        if (!on_boundary(i)) out.rhs[static_cast<size_t>(li)] = 2.0 * u - 1.0;
+      }
+      at = g.second;
     }
   }
   out.has_exact = false;
@@ -312,6 +327,8 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
   out.cells = C;
   out.degree = p;
   out.components = 1;
+  out.n_global = n;
+  if (win) out.row_ranges.assign(win->ranges.begin(), win->ranges.end());
 }
 
 // ---- vector systems: Stokes (config 4) and linear elasticity (config 5) ----
@@ -335,7 +352,7 @@ void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out) {
 // 2 = lognormal exp(coeff_value * z), z ~ N(0,1) by Box-Muller on the seed+1
 // stream.  Right-hand side: U[-1,1] on free velocity / displacement rows,
 // 0 on Dirichlet and pressure rows (seed+2 stream, one draw per DoF).
-void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
+void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win) {
   require(o.physics == 1 || o.physics == 2, Errc::invalid_argument, "physics must be 1 (Stokes) or 2 (elasticity)");
   const bool stokes = o.physics == 1;
   require(o.dim == 2 || o.dim == 3, Errc::invalid_argument, "mesh dimension must be 2 or 3");
@@ -467,11 +484,16 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
     return r;
   };
 
+  RowWindow all;
+  all.ranges = {{0, n}};
+  const RowWindow& Wn = win ? *win : all;
+  const Index nr = Wn.rows();
   HostCsr& A = out.a;
-  A.n = n;
-  A.row_ptr.assign(static_cast<size_t>(n + 1), 0);
-  parallel_for(n, threads, [&](Index b, Index e) {
-    for (Index i = b; i < e; ++i) {
+  A.n = nr;
+  A.row_ptr.assign(static_cast<size_t>(nr + 1), 0);
+  parallel_for(nr, threads, [&](Index b, Index e) {
+    for (Index li = b; li < e; ++li) {
+      const Index i = Wn.global(li);
       Index cnt;
       if (i < nu) {
         const Index v = i / ncomp;
@@ -488,16 +510,17 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
         lattice(i - nu, ppa, q);
         cnt = pres_ranges(q).nvel;
       }
-      A.row_ptr[static_cast<size_t>(i + 1)] = cnt;
+      A.row_ptr[static_cast<size_t>(li + 1)] = cnt;
     }
   });
-  for (Index i = 0; i < n; ++i) A.row_ptr[static_cast<size_t>(i + 1)] += A.row_ptr[static_cast<size_t>(i)];
-  const Index nnz = A.row_ptr[static_cast<size_t>(n)];
+  for (Index i = 0; i < nr; ++i) A.row_ptr[static_cast<size_t>(i + 1)] += A.row_ptr[static_cast<size_t>(i)];
+  const Index nnz = A.row_ptr[static_cast<size_t>(nr)];
   A.col.resize(static_cast<size_t>(nnz));
   A.val.assign(static_cast<size_t>(nnz), 0.0);
-  parallel_for(n, threads, [&](Index b, Index e) {
-    for (Index i = b; i < e; ++i) {
-      Index pos = A.row_ptr[static_cast<size_t>(i)];
+  parallel_for(nr, threads, [&](Index b, Index e) {
+    for (Index li = b; li < e; ++li) {
+      const Index i = Wn.global(li);
+      Index pos = A.row_ptr[static_cast<size_t>(li)];
       if (i < nu && boundary_node(i / ncomp)) {
         A.col[static_cast<size_t>(pos)] = static_cast<int32_t>(i);
         A.val[static_cast<size_t>(pos)] = 1.0;
@@ -590,6 +613,8 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
       for (Index t = b; t < e; ++t) {
         const Index cx = px + 2 * (t % cxn), cy = py + 2 * ((t / cxn) % cyn), cz = d == 3 ? pz + 2 * (t / (cxn * cyn)) : 0;
         const Index cell = cx + C * (cy + C * cz);
+        const Index slow = d == 3 ? cz : cy;
+        if (slow < Wn.cell_lo || slow > Wn.cell_hi) continue;  // touches no window row
         double Xc[8][3];
         for (int c = 0; c < ncorner; ++c) {
           const Index v = (cx + (c & 1)) + nva * ((cy + ((c >> 1) & 1)) + nva * (cz + ((c >> 2) & 1)));
@@ -675,7 +700,9 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
           lattice(gv, npa, l);
           const Range r = node_ranges(l);
           for (int c = 0; c < ncomp; ++c) {
-            const Index base = A.row_ptr[static_cast<size_t>(ncomp * gv + c)];
+            const Index li = win ? Wn.local(ncomp * gv + c) : ncomp * gv + c;
+            if (li < 0) continue;
+            const Index base = A.row_ptr[static_cast<size_t>(li)];
             for (int bn = 0; bn < nloc; ++bn) {
               Index jl[3];
               lattice(node[static_cast<size_t>(bn)], npa, jl);
@@ -696,7 +723,9 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
           Index ql[3];
           lattice(pnode[static_cast<size_t>(i)], ppa, ql);
           const Range r = pres_ranges(ql);
-          const Index base = A.row_ptr[static_cast<size_t>(nu + pnode[static_cast<size_t>(i)])];
+          const Index li = win ? Wn.local(nu + pnode[static_cast<size_t>(i)]) : nu + pnode[static_cast<size_t>(i)];
+          if (li < 0) continue;
+          const Index base = A.row_ptr[static_cast<size_t>(li)];
           for (int bn = 0; bn < nloc; ++bn) {
             Index jl[3];
             lattice(node[static_cast<size_t>(bn)], npa, jl);
@@ -709,19 +738,53 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out) {
     });
   }
 
-  out.rhs.assign(static_cast<size_t>(n), 0.0);
+  out.rhs.assign(static_cast<size_t>(nr), 0.0);
   {
-    std::mt19937_64 rng(o.seed + 2);
-    for (Index i = 0; i < n; ++i) {
-      const double u = unit(rng);
-      if (i < nu && !boundary_node(i / ncomp)) out.rhs[static_cast<size_t>(i)] = 2.0 * u - 1.0;
+    std::mt19937_64 rng(o.seed + 2);  // one draw per global row
+    Index at = 0, li = 0;
+    for (const auto& g : Wn.ranges) {
+      rng.discard(static_cast<unsigned long long>(g.first - at));
+      for (Index i = g.first; i < g.second; ++i, ++li) {
+        const double u = unit(rng);
+        if (i < nu && !boundary_node(i / ncomp)) out.rhs[static_cast<size_t>(li)] = 2.0 * u - 1.0;
+      }
+      at = g.second;
     }
   }
+  out.n_global = n;
+  if (win) out.row_ranges.assign(win->ranges.begin(), win->ranges.end());
   out.has_exact = false;
   out.dim = d;
   out.cells = C;
   out.degree = p;
   out.components = 0;  // vector / mixed DoFs: no scalar lattice
+}
+
+RowWindow slab_window(const pdb_gen_options& o, int rank, int nranks) {
+  require(nranks >= 1 && rank >= 0 && rank < nranks, Errc::invalid_argument, "rank must be in [0, nranks)");
+  const Index C = o.cells;
+  const int d = o.dim, p = o.degree;
+  const Index s0 = C * rank / nranks, s1 = C * (rank + 1) / nranks;
+  require(nranks == 1 || C / nranks >= 2, Errc::invalid_argument,
+          "slab partition too thin: every rank needs at least two cell layers");
+  const Index npa = C * p + 1;
+  const Index layer = d == 3 ? npa * npa : npa;  // nodes per slowest-axis layer
+  RowWindow w;
+  w.cell_lo = s0 > 0 ? s0 - 1 : 0;
+  w.cell_hi = std::min<Index>(C - 1, s1);
+  if (o.physics == 0) {
+    w.ranges.push_back({s0 * p * layer, (s1 * p + 1) * layer});
+  } else {
+    const Index ncomp = d;
+    w.ranges.push_back({ncomp * s0 * p * layer, ncomp * (s1 * p + 1) * layer});
+    if (o.physics == 1) {
+      const Index pp = p - 1, ppa = C * pp + 1;
+      const Index player = d == 3 ? ppa * ppa : ppa;
+      const Index nu = ncomp * (d == 3 ? npa * npa * npa : npa * npa);
+      w.ranges.push_back({nu + s0 * pp * player, nu + (s1 * pp + 1) * player});
+    }
+  }
+  return w;
 }
 
 void gen_options_defaults(pdb_gen_options* o) {

@@ -2,6 +2,7 @@
 // the per-subsystem sources.
 #pragma once
 
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -25,9 +26,42 @@ HostCsr read_matrix_market_host(const std::string& path);
 void write_matrix_market_host(const HostCsr& a, const std::string& path);
 
 // generator.cpp
-void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out);
+// Rows a generator assembles: sorted disjoint global ranges [lo, hi), and the
+// cells along the slowest axis that touch them (inclusive).  Default: all.
+struct RowWindow {
+  std::vector<std::pair<Index, Index>> ranges;
+  Index cell_lo = 0, cell_hi = INT64_MAX;
+  Index rows() const {
+    Index r = 0;
+    for (const auto& g : ranges) r += g.second - g.first;
+    return r;
+  }
+  Index global(Index li) const {
+    for (const auto& g : ranges) {
+      if (li < g.second - g.first) return g.first + li;
+      li -= g.second - g.first;
+    }
+    return -1;
+  }
+  Index local(Index gi) const {
+    Index off = 0;
+    for (const auto& g : ranges) {
+      if (gi >= g.first && gi < g.second) return off + gi - g.first;
+      off += g.second - g.first;
+    }
+    return -1;
+  }
+};
+// win == nullptr: the whole problem.  Otherwise only the window's rows, with
+// global column ids, bitwise equal to the same rows of the whole problem
+// (cells are assembled colour by colour in the same order; skipping cells
+// that touch no window row removes no contribution to a window row).
+void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win = nullptr);
 // physics 1 (Stokes Q_p-Q_{p-1}, 2D) and 2 (linear elasticity): node-major vector DoFs
-void generate_system(const pdb_gen_options& o, pdb_problem_s& out);
+void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win = nullptr);
+// Slab of rank r of W along the slowest axis: cells [C r / W, C (r+1) / W);
+// the rows are every DoF of those cells (both faces included).
+RowWindow slab_window(const pdb_gen_options& o, int rank, int nranks);
 // pdb_gen_options defaults and the BASELINE config presets (false: config not in 1..5)
 void gen_options_defaults(pdb_gen_options* o);
 bool gen_options_preset(int config, int64_t cells, pdb_gen_options* o);

@@ -88,6 +88,12 @@ struct pdb_problem_s {
   int64_t cells = 0;
   int degree = 1;
   int components = 1;  // DoFs per lattice node (vector generators: > 1)
+  // slab problems (pdb_problem_generate_slab): the global row ranges held,
+  // the global size; a.n is the local row count, a.col holds global ids
+  std::vector<std::pair<int64_t, int64_t>> row_ranges;
+  int64_t n_global = 0;
+  int slab_rank = 0, slab_ranks = 1;
+  bool is_slab() const { return !row_ranges.empty(); }
 };
 
 struct pdb_matrix_s {

@@ -116,6 +116,10 @@ _sig("pdb_problem_free", None, _P)
 _sig("pdb_gen_options_init", None, C.POINTER(GenOptions))
 _sig("pdb_gen_options_config", C.c_int, C.c_int, C.c_int64, C.POINTER(GenOptions))
 _sig("pdb_problem_generate", C.c_int, C.POINTER(GenOptions), C.POINTER(_P))
+_sig("pdb_problem_generate_slab", C.c_int, C.POINTER(GenOptions), C.c_int, C.c_int, C.POINTER(_P))
+_sig("pdb_problem_rows_global", C.c_int64, _P)
+_sig("pdb_problem_row_range_count", C.c_int64, _P)
+_sig("pdb_problem_row_ranges", C.c_int, _P, _I64)
 _sig("pdb_patchset_detect", C.c_int, _P, C.c_int64, C.POINTER(_P))
 _sig("pdb_patchset_count", C.c_int64, _P)
 _sig("pdb_patchset_patch_size", C.c_int64, _P)
@@ -295,8 +299,8 @@ class Problem(_Handle):
         _check(_lib.pdb_problem_l2_error(self._ptr, _dp(u), C.byref(out)))
         return out.value
 
-    @classmethod
-    def generate(cls, config: int = 1, cells: int = 0, **overrides) -> "Problem":
+    @staticmethod
+    def _options(config, cells, overrides):
         o = GenOptions()
         _check(_lib.pdb_gen_options_config(config, cells, C.byref(o)))
         for k, v in overrides.items():
@@ -306,9 +310,35 @@ class Problem(_Handle):
                 o.n_levels = len(v)
             else:
                 setattr(o, k, v)
+        return o
+
+    @classmethod
+    def generate(cls, config: int = 1, cells: int = 0, **overrides) -> "Problem":
+        o = cls._options(config, cells, overrides)
         out = C.c_void_p()
         _check(_lib.pdb_problem_generate(C.byref(o), C.byref(out)))
         return cls(out)
+
+    @classmethod
+    def generate_slab(cls, config: int, cells: int, rank: int, nranks: int, **overrides) -> "Problem":
+        """Rows of rank `rank`'s slab only (global column ids); pdb_problem_generate_slab."""
+        o = cls._options(config, cells, overrides)
+        out = C.c_void_p()
+        _check(_lib.pdb_problem_generate_slab(C.byref(o), rank, nranks, C.byref(out)))
+        return cls(out)
+
+    @property
+    def rows_global(self) -> int:
+        return _lib.pdb_problem_rows_global(self._ptr)
+
+    def row_ranges(self) -> np.ndarray:
+        k = _lib.pdb_problem_row_range_count(self._ptr)
+        out = np.empty(2 * k, np.int64)
+        _check(_lib.pdb_problem_row_ranges(self._ptr, _ip(out)))
+        return out.reshape(k, 2)
+
+    def row_ids(self) -> np.ndarray:
+        return np.concatenate([np.arange(lo, hi) for lo, hi in self.row_ranges()])
 
     @property
     def ndofs(self) -> int:

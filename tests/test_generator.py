@@ -102,3 +102,39 @@ def test_standalone_generator_library_matches(P, cfg, cells):
     p = P.Problem.generate(cfg, cells)
     assert all(np.array_equal(x, y) for x, y in zip(g.csr(), p.csr()))
     assert np.array_equal(g.rhs(), p.rhs())
+
+
+@pytest.mark.parametrize("cfg,cells,ranks", [(1, 8, 2), (1, 9, 4), (2, 8, 3), (3, 6, 2), (3, 7, 3), (4, 8, 2),
+                                             (4, 9, 4), (5, 4, 2)])
+def test_slab_rows_equal_global_rows(P, cfg, cells, ranks):
+    """pdb_problem_generate_slab: each rank's rows are bitwise the same rows of
+    the whole problem (global column ids), the right-hand side too, and the
+    slabs' rows cover every row (neighbours share their face rows)."""
+    g = P.Problem.generate(cfg, cells)
+    rp, ci, v = g.csr()
+    b = g.rhs()
+    seen = np.zeros(g.ndofs, bool)
+    for r in range(ranks):
+        s = P.Problem.generate_slab(cfg, cells, r, ranks)
+        assert s.rows_global == g.ndofs
+        rows = s.row_ids()
+        srp, sci, sv = s.csr()
+        assert len(rows) == s.ndofs
+        lens = rp[rows + 1] - rp[rows]
+        assert np.array_equal(np.diff(srp), lens)
+        take = np.concatenate([np.arange(rp[i], rp[i + 1]) for i in rows])
+        assert np.array_equal(sci, ci[take])
+        assert np.array_equal(sv.view(np.uint64), v[take].view(np.uint64))
+        assert np.array_equal(s.rhs(), b[rows])
+        seen[rows] = True
+    assert seen.all()
+
+
+def test_slab_errors(P):
+    with pytest.raises(P.PatchdbError):
+        P.Problem.generate_slab(3, 6, 0, 4)  # 6 cells over 4 ranks: < 2 layers each
+    with pytest.raises(P.PatchdbError):
+        P.Problem.generate_slab(3, 6, 2, 2)
+    s = P.Problem.generate_slab(3, 6, 0, 2)
+    with pytest.raises(P.PatchdbError):
+        s.matrix()
