@@ -323,6 +323,32 @@ PDB_API pdb_status pdb_shard_owned(pdb_shard sh, int64_t* local_idx);
 PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, double* d_x, int64_t sweeps, void* stream);
 PDB_API void pdb_shard_free(pdb_shard sh);
 
+/* Multi-GPU sweep with rank-local data.
+ * A rank passes only its slab problem (pdb_problem_generate_slab: its rows,
+ * global column ids); patches, global weights, ownership and the exchange
+ * lists are set up with the neighbours, factors of the rank's own patches
+ * (db == NULL: exact) or the replicated database with the rank's phi slice.
+ *   nccl_id != NULL: this process is rank `rank` of `nranks` (count == 1),
+ *                    collective over the ranks; NCCL carries the exchanges;
+ *   nccl_id == NULL, count == nranks: an emulated group of all ranks on this
+ *                    GPU, exchanges as device copies (tests, single-GPU runs);
+ *   nranks == 1: one rank, no exchanges. */
+typedef struct pdb_slab_s* pdb_slab;
+PDB_API pdb_status pdb_slab_create(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
+                                   pdb_database db, double omega, const unsigned char* nccl_id, pdb_slab* out);
+/* Local ranks held by the handle (1, or nranks for an emulated group). */
+PDB_API int pdb_slab_local_ranks(pdb_slab sh);
+/* info[12]: rank, nranks, local DoFs, local rows, local patches, first global
+ * patch, interface split, owned DoFs, partials sent / received, x halo sent / received. */
+PDB_API pdb_status pdb_slab_info(pdb_slab sh, int i, int64_t* info);
+PDB_API pdb_status pdb_slab_local_dofs(pdb_slab sh, int i, int64_t* global_ids);
+/* Local indices of the DoFs rank i finishes (ascending). */
+PDB_API pdb_status pdb_slab_owned(pdb_slab sh, int i, int64_t* local_idx);
+/* Sweeps on device vectors of the local DoFs, one b / x per local rank. */
+PDB_API pdb_status pdb_slab_relax_device(pdb_slab sh, const double* const* d_b, double* const* d_x, int64_t sweeps,
+                                         void* stream);
+PDB_API void pdb_slab_free(pdb_slab sh);
+
 /* Sharded setup: a communicator over nranks processes (one GPU each; id from
  * pdb_comm_unique_id on one rank, shared out of band), and database builds
  * whose dominant step is split across the ranks -- the k-means assignment, the

@@ -786,6 +786,65 @@ PDB_API pdb_status pdb_shard_relax_device(pdb_shard sh, const double* d_b, doubl
 
 PDB_API void pdb_shard_free(pdb_shard sh) { shard_delete(sh); }
 
+/* ---- rank-local multi-GPU shards (slab.cu) ---- */
+
+PDB_API pdb_status pdb_slab_create(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
+                                   pdb_database db, double omega, const unsigned char* nccl_id, pdb_slab* out) {
+  if (slabs == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(count >= 1, Errc::invalid_argument, "need at least one slab");
+    require(patch_size >= 1, Errc::invalid_argument, "patch_size must be >= 1");
+    const bool emulated = nccl_id == nullptr && nranks > 1;
+    require(emulated ? count == nranks : count == 1, Errc::invalid_argument,
+            "one slab per process with a communicator, all nranks slabs for an emulated group");
+    std::vector<pdb_problem_s*> probs;
+    for (int i = 0; i < count; ++i) {
+      require(slabs[i] != nullptr, Errc::invalid_argument, "null argument");
+      probs.push_back(slabs[i]);
+    }
+    std::unique_ptr<pdb_slab_s, void (*)(pdb_slab_s*)> g(slab_new(rank, nranks, emulated), slab_delete);
+    if (nccl_id != nullptr && nranks > 1) slab_attach(*g, nccl_id);
+    slab_setup(*g, probs, patch_size, db, omega, default_stream());
+    *out = g.release();
+  });
+}
+
+PDB_API int pdb_slab_local_ranks(pdb_slab sh) { return sh == nullptr ? 0 : slab_local_ranks(*sh); }
+
+PDB_API pdb_status pdb_slab_info(pdb_slab sh, int i, int64_t* info) {
+  if (sh == nullptr || info == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const SlabInfo f = slab_info(*sh, i);
+    const int64_t v[12] = {f.rank, f.nranks, f.n_local, f.n_rows, f.n_patches, f.first_patch, f.split, f.n_owned,
+                           f.n_up, f.n_pin, f.n_xs, f.n_xr};
+    std::memcpy(info, v, sizeof(v));
+  });
+}
+
+PDB_API pdb_status pdb_slab_local_dofs(pdb_slab sh, int i, int64_t* global_ids) {
+  if (sh == nullptr || global_ids == nullptr) return arg_error("null argument");
+  return guarded([&] { slab_local_dofs(*sh, i, global_ids); });
+}
+
+PDB_API pdb_status pdb_slab_owned(pdb_slab sh, int i, int64_t* local_idx) {
+  if (sh == nullptr || local_idx == nullptr) return arg_error("null argument");
+  return guarded([&] { slab_owned(*sh, i, local_idx); });
+}
+
+PDB_API pdb_status pdb_slab_relax_device(pdb_slab sh, const double* const* d_b, double* const* d_x, int64_t sweeps,
+                                         void* stream) {
+  if (sh == nullptr || d_b == nullptr || d_x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(sweeps >= 0, Errc::invalid_argument, "sweeps must be >= 0");
+    const int L = slab_local_ranks(*sh);
+    std::vector<const double*> b(d_b, d_b + L);
+    std::vector<double*> x(d_x, d_x + L);
+    slab_relax(*sh, b, x, sweeps, stream_of(stream));
+  });
+}
+
+PDB_API void pdb_slab_free(pdb_slab sh) { slab_delete(sh); }
+
 /* ---- experiment drivers (reference experiments.cpp; outside the hot path) ---- */
 
 PDB_API pdb_status pdb_run_experiment(const char* config_json, const char* out_csv) {

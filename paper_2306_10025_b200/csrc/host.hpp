@@ -11,6 +11,7 @@
 #include "objects.hpp"
 
 struct pdb_shard_s;
+struct pdb_slab_s;
 struct pdb_comm_s;
 struct pdb_shard_plan_s;
 
@@ -152,6 +153,9 @@ void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, doub
 void precond_compressed_shard(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
                               cudaStream_t s);
 void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scale, double* sols, cudaStream_t s);
+// DoF -> (patch, slot) map of pc.patches (inv_ptr / inv, ascending patch), plus the padded copy
+void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = nullptr);
+void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cudaStream_t s);
 // z = M^{-1} r on device pointers (symmetric: omega W^1/2 S W^1/2, used by PCG).
 void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s,
                           bool symmetric = false);
@@ -205,4 +209,22 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
 void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol, int64_t max_iters,
                 double* x_host, pdb_report_s& rep, cudaStream_t s);
 
+// slab.cu -- multi-GPU sweep shards with rank-local data
+struct SlabRank;
+pdb_slab_s* slab_new(int rank, int nranks, bool emulated);
+void slab_delete(pdb_slab_s* g);
+void slab_attach(pdb_slab_s& g, const unsigned char* id128);
+void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
+                double omega, cudaStream_t s);
+void slab_relax(pdb_slab_s& g, const std::vector<const double*>& b, const std::vector<double*>& x, int64_t sweeps,
+                cudaStream_t s);
+// per local rank i: sizes / lists for the C-ABI getters
+struct SlabInfo {
+  int rank, nranks;
+  int64_t n_local, n_rows, n_patches, first_patch, split, n_owned, n_up, n_pin, n_xs, n_xr;
+};
+SlabInfo slab_info(const pdb_slab_s& g, int i);
+void slab_local_dofs(const pdb_slab_s& g, int i, int64_t* out);
+void slab_owned(const pdb_slab_s& g, int i, int64_t* out);
+int slab_local_ranks(const pdb_slab_s& g);
 }  // namespace pdb

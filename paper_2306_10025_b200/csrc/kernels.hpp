@@ -94,6 +94,9 @@ void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, 
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
                    const double* init, const double* omega_w, double* z_out, double* x, cudaStream_t s);
 void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+// bad = 1 when some omega_w[i] != omega * (1 / patches covering i) (the padded scatter's weight)
+void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
+                       cudaStream_t s);
 void scatter_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
 // Binv (column-major) from row-major LU + pivots: column c = lu_solve(e_c).
 void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s);

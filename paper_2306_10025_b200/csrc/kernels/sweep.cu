@@ -354,7 +354,16 @@ __global__ void shard_scatter_kernel(int64_t count, const int32_t* __restrict__ 
   double z = init ? init[d] : 0.0;
   for (int32_t q = inv_ptr[d]; q < inv_ptr[d + 1]; ++q) z += __ldg(sols + __ldg(inv + q));
   if (z_out) z_out[t] = z;
-  if (x) x[d] = z * omega_w[d] + x[d];
+  if (x) x[d] = __dadd_rn(__dmul_rn(z, omega_w[d]), x[d]);  // the serial scatter's rounding
+}
+
+__global__ void check_pad_weights_kernel(int64_t n, double omega, const int32_t* __restrict__ inv_ptr,
+                                         const double* __restrict__ omega_w, int32_t* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t cnt = inv_ptr[i + 1] - inv_ptr[i];
+  const double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+  if (omega_w[i] != omega * w) atomicOr(bad, 1);
 }
 
 __global__ void gather_vals_kernel(int64_t count, const int32_t* __restrict__ idx, const double* __restrict__ src,
@@ -424,9 +433,9 @@ __global__ void scatter_update_pad_kernel(int64_t n, const int32_t* __restrict__
       }
     double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
     if (sym) w = sqrt(w);
-    z *= omega * w;
+    z = __dmul_rn(z, omega * w);  // explicit: the shard scatter must round the same way
     if (z_out) z_out[i] = z;
-    if (x_out) x_out[i] = z + xi[u];
+    if (x_out) x_out[i] = __dadd_rn(z, xi[u]);
   }
 }
 
@@ -561,9 +570,9 @@ __global__ void scatter_update_kernel(int64_t n, const int32_t* __restrict__ inv
   double z = 0.0;
   const int32_t lo = inv_ptr[i], hi = inv_ptr[i + 1];
   for (int32_t q = lo; q < hi; ++q) z += __ldg(sols + __ldg(inv + q));
-  z *= omega_w[i];
+  z = __dmul_rn(z, omega_w[i]);
   if (z_out) z_out[i] = z;
-  if (x_out) x_out[i] = z + x_in[i];
+  if (x_out) x_out[i] = __dadd_rn(z, x_in[i]);
 }
 
 __global__ void inverse_count_kernel(int64_t total, const int32_t* __restrict__ patches, int32_t* counts) {
@@ -726,6 +735,11 @@ void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, c
   if (count > 0)
     shard_scatter_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, list, inv_ptr, inv, sols, init, omega_w,
                                                                     z_out, x);
+}
+
+void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
+                       cudaStream_t s) {
+  if (n > 0) check_pad_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, inv_ptr, omega_w, bad);
 }
 
 void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s) {

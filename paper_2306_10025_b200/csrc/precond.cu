@@ -18,12 +18,10 @@ namespace pdb {
 
 bool use_dmma_apply(int ps);
 
-namespace {
-
 // DoF -> solution-slot inverse map.  Entries are first k*ps + l sorted by k
 // (the reference's scatter order, precond.cpp:81-86); remapped to
 // slot_of[k]*ps + l only for callers that store solutions in tile order.
-void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = nullptr) {
+void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of) {
   const int64_t n = pc.n;
   pc.inv_ptr.alloc(static_cast<size_t>(n + 1));
   pc.inv.alloc(static_cast<size_t>(std::max<int64_t>(pc.np * pc.ps, 1)));
@@ -56,8 +54,24 @@ void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = n
     pc.inv_pad.alloc(static_cast<size_t>(pc.maxc_pad * std::max<int64_t>(n, 1)));
     k::build_inverse_pad(n, pc.maxc_pad, pc.inv_ptr.get(), pc.inv.get(), pc.inv_pad.get(), s);
     PDB_LAUNCH_CHECK();
+    // the padded scatter recomputes omega * (1 / count); keep it only when the
+    // patch set's weights are exactly that (detect_patches' compute_weights)
+    if (pc.omega_w.get()) {
+      Scratch<int32_t> bad(1, s);
+      PDB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), s));
+      k::check_pad_weights(n, pc.omega, pc.inv_ptr.get(), pc.omega_w.get(), bad.get(), s);
+      int32_t bh = 0;
+      PDB_CUDA(cudaMemcpyAsync(&bh, bad.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (bh) {
+        pc.maxc_pad = 0;
+        pc.inv_pad = DevBuf<int32_t>();
+      }
+    }
   }
 }
+
+namespace {
 
 void scatter_stage(const pdb_precond_s& pc, const double* sols, bool symmetric, const double* x_in, double* z_out,
                    double* x_out, cudaStream_t s) {
@@ -67,6 +81,8 @@ void scatter_stage(const pdb_precond_s& pc, const double* sols, bool symmetric, 
     k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols, symmetric ? pc.omega_sw.get() : pc.omega_w.get(),
                       x_in, z_out, x_out, s);
 }
+
+}  // namespace
 
 void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cudaStream_t s) {
   require(ps.np * ps.ps < (int64_t{1} << 31), Errc::invalid_argument, "patch set too large for 32-bit slot ids");
@@ -83,6 +99,8 @@ void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cud
   pc.omega_sw.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
   k::sqrt_weights(ps.n, omega, ps.weights.get(), pc.sqrt_w.get(), pc.omega_sw.get(), s);
 }
+
+namespace {
 
 // Sweep factor layout: explicit column-major inverses (default) or the
 // column-major LU for the triangular-solve kernel (PDB_APPLY=lu).

@@ -1,0 +1,702 @@
+// Multi-GPU relaxation sweep with rank-local data.
+//
+// Every rank holds only its own rows: the rows of the DoFs of its patches
+// (a slab of cells from pdb_problem_generate_slab, or any row block), with
+// global column ids.  Nothing global is ever materialised:
+//
+// setup (per rank, exchanges with the ranks whose DoF ranges overlap)
+//   local index space L = rows + their columns (sorted global ids), local CSR
+//   patches detected on the local rows (detect_patches, patch.cpp:37-90): a
+//     slab's candidate rows and their footprints are all local
+//   global patch offset k0 = patches of lower ranks (patches are ordered by
+//     front, so the slabs' patch ranges are consecutive)
+//   cover counts of shared DoFs summed with the neighbours -> the global
+//     weights 1 / count (compute_weights, patch.cpp:12-20)
+//   ownership: a DoF is finished by the HIGHEST rank whose patches touch it;
+//     the reference's scatter adds contributions in ascending patch order
+//     (precond.cpp:81-86), so a lower rank's partial sum is a prefix of the
+//     owner's sum: the lower rank sends it, the owner continues from it
+//   x halo: every local DoF the rank does not own is requested from the
+//     ranks whose ranges contain it; exactly one must own it
+//   factors: exact -> extract + LU of the local patches only; compressed ->
+//     the small replicated database and the rank's phi slice
+//
+// sweep (per rank), the interface first so the exchange hides behind the
+// interior work:
+//   r = b - A x on the local rows                               [main]
+//   patches touching DoFs finished by the upper neighbour (the top cell
+//   layer: a suffix of the local patches) -> their partial sums  [main]
+//   -> ncclSend up / ncclRecv from below                         [comm stream]
+//   the other patches; owned DoFs without a lower contribution   [main]
+//   owned DoFs with a lower contribution, from the received sum  [main]
+//   x of owned DoFs the neighbours read -> x halo exchange       [comm stream]
+// On one GPU an emulated group runs W ranks' phases in order and moves the
+// exchanged values with device copies: the same code, bitwise the single-GPU
+// pdb_relax (tests/test_slab.py).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <thread>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+#define PDB_NCCL_S(call)                                                                            \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess) ::pdb::fail(::pdb::Errc::internal, std::string("NCCL error in " #call ": ") + \
+                                                             ncclGetErrorString(r_));               \
+  } while (0)
+
+namespace pdb {
+
+namespace {
+
+struct Seg {
+  int peer;
+  int64_t off, cnt;
+};
+
+int64_t seg_total(const std::vector<Seg>& v) { return v.empty() ? 0 : v.back().off + v.back().cnt; }
+
+template <typename T>
+void put(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
+  d.alloc(std::max<size_t>(h.size(), 1));
+  if (!h.empty()) d.upload(h.data(), h.size(), s);
+}
+
+// contiguous patch range [k0, k1) of a local patch set as its own patch set
+void sub_patchset(const pdb_patchset_s& ps, int64_t k0, int64_t k1, pdb_patchset_s& out, cudaStream_t s) {
+  out.n = ps.n;
+  out.np = k1 - k0;
+  out.ps = ps.ps;
+  out.patches.alloc(static_cast<size_t>(std::max<int64_t>(out.np * out.ps, 1)));
+  if (out.np > 0)
+    PDB_CUDA(cudaMemcpyAsync(out.patches.get(), ps.patches.get() + k0 * ps.ps, out.np * ps.ps * sizeof(int32_t),
+                             cudaMemcpyDeviceToDevice, s));
+  out.weights.alloc(static_cast<size_t>(std::max<int64_t>(ps.n, 1)));
+  PDB_CUDA(cudaMemcpyAsync(out.weights.get(), ps.weights.get(), ps.n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+}  // namespace
+
+// One rank's state.
+struct SlabRank {
+  int rank = 0, nranks = 1;
+  std::vector<int64_t> gid;  // local -> global DoF (ascending)
+  int64_t nl = 0;
+  std::vector<int32_t> rows;  // local ids of the rank's rows (its patch DoFs)
+  DeviceCsr a;
+  pdb_patchset_s ps;  // local patches, global weights
+  int64_t np = 0, k0 = 0, kb = 0;  // local patches; global offset; start of the top-interface suffix
+  pdb_precond_s pc_lo, pc_hi;      // patches [0, kb) and [kb, np)
+  pdb_precond_s map;               // DoF -> (patch, slot) over all local patches
+  DevBuf<double> omega_w;
+  DevBuf<int32_t> own_plain, own_pin, up, pin, xs, xr;
+  std::vector<Seg> up_seg, pin_seg, xs_seg, xr_seg;
+  DevBuf<double> zup, zin, init, xsend, xrecv, r, sols;
+  int64_t n_own = 0;
+  // NCCL mode
+  ncclComm_t comm = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev[4] = {};
+  ~SlabRank() {
+    if (comm) ncclCommDestroy(comm);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
+  }
+};
+
+}  // namespace pdb
+
+struct pdb_slab_s {
+  std::vector<std::unique_ptr<pdb::SlabRank>> ranks;  // 1 (NCCL rank) or W (emulated group)
+  bool emulated = false;
+  int64_t n_global = 0;
+};
+
+namespace pdb {
+
+namespace {
+
+// ---- setup message passing: out[r][q] -> in[q][r] for the local ranks ----
+using Mail = std::vector<std::vector<int64_t>>;  // [peer] -> payload
+
+void deliver(pdb_slab_s& g, std::vector<Mail>& out, std::vector<Mail>& in, cudaStream_t s) {
+  const int W = g.ranks[0]->nranks;
+  in.assign(out.size(), Mail(static_cast<size_t>(W)));
+  if (g.emulated) {
+    for (int r = 0; r < W; ++r)
+      for (int q = 0; q < W; ++q) in[static_cast<size_t>(q)][static_cast<size_t>(r)] = out[static_cast<size_t>(r)][static_cast<size_t>(q)];
+    return;
+  }
+  SlabRank& R = *g.ranks[0];
+  if (W == 1) {
+    in[0][0] = out[0][0];
+    return;
+  }
+  const Mail& o = out[0];
+  // sizes, then payloads (grouped point-to-point on device buffers)
+  DevBuf<int64_t> ssz(static_cast<size_t>(W)), rsz(static_cast<size_t>(W));
+  std::vector<int64_t> sz(static_cast<size_t>(W));
+  for (int q = 0; q < W; ++q) sz[static_cast<size_t>(q)] = static_cast<int64_t>(o[static_cast<size_t>(q)].size());
+  ssz.upload(sz.data(), sz.size(), s);
+  PDB_NCCL_S(ncclGroupStart());
+  for (int q = 0; q < W; ++q) {
+    if (q == R.rank) continue;
+    PDB_NCCL_S(ncclSend(ssz.get() + q, 1, ncclInt64, q, R.comm, s));
+    PDB_NCCL_S(ncclRecv(rsz.get() + q, 1, ncclInt64, q, R.comm, s));
+  }
+  PDB_NCCL_S(ncclGroupEnd());
+  std::vector<int64_t> rs = rsz.to_host(s);
+  std::vector<int64_t> so(static_cast<size_t>(W + 1), 0), ro(static_cast<size_t>(W + 1), 0);
+  for (int q = 0; q < W; ++q) {
+    so[static_cast<size_t>(q) + 1] = so[static_cast<size_t>(q)] + (q == R.rank ? 0 : sz[static_cast<size_t>(q)]);
+    ro[static_cast<size_t>(q) + 1] = ro[static_cast<size_t>(q)] + (q == R.rank ? 0 : rs[static_cast<size_t>(q)]);
+  }
+  std::vector<int64_t> flat(static_cast<size_t>(so[static_cast<size_t>(W)]));
+  for (int q = 0; q < W; ++q)
+    if (q != R.rank) std::copy(o[static_cast<size_t>(q)].begin(), o[static_cast<size_t>(q)].end(), flat.begin() + so[static_cast<size_t>(q)]);
+  DevBuf<int64_t> sb(std::max<size_t>(flat.size(), 1)), rb(static_cast<size_t>(std::max<int64_t>(ro[static_cast<size_t>(W)], 1)));
+  if (!flat.empty()) sb.upload(flat.data(), flat.size(), s);
+  PDB_NCCL_S(ncclGroupStart());
+  for (int q = 0; q < W; ++q) {
+    if (q == R.rank) continue;
+    if (sz[static_cast<size_t>(q)] > 0)
+      PDB_NCCL_S(ncclSend(sb.get() + so[static_cast<size_t>(q)], static_cast<size_t>(sz[static_cast<size_t>(q)]), ncclInt64, q, R.comm, s));
+    if (rs[static_cast<size_t>(q)] > 0)
+      PDB_NCCL_S(ncclRecv(rb.get() + ro[static_cast<size_t>(q)], static_cast<size_t>(rs[static_cast<size_t>(q)]), ncclInt64, q, R.comm, s));
+  }
+  PDB_NCCL_S(ncclGroupEnd());
+  std::vector<int64_t> all = rb.to_host(s);
+  for (int q = 0; q < W; ++q)
+    if (q != R.rank)
+      in[0][static_cast<size_t>(q)].assign(all.begin() + ro[static_cast<size_t>(q)], all.begin() + ro[static_cast<size_t>(q) + 1]);
+  in[0][static_cast<size_t>(R.rank)] = o[static_cast<size_t>(R.rank)];
+}
+
+std::vector<Seg> segments_of(const std::vector<int32_t>& peer) {
+  std::vector<Seg> out;
+  for (size_t i = 0; i < peer.size(); ++i) {
+    if (out.empty() || out.back().peer != peer[i]) out.push_back({peer[i], static_cast<int64_t>(i), 0});
+    ++out.back().cnt;
+  }
+  return out;
+}
+
+template <typename F>
+void parallel_rows(int64_t n, F&& fn) {
+  const int T = static_cast<int>(std::max(1u, std::min(32u, std::thread::hardware_concurrency())));
+  if (n < (1 << 16) || T == 1) {
+    fn(int64_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t) pool.emplace_back([&, t] { fn(n * t / T, n * (t + 1) / T); });
+  for (auto& th : pool) th.join();
+}
+
+// Phase A: local index space, local CSR, patches, touched set.
+void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaStream_t s,
+                     std::vector<int64_t>& touched, std::vector<int64_t>& tcount) {
+  HostCsr& h = prob.a;
+  std::vector<int64_t> rows_g;
+  for (const auto& g : prob.row_ranges)
+    for (int64_t i = g.first; i < g.second; ++i) rows_g.push_back(i);
+  require(static_cast<int64_t>(rows_g.size()) == h.n, Errc::invalid_argument, "slab rows do not match the row ranges");
+  int64_t gmin = rows_g.empty() ? 0 : rows_g.front(), gmax = rows_g.empty() ? -1 : rows_g.back();
+  for (int32_t c : h.col) {
+    gmin = std::min<int64_t>(gmin, c);
+    gmax = std::max<int64_t>(gmax, c);
+  }
+  const int64_t span = gmax - gmin + 1;
+  std::vector<int32_t> g2l(static_cast<size_t>(std::max<int64_t>(span, 1)), -1);
+  for (int64_t gi : rows_g) g2l[static_cast<size_t>(gi - gmin)] = 0;
+  for (int32_t c : h.col) g2l[static_cast<size_t>(c - gmin)] = 0;
+  R.gid.clear();
+  for (int64_t q = 0; q < span; ++q)
+    if (g2l[static_cast<size_t>(q)] == 0) {
+      g2l[static_cast<size_t>(q)] = static_cast<int32_t>(R.gid.size());
+      R.gid.push_back(gmin + q);
+    }
+  R.nl = static_cast<int64_t>(R.gid.size());
+  // local CSR: the rank's rows keep their entries, the halo rows are empty
+  HostCsr loc;
+  loc.n = R.nl;
+  loc.row_ptr.assign(static_cast<size_t>(R.nl + 1), 0);
+  R.rows.resize(rows_g.size());
+  for (size_t i = 0; i < rows_g.size(); ++i) {
+    const int32_t l = g2l[static_cast<size_t>(rows_g[i] - gmin)];
+    R.rows[i] = l;
+    loc.row_ptr[static_cast<size_t>(l) + 1] = h.row_ptr[i + 1] - h.row_ptr[i];
+  }
+  for (int64_t l = 0; l < R.nl; ++l) loc.row_ptr[static_cast<size_t>(l) + 1] += loc.row_ptr[static_cast<size_t>(l)];
+  loc.col.resize(h.col.size());
+  loc.val.resize(h.val.size());
+  parallel_rows(static_cast<int64_t>(rows_g.size()), [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) {
+      int64_t o = loc.row_ptr[static_cast<size_t>(R.rows[static_cast<size_t>(i)])];
+      for (int64_t q = h.row_ptr[static_cast<size_t>(i)]; q < h.row_ptr[static_cast<size_t>(i) + 1]; ++q, ++o) {
+        loc.col[static_cast<size_t>(o)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
+        loc.val[static_cast<size_t>(o)] = h.val[static_cast<size_t>(q)];
+      }
+    }
+  });
+  upload_csr(loc, R.a, s);
+  detect_patches(R.a, patch_size, R.ps, s);
+  R.np = R.ps.np;
+  // touched DoFs (global ids, ascending) and the local cover counts
+  const std::vector<int32_t> pt = R.ps.patches.to_host(s);
+  std::vector<int32_t> cnt(static_cast<size_t>(R.nl), 0);
+  for (int32_t l : pt) ++cnt[static_cast<size_t>(l)];
+  touched.clear();
+  tcount.clear();
+  for (int64_t l = 0; l < R.nl; ++l)
+    if (cnt[static_cast<size_t>(l)]) {
+      touched.push_back(R.gid[static_cast<size_t>(l)]);
+      tcount.push_back(cnt[static_cast<size_t>(l)]);
+    }
+}
+
+int64_t local_of(const SlabRank& R, int64_t g) {
+  auto it = std::lower_bound(R.gid.begin(), R.gid.end(), g);
+  return it != R.gid.end() && *it == g ? static_cast<int64_t>(it - R.gid.begin()) : -1;
+}
+
+}  // namespace
+
+// Collective setup of the ranks in g (each with its slab problem).
+void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
+                double omega, cudaStream_t s) {
+  require_device();
+  const int L = static_cast<int>(g.ranks.size());
+  const int W = g.ranks[0]->nranks;
+  std::vector<std::vector<int64_t>> T(static_cast<size_t>(L)), Tc(static_cast<size_t>(L));
+  for (int i = 0; i < L; ++i) {
+    require(probs[static_cast<size_t>(i)]->is_slab() || W == 1, Errc::invalid_argument,
+            "shard needs a slab problem (pdb_problem_generate_slab)");
+    if (!probs[static_cast<size_t>(i)]->is_slab()) probs[static_cast<size_t>(i)]->row_ranges = {{0, probs[static_cast<size_t>(i)]->a.n}};
+    local_structure(*g.ranks[static_cast<size_t>(i)], *probs[static_cast<size_t>(i)], patch_size, s, T[static_cast<size_t>(i)], Tc[static_cast<size_t>(i)]);
+  }
+  g.n_global = probs[0]->n_global > 0 ? probs[0]->n_global : probs[0]->a.n;
+  // (1) all ranks: patch count and touched range
+  std::vector<Mail> out(static_cast<size_t>(L), Mail(static_cast<size_t>(W))), in;
+  for (int i = 0; i < L; ++i) {
+    const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    const auto& t = T[static_cast<size_t>(i)];
+    for (int q = 0; q < W; ++q)
+      out[static_cast<size_t>(i)][static_cast<size_t>(q)] = {R.np, t.empty() ? INT64_MAX : t.front(), t.empty() ? -1 : t.back()};
+  }
+  deliver(g, out, in, s);
+  std::vector<std::vector<int64_t>> info(static_cast<size_t>(L));  // [i] -> np, tmin, tmax per rank
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    R.k0 = 0;
+    for (int q = 0; q < W; ++q) {
+      const auto& m = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      info[static_cast<size_t>(i)].insert(info[static_cast<size_t>(i)].end(), m.begin(), m.end());
+      if (q < R.rank) R.k0 += m[0];
+    }
+  }
+  int64_t np_total = 0;
+  for (int q = 0; q < W; ++q) np_total += info[0][static_cast<size_t>(3 * q)];
+  // (2) touched DoFs (with counts) to every rank whose touched range overlaps
+  for (int i = 0; i < L; ++i) {
+    const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    const auto& t = T[static_cast<size_t>(i)];
+    const auto& c = Tc[static_cast<size_t>(i)];
+    for (int q = 0; q < W; ++q) {
+      auto& m = out[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      m.clear();
+      if (q == R.rank) continue;
+      const int64_t lo = info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 1)], hi = info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 2)];
+      for (size_t k = std::lower_bound(t.begin(), t.end(), lo) - t.begin(); k < t.size() && t[k] <= hi; ++k) {
+        m.push_back(t[k]);
+        m.push_back(c[k]);
+      }
+    }
+  }
+  deliver(g, out, in, s);
+  std::vector<std::vector<int64_t>> need(static_cast<size_t>(L));       // local ids whose x comes from elsewhere
+  std::vector<std::vector<int32_t>> owner_of(static_cast<size_t>(L));  // per touched DoF
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    const auto& t = T[static_cast<size_t>(i)];
+    std::vector<int64_t> total(Tc[static_cast<size_t>(i)]);
+    std::vector<int32_t> lo_rank(t.size(), R.rank), hi_rank(t.size(), R.rank);
+    for (int q = 0; q < W; ++q) {
+      const auto& m = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      for (size_t k = 0; k + 1 < m.size(); k += 2) {
+        const auto it = std::lower_bound(t.begin(), t.end(), m[k]);
+        if (it == t.end() || *it != m[k]) continue;  // in my range but not touched by me
+        const size_t j = static_cast<size_t>(it - t.begin());
+        total[j] += m[k + 1];
+        lo_rank[j] = std::min(lo_rank[j], q);
+        hi_rank[j] = std::max(hi_rank[j], q);
+      }
+    }
+    std::vector<double> w(static_cast<size_t>(R.nl), 0.0);
+    std::vector<int32_t> up_l, up_p, pin_l, pin_p, plain;
+    std::vector<char> owned(static_cast<size_t>(R.nl), 0);
+    for (size_t j = 0; j < t.size(); ++j) {
+      const int64_t l = local_of(R, t[j]);
+      w[static_cast<size_t>(l)] = 1.0 / static_cast<double>(total[j]);  // compute_weights (patch.cpp:12-20)
+      require(hi_rank[j] - lo_rank[j] <= 1, Errc::invalid_argument,
+              "slab partition too thin: a DoF is shared by non-adjacent ranks (use fewer ranks)");
+      if (hi_rank[j] > R.rank) {
+        up_l.push_back(static_cast<int32_t>(l));
+        up_p.push_back(hi_rank[j]);
+      } else {
+        owned[static_cast<size_t>(l)] = 1;
+        if (lo_rank[j] < R.rank) {
+          pin_l.push_back(static_cast<int32_t>(l));
+          pin_p.push_back(lo_rank[j]);
+        } else {
+          plain.push_back(static_cast<int32_t>(l));
+        }
+      }
+    }
+    // lists are in ascending global order already; group by peer (stable)
+    auto group = [](std::vector<int32_t>& l, std::vector<int32_t>& p) {
+      std::vector<size_t> o(l.size());
+      for (size_t k = 0; k < o.size(); ++k) o[k] = k;
+      std::stable_sort(o.begin(), o.end(), [&](size_t a, size_t b) { return p[a] < p[b]; });
+      std::vector<int32_t> l2, p2;
+      for (size_t k : o) l2.push_back(l[k]), p2.push_back(p[k]);
+      l.swap(l2);
+      p.swap(p2);
+    };
+    group(up_l, up_p);
+    group(pin_l, pin_p);
+    R.up_seg = segments_of(up_p);
+    R.pin_seg = segments_of(pin_p);
+    put(R.up, up_l, s);
+    put(R.pin, pin_l, s);
+    put(R.own_plain, plain, s);
+    put(R.own_pin, pin_l, s);
+    R.n_own = static_cast<int64_t>(plain.size() + pin_l.size());
+    R.zup.alloc(std::max<size_t>(up_l.size(), 1));
+    R.zin.alloc(std::max<size_t>(pin_l.size(), 1));
+    // global weights for the local patch set
+    R.ps.weights.alloc(static_cast<size_t>(std::max<int64_t>(R.nl, 1)));
+    R.ps.weights.upload(w.data(), w.size(), s);
+    std::vector<double> ow(w.size());
+    for (size_t k = 0; k < w.size(); ++k) ow[k] = omega * w[k];
+    put(R.omega_w, ow, s);
+    for (int64_t l = 0; l < R.nl; ++l)
+      if (!owned[static_cast<size_t>(l)]) need[static_cast<size_t>(i)].push_back(l);
+    // split point: the patches touching a DoF finished above must be a suffix
+    std::vector<char> is_up(static_cast<size_t>(R.nl), 0);
+    for (int32_t l : up_l) is_up[static_cast<size_t>(l)] = 1;
+    const std::vector<int32_t> pt = R.ps.patches.to_host(s);
+    int64_t first = R.np;
+    bool suffix = true;
+    for (int64_t k = 0; k < R.np; ++k) {
+      bool touches = false;
+      for (int64_t q = 0; q < patch_size; ++q) touches = touches || is_up[static_cast<size_t>(pt[static_cast<size_t>(k * patch_size + q)])];
+      if (touches && first == R.np) first = k;
+      if (!touches && first < R.np) suffix = false;
+    }
+    R.kb = suffix ? first : R.np;
+  }
+  // (3) x halo requests to every rank whose touched range holds the DoF
+  for (int i = 0; i < L; ++i) {
+    const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    for (int q = 0; q < W; ++q) out[static_cast<size_t>(i)][static_cast<size_t>(q)].clear();
+    for (int64_t l : need[static_cast<size_t>(i)]) {
+      const int64_t gd = R.gid[static_cast<size_t>(l)];
+      for (int q = 0; q < W; ++q)
+        if (q != R.rank && gd >= info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 1)] && gd <= info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 2)])
+          out[static_cast<size_t>(i)][static_cast<size_t>(q)].push_back(gd);
+    }
+  }
+  deliver(g, out, in, s);
+  std::vector<Mail> req = in;
+  // (4) replies: 1 where the requested DoF is owned here; those become xs
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    std::vector<char> own(static_cast<size_t>(R.nl), 0);
+    if (R.n_own > 0) {
+      const std::vector<int32_t> plain = R.own_plain.to_host(s), pinv = R.own_pin.to_host(s);
+      const int64_t npin = seg_total(R.pin_seg);
+      for (int64_t k = 0; k < R.n_own - npin; ++k) own[static_cast<size_t>(plain[static_cast<size_t>(k)])] = 1;
+      for (int64_t k = 0; k < npin; ++k) own[static_cast<size_t>(pinv[static_cast<size_t>(k)])] = 1;
+    }
+    std::vector<int32_t> xs_l, xs_p;
+    for (int q = 0; q < W; ++q) {
+      auto& m = out[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      m.clear();
+      for (int64_t gd : req[static_cast<size_t>(i)][static_cast<size_t>(q)]) {
+        const int64_t l = local_of(R, gd);
+        const bool mine = l >= 0 && own[static_cast<size_t>(l)];
+        m.push_back(mine ? 1 : 0);
+        if (mine) xs_l.push_back(static_cast<int32_t>(l)), xs_p.push_back(q);
+      }
+    }
+    R.xs_seg = segments_of(xs_p);
+    put(R.xs, xs_l, s);
+    R.xsend.alloc(std::max<size_t>(xs_l.size(), 1));
+  }
+  deliver(g, out, in, s);
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    std::vector<int32_t> xr_l, xr_p;
+    std::vector<int> got(static_cast<size_t>(R.nl), 0);
+    // re-derive what this rank asked each peer (same order as step 3)
+    std::vector<std::vector<int64_t>> asked(static_cast<size_t>(W));
+    for (int64_t l : need[static_cast<size_t>(i)]) {
+      const int64_t gd = R.gid[static_cast<size_t>(l)];
+      for (int q = 0; q < W; ++q)
+        if (q != R.rank && gd >= info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 1)] && gd <= info[static_cast<size_t>(i)][static_cast<size_t>(3 * q + 2)])
+          asked[static_cast<size_t>(q)].push_back(gd);
+    }
+    for (int q = 0; q < W; ++q) {
+      const auto& rep = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      require(rep.size() == asked[static_cast<size_t>(q)].size(), Errc::internal, "slab setup: reply size mismatch");
+      for (size_t k = 0; k < rep.size(); ++k)
+        if (rep[k]) {
+          const int64_t l = local_of(R, asked[static_cast<size_t>(q)][k]);
+          ++got[static_cast<size_t>(l)];
+          xr_l.push_back(static_cast<int32_t>(l));
+          xr_p.push_back(q);
+        }
+    }
+    for (int64_t l : need[static_cast<size_t>(i)])
+      require(got[static_cast<size_t>(l)] <= 1, Errc::internal, "slab setup: a DoF has two owners");
+    // DoFs no rank touches keep their initial x (the serial sweep leaves them unchanged)
+    R.xr_seg = segments_of(xr_p);
+    put(R.xr, xr_l, s);
+    R.xrecv.alloc(std::max<size_t>(xr_l.size(), 1));
+  }
+  // (5) factors and the DoF -> slot map
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    pdb_patchset_s lo, hi;
+    sub_patchset(R.ps, 0, R.kb, lo, s);
+    sub_patchset(R.ps, R.kb, R.np, hi, s);
+    if (db) {
+      require(db->np == np_total, Errc::dimension_mismatch, "database does not cover the global patch set");
+      require(db->ps == patch_size, Errc::dimension_mismatch, "database entry dimension does not match the patch size");
+      auto part = [&](pdb_patchset_s& sp, int64_t off, pdb_precond_s& pc) {
+        if (sp.np == 0) return;
+        pdb_database_s ldb;
+        ldb.m = db->m;
+        ldb.np = sp.np;
+        ldb.ps = db->ps;
+        const size_t len = static_cast<size_t>(db->ps * db->ps);
+        ldb.lu.alloc(db->m * len);
+        PDB_CUDA(cudaMemcpyAsync(ldb.lu.get(), db->lu.get(), db->m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        ldb.piv.alloc(static_cast<size_t>(db->m * db->ps));
+        PDB_CUDA(cudaMemcpyAsync(ldb.piv.get(), db->piv.get(), db->m * db->ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        ldb.phi.alloc(static_cast<size_t>(sp.np));
+        PDB_CUDA(cudaMemcpyAsync(ldb.phi.get(), db->phi.get() + R.k0 + off, sp.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        precond_compressed_shard(sp, ldb, omega, pc, s);
+      };
+      part(lo, 0, R.pc_lo);
+      part(hi, R.kb, R.pc_hi);
+    } else {
+      if (lo.np > 0) precond_exact(R.a, lo, omega, R.pc_lo, s);
+      if (hi.np > 0) precond_exact(R.a, hi, omega, R.pc_hi, s);
+    }
+    common_setup(R.ps, omega, R.map, s);
+    build_inverse(R.map, s);
+    R.r.alloc(static_cast<size_t>(std::max<int64_t>(R.nl, 1)));
+    R.sols.alloc(static_cast<size_t>(std::max<int64_t>(R.np * patch_size, 1)));
+    R.init.alloc(static_cast<size_t>(std::max<int64_t>(R.nl, 1)));
+    R.init.zero(s);
+  }
+  sync(s);
+}
+
+namespace {
+
+// sweep phases of one rank
+void phase_interface(SlabRank& R, const double* b, double* x, cudaStream_t s) {
+  const k::SpmvPlan plan = plan_of(R.a);
+  k::residual(plan, R.nl, R.a.row_ptr.get(), R.a.col.get(), R.a.val.get(), x, b, R.r.get(), nullptr, s);
+  if (R.np > R.kb) patch_stage(R.pc_hi, R.r.get(), nullptr, R.sols.get() + R.kb * R.ps.ps, s);
+  if (R.kb == R.np && R.kb > 0) patch_stage(R.pc_lo, R.r.get(), nullptr, R.sols.get(), s);  // no split: everything now
+  // partial sums of the DoFs finished above (their patches are all done)
+  k::shard_scatter(seg_total(R.up_seg), R.up.get(), R.map.inv_ptr.get(), R.map.inv.get(), R.sols.get(), nullptr, nullptr, R.zup.get(),
+                   nullptr, s);
+}
+
+void phase_interior(SlabRank& R, double* x, cudaStream_t s) {
+  if (R.kb < R.np && R.kb > 0) patch_stage(R.pc_lo, R.r.get(), nullptr, R.sols.get(), s);
+  const int64_t nplain = R.n_own - seg_total(R.pin_seg);
+  k::shard_scatter(nplain, R.own_plain.get(), R.map.inv_ptr.get(), R.map.inv.get(), R.sols.get(), nullptr,
+                   R.omega_w.get(), nullptr, x, s);
+}
+
+void phase_lower(SlabRank& R, double* x, cudaStream_t s) {
+  const int64_t npin = seg_total(R.pin_seg);
+  if (npin == 0) return;
+  k::scatter_vals(npin, R.pin.get(), R.zin.get(), R.init.get(), s);
+  k::shard_scatter(npin, R.own_pin.get(), R.map.inv_ptr.get(), R.map.inv.get(), R.sols.get(), R.init.get(),
+                   R.omega_w.get(), nullptr, x, s);
+}
+
+void exchange_nccl(SlabRank& R, const std::vector<Seg>& sends, double* sbuf, const std::vector<Seg>& recvs,
+                   double* rbuf, cudaStream_t s) {
+  if (sends.empty() && recvs.empty()) return;
+  PDB_NCCL_S(ncclGroupStart());
+  for (const auto& g : sends) PDB_NCCL_S(ncclSend(sbuf + g.off, static_cast<size_t>(g.cnt), ncclDouble, g.peer, R.comm, s));
+  for (const auto& g : recvs) PDB_NCCL_S(ncclRecv(rbuf + g.off, static_cast<size_t>(g.cnt), ncclDouble, g.peer, R.comm, s));
+  PDB_NCCL_S(ncclGroupEnd());
+}
+
+// emulated group: copy rank r's segment for q into q's receive segment from r
+void exchange_local(pdb_slab_s& g, bool partials, cudaStream_t s) {
+  for (auto& Rp : g.ranks) {
+    SlabRank& R = *Rp;
+    const auto& sends = partials ? R.up_seg : R.xs_seg;
+    const double* sbuf = partials ? R.zup.get() : R.xsend.get();
+    for (const auto& sg : sends) {
+      SlabRank& Q = *g.ranks[static_cast<size_t>(sg.peer)];
+      const auto& recvs = partials ? Q.pin_seg : Q.xr_seg;
+      double* rbuf = partials ? Q.zin.get() : Q.xrecv.get();
+      bool found = false;
+      for (const auto& rg : recvs)
+        if (rg.peer == R.rank) {
+          require(rg.cnt == sg.cnt, Errc::internal, "slab exchange: segment sizes differ");
+          PDB_CUDA(cudaMemcpyAsync(rbuf + rg.off, sbuf + sg.off, sg.cnt * sizeof(double), cudaMemcpyDeviceToDevice, s));
+          found = true;
+        }
+      require(found, Errc::internal, "slab exchange: no matching receive");
+    }
+  }
+}
+
+}  // namespace
+
+// NCCL rank: interface first, exchanges on the side stream.
+void slab_relax_rank(SlabRank& R, const double* b, double* x, int64_t sweeps, cudaStream_t s) {
+  if (R.nranks > 1) {
+    require(R.comm != nullptr, Errc::invalid_argument, "shard has no communicator");
+    if (!R.side) {
+      PDB_CUDA(cudaStreamCreateWithFlags(&R.side, cudaStreamNonBlocking));
+      for (auto& e : R.ev) PDB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+  }
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    phase_interface(R, b, x, s);
+    if (R.nranks > 1) {
+      PDB_CUDA(cudaEventRecord(R.ev[0], s));
+      PDB_CUDA(cudaStreamWaitEvent(R.side, R.ev[0], 0));
+      exchange_nccl(R, R.up_seg, R.zup.get(), R.pin_seg, R.zin.get(), R.side);
+      PDB_CUDA(cudaEventRecord(R.ev[1], R.side));
+    }
+    phase_interior(R, x, s);  // overlaps the partial-sum exchange
+    if (R.nranks > 1) PDB_CUDA(cudaStreamWaitEvent(s, R.ev[1], 0));
+    phase_lower(R, x, s);
+    const int64_t nxs = seg_total(R.xs_seg);
+    if (R.nranks > 1) {
+      if (nxs) k::gather_vals(nxs, R.xs.get(), x, R.xsend.get(), s);
+      PDB_CUDA(cudaEventRecord(R.ev[2], s));
+      PDB_CUDA(cudaStreamWaitEvent(R.side, R.ev[2], 0));
+      exchange_nccl(R, R.xs_seg, R.xsend.get(), R.xr_seg, R.xrecv.get(), R.side);
+      PDB_CUDA(cudaEventRecord(R.ev[3], R.side));
+      PDB_CUDA(cudaStreamWaitEvent(s, R.ev[3], 0));
+      const int64_t nxr = seg_total(R.xr_seg);
+      if (nxr) k::scatter_vals(nxr, R.xr.get(), R.xrecv.get(), x, s);
+    }
+  }
+  PDB_LAUNCH_CHECK();
+}
+
+// Emulated group: W ranks' phases in order, exchanges as device copies.
+void slab_relax_group(pdb_slab_s& g, const std::vector<const double*>& b, const std::vector<double*>& x,
+                      int64_t sweeps, cudaStream_t s) {
+  const size_t W = g.ranks.size();
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    for (size_t r = 0; r < W; ++r) phase_interface(*g.ranks[r], b[r], x[r], s);
+    exchange_local(g, true, s);
+    for (size_t r = 0; r < W; ++r) phase_interior(*g.ranks[r], x[r], s);
+    for (size_t r = 0; r < W; ++r) phase_lower(*g.ranks[r], x[r], s);
+    for (size_t r = 0; r < W; ++r) {
+      SlabRank& R = *g.ranks[r];
+      const int64_t nxs = seg_total(R.xs_seg);
+      if (nxs) k::gather_vals(nxs, R.xs.get(), x[r], R.xsend.get(), s);
+    }
+    exchange_local(g, false, s);
+    for (size_t r = 0; r < W; ++r) {
+      SlabRank& R = *g.ranks[r];
+      const int64_t nxr = seg_total(R.xr_seg);
+      if (nxr) k::scatter_vals(nxr, R.xr.get(), R.xrecv.get(), x[r], s);
+    }
+  }
+  PDB_LAUNCH_CHECK();
+}
+
+pdb_slab_s* slab_new(int rank, int nranks, bool emulated) {
+  require(nranks >= 1 && rank >= 0 && rank < nranks, Errc::invalid_argument, "rank must be in [0, nranks)");
+  auto g = std::make_unique<pdb_slab_s>();
+  g->emulated = emulated;
+  if (emulated) {
+    for (int r = 0; r < nranks; ++r) {
+      g->ranks.push_back(std::make_unique<SlabRank>());
+      g->ranks.back()->rank = r;
+      g->ranks.back()->nranks = nranks;
+    }
+  } else {
+    g->ranks.push_back(std::make_unique<SlabRank>());
+    g->ranks.back()->rank = rank;
+    g->ranks.back()->nranks = nranks;
+  }
+  return g.release();
+}
+
+void slab_delete(pdb_slab_s* g) { delete g; }
+
+void slab_attach(pdb_slab_s& g, const unsigned char* id128) {
+  require(!g.emulated, Errc::invalid_argument, "an emulated group needs no communicator");
+  SlabRank& R = *g.ranks[0];
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id128, sizeof(uid.internal));
+  PDB_NCCL_S(ncclCommInitRank(&R.comm, R.nranks, uid, R.rank));
+}
+
+const SlabRank& slab_rank(const pdb_slab_s& g, int i) {
+  require(i >= 0 && i < static_cast<int>(g.ranks.size()), Errc::invalid_argument, "rank index out of range");
+  return *g.ranks[static_cast<size_t>(i)];
+}
+
+void slab_relax(pdb_slab_s& g, const std::vector<const double*>& b, const std::vector<double*>& x, int64_t sweeps,
+                cudaStream_t s) {
+  if (g.emulated)
+    slab_relax_group(g, b, x, sweeps, s);
+  else
+    slab_relax_rank(*g.ranks[0], b[0], x[0], sweeps, s);
+}
+
+int slab_local_ranks(const pdb_slab_s& g) { return static_cast<int>(g.ranks.size()); }
+
+SlabInfo slab_info(const pdb_slab_s& g, int i) {
+  const SlabRank& R = slab_rank(g, i);
+  return SlabInfo{R.rank, R.nranks, R.nl, static_cast<int64_t>(R.rows.size()), R.np, R.k0, R.kb, R.n_own,
+                  seg_total(R.up_seg), seg_total(R.pin_seg), seg_total(R.xs_seg), seg_total(R.xr_seg)};
+}
+
+void slab_local_dofs(const pdb_slab_s& g, int i, int64_t* out) {
+  const SlabRank& R = slab_rank(g, i);
+  std::copy(R.gid.begin(), R.gid.end(), out);
+}
+
+void slab_owned(const pdb_slab_s& g, int i, int64_t* out) {
+  const SlabRank& R = slab_rank(g, i);
+  cudaStream_t s = cudaStreamPerThread;
+  const int64_t npin = seg_total(R.pin_seg);
+  std::vector<int64_t> o;
+  if (R.n_own > 0) {
+    const std::vector<int32_t> plain = R.own_plain.to_host(s), pinv = R.own_pin.to_host(s);
+    for (int64_t k = 0; k < R.n_own - npin; ++k) o.push_back(plain[static_cast<size_t>(k)]);
+    for (int64_t k = 0; k < npin; ++k) o.push_back(pinv[static_cast<size_t>(k)]);
+  }
+  std::sort(o.begin(), o.end());
+  std::copy(o.begin(), o.end(), out);
+}
+
+}  // namespace pdb

@@ -731,6 +731,62 @@ class Shard(_Handle):
         _check(_lib.pdb_shard_relax_device(self._ptr, d_b, d_x, sweeps, stream or None))
 
 
+_sig("pdb_slab_create", C.c_int, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int64, _P, C.c_double, C.c_char_p,
+     C.POINTER(_P))
+_sig("pdb_slab_local_ranks", C.c_int, _P)
+_sig("pdb_slab_info", C.c_int, _P, C.c_int, _I64)
+_sig("pdb_slab_local_dofs", C.c_int, _P, C.c_int, _I64)
+_sig("pdb_slab_owned", C.c_int, _P, C.c_int, _I64)
+_sig("pdb_slab_relax_device", C.c_int, _P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int64, C.c_void_p)
+_sig("pdb_slab_free", None, _P)
+
+SLAB_INFO = ("rank", "nranks", "n_local", "n_rows", "n_patches", "first_patch", "split", "n_owned", "n_up", "n_pin",
+             "n_xs", "n_xr")
+
+
+class Slab(_Handle):
+    """Rank-local multi-GPU sweep shards (pdb_slab_*): one rank with an NCCL
+    id, or an emulated group of all ranks on one GPU (nccl_id None)."""
+    _free = _lib.pdb_slab_free
+
+    @classmethod
+    def create(cls, slabs, rank: int, nranks: int, patch_size: int, db: Optional["Database"] = None,
+               omega: float = 1.0, nccl_id: Optional[bytes] = None) -> "Slab":
+        arr = (C.c_void_p * len(slabs))(*[p.ptr for p in slabs])
+        out = C.c_void_p()
+        _check(_lib.pdb_slab_create(arr, len(slabs), rank, nranks, patch_size, db.ptr if db is not None else None,
+                                    omega, nccl_id, C.byref(out)))
+        h = cls(out)
+        h._keep = list(slabs)
+        return h
+
+    @property
+    def local_ranks(self) -> int:
+        return _lib.pdb_slab_local_ranks(self._ptr)
+
+    def info(self, i: int = 0) -> dict:
+        out = np.zeros(12, np.int64)
+        _check(_lib.pdb_slab_info(self._ptr, i, _ip(out)))
+        return dict(zip(SLAB_INFO, (int(v) for v in out)))
+
+    def local_dofs(self, i: int = 0) -> np.ndarray:
+        out = np.empty(self.info(i)["n_local"], np.int64)
+        _check(_lib.pdb_slab_local_dofs(self._ptr, i, _ip(out)))
+        return out
+
+    def owned(self, i: int = 0) -> np.ndarray:
+        out = np.empty(self.info(i)["n_owned"], np.int64)
+        _check(_lib.pdb_slab_owned(self._ptr, i, _ip(out)))
+        return out
+
+    def relax_device(self, d_b, d_x, sweeps: int, stream: int = 0) -> None:
+        """d_b, d_x: one device pointer per local rank (vectors of its local DoFs)."""
+        L = self.local_ranks
+        bb = (C.c_void_p * L)(*d_b)
+        xx = (C.c_void_p * L)(*d_x)
+        _check(_lib.pdb_slab_relax_device(self._ptr, bb, xx, sweeps, stream or None))
+
+
 def compressibility_curve(m: Matrix, ps: "PatchSet", method: int, eps_grid) -> list:
     """Reference compressibility_curve: [(eps, db_size, ratio)] for greedy
     first-match compression over an ascending tolerance grid."""

@@ -1,0 +1,85 @@
+"""Rank-local multi-GPU sweep (csrc/slab.cu) on one GPU as an emulated group
+(pytest -m gpu): W ranks, each built only from its own slab rows
+(pdb_problem_generate_slab), patches detected locally, weights / ownership /
+exchange lists set up with the neighbours, exchanges as device copies.  After
+k sweeps the owned DoFs of all ranks must be BITWISE the single-GPU
+pdb_relax of the whole problem (the interface partial sums continue in the
+reference's ascending patch order, precond.cpp:81-86), for exact and
+compressed preconditioners, W = 2, 3, 8, at configs 2 and 3 (full size) and
+reduced configs 1-5.  Also: every global DoF is owned by exactly one rank,
+the ranks' patch ranges are consecutive, and setup rejects slabs thinner than
+two cell layers.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def emulated_relax(P, sl, b, x0, sweeps):
+    L = sl.local_ranks
+    gids = [sl.local_dofs(i) for i in range(L)]
+    bs = [torch.from_numpy(b[g].copy()).cuda() for g in gids]
+    xs = [torch.from_numpy(x0[g].copy()).cuda() for g in gids]
+    sl.relax_device([t.data_ptr() for t in bs], [t.data_ptr() for t in xs], sweeps)
+    torch.cuda.synchronize()
+    x = np.full_like(x0, np.nan)
+    owner = np.full(len(x0), -1)
+    for i in range(L):
+        own = sl.owned(i)
+        g = gids[i][own]
+        assert (owner[g] < 0).all(), "a DoF owned twice"
+        owner[g] = i
+        x[g] = xs[i].cpu().numpy()[own]
+    return x, owner
+
+
+CASES = [  # config, cells, patch size, ranks, database
+    (2, 0, 25, 2, "kmeans"), (2, 0, 25, 8, "exact"), (3, 0, 27, 3, "greedy"), (3, 0, 27, 8, "exact"),
+    (1, 0, 9, 3, "greedy"), (2, 16, 25, 2, "exact"), (3, 8, 27, 4, "greedy"), (4, 8, 22, 2, "kmeans"),
+    (5, 4, 192, 2, "exact"),
+]
+
+
+@pytest.mark.parametrize("cfg,cells,ps,ranks,method", CASES)
+def test_emulated_slabs_match_single_gpu(P, cfg, cells, ps, ranks, method):
+    g = P.Problem.generate(cfg, cells)
+    A = g.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    db = None
+    if method == "greedy":
+        db = P.Database.build(A, pset, P.GREEDY_L1, eps=0.5 if cfg != 3 else 0.137)
+    elif method == "kmeans":
+        db = P.Database.build(A, pset, P.KMEANS_ENTRYWISE, db_size=64, seed=42, max_iters=5)
+    pc = P.Preconditioner.create(A, pset, db, omega=0.9)
+    b = g.rhs()
+    x0 = np.random.default_rng(cfg).uniform(-1, 1, len(b))
+    want, _ = pc.relax(A, b, x0, 3, history=False)
+    slabs = [P.Problem.generate_slab(cfg, cells, r, ranks) for r in range(ranks)]
+    sl = P.Slab.create(slabs, 0, ranks, ps, db, omega=0.9)
+    info = [sl.info(i) for i in range(ranks)]
+    assert sum(f["n_patches"] for f in info) == pset.count
+    assert [f["first_patch"] for f in info] == list(np.cumsum([0] + [f["n_patches"] for f in info[:-1]]))
+    got, owner = emulated_relax(P, sl, b, x0, 3)
+    assert (owner >= 0).all(), "a DoF without owner"
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def test_single_rank_slab_equals_relax(P):
+    g = P.Problem.generate(3, 6)
+    A = g.matrix()
+    pset = P.PatchSet.detect(A, 27)
+    pc = P.Preconditioner.create(A, pset, None, omega=1.0)
+    b = g.rhs()
+    x0 = np.zeros_like(b)
+    want, _ = pc.relax(A, b, x0, 4, history=False)
+    sl = P.Slab.create([P.Problem.generate_slab(3, 6, 0, 1)], 0, 1, 27)
+    got, _ = emulated_relax(P, sl, b, x0, 4)
+    assert np.array_equal(got, want)
+
+
+def test_thin_slabs_rejected(P):
+    with pytest.raises(P.PatchdbError):
+        [P.Problem.generate_slab(3, 6, r, 4) for r in range(4)]
