@@ -198,6 +198,10 @@ PDB_API int64_t pdb_problem_nnz(pdb_problem p);
 PDB_API pdb_status pdb_problem_generate_slab(const pdb_gen_options* opts, int rank, int nranks, pdb_problem* out);
 /* Global row count of the (slab) problem, and its global row ranges
  * [lo, hi) as 2 * count int64 values (count = pdb_problem_row_range_count). */
+/* Rows of the DoFs of cell layers [c0, c1) along the slowest axis, labelled
+ * rank `rank` of `nranks` (a slab, or a thin neighbour of one). */
+PDB_API pdb_status pdb_problem_generate_cells(const pdb_gen_options* opts, int64_t c0, int64_t c1, int rank,
+                                              int nranks, pdb_problem* out);
 PDB_API int64_t pdb_problem_rows_global(pdb_problem p);
 PDB_API int64_t pdb_problem_row_range_count(pdb_problem p);
 PDB_API pdb_status pdb_problem_row_ranges(pdb_problem p, int64_t* ranges);
@@ -336,6 +340,13 @@ PDB_API void pdb_shard_free(pdb_shard sh);
 typedef struct pdb_slab_s* pdb_slab;
 PDB_API pdb_status pdb_slab_create(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
                                    pdb_database db, double omega, const unsigned char* nccl_id, pdb_slab* out);
+/* Emulated group of a SUBSET of the ranks (ascending `ranks`, count of them;
+ * exact preconditioners only): messages to or from absent ranks are dropped,
+ * so a rank's slab plus thin neighbours (pdb_problem_generate_cells) runs one
+ * rank's share of a job larger than one GPU (config 5 at 96^3). */
+PDB_API pdb_status pdb_slab_create_subset(pdb_problem* slabs, int count, const int* ranks, int rank, int nranks,
+                                          int64_t patch_size, pdb_database db, double omega,
+                                          const unsigned char* nccl_id, pdb_slab* out);
 /* Local ranks held by the handle (1, or nranks for an emulated group). */
 PDB_API int pdb_slab_local_ranks(pdb_slab sh);
 /* info[12]: rank, nranks, local DoFs, local rows, local patches, first global
@@ -347,6 +358,10 @@ PDB_API pdb_status pdb_slab_owned(pdb_slab sh, int i, int64_t* local_idx);
 /* Sweeps on device vectors of the local DoFs, one b / x per local rank. */
 PDB_API pdb_status pdb_slab_relax_device(pdb_slab sh, const double* const* d_b, double* const* d_x, int64_t sweeps,
                                          void* stream);
+/* Local rank i's sweep phases alone, exchanges skipped (per-rank timing of a
+ * slice of a job larger than this GPU; the values are not a valid sweep). */
+PDB_API pdb_status pdb_slab_relax_rank_device(pdb_slab sh, int i, const double* d_b, double* d_x, int64_t sweeps,
+                                              void* stream);
 PDB_API void pdb_slab_free(pdb_slab sh);
 
 /* Sharded setup: a communicator over nranks processes (one GPU each; id from

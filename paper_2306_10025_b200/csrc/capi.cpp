@@ -286,6 +286,24 @@ PDB_API pdb_status pdb_problem_generate_slab(const pdb_gen_options* o, int rank,
   });
 }
 
+PDB_API pdb_status pdb_problem_generate_cells(const pdb_gen_options* o, int64_t c0, int64_t c1, int rank, int nranks,
+                                              pdb_problem* out) {
+  if (o == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(o->physics >= 0 && o->physics <= 2, Errc::invalid_argument,
+            "physics must be 0 (diffusion), 1 (Stokes) or 2 (elasticity)");
+    const RowWindow w = cells_window(*o, c0, c1);
+    auto p = std::make_unique<pdb_problem_s>();
+    if (o->physics == 0)
+      generate_scalar(*o, *p, &w);
+    else
+      generate_system(*o, *p, &w);
+    p->slab_rank = rank;
+    p->slab_ranks = nranks;
+    *out = p.release();
+  });
+}
+
 PDB_API int64_t pdb_problem_rows_global(pdb_problem p) {
   return p == nullptr ? 0 : (p->is_slab() ? p->n_global : p->a.n);
 }
@@ -790,19 +808,37 @@ PDB_API void pdb_shard_free(pdb_shard sh) { shard_delete(sh); }
 
 PDB_API pdb_status pdb_slab_create(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
                                    pdb_database db, double omega, const unsigned char* nccl_id, pdb_slab* out) {
+  return pdb_slab_create_subset(slabs, count, nullptr, rank, nranks, patch_size, db, omega, nccl_id, out);
+}
+
+PDB_API pdb_status pdb_slab_create_subset(pdb_problem* slabs, int count, const int* ranks, int rank, int nranks,
+                                          int64_t patch_size, pdb_database db, double omega,
+                                          const unsigned char* nccl_id, pdb_slab* out) {
   if (slabs == nullptr || out == nullptr) return arg_error("null argument");
   return guarded([&] {
     require(count >= 1, Errc::invalid_argument, "need at least one slab");
     require(patch_size >= 1, Errc::invalid_argument, "patch_size must be >= 1");
     const bool emulated = nccl_id == nullptr && nranks > 1;
-    require(emulated ? count == nranks : count == 1, Errc::invalid_argument,
-            "one slab per process with a communicator, all nranks slabs for an emulated group");
+    std::vector<int> rl;
+    if (emulated) {
+      for (int i = 0; i < count; ++i) rl.push_back(ranks ? ranks[i] : i);
+      for (int i = 0; i < count; ++i)
+        require(rl[static_cast<size_t>(i)] >= 0 && rl[static_cast<size_t>(i)] < nranks &&
+                    (i == 0 || rl[static_cast<size_t>(i)] > rl[static_cast<size_t>(i) - 1]),
+                Errc::invalid_argument, "emulated ranks must be ascending in [0, nranks)");
+      require(ranks != nullptr || count == nranks, Errc::invalid_argument,
+              "an emulated group holds all nranks slabs (or name its subset of ranks)");
+      require(ranks == nullptr || db == nullptr, Errc::invalid_argument,
+              "a subset of ranks cannot place the database's phi: exact preconditioners only");
+    } else {
+      require(count == 1, Errc::invalid_argument, "one slab per process with a communicator");
+    }
     std::vector<pdb_problem_s*> probs;
     for (int i = 0; i < count; ++i) {
       require(slabs[i] != nullptr, Errc::invalid_argument, "null argument");
       probs.push_back(slabs[i]);
     }
-    std::unique_ptr<pdb_slab_s, void (*)(pdb_slab_s*)> g(slab_new(rank, nranks, emulated), slab_delete);
+    std::unique_ptr<pdb_slab_s, void (*)(pdb_slab_s*)> g(slab_new(rank, nranks, emulated, rl), slab_delete);
     if (nccl_id != nullptr && nranks > 1) slab_attach(*g, nccl_id);
     slab_setup(*g, probs, patch_size, db, omega, default_stream());
     *out = g.release();
@@ -840,6 +876,15 @@ PDB_API pdb_status pdb_slab_relax_device(pdb_slab sh, const double* const* d_b, 
     std::vector<const double*> b(d_b, d_b + L);
     std::vector<double*> x(d_x, d_x + L);
     slab_relax(*sh, b, x, sweeps, stream_of(stream));
+  });
+}
+
+PDB_API pdb_status pdb_slab_relax_rank_device(pdb_slab sh, int i, const double* d_b, double* d_x, int64_t sweeps,
+                                              void* stream) {
+  if (sh == nullptr || d_b == nullptr || d_x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(i >= 0 && i < slab_local_ranks(*sh), Errc::invalid_argument, "rank index out of range");
+    slab_relax_one(*sh, i, d_b, d_x, sweeps, stream_of(stream));
   });
 }
 

@@ -41,9 +41,13 @@ std::string fmt_f(double v) {  // std::to_string(double)
   return buf;
 }
 
+}  // namespace
+
 std::string singular_msg(int32_t status, double best) {
   return "singular matrix: pivot " + fmt_f(best) + " below threshold in column " + std::to_string(status - 1);
 }
+
+namespace {
 
 template <typename T>
 std::vector<T> d2h(const T* d, size_t n, cudaStream_t s) {

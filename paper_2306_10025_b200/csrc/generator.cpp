@@ -763,10 +763,15 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWind
 RowWindow slab_window(const pdb_gen_options& o, int rank, int nranks) {
   require(nranks >= 1 && rank >= 0 && rank < nranks, Errc::invalid_argument, "rank must be in [0, nranks)");
   const Index C = o.cells;
-  const int d = o.dim, p = o.degree;
-  const Index s0 = C * rank / nranks, s1 = C * (rank + 1) / nranks;
   require(nranks == 1 || C / nranks >= 2, Errc::invalid_argument,
           "slab partition too thin: every rank needs at least two cell layers");
+  return cells_window(o, C * rank / nranks, C * (rank + 1) / nranks);
+}
+
+RowWindow cells_window(const pdb_gen_options& o, Index s0, Index s1) {
+  const Index C = o.cells;
+  require(s0 >= 0 && s1 <= C && s0 < s1, Errc::invalid_argument, "cell layer range must satisfy 0 <= c0 < c1 <= cells");
+  const int d = o.dim, p = o.degree;
   const Index npa = C * p + 1;
   const Index layer = d == 3 ? npa * npa : npa;  // nodes per slowest-axis layer
   RowWindow w;

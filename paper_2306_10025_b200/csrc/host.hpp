@@ -63,6 +63,8 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWind
 // Slab of rank r of W along the slowest axis: cells [C r / W, C (r+1) / W);
 // the rows are every DoF of those cells (both faces included).
 RowWindow slab_window(const pdb_gen_options& o, int rank, int nranks);
+// Rows of the DoFs of the cells [c0, c1) along the slowest axis.
+RowWindow cells_window(const pdb_gen_options& o, Index c0, Index c1);
 // pdb_gen_options defaults and the BASELINE config presets (false: config not in 1..5)
 void gen_options_defaults(pdb_gen_options* o);
 bool gen_options_preset(int config, int64_t cells, pdb_gen_options* o);
@@ -146,6 +148,9 @@ void compressibility_curve(const DeviceCsr& a, const pdb_patchset_s& ps, bool sp
 void export_database(const pdb_database_s& db, const std::string& json_path, const std::string& bin_path,
                      cudaStream_t s);
 
+// database.cu: the reference's lu_factor failure text (dense.cpp:59-61)
+std::string singular_msg(int32_t status, double best);
+
 // precond.cpp
 void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& out, cudaStream_t s);
 void precond_compressed(const pdb_patchset_s& ps, const pdb_database_s& db, double omega, pdb_precond_s& out,
@@ -211,7 +216,9 @@ void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* p
 
 // slab.cu -- multi-GPU sweep shards with rank-local data
 struct SlabRank;
-pdb_slab_s* slab_new(int rank, int nranks, bool emulated);
+// emulated: one state per rank in `ranks` (all ranks, or a subset whose absent
+// neighbours' messages are empty -- single-GPU slices of a larger job)
+pdb_slab_s* slab_new(int rank, int nranks, bool emulated, const std::vector<int>& ranks = {});
 void slab_delete(pdb_slab_s* g);
 void slab_attach(pdb_slab_s& g, const unsigned char* id128);
 void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
@@ -227,4 +234,5 @@ SlabInfo slab_info(const pdb_slab_s& g, int i);
 void slab_local_dofs(const pdb_slab_s& g, int i, int64_t* out);
 void slab_owned(const pdb_slab_s& g, int i, int64_t* out);
 int slab_local_ranks(const pdb_slab_s& g);
+void slab_relax_one(pdb_slab_s& g, int i, const double* b, double* x, int64_t sweeps, cudaStream_t s);
 }  // namespace pdb

@@ -113,9 +113,11 @@ struct SlabRank {
 }  // namespace pdb
 
 struct pdb_slab_s {
-  std::vector<std::unique_ptr<pdb::SlabRank>> ranks;  // 1 (NCCL rank) or W (emulated group)
+  std::vector<std::unique_ptr<pdb::SlabRank>> ranks;  // 1 (NCCL rank), or the emulated ranks (ascending)
   bool emulated = false;
   int64_t n_global = 0;
+  std::vector<int> slot;  // emulated: rank -> index in `ranks`, -1 when absent
+  int slot_of(int rank) const { return slot.empty() ? rank : slot[static_cast<size_t>(rank)]; }
 };
 
 namespace pdb {
@@ -128,9 +130,12 @@ using Mail = std::vector<std::vector<int64_t>>;  // [peer] -> payload
 void deliver(pdb_slab_s& g, std::vector<Mail>& out, std::vector<Mail>& in, cudaStream_t s) {
   const int W = g.ranks[0]->nranks;
   in.assign(out.size(), Mail(static_cast<size_t>(W)));
-  if (g.emulated) {
-    for (int r = 0; r < W; ++r)
-      for (int q = 0; q < W; ++q) in[static_cast<size_t>(q)][static_cast<size_t>(r)] = out[static_cast<size_t>(r)][static_cast<size_t>(q)];
+  if (g.emulated) {  // messages to absent ranks are dropped, absent ranks send nothing
+    for (size_t i = 0; i < g.ranks.size(); ++i)
+      for (int q = 0; q < W; ++q) {
+        const int j = g.slot_of(q);
+        if (j >= 0) in[static_cast<size_t>(j)][static_cast<size_t>(g.ranks[i]->rank)] = out[i][static_cast<size_t>(q)];
+      }
     return;
   }
   SlabRank& R = *g.ranks[0];
@@ -234,18 +239,22 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
     loc.row_ptr[static_cast<size_t>(l) + 1] = h.row_ptr[i + 1] - h.row_ptr[i];
   }
   for (int64_t l = 0; l < R.nl; ++l) loc.row_ptr[static_cast<size_t>(l) + 1] += loc.row_ptr[static_cast<size_t>(l)];
+  // rows keep their order and the halo rows are empty, so the local entry
+  // arrays are the slab's in the same order: columns remapped, values lent
+  // (swapped in for the upload and back: config 5 holds 46 GB of them)
   loc.col.resize(h.col.size());
-  loc.val.resize(h.val.size());
-  parallel_rows(static_cast<int64_t>(rows_g.size()), [&](int64_t b, int64_t e) {
-    for (int64_t i = b; i < e; ++i) {
-      int64_t o = loc.row_ptr[static_cast<size_t>(R.rows[static_cast<size_t>(i)])];
-      for (int64_t q = h.row_ptr[static_cast<size_t>(i)]; q < h.row_ptr[static_cast<size_t>(i) + 1]; ++q, ++o) {
-        loc.col[static_cast<size_t>(o)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
-        loc.val[static_cast<size_t>(o)] = h.val[static_cast<size_t>(q)];
-      }
-    }
+  parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
+    for (int64_t q = b; q < e; ++q)
+      loc.col[static_cast<size_t>(q)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
   });
-  upload_csr(loc, R.a, s);
+  loc.val.swap(h.val);
+  try {
+    upload_csr(loc, R.a, s);
+  } catch (...) {
+    loc.val.swap(h.val);
+    throw;
+  }
+  loc.val.swap(h.val);
   detect_patches(R.a, patch_size, R.ps, s);
   R.np = R.ps.np;
   // touched DoFs (global ids, ascending) and the local cover counts
@@ -296,7 +305,8 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     SlabRank& R = *g.ranks[static_cast<size_t>(i)];
     R.k0 = 0;
     for (int q = 0; q < W; ++q) {
-      const auto& m = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      auto m = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      if (m.empty()) m = {0, INT64_MAX, -1};  // absent rank (emulated subset)
       info[static_cast<size_t>(i)].insert(info[static_cast<size_t>(i)].end(), m.begin(), m.end());
       if (q < R.rank) R.k0 += m[0];
     }
@@ -455,6 +465,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     }
     for (int q = 0; q < W; ++q) {
       const auto& rep = in[static_cast<size_t>(i)][static_cast<size_t>(q)];
+      if (g.emulated && g.slot_of(q) < 0) continue;  // absent rank: no reply
       require(rep.size() == asked[static_cast<size_t>(q)].size(), Errc::internal, "slab setup: reply size mismatch");
       for (size_t k = 0; k < rep.size(); ++k)
         if (rep[k]) {
@@ -503,6 +514,12 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     }
     common_setup(R.ps, omega, R.map, s);
     build_inverse(R.map, s);
+    // the residual streams the SELL copy: drop the CSR's columns and values
+    // (config 5: 40 GB per rank) once the patches are extracted
+    if (R.a.nslices > 0 && plan_of(R.a).version == 9) {
+      R.a.col = DevBuf<int32_t>();
+      R.a.val = DevBuf<double>();
+    }
     R.r.alloc(static_cast<size_t>(std::max<int64_t>(R.nl, 1)));
     R.sols.alloc(static_cast<size_t>(std::max<int64_t>(R.np * patch_size, 1)));
     R.init.alloc(static_cast<size_t>(std::max<int64_t>(R.nl, 1)));
@@ -555,7 +572,8 @@ void exchange_local(pdb_slab_s& g, bool partials, cudaStream_t s) {
     const auto& sends = partials ? R.up_seg : R.xs_seg;
     const double* sbuf = partials ? R.zup.get() : R.xsend.get();
     for (const auto& sg : sends) {
-      SlabRank& Q = *g.ranks[static_cast<size_t>(sg.peer)];
+      if (g.slot_of(sg.peer) < 0) continue;  // absent rank (emulated subset)
+      SlabRank& Q = *g.ranks[static_cast<size_t>(g.slot_of(sg.peer))];
       const auto& recvs = partials ? Q.pin_seg : Q.xr_seg;
       double* rbuf = partials ? Q.zin.get() : Q.xrecv.get();
       bool found = false;
@@ -631,12 +649,32 @@ void slab_relax_group(pdb_slab_s& g, const std::vector<const double*>& b, const 
   PDB_LAUNCH_CHECK();
 }
 
-pdb_slab_s* slab_new(int rank, int nranks, bool emulated) {
+// One local rank's sweep phases alone (exchanges skipped): the per-rank work
+// of a sweep, timed on a single GPU for a slice of a larger job.
+void slab_relax_one(pdb_slab_s& g, int i, const double* b, double* x, int64_t sweeps, cudaStream_t s) {
+  SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+  for (int64_t sw = 0; sw < sweeps; ++sw) {
+    phase_interface(R, b, x, s);
+    phase_interior(R, x, s);
+    phase_lower(R, x, s);
+    const int64_t nxs = seg_total(R.xs_seg), nxr = seg_total(R.xr_seg);
+    if (nxs) k::gather_vals(nxs, R.xs.get(), x, R.xsend.get(), s);
+    if (nxr) k::scatter_vals(nxr, R.xr.get(), R.xrecv.get(), x, s);
+  }
+  PDB_LAUNCH_CHECK();
+}
+
+pdb_slab_s* slab_new(int rank, int nranks, bool emulated, const std::vector<int>& ranks) {
   require(nranks >= 1 && rank >= 0 && rank < nranks, Errc::invalid_argument, "rank must be in [0, nranks)");
   auto g = std::make_unique<pdb_slab_s>();
   g->emulated = emulated;
   if (emulated) {
-    for (int r = 0; r < nranks; ++r) {
+    std::vector<int> rl = ranks;
+    if (rl.empty())
+      for (int r = 0; r < nranks; ++r) rl.push_back(r);
+    g->slot.assign(static_cast<size_t>(nranks), -1);
+    for (int r : rl) {
+      g->slot[static_cast<size_t>(r)] = static_cast<int>(g->ranks.size());
       g->ranks.push_back(std::make_unique<SlabRank>());
       g->ranks.back()->rank = r;
       g->ranks.back()->nranks = nranks;

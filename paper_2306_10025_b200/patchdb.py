@@ -327,6 +327,15 @@ class Problem(_Handle):
         _check(_lib.pdb_problem_generate_slab(C.byref(o), rank, nranks, C.byref(out)))
         return cls(out)
 
+    @classmethod
+    def generate_cells(cls, config: int, cells: int, c0: int, c1: int, rank: int, nranks: int,
+                       **overrides) -> "Problem":
+        """Rows of the cell layers [c0, c1) (pdb_problem_generate_cells)."""
+        o = cls._options(config, cells, overrides)
+        out = C.c_void_p()
+        _check(_lib.pdb_problem_generate_cells(C.byref(o), c0, c1, rank, nranks, C.byref(out)))
+        return cls(out)
+
     @property
     def rows_global(self) -> int:
         return _lib.pdb_problem_rows_global(self._ptr)
@@ -739,6 +748,11 @@ _sig("pdb_slab_local_dofs", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_owned", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_relax_device", C.c_int, _P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int64, C.c_void_p)
 _sig("pdb_slab_free", None, _P)
+_sig("pdb_slab_create_subset", C.c_int, C.POINTER(_P), C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int64, _P,
+     C.c_double, C.c_char_p, C.POINTER(_P))
+_sig("pdb_slab_relax_rank_device", C.c_int, _P, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+_sig("pdb_problem_generate_cells", C.c_int, C.POINTER(GenOptions), C.c_int64, C.c_int64, C.c_int, C.c_int,
+     C.POINTER(_P))
 
 SLAB_INFO = ("rank", "nranks", "n_local", "n_rows", "n_patches", "first_patch", "split", "n_owned", "n_up", "n_pin",
              "n_xs", "n_xr")
@@ -759,6 +773,21 @@ class Slab(_Handle):
         h = cls(out)
         h._keep = list(slabs)
         return h
+
+    @classmethod
+    def create_subset(cls, slabs, ranks, rank: int, nranks: int, patch_size: int, omega: float = 1.0) -> "Slab":
+        """Emulated group of a subset of the ranks (exact preconditioners)."""
+        arr = (C.c_void_p * len(slabs))(*[p.ptr for p in slabs])
+        rk = (C.c_int * len(ranks))(*ranks)
+        out = C.c_void_p()
+        _check(_lib.pdb_slab_create_subset(arr, len(slabs), rk, rank, nranks, patch_size, None, omega, None,
+                                           C.byref(out)))
+        h = cls(out)
+        h._keep = list(slabs)
+        return h
+
+    def relax_rank_device(self, i: int, d_b: int, d_x: int, sweeps: int, stream: int = 0) -> None:
+        _check(_lib.pdb_slab_relax_rank_device(self._ptr, i, d_b, d_x, sweeps, stream or None))
 
     @property
     def local_ranks(self) -> int:

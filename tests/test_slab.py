@@ -83,3 +83,34 @@ def test_single_rank_slab_equals_relax(P):
 def test_thin_slabs_rejected(P):
     with pytest.raises(P.PatchdbError):
         [P.Problem.generate_slab(3, 6, r, 4) for r in range(4)]
+
+
+@pytest.mark.parametrize("cfg,cells,ps,ranks,r", [(3, 12, 27, 4, 1), (5, 8, 192, 4, 2)])
+def test_subset_group_one_rank_slice(P, cfg, cells, ps, ranks, r):
+    """A slice of a larger job on one GPU: rank r's slab plus one-cell-layer
+    neighbours (pdb_problem_generate_cells) as an emulated subset.  After one
+    sweep from the same x0, rank r's owned DoFs are bitwise the whole
+    problem's single-GPU sweep (exact patches)."""
+    g = P.Problem.generate(cfg, cells)
+    A = g.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    pc = P.Preconditioner.create(A, pset, None, omega=1.0)
+    b = g.rhs()
+    x0 = np.random.default_rng(4).uniform(-1, 1, len(b))
+    want, _ = pc.relax(A, b, x0, 1, history=False)
+    s0, s1 = cells * r // ranks, cells * (r + 1) // ranks
+    probs = [P.Problem.generate_cells(cfg, cells, s0 - 1, s0, r - 1, ranks), P.Problem.generate_slab(cfg, cells, r, ranks),
+             P.Problem.generate_cells(cfg, cells, s1, s1 + 1, r + 1, ranks)]
+    sl = P.Slab.create_subset(probs, [r - 1, r, r + 1], r, ranks, ps)
+    gid = sl.local_dofs(1)
+    bl = torch.from_numpy(b[gid].copy()).cuda()
+    xl = torch.from_numpy(x0[gid].copy()).cuda()
+    bs = [torch.from_numpy(b[sl.local_dofs(i)].copy()).cuda() for i in range(3)]
+    xs = [torch.from_numpy(x0[sl.local_dofs(i)].copy()).cuda() for i in range(3)]
+    sl.relax_device([t.data_ptr() for t in bs], [t.data_ptr() for t in xs], 1)
+    own = sl.owned(1)
+    got = xs[1].cpu().numpy()[own]
+    assert np.array_equal(got, want[gid[own]])
+    # the rank-alone timing path runs (values not a sweep: exchanges skipped)
+    sl.relax_rank_device(1, bl.data_ptr(), xl.data_ptr(), 2)
+    torch.cuda.synchronize()
