@@ -198,9 +198,9 @@ constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
 
 // Solutions are written in patch order (sols[order[slot] * ps + i]).  R is
 // staged unpadded (patch p, local row k at p * ps + k), so the copy is a
-// flat, division-free loop; the A fragments are zero for k >= ps, which
-// cancels the neighbouring patch's values a B fragment reads there, and the
-// stage is zero-filled past the tile's cnt * ps live values (no NaN garbage).
+// flat, division-free loop; the B operand is masked to 0 for k >= ps (those
+// stage entries belong to the next patch), and the stage is zero-filled past
+// the tile's cnt * ps live values.
 template <int MT, int KS>
 __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
                                                                    const int32_t* __restrict__ tile_start,
@@ -253,7 +253,12 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
       double c0 = 0.0, c1 = 0.0;
       const double* bp = rk + (nt * 8 + g) * ps + tg;
 #pragma unroll
-      for (int q = 0; q < KS; ++q) dmma_m8n8k4(c0, c1, a[q], bp[q * 4]);
+      for (int q = 0; q < KS; ++q) {
+        // rows k >= ps of the last k-step belong to the next patch: mask them
+        // (a zero A entry times a non-finite neighbour value would be NaN)
+        const double bv = (q < KS - 1 || q * 4 + tg < ps) ? bp[q * 4] : 0.0;
+        dmma_m8n8k4(c0, c1, a[q], bv);
+      }
       const int p0 = nt * 8 + 2 * tg;
       if (row < ps) {
         if (p0 < cnt) out[(int64_t)ko[p0] * ps + row] = c0;

@@ -61,7 +61,7 @@ def big_text(n=40000, seed=0, bad_at=None):
     rows = rng.integers(1, n + 1, 6 * n)
     cols = rng.integers(1, n + 1, 6 * n)
     vals = rng.standard_normal(6 * n)
-    lines = [f"{r} {c} {v!r}" for r, c, v in zip(rows, cols, vals)]
+    lines = [f"{int(r)} {int(c)} {float(v)!r}" for r, c, v in zip(rows, cols, vals)]
     for k in range(0, len(lines), 997):
         lines.insert(k, "")  # blank lines inside the entry list
     if bad_at is not None:
