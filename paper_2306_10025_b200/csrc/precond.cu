@@ -266,6 +266,9 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
   require(db.np == ps.np, Errc::dimension_mismatch, "database does not cover the patch set");
   // phi onto the database (Database::phi_onto, compress.cpp:3-10)
   const std::vector<int32_t> phi = db.phi.to_host(s);
+  if (!check_onto)  // shards: not onto, but out-of-range ids must never reach the apply kernels
+    for (int32_t j : phi)
+      require(j >= 0 && j < db.m, Errc::invalid_argument, "assignment map entry outside the database");
   if (check_onto) {
     std::vector<char> hit(static_cast<size_t>(db.m), 0);
     bool ok = true;

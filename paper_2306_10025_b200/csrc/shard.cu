@@ -72,6 +72,13 @@ void put(DevBuf<T>& d, const std::vector<T>& h, cudaStream_t s) {
 void shard_create(const HostCsr& A, const pdb_patchset_s& gps, const pdb_database_s* db, double omega, int rank,
                   int nranks, pdb_shard_s& sh, cudaStream_t s) {
   require_device();
+  // the patch set and the database must describe this matrix (the reference
+  // rejects mismatches with dimension_mismatch, precond.cpp:38-52)
+  require(gps.n == A.n, Errc::dimension_mismatch, "patch set does not match the matrix size");
+  if (db) {
+    require(db->np == gps.np, Errc::dimension_mismatch, "database does not cover the patch set");
+    require(db->ps == gps.ps, Errc::dimension_mismatch, "database entry dimension does not match the patch size");
+  }
   const std::vector<int32_t> patches = gps.patches.to_host(s);
   const std::vector<double> weights = gps.weights.to_host(s);
   sh.plan = plan_shard(A.n, A.row_ptr.data(), A.col.data(), A.val.data(), gps.np, gps.ps, patches.data(),

@@ -225,3 +225,20 @@ def test_sharded_bisection_matches_single_gpu(P):
     comm = P.Comm.create(P.comm_unique_id(), 0, 1)
     got, ge = P.Database.build_to_size(A, ps, 12, 20, 2, comm=comm)
     assert ge == we and np.array_equal(got.phi(), want.phi())
+
+
+@pytest.mark.gpu
+def test_shard_create_rejects_mismatched_inputs(P):
+    """pdb_shard_create checks the patch set and the database against the
+    matrix (dimension_mismatch), as the reference's preconditioner does."""
+    small = P.Problem.generate(1, 8)
+    big = P.Problem.generate(1, 12)
+    As, Ab = small.matrix(), big.matrix()
+    pss, psb = P.PatchSet.detect(As, 9), P.PatchSet.detect(Ab, 9)
+    with pytest.raises(P.PatchdbError) as e:
+        P.Shard.create(As, psb, None, 1.0, 0, 1)
+    assert e.value.status == P.PDB_ERR_DIMENSION_MISMATCH
+    dbb = P.Database.build(Ab, psb, P.GREEDY_L1, eps=2.0)
+    with pytest.raises(P.PatchdbError) as e:
+        P.Shard.create(As, pss, dbb, 1.0, 0, 1)
+    assert e.value.status == P.PDB_ERR_DIMENSION_MISMATCH
