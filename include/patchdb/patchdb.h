@@ -347,6 +347,20 @@ PDB_API pdb_status pdb_slab_create(pdb_problem* slabs, int count, int rank, int 
 PDB_API pdb_status pdb_slab_create_subset(pdb_problem* slabs, int count, const int* ranks, int rank, int nranks,
                                           int64_t patch_size, pdb_database db, double omega,
                                           const unsigned char* nccl_id, pdb_slab* out);
+/* The same, with the compressed database built from the ranks' OWN patches
+ * (no rank sees the others' matrices): greedy-l1 (opts->method, eps,
+ * best_match) in the round-batched form -- each round's batch matrices are
+ * broadcast by their owners, the resolution is replicated, every rank scans
+ * only its own patches.  The database (entries replicated, phi per rank) is
+ * bitwise the single-GPU pdb_database_build's. */
+PDB_API pdb_status pdb_slab_create_built(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
+                                         const pdb_compress_options* opts, double omega, const unsigned char* nccl_id,
+                                         pdb_slab* out);
+PDB_API int64_t pdb_slab_database_size(pdb_slab sh);
+/* phi of local rank i's patches (its slice of the global phi), and the global
+ * creator patch of every entry (pdb_slab_database_size of them). */
+PDB_API pdb_status pdb_slab_phi(pdb_slab sh, int i, int64_t* phi);
+PDB_API pdb_status pdb_slab_creators(pdb_slab sh, int64_t* creators);
 /* Local ranks held by the handle (1, or nranks for an emulated group). */
 PDB_API int pdb_slab_local_ranks(pdb_slab sh);
 /* info[12]: rank, nranks, local DoFs, local rows, local patches, first global

@@ -845,6 +845,44 @@ PDB_API pdb_status pdb_slab_create_subset(pdb_problem* slabs, int count, const i
   });
 }
 
+PDB_API pdb_status pdb_slab_create_built(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
+                                         const pdb_compress_options* opts, double omega, const unsigned char* nccl_id,
+                                         pdb_slab* out) {
+  if (slabs == nullptr || opts == nullptr || out == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    require(count >= 1, Errc::invalid_argument, "need at least one slab");
+    require(patch_size >= 1, Errc::invalid_argument, "patch_size must be >= 1");
+    const bool emulated = nccl_id == nullptr && nranks > 1;
+    require(emulated ? count == nranks : count == 1, Errc::invalid_argument,
+            "one slab per process with a communicator, all nranks slabs for an emulated group");
+    std::vector<pdb_problem_s*> probs;
+    for (int i = 0; i < count; ++i) {
+      require(slabs[i] != nullptr, Errc::invalid_argument, "null argument");
+      probs.push_back(slabs[i]);
+    }
+    BuildParams p;
+    p.method = opts->method;
+    p.eps = opts->eps;
+    p.best_match = opts->best_match != 0;
+    std::unique_ptr<pdb_slab_s, void (*)(pdb_slab_s*)> g(slab_new(rank, nranks, emulated), slab_delete);
+    if (nccl_id != nullptr && nranks > 1) slab_attach(*g, nccl_id);
+    slab_setup(*g, probs, patch_size, nullptr, omega, default_stream(), &p);
+    *out = g.release();
+  });
+}
+
+PDB_API int64_t pdb_slab_database_size(pdb_slab sh) { return sh == nullptr ? 0 : slab_database_size(*sh); }
+
+PDB_API pdb_status pdb_slab_phi(pdb_slab sh, int i, int64_t* phi) {
+  if (sh == nullptr || phi == nullptr) return arg_error("null argument");
+  return guarded([&] { slab_phi(*sh, i, phi); });
+}
+
+PDB_API pdb_status pdb_slab_creators(pdb_slab sh, int64_t* creators) {
+  if (sh == nullptr || creators == nullptr) return arg_error("null argument");
+  return guarded([&] { slab_creators(*sh, creators); });
+}
+
 PDB_API int pdb_slab_local_ranks(pdb_slab sh) { return sh == nullptr ? 0 : slab_local_ranks(*sh); }
 
 PDB_API pdb_status pdb_slab_info(pdb_slab sh, int i, int64_t* info) {

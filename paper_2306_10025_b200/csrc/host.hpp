@@ -221,8 +221,14 @@ struct SlabRank;
 pdb_slab_s* slab_new(int rank, int nranks, bool emulated, const std::vector<int>& ranks = {});
 void slab_delete(pdb_slab_s* g);
 void slab_attach(pdb_slab_s& g, const unsigned char* id128);
+// db: replicated database (phi sliced by the global patch offset); build:
+// construct the compressed database from the ranks' own patches instead
+// (greedy-l1); neither: exact factors of the local patches.
 void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
-                double omega, cudaStream_t s);
+                double omega, cudaStream_t s, const BuildParams* build = nullptr);
+int64_t slab_database_size(const pdb_slab_s& g);
+void slab_phi(const pdb_slab_s& g, int i, int64_t* out);
+void slab_creators(const pdb_slab_s& g, int64_t* out);
 void slab_relax(pdb_slab_s& g, const std::vector<const double*>& b, const std::vector<double*>& x, int64_t sweeps,
                 cudaStream_t s);
 // per local rank i: sizes / lists for the C-ABI getters

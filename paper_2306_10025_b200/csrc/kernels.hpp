@@ -94,6 +94,7 @@ void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, 
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
                    const double* init, const double* omega_w, double* z_out, double* x, cudaStream_t s);
 void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
+void scatter_ints(int64_t count, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s);
 // bad = 1 when some omega_w[i] != omega * (1 / patches covering i) (the padded scatter's weight)
 void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
                        cudaStream_t s);
@@ -208,6 +209,11 @@ void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int be
 // (L1 flavour, reps are patch matrices of creators).  For first-match,
 // phi[pid] = first j with d < eps; best-match tracks (best_d, best_j) over
 // entries with creator < patch.
+// l1_scan with the entries' matrices in their own array (entries + e*len) and
+// creator ids in the numbering pid[t] + id_offset (distributed greedy)
+void l1_scan_entries(int64_t nu, const int32_t* pid, int64_t id_offset, int64_t e0, int64_t e1, int len,
+                     const double* mats, const double* entries, const int32_t* creators, double eps, int best_match,
+                     int32_t* phi, double* best_d, cudaStream_t s);
 void l1_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t e1, int len, const double* mats,
              const int32_t* creators, double eps, int best_match, int32_t* phi, double* best_d, cudaStream_t s);
 // Apply a precomputed distance block d[t*ne + e] (entries e0+e) to the match state.

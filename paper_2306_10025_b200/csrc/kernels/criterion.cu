@@ -98,6 +98,10 @@ struct L1Args {
   int32_t* new_phi;
   double* min_dist;
   int32_t* changed;
+  // scan, best match: creator id of entry e (default rep_src) and the id of
+  // patch row t = pid[t] + id_offset (distributed greedy: global ids)
+  const int32_t* creator;
+  int64_t id_offset;
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
     if (Mode == kL1Scan) {
       cur = a.eps;
       if (a.best_match) {
-        const int32_t me = a.pid[p0 + t];
+        const int32_t me = a.pid[p0 + t];  // phi / best_d are indexed by the row id
         cur = a.best_d[me];
         cur_j = a.phi[me];
       }
@@ -224,10 +228,11 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
             cur_j = (int32_t)(et0 + e);
           }
       } else if (a.best_match) {
-        const int32_t me = pme[t];
+        const int64_t me = pme[t] + a.id_offset;
+        const int32_t* cr = a.creator ? a.creator : a.rep_src;
         for (int e = 0; e < ne; ++e) {
           const int64_t j = et0 + e;
-          if (a.rep_src[j] < me && Dr[e] < cur) {
+          if (cr[j] < me && Dr[e] < cur) {
             cur = Dr[e];
             cur_j = (int32_t)j;
           }
@@ -1272,6 +1277,17 @@ void l1_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t e1, int len, co
   }
   l1_scan_kernel<<<grid_for(nu, kL1Threads), kL1Threads, 0, s>>>(nu, pid, e0, e1, len, mats, creators, eps, best_match,
                                                                  phi, best_d);
+}
+
+void l1_scan_entries(int64_t nu, const int32_t* pid, int64_t id_offset, int64_t e0, int64_t e1, int len,
+                     const double* mats, const double* entries, const int32_t* creators, double eps, int best_match,
+                     int32_t* phi, double* best_d, cudaStream_t s) {
+  if (nu <= 0 || e1 <= e0) return;
+  L1Args a{};
+  a.npat = nu, a.pid = pid, a.len = len, a.mats = mats, a.e0 = e0, a.e1 = e1, a.reps = entries;
+  a.creator = creators, a.id_offset = id_offset;
+  a.eps = eps, a.best_match = best_match, a.phi = phi, a.best_d = best_d;
+  l1_tile_launch<kL1Scan>(a, s);
 }
 
 void apply_scan(int64_t nu, const int32_t* pid, int64_t e0, int64_t ne, const double* d, const int32_t* creators,

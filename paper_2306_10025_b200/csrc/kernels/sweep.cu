@@ -371,6 +371,12 @@ __global__ void check_pad_weights_kernel(int64_t n, double omega, const int32_t*
   if (omega_w[i] != omega * w) atomicOr(bad, 1);
 }
 
+__global__ void scatter_ints_kernel(int64_t count, const int32_t* __restrict__ idx, const int32_t* __restrict__ src,
+                                    int32_t* __restrict__ dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < count) dst[idx[t]] = src[t];
+}
+
 __global__ void gather_vals_kernel(int64_t count, const int32_t* __restrict__ idx, const double* __restrict__ src,
                                    double* __restrict__ dst) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -745,6 +751,10 @@ void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, c
 void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
                        cudaStream_t s) {
   if (n > 0) check_pad_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, inv_ptr, omega_w, bad);
+}
+
+void scatter_ints(int64_t count, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s) {
+  if (count > 0) scatter_ints_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, idx, src, dst);
 }
 
 void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s) {

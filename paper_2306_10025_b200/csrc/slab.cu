@@ -98,6 +98,7 @@ struct SlabRank {
   std::vector<Seg> up_seg, pin_seg, xs_seg, xr_seg;
   DevBuf<double> zup, zin, init, xsend, xrecv, r, sols;
   int64_t n_own = 0;
+  std::vector<int32_t> phi;  // compressed: the rank's slice of phi
   // NCCL mode
   ncclComm_t comm = nullptr;
   cudaStream_t side = nullptr;
@@ -116,6 +117,9 @@ struct pdb_slab_s {
   std::vector<std::unique_ptr<pdb::SlabRank>> ranks;  // 1 (NCCL rank), or the emulated ranks (ascending)
   bool emulated = false;
   int64_t n_global = 0;
+  std::vector<int64_t> k0_of, np_of;  // every rank's first global patch and patch count
+  int64_t m = 0;                       // database entries (compressed)
+  std::vector<int64_t> creators;       // global patch id of each entry (distributed greedy)
   std::vector<int> slot;  // emulated: rank -> index in `ranks`, -1 when absent
   int slot_of(int rank) const { return slot.empty() ? rank : slot[static_cast<size_t>(rank)]; }
 };
@@ -278,8 +282,214 @@ int64_t local_of(const SlabRank& R, int64_t g) {
 }  // namespace
 
 // Collective setup of the ranks in g (each with its slab problem).
+// Distributed greedy-l1 over the ranks' own patches (greedy_impl,
+// compress.cpp:40-95, in the round-batched exact form of database.cu
+// section "Greedy on the GPU").  Global patch order is rank-major, so each
+// round's batch -- the first B unresolved patches -- is the unresolved prefix
+// of rank 0, then of rank 1, ...: the owners contribute those matrices
+// (broadcast), every rank computes the same batch distances and the same
+// sequential resolution, keeps the new entries' matrices (the small
+// replicated set), and scans only its OWN remaining patches against them.
+// The decisions are those of the single-GPU build, hence the reference's.
+void slab_greedy(pdb_slab_s& g, int64_t patch_size, const BuildParams& bp, pdb_database_s& out, cudaStream_t s) {
+  require(bp.method == PDB_METHOD_GREEDY_L1, Errc::invalid_argument,
+          "rank-local database build: greedy-l1 only (other methods need the whole patch set)");
+  require(bp.eps > 0.0, Errc::invalid_argument, "tolerance must be positive");
+  const int L = static_cast<int>(g.ranks.size());
+  const int W = g.ranks[0]->nranks;
+  const int ps = static_cast<int>(patch_size);
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  const int64_t Bmax = 1024;
+  const bool best = bp.best_match;
+  // per local rank: patch matrices, unresolved list, phi / best distances
+  std::vector<DevBuf<double>> mats(static_cast<size_t>(L));
+  std::vector<std::vector<int32_t>> U(static_cast<size_t>(L));
+  std::vector<DevBuf<int32_t>> phi(static_cast<size_t>(L));
+  std::vector<DevBuf<double>> bd(static_cast<size_t>(L));
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    extract_patches(R.a, R.ps, mats[static_cast<size_t>(i)], s);
+    U[static_cast<size_t>(i)].resize(static_cast<size_t>(R.np));
+    for (int64_t k = 0; k < R.np; ++k) U[static_cast<size_t>(i)][static_cast<size_t>(k)] = static_cast<int32_t>(k);
+    phi[static_cast<size_t>(i)].alloc(static_cast<size_t>(std::max<int64_t>(R.np, 1)));
+    PDB_CUDA(cudaMemsetAsync(phi[static_cast<size_t>(i)].get(), 0xff, R.np * sizeof(int32_t), s));
+    if (best) {
+      std::vector<double> init(static_cast<size_t>(std::max<int64_t>(R.np, 1)), bp.eps);
+      put(bd[static_cast<size_t>(i)], init, s);
+    }
+  }
+  DevBuf<double> batch(static_cast<size_t>(Bmax * len)), D(static_cast<size_t>(Bmax * Bmax));
+  DevBuf<int32_t> S(static_cast<size_t>(Bmax)), phib(static_cast<size_t>(Bmax)), entry_of(static_cast<size_t>(Bmax));
+  DevBuf<int64_t> state(3);
+  k::iota(Bmax, S.get(), s);
+  int64_t cap = 1024, m = 0;
+  DevBuf<double> entries(static_cast<size_t>(cap * len));
+  DevBuf<int32_t> cre_b(static_cast<size_t>(cap)), cre_g(static_cast<size_t>(cap));
+  g.creators.clear();
+  auto grow = [&](int64_t need) {
+    if (need <= cap) return;
+    int64_t nc = cap;
+    while (nc < need) nc *= 2;
+    DevBuf<double> e2(static_cast<size_t>(nc * len));
+    DevBuf<int32_t> b2(static_cast<size_t>(nc)), g2(static_cast<size_t>(nc));
+    if (m > 0) {
+      PDB_CUDA(cudaMemcpyAsync(e2.get(), entries.get(), m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      PDB_CUDA(cudaMemcpyAsync(g2.get(), cre_g.get(), m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    entries = std::move(e2);
+    cre_b = std::move(b2);
+    cre_g = std::move(g2);
+    cap = nc;
+  };
+  std::vector<Mail> outm(static_cast<size_t>(L), Mail(static_cast<size_t>(W))), inm;
+  for (;;) {
+    // unresolved counts of every rank
+    std::vector<int64_t> cnt(static_cast<size_t>(W), 0);
+    for (int i = 0; i < L; ++i)
+      for (int q = 0; q < W; ++q) outm[static_cast<size_t>(i)][static_cast<size_t>(q)] = {static_cast<int64_t>(U[static_cast<size_t>(i)].size())};
+    deliver(g, outm, inm, s);
+    for (int q = 0; q < W; ++q)
+      if (!inm[0][static_cast<size_t>(q)].empty()) cnt[static_cast<size_t>(q)] = inm[0][static_cast<size_t>(q)][0];
+    int64_t total = 0;
+    for (int64_t c : cnt) total += c;
+    if (total == 0) break;
+    const int64_t B = std::min(total, Bmax);
+    std::vector<int64_t> take(static_cast<size_t>(W)), off(static_cast<size_t>(W) + 1, 0);
+    for (int q = 0; q < W; ++q) {
+      take[static_cast<size_t>(q)] = std::min(cnt[static_cast<size_t>(q)], B - off[static_cast<size_t>(q)]);
+      off[static_cast<size_t>(q) + 1] = off[static_cast<size_t>(q)] + take[static_cast<size_t>(q)];
+    }
+    // the owners' batch matrices and the batch's global ids
+    std::vector<int32_t> Sg(static_cast<size_t>(B));
+    for (int i = 0; i < L; ++i) {
+      const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+      const int64_t t = take[static_cast<size_t>(R.rank)];
+      if (t == 0) continue;
+      std::vector<int32_t> ids(U[static_cast<size_t>(i)].begin(), U[static_cast<size_t>(i)].begin() + t);
+      DevBuf<int32_t> d_ids;
+      put(d_ids, ids, s);
+      k::gather_mats(t, d_ids.get(), len, mats[static_cast<size_t>(i)].get(), batch.get() + off[static_cast<size_t>(R.rank)] * len, s);
+      sync(s);
+    }
+    if (!g.emulated && W > 1) {
+      SlabRank& R = *g.ranks[0];
+      PDB_NCCL_S(ncclGroupStart());
+      for (int q = 0; q < W; ++q)
+        if (take[static_cast<size_t>(q)] > 0)
+          PDB_NCCL_S(ncclBroadcast(batch.get() + off[static_cast<size_t>(q)] * len, batch.get() + off[static_cast<size_t>(q)] * len,
+                                   static_cast<size_t>(take[static_cast<size_t>(q)] * len), ncclDouble, q, R.comm, s));
+      PDB_NCCL_S(ncclGroupEnd());
+    }
+    // global ids: every rank's unresolved prefix (ids exchanged with the counts' partners)
+    for (int i = 0; i < L; ++i) {
+      const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+      std::vector<int64_t> mine;
+      for (int64_t j = 0; j < take[static_cast<size_t>(R.rank)]; ++j)
+        mine.push_back(g.k0_of[static_cast<size_t>(R.rank)] + U[static_cast<size_t>(i)][static_cast<size_t>(j)]);
+      for (int q = 0; q < W; ++q) outm[static_cast<size_t>(i)][static_cast<size_t>(q)] = mine;
+    }
+    deliver(g, outm, inm, s);
+    for (int q = 0; q < W; ++q)
+      for (int64_t j = 0; j < take[static_cast<size_t>(q)]; ++j)
+        Sg[static_cast<size_t>(off[static_cast<size_t>(q)] + j)] = static_cast<int32_t>(inm[0][static_cast<size_t>(q)][static_cast<size_t>(j)]);
+    // batch distances and the sequential resolution (replicated)
+    k::l1_pairs(B, nullptr, B, static_cast<int>(len), batch.get(), nullptr, batch.get(), D.get(), s);
+    PDB_CUDA(cudaMemsetAsync(entry_of.get(), 0xff, B * sizeof(int32_t), s));
+    PDB_CUDA(cudaMemsetAsync(phib.get(), 0xff, B * sizeof(int32_t), s));
+    grow(m + B);
+    std::vector<int64_t> st = {m, 0, -1};
+    PDB_CUDA(cudaMemcpyAsync(state.get(), st.data(), 3 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    k::greedy_resolve(static_cast<int>(B), S.get(), D.get(), bp.eps, best ? 1 : 0, -1, nullptr, phib.get(),
+                      cre_b.get(), entry_of.get(), state.get(), s);
+    PDB_LAUNCH_CHECK();
+    PDB_CUDA(cudaMemcpyAsync(st.data(), state.get(), 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    const int64_t m_new = st[0];
+    // new entries: matrices and global creator ids
+    if (m_new > m) {
+      k::gather_mats(m_new - m, cre_b.get() + m, len, batch.get(), entries.get() + m * len, s);
+      const std::vector<int32_t> cb = cre_b.to_host(s);
+      std::vector<int32_t> cg(static_cast<size_t>(m_new - m));
+      for (int64_t e = m; e < m_new; ++e) {
+        cg[static_cast<size_t>(e - m)] = Sg[static_cast<size_t>(cb[static_cast<size_t>(e)])];
+        g.creators.push_back(cg[static_cast<size_t>(e - m)]);
+      }
+      PDB_CUDA(cudaMemcpyAsync(cre_g.get() + m, cg.data(), cg.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    }
+    const std::vector<int32_t> pb = phib.to_host(s);
+    // owners record their batch members' phi; scan their other patches against the new entries
+    for (int i = 0; i < L; ++i) {
+      SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+      auto& Ui = U[static_cast<size_t>(i)];
+      const int64_t t = take[static_cast<size_t>(R.rank)], o = off[static_cast<size_t>(R.rank)];
+      if (t > 0) {
+        std::vector<int32_t> vals(pb.begin() + o, pb.begin() + o + t);
+        std::vector<int32_t> ids(Ui.begin(), Ui.begin() + t);
+        DevBuf<int32_t> d_ids, d_vals;
+        put(d_ids, ids, s);
+        put(d_vals, vals, s);
+        k::scatter_ints(t, d_ids.get(), d_vals.get(), phi[static_cast<size_t>(i)].get(), s);
+      }
+      if (m_new > m) {
+        std::vector<int32_t> rest;
+        if (best) {  // every patch after the batch start except the batch itself (database.cu best match)
+          const int64_t first = Sg[0];
+          std::vector<char> inb(static_cast<size_t>(std::max<int64_t>(R.np, 1)), 0);
+          for (int64_t j = 0; j < t; ++j) inb[static_cast<size_t>(Ui[static_cast<size_t>(j)])] = 1;
+          for (int64_t k = 0; k < R.np; ++k)
+            if (g.k0_of[static_cast<size_t>(R.rank)] + k > first && !inb[static_cast<size_t>(k)]) rest.push_back(static_cast<int32_t>(k));
+        } else {
+          rest.assign(Ui.begin() + t, Ui.end());
+        }
+        if (!rest.empty()) {
+          DevBuf<int32_t> d_rest;
+          put(d_rest, rest, s);
+          k::l1_scan_entries(static_cast<int64_t>(rest.size()), d_rest.get(), g.k0_of[static_cast<size_t>(R.rank)], m,
+                             m_new, static_cast<int>(len), mats[static_cast<size_t>(i)].get(), entries.get(),
+                             cre_g.get(), bp.eps, best ? 1 : 0, phi[static_cast<size_t>(i)].get(),
+                             best ? bd[static_cast<size_t>(i)].get() : nullptr, s);
+          PDB_LAUNCH_CHECK();
+        }
+      }
+      // unresolved: the unmatched among the rank's remaining patches
+      const std::vector<int32_t> ph = phi[static_cast<size_t>(i)].to_host(s);
+      std::vector<int32_t> keep;
+      for (size_t j = static_cast<size_t>(t); j < Ui.size(); ++j)
+        if (ph[static_cast<size_t>(Ui[j])] < 0) keep.push_back(Ui[j]);
+      Ui.swap(keep);
+    }
+    m = m_new;
+  }
+  // factors of the entries (replicated; the reference factors each new entry, compress.cpp:91)
+  out.m = m;
+  out.ps = ps;
+  out.np = 0;
+  for (int64_t c : g.np_of) out.np += c;
+  out.method = "greedy-l1";
+  out.eps = bp.eps;
+  out.lu.alloc(static_cast<size_t>(std::max<int64_t>(m, 1) * len));
+  out.piv.alloc(static_cast<size_t>(std::max<int64_t>(m, 1) * ps));
+  DevBuf<int32_t> status(static_cast<size_t>(std::max<int64_t>(m, 1)));
+  DevBuf<double> bst(static_cast<size_t>(std::max<int64_t>(m, 1)));
+  k::lu_batched(m, ps, entries.get(), nullptr, out.lu.get(), out.piv.get(), status.get(), bst.get(), s);
+  PDB_LAUNCH_CHECK();
+  const std::vector<int32_t> sth = status.to_host(s);
+  for (int64_t e = 0; e < m; ++e)
+    if (sth[static_cast<size_t>(e)] != 0) {
+      const std::vector<double> bh = bst.to_host(s);
+      fail(Errc::singular_matrix, "patch " + std::to_string(g.creators[static_cast<size_t>(e)]) + ": " +
+                                      singular_msg(sth[static_cast<size_t>(e)], bh[static_cast<size_t>(e)]));
+    }
+  out.reps = std::move(entries);
+  g.m = m;
+  for (int i = 0; i < L; ++i) g.ranks[static_cast<size_t>(i)]->phi = phi[static_cast<size_t>(i)].to_host(s);
+  sync(s);
+}
+
+
+
 void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
-                double omega, cudaStream_t s) {
+                double omega, cudaStream_t s, const BuildParams* build) {
   require_device();
   const int L = static_cast<int>(g.ranks.size());
   const int W = g.ranks[0]->nranks;
@@ -313,6 +523,12 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
   }
   int64_t np_total = 0;
   for (int q = 0; q < W; ++q) np_total += info[0][static_cast<size_t>(3 * q)];
+  g.k0_of.assign(static_cast<size_t>(W), 0);
+  g.np_of.assign(static_cast<size_t>(W), 0);
+  for (int q = 0; q < W; ++q) {
+    g.np_of[static_cast<size_t>(q)] = info[0][static_cast<size_t>(3 * q)];
+    if (q > 0) g.k0_of[static_cast<size_t>(q)] = g.k0_of[static_cast<size_t>(q) - 1] + g.np_of[static_cast<size_t>(q) - 1];
+  }
   // (2) touched DoFs (with counts) to every rank whose touched range overlaps
   for (int i = 0; i < L; ++i) {
     const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
@@ -483,12 +699,35 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     R.xrecv.alloc(std::max<size_t>(xr_l.size(), 1));
   }
   // (5) factors and the DoF -> slot map
+  pdb_database_s built;  // distributed greedy: replicated entries, per-rank phi in R.phi
+  if (!db && build) {
+    slab_greedy(g, patch_size, *build, built, s);
+    db = &built;
+  }
   for (int i = 0; i < L; ++i) {
     SlabRank& R = *g.ranks[static_cast<size_t>(i)];
     pdb_patchset_s lo, hi;
     sub_patchset(R.ps, 0, R.kb, lo, s);
     sub_patchset(R.ps, R.kb, R.np, hi, s);
-    if (db) {
+    if (db == &built) {
+      auto part = [&](pdb_patchset_s& sp, int64_t off, pdb_precond_s& pc) {
+        if (sp.np == 0) return;
+        pdb_database_s ldb;
+        ldb.m = built.m;
+        ldb.np = sp.np;
+        ldb.ps = built.ps;
+        const size_t len = static_cast<size_t>(built.ps * built.ps);
+        ldb.lu.alloc(built.m * len);
+        PDB_CUDA(cudaMemcpyAsync(ldb.lu.get(), built.lu.get(), built.m * len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        ldb.piv.alloc(static_cast<size_t>(built.m * built.ps));
+        PDB_CUDA(cudaMemcpyAsync(ldb.piv.get(), built.piv.get(), built.m * built.ps * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        std::vector<int32_t> ph(R.phi.begin() + off, R.phi.begin() + off + sp.np);
+        put(ldb.phi, ph, s);
+        precond_compressed_shard(sp, ldb, omega, pc, s);
+      };
+      part(lo, 0, R.pc_lo);
+      part(hi, R.kb, R.pc_hi);
+    } else if (db) {
       require(db->np == np_total, Errc::dimension_mismatch, "database does not cover the global patch set");
       require(db->ps == patch_size, Errc::dimension_mismatch, "database entry dimension does not match the patch size");
       auto part = [&](pdb_patchset_s& sp, int64_t off, pdb_precond_s& pc) {
@@ -736,5 +975,15 @@ void slab_owned(const pdb_slab_s& g, int i, int64_t* out) {
   std::sort(o.begin(), o.end());
   std::copy(o.begin(), o.end(), out);
 }
+
+int64_t slab_database_size(const pdb_slab_s& g) { return g.m; }
+
+void slab_phi(const pdb_slab_s& g, int i, int64_t* out) {
+  const SlabRank& R = slab_rank(g, i);
+  require(!R.phi.empty() || R.np == 0, Errc::invalid_argument, "slab has no rank-local database");
+  for (int64_t k = 0; k < R.np; ++k) out[k] = R.phi[static_cast<size_t>(k)];
+}
+
+void slab_creators(const pdb_slab_s& g, int64_t* out) { std::copy(g.creators.begin(), g.creators.end(), out); }
 
 }  // namespace pdb

@@ -748,6 +748,11 @@ _sig("pdb_slab_local_dofs", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_owned", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_relax_device", C.c_int, _P, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int64, C.c_void_p)
 _sig("pdb_slab_free", None, _P)
+_sig("pdb_slab_create_built", C.c_int, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int64, C.POINTER(CompressOptions),
+     C.c_double, C.c_char_p, C.POINTER(_P))
+_sig("pdb_slab_database_size", C.c_int64, _P)
+_sig("pdb_slab_phi", C.c_int, _P, C.c_int, _I64)
+_sig("pdb_slab_creators", C.c_int, _P, _I64)
 _sig("pdb_slab_create_subset", C.c_int, C.POINTER(_P), C.c_int, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int64, _P,
      C.c_double, C.c_char_p, C.POINTER(_P))
 _sig("pdb_slab_relax_rank_device", C.c_int, _P, C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
@@ -773,6 +778,33 @@ class Slab(_Handle):
         h = cls(out)
         h._keep = list(slabs)
         return h
+
+    @classmethod
+    def create_built(cls, slabs, rank: int, nranks: int, patch_size: int, method: int = 2, eps: float = 1e-7,
+                     best_match: bool = False, omega: float = 1.0, nccl_id: Optional[bytes] = None) -> "Slab":
+        """Compressed database built from the ranks' own patches (pdb_slab_create_built)."""
+        arr = (C.c_void_p * len(slabs))(*[p.ptr for p in slabs])
+        o = compress_options(method, eps=eps, best_match=int(best_match))
+        out = C.c_void_p()
+        _check(_lib.pdb_slab_create_built(arr, len(slabs), rank, nranks, patch_size, C.byref(o), omega, nccl_id,
+                                          C.byref(out)))
+        h = cls(out)
+        h._keep = list(slabs)
+        return h
+
+    @property
+    def database_size(self) -> int:
+        return _lib.pdb_slab_database_size(self._ptr)
+
+    def phi(self, i: int = 0) -> np.ndarray:
+        out = np.empty(self.info(i)["n_patches"], np.int64)
+        _check(_lib.pdb_slab_phi(self._ptr, i, _ip(out)))
+        return out
+
+    def creators(self) -> np.ndarray:
+        out = np.empty(self.database_size, np.int64)
+        _check(_lib.pdb_slab_creators(self._ptr, _ip(out)))
+        return out
 
     @classmethod
     def create_subset(cls, slabs, ranks, rank: int, nranks: int, patch_size: int, omega: float = 1.0) -> "Slab":

@@ -114,3 +114,31 @@ def test_subset_group_one_rank_slice(P, cfg, cells, ps, ranks, r):
     # the rank-alone timing path runs (values not a sweep: exchanges skipped)
     sl.relax_rank_device(1, bl.data_ptr(), xl.data_ptr(), 2)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("cfg,cells,ps,ranks,eps,best", [(3, 0, 27, 3, 0.13699942677165544, False),
+                                                          (3, 0, 27, 8, 0.13699942677165544, False),
+                                                          (1, 0, 9, 2, 2.0, False), (1, 0, 9, 4, 2.0, True),
+                                                          (2, 16, 25, 2, 0.5, True), (3, 8, 27, 4, 0.3, False)])
+def test_rank_local_greedy_equals_single_gpu(P, cfg, cells, ps, ranks, eps, best):
+    """pdb_slab_create_built: the greedy-l1 database built from the ranks' own
+    patches (batches broadcast by their owners, each rank scanning only its
+    patches) is bitwise the single-GPU build -- size, creators, phi -- and the
+    sweeps with it are bitwise pdb_relax's."""
+    g = P.Problem.generate(cfg, cells)
+    A = g.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    db = P.Database.build(A, pset, P.GREEDY_L1, eps=eps, best_match=int(best))
+    slabs = [P.Problem.generate_slab(cfg, cells, r, ranks) for r in range(ranks)]
+    sl = P.Slab.create_built(slabs, 0, ranks, ps, P.GREEDY_L1, eps=eps, best_match=best, omega=0.9)
+    assert sl.database_size == db.size
+    phi = db.phi()
+    assert np.array_equal(np.concatenate([sl.phi(i) for i in range(ranks)]), phi)
+    _, first = np.unique(phi, return_index=True)
+    assert np.array_equal(sl.creators(), first[np.argsort(phi[first])])
+    pc = P.Preconditioner.create(A, pset, db, omega=0.9)
+    b = g.rhs()
+    x0 = np.zeros_like(b)
+    want, _ = pc.relax(A, b, x0, 3, history=False)
+    got, _ = emulated_relax(P, sl, b, x0, 3)
+    assert np.array_equal(got, want)
