@@ -278,6 +278,198 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked right-looking LU, CTA per matrix (default for ps > kSmemMaxPs).
+// The matrix is factored in a per-CTA scratch copy (L2-resident) with its
+// rows addressed through a row map: a row swap exchanges two map entries
+// (and the two rows of the shared-memory panel), never moves data in global
+// memory; the factor is written out in the pivoted order at the end.  Panels
+// of kNb columns: (1) the panel (rows k0.., nb columns) is factored in
+// shared memory with partial pivoting; (2) U12 by forward substitution with
+// the unit L11, thread per column, rows in order; (3) the trailing block
+// A22 -= L21 U12 with each element held in a register through its nb
+// updates (warp per row, a lane holding kCols columns so the dependent
+// mul/sub chains interleave).  Every element still sees
+// a_ij <- a_ij - l_ik u_kj for k = 0, 1, ... in order, unfused, skipped where
+// l_ik == 0, and the pivot of column k is chosen after all updates 0..k-1 --
+// the unblocked algorithm's per-element sequence (dense.cpp:31-75), so
+// factors and pivots are bitwise identical (tests/test_lu_large.py).
+constexpr int kNb = 16;
+constexpr int kCols = 6;  // trailing-update columns per lane (6 x 32 >= 192 - 16)
+constexpr int kBlkThreads = 256;
+constexpr int kBlkWarps = kBlkThreads / 32;
+
+inline size_t blk_smem_bytes(int ps) {
+  // panel [ps][kNb+1], U12 [kNb][ps], colmax [ps], perm [ps] (int), row map [ps] (int)
+  return ((size_t)ps * (kNb + 1) + (size_t)kNb * ps + ps) * sizeof(double) + 2 * (size_t)ps * sizeof(int32_t);
+}
+
+__global__ void __launch_bounds__(kBlkThreads)
+    lu_blocked_kernel(int64_t count, int ps, const double* __restrict__ mats, const int32_t* __restrict__ src,
+                      double* __restrict__ lu, int32_t* __restrict__ piv, int32_t* __restrict__ status,
+                      double* __restrict__ fail_best, double* __restrict__ scratch) {
+  extern __shared__ double smem[];
+  constexpr int LP = kNb + 1;
+  double* Pn = smem;                       // panel rows [ps][LP] (row r = logical row k0 + r)
+  double* Us = Pn + (size_t)ps * LP;       // U12 [kNb][ps]
+  double* colmax = Us + (size_t)kNb * ps;  // [ps]
+  int32_t* perm = reinterpret_cast<int32_t*>(colmax + ps);
+  int32_t* rmap = perm + ps;  // logical row -> row of the scratch copy
+  __shared__ double s_best;
+  __shared__ int s_p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t len = (int64_t)ps * ps;
+  double* S = scratch + (int64_t)blockIdx.x * len;
+  for (int64_t t = blockIdx.x; t < count; t += gridDim.x) {
+    const double* A = mats + (src ? (int64_t)src[t] : t) * len;
+    for (int64_t e = threadIdx.x; e < len; e += kBlkThreads) S[e] = A[e];
+    for (int j = threadIdx.x; j < ps; j += kBlkThreads) {  // column maxima, 8 loads in flight
+      double m = 0.0;
+      for (int i0 = 0; i0 < ps; i0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = i0 + u < ps ? A[(int64_t)(i0 + u) * ps + j] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) m = fmax(m, fabs(v[u]));
+      }
+      colmax[j] = m;
+      perm[j] = j;
+      rmap[j] = j;
+    }
+    __syncthreads();
+    bool failed = false;
+    for (int k0 = 0; k0 < ps && !failed; k0 += kNb) {
+      const int nb = min(kNb, ps - k0), nr = ps - k0;
+      // (1) panel into shared memory (logical row order) and its factorisation
+      for (int e = threadIdx.x; e < nr * nb; e += kBlkThreads) {
+        const int r = e / nb, c = e - r * nb;
+        Pn[r * LP + c] = S[(int64_t)rmap[k0 + r] * ps + k0 + c];
+      }
+      __syncthreads();
+      for (int kk = 0; kk < nb; ++kk) {
+        const int k = k0 + kk;
+        if (warp == 0) {
+          double best = -1.0;
+          int p = ps;
+          for (int r = kk + lane; r < nr; r += 32) {
+            const double v = fabs(Pn[r * LP + kk]);
+            if (v > best) {
+              best = v;
+              p = k0 + r;
+            }
+          }
+          warp_pivot(best, p);  // every lane holds the result
+          const bool ok = !(best == 0.0 || best < __dmul_rn(1e-14, colmax[k]));
+          if (lane == 0) {
+            s_best = best;
+            s_p = p;
+            if (ok && p != k) {  // full row swap (dense.cpp:62-65): the map, the permutation
+              int32_t x = perm[k];
+              perm[k] = perm[p];
+              perm[p] = x;
+              x = rmap[k];
+              rmap[k] = rmap[p];
+              rmap[p] = x;
+            }
+          }
+          if (ok && p != k && lane < nb) {  // and the two panel rows (lanes over the nb columns)
+            const double x = Pn[kk * LP + lane];
+            Pn[kk * LP + lane] = Pn[(p - k0) * LP + lane];
+            Pn[(p - k0) * LP + lane] = x;
+          }
+        }
+        __syncthreads();
+        const double best = s_best;
+        if (best == 0.0 || best < __dmul_rn(1e-14, colmax[k])) {
+          if (threadIdx.x == 0) {
+            status[t] = k + 1;
+            fail_best[t] = best;
+          }
+          failed = true;
+          break;
+        }
+        const double pv = Pn[kk * LP + kk];
+        for (int r = kk + 1 + threadIdx.x; r < nr; r += kBlkThreads) Pn[r * LP + kk] = __ddiv_rn(Pn[r * LP + kk], pv);
+        __syncthreads();
+        const int w = nb - kk - 1;  // panel columns right of kk
+        if (w > 0)
+          for (int e = threadIdx.x; e < (nr - kk - 1) * w; e += kBlkThreads) {
+            const int r = kk + 1 + e / w, c = kk + 1 + e % w;
+            const double l = Pn[r * LP + kk];
+            if (l != 0.0) Pn[r * LP + c] = __dsub_rn(Pn[r * LP + c], __dmul_rn(l, Pn[kk * LP + c]));
+          }
+        __syncthreads();
+      }
+      if (failed) break;
+      for (int e = threadIdx.x; e < nr * nb; e += kBlkThreads) {  // panel back (logical rows via the map)
+        const int r = e / nb, c = e - r * nb;
+        S[(int64_t)rmap[k0 + r] * ps + k0 + c] = Pn[r * LP + c];
+      }
+      const int j0 = k0 + nb, nc = ps - j0;
+      if (nc <= 0) {
+        __syncthreads();
+        break;
+      }
+      // (2) U12 = L11^{-1} A12, thread per column, rows in order
+      for (int j = threadIdx.x; j < nc; j += kBlkThreads) {
+        double u[kNb];
+#pragma unroll
+        for (int kk = 0; kk < kNb; ++kk) {
+          if (kk >= nb) break;
+          double* sp = S + (int64_t)rmap[k0 + kk] * ps + j0 + j;
+          double a = *sp;
+#pragma unroll
+          for (int mm = 0; mm < kk; ++mm) {
+            const double l = Pn[kk * LP + mm];
+            if (l != 0.0) a = __dsub_rn(a, __dmul_rn(l, u[mm]));
+          }
+          u[kk] = a;
+          *sp = a;
+          Us[kk * ps + j] = a;
+        }
+      }
+      __syncthreads();
+      // (3) A22 -= L21 U12
+      for (int i = j0 + warp; i < ps; i += kBlkWarps) {
+        const double* Li = Pn + (i - k0) * LP;
+        double* Wi = S + (int64_t)rmap[i] * ps + j0;
+        for (int jb = 0; jb < nc; jb += 32 * kCols) {
+          double a[kCols];
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            const int j = jb + lane + 32 * c;
+            a[c] = j < nc ? Wi[j] : 0.0;
+          }
+          for (int kk = 0; kk < nb; ++kk) {
+            const double l = Li[kk];
+            if (l == 0.0) continue;  // warp-uniform (dense.cpp:70)
+            const double* Uk = Us + kk * ps + jb + lane;
+#pragma unroll
+            for (int c = 0; c < kCols; ++c)
+              if (jb + lane + 32 * c < nc) a[c] = __dsub_rn(a[c], __dmul_rn(l, Uk[32 * c]));
+          }
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            const int j = jb + lane + 32 * c;
+            if (j < nc) Wi[j] = a[c];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (!failed) {
+      double* W = lu + t * len;
+      for (int64_t e = threadIdx.x; e < len; e += kBlkThreads) {
+        const int i = (int)(e / ps), j = (int)(e - (int64_t)i * ps);
+        W[e] = S[(int64_t)rmap[i] * ps + j];
+      }
+      for (int j = threadIdx.x; j < ps; j += kBlkThreads) piv[t * ps + j] = perm[j];
+      if (threadIdx.x == 0) status[t] = 0;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, double* lu, int32_t* piv,
@@ -288,6 +480,22 @@ void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, d
     const size_t smem = (size_t)kWarps * ((size_t)ps * (ps | 1) + ps) * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(lu_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lu_kernel<true><<<grid, kWarps * 32, smem, s>>>(count, ps, mats, src, lu, piv, status, fail_best);
+  } else if (std::getenv("PDB_LU_WARP") == nullptr && std::getenv("PDB_LU_CTA") == nullptr &&
+             blk_smem_bytes(ps) <= 200 * 1024) {
+    const size_t smem = blk_smem_bytes(ps);
+    static int configured[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (smem > 48 * 1024 && dev < 64 && !configured[dev]) {
+      PDB_CUDA(cudaFuncSetAttribute(lu_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      configured[dev] = 1;
+    }
+    int sms = 148, per = 1;
+    PDB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lu_blocked_kernel, kBlkThreads, smem));
+    const unsigned g = (unsigned)std::min<int64_t>(count, (int64_t)sms * std::max(per, 1));
+    Scratch<double> work(static_cast<size_t>(g) * ps * ps, s);  // one pivoting copy per CTA
+    lu_blocked_kernel<<<g, kBlkThreads, smem, s>>>(count, ps, mats, src, lu, piv, status, fail_best, work.get());
   } else if (cta_smem_bytes(ps, cta_k0(ps)) <= kCtaSmemCap && std::getenv("PDB_LU_WARP") == nullptr) {
     const int k0 = cta_k0(ps);
     const size_t smem = cta_smem_bytes(ps, k0);

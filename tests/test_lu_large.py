@@ -1,6 +1,6 @@
-"""Batched LU of large patches (pytest -m gpu): the CTA-per-matrix kernel
-(ps > 48; global phase for the first k0 steps when the matrix exceeds
-shared memory, k0 = 32 at ps = 192) against the oracle's lu_factor
+"""Batched LU of large patches (pytest -m gpu): the blocked CTA-per-matrix
+kernel (ps > 48, panels of 16 columns) and the unblocked CTA kernel against
+the oracle's lu_factor
 (dense.cpp:31-75), bitwise, on block-diagonal matrices of random dense
 nonsymmetric blocks (every block is one patch, partial pivoting swaps rows
 at almost every step).  Also: the explicit inverses the sweep streams
@@ -47,16 +47,22 @@ def test_large_lu_bitwise(P, orc, ps):
         assert np.array_equal(lu[b].view(np.uint64), lo.view(np.uint64)), b
 
 
-@pytest.mark.parametrize("ps", [64, 192])
-def test_large_lu_matches_warp_kernel(P, monkeypatch, ps):
+@pytest.mark.parametrize("ps", [64, 100, 192])
+def test_large_lu_kernels_agree(P, monkeypatch, ps):
+    """Blocked (default), CTA-unblocked (PDB_LU_CTA) and warp (PDB_LU_WARP)
+    kernels: bitwise the same factors and pivots."""
     blocks = random_blocks(6, ps, 3 * ps)
     A = P.Matrix.from_csr(*block_diag_csr(blocks))
     pset = P.PatchSet.detect(A, ps)
-    lu_cta, piv_cta = P.Database.build(A, pset, P.EXACT).factors()
+    lu_b, piv_b = P.Database.build(A, pset, P.EXACT).factors()
+    monkeypatch.setenv("PDB_LU_CTA", "1")
+    lu_c, piv_c = P.Database.build(A, pset, P.EXACT).factors()
+    monkeypatch.delenv("PDB_LU_CTA")
     monkeypatch.setenv("PDB_LU_WARP", "1")
     lu_w, piv_w = P.Database.build(A, pset, P.EXACT).factors()
-    assert np.array_equal(piv_cta, piv_w)
-    assert np.array_equal(lu_cta.view(np.uint64), lu_w.view(np.uint64))
+    assert np.array_equal(piv_b, piv_w) and np.array_equal(piv_c, piv_w)
+    assert np.array_equal(lu_b.view(np.uint64), lu_w.view(np.uint64))
+    assert np.array_equal(lu_c.view(np.uint64), lu_w.view(np.uint64))
 
 
 @pytest.mark.parametrize("ps", [40, 64, 192])
