@@ -493,10 +493,11 @@ __global__ void invert_factors_kernel(int64_t nf, int ps, const double* __restri
 // rows before the block (the dense part), warp 0 finishes the 8 rows in
 // order.  Not bit-exact with the thread-per-column kernel (the sweep
 // tolerance is 1e-9).
-constexpr int kInvRows = 8;
+constexpr int kInvWarps = 8;
+constexpr int kInvRows = 16;  // rows per block step: two per warp (each loaded X value feeds both)
 constexpr int kInvLd = 33;
 
-__global__ void __launch_bounds__(kInvRows * 32)
+__global__ void __launch_bounds__(kInvWarps * 32)
     invert_block_kernel(int64_t nf, int ps, const double* __restrict__ lu, const int32_t* __restrict__ piv,
                         double* __restrict__ inv) {
   extern __shared__ double X[];  // [ps][kInvLd]
@@ -507,23 +508,30 @@ __global__ void __launch_bounds__(kInvRows * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* L = lu + f * (int64_t)ps * ps;
   const int32_t* P = piv + f * ps;
-  for (int i = warp; i < ps; i += kInvRows) X[i * kInvLd + lane] = P[i] == c0 + lane ? 1.0 : 0.0;
+  for (int i = warp; i < ps; i += kInvWarps) X[i * kInvLd + lane] = P[i] == c0 + lane ? 1.0 : 0.0;
   __syncthreads();
-  // forward: L y = P e_c (unit lower)
+  // forward: L y = P e_c (unit lower); rows b0 + w and b0 + 8 + w per warp
   for (int b0 = 0; b0 < ps; b0 += kInvRows) {
-    const int i = b0 + warp;
-    if (i < ps) {
-      const double* Li = L + (int64_t)i * ps;
-      double s0 = X[i * kInvLd + lane], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int i1 = b0 + warp, i2 = b0 + kInvWarps + warp;
+    if (i1 < ps) {
+      const double* L1 = L + (int64_t)i1 * ps;
+      const double* L2 = L + (int64_t)(i2 < ps ? i2 : i1) * ps;
+      double s1 = X[i1 * kInvLd + lane], s2 = i2 < ps ? X[i2 * kInvLd + lane] : 0.0, t1 = 0.0, t2 = 0.0;
       int j = 0;
-      for (; j + 4 <= b0; j += 4) {
-        s0 -= Li[j] * X[j * kInvLd + lane];
-        s1 -= Li[j + 1] * X[(j + 1) * kInvLd + lane];
-        s2 -= Li[j + 2] * X[(j + 2) * kInvLd + lane];
-        s3 -= Li[j + 3] * X[(j + 3) * kInvLd + lane];
+      for (; j + 2 <= b0; j += 2) {
+        const double x0 = X[j * kInvLd + lane], x1 = X[(j + 1) * kInvLd + lane];
+        s1 -= L1[j] * x0;
+        s2 -= L2[j] * x0;
+        t1 -= L1[j + 1] * x1;
+        t2 -= L2[j + 1] * x1;
       }
-      for (; j < b0; ++j) s0 -= Li[j] * X[j * kInvLd + lane];
-      part[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
+      for (; j < b0; ++j) {
+        const double x0 = X[j * kInvLd + lane];
+        s1 -= L1[j] * x0;
+        s2 -= L2[j] * x0;
+      }
+      part[warp * 32 + lane] = s1 + t1;
+      if (i2 < ps) part[(kInvWarps + warp) * 32 + lane] = s2 + t2;
     }
     __syncthreads();
     if (warp == 0)
@@ -536,22 +544,30 @@ __global__ void __launch_bounds__(kInvRows * 32)
       }
     __syncthreads();
   }
-  // backward: U x = y
-  for (int e0 = ps; e0 > 0; e0 -= kInvRows) {  // rows [max(e0-8,0), e0)
+  // backward: U x = y; rows e0 - 1 - w and e0 - 9 - w per warp
+  for (int e0 = ps; e0 > 0; e0 -= kInvRows) {  // rows [max(e0 - 16, 0), e0)
     const int lo = e0 - kInvRows > 0 ? e0 - kInvRows : 0;
-    const int i = e0 - 1 - warp;
-    if (i >= lo) {
-      const double* Ui = L + (int64_t)i * ps;
-      double s0 = X[i * kInvLd + lane], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const int i1 = e0 - 1 - warp, i2 = e0 - 1 - kInvWarps - warp;
+    if (i1 >= lo) {
+      const bool two = i2 >= lo;
+      const double* U1 = L + (int64_t)i1 * ps;
+      const double* U2 = L + (int64_t)(two ? i2 : i1) * ps;
+      double s1 = X[i1 * kInvLd + lane], s2 = two ? X[i2 * kInvLd + lane] : 0.0, t1 = 0.0, t2 = 0.0;
       int j = e0;
-      for (; j + 4 <= ps; j += 4) {
-        s0 -= Ui[j] * X[j * kInvLd + lane];
-        s1 -= Ui[j + 1] * X[(j + 1) * kInvLd + lane];
-        s2 -= Ui[j + 2] * X[(j + 2) * kInvLd + lane];
-        s3 -= Ui[j + 3] * X[(j + 3) * kInvLd + lane];
+      for (; j + 2 <= ps; j += 2) {
+        const double x0 = X[j * kInvLd + lane], x1 = X[(j + 1) * kInvLd + lane];
+        s1 -= U1[j] * x0;
+        s2 -= U2[j] * x0;
+        t1 -= U1[j + 1] * x1;
+        t2 -= U2[j + 1] * x1;
       }
-      for (; j < ps; ++j) s0 -= Ui[j] * X[j * kInvLd + lane];
-      part[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
+      for (; j < ps; ++j) {
+        const double x0 = X[j * kInvLd + lane];
+        s1 -= U1[j] * x0;
+        s2 -= U2[j] * x0;
+      }
+      part[(e0 - 1 - i1) * 32 + lane] = s1 + t1;
+      if (two) part[(e0 - 1 - i2) * 32 + lane] = s2 + t2;
     }
     __syncthreads();
     if (warp == 0)
@@ -566,7 +582,7 @@ __global__ void __launch_bounds__(kInvRows * 32)
   // column-major output: column c0 + c, rows contiguous
   const int nc = ps - c0 < 32 ? ps - c0 : 32;
   double* out = inv + f * (int64_t)ps * ps + (int64_t)c0 * ps;
-  for (int e = threadIdx.x; e < nc * ps; e += kInvRows * 32) {
+  for (int e = threadIdx.x; e < nc * ps; e += kInvWarps * 32) {
     const int c = e / ps, i = e % ps;
     out[(int64_t)c * ps + i] = X[i * kInvLd + c];
   }
@@ -793,7 +809,7 @@ void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, do
     invert_factors_kernel<<<(unsigned)((nf + 3) / 4), 128, 0, s>>>(nf, ps, lu, piv, inv);
     return;
   }
-  const size_t smem = ((size_t)ps * kInvLd + kInvRows * 32) * sizeof(double);
+  const size_t smem = ((size_t)ps * kInvLd + kInvRows * 32) * sizeof(double);  // rows x 33 + 16 x 32
   if (smem > 48 * 1024) {
     static int configured[64] = {};
     int dev = 0;
@@ -804,7 +820,7 @@ void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, do
     }
   }
   const int64_t blocks = nf * ((ps + 31) / 32);
-  invert_block_kernel<<<(unsigned)blocks, kInvRows * 32, smem, s>>>(nf, ps, lu, piv, inv);
+  invert_block_kernel<<<(unsigned)blocks, kInvWarps * 32, smem, s>>>(nf, ps, lu, piv, inv);
 }
 
 void scatter_update(int64_t n, const int32_t* inv_ptr, const int32_t* inv, const double* sols, const double* omega_w,
