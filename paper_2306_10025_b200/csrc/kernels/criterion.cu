@@ -18,6 +18,7 @@
 
 #include <math_constants.h>
 
+#include "../common.hpp"
 #include "../kernels.hpp"
 
 namespace pdb::k {
@@ -395,22 +396,31 @@ __global__ void apply_scan_kernel(int64_t nu, const int32_t* __restrict__ pid, i
 // exactly the scan of the one-warp kernel below (compress.cpp:63-92).
 constexpr int kResolveMax = 1024;
 
+// phase 1 over the whole GPU: cand[a][w] = bits of b in [32w, 32w+32), b < a, D[a][b] < eps
+__global__ void greedy_cand_bits_kernel(int B, const double* __restrict__ D, double eps, uint32_t* __restrict__ cand) {
+  const int words = (B + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // global warp = (a, w) item
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t item = gw; item < (int64_t)B * words; item += nwarps) {
+    const int a = (int)(item / words), w = (int)(item % words);
+    const int b = w * 32 + lane;
+    const bool c = b < a && D[(int64_t)a * B + b] < eps;
+    const uint32_t bits = __ballot_sync(0xffffffffu, c);
+    if (lane == 0) cand[a * 32 + w] = bits;
+  }
+}
+
 __global__ void __launch_bounds__(1024) greedy_resolve_bits_kernel(
     int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps, int best_match,
     int64_t abort_above, const int32_t* __restrict__ lu_status, int32_t* __restrict__ phi,
-    int32_t* __restrict__ creators, int32_t* __restrict__ entry_of, int64_t* state) {
+    int32_t* __restrict__ creators, int32_t* __restrict__ entry_of, int64_t* state,
+    const uint32_t* __restrict__ cand_g) {
   extern __shared__ uint32_t cand[];  // [B][32]
   __shared__ int32_t ent_s[kResolveMax];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int words = (B + 31) / 32;
-  for (int a = warp; a < B; a += 32) {
-    for (int w = 0; w < words; ++w) {
-      const int b = w * 32 + lane;
-      const bool c = b < a && D[(int64_t)a * B + b] < eps;
-      const uint32_t bits = __ballot_sync(0xffffffffu, c);
-      if (lane == 0) cand[a * 32 + w] = bits;
-    }
-  }
+  for (int e = threadIdx.x; e < B * 32; e += blockDim.x) cand[e] = cand_g[e];
   __syncthreads();
   if (warp != 0) return;
   uint32_t ent = 0;  // word `lane` of the entry bit set
@@ -1257,8 +1267,13 @@ void greedy_resolve(int B, const int32_t* S, const double* D, double eps, int be
     const size_t smem = (size_t)B * 32 * sizeof(uint32_t);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(greedy_resolve_bits_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    uint32_t* cand = nullptr;
+    PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cand), smem, s));
+    PDB_CUDA(cudaMemsetAsync(cand, 0, smem, s));
+    greedy_cand_bits_kernel<<<4 * 148, 256, 0, s>>>(B, D, eps, cand);
     greedy_resolve_bits_kernel<<<1, 1024, smem, s>>>(B, S, D, eps, best_match, abort_above, lu_status, phi, creators,
-                                                     entry_of, state);
+                                                     entry_of, state, cand);
+    PDB_CUDA(cudaFreeAsync(cand, s));
     return;
   }
   greedy_resolve_kernel<<<1, 32, 0, s>>>(B, S, D, eps, best_match, abort_above, lu_status, phi, creators, entry_of,
