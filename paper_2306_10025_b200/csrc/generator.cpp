@@ -19,6 +19,7 @@
 // share no DoF), so the accumulated values do not depend on thread count.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <random>
 #include <thread>
 
@@ -26,6 +27,8 @@
 #include "host.hpp"
 
 namespace pdb {
+
+ElasticHook g_elastic_device_hook = nullptr;
 
 namespace {
 
@@ -602,7 +605,17 @@ void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWind
     }
   }
 
-  const int ncolors = 1 << d;
+  bool on_device = false;
+  if (!stokes && g_elastic_device_hook != nullptr) {
+    const char* ge = getenv("PDB_GEN_DEVICE");
+    if (!(ge && ge[0] == '0')) {
+      ElasticAssembly ea{d, p, ncomp, nloc, nq, ncorner, C, nva, npa, X.data(), coef.data(), gref.data(),
+                         cgrad.data(), qw.data(), lam_f, mu_f, Wn.cell_lo, Wn.cell_hi, Wn.ranges,
+                         A.row_ptr.data(), A.val.data(), nnz};
+      on_device = g_elastic_device_hook(ea);
+    }
+  }
+  const int ncolors = on_device ? 0 : 1 << d;
   for (int color = 0; color < ncolors; ++color) {
     const int px = color & 1, py = (color >> 1) & 1, pz = (color >> 2) & 1;
     const Index cxn = (C - px + 1) / 2, cyn = (C - py + 1) / 2, czn = d == 3 ? (C - pz + 1) / 2 : 1;

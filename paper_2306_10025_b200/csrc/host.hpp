@@ -60,6 +60,26 @@ struct RowWindow {
 void generate_scalar(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win = nullptr);
 // physics 1 (Stokes Q_p-Q_{p-1}, 2D) and 2 (linear elasticity): node-major vector DoFs
 void generate_system(const pdb_gen_options& o, pdb_problem_s& out, const RowWindow* win = nullptr);
+// Device assembly of the elasticity element matrices (generator_dev.cu).  The
+// generator (host C++, also built into the CUDA-free libpdbgen.so) calls it
+// through this hook, which libpatchdb sets when it loads; it returns false
+// (host assembly) when no device is usable.  Same per-entry operation order
+// as the host loop (colour by colour, cells of a colour sharing no DoF, the
+// element sums over quadrature points in order, no FMA): bitwise equal.
+struct ElasticAssembly {
+  int d, p, ncomp, nloc, nq, ncorner;
+  Index C, nva, npa;
+  const double *X, *coef, *gref, *cgrad, *qw;  // host tables
+  double lam_f, mu_f;
+  Index cell_lo, cell_hi;                       // slowest-axis cells touching the rows
+  std::vector<std::pair<Index, Index>> ranges;  // global row ranges held (local = concatenation)
+  const int64_t* row_ptr;                       // host, local rows + 1
+  double* val;                                  // host, filled (nnz)
+  Index nnz;
+};
+using ElasticHook = bool (*)(const ElasticAssembly&);
+extern ElasticHook g_elastic_device_hook;
+
 // Slab of rank r of W along the slowest axis: cells [C r / W, C (r+1) / W);
 // the rows are every DoF of those cells (both faces included).
 RowWindow slab_window(const pdb_gen_options& o, int rank, int nranks);
