@@ -15,6 +15,8 @@ tests/test_fullsize_pins.py compare the GPU path with:
                       (precond.cpp:90-101) from x = 0 with omega 1 and the
                       residual history ||b - A x_k||_2, k = 0..10.
   c3_exact.npz        the same 10 sweeps with PatchPreconditioner::exact.
+  c2_pcg_exact.npz    config 2, exact patch preconditioner: the oracle's PCG
+                      restatement to 1e-8, iteration count and history.
   c2_kmeans.npz       config 2 at 256^2 (65,536 x 25-DoF patches):
                       KMEANS_SPECTRAL through the reference's
                       partitioned_build (capi.cpp:268-271), k = 64, seed 42,
@@ -26,6 +28,7 @@ tests/test_fullsize_pins.py compare the GPU path with:
     python tests/golden/make_fullsize.py c3 1      # one band per process
     python tests/golden/make_fullsize.py c3exact
     python tests/golden/make_fullsize.py c2 [threads]
+    python tests/golden/make_fullsize.py c2pcg     # exact patches, PCG only
 """
 import hashlib
 import os
@@ -147,6 +150,29 @@ def job_c2(threads: int):
     log("c2: wrote")
 
 
+def job_c2pcg_exact():
+    """Config 2, exact patch preconditioner (one LU per patch, the reference's
+    exact_database), the oracle's PCG restatement to 1e-8 from x = 0."""
+    prob = P.Problem.generate(2, 0)
+    csr = prob.csr()
+    b = prob.rhs()
+    ref = O.RefLib()
+    rm = ref.matrix(csr)
+    rps = rm.detect(25)
+    db = rps.build(rm, 0, threads=4)  # PDB_METHOD_EXACT
+    lu, piv = db.factors(25)
+    orc = O.Oracle()
+    t0 = time.time()
+    _, rep = orc.pcg(csr, b, dict(patches=rps.patches(), weights=rps.weights(prob.ndofs), omega=1.0, lu=lu, piv=piv,
+                                  phi=None), tol=1e-8, max_iters=20000)
+    tp = time.time() - t0
+    log(f"c2 exact pcg: {rep['iterations']} iterations converged={rep['converged']} in {tp:.0f} s")
+    np.savez_compressed(os.path.join(HERE, "c2_pcg_exact.npz"), csr_sha256=np.array(csr_digest(csr)),
+                        rhs_sha256=np.array(sha(b)), pcg_iterations=np.array(rep["iterations"]),
+                        pcg_converged=np.array(rep["converged"]), pcg_history=rep["residual_history"],
+                        pcg_seconds=np.array(tp))
+
+
 if __name__ == "__main__":
     job = sys.argv[1]
     if job == "c3":
@@ -155,5 +181,7 @@ if __name__ == "__main__":
         job_c3exact()
     elif job == "c2":
         job_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
+    elif job == "c2pcg":
+        job_c2pcg_exact()
     else:
         raise SystemExit(__doc__)

@@ -129,3 +129,20 @@ def test_config2_spectral_kmeans_matches_reference(c2, P):
     h, ho = np.asarray(rep.residual_history), g["pcg_history"]
     k = min(len(h), len(ho), 200)
     np.testing.assert_allclose(h[:k], ho[:k], rtol=1e-9, atol=0)
+
+
+def test_config2_pcg_exact_iterations_match_oracle(c2, P):
+    """CG preconditioned by the exact patch relaxation (symmetric weighting,
+    DESIGN.md section 9) to 1e-8 at full config-2 size: the iteration count of
+    the oracle's PCG restatement run on the reference's own factors, exactly;
+    the residual history within 1e-9 over its first 200 iterations."""
+    prob, A, ps = c2
+    g = fixture("c2_pcg_exact.npz")
+    check_inputs(prob, g)
+    pc = P.Preconditioner.create(A, ps, None, omega=1.0)
+    _, rep = P.pcg(A, prob.rhs(), pc, tol=1e-8, max_iters=20000)
+    assert rep.converged == bool(g["pcg_converged"])
+    assert rep.iterations == int(g["pcg_iterations"])
+    h, ho = np.asarray(rep.residual_history), g["pcg_history"]
+    k = min(len(h), len(ho), 200)
+    np.testing.assert_allclose(h[:k], ho[:k], rtol=1e-9, atol=0)
