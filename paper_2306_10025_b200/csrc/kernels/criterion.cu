@@ -103,6 +103,12 @@ struct L1Args {
   // patch row t = pid[t] + id_offset (distributed greedy: global ids)
   const int32_t* creator;
   int64_t id_offset;
+  // scan split over entries (few patch tiles, many entries): block y scans
+  // entries [e0 + y chunk, e0 + (y+1) chunk) and records its first / best
+  // match in part_j / part_d [y][t]; l1_scan_reduce merges the chunks in order
+  int64_t chunk;
+  int32_t* part_j;
+  double* part_d;
 };
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -143,14 +149,18 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
     }
   }
   const int nchunk = (len + kTK - 1) / kTK;
-  // pairs: entry tiles split over gridDim.y; scan / argmin keep one block per patch tile (ordered state)
-  for (int64_t et0 = a.e0 + (int64_t)blockIdx.y * kTE; et0 < a.e1; et0 += (int64_t)gridDim.y * kTE) {
+  // pairs: entry tiles split over gridDim.y; scan / argmin keep one block per patch tile (ordered state),
+  // or (scan, a.chunk > 0) one block per (patch tile, entry chunk), merged afterwards
+  const int64_t ebeg = a.chunk ? a.e0 + (int64_t)blockIdx.y * a.chunk : a.e0 + (int64_t)blockIdx.y * kTE;
+  const int64_t eend = a.chunk ? (a.e1 < ebeg + a.chunk ? a.e1 : ebeg + a.chunk) : a.e1;
+  const int64_t estep = a.chunk ? kTE : (int64_t)gridDim.y * kTE;
+  for (int64_t et0 = ebeg; et0 < eend; et0 += estep) {
     if (Mode == kL1Scan && !a.best_match) {
       if (__syncthreads_and(done)) break;
     } else {
       __syncthreads();
     }
-    const int ne = a.e1 - et0 < kTE ? (int)(a.e1 - et0) : kTE;
+    const int ne = eend - et0 < kTE ? (int)(eend - et0) : kTE;
     if (t < kTE) {
       const int64_t e = et0 + t;
       esrc[t] = t < ne ? (a.rep_src ? a.mats + (int64_t)a.rep_src[e] * len : a.reps + e * len) : nullptr;
@@ -249,6 +259,12 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
     }
   }
   if (t >= kTP || p0 + t >= a.npat) return;
+  if (Mode == kL1Scan && a.chunk) {
+    const int64_t q = (int64_t)blockIdx.y * a.npat + p0 + t;
+    a.part_j[q] = cur_j;
+    if (a.best_match) a.part_d[q] = cur;
+    return;
+  }
   if (Mode == kL1Scan) {
     const int32_t me = pme[t];
     if (a.best_match) {
@@ -265,6 +281,36 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
   }
 }
 
+// merge of the entry chunks of a split scan, in chunk (= entry) order
+__global__ void l1_scan_reduce_kernel(int64_t npat, int gy, const int32_t* __restrict__ pid, int best_match,
+                                      const int32_t* __restrict__ part_j, const double* __restrict__ part_d,
+                                      int32_t* __restrict__ phi, double* __restrict__ best_d) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= npat) return;
+  const int32_t me = pid[g];
+  if (!best_match) {
+    for (int y = 0; y < gy; ++y) {
+      const int32_t j = part_j[(int64_t)y * npat + g];
+      if (j >= 0) {  // the first chunk holding a match has the first match
+        phi[me] = j;
+        return;
+      }
+    }
+    return;
+  }
+  double cur = best_d[me];
+  int32_t cj = phi[me];
+  for (int y = 0; y < gy; ++y) {
+    const double d = part_d[(int64_t)y * npat + g];
+    if (d < cur) {  // strict: the earlier chunk keeps ties
+      cur = d;
+      cj = part_j[(int64_t)y * npat + g];
+    }
+  }
+  best_d[me] = cur;
+  phi[me] = cj;
+}
+
 template <int Mode>
 void l1_tile_launch(const L1Args& a, cudaStream_t s) {
   const size_t smem = 2 * kTStage * sizeof(double);
@@ -276,6 +322,28 @@ void l1_tile_launch(const L1Args& a, cudaStream_t s) {
     const int64_t tiles = (a.e1 - a.e0 + kTE - 1) / kTE;
     const int64_t px = (a.npat + kTP - 1) / kTP;
     gy = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (4 * 148 + px - 1) / px));
+  }
+  if (Mode == kL1Scan) {
+    const int64_t px = (a.npat + kTP - 1) / kTP, ne = a.e1 - a.e0;
+    const char* sp = getenv("PDB_L1_SPLIT");
+    if (px < 2 * 148 && ne > 2 * kTE && !(sp && sp[0] == '0')) {
+      const int64_t want = std::min<int64_t>((ne + kTE - 1) / kTE, (4 * 148 + px - 1) / px);
+      int64_t chunk = (ne + want - 1) / want;
+      chunk = (chunk + kTE - 1) / kTE * kTE;
+      const int gys = (int)((ne + chunk - 1) / chunk);
+      if (gys > 1) {
+        L1Args b = a;
+        b.chunk = chunk;
+        PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.part_j), (size_t)gys * a.npat * sizeof(int32_t), s));
+        PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.part_d), (size_t)gys * a.npat * sizeof(double), s));
+        l1_tile_kernel<Mode><<<dim3(grid_for(a.npat, kTP), (unsigned)gys), kTThreads, smem, s>>>(b);
+        l1_scan_reduce_kernel<<<grid_for(a.npat, 256), 256, 0, s>>>(a.npat, gys, a.pid, a.best_match, b.part_j,
+                                                                     b.part_d, a.phi, a.best_d);
+        PDB_CUDA(cudaFreeAsync(b.part_j, s));
+        PDB_CUDA(cudaFreeAsync(b.part_d, s));
+        return;
+      }
+    }
   }
   l1_tile_kernel<Mode><<<dim3(grid_for(a.npat, kTP), gy), kTThreads, smem, s>>>(a);
 }
