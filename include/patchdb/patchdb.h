@@ -348,11 +348,15 @@ PDB_API pdb_status pdb_slab_create_subset(pdb_problem* slabs, int count, const i
                                           int64_t patch_size, pdb_database db, double omega,
                                           const unsigned char* nccl_id, pdb_slab* out);
 /* The same, with the compressed database built from the ranks' OWN patches
- * (no rank sees the others' matrices): greedy-l1 (opts->method, eps,
- * best_match) in the round-batched form -- each round's batch matrices are
- * broadcast by their owners, the resolution is replicated, every rank scans
- * only its own patches.  The database (entries replicated, phi per rank) is
- * bitwise the single-GPU pdb_database_build's. */
+ * (no rank sees the others' matrices).  opts->method:
+ *   PDB_METHOD_GREEDY_L1 (eps, best_match): the round-batched greedy -- each
+ *     round's batch matrices are broadcast by their owners, the resolution is
+ *     replicated, every rank scans only its own patches;
+ *   PDB_METHOD_KMEANS_ENTRYWISE (db_size, seed, max_iters): boundary-partitioned
+ *     k-means -- local assignment, gathered reseed, the in-order member sums
+ *     chain-folded along the ranks.
+ * The database (entries replicated, phi per rank) is bitwise the single-GPU
+ * pdb_database_build's. */
 PDB_API pdb_status pdb_slab_create_built(pdb_problem* slabs, int count, int rank, int nranks, int64_t patch_size,
                                          const pdb_compress_options* opts, double omega, const unsigned char* nccl_id,
                                          pdb_slab* out);

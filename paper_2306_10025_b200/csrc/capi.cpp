@@ -864,6 +864,9 @@ PDB_API pdb_status pdb_slab_create_built(pdb_problem* slabs, int count, int rank
     p.method = opts->method;
     p.eps = opts->eps;
     p.best_match = opts->best_match != 0;
+    p.db_size = opts->db_size;
+    p.seed = opts->seed;
+    p.max_iters = opts->max_iters;
     std::unique_ptr<pdb_slab_s, void (*)(pdb_slab_s*)> g(slab_new(rank, nranks, emulated), slab_delete);
     if (nccl_id != nullptr && nranks > 1) slab_attach(*g, nccl_id);
     slab_setup(*g, probs, patch_size, nullptr, omega, default_stream(), &p);

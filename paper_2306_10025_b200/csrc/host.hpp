@@ -170,6 +170,8 @@ void export_database(const pdb_database_s& db, const std::string& json_path, con
 
 // database.cu: the reference's lu_factor failure text (dense.cpp:59-61)
 std::string singular_msg(int32_t status, double best);
+// split_budget (compress.cpp:336-392): the k-means budget per boundary partition
+std::vector<int64_t> split_budget(int64_t m_p, const std::vector<int64_t>& sizes);
 
 // precond.cpp
 void precond_exact(const DeviceCsr& a, const pdb_patchset_s& ps, double omega, pdb_precond_s& out, cudaStream_t s);

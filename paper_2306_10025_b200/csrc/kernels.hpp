@@ -228,6 +228,11 @@ void argmin_assign(int64_t n, int64_t ne, const double* d, const int32_t* phi, i
 void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double* reps, const int32_t* phi,
                int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s);
 // In-order entrywise mean of each cluster (dense.cpp:211-223): members CSR (ascending).
+void cluster_sum_chain(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats,
+                       const double* init, const int64_t* counts, double* out, cudaStream_t s);
+// l1 argmin (strict <) of the listed patch rows pid[t] against ne entries
+void l1_argmin_ids(int64_t n, const int32_t* pid, int64_t ne, int len, const double* mats, const double* reps,
+                   const int32_t* phi, int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s);
 void cluster_mean(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats, double* reps,
                   cudaStream_t s);
 

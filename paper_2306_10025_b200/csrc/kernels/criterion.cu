@@ -1398,6 +1398,48 @@ void l1_argmin(int64_t n, int64_t ne, int len, const double* mats, const double*
                                                                     changed);
 }
 
+// In-order member sums continued from a previous rank's partial (the chain
+// fold of entrywise_mean_indexed, dense.cpp:211-223, across ranks): out[j] =
+// (init ? init[j] : 0) + members of j in ascending order; with counts (the
+// last rank) multiplied by 1 / counts[j] as the reference's mean.
+__global__ void cluster_sum_chain_kernel(int64_t m, int len, const int32_t* __restrict__ mem_ptr,
+                                         const int32_t* __restrict__ mem, const double* __restrict__ mats,
+                                         const double* __restrict__ init, const int64_t* __restrict__ counts,
+                                         double* __restrict__ out) {
+  const int64_t j = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= len || j >= m) return;
+  double s = init ? init[j * len + q] : 0.0;
+  const int32_t lo = mem_ptr[j], hi = mem_ptr[j + 1];
+  int32_t c = lo;
+  for (; c + 8 <= hi; c += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = mats[(int64_t)__ldg(mem + c + u) * len + q];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; c < hi; ++c) s = __dadd_rn(s, mats[(int64_t)mem[c] * len + q]);
+  if (counts) s = __dmul_rn(s, __ddiv_rn(1.0, (double)counts[j]));
+  out[j * len + q] = s;
+}
+
+void cluster_sum_chain(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats,
+                       const double* init, const int64_t* counts, double* out, cudaStream_t s) {
+  if (m <= 0) return;
+  cluster_sum_chain_kernel<<<dim3(grid_for(len, 128), (unsigned)m), 128, 0, s>>>(m, len, mem_ptr, mem, mats, init,
+                                                                                counts, out);
+}
+
+void l1_argmin_ids(int64_t n, const int32_t* pid, int64_t ne, int len, const double* mats, const double* reps,
+                   const int32_t* phi, int32_t* new_phi, double* min_dist, int32_t* changed, cudaStream_t s) {
+  if (n <= 0) return;
+  L1Args a{};
+  a.npat = n, a.pid = pid, a.len = len, a.mats = mats, a.e0 = 0, a.e1 = ne, a.reps = reps;
+  a.phi = const_cast<int32_t*>(phi), a.new_phi = new_phi, a.min_dist = min_dist, a.changed = changed;
+  l1_tile_launch<kL1Argmin>(a, s);
+}
+
 void cluster_mean(int64_t m, int len, const int32_t* mem_ptr, const int32_t* mem, const double* mats, double* reps,
                   cudaStream_t s) {
   if (m <= 0) return;

@@ -37,7 +37,10 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <numeric>
+#include <random>
 #include <thread>
 
 #include "host.hpp"
@@ -488,6 +491,291 @@ void slab_greedy(pdb_slab_s& g, int64_t patch_size, const BuildParams& bp, pdb_d
 
 
 
+// Distributed entrywise k-means, boundary-partitioned (partitioned_build,
+// compress.cpp:394-421; kmeans / kmeans_loop, compress.cpp:138-324) over the
+// ranks' own patches.  Partitions in global first-occurrence order (every
+// rank's pattern list in rank order), budgets by split_budget, per partition:
+// the seeded partial Fisher-Yates picks (their owners broadcast the initial
+// representatives), then Lloyd iterations whose assignment is local (l1
+// argmin, strict <) and whose assignment vector and distances are gathered so
+// every rank applies the same reseed rule; the new means are the in-order
+// member sums folded along the ranks (rank r continues rank r-1's partial
+// sums, the last rank scales by 1/size, exactly entrywise_mean_indexed) and
+// broadcast.  The database is bitwise the single-GPU partitioned_build's.
+void slab_kmeans(pdb_slab_s& g, int64_t patch_size, const BuildParams& bp, pdb_database_s& out, cudaStream_t s) {
+  require(bp.method == PDB_METHOD_KMEANS_ENTRYWISE, Errc::invalid_argument,
+          "rank-local k-means: the entrywise variant only");
+  const int L = static_cast<int>(g.ranks.size());
+  const int W = g.ranks[0]->nranks;
+  const int ps = static_cast<int>(patch_size);
+  const int64_t len = static_cast<int64_t>(ps) * ps;
+  const int words = (ps + 63) / 64;
+  const bool nccl = !g.emulated && W > 1;
+  std::vector<DevBuf<double>> mats(static_cast<size_t>(L));
+  std::vector<std::vector<std::vector<unsigned long long>>> keys(static_cast<size_t>(L));  // per local patch
+  for (int i = 0; i < L; ++i) {
+    SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+    extract_patches(R.a, R.ps, mats[static_cast<size_t>(i)], s);
+    DevBuf<unsigned long long> mk(static_cast<size_t>(std::max<int64_t>(R.np * words, 1)));
+    if (R.np > 0) k::boundary_masks(R.np, ps, mats[static_cast<size_t>(i)].get(), words, mk.get(), s);
+    const std::vector<unsigned long long> mh = mk.to_host(s);
+    keys[static_cast<size_t>(i)].resize(static_cast<size_t>(R.np));
+    for (int64_t kk = 0; kk < R.np; ++kk)
+      keys[static_cast<size_t>(i)][static_cast<size_t>(kk)].assign(mh.begin() + kk * words, mh.begin() + (kk + 1) * words);
+  }
+  // every rank's distinct patterns in local first-occurrence order, with counts
+  std::vector<Mail> outm(static_cast<size_t>(L), Mail(static_cast<size_t>(W))), inm;
+  std::vector<std::vector<std::vector<unsigned long long>>> lpat(static_cast<size_t>(L));
+  std::vector<std::vector<int64_t>> lcnt(static_cast<size_t>(L));
+  std::vector<std::vector<int32_t>> lpid(static_cast<size_t>(L));  // local pattern index per patch
+  for (int i = 0; i < L; ++i) {
+    std::map<std::vector<unsigned long long>, int32_t> idx;
+    for (const auto& kv : keys[static_cast<size_t>(i)]) {
+      auto it = idx.find(kv);
+      if (it == idx.end()) {
+        it = idx.emplace(kv, static_cast<int32_t>(lpat[static_cast<size_t>(i)].size())).first;
+        lpat[static_cast<size_t>(i)].push_back(kv);
+        lcnt[static_cast<size_t>(i)].push_back(0);
+      }
+      ++lcnt[static_cast<size_t>(i)][static_cast<size_t>(it->second)];
+      lpid[static_cast<size_t>(i)].push_back(it->second);
+    }
+    std::vector<int64_t> msg;
+    for (size_t p = 0; p < lpat[static_cast<size_t>(i)].size(); ++p) {
+      msg.push_back(lcnt[static_cast<size_t>(i)][p]);
+      for (unsigned long long w : lpat[static_cast<size_t>(i)][p]) msg.push_back(static_cast<int64_t>(w));
+    }
+    for (int q = 0; q < W; ++q) outm[static_cast<size_t>(i)][static_cast<size_t>(q)] = msg;
+  }
+  deliver(g, outm, inm, s);
+  // global partitions: first occurrence over the ranks in order; per-rank counts
+  std::map<std::vector<unsigned long long>, int32_t> gidx;
+  std::vector<std::vector<unsigned long long>> gpat;
+  std::vector<std::vector<int64_t>> gcnt;  // [partition][rank]
+  for (int q = 0; q < W; ++q) {
+    const auto& m = inm[0][static_cast<size_t>(q)];
+    for (size_t o = 0; o + 1 + static_cast<size_t>(words) <= m.size(); o += 1 + static_cast<size_t>(words)) {
+      std::vector<unsigned long long> kv(static_cast<size_t>(words));
+      for (int w = 0; w < words; ++w) kv[static_cast<size_t>(w)] = static_cast<unsigned long long>(m[o + 1 + static_cast<size_t>(w)]);
+      auto it = gidx.find(kv);
+      if (it == gidx.end()) {
+        it = gidx.emplace(kv, static_cast<int32_t>(gpat.size())).first;
+        gpat.push_back(kv);
+        gcnt.emplace_back(static_cast<size_t>(W), 0);
+      }
+      gcnt[static_cast<size_t>(it->second)][static_cast<size_t>(q)] += m[o];
+    }
+  }
+  const size_t G = gpat.size();
+  std::vector<int64_t> sizes(G);
+  for (size_t p = 0; p < G; ++p)
+    for (int q = 0; q < W; ++q) sizes[p] += gcnt[p][static_cast<size_t>(q)];
+  const std::vector<int64_t> alloc = split_budget(bp.db_size, sizes);
+  // per local rank: its patches of each partition (ascending local ids)
+  std::vector<std::vector<std::vector<int32_t>>> mine(static_cast<size_t>(L), std::vector<std::vector<int32_t>>(G));
+  for (int i = 0; i < L; ++i)
+    for (size_t kk = 0; kk < lpid[static_cast<size_t>(i)].size(); ++kk) {
+      const int32_t gp = gidx[lpat[static_cast<size_t>(i)][static_cast<size_t>(lpid[static_cast<size_t>(i)][kk])]];
+      mine[static_cast<size_t>(i)][static_cast<size_t>(gp)].push_back(static_cast<int32_t>(kk));
+    }
+  int64_t total = 0;
+  for (int64_t c : alloc) total += c;
+  DevBuf<double> reps_all(static_cast<size_t>(std::max<int64_t>(total, 1) * len));
+  for (int i = 0; i < L; ++i) g.ranks[static_cast<size_t>(i)]->phi.assign(static_cast<size_t>(g.ranks[static_cast<size_t>(i)]->np), -1);
+  int64_t eoff = 0;
+  DevBuf<int32_t> changed(1);
+  for (size_t p = 0; p < G; ++p) {
+    const int64_t n = sizes[p], m = alloc[p];
+    std::vector<int64_t> off(static_cast<size_t>(W) + 1, 0);
+    for (int q = 0; q < W; ++q) off[static_cast<size_t>(q) + 1] = off[static_cast<size_t>(q)] + gcnt[p][static_cast<size_t>(q)];
+    auto owner_of = [&](int64_t o) {
+      int q = 0;
+      while (off[static_cast<size_t>(q) + 1] <= o) ++q;
+      return q;
+    };
+    require(n >= 1 && m >= 1 && m <= n, Errc::invalid_argument, "kmeans requires 1 <= m_p <= n_p");
+    // seeded picks (compress.cpp:302-308) and the initial representatives from their owners
+    std::mt19937_64 rng(bp.seed + p);
+    std::vector<int64_t> perm(static_cast<size_t>(n));
+    std::iota(perm.begin(), perm.end(), int64_t{0});
+    for (int64_t i2 = 0; i2 < m; ++i2) {
+      const int64_t j = i2 + static_cast<int64_t>(rng() % static_cast<uint64_t>(n - i2));
+      std::swap(perm[static_cast<size_t>(i2)], perm[static_cast<size_t>(j)]);
+    }
+    double* reps = reps_all.get() + eoff * len;
+    std::vector<int> pick_owner(static_cast<size_t>(m));
+    for (int i = 0; i < L; ++i) {
+      const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+      std::vector<int32_t> src, dst;
+      for (int64_t c = 0; c < m; ++c) {
+        const int64_t o = perm[static_cast<size_t>(c)];
+        const int q = owner_of(o);
+        pick_owner[static_cast<size_t>(c)] = q;
+        if (q != R.rank) continue;
+        src.push_back(mine[static_cast<size_t>(i)][p][static_cast<size_t>(o - off[static_cast<size_t>(q)])]);
+        dst.push_back(static_cast<int32_t>(c));
+      }
+      for (size_t t = 0; t < src.size(); ++t)
+        PDB_CUDA(cudaMemcpyAsync(reps + dst[t] * len, mats[static_cast<size_t>(i)].get() + static_cast<int64_t>(src[t]) * len,
+                                 len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    if (nccl) {
+      SlabRank& R = *g.ranks[0];
+      PDB_NCCL_S(ncclGroupStart());
+      for (int64_t c = 0; c < m; ++c)
+        PDB_NCCL_S(ncclBroadcast(reps + c * len, reps + c * len, static_cast<size_t>(len), ncclDouble,
+                                 pick_owner[static_cast<size_t>(c)], R.comm, s));
+      PDB_NCCL_S(ncclGroupEnd());
+    }
+    // Lloyd iterations (kmeans_loop, Reseed policy)
+    std::vector<int32_t> phi_h(static_cast<size_t>(n), -1);
+    std::vector<DevBuf<int32_t>> dpid(static_cast<size_t>(L)), dphi(static_cast<size_t>(L)), dnew(static_cast<size_t>(L));
+    std::vector<DevBuf<double>> dmin(static_cast<size_t>(L));
+    for (int i = 0; i < L; ++i) {
+      const auto& li = mine[static_cast<size_t>(i)][p];
+      put(dpid[static_cast<size_t>(i)], li, s);
+      dphi[static_cast<size_t>(i)].alloc(std::max<size_t>(li.size(), 1));
+      PDB_CUDA(cudaMemsetAsync(dphi[static_cast<size_t>(i)].get(), 0xff, li.size() * sizeof(int32_t), s));
+      dnew[static_cast<size_t>(i)].alloc(std::max<size_t>(li.size(), 1));
+      dmin[static_cast<size_t>(i)].alloc(std::max<size_t>(li.size(), 1));
+    }
+    DevBuf<double> partial(static_cast<size_t>(m * len)), next(static_cast<size_t>(m * len));
+    for (int iter = 0; iter < bp.max_iters; ++iter) {
+      for (int i = 0; i < L; ++i) {
+        const auto& li = mine[static_cast<size_t>(i)][p];
+        k::l1_argmin_ids(static_cast<int64_t>(li.size()), dpid[static_cast<size_t>(i)].get(), m, static_cast<int>(len),
+                         mats[static_cast<size_t>(i)].get(), reps, dphi[static_cast<size_t>(i)].get(),
+                         dnew[static_cast<size_t>(i)].get(), dmin[static_cast<size_t>(i)].get(), changed.get(), s);
+        PDB_LAUNCH_CHECK();
+        const std::vector<int32_t> nh = dnew[static_cast<size_t>(i)].to_host(s);
+        const std::vector<double> mh = dmin[static_cast<size_t>(i)].to_host(s);
+        std::vector<int64_t> msg(2 * li.size());
+        for (size_t t = 0; t < li.size(); ++t) {
+          msg[2 * t] = nh[t];
+          std::memcpy(&msg[2 * t + 1], &mh[t], sizeof(double));
+        }
+        for (int q = 0; q < W; ++q) outm[static_cast<size_t>(i)][static_cast<size_t>(q)] = msg;
+      }
+      deliver(g, outm, inm, s);
+      const std::vector<int32_t> prev = phi_h;
+      std::vector<double> min_dist(static_cast<size_t>(n));
+      for (int q = 0; q < W; ++q) {
+        const auto& mm = inm[0][static_cast<size_t>(q)];
+        for (int64_t t = 0; t < gcnt[p][static_cast<size_t>(q)]; ++t) {
+          phi_h[static_cast<size_t>(off[static_cast<size_t>(q)] + t)] = static_cast<int32_t>(mm[static_cast<size_t>(2 * t)]);
+          std::memcpy(&min_dist[static_cast<size_t>(off[static_cast<size_t>(q)] + t)], &mm[static_cast<size_t>(2 * t + 1)], sizeof(double));
+        }
+      }
+      if (prev == phi_h) break;
+      std::vector<std::vector<int32_t>> members(static_cast<size_t>(m));
+      for (int64_t o = 0; o < n; ++o) members[static_cast<size_t>(phi_h[static_cast<size_t>(o)])].push_back(static_cast<int32_t>(o));
+      for (int64_t j = 0; j < m; ++j) {  // reseed empty clusters (compress.cpp:195-217)
+        if (!members[static_cast<size_t>(j)].empty()) continue;
+        int64_t far = -1;
+        double far_d = -1.0;
+        for (int64_t o = 0; o < n; ++o) {
+          const int32_t own = phi_h[static_cast<size_t>(o)];
+          if (members[static_cast<size_t>(own)].size() <= 1) continue;
+          if (min_dist[static_cast<size_t>(o)] > far_d) {
+            far_d = min_dist[static_cast<size_t>(o)];
+            far = o;
+          }
+        }
+        if (far < 0) continue;
+        auto& ow = members[static_cast<size_t>(phi_h[static_cast<size_t>(far)])];
+        ow.erase(std::find(ow.begin(), ow.end(), static_cast<int32_t>(far)));
+        members[static_cast<size_t>(j)].push_back(static_cast<int32_t>(far));
+        phi_h[static_cast<size_t>(far)] = static_cast<int32_t>(j);
+        min_dist[static_cast<size_t>(far)] = 0.0;
+      }
+      for (int64_t j = 0; j < m; ++j)
+        if (members[static_cast<size_t>(j)].empty())
+          fail(Errc::singular_matrix, "cluster " + std::to_string(j) + ": entrywise_mean of an empty cluster");
+      std::vector<int64_t> counts(static_cast<size_t>(m));
+      for (int64_t j = 0; j < m; ++j) counts[static_cast<size_t>(j)] = static_cast<int64_t>(members[static_cast<size_t>(j)].size());
+      DevBuf<int64_t> dcounts;
+      put(dcounts, counts, s);
+      // each rank's members (local ids), cluster-major, ascending
+      auto local_members = [&](int q, int i) {
+        std::vector<int32_t> ptr(static_cast<size_t>(m) + 1, 0), mem;
+        for (int64_t j = 0; j < m; ++j) {
+          for (int32_t o : members[static_cast<size_t>(j)])
+            if (o >= off[static_cast<size_t>(q)] && o < off[static_cast<size_t>(q) + 1])
+              mem.push_back(mine[static_cast<size_t>(i)][p][static_cast<size_t>(o - off[static_cast<size_t>(q)])]);
+          ptr[static_cast<size_t>(j) + 1] = static_cast<int32_t>(mem.size());
+        }
+        return std::make_pair(ptr, mem);
+      };
+      // the chain fold: ranks in order continue the partial sums, the last scales
+      const int last = W - 1;
+      if (g.emulated || W == 1) {
+        for (int i = 0; i < L; ++i) {
+          const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+          auto pm = local_members(R.rank, i);
+          DevBuf<int32_t> dp, dm;
+          put(dp, pm.first, s);
+          put(dm, pm.second, s);
+          k::cluster_sum_chain(m, static_cast<int>(len), dp.get(), dm.get(), mats[static_cast<size_t>(i)].get(),
+                               i == 0 ? nullptr : partial.get(), R.rank == last ? dcounts.get() : nullptr,
+                               R.rank == last ? reps : next.get(), s);
+          sync(s);
+          std::swap(partial, next);
+        }
+      } else {
+        SlabRank& R = *g.ranks[0];
+        auto pm = local_members(R.rank, 0);
+        DevBuf<int32_t> dp, dm;
+        put(dp, pm.first, s);
+        put(dm, pm.second, s);
+        if (R.rank > 0) PDB_NCCL_S(ncclRecv(partial.get(), static_cast<size_t>(m * len), ncclDouble, R.rank - 1, R.comm, s));
+        k::cluster_sum_chain(m, static_cast<int>(len), dp.get(), dm.get(), mats[0].get(), R.rank > 0 ? partial.get() : nullptr,
+                             R.rank == last ? dcounts.get() : nullptr, R.rank == last ? reps : next.get(), s);
+        if (R.rank < last) PDB_NCCL_S(ncclSend(next.get(), static_cast<size_t>(m * len), ncclDouble, R.rank + 1, R.comm, s));
+        PDB_NCCL_S(ncclBroadcast(reps, reps, static_cast<size_t>(m * len), ncclDouble, last, R.comm, s));
+        sync(s);
+      }
+      // the next assignment compares against this one
+      for (int i = 0; i < L; ++i) {
+        const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+        const std::vector<int32_t> mp(phi_h.begin() + off[static_cast<size_t>(R.rank)],
+                                      phi_h.begin() + off[static_cast<size_t>(R.rank) + 1]);
+        if (!mp.empty()) dphi[static_cast<size_t>(i)].upload(mp.data(), mp.size(), s);
+      }
+    }
+    // phi of this partition -> the ranks' patches
+    for (int i = 0; i < L; ++i) {
+      SlabRank& R = *g.ranks[static_cast<size_t>(i)];
+      const auto& li = mine[static_cast<size_t>(i)][p];
+      for (size_t t = 0; t < li.size(); ++t)
+        R.phi[static_cast<size_t>(li[t])] = static_cast<int32_t>(eoff + phi_h[static_cast<size_t>(off[static_cast<size_t>(R.rank)] + static_cast<int64_t>(t))]);
+    }
+    eoff += m;
+  }
+  // factors of the representatives (finalize_factors; replicated)
+  out.m = total;
+  out.ps = ps;
+  out.np = 0;
+  for (int64_t c : g.np_of) out.np += c;
+  out.method = "kmeans-entrywise-partitioned";
+  out.lu.alloc(static_cast<size_t>(std::max<int64_t>(total, 1) * len));
+  out.piv.alloc(static_cast<size_t>(std::max<int64_t>(total, 1) * ps));
+  DevBuf<int32_t> status(static_cast<size_t>(std::max<int64_t>(total, 1)));
+  DevBuf<double> bst(static_cast<size_t>(std::max<int64_t>(total, 1)));
+  k::lu_batched(total, ps, reps_all.get(), nullptr, out.lu.get(), out.piv.get(), status.get(), bst.get(), s);
+  PDB_LAUNCH_CHECK();
+  const std::vector<int32_t> sth = status.to_host(s);
+  for (int64_t e = 0; e < total; ++e)
+    if (sth[static_cast<size_t>(e)] != 0) {
+      const std::vector<double> bh = bst.to_host(s);
+      fail(Errc::singular_matrix, "cluster " + std::to_string(e) + ": " +
+                                      singular_msg(sth[static_cast<size_t>(e)], bh[static_cast<size_t>(e)]));
+    }
+  out.reps = std::move(reps_all);
+  g.m = total;
+  g.creators.clear();
+  sync(s);
+}
+
 void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch_size, const pdb_database_s* db,
                 double omega, cudaStream_t s, const BuildParams* build) {
   require_device();
@@ -701,7 +989,10 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
   // (5) factors and the DoF -> slot map
   pdb_database_s built;  // distributed greedy: replicated entries, per-rank phi in R.phi
   if (!db && build) {
-    slab_greedy(g, patch_size, *build, built, s);
+    if (build->method == PDB_METHOD_KMEANS_ENTRYWISE)
+      slab_kmeans(g, patch_size, *build, built, s);
+    else
+      slab_greedy(g, patch_size, *build, built, s);
     db = &built;
   }
   for (int i = 0; i < L; ++i) {

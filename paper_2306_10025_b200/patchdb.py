@@ -781,10 +781,12 @@ class Slab(_Handle):
 
     @classmethod
     def create_built(cls, slabs, rank: int, nranks: int, patch_size: int, method: int = 2, eps: float = 1e-7,
-                     best_match: bool = False, omega: float = 1.0, nccl_id: Optional[bytes] = None) -> "Slab":
-        """Compressed database built from the ranks' own patches (pdb_slab_create_built)."""
+                     best_match: bool = False, omega: float = 1.0, nccl_id: Optional[bytes] = None,
+                     **kmeans) -> "Slab":
+        """Compressed database built from the ranks' own patches (pdb_slab_create_built):
+        greedy-l1 (eps, best_match) or entrywise k-means (db_size, seed, max_iters)."""
         arr = (C.c_void_p * len(slabs))(*[p.ptr for p in slabs])
-        o = compress_options(method, eps=eps, best_match=int(best_match))
+        o = compress_options(method, eps=eps, best_match=int(best_match), **kmeans)
         out = C.c_void_p()
         _check(_lib.pdb_slab_create_built(arr, len(slabs), rank, nranks, patch_size, C.byref(o), omega, nccl_id,
                                           C.byref(out)))

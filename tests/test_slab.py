@@ -142,3 +142,26 @@ def test_rank_local_greedy_equals_single_gpu(P, cfg, cells, ps, ranks, eps, best
     want, _ = pc.relax(A, b, x0, 3, history=False)
     got, _ = emulated_relax(P, sl, b, x0, 3)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("cfg,cells,ps,ranks,k,iters", [(2, 16, 25, 2, 30, 20), (3, 8, 27, 4, 40, 20),
+                                                         (4, 8, 22, 2, 24, 20), (5, 4, 192, 2, 40, 8),
+                                                         (2, 0, 25, 8, 64, 50), (4, 0, 22, 4, 128, 10)])
+def test_rank_local_kmeans_equals_single_gpu(P, cfg, cells, ps, ranks, k, iters):
+    """pdb_slab_create_built with KMEANS_ENTRYWISE: boundary partitions in
+    global first-occurrence order, local assignment, gathered reseed, means
+    chain-folded along the ranks -- bitwise the single-GPU partitioned build
+    (phi and sweeps)."""
+    g = P.Problem.generate(cfg, cells)
+    A = g.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    db = P.Database.build(A, pset, P.KMEANS_ENTRYWISE, db_size=k, seed=42, max_iters=iters)
+    slabs = [P.Problem.generate_slab(cfg, cells, r, ranks) for r in range(ranks)]
+    sl = P.Slab.create_built(slabs, 0, ranks, ps, P.KMEANS_ENTRYWISE, omega=0.9, db_size=k, seed=42, max_iters=iters)
+    assert sl.database_size == db.size
+    assert np.array_equal(np.concatenate([sl.phi(i) for i in range(ranks)]), db.phi())
+    pc = P.Preconditioner.create(A, pset, db, omega=0.9)
+    b = g.rhs()
+    want, _ = pc.relax(A, b, np.zeros_like(b), 3, history=False)
+    got, _ = emulated_relax(P, sl, b, np.zeros_like(b), 3)
+    assert np.array_equal(got, want)
