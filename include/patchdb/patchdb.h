@@ -282,6 +282,14 @@ PDB_API pdb_status pdb_precond_coarse_factor(pdb_precond pc, double* band, int64
  * omega W^1/2 S W^1/2 (CG needs a symmetric preconditioner). */
 PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
                                  double* x, pdb_report* out_report);
+/* pdb_pcg_solve with flags.  PDB_PCG_REPRODUCIBLE: the CPU restatement's
+ * sequence bit for bit (reference-order patch solves -- the preconditioner
+ * must be created with PDB_APPLY=lu -- the ordered scatter, unfused updates,
+ * inner products in chunks of 256 summed in order): identical iteration
+ * counts and residual histories; host-driven, for verification. */
+#define PDB_PCG_REPRODUCIBLE 1
+PDB_API pdb_status pdb_pcg_solve_ex(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
+                                    int flags, double* x, pdb_report* out_report);
 
 /* ---- multi-GPU: slab-partitioned sweep ----------
  * Rank r of N owns the contiguous patch range [np*r/N, np*(r+1)/N); DoFs are

@@ -1260,9 +1260,33 @@ static void pc_apply_sym(const pc_t* pc, const double* r, double* z) {
   free(local);
 }
 
+/* Inner products of the PCG restatement in a fixed blocked order, so that a
+ * parallel implementation can reproduce them bit for bit: chunks of
+ * PCG_CHUNK consecutive elements summed from 0.0 in order (a[i] * b[i] rounded,
+ * then added), the chunk sums summed in groups of PCG_CHUNK in order, the
+ * group sums in order.  (The reference has no CG; this order is part of the
+ * restatement's definition.) */
+#define PCG_CHUNK 256
+static double dot_blocked(int64_t n, const double* a, const double* b) {
+  const int64_t nch = (n + PCG_CHUNK - 1) / PCG_CHUNK;
+  const int64_t ngr = (nch + PCG_CHUNK - 1) / PCG_CHUNK;
+  double total = 0.0;
+  for (int64_t g = 0; g < ngr; ++g) {
+    double gs = 0.0;
+    for (int64_t c = g * PCG_CHUNK; c < nch && c < (g + 1) * PCG_CHUNK; ++c) {
+      double cs = 0.0;
+      for (int64_t i = c * PCG_CHUNK; i < n && i < (c + 1) * PCG_CHUNK; ++i) cs += a[i] * b[i];
+      gs += cs;
+    }
+    total += gs;
+  }
+  return total;
+}
+
 /* Preconditioned CG (not in the reference; SPEC.md:509 lists CG as absent).
- * Textbook Hestenes-Stiefel form with z = M_sym^{-1} r (pc_apply_sym); the GPU
- * implementation (pdb_pcg_solve) follows the same recurrence. */
+ * Textbook Hestenes-Stiefel form with z = M_sym^{-1} r (pc_apply_sym) and the
+ * blocked inner products above; the GPU's reproducible mode
+ * (pdb_pcg_solve_ex with PDB_PCG_REPRODUCIBLE) computes the same sequence. */
 int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, const double* b, int64_t np, int64_t ps,
             const int64_t* patches, const double* weights, double omega, const double* lu, const int64_t* piv,
             const int64_t* phi, int have_pc, double tol, int64_t max_iters, double* x, int64_t* iters_out,
@@ -1278,7 +1302,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, co
     x[i] = 0.0;
     r[i] = b[i];
   }
-  const double bnorm = norm2(n, b);
+  const double bnorm = sqrt(dot_blocked(n, b, b));
   int converged = 0;
   int64_t it = 0;
   if (bnorm == 0.0) {
@@ -1289,14 +1313,14 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, co
     if (have_pc) pc_apply_sym(&pc, r, z);
     else memcpy(z, r, sizeof(double) * (size_t)n);
     memcpy(p, z, sizeof(double) * (size_t)n);
-    double rz = dot(n, r, z);
+    double rz = dot_blocked(n, r, z);
     while (it < max_iters) {
       orc_spmv(n, rp, ci, v, p, q);
-      const double alpha = rz / dot(n, p, q);
+      const double alpha = rz / dot_blocked(n, p, q);
       for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
       for (int64_t i = 0; i < n; ++i) r[i] -= alpha * q[i];
       ++it;
-      const double rel = norm2(n, r) / bnorm;
+      const double rel = sqrt(dot_blocked(n, r, r)) / bnorm;
       if (hl < hcap) hist[hl] = rel;
       ++hl;
       if (rel <= tol) {
@@ -1305,7 +1329,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, co
       }
       if (have_pc) pc_apply_sym(&pc, r, z);
       else memcpy(z, r, sizeof(double) * (size_t)n);
-      const double rz_new = dot(n, r, z);
+      const double rz_new = dot_blocked(n, r, z);
       const double beta = rz_new / rz;
       rz = rz_new;
       for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];

@@ -700,6 +700,16 @@ PDB_API pdb_status pdb_pcg_solve(pdb_matrix m, const double* b, pdb_precond pc, 
   });
 }
 
+PDB_API pdb_status pdb_pcg_solve_ex(pdb_matrix m, const double* b, pdb_precond pc, double tol, int64_t max_iters,
+                                    int flags, double* x, pdb_report* out_report) {
+  if (m == nullptr || b == nullptr || x == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    auto rep = std::make_unique<pdb_report_s>();
+    pcg_device(m->a, b, pc, tol, max_iters, x, *rep, default_stream(), (flags & PDB_PCG_REPRODUCIBLE) != 0);
+    if (out_report != nullptr) *out_report = rep.release();
+  });
+}
+
 PDB_API int64_t pdb_report_iterations(pdb_report rep) { return rep == nullptr ? 0 : rep->iterations; }
 PDB_API int64_t pdb_report_restarts(pdb_report rep) { return rep == nullptr ? 0 : rep->restarts; }
 PDB_API int pdb_report_converged(pdb_report rep) { return rep != nullptr && rep->converged ? 1 : 0; }

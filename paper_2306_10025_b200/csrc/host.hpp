@@ -184,8 +184,9 @@ void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scal
 void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of = nullptr);
 void common_setup(const pdb_patchset_s& ps, double omega, pdb_precond_s& pc, cudaStream_t s);
 // z = M^{-1} r on device pointers (symmetric: omega W^1/2 S W^1/2, used by PCG).
+// reference_order: the patch solves in lu_solve_into's order (reproducible PCG; needs lu_apply)
 void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s,
-                          bool symmetric = false);
+                          bool symmetric = false, bool reference_order = false);
 // sweeps of smooth(); history (device, may be null) gets sweeps+1 norms.
 void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                   double* history, cudaStream_t s);
@@ -233,8 +234,9 @@ void shard_relax(pdb_shard_s& sh, const double* b, double* x, int64_t sweeps, cu
 // krylov.cpp
 void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, const pdb_gmres_options& o,
                   double* x_host, pdb_report_s& rep, cudaStream_t s);
+// reproducible: the oracle's orc_pcg sequence bit for bit (verification mode)
 void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol, int64_t max_iters,
-                double* x_host, pdb_report_s& rep, cudaStream_t s);
+                double* x_host, pdb_report_s& rep, cudaStream_t s, bool reproducible = false);
 
 // slab.cu -- multi-GPU sweep shards with rank-local data
 struct SlabRank;

@@ -62,6 +62,13 @@ void finish_ratio(const double* partials, int count, double* num, double* out, b
 // ---- sweep.cu : patch stage and scatter -----------------------------------
 // Per-patch gather + LU solve (column-major factors):
 //   sols[k*ps + i] = (B_f^{-1} (r .* in_scale)[patch_k])_i,  f = phi ? phi[k] : k; in_scale may be null.
+// Reproducible PCG (oracle orc_pcg order): reference-order patch solve on the
+// column-major LU, chunk sums of the blocked inner product, unfused axpys
+// (mode 0: y += a x, 1: y -= a x, 2: y = x + a y).
+void patch_solve_ref(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
+                     const int32_t* phi, const double* r, const double* in_scale, double* sols, cudaStream_t s);
+void dot_chunks(int64_t n, int chunk, const double* a, const double* b, double* out, cudaStream_t s);
+void axpy_ref(int64_t n, double alpha, const double* x, double* y, int mode, cudaStream_t s);
 void patch_solve(int64_t np, int ps, const int32_t* patches, const double* factors_cm, const int32_t* piv,
                  const int32_t* phi, const double* r, const double* in_scale, double* sols, cudaStream_t s);
 // Same product with explicit column-major inverses Binv (default sweep path).

@@ -470,6 +470,61 @@ __global__ void __launch_bounds__(kBlkThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Reproducible PCG pieces (the oracle's orc_pcg order, oracle/pdb_oracle.c):
+// the patch solve of lu_solve_into (dense.cpp:77-94) in the reference's
+// order -- permutation, forward and backward substitution both row-oriented
+// with ascending j -- on the column-major LU (F[j * ps + i] = LU(i, j)), one
+// thread per patch; chunk sums of the blocked inner product; unfused axpys.
+__global__ void patch_solve_ref_kernel(int64_t np, int ps, const int32_t* __restrict__ patches,
+                                       const double* __restrict__ F, const int32_t* __restrict__ piv,
+                                       const int32_t* __restrict__ phi, const double* __restrict__ r,
+                                       const double* __restrict__ in_scale, double* __restrict__ sols) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  const int64_t f = phi ? (int64_t)phi[k] : k;
+  const double* Fk = F + f * (int64_t)ps * ps;
+  const int32_t* P = piv + f * ps;
+  double* y = sols + k * ps;
+  for (int i = 0; i < ps; ++i) {
+    const int32_t g = patches[k * ps + P[i]];
+    y[i] = in_scale ? __dmul_rn(r[g], in_scale[g]) : r[g];
+  }
+  for (int i = 1; i < ps; ++i) {
+    double s = y[i];
+    for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(Fk[(int64_t)j * ps + i], y[j]));
+    y[i] = s;
+  }
+  for (int i = ps - 1; i >= 0; --i) {
+    double s = y[i];
+    for (int j = i + 1; j < ps; ++j) s = __dsub_rn(s, __dmul_rn(Fk[(int64_t)j * ps + i], y[j]));
+    y[i] = __ddiv_rn(s, Fk[(int64_t)i * ps + i]);
+  }
+}
+
+__global__ void dot_chunks_kernel(int64_t n, int chunk, const double* __restrict__ a, const double* __restrict__ b,
+                                  double* __restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = c * chunk;
+  if (i0 >= n) return;
+  const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
+  double s = 0.0;
+  for (int64_t i = i0; i < i1; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+  out[c] = s;
+}
+
+__global__ void axpy_ref_kernel(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y,
+                                int mode) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (mode == 0)
+    y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));  // y += alpha x
+  else if (mode == 1)
+    y[i] = __dsub_rn(y[i], __dmul_rn(alpha, x[i]));  // y -= alpha x
+  else
+    y[i] = __dadd_rn(x[i], __dmul_rn(alpha, y[i]));  // y = x + alpha y
+}
+
 }  // namespace
 
 void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, double* lu, int32_t* piv,
@@ -514,6 +569,21 @@ void lu_batched(int64_t count, int ps, const double* mats, const int32_t* src, d
     const size_t smem = (size_t)kWarps * ps * sizeof(double);
     lu_kernel<false><<<grid, kWarps * 32, smem, s>>>(count, ps, mats, src, lu, piv, status, fail_best);
   }
+}
+
+void patch_solve_ref(int64_t np, int ps, const int32_t* patches, const double* F, const int32_t* piv,
+                     const int32_t* phi, const double* r, const double* in_scale, double* sols, cudaStream_t s) {
+  if (np > 0) patch_solve_ref_kernel<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(np, ps, patches, F, piv, phi, r,
+                                                                                 in_scale, sols);
+}
+
+void dot_chunks(int64_t n, int chunk, const double* a, const double* b, double* out, cudaStream_t s) {
+  const int64_t nch = (n + chunk - 1) / chunk;
+  if (nch > 0) dot_chunks_kernel<<<(unsigned)((nch + 127) / 128), 128, 0, s>>>(n, chunk, a, b, out);
+}
+
+void axpy_ref(int64_t n, double alpha, const double* x, double* y, int mode, cudaStream_t s) {
+  if (n > 0) axpy_ref_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, alpha, x, y, mode);
 }
 
 }  // namespace pdb::k

@@ -189,9 +189,84 @@ void gmres_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s*
   sync(s);
 }
 
+// Reproducible PCG: the oracle's orc_pcg sequence bit for bit -- the bitwise
+// SpMV, the patch solves in lu_solve_into's order (PDB_APPLY=lu factors), the
+// ordered scatter, unfused axpys and the blocked inner products (chunks of
+// 256 summed in order, chunk sums in groups of 256 in order, then the groups;
+// oracle/pdb_oracle.c dot_blocked) -- so iteration counts and residual
+// histories are identical to the CPU restatement's.  Host-driven (a few
+// synchronisations per iteration): a verification mode, not the fast path.
+static void pcg_reproducible(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol,
+                             int64_t max_iters, double* x_host, pdb_report_s& rep, cudaStream_t s) {
+  constexpr int kChunk = 256;
+  const int64_t n = a.n;
+  const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
+  const int64_t nch = (n + kChunk - 1) / kChunk;
+  Scratch<double> b(un, s), x(un, s), r(un, s), z(un, s), p(un, s), q(un, s);
+  Scratch<double> chunks(static_cast<size_t>(std::max<int64_t>(nch, 1)), s);
+  std::vector<double> ch(static_cast<size_t>(std::max<int64_t>(nch, 1)));
+  const k::SpmvPlan plan = plan_of(a);
+  auto dotb = [&](const double* u, const double* v) {
+    k::dot_chunks(n, kChunk, u, v, chunks.get(), s);
+    PDB_CUDA(cudaMemcpyAsync(ch.data(), chunks.get(), nch * sizeof(double), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    double total = 0.0;
+    for (int64_t g0 = 0; g0 < nch; g0 += kChunk) {
+      double gs = 0.0;
+      for (int64_t c = g0; c < nch && c < g0 + kChunk; ++c) gs += ch[static_cast<size_t>(c)];
+      total += gs;
+    }
+    return total;
+  };
+  auto precond = [&]() {
+    if (pc) precond_apply_device(*pc, r.get(), z.get(), s, /*symmetric=*/true, /*reference_order=*/true);
+    else PDB_CUDA(cudaMemcpyAsync(z.get(), r.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  };
+  b.upload(b_host, static_cast<size_t>(n));
+  x.zero();
+  PDB_CUDA(cudaMemcpyAsync(r.get(), b.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  rep = pdb_report_s();
+  const double bnorm = std::sqrt(dotb(b.get(), b.get()));
+  if (bnorm == 0.0) {
+    rep.converged = true;
+  } else {
+    rep.residual_history.push_back(1.0);
+    precond();
+    PDB_CUDA(cudaMemcpyAsync(p.get(), z.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    double rz = dotb(r.get(), z.get());
+    while (rep.iterations < max_iters) {
+      k::spmv(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), p.get(), q.get(), s);
+      const double alpha = rz / dotb(p.get(), q.get());
+      k::axpy_ref(n, alpha, p.get(), x.get(), 0, s);
+      k::axpy_ref(n, alpha, q.get(), r.get(), 1, s);
+      ++rep.iterations;
+      const double rel = std::sqrt(dotb(r.get(), r.get())) / bnorm;
+      rep.residual_history.push_back(rel);
+      if (rel <= tol) {
+        rep.converged = true;
+        break;
+      }
+      precond();
+      const double rz_new = dotb(r.get(), z.get());
+      const double beta = rz_new / rz;
+      rz = rz_new;
+      k::axpy_ref(n, beta, z.get(), p.get(), 2, s);
+    }
+  }
+  PDB_LAUNCH_CHECK();
+  rep.final_relative_residual = rep.residual_history.empty() ? 0.0 : rep.residual_history.back();
+  x.download(x_host, static_cast<size_t>(n));
+  sync(s);
+}
+
 void pcg_device(const DeviceCsr& a, const double* b_host, const pdb_precond_s* pc, double tol, int64_t max_iters,
-                double* x_host, pdb_report_s& rep, cudaStream_t s) {
+                double* x_host, pdb_report_s& rep, cudaStream_t s, bool reproducible) {
   require_device();
+  if (reproducible) {
+    if (pc) require(pc->n == a.n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
+    pcg_reproducible(a, b_host, pc, tol, max_iters, x_host, rep, s);
+    return;
+  }
   const int64_t n = a.n;
   if (pc) require(pc->n == n, Errc::dimension_mismatch, "preconditioner does not match the matrix");
   Ops ops(a, pc, s);

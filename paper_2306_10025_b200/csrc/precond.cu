@@ -302,9 +302,17 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
   sync(s);
 }
 
-void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s, bool symmetric) {
+void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, cudaStream_t s, bool symmetric,
+                          bool reference_order) {
   Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
-  patch_stage(pc, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
+  if (reference_order) {
+    require(pc.lu_apply, Errc::invalid_argument,
+            "reproducible mode needs the LU factors (preconditioner created with PDB_APPLY=lu)");
+    k::patch_solve_ref(pc.np, static_cast<int>(pc.ps), pc.patches.get(), pc.factors.get(), pc.piv.get(),
+                       pc.compressed ? pc.phi.get() : nullptr, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
+  } else {
+    patch_stage(pc, r, symmetric ? pc.sqrt_w.get() : nullptr, sols.get(), s);
+  }
   scatter_stage(pc, sols.get(), symmetric, nullptr, z, nullptr, s);
   if (pc.coarse) coarse_correct(*pc.coarse, r, z, s);  // combo: z += P0 Ac^{-1} R0 r
   PDB_LAUNCH_CHECK();

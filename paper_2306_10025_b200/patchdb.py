@@ -615,15 +615,23 @@ def gmres(m: Matrix, b, pc: Optional[Preconditioner] = None, restart: int = 20, 
     return x, _report(rep)
 
 
-def pcg(m: Matrix, b, pc: Optional[Preconditioner] = None, tol: float = 1e-8, max_iters: int = 10000):
+def pcg(m: Matrix, b, pc: Optional[Preconditioner] = None, tol: float = 1e-8, max_iters: int = 10000,
+        reproducible: bool = False):
+    """pdb_pcg_solve; reproducible=True: pdb_pcg_solve_ex(PDB_PCG_REPRODUCIBLE), the
+    oracle's sequence bit for bit (the preconditioner must be created with PDB_APPLY=lu)."""
     b = _f64(b)
     x = np.empty(m.rows)
     rep = C.c_void_p()
-    _check(_lib.pdb_pcg_solve(m.ptr, _dp(b), pc.ptr if pc is not None else None, tol, max_iters, _dp(x),
-                              C.byref(rep)))
+    if reproducible:
+        _check(_lib.pdb_pcg_solve_ex(m.ptr, _dp(b), pc.ptr if pc is not None else None, tol, max_iters, 1, _dp(x),
+                                     C.byref(rep)))
+    else:
+        _check(_lib.pdb_pcg_solve(m.ptr, _dp(b), pc.ptr if pc is not None else None, tol, max_iters, _dp(x),
+                                  C.byref(rep)))
     return x, _report(rep)
 
 
+_sig("pdb_pcg_solve_ex", C.c_int, _P, _D, _P, C.c_double, C.c_int64, C.c_int, _D, C.POINTER(_P))
 _sig("pdb_relax_profile", C.c_int, _P, _P, C.c_void_p, C.c_void_p, C.c_int64, _D, C.c_void_p)
 _sig("pdb_precond_stored_factors", C.c_int64, _P)
 _sig("pdb_precond_patch_count", C.c_int64, _P)

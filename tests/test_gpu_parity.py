@@ -224,6 +224,28 @@ def test_pcg_iterations(c2s, P, orc):
     np.testing.assert_allclose(rep.residual_history[:10], ro["residual_history"][:10], rtol=1e-9)
 
 
+@pytest.mark.parametrize("compressed", [False, True])
+def test_pcg_reproducible_bitwise(c2s, P, orc, monkeypatch, compressed):
+    """pdb_pcg_solve_ex(PDB_PCG_REPRODUCIBLE): the oracle's PCG sequence bit for
+    bit -- identical iteration count, residual history and solution."""
+    db = P.Database.build(c2s.A, c2s.ps, P.KMEANS_ENTRYWISE, db_size=16) if compressed else None
+    monkeypatch.setenv("PDB_APPLY", "lu")
+    pc = P.Preconditioner.create(c2s.A, c2s.ps, db, omega=1.0)
+    monkeypatch.delenv("PDB_APPLY")
+    x, rep = P.pcg(c2s.A, c2s.b, pc, tol=1e-10, reproducible=True)
+    if compressed:
+        lu, piv, phi = _oracle_pc(orc, c2s, db)
+    else:
+        lu = np.stack([orc.lu_factor(m)[0] for m in c2s.mats])
+        piv = np.stack([orc.lu_factor(m)[1] for m in c2s.mats])
+        phi = None
+    xo, ro = orc.pcg(c2s.csr, c2s.b, dict(patches=c2s.patches, weights=c2s.w, omega=1.0, lu=lu, piv=piv, phi=phi),
+                     tol=1e-10)
+    assert rep.iterations == ro["iterations"]
+    assert np.array_equal(np.asarray(rep.residual_history), ro["residual_history"])
+    assert np.array_equal(x, xo)
+
+
 def test_singular_patch_error(c1, P, orc):
     rp, ci, v = [a.copy() for a in c1.csr]
     # zero one cell-interior row (its stored entries stay in the pattern)
