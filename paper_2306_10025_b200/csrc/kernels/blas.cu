@@ -234,13 +234,24 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_kernel(int64_t n, int j, cons
 
 template <int E>
 bool launch_mgs(int64_t n, int j, const double* V, int64_t ldv, double* w, double* h, cudaStream_t s) {
-  static thread_local MgsSync* sy = nullptr;
+  // per device: the barrier struct lives in that device's memory
+  constexpr int kMaxDev = 64;
+  int dev = 0;
+  PDB_CUDA(cudaGetDevice(&dev));
+  require(dev < kMaxDev, Errc::internal, "device ordinal beyond the per-device caches");
+  static thread_local MgsSync* sy_of[kMaxDev] = {};
+  MgsSync*& sy = sy_of[dev];
   if (!sy) {
     PDB_CUDA(cudaMalloc(&sy, sizeof(MgsSync)));
     PDB_CUDA(cudaMemset(sy, 0, sizeof(MgsSync)));
   }
-  static int per_sm = -1;
-  if (per_sm < 0) PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel<E>, kMgsThreads, 0));
+  static int per_sm_of[kMaxDev];
+  static bool have_of[kMaxDev] = {};
+  if (!have_of[dev]) {
+    PDB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_of[dev], mgs_kernel<E>, kMgsThreads, 0));
+    have_of[dev] = true;
+  }
+  const int per_sm = per_sm_of[dev];
   const int64_t need = (n + static_cast<int64_t>(kMgsThreads) * E - 1) / (static_cast<int64_t>(kMgsThreads) * E);
   const int64_t cap = std::min<int64_t>(kMgsMaxBlocks, static_cast<int64_t>(per_sm) * num_sms());
   if (need > cap) return false;

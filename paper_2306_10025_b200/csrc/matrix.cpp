@@ -46,11 +46,13 @@ void require_device() {
   if (state == 0) fail(Errc::internal, "CUDA device unavailable (" + why + "); patchdb-b200 has no CPU path");
 }
 
-int num_sms() {
-  static int sms = 0;
+int num_sms() {  // of the current device (cached per device)
+  static int sms_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int dummy = 0;
+  int& sms = dev < 64 ? sms_of[dev] : dummy;
   if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (!sms) sms = 148;
   }

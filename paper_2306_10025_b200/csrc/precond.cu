@@ -371,7 +371,11 @@ void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, 
     sync(s);
     return;
   }
-  static thread_local cudaStream_t cs = nullptr;
+  static thread_local cudaStream_t cs_of[64] = {};  // per device (a stream belongs to one device)
+  int dev = 0;
+  PDB_CUDA(cudaGetDevice(&dev));
+  require(dev < 64, Errc::internal, "device ordinal beyond the per-device caches");
+  cudaStream_t& cs = cs_of[dev];
   if (!cs) PDB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   const int64_t win_slices = k::kSellSigma / k::kSellC;
   const int64_t nwin = (a.n + k::kSellSigma - 1) / k::kSellSigma;
