@@ -147,7 +147,7 @@ PDB_API void pdb_report_free(pdb_report rep);
  * Not part of this build (the paper's CSV study
  * drivers are outside the hot path).  The symbols exist so a host links;
  * every call returns PDB_ERR_INTERNAL with pdb_last_error() =
- * "<name>: experiment drivers are not part of this build ..." -- distinguishable
+ * "<name> is outside the B200 hot path of this build (...)" -- distinguishable
  * from a real internal failure by that message.  pdb_export_matrix is built. */
 PDB_API pdb_status pdb_run_experiment(const char* config_json, const char* out_csv);
 PDB_API pdb_status pdb_run_analyze(const char* config_json, const char* curve_csv, const char* histogram_csv);
