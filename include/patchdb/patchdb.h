@@ -270,6 +270,18 @@ PDB_API pdb_status pdb_relax_profile(pdb_matrix m, pdb_precond pc, const double*
  * zero without a SELL copy.  (No reference counterpart: bench.py's roofline
  * accounting.) */
 PDB_API pdb_status pdb_matrix_sell_info(pdb_matrix m, int64_t* out4);
+/* Half-storage ("mirror") residual layout (opt-in with
+ * PDB_SELL_MIRROR=1 at matrix creation): out[0] = 1 when in use, out[1] = values stored, out[2] = identity rows storing
+ * mirrored values, out[3] = class offsets; *why (may be null) = why the
+ * layout is not in use (empty when it is).  (No reference counterpart.) */
+PDB_API pdb_status pdb_matrix_mirror_info(pdb_matrix m, int64_t* out4, const char** why);
+/* Test hook, host only: builds the mirror layout of a CSR matrix and
+ * evaluates y = A x through it in the GPU kernel's order (no device needed).
+ * out[0] = built, out[1] = slices, out[2] = values stored, out[3] = class
+ * offsets, out[4] = classes, out[5] = identity rows storing mirrored values;
+ * y is untouched when not built (pdb_last_error says why). */
+PDB_API pdb_status pdb_debug_mirror_check(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                          const double* values, const double* x, double* y, int64_t* out6);
 /* Sweep-structure sizes: stored factors (n_p exact, m_p compressed), patches, patch size. */
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc);
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc);

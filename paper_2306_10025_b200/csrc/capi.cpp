@@ -635,6 +635,40 @@ PDB_API pdb_status pdb_matrix_sell_info(pdb_matrix m, int64_t* out4) {
   });
 }
 
+PDB_API pdb_status pdb_matrix_mirror_info(pdb_matrix m, int64_t* out4, const char** why) {
+  if (m == nullptr || out4 == nullptr) return arg_error("null argument");
+  return guarded([&] {
+    const DeviceCsr& a = m->a;
+    out4[0] = a.mirror ? 1 : 0;
+    out4[1] = a.mirror ? static_cast<int64_t>(a.sell_val.size()) : 0;
+    out4[2] = a.mirror ? a.mir_virtual : 0;
+    out4[3] = a.mirror ? static_cast<int64_t>(a.sell_tab.size()) : 0;
+    if (why) *why = a.mir_why.c_str();
+  });
+}
+
+PDB_API pdb_status pdb_debug_mirror_check(int64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                                          const double* values, const double* x, double* y, int64_t* out6) {
+  if (row_ptr == nullptr || out6 == nullptr || (n > 0 && (col_idx == nullptr || values == nullptr || x == nullptr ||
+                                                          y == nullptr)))
+    return arg_error("null argument");
+  return guarded([&] {
+    const HostCsr h = validated_csr(n, row_ptr, col_idx, values);
+    std::vector<int32_t> cls, tab, tstart;
+    MirrorHost M;
+    const bool classed = sell_classes(h, cls, tab, tstart);
+    const bool built = classed && build_mirror_host(h, cls, tab, tstart, k::kSellSigma, M);
+    out6[0] = built ? 1 : 0;
+    out6[1] = built ? M.nslices : 0;
+    out6[2] = built ? static_cast<int64_t>(M.val.size()) : 0;
+    out6[3] = built ? static_cast<int64_t>(tab.size()) : 0;
+    out6[4] = built ? static_cast<int64_t>(tstart.size()) - 1 : 0;
+    out6[5] = built ? M.virtual_rows : 0;
+    if (built) mirror_spmv_host(M, tab, tstart, x, y);
+    g_last_error = built ? "" : (classed ? M.why : std::string("rows do not share column patterns"));
+  });
+}
+
 PDB_API int64_t pdb_precond_stored_factors(pdb_precond pc) { return pc == nullptr ? 0 : pc->nf; }
 PDB_API int64_t pdb_precond_patch_count(pdb_precond pc) { return pc == nullptr ? 0 : pc->np; }
 PDB_API int64_t pdb_precond_patch_size(pdb_precond pc) { return pc == nullptr ? 0 : pc->ps; }

@@ -23,6 +23,27 @@ HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const doubl
 HostCsr download_csr(const DeviceCsr& d, cudaStream_t s);
 void spmv_device(const DeviceCsr& a, const double* x, double* y, cudaStream_t s);
 k::SpmvPlan plan_of(const DeviceCsr& a);  // SpMV launch plan (streaming partition when available)
+// Column-pattern classes of the SELL copy (every row's columns are row + one
+// of a few offset lists); false when the rows do not share patterns.
+bool sell_classes(const HostCsr& h, std::vector<int32_t>& cls, std::vector<int32_t>& tab, std::vector<int32_t>& tstart);
+
+// sell_mirror.cpp: the half-storage residual layout (see there).
+struct MirrorHost {
+  int64_t nslices = 0;
+  std::vector<int64_t> soff;       // per slice: value index of (slot 0, lane 0)
+  std::vector<int32_t> rows;       // per slice lane: row (-1: padding), length | (class + 1) << 16
+  std::vector<double> val;
+  std::vector<int32_t> clo;        // per class: lower (mirrored) entries
+  std::vector<int32_t> rbase;      // per row: value index of its slot 0
+  std::vector<int32_t> kslot;      // per class offset (tab index): 32 * slot of the mirrored value
+  std::vector<int64_t> win_slice;  // first slice per window (+ end)
+  int64_t virtual_rows = 0;
+  std::string why;                 // reason when not built
+};
+bool build_mirror_host(const HostCsr& h, const std::vector<int32_t>& cls, const std::vector<int32_t>& tab,
+                       const std::vector<int32_t>& tstart, int64_t sigma, MirrorHost& out);
+void mirror_spmv_host(const MirrorHost& m, const std::vector<int32_t>& tab, const std::vector<int32_t>& tstart,
+                      const double* x, double* y);
 HostCsr read_matrix_market_host(const std::string& path);
 void write_matrix_market_host(const HostCsr& a, const std::string& path);
 

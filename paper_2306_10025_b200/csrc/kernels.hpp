@@ -31,6 +31,14 @@ struct SpmvPlan {
   // all rows in column-pattern classes (see DeviceCsr): no column stream
   const int32_t* sell_tab = nullptr;
   const int32_t* sell_tstart = nullptr;
+  // half ("mirror") storage (sell_mirror.cpp): own slot t of slice s at
+  // sell_off[s] + 32 t + lane; lower entry m of a class-c row at
+  // mir_rbase[j] + mir_kslot[tstart[c] + m]
+  const int32_t* mir_clo = nullptr;
+  const int32_t* mir_rbase = nullptr;
+  const int32_t* mir_kslot = nullptr;
+  int mir_ntab = 0, mir_ncls = 0;
+  int64_t mir_nval = 0;  // values stored
 };
 constexpr int kSellC = 32;          // rows per SELL slice (one warp)
 constexpr int kSellSigma = 8192;    // sorting window (rows)

@@ -257,6 +257,190 @@ __global__ void __launch_bounds__(256, 1) residual_sell_kernel(int64_t nslices, 
   }
 }
 
+// -- half ("mirror") storage (sell_mirror.cpp) -------------------------------
+// Same warp-per-slice, lane-per-row scheme and the same per-row CSR-order
+// summation as residual_sell_kernel over the half-storage layout.  The class
+// tables (column offsets, and per lower entry 32 * the slot of the mirrored
+// value in the target row's storage) sit in shared memory.  Lower entries
+// first (CSR order): the target row j = i + offset gives both x[j] and
+// rbase[j] (same gather index), the value is sval[rbase[j] + kslot] -- a_ji,
+// stored once in row j, an L2 hit when j's warp streamed it shortly before.
+// Then the row's own upper entries stream from its slice block (slot t at
+// soff + 32 t + lane), prefetched into L2 in one bulk request at the start.
+// Bitwise the CSR residual.
+__device__ __forceinline__ double ld_na(const double* p) {  // no L1 allocation
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <int U>
+__global__ void __launch_bounds__(256, 1) residual_mirror_kernel(
+    int64_t nslices, const int64_t* __restrict__ soff, const int2* __restrict__ srow,
+    const double* __restrict__ sval, const int32_t* __restrict__ tab, const int32_t* __restrict__ kslot,
+    const int32_t* __restrict__ tstart, const int32_t* __restrict__ clo, int ntab, int ncls,
+    const int32_t* __restrict__ rbase, const double* __restrict__ x, const double* __restrict__ b,
+    double* __restrict__ r, double* __restrict__ block_sumsq, bool negate_b_absent, int pf,
+    const double* __restrict__ dotv, int64_t ahead, int64_t nval) {
+  extern __shared__ int32_t mirror_tab[];  // int2 {offset, 32 slot} [ntab], lower counts [ncls], starts [ncls + 1]
+  __shared__ double red[8];
+  int2* s_k = reinterpret_cast<int2*>(mirror_tab);
+  int32_t* s_lo = mirror_tab + 2 * ntab;
+  int32_t* s_ts = s_lo + ncls;
+  for (int q = threadIdx.x; q < ntab; q += blockDim.x) s_k[q] = make_int2(__ldg(tab + q), __ldg(kslot + q));
+  for (int q = threadIdx.x; q < ncls; q += blockDim.x) s_lo[q] = __ldg(clo + q);
+  for (int q = threadIdx.x; q <= ncls; q += blockDim.x) s_ts[q] = __ldg(tstart + q);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t sl = (int64_t)blockIdx.x * 8 + wib;
+  double sq = 0.0;
+  if (sl >= nslices) {
+    grid_dep_wait();
+    grid_dep_trigger();
+  }
+  if (sl < nslices) {
+    const int2 rl = __ldg(srow + sl * 32 + lane);
+    const bool live = rl.x >= 0;
+    const int len = live ? (rl.y & 0xFFFF) : 0;
+    const int c = live ? (rl.y >> 16) - 1 : 0;
+    const int lo = live ? s_lo[c] : 0;
+    const int own = len - lo;
+    const int M = (int)__reduce_max_sync(0xffffffffu, (unsigned)lo);
+    const int W = (int)__reduce_max_sync(0xffffffffu, (unsigned)own);
+    const int64_t o = __ldg(soff + sl);
+    // L2 prefetch: this slice's own block, and the block of slice sl + ahead
+    // (beyond the slices in flight) so that rows read as mirror targets
+    // later are L2-resident before their readers run
+    if (pf > 0 && lane == 0) {
+      if (W > 0 && sl < ahead)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + o), "r"((unsigned)W * 256u));
+      if (ahead > 0 && sl + ahead < nslices) {
+        const int64_t oa = __ldg(soff + sl + ahead);
+        const int64_t ob = sl + ahead + 1 < nslices ? __ldg(soff + sl + ahead + 1) : nval;
+        if (ob > oa) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + oa), "r"((unsigned)((ob - oa) * 8)));
+      }
+    }
+    const int2* kp = s_k + (live ? s_ts[c] : 0);
+    const int row = live ? rl.x : 0;
+    const int Mmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)(live ? lo : 0));
+    const double* vo = sval + o + lane;
+    const double bl = (live && b) ? __ldcs(b + rl.x) : 0.0;
+    // full step groups for the lanes' common counts (no predicates: a
+    // uniform slice runs only these), predicated single steps after
+    const int Wmin = (int)__reduce_min_sync(0xffffffffu, (unsigned)(live ? own : 0));
+    grid_dep_wait();  // x is the predecessor's (the scatter's) output
+    grid_dep_trigger();
+    double acc = 0.0;
+    // lower entries, CSR order: the target row j = i + offset gives x[j]
+    // and rbase[j] (same gather index); the value is sval[rbase[j] + kslot]
+    int m = 0;
+    for (; m + U <= Mmin; m += U) {
+      int j[U], ks[U], rb[U];
+      double xv[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int2 k = kp[m + u];
+        j[u] = row + k.x;
+        ks[u] = k.y;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        rb[u] = __ldg(rbase + j[u]);
+        xv[u] = __ldg(x + j[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_na(sval + (rb[u] + ks[u]));
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    for (; m < M; m += U) {  // remainder: predicated (inactive steps add +0 * +0, acc unchanged)
+      int j[U], ks[U], rb[U];
+      double xv[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int2 k = m + u < lo ? kp[m + u] : make_int2(0, 0);
+        j[u] = row + k.x;
+        ks[u] = k.y;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        rb[u] = m + u < lo ? __ldg(rbase + j[u]) : 0;
+        xv[u] = m + u < lo ? __ldg(x + j[u]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = m + u < lo ? ld_na(sval + (rb[u] + ks[u])) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    const int2* ku = kp + lo;
+    int t = 0;
+    for (; t + U <= Wmin; t += U) {
+      double xv[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = ld_na(vo + 32 * (t + u));
+        xv[u] = __ldg(x + (row + ku[t + u].x));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    for (; t < W; t += U) {
+      double xv[U], v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        v[u] = t + u < own ? ld_na(vo + 32 * (t + u)) : 0.0;
+        xv[u] = t + u < own ? __ldg(x + (row + ku[t + u].x)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
+    }
+    if (live) {
+      const double rv = b ? __dsub_rn(bl, acc) : (negate_b_absent ? -acc : acc);
+      r[rl.x] = rv;
+      sq += rv * (dotv ? dotv[rl.x] : rv);
+    }
+  }
+  if (block_sumsq) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+    if (lane == 0) red[wib] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q];
+      block_sumsq[blockIdx.x] = t;
+    }
+  }
+}
+
+inline size_t mirror_smem(int ntab, int ncls) { return (size_t)(2 * ntab + 2 * ncls + 1) * sizeof(int32_t); }
+
+// opt the mirror kernels into dynamic shared memory above 48 KB when the
+// class tables need it (once per device and instance)
+template <class K>
+void mirror_smem_attr(K kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  struct Done {
+    const void* f;
+    int dev;
+    size_t bytes;
+  };
+  static thread_local Done done[16];
+  static thread_local int ndone = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* f = reinterpret_cast<const void*>(kern);
+  for (int i = 0; i < ndone; ++i)
+    if (done[i].f == f && done[i].dev == dev) {
+      if (done[i].bytes >= bytes) return;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      done[i].bytes = bytes;
+      return;
+    }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (ndone < 16) done[ndone++] = {f, dev, bytes};
+}
+
 __global__ void finish_sum_kernel(const double* __restrict__ partials, int count, double* out, bool take_sqrt) {
   __shared__ double red[1024];
   double t = 0.0;
@@ -288,6 +472,22 @@ void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const in
     // L2 bulk prefetch one step group ahead (PDB_SELL_PF; measured best at 1)
     const char* pfe = getenv("PDB_SELL_PF");
     const int pf = pfe ? atoi(pfe) : 1;
+    if (p.mir_rbase) {
+      // PDB_MIRROR_U (A/B): steps in flight per lane, 4 (default: 4 blocks
+      // per SM at 64 registers, measured best) or 8
+      const char* ue = getenv("PDB_MIRROR_U");
+      auto kern = ue && atoi(ue) == 8 ? residual_mirror_kernel<8> : residual_mirror_kernel<4>;
+      const size_t sm = mirror_smem(p.mir_ntab, p.mir_ncls);
+      mirror_smem_attr(kern, sm);
+      // PDB_MIRROR_AHEAD: slices between a warp's slice and the one whose
+      // block it prefetches (0: only its own block)
+      const char* ae = getenv("PDB_MIRROR_AHEAD");
+      const int64_t ahead = ae ? atoll(ae) : 2048;
+      launch_pdl(kern, dim3((unsigned)p.blocks), dim3(256), sm, s, p.nslices, p.sell_off, sr, p.sell_val, p.sell_tab,
+                 p.mir_kslot, p.sell_tstart, p.mir_clo, p.mir_ntab, p.mir_ncls, p.mir_rbase, x, b, r, sumsq, negate, pf,
+                 dotv, ahead, p.mir_nval);
+      return;
+    }
     if (p.sell_tab) {
       const char* ue = getenv("PDB_SELL_CLS_U");
       if (ue && atoi(ue) == 16)
@@ -371,7 +571,13 @@ void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x,
                      cudaStream_t s) {
   if (s1 <= s0 || p.version != 9) return;
   const int2* sr = reinterpret_cast<const int2*>(p.sell_row) + s0 * 32;
-  if (p.sell_tab)
+  if (p.mir_rbase) {
+    const size_t sm = mirror_smem(p.mir_ntab, p.mir_ncls);
+    mirror_smem_attr(residual_mirror_kernel<4>, sm);
+    residual_mirror_kernel<4><<<grid_for(s1 - s0, 8), 256, sm, s>>>(
+        s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_tab, p.mir_kslot, p.sell_tstart, p.mir_clo, p.mir_ntab,
+        p.mir_ncls, p.mir_rbase, x, b, r, nullptr, true, 1, nullptr, int64_t{2048}, p.mir_nval);
+  } else if (p.sell_tab)
     residual_sell_kernel<8, true><<<grid_for(s1 - s0, 8), 256, 0, s>>>(
         s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x, b, r, nullptr, true, 1, nullptr, p.sell_tab,
         p.sell_tstart);

@@ -67,6 +67,109 @@ int num_sms() {  // of the current device (cached per device)
 // contiguous 256-byte (values) / 128-byte (columns) span.  Each lane sums its
 // row sequentially in CSR order -- no cross-lane reduction, and with
 // unfused multiply/add the residual is bitwise the reference spmv's.
+bool sell_classes(const HostCsr& h, std::vector<int32_t>& cls, std::vector<int32_t>& tab, std::vector<int32_t>& tstart) {
+  const int64_t n = h.n;
+  cls.assign(static_cast<size_t>(n), -1);
+  tab.clear();
+  tstart.assign(1, 0);
+  if (n == 0) return false;
+  const int64_t nwin = (n + k::kSellSigma - 1) / k::kSellSigma;
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  auto len = [&](int64_t i) { return h.row_ptr[static_cast<size_t>(i + 1)] - h.row_ptr[static_cast<size_t>(i)]; };
+  auto par = [&](auto&& body) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+      pool.emplace_back([&, t] {
+        for (int64_t w = nwin * t / T; w < nwin * (t + 1) / T; ++w) body(w);
+      });
+    for (auto& th : pool) th.join();
+  };
+  int64_t max_len = 0;
+  for (int64_t i = 0; i < n; ++i) max_len = std::max<int64_t>(max_len, len(i));
+  if (max_len > 0xFFFF) return false;
+  std::vector<uint64_t> hash(static_cast<size_t>(n));
+  par([&](int64_t w) {
+    const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
+    for (int64_t i = r0; i < r1; ++i) {
+      uint64_t x = 1469598103934665603ull ^ static_cast<uint64_t>(len(i));
+      for (int64_t p = h.row_ptr[static_cast<size_t>(i)]; p < h.row_ptr[static_cast<size_t>(i + 1)]; ++p) {
+        x ^= static_cast<uint64_t>(static_cast<uint32_t>(h.col[static_cast<size_t>(p)] - static_cast<int32_t>(i)));
+        x *= 1099511628211ull;
+      }
+      hash[static_cast<size_t>(i)] = x;
+    }
+  });
+  auto same = [&](int64_t a, int64_t b) {
+    const int64_t la = len(a);
+    if (la != len(b)) return false;
+    const int32_t* ca = h.col.data() + h.row_ptr[static_cast<size_t>(a)];
+    const int32_t* cb = h.col.data() + h.row_ptr[static_cast<size_t>(b)];
+    for (int64_t j = 0; j < la; ++j)
+      if (ca[j] - static_cast<int32_t>(a) != cb[j] - static_cast<int32_t>(b)) return false;
+    return true;
+  };
+  std::unordered_map<uint64_t, int32_t> pid;
+  std::vector<int64_t> rep;
+  for (int64_t i = 0; i < n; ++i) {
+    auto it = pid.find(hash[static_cast<size_t>(i)]);
+    if (it == pid.end()) {
+      // a lattice has a handful of patterns; past n/8 of them (or a 4 MB
+      // offset table) the rows do not share patterns: explicit columns
+      if (static_cast<int64_t>(rep.size()) >= std::max<int64_t>(1, std::min<int64_t>(4096, n / 8)) ||
+          tab.size() + static_cast<size_t>(len(i)) > (size_t{1} << 20)) {
+        cls.assign(static_cast<size_t>(n), -1);
+        tab.clear();
+        tstart.assign(1, 0);
+        return false;
+      }
+      it = pid.emplace(hash[static_cast<size_t>(i)], static_cast<int32_t>(rep.size())).first;
+      rep.push_back(i);
+      const int32_t* c = h.col.data() + h.row_ptr[static_cast<size_t>(i)];
+      for (int64_t j = 0; j < len(i); ++j) tab.push_back(c[j] - static_cast<int32_t>(i));
+      tstart.push_back(static_cast<int32_t>(tab.size()));
+    }
+    if (!same(rep[static_cast<size_t>(it->second)], i)) {
+      cls.assign(static_cast<size_t>(n), -1);
+      tab.clear();
+      tstart.assign(1, 0);
+      return false;
+    }
+    cls[static_cast<size_t>(i)] = it->second;
+  }
+  return true;
+}
+
+namespace {
+
+void upload_mirror(MirrorHost& M, const std::vector<int32_t>& tab, const std::vector<int32_t>& tstart, DeviceCsr& d,
+                   cudaStream_t s) {
+  d.sell_off.alloc(M.soff.size());
+  d.sell_off.upload(M.soff.data(), M.soff.size(), s);
+  d.sell_row.alloc(M.rows.size());
+  d.sell_row.upload(M.rows.data(), M.rows.size(), s);
+  d.sell_val.alloc(M.val.size());
+  d.sell_val.upload(M.val.data(), M.val.size(), s);
+  d.sell_col.alloc(1);
+  d.sell_tab.alloc(tab.size());
+  d.sell_tab.upload(tab.data(), tab.size(), s);
+  d.sell_tstart.alloc(tstart.size());
+  d.sell_tstart.upload(tstart.data(), tstart.size(), s);
+  d.sell_classes = static_cast<int64_t>(tstart.size()) - 1;
+  d.mir_clo.alloc(M.clo.size());
+  d.mir_clo.upload(M.clo.data(), M.clo.size(), s);
+  d.mir_rbase.alloc(M.rbase.size());
+  d.mir_rbase.upload(M.rbase.data(), M.rbase.size(), s);
+  d.mir_kslot.alloc(M.kslot.size());
+  d.mir_kslot.upload(M.kslot.data(), M.kslot.size(), s);
+  d.mir_virtual = M.virtual_rows;
+  d.win_slice = M.win_slice;
+  d.nslices = M.nslices;
+  d.mirror = true;
+  sync(s);  // the host vectors go out of scope after the copies
+}
+
+}  // namespace
+
 void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   const int64_t n = h.n;
   if (n == 0 || h.nnz() == 0) return;
@@ -84,62 +187,31 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
     for (auto& th : pool) th.join();
   };
   // ---- column-pattern classes: used only when every row falls into one
-  // (PDB_SELL_CLASSES=0 disables them)
-  std::vector<int32_t> cls(static_cast<size_t>(n), -1), tab, tstart(1, 0);
-  bool classed = false;
-  {
-    int64_t max_len = 0;
-    for (int64_t i = 0; i < n; ++i) max_len = std::max<int64_t>(max_len, len(i));
-    const char* ce = getenv("PDB_SELL_CLASSES");
-    if (!(ce && ce[0] == '0') && max_len <= 0xFFFF) {
-      std::vector<uint64_t> hash(static_cast<size_t>(n));
-      par([&](int64_t w) {
-        const int64_t r0 = w * k::kSellSigma, r1 = std::min(n, r0 + k::kSellSigma);
-        for (int64_t i = r0; i < r1; ++i) {
-          uint64_t x = 1469598103934665603ull ^ static_cast<uint64_t>(len(i));
-          for (int64_t p = h.row_ptr[static_cast<size_t>(i)]; p < h.row_ptr[static_cast<size_t>(i + 1)]; ++p) {
-            x ^= static_cast<uint64_t>(static_cast<uint32_t>(h.col[static_cast<size_t>(p)] - static_cast<int32_t>(i)));
-            x *= 1099511628211ull;
-          }
-          hash[static_cast<size_t>(i)] = x;
-        }
-      });
-      auto same = [&](int64_t a, int64_t b) {
-        const int64_t la = len(a);
-        if (la != len(b)) return false;
-        const int32_t* ca = h.col.data() + h.row_ptr[static_cast<size_t>(a)];
-        const int32_t* cb = h.col.data() + h.row_ptr[static_cast<size_t>(b)];
-        for (int64_t j = 0; j < la; ++j)
-          if (ca[j] - static_cast<int32_t>(a) != cb[j] - static_cast<int32_t>(b)) return false;
-        return true;
-      };
-      std::unordered_map<uint64_t, int32_t> pid;
-      std::vector<int64_t> rep;
-      classed = true;
-      for (int64_t i = 0; i < n && classed; ++i) {
-        auto it = pid.find(hash[static_cast<size_t>(i)]);
-        if (it == pid.end()) {
-          // a lattice has a handful of patterns; past n/8 of them (or a 4 MB
-          // offset table) the rows do not share patterns: explicit columns
-          if (static_cast<int64_t>(rep.size()) >= std::max<int64_t>(1, std::min<int64_t>(4096, n / 8)) ||
-              tab.size() + static_cast<size_t>(len(i)) > (size_t{1} << 20)) {
-            classed = false;
-            break;
-          }
-          it = pid.emplace(hash[static_cast<size_t>(i)], static_cast<int32_t>(rep.size())).first;
-          rep.push_back(i);
-          const int32_t* c = h.col.data() + h.row_ptr[static_cast<size_t>(i)];
-          for (int64_t j = 0; j < len(i); ++j) tab.push_back(c[j] - static_cast<int32_t>(i));
-          tstart.push_back(static_cast<int32_t>(tab.size()));
-        }
-        classed = same(rep[static_cast<size_t>(it->second)], i);
-        cls[static_cast<size_t>(i)] = it->second;
+  // (PDB_SELL_CLASSES=0 disables them); then the half-storage layout when
+  // its preconditions hold (PDB_SELL_MIRROR=0 disables it)
+  std::vector<int32_t> cls, tab, tstart;
+  const char* ce = getenv("PDB_SELL_CLASSES");
+  const bool classed = !(ce && ce[0] == '0') && sell_classes(h, cls, tab, tstart);
+  if (!classed) {
+    cls.assign(static_cast<size_t>(n), -1);
+    tab.clear();
+    tstart.assign(1, 0);
+  }
+  d.mirror = false;
+  d.mir_why = classed ? "" : "rows do not share column patterns";
+  if (classed) {
+    // opt-in (capacity mode): half the residual bytes, but measured slower
+    // than the plain classed copy on B200
+    const char* me = getenv("PDB_SELL_MIRROR");
+    if (!(me && me[0] == '1')) {
+      d.mir_why = "not requested (PDB_SELL_MIRROR=1)";
+    } else {
+      MirrorHost M;
+      if (build_mirror_host(h, cls, tab, tstart, k::kSellSigma, M)) {
+        upload_mirror(M, tab, tstart, d, s);
+        return;
       }
-    }
-    if (!classed) {
-      std::fill(cls.begin(), cls.end(), -1);
-      tab.clear();
-      tstart.assign(1, 0);
+      d.mir_why = M.why;
     }
   }
   par([&](int64_t w) {
@@ -208,6 +280,7 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
     d.sell_tstart.upload(tstart.data(), tstart.size(), s);
   }
   d.nslices = ns;
+  d.win_slice = win_slices;
   sync(s);
 }
 
@@ -258,6 +331,14 @@ k::SpmvPlan plan_of(const DeviceCsr& a) {
     if (a.sell_classes > 0) {
       p.sell_tab = a.sell_tab.get();
       p.sell_tstart = a.sell_tstart.get();
+    }
+    if (a.mirror) {
+      p.mir_clo = a.mir_clo.get();
+      p.mir_rbase = a.mir_rbase.get();
+      p.mir_kslot = a.mir_kslot.get();
+      p.mir_ntab = static_cast<int>(a.sell_tab.size());
+      p.mir_ncls = static_cast<int>(a.sell_classes);
+      p.mir_nval = static_cast<int64_t>(a.sell_val.size());
     }
     p.blocks = static_cast<int>((a.nslices + 7) / 8);
     return p;

@@ -49,6 +49,15 @@ struct DeviceCsr {
   // length | (class + 1) << 16 and the offsets sit in sell_tab.
   DevBuf<int32_t> sell_tab, sell_tstart;
   int64_t sell_classes = 0;  // 0: explicit columns
+  // Half ("mirror") storage (sell_mirror.cpp): slices as above but holding
+  // only each row's upper entries; lower entry m of a class-c row i reads
+  // value mir_rbase[j] + mir_kslot[tstart[c] + m], j = i + offset (the row
+  // that stores a_ji == a_ij).  mirror == false: the plain SELL layout above.
+  bool mirror = false;
+  DevBuf<int32_t> mir_clo, mir_rbase, mir_kslot;
+  int64_t mir_virtual = 0;
+  std::string mir_why;             // why the mirror layout is not in use
+  std::vector<int64_t> win_slice;  // first slice of each kSellSigma-row window (+ end)
 };
 
 // Two-level coarse correction of the combo preconditioner (reference

@@ -357,7 +357,7 @@ void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, 
   Scratch<double> db(std::max<size_t>(n, 1), s), dx(std::max<size_t>(n, 1), s);
   const k::SpmvPlan plan = plan_of(a);
   const char* e = getenv("PDB_PIPELINE");
-  const bool pipelined = plan.version == 9 && sweeps >= 1 && history_h == nullptr && n > 0 && !pc.coarse &&
+  const bool pipelined = plan.version == 9 && !a.win_slice.empty() && sweeps >= 1 && history_h == nullptr && n > 0 && !pc.coarse &&
                          !(e && std::string(e) == "0");
   if (!pipelined) {
     Scratch<double> dh(static_cast<size_t>(sweeps + 1), s);
@@ -377,7 +377,6 @@ void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, 
   require(dev < 64, Errc::internal, "device ordinal beyond the per-device caches");
   cudaStream_t& cs = cs_of[dev];
   if (!cs) PDB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  const int64_t win_slices = k::kSellSigma / k::kSellC;
   const int64_t nwin = (a.n + k::kSellSigma - 1) / k::kSellSigma;
   const int64_t chunks = std::min<int64_t>(8, nwin);
   std::vector<cudaEvent_t> ev(static_cast<size_t>(chunks + 2));
@@ -397,7 +396,7 @@ void relax_host(const DeviceCsr& a, const pdb_precond_s& pc, const double* b_h, 
   for (int64_t c = 0; c < chunks; ++c) {
     const int64_t w0 = nwin * c / chunks, w1 = nwin * (c + 1) / chunks;
     PDB_CUDA(cudaStreamWaitEvent(s, ev[static_cast<size_t>(c + 1)], 0));
-    k::residual_slices(plan, w0 * win_slices, std::min<int64_t>(plan.nslices, w1 * win_slices), dx.get(), db.get(),
+    k::residual_slices(plan, a.win_slice[static_cast<size_t>(w0)], a.win_slice[static_cast<size_t>(w1)], dx.get(), db.get(),
                        r.get(), s);
   }
   patch_stage(pc, r.get(), nullptr, sols.get(), s);

@@ -103,6 +103,8 @@ _sig("pdb_matrix_spmv_device", C.c_int, _P, C.c_void_p, C.c_void_p, C.c_void_p)
 _sig("pdb_matrix_free", None, _P)
 _sig("pdb_matrix_from_csr", C.c_int, C.c_int64, _I64, _I64, _D, C.POINTER(_P))
 _sig("pdb_matrix_sell_info", C.c_int, _P, _I64)
+_sig("pdb_matrix_mirror_info", C.c_int, _P, _I64, C.POINTER(C.c_char_p))
+_sig("pdb_debug_mirror_check", C.c_int, C.c_int64, _I64, _I64, _D, _D, _D, _I64)
 _sig("pdb_matrix_csr", C.c_int, _P, _I64, _I64, _D)
 _sig("pdb_problem_assemble", C.c_int, C.c_char_p, C.POINTER(_P))
 _sig("pdb_problem_ndofs", C.c_int64, _P)
@@ -253,6 +255,16 @@ class Matrix(_Handle):
         _check(_lib.pdb_matrix_sell_info(self._ptr, _ip(out)))
         return {"classes": int(out[0]), "col_entries": int(out[1]), "slices": int(out[2]),
                 "val_entries": int(out[3])}
+
+    def mirror_info(self) -> dict:
+        """Half-storage residual layout: in use or why
+        not, values stored, identity rows storing mirrored values, class
+        offsets."""
+        out = np.zeros(4, dtype=np.int64)
+        why = C.c_char_p()
+        _check(_lib.pdb_matrix_mirror_info(self._ptr, _ip(out), C.byref(why)))
+        return {"mirror": bool(out[0]), "values": int(out[1]), "virtual_rows": int(out[2]),
+                "class_offsets": int(out[3]), "why": (why.value or b"").decode()}
 
     def spmv(self, x) -> np.ndarray:
         x = _f64(x)
@@ -866,3 +878,25 @@ def compressibility_curve(m: Matrix, ps: "PatchSet", method: int, eps_grid) -> l
     ratios = np.zeros(len(g))
     _check(_lib.pdb_compressibility_curve(m.ptr, ps.ptr, int(method), _dp(g), len(g), _ip(sizes), _dp(ratios)))
     return [(float(e), int(n), float(r)) for e, n, r in zip(g, sizes, ratios)]
+
+
+def debug_mirror_check(csr, x):
+    """Test hook (host only, no device): build the half-storage residual
+    layout of a CSR matrix and evaluate y = A x through it in the GPU
+    kernel's order.  Returns (y or None when the layout does not apply,
+    stats dict with the reason)."""
+    rp, ci, v = (np.ascontiguousarray(a) for a in csr)
+    rp = rp.astype(np.int64)
+    ci = ci.astype(np.int64)
+    v = _f64(v)
+    x = _f64(x)
+    n = len(rp) - 1
+    y = np.full(n, np.nan)
+    out = np.zeros(6, dtype=np.int64)
+    _check(_lib.pdb_debug_mirror_check(n, _ip(rp), _ip(ci), _dp(v), _dp(x), _dp(y), _ip(out)))
+    stats = {"built": bool(out[0]), "slices": int(out[1]), "values": int(out[2]), "class_offsets": int(out[3]),
+             "classes": int(out[4]), "virtual_rows": int(out[5])}
+    if not out[0]:
+        stats["why"] = _lib.pdb_last_error().decode()
+        return None, stats
+    return y, stats
