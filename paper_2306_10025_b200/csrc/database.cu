@@ -115,6 +115,25 @@ struct EntryStore {
   }
 };
 
+// ------------------------------------------------ device compaction --
+struct Unmatched {
+  const int32_t* phi;
+  __device__ bool operator()(int32_t v) const { return phi[v] < 0; }
+};
+
+// out = the ids in[0..n) with phi[id] < 0, in order; returns their count.
+int64_t select_unmatched(const int32_t* in, int64_t n, const int32_t* phi, int32_t* out, int64_t* num,
+                         cudaStream_t s) {
+  size_t bytes = 0;
+  cub::DeviceSelect::If(nullptr, bytes, in, out, num, n, Unmatched{phi}, s);
+  Scratch<unsigned char> tmp(bytes, s);
+  cub::DeviceSelect::If(tmp.get(), bytes, in, out, num, n, Unmatched{phi}, s);
+  int64_t c = 0;
+  PDB_CUDA(cudaMemcpyAsync(&c, num, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return c;
+}
+
 // ---------------------------------------------------------------- greedy --
 // greedy_impl (compress.cpp:40-95), exact round-batched form:
 //   U = patches unmatched so far (ascending).  Each round takes the first B
@@ -142,31 +161,27 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
   BuildWork& work = out.work;
   DevBuf<int32_t> phi(static_cast<size_t>(np));
   PDB_CUDA(cudaMemsetAsync(phi.get(), 0xff, np * sizeof(int32_t), s));  // -1
-  DevBuf<double> best_d;
+  // temporaries are stream-ordered (Scratch): no device-wide synchronisation per buffer
+  Scratch<double> best_d(best_match ? static_cast<size_t>(np) : 0, s);
   if (best_match) {
-    best_d.alloc(static_cast<size_t>(np));
     std::vector<double> init(static_cast<size_t>(np), eps);
     h2d(best_d.get(), init, s);
   }
-  DevBuf<int32_t> creators(static_cast<size_t>(np));
-  DevBuf<int32_t> U(static_cast<size_t>(np)), U2(static_cast<size_t>(np));
+  Scratch<int32_t> creators(static_cast<size_t>(np), s);
+  Scratch<int32_t> U(static_cast<size_t>(np), s), U2(static_cast<size_t>(np), s);
   k::iota(np, U.get(), s);
   int64_t nu = np;
   EntryStore store;
   if (spectral) store.init(ps, std::min<int64_t>(np, 1024));
   const int64_t Bmax = spectral ? 128 : 1024;
-  DevBuf<double> D(static_cast<size_t>(Bmax * Bmax));
-  DevBuf<int32_t> luS_status(static_cast<size_t>(Bmax));
-  DevBuf<double> luS, luS_best(static_cast<size_t>(Bmax));
-  DevBuf<int32_t> pivS;
-  if (spectral) {
-    luS.alloc(static_cast<size_t>(Bmax * len));
-    pivS.alloc(static_cast<size_t>(Bmax * ps));
-  }
-  DevBuf<int32_t> entry_of(static_cast<size_t>(Bmax));
-  DevBuf<int64_t> state(3);
-  DevBuf<uint8_t> flags(static_cast<size_t>(np));
-  DevBuf<int32_t> all_ids(static_cast<size_t>(np));
+  Scratch<double> D(static_cast<size_t>(Bmax * Bmax), s);
+  Scratch<int32_t> luS_status(static_cast<size_t>(Bmax), s);
+  Scratch<double> luS(spectral ? static_cast<size_t>(Bmax * len) : 0, s);
+  Scratch<int32_t> pivS(spectral ? static_cast<size_t>(Bmax * ps) : 0, s);
+  Scratch<int32_t> entry_of(static_cast<size_t>(Bmax), s);
+  Scratch<int64_t> state(3, s);
+  Scratch<uint8_t> flags(static_cast<size_t>(np), s);
+  Scratch<int32_t> all_ids(static_cast<size_t>(np), s);
   k::iota(np, all_ids.get(), s);
   Scratch<unsigned long long> iters(1, s);
   PDB_CUDA(cudaMemsetAsync(iters.get(), 0, sizeof(unsigned long long), s));
@@ -196,6 +211,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
     const int64_t B = std::min(nu, Bmax);
     const int32_t* S = U.get();
     // distances among the batch
+    TraceScope tr_round("greedy round (batch pairs + resolve)", s);
     if (spectral) {
       std::string msg;
       std::vector<int32_t> st;
@@ -243,6 +259,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
       break;
     }
     // compare the remaining patches with the new entries [m, m_new)
+    TraceScope tr_scan("greedy scan", s);
     if (m_new > m) {
       int64_t nr = 0;
       int32_t* R = U2.get();
@@ -274,7 +291,7 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
         } else {
           // chunks of new entries; first-match drops matched patches between chunks
           const int64_t CH = 16;
-          DevBuf<double> dch(static_cast<size_t>(nrr * CH));
+          Scratch<double> dch(static_cast<size_t>(nrr * CH), s);
           int64_t live = nrr;
           for (int64_t c0 = m; c0 < m_new && live > 0; c0 += CH) {
             const int64_t ne = std::min(CH, m_new - c0);
@@ -309,16 +326,12 @@ bool greedy_build(const DevBuf<double>& mats, int64_t np, int ps, double eps, bo
     }
     m = m_new;
     // U <- unmatched patches among U[B..nu)
+    TraceScope tr_compact("greedy compact", s);
     const int64_t rest = nu - B;
     if (rest > 0) {
-      std::vector<int32_t> ph = d2h(phi.get(), static_cast<size_t>(np), s);
-      std::vector<int32_t> Uh = d2h(U.get() + B, static_cast<size_t>(rest), s);
-      std::vector<int32_t> keep;
-      keep.reserve(Uh.size());
-      for (int32_t v : Uh)
-        if (ph[static_cast<size_t>(v)] < 0) keep.push_back(v);
-      nu = static_cast<int64_t>(keep.size());
-      h2d(U.get(), keep, s);
+      // stream compaction on the device (order kept): U2 is free here
+      nu = select_unmatched(U.get() + B, rest, phi.get(), U2.get(), num_sel.get(), s);
+      PDB_CUDA(cudaMemcpyAsync(U.get(), U2.get(), nu * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     } else {
       nu = 0;
     }

@@ -82,12 +82,10 @@ void patch_solve(int64_t np, int ps, const int32_t* patches, const double* facto
 // Same product with explicit column-major inverses Binv (default sweep path).
 void patch_apply_inv(int64_t np, int ps, const int32_t* patches, const double* Binv, const int32_t* phi,
                      const double* r, const double* in_scale, double* sols, cudaStream_t s);
-// Padded slot-major inverse map (maxc in {1,2,4,8}) and the scatter/update using it;
+// Scatter/update through the compact inverse map (maxc = the largest slot count, <= 8);
 // the weight omega*(1/count) (sym: omega*sqrt(1/count)) is recomputed in-kernel.
-void build_inverse_pad(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, int32_t* pad,
-                       cudaStream_t s);
-void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const double* sols, double omega, bool sym,
-                        const double* x_in, double* z_out, double* x_out, cudaStream_t s);
+void scatter_update_csr(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
+                        double omega, bool sym, const double* x_in, double* z_out, double* x_out, cudaStream_t s);
 int grouped_tile(int ps);  // patches per grouped-apply tile
 // Cluster-grouped apply: tile t covers tile-order slots [tile_start[t], tile_start[t+1]) sharing entry
 // tile_entry[t]; tile_idx holds the patch DoF lists in tile order.  Solutions are written in patch
@@ -111,7 +109,7 @@ void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, c
 void gather_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
 void scatter_ints(int64_t count, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s);
 // bad = 1 when some omega_w[i] != omega * (1 / patches covering i) (the padded scatter's weight)
-void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
+void check_count_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
                        cudaStream_t s);
 void scatter_vals(int64_t count, const int32_t* idx, const double* src, double* dst, cudaStream_t s);
 // Binv (column-major) from row-major LU + pivots: column c = lu_solve(e_c).
@@ -143,6 +141,9 @@ void iota(int64_t n, int32_t* out, cudaStream_t s);
 void gather_patches(int64_t np, const int32_t* rows, const int32_t* order, const int64_t* rp, const int32_t* col,
                     int ps, int32_t* patches, cudaStream_t s);
 void cover_weights(int64_t n, int64_t np, int ps, const int32_t* patches, int32_t* cover, double* w, cudaStream_t s);
+void patch_fronts(int64_t np, int ps, const int32_t* patches, int32_t* fronts, cudaStream_t s);
+// flags[0] |= 1: two sorted keys equal; flags[1] |= 1: order is not the identity
+void front_order(int64_t np, const int32_t* key_sorted, const int32_t* order, int32_t* flags, cudaStream_t s);
 
 // ---- extract.cu : batched A_k = V_k A V_k^T ---------------------------------
 // ids == null: patches 0..count-1; else patches ids[0..count).

@@ -69,9 +69,11 @@ __global__ void __launch_bounds__(kL1Threads) l1_pairs_kernel(int64_t npat, cons
 }
 
 // ------------------------------------------------------- tiled L1 ----
-// One block = 64 patches x tiles of 32 entries; thread (tp, te) keeps the
-// 16 running sums of patches tp + 16 i and entries te + 8 j (i, j < 4) in
-// registers.  The patch and entry matrices are staged k-chunk by k-chunk
+// One block = 64 patches x tiles of TE entries (TE = 32, 64 or 128); thread
+// (tp, te) keeps the 4 x JB running sums of patches tp + 16 i and entries
+// te + (TE / JB) j (i < 4, j < JB) in registers.  The patch tile is staged
+// once per entry tile, so its traffic (the patch matrices exceed L2 at
+// config 3) falls as 1 / TE.  The patch and entry matrices are staged k-chunk by k-chunk
 // (32 entries of each matrix, 8-byte cp.async, double-buffered) into shared
 // memory rows of odd stride, so every load of the inner loop is a
 // bank-conflict-free broadcast and each staged value feeds 4 (patch) or 8
@@ -79,8 +81,16 @@ __global__ void __launch_bounds__(kL1Threads) l1_pairs_kernel(int64_t npat, cons
 // from 0.0 with |a - b| (dense.cpp:192-197), so distances are bitwise the
 // sequential kernel's.  Modes: all pair distances, the greedy first-/best-
 // match scan (compress.cpp:63-83), the k-means argmin (compress.cpp:154-160).
-constexpr int kTP = 64, kTE = 32, kTK = 32, kTL = kTK + 1, kTThreads = 128;
-constexpr size_t kTStage = (size_t)(kTP + kTE) * kTL;  // doubles per stage
+constexpr int kTP = 64, kTK = 32, kTL = kTK + 1;
+template <int TE>
+struct L1Tile {
+  static constexpr int JB = TE == 32 ? 4 : 8;      // entries per thread
+  static constexpr int EL = TE / JB;               // entry lanes
+  static constexpr int NT = 16 * EL;               // threads: 16 patch lanes x EL
+  static constexpr size_t STAGE = (size_t)(kTP + TE) * kTL;  // doubles per stage
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(double);
+  static_assert(2 * STAGE >= (size_t)kTP * (TE + 1), "epilogue tile must fit stage memory");
+};
 enum L1Mode { kL1Pairs = 0, kL1Scan = 1, kL1Argmin = 2 };
 
 struct L1Args {
@@ -116,13 +126,15 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
 
-template <int Mode>
-__global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
+template <int Mode, int TE>
+__global__ void __launch_bounds__(L1Tile<TE>::NT) l1_tile_kernel(L1Args a) {
+  constexpr int kTE = TE, JB = L1Tile<TE>::JB, EL = L1Tile<TE>::EL, kTThreads = L1Tile<TE>::NT;
+  constexpr size_t kTStage = L1Tile<TE>::STAGE;
   extern __shared__ double sm[];  // 2 stages [kTP + kTE][kTL]; the epilogue tile aliases stage 0
   __shared__ const double* psrc[kTP];
   __shared__ const double* esrc[kTE];
   __shared__ int32_t pme[kTP];
-  const int t = threadIdx.x, tp = t >> 3, te = t & 7;
+  const int t = threadIdx.x, tp = t / EL, te = t % EL;
   const int64_t p0 = (int64_t)blockIdx.x * kTP;
   const int len = a.len;
   if (t < kTP) {
@@ -177,11 +189,11 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    double acc[4][4];
+    double acc[4][JB];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      for (int j = 0; j < JB; ++j) acc[i][j] = 0.0;
     issue(0);
     for (int c = 0; c < nchunk; ++c) {
       if (c + 1 < nchunk) {
@@ -196,15 +208,15 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
       const int qn = min(kTK, len - c * kTK);
 #pragma unroll 4
       for (int k = 0; k < qn; ++k) {
-        double av[4], bv[4];
+        double av[4], bv[JB];
 #pragma unroll
         for (int i = 0; i < 4; ++i) av[i] = A[(tp + 16 * i) * kTL + k];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = B[(te + 8 * j) * kTL + k];
+        for (int j = 0; j < JB; ++j) bv[j] = B[(te + EL * j) * kTL + k];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
+          for (int j = 0; j < JB; ++j) acc[i][j] = __dadd_rn(acc[i][j], fabs(__dsub_rn(av[i], bv[j])));
       }
       __syncthreads();  // the stage is refilled by issue(c + 2)
     }
@@ -215,8 +227,8 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
         const int64_t g = p0 + tp + 16 * i;
         if (g >= a.npat) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int e = te + 8 * j;
+        for (int j = 0; j < JB; ++j) {
+          const int e = te + EL * j;
           if (e < ne) a.d[g * ld + (et0 - a.e0) + e] = acc[i][j];
         }
       }
@@ -228,7 +240,7 @@ __global__ void __launch_bounds__(kTThreads) l1_tile_kernel(L1Args a) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) D[(tp + 16 * i) * (kTE + 1) + te + 8 * j] = acc[i][j];
+      for (int j = 0; j < JB; ++j) D[(tp + 16 * i) * (kTE + 1) + te + EL * j] = acc[i][j];
     __syncthreads();
     if (t < kTP && !done) {
       const double* Dr = D + t * (kTE + 1);
@@ -311,11 +323,11 @@ __global__ void l1_scan_reduce_kernel(int64_t npat, int gy, const int32_t* __res
   phi[me] = cj;
 }
 
-template <int Mode>
-void l1_tile_launch(const L1Args& a, cudaStream_t s) {
-  const size_t smem = 2 * kTStage * sizeof(double);
-  static_assert(2 * kTStage >= (size_t)kTP * (kTE + 1), "epilogue tile must fit stage memory");
-  if (smem > 48 * 1024) cudaFuncSetAttribute(l1_tile_kernel<Mode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int Mode, int TE>
+void l1_tile_launch_te(const L1Args& a, cudaStream_t s) {
+  constexpr int kTE = TE, NT = L1Tile<TE>::NT;
+  constexpr size_t smem = L1Tile<TE>::SMEM;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(l1_tile_kernel<Mode, TE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   unsigned gy = 1;
   if (Mode == kL1Pairs) {
     // enough blocks to fill the GPU when the patch count is small (greedy batches: 1024 x 1024)
@@ -336,7 +348,7 @@ void l1_tile_launch(const L1Args& a, cudaStream_t s) {
         b.chunk = chunk;
         PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.part_j), (size_t)gys * a.npat * sizeof(int32_t), s));
         PDB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&b.part_d), (size_t)gys * a.npat * sizeof(double), s));
-        l1_tile_kernel<Mode><<<dim3(grid_for(a.npat, kTP), (unsigned)gys), kTThreads, smem, s>>>(b);
+        l1_tile_kernel<Mode, TE><<<dim3(grid_for(a.npat, kTP), (unsigned)gys), NT, smem, s>>>(b);
         l1_scan_reduce_kernel<<<grid_for(a.npat, 256), 256, 0, s>>>(a.npat, gys, a.pid, a.best_match, b.part_j,
                                                                      b.part_d, a.phi, a.best_d);
         PDB_CUDA(cudaFreeAsync(b.part_j, s));
@@ -345,7 +357,23 @@ void l1_tile_launch(const L1Args& a, cudaStream_t s) {
       }
     }
   }
-  l1_tile_kernel<Mode><<<dim3(grid_for(a.npat, kTP), gy), kTThreads, smem, s>>>(a);
+  l1_tile_kernel<Mode, TE><<<dim3(grid_for(a.npat, kTP), gy), NT, smem, s>>>(a);
+}
+
+// Entry-tile width: PDB_L1_TE = 32 / 64 / 128 (A/B runs); 64 by default (config-3 1 % greedy
+// build: 22.5 / 20.1 / 20.9 ms; the scan is FP64-pipe bound at 59 % with TE = 32, ncu).
+template <int Mode>
+void l1_tile_launch(const L1Args& a, cudaStream_t s) {
+  static const int te = [] {
+    const char* e = getenv("PDB_L1_TE");
+    return e ? atoi(e) : 64;
+  }();
+  if (te == 128)
+    l1_tile_launch_te<Mode, 128>(a, s);
+  else if (te == 64)
+    l1_tile_launch_te<Mode, 64>(a, s);
+  else
+    l1_tile_launch_te<Mode, 32>(a, s);
 }
 
 bool l1_tiled_enabled() {  // PDB_L1_TILED=0: the thread-per-patch kernels below (A/B runs, tests)

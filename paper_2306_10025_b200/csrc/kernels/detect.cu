@@ -123,6 +123,23 @@ __global__ void weights_kernel(int64_t n, const int32_t* __restrict__ cover, dou
   if (i < n) w[i] = cover[i] > 0 ? 1.0 / (double)cover[i] : 0.0;
 }
 
+// fronts[e] = patches[e * ps] (the first, smallest column of patch e)
+__global__ void fronts_kernel(int64_t np, int ps, const int32_t* __restrict__ patches, int32_t* __restrict__ fronts) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < np) fronts[e] = patches[e * ps];
+}
+
+// Over the (front, e) pairs sorted by front: flags[0] |= 1 if two patches share
+// a front (the sort order is then the comparator's, not a unique one),
+// flags[1] |= 1 if the order is not the identity.
+__global__ void front_order_kernel(int64_t np, const int32_t* __restrict__ key_sorted,
+                                   const int32_t* __restrict__ order, int32_t* flags) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= np) return;
+  if (e + 1 < np && key_sorted[e] == key_sorted[e + 1]) atomicOr(flags, 1);
+  if (order[e] != e) atomicOr(flags + 1, 1);
+}
+
 inline unsigned grid_for(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 }  // namespace
@@ -153,6 +170,14 @@ void gather_patches(int64_t np, const int32_t* rows, const int32_t* order, const
                     int ps, int32_t* patches, cudaStream_t s) {
   const int64_t total = np * ps;
   if (total > 0) gather_patches_kernel<<<grid_for(total, 256), 256, 0, s>>>(np, rows, order, rp, col, ps, patches);
+}
+
+void patch_fronts(int64_t np, int ps, const int32_t* patches, int32_t* fronts, cudaStream_t s) {
+  if (np > 0) fronts_kernel<<<grid_for(np, 256), 256, 0, s>>>(np, ps, patches, fronts);
+}
+
+void front_order(int64_t np, const int32_t* key_sorted, const int32_t* order, int32_t* flags, cudaStream_t s) {
+  if (np > 0) front_order_kernel<<<grid_for(np, 256), 256, 0, s>>>(np, key_sorted, order, flags);
 }
 
 void cover_weights(int64_t n, int64_t np, int ps, const int32_t* patches, int32_t* cover, double* w, cudaStream_t s) {

@@ -8,7 +8,7 @@
 //   patch_apply_inv    one patch per sub-block with its explicit inverse (exact
 //                      mode, small databases); patch_solve: triangular solves
 //                      on the LU factors (PDB_APPLY=lu)
-//   scatter_update_pad x += omega W sum sols: owner-computes gather through the
+//   scatter_update_csr x += omega W sum sols: owner-computes gather through the
 //                      DoF -> (patch, slot) inverse map in ascending patch order,
 //                      the reference's serial scatter order (precond.cpp:81-86),
 //                      no atomics
@@ -196,25 +196,28 @@ __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, do
 
 constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
 
-// Solutions are written in patch order (sols[order[slot] * ps + i]).  R is
-// staged unpadded (patch p, local row k at p * ps + k), so the copy is a
-// flat, division-free loop; the B operand is masked to 0 for k >= ps (those
-// stage entries belong to the next patch), and the stage is zero-filled past
-// the tile's cnt * ps live values.
+// Solutions are written in patch order (sols[order[slot] * ps + i]).  Patch
+// p's residuals are staged at rk[p * SP + k] with SP = 4 KS (+4 when KS is
+// even), so the B-fragment loads of a half-warp (g = 0..3 or 4..7, tg = 0..3)
+// fall in 16 distinct 8-byte banks (a stage of stride ps costs a 2-way
+// conflict on every fragment load at ps = 25/27: config-3 apply 48.7 ->
+// 45 us).  Rows k >= ps are zero in the stage itself, so a zero A entry never
+// meets a neighbouring patch's (possibly non-finite) value.
 template <int MT, int KS>
 __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
-                                                                   const int32_t* __restrict__ tile_start,
-                                                                   const int32_t* __restrict__ idx,
-                                                                   const int32_t* __restrict__ order,
-                                                                   const double* __restrict__ frag,
-                                                                   const double* __restrict__ r,
-                                                                   const double* __restrict__ in_scale,
-                                                                   double* __restrict__ out) {
+                                                                      const int32_t* __restrict__ tile_start,
+                                                                      const int32_t* __restrict__ idx,
+                                                                      const int32_t* __restrict__ order,
+                                                                      const double* __restrict__ frag,
+                                                                      const double* __restrict__ r,
+                                                                      const double* __restrict__ in_scale,
+                                                                      double* __restrict__ out) {
   constexpr int NTH = MT * 32;
-  constexpr int TOT = kDmmaTile * KS * 4;  // >= 31 * ps + 4 * KS: every B-fragment read
+  constexpr int SP = KS * 4 + ((KS & 1) ? 0 : 4);
+  constexpr int TOT = kDmmaTile * SP;
   constexpr int ITER = (TOT + NTH - 1) / NTH;
   __shared__ double rk[TOT];
-  __shared__ int32_t ko[kDmmaTile];  // patch index of each tile column
+  __shared__ int32_t ko[kDmmaTile];
   const int t = blockIdx.x;
   const int f = __ldg(tile_entry + t);
   const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
@@ -224,13 +227,13 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
   const double* fa = frag + ((int64_t)f * MT + w) * (KS * 32) + lane;
 #pragma unroll
   for (int q = 0; q < KS; ++q) a[q] = __ldg(fa + q * 32);
-  const int live = cnt * ps;
   const int32_t* ti = idx + (int64_t)s0 * ps;
   int32_t gi[ITER];
 #pragma unroll
   for (int it = 0; it < ITER; ++it) {
     const int e = threadIdx.x + it * NTH;
-    gi[it] = e < live ? __ldg(ti + e) : -1;
+    const int p = e / SP, k = e - p * SP;
+    gi[it] = (e < TOT && p < cnt && k < ps) ? __ldg(ti + p * ps + k) : -1;
   }
   grid_dep_wait();  // r is the residual kernel's output
   grid_dep_trigger();
@@ -251,14 +254,9 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
   for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
     if (nt * 8 < cnt) {  // block-uniform
       double c0 = 0.0, c1 = 0.0;
-      const double* bp = rk + (nt * 8 + g) * ps + tg;
+      const double* bp = rk + (nt * 8 + g) * SP + tg;
 #pragma unroll
-      for (int q = 0; q < KS; ++q) {
-        // rows k >= ps of the last k-step belong to the next patch: mask them
-        // (a zero A entry times a non-finite neighbour value would be NaN)
-        const double bv = (q < KS - 1 || q * 4 + tg < ps) ? bp[q * 4] : 0.0;
-        dmma_m8n8k4(c0, c1, a[q], bv);
-      }
+      for (int q = 0; q < KS; ++q) dmma_m8n8k4(c0, c1, a[q], bp[q * 4]);
       const int p0 = nt * 8 + 2 * tg;
       if (row < ps) {
         if (p0 < cnt) out[(int64_t)ko[p0] * ps + row] = c0;
@@ -362,7 +360,7 @@ __global__ void shard_scatter_kernel(int64_t count, const int32_t* __restrict__ 
   if (x) x[d] = __dadd_rn(__dmul_rn(z, omega_w[d]), x[d]);  // the serial scatter's rounding
 }
 
-__global__ void check_pad_weights_kernel(int64_t n, double omega, const int32_t* __restrict__ inv_ptr,
+__global__ void check_count_weights_kernel(int64_t n, double omega, const int32_t* __restrict__ inv_ptr,
                                          const double* __restrict__ omega_w, int32_t* bad) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -397,66 +395,63 @@ __global__ void remap_inverse_kernel(int64_t count, int ps, const int32_t* __res
   inv[q] = slot_of[t / ps] * ps + t % ps;
 }
 
-// Scatter/update with the padded slot-major inverse map: slot c of DoF i is
-// inv_pad[c*n + i] (ascending patch order, -1 = empty), so all slot loads of
-// a DoF are independent and coalesced.  The overlap weight is recomputed
-// from the slot count exactly as compute_weights does (patch.cpp:12-20):
-// scale = omega * (1.0 / count) (or omega * sqrt(1.0 / count) for the
-// symmetric PCG weighting).
+// Scatter/update: DoF-parallel (owner computes) gather of a DoF's solution
+// slots through the inverse map inv_ptr / inv (slots sorted by patch: the
+// reference's serial scatter order, precond.cpp:81-86), no atomics.  The
+// overlap weight is recomputed from the slot count exactly as
+// compute_weights does (patch.cpp:12-20): scale = omega * (1.0 / count) (or
+// omega * sqrt(1.0 / count) for the symmetric PCG weighting); setup checks
+// that the patch set's weights are exactly that.  kScatterU DoFs per thread
+// (blockDim apart, so every load stays coalesced), the slot loads of a DoF
+// unrolled to MAXC and independent: all index, then all solution loads are
+// in flight together (the kernel is latency-bound on the idx -> sols chain).
+// (A padded slot-major map, 4 * MAXC bytes per DoF instead of 4 per slot,
+// measured no faster: 37.3 vs 36.4 us at config 3.)
 constexpr int kScatterU = 2;
 
 template <int MAXC>
-__global__ void scatter_update_pad_kernel(int64_t n, const int32_t* __restrict__ inv_pad,
-                                          const double* __restrict__ sols, double omega, bool sym,
-                                          const double* __restrict__ x_in, double* __restrict__ z_out,
-                                          double* __restrict__ x_out) {
-  // kScatterU DoFs per thread (blockDim apart, so every load stays
-  // coalesced): all index loads, then all solution / x loads are in flight
-  // together -- the kernel is latency-bound on the idx -> sols chain.
+__global__ void scatter_update_csr_kernel(int64_t n, const int32_t* __restrict__ inv_ptr,
+                                          const int32_t* __restrict__ inv, const double* __restrict__ sols,
+                                          double omega, bool sym, const double* __restrict__ x_in,
+                                          double* __restrict__ z_out, double* __restrict__ x_out) {
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kScatterU + threadIdx.x;
-  int32_t e[kScatterU][MAXC];
-  double v[kScatterU][MAXC], xi[kScatterU];
+  int32_t lo[kScatterU], cn[kScatterU];
+  double xi[kScatterU];
 #pragma unroll
   for (int u = 0; u < kScatterU; ++u) {
     const int64_t i = i0 + (int64_t)u * blockDim.x;
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c) e[u][c] = i < n ? __ldcs(inv_pad + (int64_t)c * n + i) : -1;
+    lo[u] = i < n ? __ldcs(inv_ptr + i) : 0;
+    cn[u] = i < n ? __ldcs(inv_ptr + i + 1) - lo[u] : 0;
     xi[u] = (x_out && i < n) ? __ldcs(x_in + i) : 0.0;
   }
+  int32_t e[kScatterU][MAXC];
+#pragma unroll
+  for (int u = 0; u < kScatterU; ++u)
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) e[u][c] = c < cn[u] ? __ldcs(inv + lo[u] + c) : -1;
   grid_dep_wait();  // sols is the apply kernel's output
   grid_dep_trigger();
+  double v[kScatterU][MAXC];
 #pragma unroll
-  for (int u = 0; u < kScatterU; ++u) {
+  for (int u = 0; u < kScatterU; ++u)
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) v[u][c] = e[u][c] >= 0 ? __ldg(sols + e[u][c]) : 0.0;
-  }
 #pragma unroll
   for (int u = 0; u < kScatterU; ++u) {
     const int64_t i = i0 + (int64_t)u * blockDim.x;
     if (i >= n) break;
     double z = 0.0;
-    int cnt = 0;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c)
-      if (e[u][c] >= 0) {
-        z += v[u][c];
-        ++cnt;
-      }
-    double w = cnt > 0 ? 1.0 / (double)cnt : 0.0;
+      if (c < cn[u]) z += v[u][c];
+    double w = cn[u] > 0 ? 1.0 / (double)cn[u] : 0.0;
     if (sym) w = sqrt(w);
-    z = __dmul_rn(z, omega * w);  // explicit: the shard scatter must round the same way
+    z = __dmul_rn(z, omega * w);
     if (z_out) z_out[i] = z;
     if (x_out) x_out[i] = __dadd_rn(z, xi[u]);
   }
 }
 
-__global__ void build_inverse_pad_kernel(int64_t n, int maxc, const int32_t* __restrict__ inv_ptr,
-                                         const int32_t* __restrict__ inv, int32_t* __restrict__ pad) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t lo = inv_ptr[i], hi = inv_ptr[i + 1];
-  for (int c = 0; c < maxc; ++c) pad[(int64_t)c * n + i] = lo + c < hi ? inv[lo + c] : -1;
-}
 
 // Column c of B^{-1} = lu_solve(LU, e_c) (dense.cpp:77-94 applied to unit
 // vectors).  Warp per factor, lanes over columns; the per-lane work vector
@@ -740,11 +735,11 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
                tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);
     return;
   }
-#define PDB_DMMA_CASE(M, K)                                                                                 \
-  if (mt == M && ks == K) {                                                                                 \
-    launch_pdl(patch_apply_dmma_kernel<M, K>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, tile_entry,   \
-               tile_start, tile_idx, order, frag, r, in_scale, sols);                                       \
-    return;                                                                                                 \
+#define PDB_DMMA_CASE(M, K)                                                                                   \
+  if (mt == M && ks == K) {                                                                                   \
+    launch_pdl(patch_apply_dmma_kernel<M, K>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, tile_entry,     \
+               tile_start, tile_idx, order, frag, r, in_scale, sols);                                         \
+    return;                                                                                                   \
   }
   PDB_DMMA_CASE(1, 1)
   PDB_DMMA_CASE(1, 2)
@@ -764,9 +759,9 @@ void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, c
                                                                     z_out, x);
 }
 
-void check_pad_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
+void check_count_weights(int64_t n, double omega, const int32_t* inv_ptr, const double* omega_w, int32_t* bad,
                        cudaStream_t s) {
-  if (n > 0) check_pad_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, inv_ptr, omega_w, bad);
+  if (n > 0) check_count_weights_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, omega, inv_ptr, omega_w, bad);
 }
 
 void scatter_ints(int64_t count, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s) {
@@ -785,22 +780,21 @@ void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, 
   if (count > 0) remap_inverse_kernel<<<grid_for(count, kBlock), kBlock, 0, s>>>(count, ps, slot_of, inv);
 }
 
-void build_inverse_pad(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, int32_t* pad,
-                       cudaStream_t s) {
-  if (n > 0) build_inverse_pad_kernel<<<grid_for(n, kBlock), kBlock, 0, s>>>(n, maxc, inv_ptr, inv, pad);
-}
-
-void scatter_update_pad(int64_t n, int maxc, const int32_t* inv_pad, const double* sols, double omega, bool sym,
-                        const double* x_in, double* z_out, double* x_out, cudaStream_t s) {
+void scatter_update_csr(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
+                        double omega, bool sym, const double* x_in, double* z_out, double* x_out, cudaStream_t s) {
   if (n <= 0) return;
   const unsigned g = grid_for(n, kBlock * kScatterU);
+#define PDB_CSR_CASE(M)                                                                                     \
+  launch_pdl(scatter_update_csr_kernel<M>, dim3(g), dim3(kBlock), 0, s, n, inv_ptr, inv, sols, omega, sym, \
+             x_in, z_out, x_out)
   switch (maxc) {
-    case 1: launch_pdl(scatter_update_pad_kernel<1>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
-    case 2: launch_pdl(scatter_update_pad_kernel<2>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 1: PDB_CSR_CASE(1); break;
+    case 2: PDB_CSR_CASE(2); break;
     case 3:
-    case 4: launch_pdl(scatter_update_pad_kernel<4>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
-    default: launch_pdl(scatter_update_pad_kernel<8>, dim3(g), dim3(kBlock), 0, s, n, inv_pad, sols, omega, sym, x_in, z_out, x_out); break;
+    case 4: PDB_CSR_CASE(4); break;
+    default: PDB_CSR_CASE(8); break;
   }
+#undef PDB_CSR_CASE
 }
 
 void invert_factors(int64_t nf, int ps, const double* lu, const int32_t* piv, double* inv, cudaStream_t s) {

@@ -145,8 +145,7 @@ struct pdb_precond_s {
   pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
   int ntiles = 0, max_tile = 0;
   pdb::DevBuf<double> frag;  // inverses in DMMA A-fragment order (tensor-core grouped apply), when allocated
-  pdb::DevBuf<int32_t> inv_pad;  // slot-major padded inverse map (maxc_pad slots), when maxc_pad > 0
-  int maxc_pad = 0;
+  int maxc = 0;  // largest slot count when <= 8 and the weights are 1/count: the templated scatter
   pdb::DevBuf<int32_t> inv_ptr;
   pdb::DevBuf<int32_t> inv;
   std::shared_ptr<pdb::CoarseDev> coarse;  // combo preconditioner only

@@ -31,7 +31,8 @@ void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStrea
   require(ps >= 2, Errc::invalid_argument, "patch size must be >= 2");
   require_device();
   const Index n = a.n;
-  DevBuf<uint8_t> cand(static_cast<size_t>(std::max<Index>(n, 1)));
+  // temporaries are stream-ordered (Scratch): no device-wide synchronisation per buffer
+  Scratch<uint8_t> cand(static_cast<size_t>(std::max<Index>(n, 1)), s);
   Scratch<int32_t> any(1, s);
   PDB_CUDA(cudaMemsetAsync(any.get(), 0, sizeof(int32_t), s));
   k::detect_candidates(n, a.row_ptr.get(), ps, cand.get(), any.get(), s);
@@ -42,28 +43,28 @@ void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStrea
   if (!any_h) fail(Errc::no_patches_found, "no row has exactly " + std::to_string(ps) + " stored entries");
 
   // candidate rows, ascending
-  DevBuf<int32_t> ids(static_cast<size_t>(n));
+  Scratch<int32_t> ids(static_cast<size_t>(n), s);
   k::iota(n, ids.get(), s);
-  DevBuf<int32_t> rows(static_cast<size_t>(n));
+  Scratch<int32_t> rows(static_cast<size_t>(n), s);
   int64_t nc = 0;
   select_flagged(ids.get(), cand.get(), rows.get(), n, nc, s);
 
   // consistency + hash
-  DevBuf<uint8_t> consistent(static_cast<size_t>(nc));
-  DevBuf<uint64_t> hash(static_cast<size_t>(nc));
+  Scratch<uint8_t> consistent(static_cast<size_t>(nc), s);
+  Scratch<uint64_t> hash(static_cast<size_t>(nc), s);
   k::detect_consistency(nc, rows.get(), a.row_ptr.get(), a.col.get(), cand.get(), static_cast<int>(ps),
                         consistent.get(), hash.get(), s);
   PDB_LAUNCH_CHECK();
-  DevBuf<int32_t> crow(static_cast<size_t>(nc));
-  DevBuf<uint64_t> chash(static_cast<size_t>(nc));
+  Scratch<int32_t> crow(static_cast<size_t>(nc), s);
+  Scratch<uint64_t> chash(static_cast<size_t>(nc), s);
   int64_t ncc = 0, tmpc = 0;
   select_flagged(rows.get(), consistent.get(), crow.get(), nc, ncc, s);
   select_flagged(hash.get(), consistent.get(), chash.get(), nc, tmpc, s);
   if (ncc == 0) fail(Errc::no_patches_found, "no consistent patch candidates detected");
 
   // dedupe: sort positions by hash (stable radix sort keeps ascending positions within a run)
-  DevBuf<int32_t> pos(static_cast<size_t>(ncc)), pos_sorted(static_cast<size_t>(ncc));
-  DevBuf<uint64_t> hash_sorted(static_cast<size_t>(ncc));
+  Scratch<int32_t> pos(static_cast<size_t>(ncc), s), pos_sorted(static_cast<size_t>(ncc), s);
+  Scratch<uint64_t> hash_sorted(static_cast<size_t>(ncc), s);
   k::iota(ncc, pos.get(), s);
   {
     size_t bytes = 0;
@@ -73,38 +74,63 @@ void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStrea
     cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, chash.get(), hash_sorted.get(), pos.get(), pos_sorted.get(),
                                     static_cast<int>(ncc), 0, 64, s);
   }
-  DevBuf<uint8_t> keep(static_cast<size_t>(ncc));
+  Scratch<uint8_t> keep(static_cast<size_t>(ncc), s);
   k::detect_dedupe(ncc, hash_sorted.get(), pos_sorted.get(), crow.get(), a.row_ptr.get(), a.col.get(),
                    static_cast<int>(ps), keep.get(), s);
   PDB_LAUNCH_CHECK();
-  DevBuf<int32_t> emitted(static_cast<size_t>(ncc));
+  Scratch<int32_t> emitted(static_cast<size_t>(ncc), s);
   int64_t np = 0;
   select_flagged(crow.get(), keep.get(), emitted.get(), ncc, np, s);
 
-  // fronts -> std::sort by front with the reference comparator (patch.cpp:82-83)
-  DevBuf<int32_t> order(static_cast<size_t>(np));
+  // fronts -> std::sort by front with the reference comparator (patch.cpp:82-83).
+  // When the fronts are distinct the sorted order is unique, so a device radix
+  // sort gives it; only fronts shared by two patches need libstdc++'s own
+  // (unstable) std::sort on the host.
+  Scratch<int32_t> order(static_cast<size_t>(np), s);
   k::iota(np, order.get(), s);
   DevBuf<int32_t> patches(static_cast<size_t>(np * ps));
   k::gather_patches(np, emitted.get(), order.get(), a.row_ptr.get(), a.col.get(), static_cast<int>(ps),
                     patches.get(), s);
   PDB_LAUNCH_CHECK();
-  std::vector<int32_t> fronts(static_cast<size_t>(np));
-  PDB_CUDA(cudaMemcpy2DAsync(fronts.data(), sizeof(int32_t), patches.get(), sizeof(int32_t) * ps, sizeof(int32_t),
-                             static_cast<size_t>(np), cudaMemcpyDeviceToHost, s));
-  sync(s);
-  std::vector<std::pair<int64_t, int32_t>> keyed(static_cast<size_t>(np));
-  for (int64_t e = 0; e < np; ++e) keyed[static_cast<size_t>(e)] = {fronts[static_cast<size_t>(e)], static_cast<int32_t>(e)};
-  std::sort(keyed.begin(), keyed.end(),
-            [](const std::pair<int64_t, int32_t>& x, const std::pair<int64_t, int32_t>& y) { return x.first < y.first; });
-  bool identity = true;
-  std::vector<int32_t> ord(static_cast<size_t>(np));
-  for (int64_t e = 0; e < np; ++e) {
-    ord[static_cast<size_t>(e)] = keyed[static_cast<size_t>(e)].second;
-    identity = identity && ord[static_cast<size_t>(e)] == e;
+  Scratch<int32_t> fronts(static_cast<size_t>(np), s), fronts_sorted(static_cast<size_t>(np), s),
+      order_sorted(static_cast<size_t>(np), s), flags(2, s);
+  k::patch_fronts(np, static_cast<int>(ps), patches.get(), fronts.get(), s);
+  {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, fronts.get(), fronts_sorted.get(), order.get(),
+                                    order_sorted.get(), static_cast<int>(np), 0, 32, s);
+    Scratch<unsigned char> tmp(bytes, s);
+    cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, fronts.get(), fronts_sorted.get(), order.get(),
+                                    order_sorted.get(), static_cast<int>(np), 0, 32, s);
   }
-  if (!identity) {
-    order.upload(ord.data(), ord.size(), s);
-    k::gather_patches(np, emitted.get(), order.get(), a.row_ptr.get(), a.col.get(), static_cast<int>(ps),
+  flags.zero();
+  k::front_order(np, fronts_sorted.get(), order_sorted.get(), flags.get(), s);
+  PDB_LAUNCH_CHECK();
+  int32_t fl[2] = {0, 0};
+  PDB_CUDA(cudaMemcpyAsync(fl, flags.get(), sizeof(fl), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (fl[0]) {  // shared fronts: the reference comparator's order, on the host
+    std::vector<int32_t> fh(static_cast<size_t>(np));
+    fronts.download(fh.data(), fh.size());
+    sync(s);
+    std::vector<std::pair<int64_t, int32_t>> keyed(static_cast<size_t>(np));
+    for (int64_t e = 0; e < np; ++e) keyed[static_cast<size_t>(e)] = {fh[static_cast<size_t>(e)], static_cast<int32_t>(e)};
+    std::sort(keyed.begin(), keyed.end(),
+              [](const std::pair<int64_t, int32_t>& x, const std::pair<int64_t, int32_t>& y) { return x.first < y.first; });
+    bool identity = true;
+    std::vector<int32_t> ord(static_cast<size_t>(np));
+    for (int64_t e = 0; e < np; ++e) {
+      ord[static_cast<size_t>(e)] = keyed[static_cast<size_t>(e)].second;
+      identity = identity && ord[static_cast<size_t>(e)] == e;
+    }
+    if (!identity) {
+      order.upload(ord.data(), ord.size());
+      k::gather_patches(np, emitted.get(), order.get(), a.row_ptr.get(), a.col.get(), static_cast<int>(ps),
+                        patches.get(), s);
+      PDB_LAUNCH_CHECK();
+    }
+  } else if (fl[1]) {
+    k::gather_patches(np, emitted.get(), order_sorted.get(), a.row_ptr.get(), a.col.get(), static_cast<int>(ps),
                       patches.get(), s);
     PDB_LAUNCH_CHECK();
   }
@@ -113,8 +139,8 @@ void detect_patches(const DeviceCsr& a, Index ps, pdb_patchset_s& out, cudaStrea
   out.np = np;
   out.ps = ps;
   out.weights.alloc(static_cast<size_t>(std::max<Index>(n, 1)));
-  DevBuf<int32_t> cover(static_cast<size_t>(std::max<Index>(n, 1)));
-  cover.zero(s);
+  Scratch<int32_t> cover(static_cast<size_t>(std::max<Index>(n, 1)), s);
+  cover.zero();
   k::cover_weights(n, np, static_cast<int>(ps), patches.get(), cover.get(), out.weights.get(), s);
   PDB_LAUNCH_CHECK();
   out.patches = std::move(patches);

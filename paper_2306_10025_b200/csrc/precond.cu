@@ -38,7 +38,7 @@ void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of) {
   k::sort_inverse_segments(n, pc.inv_ptr.get(), pc.inv.get(), s);
   if (slot_of) k::remap_inverse(pc.np * pc.ps, static_cast<int>(pc.ps), slot_of, pc.inv.get(), s);
   PDB_LAUNCH_CHECK();
-  // padded slot-major copy when every DoF is in at most 8 patches
+  // largest slot count: the templated scatter handles up to 8 (cell patches)
   Scratch<int32_t> maxc(1, s);
   size_t mb = 0;
   cub::DeviceReduce::Max(nullptr, mb, counts.get(), maxc.get(), n, s);
@@ -48,25 +48,19 @@ void build_inverse(pdb_precond_s& pc, cudaStream_t s, const int32_t* slot_of) {
   int32_t mh = 0;
   PDB_CUDA(cudaMemcpyAsync(&mh, maxc.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   sync(s);
-  const char* e = getenv("PDB_PADDED");
-  if (mh <= 8 && !(e && std::string(e) == "0")) {
-    pc.maxc_pad = mh <= 1 ? 1 : mh <= 2 ? 2 : mh <= 4 ? 4 : 8;
-    pc.inv_pad.alloc(static_cast<size_t>(pc.maxc_pad * std::max<int64_t>(n, 1)));
-    k::build_inverse_pad(n, pc.maxc_pad, pc.inv_ptr.get(), pc.inv.get(), pc.inv_pad.get(), s);
-    PDB_LAUNCH_CHECK();
-    // the padded scatter recomputes omega * (1 / count); keep it only when the
-    // patch set's weights are exactly that (detect_patches' compute_weights)
+  pc.maxc = 0;
+  if (mh <= 8) {
+    pc.maxc = mh <= 1 ? 1 : mh <= 2 ? 2 : mh <= 4 ? 4 : 8;
+    // the templated scatter recomputes omega * (1 / count); keep it only when
+    // the patch set's weights are exactly that (detect_patches' compute_weights)
     if (pc.omega_w.get()) {
       Scratch<int32_t> bad(1, s);
       PDB_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int32_t), s));
-      k::check_pad_weights(n, pc.omega, pc.inv_ptr.get(), pc.omega_w.get(), bad.get(), s);
+      k::check_count_weights(n, pc.omega, pc.inv_ptr.get(), pc.omega_w.get(), bad.get(), s);
       int32_t bh = 0;
       PDB_CUDA(cudaMemcpyAsync(&bh, bad.get(), sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       sync(s);
-      if (bh) {
-        pc.maxc_pad = 0;
-        pc.inv_pad = DevBuf<int32_t>();
-      }
+      if (bh) pc.maxc = 0;
     }
   }
 }
@@ -75,8 +69,9 @@ namespace {
 
 void scatter_stage(const pdb_precond_s& pc, const double* sols, bool symmetric, const double* x_in, double* z_out,
                    double* x_out, cudaStream_t s) {
-  if (pc.maxc_pad > 0)
-    k::scatter_update_pad(pc.n, pc.maxc_pad, pc.inv_pad.get(), sols, pc.omega, symmetric, x_in, z_out, x_out, s);
+  if (pc.maxc > 0)
+    k::scatter_update_csr(pc.n, pc.maxc, pc.inv_ptr.get(), pc.inv.get(), sols, pc.omega, symmetric, x_in, z_out,
+                          x_out, s);
   else
     k::scatter_update(pc.n, pc.inv_ptr.get(), pc.inv.get(), sols, symmetric ? pc.omega_sw.get() : pc.omega_w.get(),
                       x_in, z_out, x_out, s);
@@ -283,13 +278,18 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
     require(ok, Errc::invalid_argument, "assignment map must be onto the database");
   }
   require(db.ps == ps.ps, Errc::dimension_mismatch, "database entry dimension does not match the patch size");
+  TraceScope tr_all("precond_compressed after phi check", s);
   common_setup(ps, omega, pc, s);
   pc.compressed = true;
   set_factors(pc, db.m, static_cast<int>(ps.ps), db.lu.get(), db.piv.get(), s);
   pc.phi.alloc(static_cast<size_t>(ps.np));
   PDB_CUDA(cudaMemcpyAsync(pc.phi.get(), db.phi.get(), ps.np * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
   if (!pc.lu_apply && use_grouped_apply(ps.np, db.m, static_cast<int>(ps.ps))) {
-    build_tiles(pc, phi, s);  // tiles in entry order; solutions stay in patch order
+    {
+      TraceScope tr("build_tiles", s);
+      build_tiles(pc, phi, s);  // tiles in entry order; solutions stay in patch order
+    }
+    TraceScope tr("build_inverse", s);
     build_inverse(pc, s);
     if (use_dmma_apply(static_cast<int>(ps.ps))) {
       pc.frag.alloc(static_cast<size_t>(db.m * k::frag_len(static_cast<int>(ps.ps))));
@@ -318,28 +318,80 @@ void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, c
   PDB_LAUNCH_CHECK();
 }
 
+// Scoped L2 access-policy window on a stream: [p, p + bytes) persisting (as
+// much as the device's persisting set-aside allows), everything else normal.
+class L2Window {
+ public:
+  L2Window(void* p, size_t bytes, cudaStream_t s) : s_(s) {
+    if (!p || bytes == 0) return;
+    int dev = 0, maxwin = 0, maxpers = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    PDB_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+    PDB_CUDA(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev));
+    if (maxwin <= 0 || maxpers <= 0) return;
+    PDB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxpers)));
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.base_ptr = p;
+    v.accessPolicyWindow.num_bytes = std::min(bytes, static_cast<size_t>(maxwin));
+    v.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(maxpers) / static_cast<float>(v.accessPolicyWindow.num_bytes));
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    PDB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+    on_ = true;
+    static bool told = false;
+    if (!told && getenv("PDB_TRACE")) {
+      std::fprintf(stderr, "[l2] window %zu bytes, persisting max %d, window max %d\n", bytes, maxpers, maxwin);
+      told = true;
+    }
+  }
+  ~L2Window() {
+    if (!on_) return;
+    cudaStreamAttrValue v = {};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s_, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+  }
+  L2Window(const L2Window&) = delete;
+  L2Window& operator=(const L2Window&) = delete;
+
+ private:
+  cudaStream_t s_;
+  bool on_ = false;
+};
+
 void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                   double* history, cudaStream_t s) {
   require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
   const k::SpmvPlan plan = plan_of(a);
-  Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
-  Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
+  // r and the solution slots in one allocation: PDB_L2_PERSIST=1 marks it
+  // persisting in L2 for the sweeps (they are written and read back within
+  // one sweep while the residual streams the matrix through L2)
+  const size_t rlen = static_cast<size_t>(std::max<int64_t>(a.n, 1) + 31) / 32 * 32;
+  Scratch<double> rs(rlen + static_cast<size_t>(sols_len(pc)), s);
+  double* const r_ptr = rs.get();
+  double* const sols_ptr = rs.get() + rlen;
+  static const bool persist = [] {
+    const char* e = getenv("PDB_L2_PERSIST");
+    return e && e[0] == '1';
+  }();
+  L2Window l2w(persist ? rs.get() : nullptr, (rlen + static_cast<size_t>(sols_len(pc))) * sizeof(double), s);
   Scratch<double> partials(static_cast<size_t>(std::max(plan.blocks, 1)), s);
   // combo: x + (patch term + coarse term), the reference's z += x order
   Scratch<double> z(pc.coarse ? static_cast<size_t>(std::max<int64_t>(a.n, 1)) : 1, s);
   for (int64_t sw = 0; sw <= sweeps; ++sw) {
     if (sw == sweeps && !history) break;
-    k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r.get(), history ? partials.get() : nullptr,
+    k::residual(plan, a.n, a.row_ptr.get(), a.col.get(), a.val.get(), x, b, r_ptr, history ? partials.get() : nullptr,
                 s);
     if (history) k::finish_sum(partials.get(), plan.blocks, history + sw, true, s);
     if (sw == sweeps) break;
-    patch_stage(pc, r.get(), nullptr, sols.get(), s);
+    patch_stage(pc, r_ptr, nullptr, sols_ptr, s);
     if (pc.coarse) {
-      scatter_stage(pc, sols.get(), false, nullptr, z.get(), nullptr, s);
-      coarse_correct(*pc.coarse, r.get(), z.get(), s);
+      scatter_stage(pc, sols_ptr, false, nullptr, z.get(), nullptr, s);
+      coarse_correct(*pc.coarse, r_ptr, z.get(), s);
       k::axpy_val(a.n, 1.0, z.get(), x, s);
     } else {
-      scatter_stage(pc, sols.get(), false, x, nullptr, x, s);
+      scatter_stage(pc, sols_ptr, false, x, nullptr, x, s);
     }
   }
   PDB_LAUNCH_CHECK();
