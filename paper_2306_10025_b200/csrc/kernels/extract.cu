@@ -52,91 +52,11 @@ __global__ void __launch_bounds__(kWarps * 32) extract_kernel(int64_t count, con
   }
 }
 
-// ps <= 32: the warp streams the patch's ps CSR rows as one flat list of
-// entries (lane e of every 32), so all rows' loads are in flight together
-// instead of one staged row at a time.  Entry (r, p) holds column c of row
-// idx[r]; c is searched in the patch's own (sorted) DoF list, and a hit at
-// position q writes out[r][q] = val.  A per-row bit mask records the written
-// positions; the holes (columns of the patch absent from the row) get 0.0
-// afterwards, so every output element is still written once with the
-// reference's value.
-constexpr int kFlatWarps = 8;
-
-__global__ void __launch_bounds__(kFlatWarps * 32) extract_flat_kernel(
-    int64_t count, const int32_t* __restrict__ ids, int ps, const int32_t* __restrict__ patches,
-    const int64_t* __restrict__ rp, const int32_t* __restrict__ col, const double* __restrict__ val,
-    double* __restrict__ out) {
-  __shared__ int32_t sidx[kFlatWarps][32];
-  __shared__ int32_t soff[kFlatWarps][33];
-  __shared__ int64_t sbeg[kFlatWarps][32];
-  __shared__ uint32_t smask[kFlatWarps][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * kFlatWarps + warp;
-  if (t >= count) return;
-  const int64_t k = ids ? ids[t] : t;
-  const int32_t* idx = patches + k * ps;
-  double* o = out + t * (int64_t)ps * ps;
-  int len = 0;
-  if (lane < ps) {
-    const int32_t gi = idx[lane];
-    const int64_t lo = rp[gi];
-    len = (int)(rp[gi + 1] - lo);
-    sidx[warp][lane] = gi;
-    sbeg[warp][lane] = lo;
-  }
-  smask[warp][lane] = 0u;
-  // inclusive warp scan of the row lengths -> row offsets
-  int incl = len;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  soff[warp][lane + 1] = incl;
-  if (lane == 0) soff[warp][0] = 0;
-  __syncwarp();
-  const int total = soff[warp][ps];
-  const int32_t* si = sidx[warp];
-  const int32_t* so = soff[warp];
-  for (int e = lane; e < total; e += 32) {
-    int a = 0, b = ps - 1;  // row r: so[r] <= e < so[r + 1]
-    while (a < b) {
-      const int m = (a + b + 1) >> 1;
-      if (so[m] <= e) a = m;
-      else b = m - 1;
-    }
-    const int r = a;
-    const int64_t g = sbeg[warp][r] + (e - so[r]);
-    const int32_t c = __ldg(col + g);
-    const double v = __ldg(val + g);
-    int lo = 0, hi = ps;  // lower_bound of c in the patch's DoF list
-    while (lo < hi) {
-      const int m = (lo + hi) >> 1;
-      if (si[m] < c) lo = m + 1;
-      else hi = m;
-    }
-    if (lo < ps && si[lo] == c) {
-      o[(int64_t)r * ps + lo] = v;
-      atomicOr(&smask[warp][r], 1u << lo);
-    }
-  }
-  __syncwarp();
-  for (int q = lane; q < ps * ps; q += 32) {
-    const int r = q / ps, c = q - r * ps;
-    if (!((smask[warp][r] >> c) & 1u)) o[q] = 0.0;
-  }
-}
-
 }  // namespace
 
 void extract(int64_t count, const int32_t* ids, int ps, const int32_t* patches, const int64_t* rp, const int32_t* col,
              const double* val, double* out, cudaStream_t s) {
   if (count <= 0) return;
-  if (ps <= 32) {
-    extract_flat_kernel<<<(unsigned)((count + kFlatWarps - 1) / kFlatWarps), kFlatWarps * 32, 0, s>>>(
-        count, ids, ps, patches, rp, col, val, out);
-    return;
-  }
   extract_kernel<<<(unsigned)((count + kWarps - 1) / kWarps), kWarps * 32, 0, s>>>(count, ids, ps, patches, rp, col,
                                                                                   val, out);
 }

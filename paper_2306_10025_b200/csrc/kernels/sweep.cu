@@ -203,7 +203,7 @@ constexpr int kDmmaTile = 32;  // patches per tile (4 column blocks of 8)
 // conflict on every fragment load at ps = 25/27: config-3 apply 48.7 ->
 // 45 us).  Rows k >= ps are zero in the stage itself, so a zero A entry never
 // meets a neighbouring patch's (possibly non-finite) value.
-template <int MT, int KS>
+template <int MT, int KS, bool SCALE>
 __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const int32_t* __restrict__ tile_entry,
                                                                       const int32_t* __restrict__ tile_start,
                                                                       const int32_t* __restrict__ idx,
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(MT * 32) patch_apply_dmma_kernel(int ps, const
     double v = 0.0;
     if (gi[it] >= 0) {
       v = __ldg(r + gi[it]);
-      if (in_scale) v *= __ldg(in_scale + gi[it]);
+      if (SCALE) v *= __ldg(in_scale + gi[it]);
     }
     if (e < TOT) rk[e] = v;
   }
@@ -737,8 +737,12 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
   }
 #define PDB_DMMA_CASE(M, K)                                                                                   \
   if (mt == M && ks == K) {                                                                                   \
-    launch_pdl(patch_apply_dmma_kernel<M, K>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps, tile_entry,     \
-               tile_start, tile_idx, order, frag, r, in_scale, sols);                                         \
+    if (in_scale)                                                                                             \
+      launch_pdl(patch_apply_dmma_kernel<M, K, true>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps,          \
+                 tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);                           \
+    else                                                                                                      \
+      launch_pdl(patch_apply_dmma_kernel<M, K, false>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps,         \
+                 tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);                           \
     return;                                                                                                   \
   }
   PDB_DMMA_CASE(1, 1)

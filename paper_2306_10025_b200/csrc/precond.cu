@@ -318,64 +318,14 @@ void precond_apply_device(const pdb_precond_s& pc, const double* r, double* z, c
   PDB_LAUNCH_CHECK();
 }
 
-// Scoped L2 access-policy window on a stream: [p, p + bytes) persisting (as
-// much as the device's persisting set-aside allows), everything else normal.
-class L2Window {
- public:
-  L2Window(void* p, size_t bytes, cudaStream_t s) : s_(s) {
-    if (!p || bytes == 0) return;
-    int dev = 0, maxwin = 0, maxpers = 0;
-    PDB_CUDA(cudaGetDevice(&dev));
-    PDB_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev));
-    PDB_CUDA(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev));
-    if (maxwin <= 0 || maxpers <= 0) return;
-    PDB_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, static_cast<size_t>(maxpers)));
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.base_ptr = p;
-    v.accessPolicyWindow.num_bytes = std::min(bytes, static_cast<size_t>(maxwin));
-    v.accessPolicyWindow.hitRatio =
-        std::min(1.0f, static_cast<float>(maxpers) / static_cast<float>(v.accessPolicyWindow.num_bytes));
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    PDB_CUDA(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
-    on_ = true;
-    static bool told = false;
-    if (!told && getenv("PDB_TRACE")) {
-      std::fprintf(stderr, "[l2] window %zu bytes, persisting max %d, window max %d\n", bytes, maxpers, maxwin);
-      told = true;
-    }
-  }
-  ~L2Window() {
-    if (!on_) return;
-    cudaStreamAttrValue v = {};
-    v.accessPolicyWindow.num_bytes = 0;
-    cudaStreamSetAttribute(s_, cudaStreamAttributeAccessPolicyWindow, &v);
-    cudaCtxResetPersistingL2Cache();
-  }
-  L2Window(const L2Window&) = delete;
-  L2Window& operator=(const L2Window&) = delete;
-
- private:
-  cudaStream_t s_;
-  bool on_ = false;
-};
-
 void relax_device(const DeviceCsr& a, const pdb_precond_s& pc, const double* b, double* x, int64_t sweeps,
                   double* history, cudaStream_t s) {
   require(pc.n == a.n, Errc::dimension_mismatch, "smooth length mismatch");
   const k::SpmvPlan plan = plan_of(a);
-  // r and the solution slots in one allocation: PDB_L2_PERSIST=1 marks it
-  // persisting in L2 for the sweeps (they are written and read back within
-  // one sweep while the residual streams the matrix through L2)
-  const size_t rlen = static_cast<size_t>(std::max<int64_t>(a.n, 1) + 31) / 32 * 32;
-  Scratch<double> rs(rlen + static_cast<size_t>(sols_len(pc)), s);
-  double* const r_ptr = rs.get();
-  double* const sols_ptr = rs.get() + rlen;
-  static const bool persist = [] {
-    const char* e = getenv("PDB_L2_PERSIST");
-    return e && e[0] == '1';
-  }();
-  L2Window l2w(persist ? rs.get() : nullptr, (rlen + static_cast<size_t>(sols_len(pc))) * sizeof(double), s);
+  Scratch<double> r(static_cast<size_t>(std::max<int64_t>(a.n, 1)), s);
+  Scratch<double> sols(static_cast<size_t>(sols_len(pc)), s);
+  double* const r_ptr = r.get();
+  double* const sols_ptr = sols.get();
   Scratch<double> partials(static_cast<size_t>(std::max(plan.blocks, 1)), s);
   // combo: x + (patch term + coarse term), the reference's z += x order
   Scratch<double> z(pc.coarse ? static_cast<size_t>(std::max<int64_t>(a.n, 1)) : 1, s);
