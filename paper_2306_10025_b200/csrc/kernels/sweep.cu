@@ -13,6 +13,8 @@
 //                      the reference's serial scatter order (precond.cpp:81-86),
 //                      no atomics
 // plus the setup kernels of these structures (inverses, inverse maps).
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "../common.hpp"
@@ -407,9 +409,8 @@ __global__ void remap_inverse_kernel(int64_t count, int ps, const int32_t* __res
 // in flight together (the kernel is latency-bound on the idx -> sols chain).
 // (A padded slot-major map, 4 * MAXC bytes per DoF instead of 4 per slot,
 // measured no faster: 37.3 vs 36.4 us at config 3.)
-constexpr int kScatterU = 2;
 
-template <int MAXC>
+template <int MAXC, int kScatterU>
 __global__ void scatter_update_csr_kernel(int64_t n, const int32_t* __restrict__ inv_ptr,
                                           const int32_t* __restrict__ inv, const double* __restrict__ sols,
                                           double omega, bool sym, const double* __restrict__ x_in,
@@ -735,14 +736,15 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
                tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);
     return;
   }
+#define PDB_DMMA_LAUNCH(KERN, GRID, BLOCK, ...)                                                               \
+  launch_pdl(KERN, dim3((unsigned)(GRID)), dim3(BLOCK), 0, s, __VA_ARGS__, tile_entry, tile_start, tile_idx,   \
+             order, frag, r, in_scale, sols)
 #define PDB_DMMA_CASE(M, K)                                                                                   \
   if (mt == M && ks == K) {                                                                                   \
     if (in_scale)                                                                                             \
-      launch_pdl(patch_apply_dmma_kernel<M, K, true>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps,          \
-                 tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);                           \
+      PDB_DMMA_LAUNCH((patch_apply_dmma_kernel<M, K, true>), ntiles, M * 32, ps);                             \
     else                                                                                                      \
-      launch_pdl(patch_apply_dmma_kernel<M, K, false>, dim3((unsigned)ntiles), dim3(M * 32), 0, s, ps,         \
-                 tile_entry, tile_start, tile_idx, order, frag, r, in_scale, sols);                           \
+      PDB_DMMA_LAUNCH((patch_apply_dmma_kernel<M, K, false>), ntiles, M * 32, ps);                            \
     return;                                                                                                   \
   }
   PDB_DMMA_CASE(1, 1)
@@ -753,6 +755,7 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
   PDB_DMMA_CASE(3, 6)
   PDB_DMMA_CASE(4, 7)
   PDB_DMMA_CASE(4, 8)
+#undef PDB_DMMA_LAUNCH
 #undef PDB_DMMA_CASE
 }
 
@@ -787,17 +790,32 @@ void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, 
 void scatter_update_csr(int64_t n, int maxc, const int32_t* inv_ptr, const int32_t* inv, const double* sols,
                         double omega, bool sym, const double* x_in, double* z_out, double* x_out, cudaStream_t s) {
   if (n <= 0) return;
-  const unsigned g = grid_for(n, kBlock * kScatterU);
-#define PDB_CSR_CASE(M)                                                                                     \
-  launch_pdl(scatter_update_csr_kernel<M>, dim3(g), dim3(kBlock), 0, s, n, inv_ptr, inv, sols, omega, sym, \
-             x_in, z_out, x_out)
+  // DoFs per thread: 1 with up to 8 slots per DoF (3D cell patches: config 3
+  // scatter 33.0 vs 35.2 us at 2, 43.1 at 4), else 2 (config 2: 14.3 vs
+  // 14.4 us); PDB_SCATTER_U = 1 / 2 / 4 overrides for A/B runs
+  static const int u_env = [] {
+    const char* e = getenv("PDB_SCATTER_U");
+    return e ? atoi(e) : 0;
+  }();
+  const int u = u_env == 1 || u_env == 2 || u_env == 4 ? u_env : (maxc > 4 ? 1 : 2);
+#define PDB_CSR_CASE(M, U)                                                                                   \
+  launch_pdl(scatter_update_csr_kernel<M, U>, dim3(grid_for(n, kBlock * U)), dim3(kBlock), 0, s, n, inv_ptr, \
+             inv, sols, omega, sym, x_in, z_out, x_out)
+#define PDB_CSR_U(M)              \
+  if (u == 1)                     \
+    PDB_CSR_CASE(M, 1);           \
+  else if (u == 4)                \
+    PDB_CSR_CASE(M, 4);           \
+  else                            \
+    PDB_CSR_CASE(M, 2)
   switch (maxc) {
-    case 1: PDB_CSR_CASE(1); break;
-    case 2: PDB_CSR_CASE(2); break;
+    case 1: PDB_CSR_U(1); break;
+    case 2: PDB_CSR_U(2); break;
     case 3:
-    case 4: PDB_CSR_CASE(4); break;
-    default: PDB_CSR_CASE(8); break;
+    case 4: PDB_CSR_U(4); break;
+    default: PDB_CSR_U(8); break;
   }
+#undef PDB_CSR_U
 #undef PDB_CSR_CASE
 }
 

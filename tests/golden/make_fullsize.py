@@ -29,6 +29,17 @@ tests/test_fullsize_pins.py compare the GPU path with:
     python tests/golden/make_fullsize.py c3exact
     python tests/golden/make_fullsize.py c2 [threads]
     python tests/golden/make_fullsize.py c2pcg     # exact patches, PCG only
+    python tests/golden/make_fullsize.py c4 [threads]
+    python tests/golden/make_fullsize.py c5 CELLS [threads]
+
+  c4_kmeans.npz       config 4 at 512^2 (262,144 x 22-DoF Vanka patches):
+                      KMEANS_ENTRYWISE through partitioned_build, k = 128,
+                      seed 42, max_iters 50: phi, sha256 of representatives
+                      and factors; then 10 reference smooth() sweeps (omega 1)
+                      with that database: the residual history.
+  c5_kmeans_<cells>.npz  config 5 (3D Q3 elasticity, 192-DoF patches) at
+                      CELLS^3: KMEANS_ENTRYWISE k = 256, seed 42, max_iters
+                      50, as c4, and 10 smooth() sweeps.
 """
 import hashlib
 import os
@@ -173,6 +184,32 @@ def job_c2pcg_exact():
                         pcg_seconds=np.array(tp))
 
 
+def job_kmeans_entrywise(cfg: int, cells: int, ps: int, k: int, name: str, threads: int):
+    """KMEANS_ENTRYWISE (capi.cpp:268-271 -> partitioned_build) at the given
+    size, then 10 smooth() sweeps from x = 0 with omega 1."""
+    prob = P.Problem.generate(cfg, cells)
+    csr = prob.csr()
+    b = prob.rhs()
+    ref = O.RefLib()
+    rm = ref.matrix(csr)
+    rps = rm.detect(ps)
+    log(f"{name}: n={prob.ndofs} nnz={len(csr[1])} patches={rps.count}")
+    t0 = time.time()
+    db = rps.build(rm, 3, db_size=k, seed=42, max_iters=50, threads=threads)  # PDB_METHOD_KMEANS_ENTRYWISE
+    tk = time.time() - t0
+    phi = db.phi()
+    lu, piv = db.factors(ps)
+    log(f"{name}: k-means m={db.size} in {tk:.0f} s")
+    pc = rps.precond(rm, db, 1.0, threads)
+    hist, x = history(rm, pc, b, 10, threads)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), csr_sha256=np.array(csr_digest(csr)),
+                        rhs_sha256=np.array(sha(b)), m=np.array(db.size), phi=phi.astype(np.int32),
+                        reps_sha256=np.array(sha(db.reps(ps))), lu_sha256=np.array(sha(lu)),
+                        piv_sha256=np.array(sha(piv)), sizes=np.bincount(phi, minlength=db.size), hist=hist,
+                        x10_sample=x[::997].copy(), kmeans_seconds=np.array(tk), cells=np.array(cells))
+    log(f"{name}: wrote; hist {hist[0]:.6e} -> {hist[-1]:.6e}")
+
+
 if __name__ == "__main__":
     job = sys.argv[1]
     if job == "c3":
@@ -183,5 +220,10 @@ if __name__ == "__main__":
         job_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
     elif job == "c2pcg":
         job_c2pcg_exact()
+    elif job == "c4":
+        job_kmeans_entrywise(4, 0, 22, 128, "c4_kmeans", int(sys.argv[2]) if len(sys.argv) > 2 else 8)
+    elif job == "c5":
+        cells = int(sys.argv[2])
+        job_kmeans_entrywise(5, cells, 192, 256, f"c5_kmeans_{cells}", int(sys.argv[3]) if len(sys.argv) > 3 else 8)
     else:
         raise SystemExit(__doc__)

@@ -19,6 +19,12 @@ CSR and right-hand side it was made from, checked first.
   iteration count of the oracle's PCG restatement (the reference has no CG);
   CG with the exact patch preconditioner: the oracle's iteration count and
   residual history bit for bit in the reproducible mode.
+* Config 4 (512^2 Stokes Q2-Q1, 262,144 x 22-DoF Vanka patches) and config 5
+  (3D Q3 elasticity, 192-DoF patches, at 16^3 and 32^3 cells): partitioned entrywise
+  k-means (k = 128 / 256, seed 42, 50 iterations) -- phi, representatives
+  and factors bitwise -- and 10 smooth() sweeps with that database within
+  1e-9 relative (the compressed Vanka relaxation diverges at omega 1, for
+  the reference and here alike: the history pins the growth too).
 """
 import hashlib
 import os
@@ -183,3 +189,21 @@ def test_config2_pcg_exact_fast_path_close(c2, P):
     h, ho = np.asarray(rep.residual_history), g["pcg_history"]
     k = min(len(h), len(ho), 200)
     np.testing.assert_allclose(h[:k], ho[:k], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("cfg,cells,ps,k,name", [(4, 0, 22, 128, "c4_kmeans.npz"), (5, 16, 192, 256, "c5_kmeans_16.npz"),
+                                                       (5, 32, 192, 256, "c5_kmeans_32.npz")])
+def test_entrywise_kmeans_matches_reference(P, cfg, cells, ps, k, name):
+    g = fixture(name)
+    prob = P.Problem.generate(cfg, cells)
+    check_inputs(prob, g)
+    A = prob.matrix()
+    pset = P.PatchSet.detect(A, ps)
+    db = P.Database.build(A, pset, P.KMEANS_ENTRYWISE, db_size=k, seed=42, max_iters=50)
+    assert db.size == int(g["m"])
+    assert np.array_equal(db.phi(), g["phi"].astype(np.int64))
+    assert sha(db.representatives()) == str(g["reps_sha256"])
+    lu, piv = db.factors()
+    assert sha(lu) == str(g["lu_sha256"])
+    assert sha(piv) == str(g["piv_sha256"])
+    check_history(P, A, pset, db, prob.rhs(), g)

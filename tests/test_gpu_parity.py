@@ -515,3 +515,44 @@ def test_l1_tiled_kernels_match_thread_per_patch(name, ps, request, P, monkeypat
         assert a.size == b.size, kw
         assert np.array_equal(a.phi(), b.phi()), kw
         assert np.array_equal(a.representatives(), b.representatives()), kw
+
+
+def _front_csr(seed, groups, per_group, ps):
+    """Patches emitted out of front order, some sharing a front.  Row 0..G-1
+    are hubs (not candidates: ps + 1 entries); each patch is {hub g} + ps - 1
+    private DoFs whose rows hold exactly that set, so the patch is emitted at
+    its first private row with front g.  Patches are laid out so emission order
+    (ascending first private row) is a shuffled order of the fronts."""
+    rng = np.random.default_rng(seed)
+    fronts = np.repeat(np.arange(groups), per_group)
+    rng.shuffle(fronts)
+    n = groups + len(fronts) * (ps - 1)
+    rows = [[] for _ in range(n)]
+    nxt = groups
+    for g in fronts:
+        priv = list(range(nxt, nxt + ps - 1))
+        nxt += ps - 1
+        for r in priv:
+            rows[r] = [int(g)] + priv
+    for g in range(groups):
+        rows[g] = sorted(set([g] + [int(c) for c in rng.choice(np.arange(groups, n), size=ps, replace=False)]))
+    rp = np.zeros(n + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.concatenate([np.array(r, dtype=np.int64) for r in rows])
+    v = rng.uniform(1, 2, rp[-1])
+    return rp, ci, v
+
+
+@pytest.mark.parametrize("seed,groups,per_group,ps", [(1, 40, 1, 3), (2, 30, 3, 4), (3, 7, 40, 3), (4, 200, 2, 5)])
+def test_detect_front_order_and_ties(P, ref, seed, groups, per_group, ps):
+    """Detection sorts patches by front (std::sort, patch.cpp:82-83).  Distinct
+    fronts emitted out of order take the device sort; shared fronts take
+    libstdc++'s own unstable std::sort on the host: either way the patch list
+    equals the reference library's on the same matrix."""
+    csr = _front_csr(seed, groups, per_group, ps)
+    A = P.Matrix.from_csr(*csr)
+    got = P.PatchSet.detect(A, ps)
+    rps = ref.matrix(csr).detect(ps)
+    assert got.count == rps.count == groups * per_group
+    assert np.array_equal(got.patches(), rps.patches().reshape(got.patches().shape))
+    assert np.array_equal(got.weights(), rps.weights(len(csr[0]) - 1))
