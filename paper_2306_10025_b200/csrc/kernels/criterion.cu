@@ -507,6 +507,11 @@ __global__ void greedy_cand_bits_kernel(int B, const double* __restrict__ D, dou
   }
 }
 
+// The sequential pass touches shared memory only: the batch ids and LU
+// statuses are staged first, each step's outcome is recorded per batch member
+// (res[a] = the entry it created or matched), and phi / creators / entry_of
+// are written by the whole block afterwards -- a global load or store inside
+// the pass would put its latency on every one of the B dependent steps.
 __global__ void __launch_bounds__(1024) greedy_resolve_bits_kernel(
     int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps, int best_match,
     int64_t abort_above, const int32_t* __restrict__ lu_status, int32_t* __restrict__ phi,
@@ -514,71 +519,99 @@ __global__ void __launch_bounds__(1024) greedy_resolve_bits_kernel(
     const uint32_t* __restrict__ cand_g) {
   extern __shared__ uint32_t cand[];  // [B][32]
   __shared__ int32_t ent_s[kResolveMax];
+  __shared__ int32_t S_s[kResolveMax];
+  __shared__ int32_t res[kResolveMax];  // >= 0: entry created (new) or matched (old); filled for a < a_end
+  __shared__ uint8_t is_new[kResolveMax];
+  __shared__ uint8_t bad_lu[kResolveMax];
+  __shared__ int a_end_s;
+  __shared__ long long m0_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int words = (B + 31) / 32;
   for (int e = threadIdx.x; e < B * 32; e += blockDim.x) cand[e] = cand_g[e];
+  for (int e = threadIdx.x; e < B; e += blockDim.x) {
+    S_s[e] = S[e];
+    bad_lu[e] = lu_status && lu_status[e] != 0;
+  }
+  if (threadIdx.x == 0) m0_s = state[0];
   __syncthreads();
-  if (warp != 0) return;
-  uint32_t ent = 0;  // word `lane` of the entry bit set
-  int64_t m = state[0];
-  for (int a = 0; a < B; ++a) {
-    const uint32_t w = lane < words ? cand[a * 32 + lane] & ent : 0u;
-    int bb = B;
-    if (!best_match) {
-      const uint32_t any = __ballot_sync(0xffffffffu, w != 0);
-      if (any) {
-        const int L = __ffs(any) - 1;
-        const uint32_t wl = __shfl_sync(0xffffffffu, w, L);
-        bb = L * 32 + __ffs(wl) - 1;
-      }
-    } else {
-      double bd = eps;
-      uint32_t r = w;
-      while (r) {
-        const int b = lane * 32 + __ffs(r) - 1;
-        r &= r - 1;
-        const double dv = D[(int64_t)a * B + b];
-        if (dv < bd) {
-          bd = dv;
-          bb = b;
+  if (warp == 0) {
+    uint32_t ent = 0;  // word `lane` of the entry bit set
+    int64_t m = m0_s;
+    int a = 0;
+    for (; a < B; ++a) {
+      const uint32_t w = lane < words ? cand[a * 32 + lane] & ent : 0u;
+      int bb = B;
+      if (!best_match) {
+        const uint32_t any = __ballot_sync(0xffffffffu, w != 0);
+        if (any) {
+          const int L = __ffs(any) - 1;
+          const uint32_t wl = __shfl_sync(0xffffffffu, w, L);
+          bb = L * 32 + __ffs(wl) - 1;
         }
-      }
+      } else {
+        double bd = eps;
+        uint32_t r = w;
+        while (r) {
+          const int b = lane * 32 + __ffs(r) - 1;
+          r &= r - 1;
+          const double dv = D[(int64_t)a * B + b];
+          if (dv < bd) {
+            bd = dv;
+            bb = b;
+          }
+        }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, bd, off);
-        const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
-        if (od < bd || (od == bd && ob < bb)) {
-          bd = od;
-          bb = ob;
+        for (int off = 16; off > 0; off >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, off);
+          const int ob = __shfl_xor_sync(0xffffffffu, bb, off);
+          if (od < bd || (od == bd && ob < bb)) {
+            bd = od;
+            bb = ob;
+          }
         }
       }
-    }
-    if (bb < B) {
-      if (lane == 0) {
-        phi[S[a]] = ent_s[bb];
-        entry_of[a] = -1;
+      if (bb < B) {
+        if (lane == 0) {
+          res[a] = ent_s[bb];
+          is_new[a] = 0;
+        }
+        __syncwarp();
+        continue;
       }
-      continue;
-    }
-    if (abort_above > 0 && m + 1 > abort_above) {
-      if (lane == 0) state[1] = 1;
-      break;
-    }
-    if (lu_status && lu_status[a] != 0) {
-      if (lane == 0) state[2] = a;
-      break;
+      if (abort_above > 0 && m + 1 > abort_above) {
+        if (lane == 0) state[1] = 1;
+        break;
+      }
+      if (bad_lu[a]) {
+        if (lane == 0) state[2] = a;
+        break;
+      }
+      if (lane == 0) {
+        res[a] = (int32_t)m;
+        is_new[a] = 1;
+        ent_s[a] = (int32_t)m;
+      }
+      if (lane == (a >> 5)) ent |= 1u << (a & 31);
+      ++m;
+      __syncwarp();
     }
     if (lane == 0) {
-      creators[m] = S[a];
-      phi[S[a]] = (int32_t)m;
-      entry_of[a] = (int32_t)m;
-      ent_s[a] = (int32_t)m;
+      state[0] = m;
+      a_end_s = a;
     }
-    if (lane == (a >> 5)) ent |= 1u << (a & 31);
-    ++m;
-    __syncwarp();
   }
-  if (lane == 0) state[0] = m;
+  __syncthreads();
+  const int a_end = a_end_s;
+  for (int a = threadIdx.x; a < a_end; a += blockDim.x) {
+    const int32_t v = res[a];
+    phi[S_s[a]] = v;
+    if (is_new[a]) {
+      creators[v] = S_s[a];
+      entry_of[a] = v;
+    } else {
+      entry_of[a] = -1;
+    }
+  }
 }
 
 __global__ void greedy_resolve_kernel(int B, const int32_t* __restrict__ S, const double* __restrict__ D, double eps,

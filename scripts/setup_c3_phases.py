@@ -16,3 +16,10 @@ for rep in range(1 + int(os.environ.get("REPS", "4"))):
     t2 = time.perf_counter(); pc = P.Preconditioner.create(A, ps, db, omega=1.0)
     t3 = time.perf_counter()
     print(f"rep {rep} detect {1e3*(t1-t0):.1f} build {1e3*(t2-t1):.1f} precond {1e3*(t3-t2):.1f} total {1e3*(t3-t0):.1f} ms m={db.size}", flush=True)
+if os.environ.get("BISECT", "0") == "1":
+    # greedy_bisect_to_size at the band of the committed fixture (BASELINE retention)
+    g = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", f"c3_l1_{os.environ.get('PCT', '1')}.npz"))
+    lo, hi = (int(v) for v in g["target"])
+    for rep in range(2):
+        t = time.perf_counter(); dbb, e = P.Database.build_to_size(A, ps, lo, hi, P.GREEDY_L1); t = time.perf_counter() - t
+        print(f"bisect {t:.3f} s eps {e!r} m={dbb.size} same_eps={e == float(g['eps'])}", flush=True)
