@@ -1235,9 +1235,6 @@ double bisect_database(const DeviceCsr& a, const pdb_patchset_s& ps, const Build
   BuildWork total;
   for (int it = 0; it < 60; ++it) {
     const double eps = std::sqrt(lo * hi);
-    BuildParams q = p;
-    q.eps = eps;
-    q.abort_above = target_hi;
     pdb_database_s db;
     const bool ok = greedy_build(mats, n_p, static_cast<int>(ps.ps), eps, p.method == PDB_METHOD_GREEDY_SPECTRAL,
                                  p.best_match, target_hi, db, s, p.comm);

@@ -26,6 +26,8 @@ k::SpmvPlan plan_of(const DeviceCsr& a);  // SpMV launch plan (streaming partiti
 // Column-pattern classes of the SELL copy (every row's columns are row + one
 // of a few offset lists); false when the rows do not share patterns.
 bool sell_classes(const HostCsr& h, std::vector<int32_t>& cls, std::vector<int32_t>& tab, std::vector<int32_t>& tstart);
+// sell_build.cu: the same SELL copy built on the device from d's CSR arrays
+void build_sell_device(DeviceCsr& d, cudaStream_t s);
 
 // sell_mirror.cpp: the half-storage residual layout (see there).
 struct MirrorHost {

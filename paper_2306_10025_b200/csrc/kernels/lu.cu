@@ -316,7 +316,6 @@ __global__ void __launch_bounds__(kBlkThreads)
   int32_t* perm = reinterpret_cast<int32_t*>(colmax + ps);
   int32_t* rmap = perm + ps;  // logical row -> row of the scratch copy
   __shared__ double s_best;
-  __shared__ int s_p;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t len = (int64_t)ps * ps;
   double* S = scratch + (int64_t)blockIdx.x * len;
@@ -362,7 +361,6 @@ __global__ void __launch_bounds__(kBlkThreads)
           const bool ok = !(best == 0.0 || best < __dmul_rn(1e-14, colmax[k]));
           if (lane == 0) {
             s_best = best;
-            s_p = p;
             if (ok && p != k) {  // full row swap (dense.cpp:62-65): the map, the permutation
               int32_t x = perm[k];
               perm[k] = perm[p];

@@ -310,7 +310,19 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   d.item_base.upload(base.data(), base.size(), s);
   sync(s);
   const char* e = getenv("PDB_SPMV_SELL");
-  if (!(e && std::string(e) == "0")) build_sell(h, d, s);
+  if (e && std::string(e) == "0") return;
+  // the SELL copy is built on the device from the uploaded CSR; the host
+  // build stays for the opt-in half storage (PDB_SELL_MIRROR=1) and for A/B
+  // runs (PDB_SELL_DEVICE=0) -- the two produce the same arrays
+  const char* me = getenv("PDB_SELL_MIRROR");
+  const char* de = getenv("PDB_SELL_DEVICE");
+  if (!(me && me[0] == '1') && !(de && de[0] == '0')) {
+    TraceScope tr("build_sell (device)", s);
+    build_sell_device(d, s);
+  } else {
+    TraceScope tr("build_sell (host)", s);
+    build_sell(h, d, s);
+  }
 }
 
 // Residual plan: the SELL-C-sigma copy by default; PDB_SPMV_VERSION=5 / 2

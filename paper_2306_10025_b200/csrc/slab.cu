@@ -36,6 +36,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -215,19 +216,34 @@ void parallel_rows(int64_t n, F&& fn) {
 void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaStream_t s,
                      std::vector<int64_t>& touched, std::vector<int64_t>& tcount) {
   HostCsr& h = prob.a;
+  TraceScope tr_ls("slab local_structure: index space", s);
   std::vector<int64_t> rows_g;
   for (const auto& g : prob.row_ranges)
     for (int64_t i = g.first; i < g.second; ++i) rows_g.push_back(i);
   require(static_cast<int64_t>(rows_g.size()) == h.n, Errc::invalid_argument, "slab rows do not match the row ranges");
   int64_t gmin = rows_g.empty() ? 0 : rows_g.front(), gmax = rows_g.empty() ? -1 : rows_g.back();
-  for (int32_t c : h.col) {
-    gmin = std::min<int64_t>(gmin, c);
-    gmax = std::max<int64_t>(gmax, c);
+  {  // column range over the slab's entries (config 5 at 96^3: 3.5G per rank), threaded
+    std::mutex mu;
+    parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
+      int64_t lo = gmin, hi = gmax;
+      for (int64_t q = b; q < e; ++q) {
+        const int64_t c = h.col[static_cast<size_t>(q)];
+        lo = c < lo ? c : lo;
+        hi = c > hi ? c : hi;
+      }
+      std::lock_guard<std::mutex> g(mu);
+      gmin = std::min(gmin, lo);
+      gmax = std::max(gmax, hi);
+    });
   }
   const int64_t span = gmax - gmin + 1;
   std::vector<int32_t> g2l(static_cast<size_t>(std::max<int64_t>(span, 1)), -1);
   for (int64_t gi : rows_g) g2l[static_cast<size_t>(gi - gmin)] = 0;
-  for (int32_t c : h.col) g2l[static_cast<size_t>(c - gmin)] = 0;
+  // mark every referenced column (threads may store the same 0: relaxed atomic stores)
+  parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
+    for (int64_t q = b; q < e; ++q)
+      __atomic_store_n(&g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)], 0, __ATOMIC_RELAXED);
+  });
   R.gid.clear();
   for (int64_t q = 0; q < span; ++q)
     if (g2l[static_cast<size_t>(q)] == 0) {
@@ -255,6 +271,7 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
       loc.col[static_cast<size_t>(q)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
   });
   loc.val.swap(h.val);
+  TraceScope tr_up("slab local_structure: upload + SELL", s);
   try {
     upload_csr(loc, R.a, s);
   } catch (...) {
@@ -987,6 +1004,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     R.xrecv.alloc(std::max<size_t>(xr_l.size(), 1));
   }
   // (5) factors and the DoF -> slot map
+  TraceScope tr_f("slab setup: database + factors + maps", s);
   pdb_database_s built;  // distributed greedy: replicated entries, per-rank phi in R.phi
   if (!db && build) {
     if (build->method == PDB_METHOD_KMEANS_ENTRYWISE)

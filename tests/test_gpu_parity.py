@@ -556,3 +556,28 @@ def test_detect_front_order_and_ties(P, ref, seed, groups, per_group, ps):
     assert got.count == rps.count == groups * per_group
     assert np.array_equal(got.patches(), rps.patches().reshape(got.patches().shape))
     assert np.array_equal(got.weights(), rps.weights(len(csr[0]) - 1))
+
+
+@pytest.mark.parametrize("kind", ["ragged", "banded", "c1", "c3s", "c4s", "c5s"])
+def test_sell_device_build_equals_host_build(P, orc, monkeypatch, kind):
+    """The SELL copy built on the device (sell_build.cu) has the host build's
+    classes, slices and stored entries, and its residual is bitwise the
+    reference sum, on unclassed (ragged), banded and FEM matrices."""
+    if kind == "ragged":
+        csr = _ragged_csr(5, 7000)
+    elif kind == "banded":
+        csr = _banded_csr(6, 20000, 7)
+    else:
+        cfg, cells = {"c1": (1, 0), "c3s": (3, 6), "c4s": (4, 16), "c5s": (5, 3)}[kind]
+        csr = P.Problem.generate(cfg, cells).csr()
+    n = len(csr[0]) - 1
+    x = np.random.default_rng(n).uniform(-1, 1, n)
+    want = orc.spmv(csr, x)
+    A = P.Matrix.from_csr(*csr)  # device build (default)
+    monkeypatch.setenv("PDB_SELL_DEVICE", "0")
+    H = P.Matrix.from_csr(*csr)  # host build
+    assert A.sell_info() == H.sell_info()
+    if kind in ("banded", "c1", "c3s"):
+        assert A.sell_info()["classes"] >= 1
+    assert np.array_equal(A.spmv(x), want)
+    assert np.array_equal(H.spmv(x), want)
