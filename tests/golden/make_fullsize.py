@@ -29,6 +29,7 @@ tests/test_fullsize_pins.py compare the GPU path with:
     python tests/golden/make_fullsize.py c3exact
     python tests/golden/make_fullsize.py c2 [threads]
     python tests/golden/make_fullsize.py c2pcg     # exact patches, PCG only
+    python tests/golden/make_fullsize.py c2pcgfix  # PCG part of c2_kmeans.npz from its phi
     python tests/golden/make_fullsize.py c4 [threads]
     python tests/golden/make_fullsize.py c5 CELLS [threads]
 
@@ -184,6 +185,50 @@ def job_c2pcg_exact():
                         pcg_seconds=np.array(tp))
 
 
+def job_c2pcg_from_phi():
+    """Completes c2_kmeans.npz with the PCG part without re-running the
+    3.2 h reference k-means: the final representatives are the in-order
+    entrywise means of the final clusters (entrywise_mean_indexed,
+    dense.cpp:211-223, after the last Lloyd update, compress.cpp:221-262),
+    rebuilt here from the recorded phi and checked against the recorded
+    sha256 of the reference's representatives, LU factors and pivots before
+    the oracle's PCG restatement runs with them."""
+    path = os.path.join(HERE, "c2_kmeans.npz")
+    d = dict(np.load(path))
+    prob = P.Problem.generate(2, 0)
+    csr = prob.csr()
+    b = prob.rhs()
+    assert csr_digest(csr) == str(d["csr_sha256"]) and sha(b) == str(d["rhs_sha256"])
+    orc = O.Oracle()
+    patches, w = orc.detect(csr, 25)
+    mats = orc.extract_all(csr, patches)
+    phi = d["phi"].astype(np.int64)
+    m = int(d["m"])
+    reps = np.zeros((m, 25, 25))
+    for j in range(m):
+        members = np.flatnonzero(phi == j)  # ascending patch order
+        acc = np.zeros((25, 25))
+        for k in members:
+            acc += mats[k]  # left fold, one entry at a time (elementwise numpy add)
+        reps[j] = acc * (1.0 / float(len(members)))
+    assert sha(reps) == str(d["reps_sha256"]), "rebuilt representatives differ from the reference's"
+    lu = np.empty_like(reps)
+    piv = np.empty((m, 25), np.int64)
+    for j in range(m):
+        lu[j], piv[j] = orc.lu_factor(reps[j])
+    assert sha(lu) == str(d["lu_sha256"]) and sha(piv) == str(d["piv_sha256"])
+    log(f"c2pcgfix: database rebuilt from phi, sha256 of reps / LU / pivots equal the reference's")
+    t0 = time.time()
+    _, rep = orc.pcg(csr, b, dict(patches=patches, weights=w, omega=1.0, lu=lu, piv=piv, phi=phi), tol=1e-8,
+                     max_iters=20000)
+    tp = time.time() - t0
+    log(f"c2pcgfix: pcg {rep['iterations']} iterations converged={rep['converged']} in {tp:.0f} s")
+    d.update(pcg_iterations=np.array(rep["iterations"]), pcg_converged=np.array(rep["converged"]),
+             pcg_history=rep["residual_history"], pcg_seconds=np.array(tp))
+    np.savez_compressed(path, **d)
+    log("c2pcgfix: wrote")
+
+
 def job_kmeans_entrywise(cfg: int, cells: int, ps: int, k: int, name: str, threads: int):
     """KMEANS_ENTRYWISE (capi.cpp:268-271 -> partitioned_build) at the given
     size, then 10 smooth() sweeps from x = 0 with omega 1."""
@@ -220,6 +265,8 @@ if __name__ == "__main__":
         job_c2(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
     elif job == "c2pcg":
         job_c2pcg_exact()
+    elif job == "c2pcgfix":
+        job_c2pcg_from_phi()
     elif job == "c4":
         job_kmeans_entrywise(4, 0, 22, 128, "c4_kmeans", int(sys.argv[2]) if len(sys.argv) > 2 else 8)
     elif job == "c5":
