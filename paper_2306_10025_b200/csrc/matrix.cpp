@@ -284,28 +284,28 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   sync(s);
 }
 
-void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
+void alloc_csr(Index n, Index nnz, DeviceCsr& d, cudaStream_t s) {
   require_device();
-  d.n = h.n;
-  d.nnz = h.nnz();
-  d.row_ptr.alloc(static_cast<size_t>(h.n + 1));
+  d.n = n;
+  d.nnz = nnz;
+  d.row_ptr.alloc(static_cast<size_t>(n + 1));
   // 32 zeroed elements of tail padding: the bulk-copy SpMV widens spans to
   // 16-byte bounds and may read past the last nonzero
   constexpr size_t kPad = 32;
-  d.col.alloc(static_cast<size_t>(d.nnz) + kPad);
-  d.val.alloc(static_cast<size_t>(d.nnz) + kPad);
-  PDB_CUDA(cudaMemsetAsync(d.col.get() + d.nnz, 0, kPad * sizeof(int32_t), s));
-  PDB_CUDA(cudaMemsetAsync(d.val.get() + d.nnz, 0, kPad * sizeof(double), s));
-  d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
-  d.col.upload(h.col.data(), h.col.size(), s);
-  d.val.upload(h.val.data(), h.val.size(), s);
+  d.col.alloc(static_cast<size_t>(nnz) + kPad);
+  d.val.alloc(static_cast<size_t>(nnz) + kPad);
+  PDB_CUDA(cudaMemsetAsync(d.col.get() + nnz, 0, kPad * sizeof(int32_t), s));
+  PDB_CUDA(cudaMemsetAsync(d.val.get() + nnz, 0, kPad * sizeof(double), s));
+}
+
+void finish_csr(const HostCsr& h, const std::vector<int64_t>& row_ptr, DeviceCsr& d, cudaStream_t s) {
   // warp items of the CSR residual (v5)
-  const std::vector<int32_t> part = k::item_partition(h.n, h.row_ptr.data());
+  const std::vector<int32_t> part = k::item_partition(d.n, row_ptr.data());
   d.nitems = static_cast<int>(part.size()) - 1;
   d.item_start.alloc(part.size());
   d.item_start.upload(part.data(), part.size(), s);
   std::vector<int64_t> base(part.size());
-  for (size_t b = 0; b < part.size(); ++b) base[b] = h.row_ptr[static_cast<size_t>(part[b])];
+  for (size_t b = 0; b < part.size(); ++b) base[b] = row_ptr[static_cast<size_t>(part[b])];
   d.item_base.alloc(base.size());
   d.item_base.upload(base.data(), base.size(), s);
   sync(s);
@@ -320,9 +320,18 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
     TraceScope tr("build_sell (device)", s);
     build_sell_device(d, s);
   } else {
+    require(h.n == d.n && h.nnz() == d.nnz, Errc::internal, "host build of the SELL copy needs the host CSR");
     TraceScope tr("build_sell (host)", s);
     build_sell(h, d, s);
   }
+}
+
+void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
+  alloc_csr(h.n, h.nnz(), d, s);
+  d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
+  d.col.upload(h.col.data(), h.col.size(), s);
+  d.val.upload(h.val.data(), h.val.size(), s);
+  finish_csr(h, h.row_ptr, d, s);
 }
 
 // Residual plan: the SELL-C-sigma copy by default; PDB_SPMV_VERSION=5 / 2

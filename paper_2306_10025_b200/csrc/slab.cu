@@ -212,6 +212,12 @@ void parallel_rows(int64_t n, F&& fn) {
   for (auto& th : pool) th.join();
 }
 
+// col[q] <- g2l[col[q] - gmin]: global column ids to the rank's local ids
+__global__ void remap_cols_kernel(int64_t nnz, int64_t gmin, const int32_t* __restrict__ g2l, int32_t* col) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < nnz) col[q] = g2l[col[q] - gmin];
+}
+
 // Phase A: local index space, local CSR, patches, touched set.
 void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaStream_t s,
                      std::vector<int64_t>& touched, std::vector<int64_t>& tcount) {
@@ -263,22 +269,43 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   }
   for (int64_t l = 0; l < R.nl; ++l) loc.row_ptr[static_cast<size_t>(l) + 1] += loc.row_ptr[static_cast<size_t>(l)];
   // rows keep their order and the halo rows are empty, so the local entry
-  // arrays are the slab's in the same order: columns remapped, values lent
-  // (swapped in for the upload and back: config 5 holds 46 GB of them)
-  loc.col.resize(h.col.size());
-  parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
-    for (int64_t q = b; q < e; ++q)
-      loc.col[static_cast<size_t>(q)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
-  });
-  loc.val.swap(h.val);
+  // arrays are the slab's in the same order: the global columns and the
+  // values are uploaded as they are and the columns remapped on the device
+  // (config 5: 3.5G entries per rank -- no host copy of them is made); the
+  // opt-in host-built half storage needs the local CSR on the host
+  const char* me = getenv("PDB_SELL_MIRROR");
   TraceScope tr_up("slab local_structure: upload + SELL", s);
-  try {
-    upload_csr(loc, R.a, s);
-  } catch (...) {
+  if (!(me && me[0] == '1')) {
+    const int64_t nnz = static_cast<int64_t>(h.col.size());
+    alloc_csr(R.nl, nnz, R.a, s);
+    R.a.row_ptr.upload(loc.row_ptr.data(), loc.row_ptr.size(), s);
+    R.a.col.upload(h.col.data(), h.col.size(), s);
+    R.a.val.upload(h.val.data(), h.val.size(), s);
+    {
+      Scratch<int32_t> dg2l(g2l.size(), s);
+      dg2l.upload(g2l.data(), g2l.size());
+      if (nnz > 0)
+        remap_cols_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, s>>>(nnz, gmin, dg2l.get(), R.a.col.get());
+      PDB_LAUNCH_CHECK();
+      sync(s);
+    }
+    HostCsr none;
+    finish_csr(none, loc.row_ptr, R.a, s);
+  } else {
+    loc.col.resize(h.col.size());
+    parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
+      for (int64_t q = b; q < e; ++q)
+        loc.col[static_cast<size_t>(q)] = g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)];
+    });
+    loc.val.swap(h.val);  // lent for the upload (config 5 holds 46 GB of them)
+    try {
+      upload_csr(loc, R.a, s);
+    } catch (...) {
+      loc.val.swap(h.val);
+      throw;
+    }
     loc.val.swap(h.val);
-    throw;
   }
-  loc.val.swap(h.val);
   detect_patches(R.a, patch_size, R.ps, s);
   R.np = R.ps.np;
   // touched DoFs (global ids, ascending) and the local cover counts

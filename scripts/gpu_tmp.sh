@@ -1,2 +1,2 @@
-REPS=3 PDB_TRACE=1 python scripts/setup_c3_phases.py > gpurun_out/ext.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -x -q -k "extract or detect or exact or lu or fullsize or configs45 or slab" >> gpurun_out/ext.log 2>&1; echo "exit $?" >> gpurun_out/ext.log
+timeout 1200 python -m pytest tests -m gpu -x -q -k "slab or shard or sell_device or spmv or mirror" > gpurun_out/slab2.log 2>&1; echo "exit $?" >> gpurun_out/slab2.log
+PDB_TRACE=1 timeout 1200 python scripts/c5_rank.py > gpurun_out/c5trace3.log 2>&1; echo "exit $?" >> gpurun_out/c5trace3.log
