@@ -1,2 +1,2 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -k "slab or shard or sell_device or spmv or mirror" > gpurun_out/slab2.log 2>&1; echo "exit $?" >> gpurun_out/slab2.log
-PDB_TRACE=1 timeout 1200 python scripts/c5_rank.py > gpurun_out/c5trace3.log 2>&1; echo "exit $?" >> gpurun_out/c5trace3.log
+for i in 1 2; do CONFIGS="3 2 4" STEPS=300 scripts/sweep_ab.sh "PDB_APPLY_TILE=32" "PDB_APPLY_TILE=64" >> gpurun_out/tile64.log 2>&1; done
+PDB_APPLY_TILE=64 timeout 900 python -m pytest tests -m gpu -x -q -k "relax or apply or history or pcg or identity" >> gpurun_out/tile64.log 2>&1
