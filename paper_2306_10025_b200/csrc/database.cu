@@ -589,12 +589,23 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
       tmark = t;
     }
     PDB_CUDA(cudaMemsetAsync(changed.get(), 0, sizeof(int32_t), s));
-    if (variant != Variant::Entrywise && il) {
+    // one centroid: the argmin over a single entry is entry 0 whatever the
+    // distances (strict <, best_j starts at 0: compress.cpp:154-160), and with
+    // every patch in it no cluster is empty, so the distances are never read
+    // (the reseed needs an empty cluster): skip them.  phi, the means and the
+    // factors are those of the full computation; only the work counters differ.
+    const bool single = m == 1;
+    if (single) {
+      PDB_CUDA(cudaMemsetAsync(d_new.get(), 0, cap * sizeof(int32_t), s));
+      PDB_CUDA(cudaMemsetAsync(d_min.get(), 0, cap * sizeof(double), s));
+    }
+    if (!single && variant != Variant::Entrywise && il) {
       lu_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, len)));
       piv_il.alloc(static_cast<size_t>(k::interleaved_len(m, 8, ps)));
       k::interleave_factors(m, ps, db.lu.get(), db.piv.get(), lu_il.get(), piv_il.get(), s);
     }
     for (AssignSlot& sl : slots) {
+      if (single) break;
       const int64_t cnt = sl.hi - sl.lo;
       if (cnt <= 0) continue;
       if (variant == Variant::Entrywise) {
@@ -711,7 +722,7 @@ void kmeans_loop(const double* sub, int64_t n, KDb& db, Variant variant, int max
                                 ncclDouble, comm->comm, s));
       PDB_NCCL_DB(ncclGroupEnd());
     }
-    work.pair_evals += n * m;
+    if (!single) work.pair_evals += n * m;
     const std::vector<int32_t> prev = phi_h;
     phi_h = d2h(d_new.get(), static_cast<size_t>(n), s);
     if (trace) {
