@@ -23,6 +23,8 @@ void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s);
 // allocation (with the kernels' tail padding), then the residual structures
 // (warp items, SELL copy; h is read only by the opt-in host SELL build)
 void alloc_csr(Index n, Index nnz, DeviceCsr& d, cudaStream_t s);
+// host -> device copy of a large pageable array through pinned staging buffers (synchronous)
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s);
 void finish_csr(const HostCsr& h, const std::vector<int64_t>& row_ptr, DeviceCsr& d, cudaStream_t s);
 HostCsr validated_csr(Index n, const int64_t* rp, const int64_t* ci, const double* v);
 HostCsr download_csr(const DeviceCsr& d, cudaStream_t s);

@@ -4,7 +4,9 @@
 #include <cctype>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <fstream>
+#include <mutex>
 #include <sstream>
 #include <thread>
 #include <unordered_map>
@@ -284,6 +286,60 @@ void build_sell(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   sync(s);
 }
 
+// Host -> device copy of a large pageable array: chunks are copied into two
+// pinned staging buffers by host threads and DMA'd from there, the copy of
+// chunk i + 1 overlapping the transfer of chunk i (the driver's own pageable
+// path moves one staging block at a time).  Pinned sources and small arrays
+// take cudaMemcpyAsync directly.  Synchronous on return.
+void h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = size_t{64} << 20;
+  if (bytes == 0) return;
+  cudaPointerAttributes at{};
+  const bool pinned = cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer may leave an error on older drivers
+  if (pinned || bytes < 4 * kChunk) {
+    PDB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    sync(s);
+    return;
+  }
+  struct Stage {
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  static Stage stage_of[64];  // per device (events belong to one device)
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  PDB_CUDA(cudaGetDevice(&dev));
+  require(dev < 64, Errc::internal, "device ordinal beyond the per-device caches");
+  Stage& st = stage_of[dev];
+  for (int b = 0; b < 2; ++b)
+    if (!st.buf[b]) {
+      PDB_CUDA(cudaMallocHost(&st.buf[b], kChunk));
+      PDB_CUDA(cudaEventCreateWithFlags(&st.ev[b], cudaEventDisableTiming));
+    }
+  const int T = static_cast<int>(std::max(1u, std::min(8u, std::thread::hardware_concurrency())));
+  const char* sp = static_cast<const char*>(src);
+  char* dp = static_cast<char*>(dst);
+  size_t i = 0;
+  for (size_t off = 0; off < bytes; off += kChunk, ++i) {
+    const size_t n = std::min(kChunk, bytes - off);
+    const int b = static_cast<int>(i & 1);
+    if (i >= 2) PDB_CUDA(cudaEventSynchronize(st.ev[b]));  // its previous transfer is done
+    char* buf = static_cast<char*>(st.buf[b]);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+      pool.emplace_back([&, t] {
+        const size_t a = n * t / T, e = n * (t + 1) / T;
+        std::memcpy(buf + a, sp + off + a, e - a);
+      });
+    for (auto& th : pool) th.join();
+    PDB_CUDA(cudaMemcpyAsync(dp + off, buf, n, cudaMemcpyHostToDevice, s));
+    PDB_CUDA(cudaEventRecord(st.ev[b], s));
+  }
+  sync(s);
+}
+
 void alloc_csr(Index n, Index nnz, DeviceCsr& d, cudaStream_t s) {
   require_device();
   d.n = n;
@@ -328,9 +384,9 @@ void finish_csr(const HostCsr& h, const std::vector<int64_t>& row_ptr, DeviceCsr
 
 void upload_csr(const HostCsr& h, DeviceCsr& d, cudaStream_t s) {
   alloc_csr(h.n, h.nnz(), d, s);
-  d.row_ptr.upload(h.row_ptr.data(), h.row_ptr.size(), s);
-  d.col.upload(h.col.data(), h.col.size(), s);
-  d.val.upload(h.val.data(), h.val.size(), s);
+  h2d_staged(d.row_ptr.get(), h.row_ptr.data(), h.row_ptr.size() * sizeof(int64_t), s);
+  h2d_staged(d.col.get(), h.col.data(), h.col.size() * sizeof(int32_t), s);
+  h2d_staged(d.val.get(), h.val.data(), h.val.size() * sizeof(double), s);
   finish_csr(h, h.row_ptr, d, s);
 }
 

@@ -278,9 +278,9 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   if (!(me && me[0] == '1')) {
     const int64_t nnz = static_cast<int64_t>(h.col.size());
     alloc_csr(R.nl, nnz, R.a, s);
-    R.a.row_ptr.upload(loc.row_ptr.data(), loc.row_ptr.size(), s);
-    R.a.col.upload(h.col.data(), h.col.size(), s);
-    R.a.val.upload(h.val.data(), h.val.size(), s);
+    h2d_staged(R.a.row_ptr.get(), loc.row_ptr.data(), loc.row_ptr.size() * sizeof(int64_t), s);
+    h2d_staged(R.a.col.get(), h.col.data(), h.col.size() * sizeof(int32_t), s);
+    h2d_staged(R.a.val.get(), h.val.data(), h.val.size() * sizeof(double), s);
     {
       Scratch<int32_t> dg2l(g2l.size(), s);
       dg2l.upload(g2l.data(), g2l.size());
