@@ -1,3 +1,5 @@
-PDB_TRACE=1 timeout 1200 python scripts/c5_rank.py > gpurun_out/c5trace4.log 2>&1; echo "exit $?" >> gpurun_out/c5trace4.log
-BENCH_SLABS=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 50 --warmup 5 > gpurun_out/slabs1c.log 2>&1; echo "exit $?" >> gpurun_out/slabs1c.log
-timeout 1200 python -m pytest tests -m gpu -x -q -k "slab or spmv or fullsize or mmio or abi or generator" > gpurun_out/staged.log 2>&1; echo "exit $?" >> gpurun_out/staged.log
+for i in 1 2; do
+  CONFIGS="3 2" STEPS=300 scripts/sweep_ab.sh "TAG=default" >> gpurun_out/async.log 2>&1
+  PDB_LIB_PATH=paper_2306_10025_b200/lib/ab/async/libpatchdb.so.0 CONFIGS="3 2" STEPS=300 scripts/sweep_ab.sh "TAG=async" >> gpurun_out/async.log 2>&1
+done
+PDB_LIB_PATH=paper_2306_10025_b200/lib/ab/async/libpatchdb.so.0 timeout 900 python -m pytest tests -m gpu -x -q -k "relax or apply or history or identity" >> gpurun_out/async.log 2>&1
