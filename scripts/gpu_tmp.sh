@@ -1,2 +1,1 @@
-for i in 1 2; do CONFIGS="5" STEPS=100 scripts/sweep_ab.sh "PDB_LARGE_TILE=32" "PDB_LARGE_TILE=64" >> gpurun_out/large64.log 2>&1; done
-timeout 900 python -m pytest tests -m gpu -x -q -k "configs45 or c5 or lu_large or entrywise_kmeans_matches_reference or slab" >> gpurun_out/large64.log 2>&1; echo "exit $?" >> gpurun_out/large64.log
+for b in 0 2 3 1; do PDB_DIAG_BPS=$b TAG=bps$b REPS=2 python scripts/lib_ab.py >> gpurun_out/bps.log 2>&1; done
