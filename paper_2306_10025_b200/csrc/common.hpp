@@ -214,4 +214,9 @@ class TraceScope {
 
 int num_sms();
 
+// TMA descriptor (a CUtensorMap) of a preconditioner's fragment-ordered inverses, see kernels.hpp.
+struct FragTensorMap {
+  alignas(64) unsigned char opaque[128];
+};
+
 }  // namespace pdb

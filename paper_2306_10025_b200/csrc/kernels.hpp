@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "common.hpp"
+
 namespace pdb::k {
 
 // ---- spmv.cu : residual and SpMV ------------------------------------------
@@ -99,9 +101,16 @@ bool dmma_apply_supported(int ps);
 int apply_tile(int ps);  // patches per tile of the grouped apply (32 on the DMMA path)
 int64_t frag_len(int ps);  // doubles per entry in fragment order
 void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag, cudaStream_t s);
+// Patches above 32 DoFs (config 5: 192): an entry's fragment-ordered inverse (295 KB) does not fit in
+// registers, so it is staged through shared memory by TMA (cp.async.bulk.tensor.2d over a tensor map of
+// the fragment array: rows = (entry, 8-row block), columns = (k-step, lane)), a ring of 8-k-step stages
+// filled ahead of the tile's gathers.  frag_tensor_map encodes the map once per preconditioner.
+using ::pdb::FragTensorMap;
+void frag_tensor_map(int64_t nf, int ps, const double* frag, FragTensorMap* out);
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
-                      const double* in_scale, double* sols, cudaStream_t s);
+                      const int32_t* tile_idx, const int32_t* order, const double* frag,
+                      const FragTensorMap* frag_map, const double* r, const double* in_scale, double* sols,
+                      cudaStream_t s);
 void remap_inverse(int64_t count, int ps, const int32_t* slot_of, int32_t* inv, cudaStream_t s);
 // Multi-GPU shard helpers: list-driven scatter (see shard.cu), pack / unpack.
 void shard_scatter(int64_t count, const int32_t* list, const int32_t* inv_ptr, const int32_t* inv, const double* sols,

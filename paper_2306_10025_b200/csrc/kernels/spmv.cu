@@ -463,6 +463,26 @@ void launch_v2(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* c
     residual_v2_kernel<G, 8><<<p.blocks, kBlock, 0, s>>>(n, rp, col, val, x, b, r, sumsq, negate, dotv);
 }
 
+// The residual gathers x through L1; it asks for the largest L1 carve-out so
+// that its blocks never run under the shared-memory-heavy split a preceding
+// kernel left on an SM (with programmatic dependent launch the SMs are never
+// idle between kernels, so the split of the 192-DoF tile apply -- 197 KB of
+// shared memory -- otherwise sticks: config-5 sweep 1.68 vs 1.51 ms).
+// PDB_RES_CARVEOUT=<percent> overrides the hint, -1 leaves the default.
+template <typename K>
+void prefer_l1(K kern) {
+  static const int carve = [] {
+    const char* e = getenv("PDB_RES_CARVEOUT");
+    return e ? atoi(e) : 0;
+  }();
+  static bool done[64] = {};
+  int dev = 0;
+  PDB_CUDA(cudaGetDevice(&dev));
+  if (carve < 0 || dev >= 64 || done[dev]) return;
+  PDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  done[dev] = true;
+}
+
 void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val,
                        const double* x, const double* b, double* r, double* sumsq, bool negate, cudaStream_t s,
                        const double* dotv = nullptr) {
@@ -490,18 +510,24 @@ void dispatch_residual(const SpmvPlan& p, int64_t n, const int64_t* rp, const in
     }
     if (p.sell_tab) {
       const char* ue = getenv("PDB_SELL_CLS_U");
-      if (ue && atoi(ue) == 16)
+      if (ue && atoi(ue) == 16) {
+        prefer_l1(residual_sell_kernel<16, true>);
         launch_pdl(residual_sell_kernel<16, true>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off,
                    sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, p.sell_tab, p.sell_tstart);
-      else
+      } else {
+        prefer_l1(residual_sell_kernel<8, true>);
         launch_pdl(residual_sell_kernel<8, true>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off,
                    sr, p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, p.sell_tab, p.sell_tstart);
-    } else if (p.entries == 4)
+      }
+    } else if (p.entries == 4) {
+      prefer_l1(residual_sell_kernel<4>);
       launch_pdl(residual_sell_kernel<4>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
                  p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, nullptr, nullptr);
-    else
+    } else {
+      prefer_l1(residual_sell_kernel<8>);
       launch_pdl(residual_sell_kernel<8>, dim3((unsigned)p.blocks), dim3(256), 0, s, p.nslices, p.sell_off, sr,
                  p.sell_val, p.sell_col, x, b, r, sumsq, negate, pf, dotv, nullptr, nullptr);
+    }
     return;
   }
   if (p.version == 5 && p.blk_start) {

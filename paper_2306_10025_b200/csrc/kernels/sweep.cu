@@ -13,8 +13,11 @@
 //                      the reference's serial scatter order (precond.cpp:81-86),
 //                      no atomics
 // plus the setup kernels of these structures (inverses, inverse maps).
+#include <algorithm>
 #include <cstdlib>
+#include <string>
 
+#include <cuda.h>  // CUtensorMap (types only; the encoder is looked up through the runtime)
 #include <cub/cub.cuh>
 
 #include "../common.hpp"
@@ -318,6 +321,148 @@ __global__ void __launch_bounds__(1024) patch_apply_dmma_large_kernel(
         for (int q = 0; q < 8; ++q)
           if (kc + q < ks) dmma_m8n8k4(c[nt][0], c[nt][1], a[q], bp[q * 4]);
       }
+    }
+  }
+  const int row = w * 8 + g;
+  if (row < ps) {
+#pragma unroll
+    for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+      const int p0 = nt * 8 + 2 * tg;
+      if (p0 < cnt) sols[(int64_t)ko[p0] * ps + row] = c[nt][0];
+      if (p0 + 1 < cnt) sols[(int64_t)ko[p0 + 1] * ps + row] = c[nt][1];
+    }
+  }
+}
+
+// The same tile product with the entry's inverse staged by TMA.  The fragment
+// array is a 2-D tensor: row (f * mt + w) holds warp w's ks * 32 fragment
+// values of entry f, so the box {kTmaQ * 32 columns, mt rows} at column
+// c * kTmaQ * 32 is k-step chunk c for every warp of the block -- one
+// cp.async.bulk.tensor.2d per stage, landing as stage[w][q][lane] (each
+// warp's fragment loads are 256 contiguous bytes: no bank conflicts).  The
+// ring's first stages are issued before the tile's gathers and before
+// griddepcontrol.wait (the inverses do not depend on the residual), so the
+// 295 KB stream of a 192-DoF entry overlaps the gather latency instead of
+// following it; a stage is refilled by warp 0 once every warp has released
+// it (mbarrier full / empty pairs).  Columns past ks * 32 are zero-filled
+// by the TMA unit (ks not a multiple of kTmaQ).
+constexpr int kTmaQ = 8;         // k-steps per stage
+constexpr int kTmaMaxIter = 10;  // gathers per thread: ceil(kstr / mt) <= 10 for 32 < ps <= 256
+constexpr int kTmaMaxStages = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(1024) patch_apply_dmma_tma_kernel(
+    const __grid_constant__ CUtensorMap fmap, int ps, int mt, int ks, int kstr, int nst,
+    const int32_t* __restrict__ tile_entry, const int32_t* __restrict__ tile_start,
+    const int32_t* __restrict__ tile_idx, const int32_t* __restrict__ order, const double* __restrict__ r,
+    const double* __restrict__ in_scale, double* __restrict__ sols) {
+  extern __shared__ __align__(128) double dyn[];  // nst stages of mt * kTmaQ * 32, then the residual stage
+  __shared__ __align__(8) uint64_t full[kTmaMaxStages], empty[kTmaMaxStages];
+  __shared__ int32_t ko[kDmmaTile];
+  const int stage_len = mt * kTmaQ * 32;
+  double* rk = dyn + (size_t)nst * stage_len;  // kDmmaTile * kstr
+  const int t = blockIdx.x;
+  const int f = __ldg(tile_entry + t);
+  const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+  const int nth = blockDim.x;
+  const int nchunks = (ks + kTmaQ - 1) / kTmaQ;
+  const unsigned stage_bytes = (unsigned)stage_len * 8u;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, (unsigned)mt);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const int pre = nchunks < nst ? nchunks : nst;
+    for (int c = 0; c < pre; ++c) {
+      mbar_expect_tx(full + c, stage_bytes);
+      tma_load_2d(dyn + (size_t)c * stage_len, &fmap, c * kTmaQ * 32, f * mt, full + c);
+    }
+  }
+  if ((int)threadIdx.x < cnt) ko[threadIdx.x] = __ldg(order + s0 + threadIdx.x);
+  const int32_t* ti = tile_idx + (int64_t)s0 * ps;
+  const int tot = kDmmaTile * kstr;
+  int32_t gi[kTmaMaxIter];
+#pragma unroll
+  for (int it = 0; it < kTmaMaxIter; ++it) {
+    const int e = threadIdx.x + it * nth;
+    const int p = e / kstr, k = e - p * kstr;
+    gi[it] = (e < tot && p < cnt && k < ps) ? __ldg(ti + p * ps + k) : -1;
+  }
+  grid_dep_wait();  // r is the residual kernel's output
+  grid_dep_trigger();
+#pragma unroll
+  for (int it = 0; it < kTmaMaxIter; ++it) {
+    const int e = threadIdx.x + it * nth;
+    double v = 0.0;
+    if (gi[it] >= 0) {
+      v = __ldg(r + gi[it]);
+      if (in_scale) v *= __ldg(in_scale + gi[it]);
+    }
+    if (e < tot) rk[e] = v;
+  }
+  __syncthreads();  // residual stage complete; barrier inits visible to every warp
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tg = lane & 3;
+  double c[kDmmaTile / 8][2];
+#pragma unroll
+  for (int nt = 0; nt < kDmmaTile / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % nst;
+    mbar_wait(full + st, (unsigned)((ch / nst) & 1));
+    const double* sa = dyn + (size_t)st * stage_len + w * (kTmaQ * 32) + lane;
+    double a[kTmaQ];
+#pragma unroll
+    for (int q = 0; q < kTmaQ; ++q) a[q] = sa[q * 32];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);  // the fragments are in registers: the stage may be refilled
+    const int kc = ch * kTmaQ;
+#pragma unroll
+    for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+      if (nt * 8 < cnt) {
+        const double* bp = rk + (nt * 8 + g) * kstr + kc * 4 + tg;
+#pragma unroll
+        for (int q = 0; q < kTmaQ; ++q)
+          if (kc + q < ks) dmma_m8n8k4(c[nt][0], c[nt][1], a[q], bp[q * 4]);
+      }
+    }
+    if (threadIdx.x == 0 && ch + nst < nchunks) {  // refill this stage with chunk ch + nst
+      mbar_wait(empty + st, (unsigned)((ch / nst) & 1));
+      mbar_expect_tx(full + st, stage_bytes);
+      tma_load_2d(dyn + (size_t)st * stage_len, &fmap, (ch + nst) * kTmaQ * 32, f * mt, full + st);
     }
   }
   const int row = w * 8 + g;
@@ -714,12 +859,68 @@ void build_frag_inverses(int64_t nf, int ps, const double* inv_cm, double* frag,
     build_frag_kernel<<<grid_for(total, kBlock), kBlock, 0, s>>>(total, ps, (ps + 7) / 8, (ps + 3) / 4, inv_cm, frag);
 }
 
+// The fragment array as a 2-D FP64 tensor {ks * 32, nf * mt} with boxes {kTmaQ * 32, mt}.
+void frag_tensor_map(int64_t nf, int ps, const double* frag, FragTensorMap* out) {
+  static_assert(sizeof(CUtensorMap) <= sizeof(FragTensorMap::opaque), "CUtensorMap is 128 bytes");
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+  PDB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    fail(Errc::internal, "cuTensorMapEncodeTiled is not available from this driver");
+  const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
+  const cuuint64_t dims[2] = {(cuuint64_t)ks * 32, (cuuint64_t)nf * mt};
+  const cuuint64_t strides[1] = {(cuuint64_t)ks * 32 * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)kTmaQ * 32, (cuuint32_t)mt};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult rc = reinterpret_cast<Encode>(fn)(
+      reinterpret_cast<CUtensorMap*>(out->opaque), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(frag), dims,
+      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) fail(Errc::internal, "cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)rc));
+}
+
 void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32_t* tile_start,
-                      const int32_t* tile_idx, const int32_t* order, const double* frag, const double* r,
-                      const double* in_scale, double* sols, cudaStream_t s) {
+                      const int32_t* tile_idx, const int32_t* order, const double* frag,
+                      const FragTensorMap* frag_map, const double* r, const double* in_scale, double* sols,
+                      cudaStream_t s) {
   if (ntiles <= 0) return;
   const int mt = (ps + 7) / 8, ks = (ps + 3) / 4;
-  if (ps > 32) {  // run-time shapes, inverse streamed from L2
+  static const bool no_tma = [] {
+    const char* e = getenv("PDB_APPLY_TMA");  // PDB_APPLY_TMA=0: the register-streamed kernel (A/B)
+    return e && e[0] == '0';
+  }();
+  if (ps > 32 && frag_map && !no_tma) {  // run-time shapes, inverse staged by TMA
+    int kstr = ks * 4;
+    if (kstr % 8 == 0) kstr += 4;
+    const size_t stage = (size_t)mt * kTmaQ * 32 * sizeof(double);
+    const size_t rkb = (size_t)kDmmaTile * kstr * sizeof(double);
+    const int nchunks = (ks + kTmaQ - 1) / kTmaQ;
+    int nst = (int)((220 * 1024 - rkb) / stage);
+    nst = std::min({nst, kTmaMaxStages, nchunks});
+    static const int cap = [] {
+      const char* e = getenv("PDB_APPLY_TMA_STAGES");  // ring depth cap (tuning)
+      return e ? atoi(e) : 0;
+    }();
+    if (cap > 0) nst = std::min(nst, cap);
+    if (nst < 1 || (kstr + mt - 1) / mt > kTmaMaxIter) fail(Errc::internal, "TMA apply: unsupported patch size");
+    const size_t smem = nst * stage + rkb;
+    static size_t opted[64] = {};
+    int dev = 0;
+    PDB_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64 || smem > opted[dev]) {
+      PDB_CUDA(cudaFuncSetAttribute(patch_apply_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      if (dev < 64) opted[dev] = smem;
+    }
+    launch_pdl(patch_apply_dmma_tma_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s,
+               *reinterpret_cast<const CUtensorMap*>(frag_map->opaque), ps, mt, ks, kstr, nst, tile_entry, tile_start,
+               tile_idx, order, r, in_scale, sols);
+    return;
+  }
+  if (ps > 32) {  // run-time shapes, inverse streamed from L2 through registers
     int kstr = ks * 4;
     if (kstr % 8 == 0) kstr += 4;
     const size_t smem = (size_t)kDmmaTile * kstr * sizeof(double);

@@ -145,6 +145,8 @@ struct pdb_precond_s {
   pdb::DevBuf<int32_t> order, slot_of, tile_entry, tile_start, tile_idx;
   int ntiles = 0, max_tile = 0;
   pdb::DevBuf<double> frag;  // inverses in DMMA A-fragment order (tensor-core grouped apply), when allocated
+  pdb::FragTensorMap frag_map{};  // TMA descriptor of frag (patches above 32 DoFs)
+  bool has_frag_map = false;
   int maxc = 0;  // largest slot count when <= 8 and the weights are 1/count: the templated scatter
   pdb::DevBuf<int32_t> inv_ptr;
   pdb::DevBuf<int32_t> inv;

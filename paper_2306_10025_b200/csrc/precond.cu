@@ -185,7 +185,8 @@ void patch_stage(const pdb_precond_s& pc, const double* r, const double* in_scal
   const int32_t* phi = pc.compressed ? pc.phi.get() : nullptr;
   if (!pc.lu_apply && pc.compressed && pc.ntiles > 0 && pc.frag.get() && use_dmma_apply(static_cast<int>(pc.ps)))
     k::patch_apply_dmma(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
-                        pc.tile_idx.get(), pc.order.get(), pc.frag.get(), r, in_scale, sols, s);
+                        pc.tile_idx.get(), pc.order.get(), pc.frag.get(), pc.has_frag_map ? &pc.frag_map : nullptr, r,
+                        in_scale, sols, s);
   else if (!pc.lu_apply && pc.compressed && pc.ntiles > 0)
     k::patch_apply_grouped(pc.ntiles, static_cast<int>(pc.ps), pc.tile_entry.get(), pc.tile_start.get(),
                            pc.tile_idx.get(), pc.order.get(), pc.factors.get(), r, in_scale, sols, pc.max_tile, s);
@@ -294,6 +295,10 @@ static void precond_compressed_impl(const pdb_patchset_s& ps, const pdb_database
     if (use_dmma_apply(static_cast<int>(ps.ps))) {
       pc.frag.alloc(static_cast<size_t>(db.m * k::frag_len(static_cast<int>(ps.ps))));
       k::build_frag_inverses(db.m, static_cast<int>(ps.ps), pc.factors.get(), pc.frag.get(), s);
+      if (ps.ps > 32) {
+        k::frag_tensor_map(db.m, static_cast<int>(ps.ps), pc.frag.get(), &pc.frag_map);
+        pc.has_frag_map = true;
+      }
     }
   } else {
     build_inverse(pc, s);

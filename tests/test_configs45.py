@@ -227,3 +227,29 @@ def test_gpu_compressed_apply(name, dev, request, P, orc):
     lu, piv = db.factors()
     want = orc.precond_apply(c.patches, c.w, 0.8, lu, piv, db.phi(), r)
     np.testing.assert_allclose(pc.apply(r), want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("degree,cells", [(5, 10), (6, 8), (7, 8)])
+def test_gpu_tma_staged_apply_ragged_sizes(degree, cells, P, orc):
+    """The TMA-staged tile apply (patches above 32 DoFs) at sizes whose k-step
+    count is not a multiple of the 8-k-step stage (36, 49 and 64 DoFs: 9, 13
+    and 16 k-steps; the box columns past the row are zero-filled by the TMA
+    unit) and with ragged last tiles, against the oracle's apply
+    (precond.cpp:58-88)."""
+    ps_size = (degree + 1) ** 2
+    prob = P.Problem.generate(1, cells, degree=degree)
+    csr = prob.csr()
+    patches, w = orc.detect(csr, ps_size)
+    assert patches.shape == (cells * cells, ps_size)
+    mats = orc.extract_all(csr, patches)
+    A = prob.matrix()
+    ps = P.PatchSet.detect(A, ps_size)
+    eps = orc.greedy_bisect(mats, 6, 12, spectral=False)["eps"]
+    db = P.Database.build(A, ps, P.GREEDY_L1, eps=eps)
+    assert len(patches) >= 4 * db.size
+    pc = P.Preconditioner.create(A, ps, db, omega=0.7)
+    r = np.random.default_rng(degree).uniform(-1, 1, A.rows)
+    lu, piv = db.factors()
+    want = orc.precond_apply(patches, w, 0.7, lu, piv, db.phi(), r)
+    np.testing.assert_allclose(pc.apply(r), want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
