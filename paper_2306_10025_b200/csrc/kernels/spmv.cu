@@ -603,13 +603,16 @@ void residual_slices(const SpmvPlan& p, int64_t s0, int64_t s1, const double* x,
     residual_mirror_kernel<4><<<grid_for(s1 - s0, 8), 256, sm, s>>>(
         s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_tab, p.mir_kslot, p.sell_tstart, p.mir_clo, p.mir_ntab,
         p.mir_ncls, p.mir_rbase, x, b, r, nullptr, true, 1, nullptr, int64_t{2048}, p.mir_nval);
-  } else if (p.sell_tab)
+  } else if (p.sell_tab) {
+    prefer_l1(residual_sell_kernel<8, true>);
     residual_sell_kernel<8, true><<<grid_for(s1 - s0, 8), 256, 0, s>>>(
         s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col, x, b, r, nullptr, true, 1, nullptr, p.sell_tab,
         p.sell_tstart);
-  else
+  } else {
+    prefer_l1(residual_sell_kernel<8>);
     residual_sell_kernel<8><<<grid_for(s1 - s0, 8), 256, 0, s>>>(s1 - s0, p.sell_off + s0, sr, p.sell_val, p.sell_col,
                                                                  x, b, r, nullptr, true, 1, nullptr);
+  }
 }
 
 void spmv(const SpmvPlan& p, int64_t n, const int64_t* rp, const int32_t* col, const double* val, const double* x,

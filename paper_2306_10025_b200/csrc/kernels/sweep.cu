@@ -476,6 +476,133 @@ __global__ void __launch_bounds__(1024) patch_apply_dmma_tma_kernel(
   }
 }
 
+// Persistent form of the TMA-staged apply: one block per SM walks tiles
+// blockIdx.x, + gridDim.x, ...; the residual stage is double-buffered and the
+// next tile's gathers are issued as 8-byte cp.async copies (index loads, then
+// r -> shared memory, no register round trip) before the current tile's
+// products, so the gather latency of tile j + 1 hides behind the tensor-core
+// work of tile j; the TMA ring runs across tile boundaries (chunk gc belongs
+// to tile gc / nchunks).  With in_scale (the PCG's W^1/2 gather scaling) the
+// gathers go through registers instead (scaled before the store).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT) patch_apply_dmma_tma_persistent_kernel(
+    const __grid_constant__ CUtensorMap fmap, int ps, int mt, int ks, int kstr, int nst, int ntiles,
+    const int32_t* __restrict__ tile_entry, const int32_t* __restrict__ tile_start,
+    const int32_t* __restrict__ tile_idx, const int32_t* __restrict__ order, const double* __restrict__ r,
+    const double* __restrict__ in_scale, double* __restrict__ sols) {
+  extern __shared__ __align__(128) double dyn[];  // nst stages of mt * kTmaQ * 32, then two residual stages
+  __shared__ __align__(8) uint64_t full[kTmaMaxStages], empty[kTmaMaxStages];
+  __shared__ int32_t ko[2][kDmmaTile];
+  __shared__ int32_t kcnt[2];
+  const int stage_len = mt * kTmaQ * 32;
+  const int tot = kDmmaTile * kstr;
+  double* rk0 = dyn + (size_t)nst * stage_len;
+  const int nth = blockDim.x;
+  const int nchunks = (ks + kTmaQ - 1) / kTmaQ;
+  const unsigned stage_bytes = (unsigned)stage_len * 8u;
+  const int my_tiles = (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int total_chunks = my_tiles * nchunks;
+  auto issue = [&](int gc) {  // thread 0: chunk gc of this block's tile sequence into its ring stage
+    const int j = gc / nchunks, c = gc - j * nchunks, st = gc % nst;
+    const int f = __ldg(tile_entry + blockIdx.x + j * gridDim.x);
+    mbar_expect_tx(full + st, stage_bytes);
+    tma_load_2d(dyn + (size_t)st * stage_len, &fmap, c * kTmaQ * 32, f * mt, full + st);
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, (unsigned)mt);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const int pre = total_chunks < nst ? total_chunks : nst;
+    for (int gc = 0; gc < pre; ++gc) issue(gc);
+  }
+  auto gather = [&](int j) {  // tile j's residuals -> stage j & 1 (asynchronously unless scaled)
+    const int t = blockIdx.x + j * gridDim.x, buf = j & 1;
+    const int s0 = __ldg(tile_start + t), cnt = __ldg(tile_start + t + 1) - s0;
+    if (threadIdx.x < kDmmaTile) ko[buf][threadIdx.x] = (int)threadIdx.x < cnt ? __ldg(order + s0 + threadIdx.x) : 0;
+    if (threadIdx.x == 0) kcnt[buf] = cnt;
+    const int32_t* ti = tile_idx + (int64_t)s0 * ps;
+    double* rk = rk0 + (size_t)buf * tot;
+    int32_t gi[kTmaMaxIter];
+#pragma unroll
+    for (int it = 0; it < kTmaMaxIter; ++it) {
+      const int e = threadIdx.x + it * nth;
+      const int p = e / kstr, k = e - p * kstr;
+      gi[it] = (e < tot && p < cnt && k < ps) ? __ldg(ti + p * ps + k) : -1;
+    }
+#pragma unroll
+    for (int it = 0; it < kTmaMaxIter; ++it) {
+      const int e = threadIdx.x + it * nth;
+      if (e < tot) {
+        if (gi[it] < 0)
+          rk[e] = 0.0;
+        else if (in_scale)
+          rk[e] = __ldg(r + gi[it]) * __ldg(in_scale + gi[it]);
+        else
+          cp_async8(rk + e, r + gi[it]);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  grid_dep_wait();  // r is the residual kernel's output
+  grid_dep_trigger();
+  gather(0);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tg = lane & 3;
+  const int row = w * 8 + g;
+  int gc = 0;
+  for (int j = 0; j < my_tiles; ++j) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // stage j & 1 complete; every warp is done with tile j - 1 (stage (j + 1) & 1 is free)
+    if (j + 1 < my_tiles) gather(j + 1);
+    const int buf = j & 1;
+    const int cnt = kcnt[buf];
+    const double* rk = rk0 + (size_t)buf * tot;
+    double c[kDmmaTile / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < kDmmaTile / 8; ++nt) c[nt][0] = c[nt][1] = 0.0;
+    for (int ch = 0; ch < nchunks; ++ch, ++gc) {
+      const int st = gc % nst;
+      const unsigned par = (unsigned)((gc / nst) & 1);
+      mbar_wait(full + st, par);
+      const double* sa = dyn + (size_t)st * stage_len + w * (kTmaQ * 32) + lane;
+      double a[kTmaQ];
+#pragma unroll
+      for (int q = 0; q < kTmaQ; ++q) a[q] = sa[q * 32];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);  // the fragments are in registers: the stage may be refilled
+      const int kc = ch * kTmaQ;
+#pragma unroll
+      for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+        if (nt * 8 < cnt) {
+          const double* bp = rk + (nt * 8 + g) * kstr + kc * 4 + tg;
+#pragma unroll
+          for (int q = 0; q < kTmaQ; ++q)
+            if (kc + q < ks) dmma_m8n8k4(c[nt][0], c[nt][1], a[q], bp[q * 4]);
+        }
+      }
+      if (threadIdx.x == 0 && gc + nst < total_chunks) {
+        mbar_wait(empty + st, par);
+        issue(gc + nst);
+      }
+    }
+    if (row < ps) {
+#pragma unroll
+      for (int nt = 0; nt < kDmmaTile / 8; ++nt) {
+        const int p0 = nt * 8 + 2 * tg;
+        if (p0 < cnt) sols[(int64_t)ko[buf][p0] * ps + row] = c[nt][0];
+        if (p0 + 1 < cnt) sols[(int64_t)ko[buf][p0 + 1] * ps + row] = c[nt][1];
+      }
+    }
+  }
+}
+
 // frag[f][w][q][lane] = B_f^{-1}[8w + lane/4][4q + lane%4] (0 outside ps x ps)
 __global__ void build_frag_kernel(int64_t total, int ps, int mt, int ks, const double* __restrict__ inv_cm,
                                   double* __restrict__ frag) {
@@ -896,7 +1023,11 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
     int kstr = ks * 4;
     if (kstr % 8 == 0) kstr += 4;
     const size_t stage = (size_t)mt * kTmaQ * 32 * sizeof(double);
-    const size_t rkb = (size_t)kDmmaTile * kstr * sizeof(double);
+    static const bool persistent = [] {
+      const char* e = getenv("PDB_APPLY_TMA_PERSISTENT");  // 0: one tile per block (A/B)
+      return !(e && e[0] == '0');
+    }();
+    const size_t rkb = (size_t)kDmmaTile * kstr * sizeof(double) * (persistent ? 2 : 1);
     const int nchunks = (ks + kTmaQ - 1) / kTmaQ;
     int nst = (int)((220 * 1024 - rkb) / stage);
     nst = std::min({nst, kTmaMaxStages, nchunks});
@@ -914,6 +1045,20 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
       PDB_CUDA(cudaFuncSetAttribute(patch_apply_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem));
       if (dev < 64) opted[dev] = smem;
+    }
+    if (persistent) {
+      // up to 24 warps (192 DoFs) the block is compiled for 768 threads (85 registers, no spills)
+      auto kern = mt <= 24 ? patch_apply_dmma_tma_persistent_kernel<768> : patch_apply_dmma_tma_persistent_kernel<1024>;
+      static size_t opted_p[64][2] = {};
+      if (dev >= 64 || smem > opted_p[dev][mt <= 24]) {
+        PDB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (dev < 64) opted_p[dev][mt <= 24] = smem;
+      }
+      const int grid = std::min(ntiles, num_sms());
+      launch_pdl(kern, dim3((unsigned)grid), dim3(mt * 32), smem, s,
+                 *reinterpret_cast<const CUtensorMap*>(frag_map->opaque), ps, mt, ks, kstr, nst, ntiles, tile_entry,
+                 tile_start, tile_idx, order, r, in_scale, sols);
+      return;
     }
     launch_pdl(patch_apply_dmma_tma_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s,
                *reinterpret_cast<const CUtensorMap*>(frag_map->opaque), ps, mt, ks, kstr, nst, tile_entry, tile_start,

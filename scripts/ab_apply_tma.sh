@@ -1,5 +1,6 @@
-# A/B of the 192-DoF tile apply: TMA-staged inverse (default) vs the register-streamed kernel
-# (PDB_APPLY_TMA=0), config 5 at 32^3 cells.  Run on the GPU box from the repo root.
+# A/B of the 192-DoF tile apply at config 5 (32^3 cells): persistent pipelined TMA kernel (default),
+# one-tile-per-block TMA kernel (PDB_APPLY_TMA_PERSISTENT=0), register-streamed kernel (PDB_APPLY_TMA=0).
+# Run on the GPU box from the repo root.
 run() {  # name, env...
   name=$1; shift
   env "$@" timeout 900 python bench.py --config 5 --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/ab_tma_$name.log 2>&1; echo "exit $?" >> gpurun_out/ab_tma_$name.log
@@ -12,7 +13,9 @@ if l:
 P
 }
 rm -f gpurun_out/ab_tma_summary.txt
-run st3_c0 PDB_RES_CARVEOUT=0
-run off_c0 PDB_APPLY_TMA=0 PDB_RES_CARVEOUT=0
-run st3 PDB_APPLY_TMA_STAGES=3
+timeout 900 python -m pytest tests/test_configs45.py tests/test_slab.py -m gpu -x -q > gpurun_out/ab_tma_pytest.log 2>&1; echo "exit $?" >> gpurun_out/ab_tma_pytest.log
+run persistent PDB_APPLY_TMA_PERSISTENT=1
+run persistent_st1 PDB_APPLY_TMA_STAGES=1
+run tile PDB_APPLY_TMA_PERSISTENT=0
 run off PDB_APPLY_TMA=0
+run persistent2 PDB_APPLY_TMA_PERSISTENT=1
