@@ -392,6 +392,10 @@ PDB_API pdb_status pdb_slab_phi(pdb_slab sh, int i, int64_t* phi);
 PDB_API pdb_status pdb_slab_creators(pdb_slab sh, int64_t* creators);
 /* Local ranks held by the handle (1, or nranks for an emulated group). */
 PDB_API int pdb_slab_local_ranks(pdb_slab sh);
+/* Seconds of the handle's setup spent uploading the slab's matrix and building
+ * the residual's storage (what pdb_matrix_from_csr does before a single-GPU
+ * setup starts), summed over the local ranks. */
+PDB_API double pdb_slab_upload_seconds(pdb_slab sh);
 /* info[12]: rank, nranks, local DoFs, local rows, local patches, first global
  * patch, interface split, owned DoFs, partials sent / received, x halo sent / received. */
 PDB_API pdb_status pdb_slab_info(pdb_slab sh, int i, int64_t* info);

@@ -932,6 +932,8 @@ PDB_API pdb_status pdb_slab_creators(pdb_slab sh, int64_t* creators) {
 
 PDB_API int pdb_slab_local_ranks(pdb_slab sh) { return sh == nullptr ? 0 : slab_local_ranks(*sh); }
 
+PDB_API double pdb_slab_upload_seconds(pdb_slab sh) { return sh == nullptr ? 0.0 : slab_upload_seconds(*sh); }
+
 PDB_API pdb_status pdb_slab_info(pdb_slab sh, int i, int64_t* info) {
   if (sh == nullptr || info == nullptr) return arg_error("null argument");
   return guarded([&] {

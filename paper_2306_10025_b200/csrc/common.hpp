@@ -185,22 +185,24 @@ inline void sync(cudaStream_t s) { PDB_CUDA(cudaStreamSynchronize(s)); }
 // PDB_TRACE=1: wall time of a scope, stream-synchronised at both ends, on stderr.
 class TraceScope {
  public:
-  TraceScope(const char* name, cudaStream_t s) : name_(name), s_(s) {
+  // accum_s (optional): the scope's seconds are also added there, traced or not
+  TraceScope(const char* name, cudaStream_t s, double* accum_s = nullptr) : name_(name), s_(s), accum_(accum_s) {
     static const bool on = [] {
       const char* e = std::getenv("PDB_TRACE");
       return e && e[0] == '1';
     }();
     on_ = on;
-    if (on_) {
+    if (on_ || accum_) {
       cudaStreamSynchronize(s_);
       t0_ = std::chrono::steady_clock::now();
     }
   }
   ~TraceScope() {
-    if (!on_) return;
+    if (!on_ && !accum_) return;
     cudaStreamSynchronize(s_);
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count();
-    std::fprintf(stderr, "[trace] %s %.2f ms\n", name_, ms);
+    if (accum_) *accum_ += ms * 1e-3;
+    if (on_) std::fprintf(stderr, "[trace] %s %.2f ms\n", name_, ms);
   }
   TraceScope(const TraceScope&) = delete;
   TraceScope& operator=(const TraceScope&) = delete;
@@ -208,6 +210,7 @@ class TraceScope {
  private:
   const char* name_;
   cudaStream_t s_;
+  double* accum_ = nullptr;
   bool on_ = false;
   std::chrono::steady_clock::time_point t0_;
 };

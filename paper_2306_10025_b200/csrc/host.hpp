@@ -294,5 +294,6 @@ SlabInfo slab_info(const pdb_slab_s& g, int i);
 void slab_local_dofs(const pdb_slab_s& g, int i, int64_t* out);
 void slab_owned(const pdb_slab_s& g, int i, int64_t* out);
 int slab_local_ranks(const pdb_slab_s& g);
+double slab_upload_seconds(const pdb_slab_s& g);  // matrix upload + residual structures inside the setup
 void slab_relax_one(pdb_slab_s& g, int i, const double* b, double* x, int64_t sweeps, cudaStream_t s);
 }  // namespace pdb

@@ -89,6 +89,7 @@ void sub_patchset(const pdb_patchset_s& ps, int64_t k0, int64_t k1, pdb_patchset
 // One rank's state.
 struct SlabRank {
   int rank = 0, nranks = 1;
+  double upload_s = 0.0;  // matrix upload + residual structures (what pdb_matrix_from_csr does on one GPU)
   std::vector<int64_t> gid;  // local -> global DoF (ascending)
   int64_t nl = 0;
   std::vector<int32_t> rows;  // local ids of the rank's rows (its patch DoFs)
@@ -274,7 +275,7 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   // (config 5: 3.5G entries per rank -- no host copy of them is made); the
   // opt-in host-built half storage needs the local CSR on the host
   const char* me = getenv("PDB_SELL_MIRROR");
-  TraceScope tr_up("slab local_structure: upload + SELL", s);
+  TraceScope tr_up("slab local_structure: upload + SELL", s, &R.upload_s);
   if (!(me && me[0] == '1')) {
     const int64_t nnz = static_cast<int64_t>(h.col.size());
     alloc_csr(R.nl, nnz, R.a, s);
@@ -1286,6 +1287,12 @@ void slab_relax(pdb_slab_s& g, const std::vector<const double*>& b, const std::v
 }
 
 int slab_local_ranks(const pdb_slab_s& g) { return static_cast<int>(g.ranks.size()); }
+
+double slab_upload_seconds(const pdb_slab_s& g) {
+  double t = 0.0;
+  for (const auto& r : g.ranks) t += r->upload_s;
+  return t;
+}
 
 SlabInfo slab_info(const pdb_slab_s& g, int i) {
   const SlabRank& R = slab_rank(g, i);

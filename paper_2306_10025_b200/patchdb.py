@@ -763,6 +763,7 @@ class Shard(_Handle):
 _sig("pdb_slab_create", C.c_int, C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int64, _P, C.c_double, C.c_char_p,
      C.POINTER(_P))
 _sig("pdb_slab_local_ranks", C.c_int, _P)
+_sig("pdb_slab_upload_seconds", C.c_double, _P)
 _sig("pdb_slab_info", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_local_dofs", C.c_int, _P, C.c_int, _I64)
 _sig("pdb_slab_owned", C.c_int, _P, C.c_int, _I64)
@@ -846,6 +847,11 @@ class Slab(_Handle):
     @property
     def local_ranks(self) -> int:
         return _lib.pdb_slab_local_ranks(self._ptr)
+
+    @property
+    def upload_seconds(self) -> float:
+        """Matrix upload + residual storage build inside the setup (pdb_slab_upload_seconds)."""
+        return _lib.pdb_slab_upload_seconds(self._ptr)
 
     def info(self, i: int = 0) -> dict:
         out = np.zeros(12, np.int64)
