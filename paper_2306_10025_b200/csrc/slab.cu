@@ -35,6 +35,8 @@
 // pdb_relax (tests/test_slab.py).
 #include <nccl.h>
 
+#include <optional>
+
 #include <algorithm>
 #include <mutex>
 #include <cstring>
@@ -89,6 +91,7 @@ void sub_patchset(const pdb_patchset_s& ps, int64_t k0, int64_t k1, pdb_patchset
 // One rank's state.
 struct SlabRank {
   int rank = 0, nranks = 1;
+  std::vector<int32_t> pt_host;  // setup only: the local patch lists on the host (released after phase 2)
   double upload_s = 0.0;  // matrix upload + residual structures (what pdb_matrix_from_csr does on one GPU)
   std::vector<int64_t> gid;  // local -> global DoF (ascending)
   int64_t nl = 0;
@@ -275,7 +278,8 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   // (config 5: 3.5G entries per rank -- no host copy of them is made); the
   // opt-in host-built half storage needs the local CSR on the host
   const char* me = getenv("PDB_SELL_MIRROR");
-  TraceScope tr_up("slab local_structure: upload + SELL", s, &R.upload_s);
+  std::optional<TraceScope> tr_up;
+  tr_up.emplace("slab local_structure: upload + SELL", s, &R.upload_s);
   if (!(me && me[0] == '1')) {
     const int64_t nnz = static_cast<int64_t>(h.col.size());
     alloc_csr(R.nl, nnz, R.a, s);
@@ -307,10 +311,16 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
     }
     loc.val.swap(h.val);
   }
-  detect_patches(R.a, patch_size, R.ps, s);
+  tr_up.reset();
+  {
+    TraceScope tr_d("slab local_structure: detect", s);
+    detect_patches(R.a, patch_size, R.ps, s);
+  }
+  TraceScope tr_t("slab local_structure: touched lists", s);
   R.np = R.ps.np;
   // touched DoFs (global ids, ascending) and the local cover counts
-  const std::vector<int32_t> pt = R.ps.patches.to_host(s);
+  R.pt_host = R.ps.patches.to_host(s);
+  const std::vector<int32_t>& pt = R.pt_host;
   std::vector<int32_t> cnt(static_cast<size_t>(R.nl), 0);
   for (int32_t l : pt) ++cnt[static_cast<size_t>(l)];
   touched.clear();
@@ -834,6 +844,8 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     local_structure(*g.ranks[static_cast<size_t>(i)], *probs[static_cast<size_t>(i)], patch_size, s, T[static_cast<size_t>(i)], Tc[static_cast<size_t>(i)]);
   }
   g.n_global = probs[0]->n_global > 0 ? probs[0]->n_global : probs[0]->a.n;
+  std::optional<TraceScope> tph;
+  tph.emplace("slab setup: phase 1 (counts, ranges)", s);
   // (1) all ranks: patch count and touched range
   std::vector<Mail> out(static_cast<size_t>(L), Mail(static_cast<size_t>(W))), in;
   for (int i = 0; i < L; ++i) {
@@ -862,6 +874,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     g.np_of[static_cast<size_t>(q)] = info[0][static_cast<size_t>(3 * q)];
     if (q > 0) g.k0_of[static_cast<size_t>(q)] = g.k0_of[static_cast<size_t>(q) - 1] + g.np_of[static_cast<size_t>(q) - 1];
   }
+  tph.emplace("slab setup: phase 2 (touched DoFs, weights, ownership)", s);
   // (2) touched DoFs (with counts) to every rank whose touched range overlaps
   for (int i = 0; i < L; ++i) {
     const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
@@ -900,8 +913,10 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     std::vector<double> w(static_cast<size_t>(R.nl), 0.0);
     std::vector<int32_t> up_l, up_p, pin_l, pin_p, plain;
     std::vector<char> owned(static_cast<size_t>(R.nl), 0);
+    plain.reserve(t.size());
+    int64_t l = 0;  // t and R.gid are both ascending and t is a subset: one merge walk
     for (size_t j = 0; j < t.size(); ++j) {
-      const int64_t l = local_of(R, t[j]);
+      while (R.gid[static_cast<size_t>(l)] != t[j]) ++l;
       w[static_cast<size_t>(l)] = 1.0 / static_cast<double>(total[j]);  // compute_weights (patch.cpp:12-20)
       require(hi_rank[j] - lo_rank[j] <= 1, Errc::invalid_argument,
               "slab partition too thin: a DoF is shared by non-adjacent ranks (use fewer ranks)");
@@ -950,7 +965,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     // split point: the patches touching a DoF finished above must be a suffix
     std::vector<char> is_up(static_cast<size_t>(R.nl), 0);
     for (int32_t l : up_l) is_up[static_cast<size_t>(l)] = 1;
-    const std::vector<int32_t> pt = R.ps.patches.to_host(s);
+    const std::vector<int32_t>& pt = R.pt_host;
     int64_t first = R.np;
     bool suffix = true;
     for (int64_t k = 0; k < R.np; ++k) {
@@ -960,7 +975,9 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
       if (!touches && first < R.np) suffix = false;
     }
     R.kb = suffix ? first : R.np;
+    std::vector<int32_t>().swap(R.pt_host);
   }
+  tph.emplace("slab setup: phase 3 (halo requests)", s);
   // (3) x halo requests to every rank whose touched range holds the DoF
   for (int i = 0; i < L; ++i) {
     const SlabRank& R = *g.ranks[static_cast<size_t>(i)];
@@ -974,6 +991,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
   }
   deliver(g, out, in, s);
   std::vector<Mail> req = in;
+  tph.emplace("slab setup: phase 4 (replies, lists)", s);
   // (4) replies: 1 where the requested DoF is owned here; those become xs
   for (int i = 0; i < L; ++i) {
     SlabRank& R = *g.ranks[static_cast<size_t>(i)];
@@ -1031,6 +1049,7 @@ void slab_setup(pdb_slab_s& g, std::vector<pdb_problem_s*>& probs, int64_t patch
     put(R.xr, xr_l, s);
     R.xrecv.alloc(std::max<size_t>(xr_l.size(), 1));
   }
+  tph.reset();
   // (5) factors and the DoF -> slot map
   TraceScope tr_f("slab setup: database + factors + maps", s);
   pdb_database_s built;  // distributed greedy: replicated entries, per-rank phi in R.phi
