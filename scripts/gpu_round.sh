@@ -3,8 +3,9 @@
 # GPU tests, the default bench line (config 3) and the reference arm, then the
 # launch list of a config-3 build + 5 sweeps (ncu, after the runs above exited 0).
 nvidia-smi --query-gpu=name,clocks.max.sm,power.limit --format=csv > gpurun_out/round_smi.txt
+timeout 600 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/round_smoke.log 2>&1; echo "exit $?" >> gpurun_out/round_smoke.log
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/round_pytest.log 2>&1; echo "exit $?" >> gpurun_out/round_pytest.log
-timeout 900 python bench.py > gpurun_out/round_bench.log 2>&1; echo "exit $?" >> gpurun_out/round_bench.log
+T0=$SECONDS; timeout 900 python bench.py > gpurun_out/round_bench.log 2>&1; echo "exit $?" >> gpurun_out/round_bench.log; echo "bench.py default run: $((SECONDS - T0)) s wall" > gpurun_out/round_bench_wall.txt
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/round_ref.log 2>&1; echo "exit $?" >> gpurun_out/round_ref.log
 SWEEPS=5 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/round_launches.csv python scripts/sweep_c3_once.py > gpurun_out/round_ncu.log 2>&1
