@@ -1038,14 +1038,8 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
     if (cap > 0) nst = std::min(nst, cap);
     if (nst < 1 || (kstr + mt - 1) / mt > kTmaMaxIter) fail(Errc::internal, "TMA apply: unsupported patch size");
     const size_t smem = nst * stage + rkb;
-    static size_t opted[64] = {};
     int dev = 0;
     PDB_CUDA(cudaGetDevice(&dev));
-    if (dev >= 64 || smem > opted[dev]) {
-      PDB_CUDA(cudaFuncSetAttribute(patch_apply_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-      if (dev < 64) opted[dev] = smem;
-    }
     if (persistent) {
       // up to 24 warps (192 DoFs) the block is compiled for 768 threads (85 registers, no spills)
       auto kern = mt <= 24 ? patch_apply_dmma_tma_persistent_kernel<768> : patch_apply_dmma_tma_persistent_kernel<1024>;
@@ -1059,6 +1053,12 @@ void patch_apply_dmma(int ntiles, int ps, const int32_t* tile_entry, const int32
                  *reinterpret_cast<const CUtensorMap*>(frag_map->opaque), ps, mt, ks, kstr, nst, ntiles, tile_entry,
                  tile_start, tile_idx, order, r, in_scale, sols);
       return;
+    }
+    static size_t opted[64] = {};  // the opt-in is per device: cache the largest size set on each
+    if (dev >= 64 || smem > opted[dev]) {
+      PDB_CUDA(cudaFuncSetAttribute(patch_apply_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+      if (dev < 64) opted[dev] = smem;
     }
     launch_pdl(patch_apply_dmma_tma_kernel, dim3((unsigned)ntiles), dim3(mt * 32), smem, s,
                *reinterpret_cast<const CUtensorMap*>(frag_map->opaque), ps, mt, ks, kstr, nst, tile_entry, tile_start,

@@ -35,6 +35,7 @@
 // pdb_relax (tests/test_slab.py).
 #include <nccl.h>
 
+#include <atomic>
 #include <optional>
 
 #include <algorithm>
@@ -228,18 +229,24 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   HostCsr& h = prob.a;
   TraceScope tr_ls("slab local_structure: index space", s);
   std::vector<int64_t> rows_g;
+  rows_g.reserve(static_cast<size_t>(h.n));
   for (const auto& g : prob.row_ranges)
     for (int64_t i = g.first; i < g.second; ++i) rows_g.push_back(i);
   require(static_cast<int64_t>(rows_g.size()) == h.n, Errc::invalid_argument, "slab rows do not match the row ranges");
   int64_t gmin = rows_g.empty() ? 0 : rows_g.front(), gmax = rows_g.empty() ? -1 : rows_g.back();
-  {  // column range over the slab's entries (config 5 at 96^3: 3.5G per rank), threaded
+  // column range: rows hold ascending columns (the CSR contract, validated at creation and kept by the
+  // generator), so a row's first and last entry bound it -- one pass over the rows, not the entries
+  // (config 5 at 96^3: 3.5G entries per rank); the marking pass below checks every column against it
+  {
     std::mutex mu;
-    parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
+    parallel_rows(h.n, [&](int64_t r0, int64_t r1) {
       int64_t lo = gmin, hi = gmax;
-      for (int64_t q = b; q < e; ++q) {
-        const int64_t c = h.col[static_cast<size_t>(q)];
-        lo = c < lo ? c : lo;
-        hi = c > hi ? c : hi;
+      for (int64_t i = r0; i < r1; ++i) {
+        const int64_t a = h.row_ptr[static_cast<size_t>(i)], b = h.row_ptr[static_cast<size_t>(i) + 1];
+        if (b > a) {
+          lo = std::min<int64_t>(lo, h.col[static_cast<size_t>(a)]);
+          hi = std::max<int64_t>(hi, h.col[static_cast<size_t>(b - 1)]);
+        }
       }
       std::lock_guard<std::mutex> g(mu);
       gmin = std::min(gmin, lo);
@@ -250,10 +257,20 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   std::vector<int32_t> g2l(static_cast<size_t>(std::max<int64_t>(span, 1)), -1);
   for (int64_t gi : rows_g) g2l[static_cast<size_t>(gi - gmin)] = 0;
   // mark every referenced column (threads may store the same 0: relaxed atomic stores)
+  std::atomic<bool> in_range{true};
   parallel_rows(static_cast<int64_t>(h.col.size()), [&](int64_t b, int64_t e) {
-    for (int64_t q = b; q < e; ++q)
-      __atomic_store_n(&g2l[static_cast<size_t>(h.col[static_cast<size_t>(q)] - gmin)], 0, __ATOMIC_RELAXED);
+    bool ok = true;
+    for (int64_t q = b; q < e; ++q) {
+      const int64_t c = h.col[static_cast<size_t>(q)];
+      if (c < gmin || c > gmax) {
+        ok = false;
+        continue;
+      }
+      __atomic_store_n(&g2l[static_cast<size_t>(c - gmin)], 0, __ATOMIC_RELAXED);
+    }
+    if (!ok) in_range.store(false, std::memory_order_relaxed);
   });
+  require(in_range.load(), Errc::invalid_argument, "slab rows must hold ascending column indices");
   R.gid.clear();
   for (int64_t q = 0; q < span; ++q)
     if (g2l[static_cast<size_t>(q)] == 0) {
@@ -325,6 +342,8 @@ void local_structure(SlabRank& R, pdb_problem_s& prob, int64_t patch_size, cudaS
   for (int32_t l : pt) ++cnt[static_cast<size_t>(l)];
   touched.clear();
   tcount.clear();
+  touched.reserve(static_cast<size_t>(R.nl));
+  tcount.reserve(static_cast<size_t>(R.nl));
   for (int64_t l = 0; l < R.nl; ++l)
     if (cnt[static_cast<size_t>(l)]) {
       touched.push_back(R.gid[static_cast<size_t>(l)]);
